@@ -1,0 +1,153 @@
+/*
+ * svd1.h — C ABI of the B200-native rank-1 SVD update (libsvd1.so).
+ *
+ * Method: Gandhi & Rajgor, "Updating Singular Value Decomposition for Rank One
+ * Matrix Perturbation", arXiv 1707.08369 (/root/reference/PAPER.md, cited "P:n").
+ *   Alg 6.1: A_hat = A + a b^T, A = U Sigma V^T, m <= n.
+ *   Alg 6.2: RankOneUpdate, called twice per side.
+ *   Secular equation w(mu) = 1 + rho sum z_i^2 / (d_i - mu).
+ *   Eigenvector factor C~ = diag(z) C diag(1/||c_j||), C_ij = 1/(d_i - mu_j)
+ *     (P:194-208), applied to every row of U — the hot path.
+ *   1-D Chebyshev FMM for that product, re-derived per
+ *     DESIGN.md §4 (the printed M2M/M2L operators are corrected).
+ *
+ * Conventions (all entry points):
+ *   - Matrix/vector pointers are DEVICE pointers (cudaMalloc / torch CUDA
+ *     tensors), caller-owned; the library never frees them.  Matrices are
+ *     fp64, row-major, leading dimension in elements (ld >= number of columns).
+ *     A row of U is one right-hand side of the Cauchy apply.
+ *   - sigma is descending; eigenvalues are handled ascending inside.
+ *   - Work is ordered on the plan's stream (svd1_config.stream, a cudaStream_t;
+ *     NULL = legacy default stream).  svd1_update blocks the host until its
+ *     result is on the device (it reads small vectors back several times).
+ *   - Errors: every function returns svd1_status; on SVD1_E_NOCONV,
+ *     SVD1_E_NONFINITE, SVD1_E_POLE or SVD1_E_ZEROCOL from svd1_update the
+ *     matrices are left UNMODIFIED (all checks happen in the spectral phase,
+ *     before any write to U, Sigma or V).  SVD1_E_CUDA leaves them undefined.
+ *   - Determinism: fixed reduction orders, no floating-point atomics: identical
+ *     inputs give bitwise-identical outputs on the same GPU model.
+ *   - A plan is not thread-safe; use one plan per stream.
+ */
+#ifndef SVD1_H
+#define SVD1_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct svd1_plan_s* svd1_plan_t;
+
+typedef enum {
+  SVD1_OK = 0,
+  SVD1_E_INVALID = 1,   /* DimensionMismatch, m > n, eps not in (0,1), NULL pointer */
+  SVD1_E_NONFINITE = 2, /* NaN/Inf in an input vector or projection */
+  SVD1_E_NOCONV = 3,    /* secular iteration did not converge */
+  SVD1_E_POLE = 4,      /* a root coincides with a pole: tau == 0 */
+  SVD1_E_ZEROCOL = 5,   /* ||c_j|| underflow/overflow */
+  SVD1_E_CUDA = 6,      /* CUDA runtime error */
+  SVD1_E_NOMEM = 7      /* device or host allocation failed */
+} svd1_status;
+
+/* flags */
+#define SVD1_FORCE_DIRECT 0x1u /* always use the direct Cauchy-on-the-fly apply */
+#define SVD1_FORCE_FMM 0x2u    /* use the FMM apply whenever n_active >= 2 leaves */
+
+typedef struct {
+  int64_t m, n;      /* global sizes, 1 <= m <= n */
+  int64_t u_rows;    /* rows of U held by this process (== m on one GPU) */
+  int64_t v_rows;    /* rows of V held by this process (== n on one GPU) */
+  int64_t u_row0;    /* global index of the first local row of U (probe rows) */
+  int64_t v_row0;    /* global index of the first local row of V */
+  double eps;        /* FMM precision: p = max(4, ceil(log5(1/eps))) rounded up to a
+                        multiple of 4 (P:701 STEP 1; DESIGN.md §3.2 D6) */
+  void* stream;      /* cudaStream_t */
+  uint32_t flags;    /* SVD1_FORCE_* */
+  int32_t fmm_min_n; /* active size from which the FMM apply is used (0 = 384) */
+} svd1_config;
+
+typedef struct {
+  double t_ms[8];        /* host wall times: [0] project+readback, [1] spectral U,
+                            [2] spectral V, [3] applies (incl. final sync), [4] total */
+  int32_t n_active[4];   /* active sizes of the four eigen-updates */
+  int32_t n_deflated[4]; /* deflated counts */
+  int32_t max_iter[4];   /* max secular iterations per eigen-update */
+  int32_t fmm_used[4];   /* 1 if that apply ran the FMM, 0 if direct */
+  int32_t p;             /* Chebyshev order used */
+  int32_t neg_clamped;   /* eigenvalues < 0 clamped before sqrt (STEP 8) */
+  int32_t sign_flips;    /* columns of V_hat flipped by the sign alignment */
+  int32_t noop;          /* 1 if a == 0 or b == 0 (A_hat = A) */
+  int64_t kernel_launches; /* CUDA kernels launched by this call */
+} svd1_report;
+
+/* Plan: owns workspaces on the device (sized for u_rows x m and v_rows x n),
+ * host scratch and the probe seed.  Returns SVD1_E_INVALID for bad sizes. */
+svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out);
+svd1_status svd1_plan_destroy(svd1_plan_t plan);
+
+/* Full rank-1 SVD update on one GPU: Alg 6.1 STEPS 1-8.
+ * U (m x m, ldu), sigma (m, descending), V (n x n, ldv) are updated IN PLACE so
+ * that on return A + a b^T = U diag(sigma) V[:, :m]^T.  a (m), b (n) device.
+ * eps <= 0 uses the plan's eps.  rep (host pointer) may be NULL.
+ * Equivalent to svd1_project + svd1_update_projected with world size 1. */
+svd1_status svd1_update(svd1_plan_t plan, double* U, int64_t ldu, double* sigma,
+                        double* V, int64_t ldv, const double* a, const double* b,
+                        double eps, svd1_report* rep);
+
+/* Row-sharded update, phase 1 (STEP 1 projections over the LOCAL rows):
+ * proj (device, 5*m + n doubles) receives the partial sums
+ *   proj[0:m]        = U_loc^T a_loc          (x_a = U^T a)
+ *   proj[(1+k)m:...] = U_loc^T g_k,loc, k=0..3 (sign probes)
+ *   proj[5m:5m+n]    = V_loc^T b_loc          (y_b = V^T b)
+ * with a_loc = a[u_row0 : u_row0+u_rows], b_loc = b[v_row0 : v_row0+v_rows]
+ * (a, b are the FULL vectors).  Sum proj over ranks (e.g. NCCL all-reduce)
+ * before phase 2. */
+svd1_status svd1_project(svd1_plan_t plan, const double* U_loc, int64_t ldu,
+                         const double* V_loc, int64_t ldv, const double* a,
+                         const double* b, double* proj);
+
+/* Phase 2: everything after the projections (STEPS 2-8) on the local rows.
+ * proj = all-reduced phase-1 output; a (m), b (n), sigma (m) full, replicated. */
+svd1_status svd1_update_projected(svd1_plan_t plan, double* U_loc, int64_t ldu,
+                                  double* sigma, double* V_loc, int64_t ldv,
+                                  const double* proj, const double* a,
+                                  const double* b, double eps, svd1_report* rep);
+
+/* Standalone Cauchy apply (Alg 6.2 STEPS 3-7; Trummer's problem
+ * for every row):
+ *   U_out[r, j] = colscale[j] * sum_i U_in[r, i] * zhat[i] / ((d[i] - d[k[j]]) - tau[j])
+ * for r < rows, i, j < n.  d ascending and distinct; roots mu_j = d[k_j] + tau_j
+ * strictly interlace d (tau_j != 0).  All pointers device.  Uses the FMM when
+ * n >= fmm_min_n (or FORCE_FMM) with precision eps (<= 0: plan eps), else the
+ * direct DMMA kernel.  U_out must not alias U_in.  rows <= plan u_rows or v_rows
+ * (the larger).  fmm_used (host, nullable) reports the path taken. */
+svd1_status svd1_cauchy_apply(svd1_plan_t plan, int64_t rows, int64_t n,
+                              const double* d, const int32_t* k, const double* tau,
+                              const double* zhat, const double* colscale,
+                              const double* U_in, int64_t ld_in, double* U_out,
+                              int64_t ld_out, double eps, int32_t* fmm_used);
+
+/* Test hooks on device arrays (same kernels as svd1_update):
+ * secular roots of D + rho z z^T, d ascending distinct, z != 0:
+ *   mu_j = d[k_out[j]] + tau_out[j]; iters (host, nullable) = max iterations. */
+svd1_status svd1_secular_solve(svd1_plan_t plan, int64_t n, const double* d,
+                               const double* z, double rho, int32_t* k_out,
+                               double* tau_out, int32_t* iters);
+/* Loewner weights zhat (device out) from the roots (north star item (2)). */
+svd1_status svd1_loewner(svd1_plan_t plan, int64_t n, const double* d,
+                         const int32_t* k, const double* tau, double rho,
+                         const double* z, double* zhat_out);
+/* Column norms ||c_j|| of diag(zhat) C into colnorm_out (device). */
+svd1_status svd1_colnorms(svd1_plan_t plan, int64_t n, const double* d,
+                          const int32_t* k, const double* tau, const double* zhat,
+                          double* colnorm_out);
+
+const char* svd1_status_string(svd1_status s);
+/* Library build identifier (for the bench/smoke evidence). */
+const char* svd1_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVD1_H */

@@ -1,0 +1,8 @@
+"""B200-native (sm_100a) rank-1 SVD update — Gandhi & Rajgor, arXiv 1707.08369.
+
+Hot path: secular-equation root solve + Cauchy-structured eigenvector apply
+(direct DMMA kernel or 1-D Chebyshev FMM) behind the C ABI in include/svd1.h
+(libsvd1.so, built in-tree).  This package is the thin Python binding.
+"""
+from ._lib import FORCE_DIRECT, FORCE_FMM, LIB_PATH, version  # noqa: F401
+from .api import Plan, SVD1Error, update  # noqa: F401

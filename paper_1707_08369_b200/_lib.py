@@ -1,0 +1,78 @@
+"""ctypes binding of libsvd1.so (include/svd1.h).  Argument marshalling only.
+
+The library is loaded from this package directory (built in-tree by build.py);
+there is no fallback: if the shared object is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsvd1.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libsvd1.so not found at {LIB_PATH}: run `python -c 'import __graft_entry__ as g; "
+                      "g.build()'` (nvcc sm_100a) — there is no CPU fallback")
+
+lib = C.CDLL(LIB_PATH)
+
+i64, i32, u32, dbl, vp = C.c_int64, C.c_int32, C.c_uint32, C.c_double, C.c_void_p
+status_t = C.c_int
+
+
+class Config(C.Structure):
+    _fields_ = [("m", i64), ("n", i64), ("u_rows", i64), ("v_rows", i64), ("u_row0", i64),
+                ("v_row0", i64), ("eps", dbl), ("stream", vp), ("flags", u32), ("fmm_min_n", i32)]
+
+
+class Report(C.Structure):
+    _fields_ = [("t_ms", dbl * 8), ("n_active", i32 * 4), ("n_deflated", i32 * 4),
+                ("max_iter", i32 * 4), ("fmm_used", i32 * 4), ("p", i32), ("neg_clamped", i32),
+                ("sign_flips", i32), ("noop", i32), ("kernel_launches", i64)]
+
+    def as_dict(self):
+        return dict(t_ms=list(self.t_ms)[:5], n_active=list(self.n_active),
+                    n_deflated=list(self.n_deflated), max_iter=list(self.max_iter),
+                    fmm_used=list(self.fmm_used), p=self.p, neg_clamped=self.neg_clamped,
+                    sign_flips=self.sign_flips, noop=self.noop,
+                    kernel_launches=self.kernel_launches)
+
+
+def _sig(name, args):
+    f = getattr(lib, name)
+    f.argtypes = args
+    f.restype = status_t
+    return f
+
+
+svd1_plan_create = _sig("svd1_plan_create", [C.POINTER(Config), C.POINTER(vp)])
+svd1_plan_destroy = _sig("svd1_plan_destroy", [vp])
+svd1_update = _sig("svd1_update", [vp, vp, i64, vp, vp, i64, vp, vp, dbl, C.POINTER(Report)])
+svd1_project = _sig("svd1_project", [vp, vp, i64, vp, i64, vp, vp, vp])
+svd1_update_projected = _sig("svd1_update_projected",
+                             [vp, vp, i64, vp, vp, i64, vp, vp, vp, dbl, C.POINTER(Report)])
+svd1_cauchy_apply = _sig("svd1_cauchy_apply", [vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, vp, i64,
+                                               dbl, C.POINTER(i32)])
+svd1_secular_solve = _sig("svd1_secular_solve", [vp, i64, vp, vp, dbl, vp, vp, C.POINTER(i32)])
+svd1_loewner = _sig("svd1_loewner", [vp, i64, vp, vp, vp, dbl, vp, vp])
+svd1_colnorms = _sig("svd1_colnorms", [vp, i64, vp, vp, vp, vp, vp])
+lib.svd1_status_string.argtypes = [status_t]
+lib.svd1_status_string.restype = C.c_char_p
+lib.svd1_version.argtypes = []
+lib.svd1_version.restype = C.c_char_p
+
+EXPORTS = ["svd1_plan_create", "svd1_plan_destroy", "svd1_update", "svd1_project",
+           "svd1_update_projected", "svd1_cauchy_apply", "svd1_secular_solve", "svd1_loewner",
+           "svd1_colnorms", "svd1_status_string", "svd1_version"]
+
+FORCE_DIRECT = 0x1
+FORCE_FMM = 0x2
+
+
+def status_string(code: int) -> str:
+    return lib.svd1_status_string(code).decode()
+
+
+def version() -> str:
+    return lib.svd1_version().decode()

@@ -1,0 +1,396 @@
+// Cauchy-apply kernels of the rank-1 SVD update (sm_100a, fp64 tensor cores):
+//   K11 direct Cauchy-on-the-fly apply: U_out = U_in diag(zhat) C diag(colscale),
+//       C_ij = 1/((d_i - d_kj) - tau_j)   (Alg 6.2 STEPS 3-7 P:365-377)
+//   K5  FMM operator construction (re-derived: DESIGN.md §4.4)
+//   K6-K10 FMM passes as row-batched small GEMMs (P2M, M2M, M2L, L2L, L2P, P2P;
+//       P:727-796) — all rows of U are right-hand sides sharing one tree.
+//   K4  Householder deflation transforms on column groups
+// FP64 tensor work uses mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4): tcgen05 has no fp64 kind.
+#include <algorithm>
+#include <cmath>
+
+#include "svd1_internal.cuh"
+
+namespace svd1 {
+namespace {
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------- K11
+constexpr int DBM = 128, DBN = 64, DBK = 16;
+constexpr int DLDA = DBK + 4;  // 20 doubles: conflict-free A fragment loads
+constexpr int DLDB = DBN + 4;  // 68 doubles: conflict-free B fragment loads
+
+__global__ void __launch_bounds__(256) apply_direct_kernel(
+    int64_t rows, int n, const double* __restrict__ d, const int32_t* __restrict__ k,
+    const double* __restrict__ tau, const double* __restrict__ zhat, const double* __restrict__ cs,
+    const double* __restrict__ U_in, int64_t ld_in, const int32_t* __restrict__ src,
+    double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst) {
+  __shared__ double As[DBM * DLDA];
+  __shared__ double Bs[DBK * DLDB];
+  __shared__ double s_dk[DBN], s_tau[DBN], s_cs[DBN];
+  __shared__ double s_di[DBK], s_zi[DBK];
+  __shared__ int32_t s_src[DBK];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps, warp tile 32 x 32
+  const int64_t row0 = int64_t(blockIdx.y) * DBM;
+  const int j0 = blockIdx.x * DBN;
+  if (tid < DBN) {
+    const int j = j0 + tid;
+    if (j < n) {
+      s_dk[tid] = d[k[j]];
+      s_tau[tid] = tau[j];
+      s_cs[tid] = cs[j];
+    } else {
+      s_dk[tid] = 0.0;
+      s_tau[tid] = 1.0;
+      s_cs[tid] = 0.0;
+    }
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  for (int i0 = 0; i0 < n; i0 += DBK) {
+    __syncthreads();
+    if (tid < DBK) {
+      const int i = i0 + tid;
+      s_di[tid] = (i < n) ? d[i] : 0.0;
+      s_zi[tid] = (i < n) ? zhat[i] : 0.0;
+      s_src[tid] = (i < n) ? (src ? src[i] : i) : 0;
+    }
+    __syncthreads();
+    // A: 128 rows x 16 sources, 8 per thread; consecutive threads -> consecutive sources
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int idx = tid + e * 256;
+      const int rr = idx >> 4, kk = idx & 15;
+      const int64_t r = row0 + rr;
+      double v = 0.0;
+      if (r < rows && i0 + kk < n) v = __ldg(U_in + r * ld_in + s_src[kk]);
+      As[rr * DLDA + kk] = v;
+    }
+    // B generated on the fly: zhat_i cs_j / ((d_i - d_kj) - tau_j), 4 per thread
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      const int kk = idx >> 6, jj = idx & 63;
+      const double del = (s_di[kk] - s_dk[jj]) - s_tau[jj];
+      Bs[kk * DLDB + jj] = (s_zi[kk] * s_cs[jj]) / del;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < DBK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = As[(wm * 32 + mt * 8 + (lane >> 2)) * DLDA + kk + (lane & 3)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(kk + (lane & 3)) * DLDB + wn * 32 + nt * 8 + (lane >> 2)];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+    }
+  }
+  // epilogue: C fragment (row = lane/4, cols 2*(lane%4) + {0,1})
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int64_t r = row0 + wm * 32 + mt * 8 + (lane >> 2);
+    if (r >= rows) continue;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = j0 + wn * 32 + nt * 8 + (lane & 3) * 2 + h;
+        if (j < n) U_out[r * ld_out + (dst ? dst[j] : j)] = acc[mt][nt][h];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K4
+__global__ void __launch_bounds__(256) householder_kernel(int64_t rows, double* __restrict__ U,
+                                                         int64_t ld, const int32_t* __restrict__ goff,
+                                                         const int32_t* __restrict__ cols,
+                                                         const double* __restrict__ hv) {
+  const int g = blockIdx.y;
+  const int o0 = goff[g], o1 = goff[g + 1], len = o1 - o0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ double s_vv;
+  if (warp == 0) {
+    double s = 0.0;
+    for (int t = lane; t < len; t += 32) s = fma(hv[o0 + t], hv[o0 + t], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) s_vv = s;
+  }
+  __syncthreads();
+  const double coef = 2.0 / s_vv;
+  const int64_t rbase = int64_t(blockIdx.x) * 32;
+  for (int rr = warp; rr < 32; rr += 8) {
+    const int64_t r = rbase + rr;
+    if (r >= rows) break;
+    double* row = U + r * ld;
+    double s = 0.0;
+    for (int t = lane; t < len; t += 32) s = fma(row[cols[o0 + t]], hv[o0 + t], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double f = coef * s;
+    for (int t = lane; t < len; t += 32) {
+      const int c = cols[o0 + t];
+      row[c] = fma(-f, hv[o0 + t], row[c]);
+    }
+  }
+}
+
+__global__ void passthrough_kernel(int64_t rows, int nq, const double* __restrict__ U_in,
+                                   int64_t ld_in, const int32_t* __restrict__ src,
+                                   double* __restrict__ U_out, int64_t ld_out,
+                                   const int32_t* __restrict__ dst, const double* __restrict__ scale) {
+  const int q = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int64_t r = int64_t(blockIdx.y) * 8 + (threadIdx.x >> 5);
+  if (q >= nq || r >= rows) return;
+  U_out[r * ld_out + dst[q]] = scale[q] * U_in[r * ld_in + src[q]];
+}
+
+// ------------------------------------------------------------------- K5
+// Chebyshev nodes t_k = cos((2k+1) pi / 2p) (k 0-based) and barycentric weights
+// w_k = (-1)^k sin((2k+1) pi / 2p); u_k(t) = [w_k/(t - t_k)] / sum_m w_m/(t - t_m).
+__device__ double lagrange(const double* __restrict__ t, const double* __restrict__ w, int p,
+                           int kk, double x) {
+  double den = 0.0, num = 0.0;
+  for (int m = 0; m < p; ++m) {
+    const double dx = x - t[m];
+    if (dx == 0.0) return (m == kk) ? 1.0 : 0.0;
+    const double q = w[m] / dx;
+    den += q;
+    if (m == kk) num = q;
+  }
+  return num / den;
+}
+
+__global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc* __restrict__ descs,
+                                                     const FmmCell* __restrict__ cells, int p,
+                                                     const double* __restrict__ d,
+                                                     const int32_t* __restrict__ k,
+                                                     const double* __restrict__ tau,
+                                                     const double* __restrict__ zhat,
+                                                     const double* __restrict__ cs,
+                                                     double* __restrict__ ops) {
+  __shared__ double t[kMaxP], w[kMaxP];
+  if (threadIdx.x < p) {
+    const double th = (2.0 * threadIdx.x + 1.0) / (2.0 * p);  // in units of pi
+    t[threadIdx.x] = cospi(th);
+    w[threadIdx.x] = ((threadIdx.x & 1) ? -1.0 : 1.0) * sinpi(th);
+  }
+  __syncthreads();
+  for (int o = blockIdx.x; o < n_ops; o += gridDim.x) {
+    const FmmOpDesc D = descs[o];
+    double* out = ops + D.off;
+    const int total = D.rows * D.cols;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int i = e / D.cols, j = e % D.cols;
+      double v = 0.0;
+      switch (D.kind) {
+        case OP_P2M: {  // Phi~_X[j] += zhat_i U_i / (t_j (x_i - c_X) - 3 r_X)
+          const FmmCell X = cells[D.a];
+          const int s = X.lo + i;
+          v = zhat[s] / (t[j] * (d[s] - X.c) - 3.0 * X.r);
+          break;
+        }
+        case OP_M2M: {  // child (a) -> parent (b): i = child node, j = parent node
+          const FmmCell C = cells[D.a], P = cells[D.b];
+          const double den = 3.0 * P.r + t[j] * (P.c - C.c);
+          const double tc = 3.0 * C.r * t[j] / den;
+          v = (3.0 * C.r / den) * lagrange(t, w, p, i, tc);
+          break;
+        }
+        case OP_M2L: {  // source X (a) -> target Y (b): i = X node, j = Y node
+          const FmmCell X = cells[D.a], Y = cells[D.b];
+          const double tx = 3.0 * X.r / ((Y.c - X.c) + Y.r * t[j]);
+          v = tx * lagrange(t, w, p, i, tx);
+          break;
+        }
+        case OP_L2L: {  // parent (a) -> child (b): i = parent node, j = child node
+          const FmmCell P = cells[D.a], C = cells[D.b];
+          v = lagrange(t, w, p, i, ((C.c - P.c) + C.r * t[j]) / P.r);
+          break;
+        }
+        case OP_L2P: {  // leaf Y (b): i = node, j = target
+          const FmmCell Y = cells[D.b];
+          const int jt = Y.lo + j;
+          v = lagrange(t, w, p, i, ((d[k[jt]] - Y.c) + tau[jt]) / Y.r) * cs[jt];
+          break;
+        }
+        default: {  // OP_P2P: source leaf X (a), target leaf Y (b)
+          const FmmCell X = cells[D.a], Y = cells[D.b];
+          const int s = X.lo + i, jt = Y.lo + j;
+          v = (zhat[s] * cs[jt]) / ((d[s] - d[k[jt]]) - tau[jt]);
+          break;
+        }
+      }
+      out[e] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K6-K10
+// out (64 rows x N<=32) = sum_t in_t (64 x K_t<=32) * op_t (K_t x N)
+constexpr int TBM = 64, TBK = 32, TBN = 32;
+constexpr int TLDA = TBK + 4, TLDB = TBN + 4;
+
+__global__ void __launch_bounds__(128) fmm_task_kernel(
+    const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int64_t rows, int p,
+    const double* __restrict__ ops, const double* __restrict__ U_in, int64_t ld_in,
+    const int32_t* __restrict__ src, double* __restrict__ U_out, int64_t ld_out,
+    const int32_t* __restrict__ dst, double* __restrict__ phi, double* __restrict__ psi) {
+  __shared__ double As[TBM * TLDA];
+  __shared__ double Bs[TBK * TLDB];
+  const FmmTask T = tasks[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t row0 = int64_t(blockIdx.y) * TBM;
+  const int64_t nrow = (rows - row0 < TBM) ? (rows - row0) : int64_t(TBM);
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int ti = T.t_begin; ti < T.t_end; ++ti) {
+    const FmmTerm R = terms[ti];
+    const int K = R.K, K4 = (K + 3) & ~3;
+    __syncthreads();
+    // A tile
+    if (R.in_kind == IO_U) {
+      for (int e = tid; e < TBM * TBK; e += 128) {
+        const int rr = e >> 5, kk = e & 31;
+        if (kk >= K4) continue;
+        double v = 0.0;
+        if (rr < nrow && kk < K) {
+          const int col = src ? src[R.in_idx + kk] : R.in_idx + kk;
+          v = __ldg(U_in + (row0 + rr) * ld_in + col);
+        }
+        As[rr * TLDA + kk] = v;
+      }
+    } else {
+      const double* base = (R.in_kind == IO_PHI ? phi : psi) + (int64_t(R.in_idx) * rows + row0) * p;
+      for (int e = tid; e < TBM * TBK; e += 128) {
+        const int rr = e >> 5, kk = e & 31;
+        if (kk >= K4) continue;
+        As[rr * TLDA + kk] = (rr < nrow && kk < K) ? base[int64_t(rr) * p + kk] : 0.0;
+      }
+    }
+    // B = op (K x N, row-major, ld N)
+    const double* op = ops + R.op_off;
+    for (int e = tid; e < TBK * TBN; e += 128) {
+      const int kk = e >> 5, jj = e & 31;
+      if (kk >= K4) continue;
+      Bs[kk * TLDB + jj] = (kk < K && jj < T.N) ? __ldg(op + kk * T.N + jj) : 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < K4; kk += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) af[mt] = As[(warp * 16 + mt * 8 + (lane >> 2)) * TLDA + kk + (lane & 3)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(kk + (lane & 3)) * TLDB + nt * 8 + (lane >> 2)];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+    }
+  }
+  // store
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int rr = warp * 16 + mt * 8 + (lane >> 2);
+    if (rr >= nrow) continue;
+    const int64_t r = row0 + rr;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jj = nt * 8 + (lane & 3) * 2 + h;
+        if (jj >= T.N) continue;
+        if (T.out_kind == IO_U) {
+          U_out[r * ld_out + (dst ? dst[T.out_idx + jj] : T.out_idx + jj)] = acc[mt][nt][h];
+        } else {
+          double* base = (T.out_kind == IO_PHI ? phi : psi) + int64_t(T.out_idx) * rows * p;
+          base[r * p + jj] = acc[mt][nt][h];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ wrappers
+svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
+                         const double* tau, const double* zhat, const double* cs,
+                         const double* U_in, int64_t ld_in, const int32_t* src,
+                         double* U_out, int64_t ld_out, const int32_t* dst,
+                         cudaStream_t st, int64_t* launches) {
+  if (rows <= 0 || n <= 0) return SVD1_OK;
+  dim3 grid(unsigned((n + DBN - 1) / DBN), unsigned((rows + DBM - 1) / DBM));
+  apply_direct_kernel<<<grid, 256, 0, st>>>(rows, n, d, k, tau, zhat, cs, U_in, ld_in, src, U_out,
+                                            ld_out, dst);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,
+                             const int32_t* goff, const int32_t* cols, const double* hv,
+                             cudaStream_t st, int64_t* launches) {
+  if (rows <= 0 || ngroups <= 0) return SVD1_OK;
+  dim3 grid(unsigned((rows + 31) / 32), unsigned(ngroups));
+  householder_kernel<<<grid, 256, 0, st>>>(rows, U, ld, goff, cols, hv);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status passthrough(int64_t rows, int nq, const double* U_in, int64_t ld_in,
+                        const int32_t* src, double* U_out, int64_t ld_out,
+                        const int32_t* dst, const double* scale, cudaStream_t st,
+                        int64_t* launches) {
+  if (rows <= 0 || nq <= 0) return SVD1_OK;
+  dim3 grid(unsigned((nq + 31) / 32), unsigned((rows + 7) / 8));
+  passthrough_kernel<<<grid, 256, 0, st>>>(rows, nq, U_in, ld_in, src, U_out, ld_out, dst, scale);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cells, int p,
+                          const double* d, const int32_t* k, const double* tau,
+                          const double* zhat, const double* cs, double* ops, cudaStream_t st,
+                          int64_t* launches) {
+  if (n_ops <= 0) return SVD1_OK;
+  const unsigned g = unsigned(std::min(n_ops, 148 * 16));
+  fmm_ops_kernel<<<g, 256, 0, st>>>(n_ops, descs, cells, p, d, k, tau, zhat, cs, ops);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
+                          int p, const double* ops, const double* U_in, int64_t ld_in,
+                          const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
+                          double* phi, double* psi, cudaStream_t st, int64_t* launches) {
+  if (n_tasks <= 0 || rows <= 0) return SVD1_OK;
+  dim3 grid(unsigned(n_tasks), unsigned((rows + TBM - 1) / TBM));
+  fmm_task_kernel<<<grid, 128, 0, st>>>(tasks, terms, rows, p, ops, U_in, ld_in, src, U_out, ld_out,
+                                        dst, phi, psi);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+}  // namespace svd1

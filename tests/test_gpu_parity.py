@@ -1,0 +1,175 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Tolerances: north star + readings Q23, Q26-Q29."""
+import numpy as np
+import pytest
+
+import oracle as O
+from compare import sigma_errors, vector_error
+from synth import config_inputs, interlaced_cauchy, random_secular
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1707_08369_b200 as P  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(x, dt=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV, dt)
+
+
+def N(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def plan():
+    return P.Plan(8, 8, eps=1e-10)
+
+
+# ------------------------------------------------------------------ K2
+CASES = [(n, kind, s) for n in (1, 2, 5, 33, 257, 1000) for kind in ("gaussian", "graded", "uniform")
+         for s in (1.0, -1.0)]
+
+
+@pytest.mark.parametrize("n,kind,sgn", CASES)
+def test_secular_parity(plan, n, kind, sgn):
+    rng = np.random.default_rng(n * 7 + len(kind))
+    d, z, rho = random_secular(n, rng, kind=kind)
+    rho = sgn * abs(rho)
+    dfl = O.deflate(d, z, rho)
+    d, z = dfl.d[dfl.active], dfl.z[dfl.active]
+    n = d.size
+    ko, to = O.secular_roots_bisect(d, z, rho)
+    kg, tg, iters = plan.secular_solve(T(d), T(z), rho)
+    kg, tg = N(kg).astype(np.int64), N(tg)
+    # same root in gap form: mu_g - mu_o = (d[kg] - d[ko]) + tg - to
+    diff = ((d[kg] - d[ko]) + tg) - to
+    scale = np.minimum(np.abs(to), np.abs(tg))
+    assert np.max(np.abs(diff) / scale) <= 2e-12, (np.max(np.abs(diff) / scale), iters)
+    # the GPU roots are inside the rounding band of w (oracle's evaluation)
+    w = O.secular_w(d, z, rho, kg, tg)
+    terms = np.abs(z[None, :] ** 2 / ((d[None, :] - d[kg][:, None]) - tg[:, None]))
+    assert np.all(np.abs(w) <= 64 * n * O.EPS * (1 + abs(rho) * terms.sum(axis=1)))
+    assert iters <= 40
+
+
+@pytest.mark.parametrize("n,kind", [(3, "gaussian"), (300, "graded"), (1000, "uniform")])
+def test_loewner_and_colnorm_parity(plan, n, kind):
+    rng = np.random.default_rng(11 + n)
+    d, z, rho = random_secular(n, rng, kind=kind)
+    k, tau = O.secular_roots_bisect(d, z, rho)
+    zo = O.loewner_zhat(d, k, tau, rho, z)
+    zg = N(plan.loewner(T(d), T(k, torch.int32), T(tau), rho, T(z)))
+    assert np.max(np.abs(zg / zo - 1)) <= 1e-12
+    _, cn = O.cauchy_X(d, k, tau, zo)
+    cg = N(plan.colnorms(T(d), T(k, torch.int32), T(tau), T(zo)))
+    assert np.max(np.abs(cg / cn - 1)) <= 1e-13
+
+
+# ------------------------------------------------------------------ K11 / FMM
+def _abs_scale(u_in, d, k, tau, zh, cs):
+    """E_rj = cs_j sum_i |U_ri zhat_i| / |(d_i - d_kj) - tau_j| (error scale of the sum)."""
+    inv = 1.0 / np.abs((d[:, None] - d[k][None, :]) - tau[None, :])
+    return (np.abs(u_in * zh[None, :]) @ inv) * np.abs(cs)[None, :]
+
+
+@pytest.mark.parametrize("rows,n,sgn", [(1, 1, 1.0), (7, 5, 1.0), (300, 200, -1.0), (129, 1000, 1.0)])
+def test_cauchy_apply_direct(rows, n, sgn):
+    d, k, tau, zh, cs, uin = interlaced_cauchy(n, rows, 40 + n, rho_sign=sgn)
+    want = O.cauchy_apply_explicit(uin, d, k, tau, zh, cs)
+    plan = P.Plan(max(rows, n), max(rows, n), flags=P.FORCE_DIRECT)
+    out, used = plan.cauchy_apply(T(uin), T(d), T(k, torch.int32), T(tau), T(zh), T(cs))
+    assert not used
+    E = _abs_scale(uin, d, k, tau, zh, cs)
+    assert np.max(np.abs(N(out) - want) / E) <= 1e-13
+
+
+@pytest.mark.parametrize("rows,n,sgn,eps", [(100, 65, 1.0, 1e-10), (257, 777, -1.0, 1e-10),
+                                            (64, 2500, 1.0, 1e-10), (70, 3000, 1.0, 5.0 ** -20)])
+def test_cauchy_apply_fmm(rows, n, sgn, eps):
+    """Q23: FMM vs the explicit product within 10 eps of the per-entry error scale."""
+    d, k, tau, zh, cs, uin = interlaced_cauchy(n, rows, 70 + n, rho_sign=sgn)
+    want = O.cauchy_apply_explicit(uin, d, k, tau, zh, cs)
+    plan = P.Plan(max(rows, n), max(rows, n), eps=eps, flags=P.FORCE_FMM)
+    out, used = plan.cauchy_apply(T(uin), T(d), T(k, torch.int32), T(tau), T(zh), T(cs))
+    assert used
+    E = _abs_scale(uin, d, k, tau, zh, cs)
+    assert np.max(np.abs(N(out) - want) / E) <= 10 * max(eps, 1e-13)
+
+
+# ------------------------------------------------------------------ full update
+def _gpu_update(U, s, V, a, b, **kw):
+    Ug, sg, Vg = T(U), T(s), T(V)
+    plan = P.Plan(U.shape[0], V.shape[0], **kw)
+    rep = plan.update(Ug, sg, Vg, T(a), T(b))
+    return Ug, sg, Vg, rep
+
+
+def _check_update(U, s, V, a, b, flags=0, fmm_min_n=0):
+    m, n = U.shape[0], V.shape[0]
+    ref = O.svd_update(U, s, V, a, b)
+    Ug, sg, Vg, rep = _gpu_update(U, s, V, a, b, flags=flags, fmm_min_n=fmm_min_n)
+    A_hat = T((U * s[None, :]) @ V[:, :m].T + np.outer(a, b))
+    res = float(torch.linalg.norm(A_hat @ Vg[:, :m] - Ug * sg[None, :], dim=0).max() / sg[0])
+    I_m = torch.eye(m, dtype=torch.float64, device=DEV)
+    I_n = torch.eye(n, dtype=torch.float64, device=DEV)
+    orth = max(float((Ug.T @ Ug - I_m).abs().max()), float((Vg.T @ Vg - I_n).abs().max()))
+    se = sigma_errors(N(sg), ref["sigma"])
+    eu = vector_error(N(Ug), ref["U"], ref["sigma"] ** 2)
+    ev = vector_error(N(Vg), ref["V"], ref["info"]["Dv_hat"])
+    return dict(sigma=se, res=res, orth=orth, U=eu, V=ev, rep=rep)
+
+
+@pytest.mark.parametrize("cfg,m,n,flags", [
+    (1, None, None, 0),                      # C1 full size (direct path)
+    (2, 256, 256, P.FORCE_FMM),              # C2 recipe, FMM path
+    (2, 300, 300, P.FORCE_DIRECT),
+    (3, 256, 256, P.FORCE_FMM),              # C3 graded recipe
+    (4, 40, 160, 0),                         # C4 recipe: rectangular, null-space Householder
+    (5, 200, 200, P.FORCE_FMM),              # C5 recipe: duplicated sigma
+])
+def test_update_parity(cfg, m, n, flags):
+    inp = config_inputs(cfg, m=m, n=n, updates=1)
+    a, b = inp["ab"][0]
+    r = _check_update(inp["U"], inp["sigma"], inp["V"], a, b, flags=flags)
+    assert r["sigma"]["gram"] <= 1e-12 and r["sigma"]["rel_top"] <= 1e-12, r
+    assert r["U"]["isolated"] <= 1e-9 and r["U"]["cluster"] <= 1e-9, r
+    assert r["V"]["isolated"] <= 1e-9 and r["V"]["cluster"] <= 1e-9, r
+    assert r["res"] <= 1e-10 and r["orth"] <= 1e-10, r
+
+
+def test_update_noop_and_errors():
+    inp = config_inputs(1, m=16, n=24, updates=1)
+    U, s, V = inp["U"], inp["sigma"], inp["V"]
+    Ug, sg, Vg, rep = _gpu_update(U, s, V, np.zeros(16), inp["ab"][0][1])
+    assert rep["noop"] == 1 and np.array_equal(N(Ug), U) and np.array_equal(N(sg), s)
+    b = inp["ab"][0][1].copy()
+    b[3] = np.nan
+    with pytest.raises(P.SVD1Error) as e:
+        _gpu_update(U, s, V, inp["ab"][0][0], b)
+    assert e.value.code == 2
+
+
+def test_update_stream_c3_small():
+    """Four chained updates on the C3 recipe: invariants hold through the stream
+    (Q30: one-step parity at each step, oracle fed the GPU's previous factors)."""
+    inp = config_inputs(3, m=192, n=192, updates=4)
+    U, s, V = inp["U"], inp["sigma"], inp["V"]
+    A = (U * s[None, :]) @ V.T
+    Ug, sg, Vg = T(U), T(s), T(V)
+    plan = P.Plan(192, 192, flags=P.FORCE_FMM)
+    for (a, b) in inp["ab"]:
+        Uprev, sprev, Vprev = N(Ug), N(sg), N(Vg)
+        ref = O.svd_update(Uprev, sprev, Vprev, a, b)
+        plan.update(Ug, sg, Vg, T(a), T(b))
+        A = A + np.outer(a, b)
+        e = sigma_errors(N(sg), ref["sigma"])
+        assert e["gram"] <= 1e-12 and e["rel_top"] <= 1e-12
+        At = T(A)
+        res = float(torch.linalg.norm(At @ Vg - Ug * sg[None, :], dim=0).max() / sg[0])
+        assert res <= 1e-10
