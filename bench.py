@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""Benchmark: rank-1 SVD updates/s (fp64, n = 4096) on BASELINE.json config C3, plus
+the FMM Cauchy-apply fraction of the FP64 (DMMA) roofline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one svd1_update (Alg 6.1) of the C3 stream
+(m = n = 4096, sigma_i = 10^(-6 i/n), a, b ~ N(0,1)); the K timed steps are updates
+1..K of that stream (indices wrap at 16), applied in place to device-resident
+factors.  N > 1: torchrun, rows of U and V sharded across ranks, the STEP-1
+projections all-reduced over NCCL (the path's only exchange), time = max over ranks.
+`--impl reference` times the CPU oracle (oracle/, the base contract's reference arm
+for this tier) on bounded samples of the same workload.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "rank-1 SVD updates/s (fp64, n=4096) and FMM Cauchy-apply % of FP64 roofline"
+UNIT = "updates/s"
+CFG_ID = 3
+WORKLOAD = ("C3: m=n=4096 fp64, A = Q1 diag(sigma) Q2^T, sigma_i = 10^(-6 i/n) (graded), "
+            "16-update stream a,b ~ N(0,1), eps=1e-10 (p=16)")
+FP64_PEAK_TFLOPS = 37.17  # measured DMMA m8n8k4 sustained on this pool's B200 (profiles/fp64_peak_r01.jsonl)
+HBM_PEAK_GBS = 6553.0
+
+
+def _measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """NVML polling thread: SM clock and clock-event reasons during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def oracle_sample_time(inp, steps, rows_sample=256):
+    """Time the CPU oracle on one C3 update per step (full spectral phase; the explicit
+    O(rows n^2) products on `rows_sample` sampled rows of U and V, O8)."""
+    import oracle as O
+    U, s, V = inp["U"], inp["sigma"], inp["V"]
+    if not isinstance(U, np.ndarray):
+        U, s, V = U.cpu().numpy(), s.cpu().numpy(), V.cpu().numpy()
+    m = U.shape[0]
+    rows = (np.arange(0, m, max(1, m // rows_sample)), np.arange(0, V.shape[0], max(1, V.shape[0] // rows_sample)))
+    t = []
+    for k in range(steps):
+        a, b = inp["ab"][k % len(inp["ab"])]
+        t0 = time.perf_counter()
+        O.svd_update(U, s, V, a, b, sign_rule="probe", rows=rows)
+        t.append(time.perf_counter() - t0)
+    return t, len(rows[0])
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from synth import config_inputs
+    inp = config_inputs(CFG_ID)
+    _, _ = oracle_sample_time(inp, args.warmup)
+    t, nr = oracle_sample_time(inp, args.steps)
+    total = sum(t)
+    val = args.steps / total
+    cores = os.cpu_count()
+    sample = (f"C3 oracle update per step: full spectral phase (bisection, Loewner, norms) + "
+              f"explicit Cauchy products on {nr} sampled rows of U and V (of 4096)")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "m": 4096, "n": 4096},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1707_08369_b200 as P
+    from synth import config_inputs
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    inp = config_inputs(CFG_ID, device=dev)
+    cfg = inp["cfg"]
+    m, n = cfg["m"], cfg["n"]
+    ab = [(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)) for a, b in inp["ab"]]
+    U0, s0, V0 = inp["U"], inp["sigma"], inp["V"]
+    # row shards
+    ur = [(m * r) // world for r in range(world + 1)]
+    vr = [(n * r) // world for r in range(world + 1)]
+    u0, u1, v0, v1 = ur[rank], ur[rank + 1], vr[rank], vr[rank + 1]
+    U = U0[u0:u1].clone()
+    V = V0[v0:v1].clone()
+    sig = s0.clone()
+    Upr, Vpr, spr = U.clone(), V.clone(), sig.clone()
+    stream = torch.cuda.current_stream()
+    plan = P.Plan(m, n, eps=cfg["eps"], stream=stream, u_rows=u1 - u0, v_rows=v1 - v0,
+                  u_row0=u0, v_row0=v0)
+    proj = torch.empty(plan.proj_size(), dtype=torch.float64, device=dev)
+
+    def step(t, a=None, b=None):
+        a_t, b_t = ab[t % len(ab)] if a is None else (a, b)
+        if world == 1:
+            return plan.update(U, sig, V, a_t, b_t)
+        plan.project(U, V, a_t, b_t, proj)
+        dist.all_reduce(proj)  # N1: sum of the row-block partial projections (NCCL)
+        return plan.update_projected(U, sig, V, proj, a_t, b_t)
+
+    def restore():
+        U.copy_(Upr)
+        V.copy_(Vpr)
+        sig.copy_(spr)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for t in range(args.warmup):
+        step(t)
+    restore()
+    torch.cuda.synchronize()
+    reps = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for t in range(args.steps):
+            reps.append(step(t))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (the FMM Cauchy apply), from live CUDA events
+    ap_ms = sum(sum(r["apply_ms"]) for r in reps)
+    ap_fl = sum(sum(r["apply_flops"]) for r in reps)
+    sp_ms = sum(sum(r["spectral_ms"]) for r in reps)
+    n_apply = sum(sum(1 for x in r["apply_ms"] if x > 0) for r in reps)
+    achieved = ap_fl / (ap_ms / 1e3) / 1e12 if ap_ms > 0 else 0.0
+    launches = sum(r["kernel_launches"] for r in reps)
+    roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "kernel": "FMM Cauchy apply (K5 ops + K6-K10 task passes + K4/passthrough), per apply",
+            "flops_per_apply": ap_fl / max(n_apply, 1), "ms_per_apply": ap_ms / max(n_apply, 1),
+            "apply_share_of_step": ap_ms / ms if ms else None,
+            "spectral_share_of_step": sp_ms / ms if ms else None,
+            "peak_source": "measured fp64 DMMA sustained (profiles/fp64_peak_r01.jsonl); "
+                           "MEASURED_PEAKS.json has no fp64 entry"}
+
+    # end-to-end: a, b from pinned host memory each step, sigma read back each step
+    e2e = None
+    if not args.no_e2e:
+        restore()
+        a_h = [x.cpu().pin_memory() for x, _ in ab]
+        b_h = [y.cpu().pin_memory() for _, y in ab]
+        a_d, b_d = torch.empty(m, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev)
+        s_h = torch.empty(m, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for t in range(args.steps):
+            a_d.copy_(a_h[t % len(ab)], non_blocking=True)
+            b_d.copy_(b_h[t % len(ab)], non_blocking=True)
+            step(t, a_d, b_d)
+            s_h.copy_(sig, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * (m + n),
+               "d2h_bytes_per_step": 8 * m,
+               "note": "factors stay resident (streaming update); a, b copied from pinned host "
+                       "memory and sigma read back every step through the public API"}
+
+    # correctness check of the timed stream (outside the timed region): residual and
+    # orthogonality against the explicitly accumulated A_hat (verification only)
+    check = None
+    if not args.no_check and world == 1:
+        restore()
+        A = (U0 * s0[None, :]) @ V0.T
+        for t in range(args.steps):
+            step(t)
+            a_t, b_t = ab[t % len(ab)]
+            A = A + torch.outer(a_t, b_t)
+        res = float(torch.linalg.norm(A @ V - U * sig[None, :], dim=0).max() / sig[0])
+        I = torch.eye(m, dtype=torch.float64, device=dev)
+        orth = max(float((U.T @ U - I).abs().max()), float((V.T @ V - I).abs().max()))
+        check = {"residual": res, "orthogonality": orth, "updates": args.steps,
+                 "n_active_last": reps[-1]["n_active"], "max_secular_iter": max(max(r["max_iter"]) for r in reps),
+                 "fmm_levels": reps[-1]["fmm_levels"], "fmm_max_near": reps[-1]["fmm_max_near"]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from synth import config_inputs as ci
+        cin = ci(CFG_ID)
+        t, nr = oracle_sample_time(cin, 1)
+        cpu = {"value": 1.0 / t[0], "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"one C3 update: full spectral phase (bisection, Loewner, norms) + explicit "
+                         f"Cauchy products on {nr} sampled rows of U and V (of 4096); numpy fp64"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, BASELINE.json C3 recipe)",
+                "config": {"workload": WORKLOAD, "m": m, "n": n, "eps": cfg["eps"], "p": reps[-1]["p"],
+                           "updates_in_stream": cfg["updates"],
+                           "l2": "inputs larger than L2 (U + V = 256 MiB > 126 MB)",
+                           "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
+                "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+                "cpu_baseline": cpu, "check": check,
+                "spectral_ms_per_step": sp_ms / args.steps, "apply_ms_per_step": ap_ms / args.steps}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -79,6 +79,13 @@ typedef struct {
   int32_t sign_flips;    /* columns of V_hat flipped by the sign alignment */
   int32_t noop;          /* 1 if a == 0 or b == 0 (A_hat = A) */
   int64_t kernel_launches; /* CUDA kernels launched by this call */
+  double apply_ms[4];    /* device time of each Cauchy apply (CUDA events on the plan
+                            stream; Householder + apply + passthrough) */
+  double apply_flops[4]; /* algorithmic flops of each apply: FMM 2*rows*sum(K*N) over the
+                            plan's P2M/M2M/M2L/L2L/L2P/P2P terms; direct 2*rows*n_a^2 */
+  double spectral_ms[4]; /* device time of secular + Loewner + norms per eigen-update */
+  int32_t fmm_levels[4]; /* tree depth L of each FMM apply (0 if direct) */
+  int32_t fmm_max_near[4]; /* largest near-field list (leaves) of each FMM apply */
 } svd1_report;
 
 /* Plan: owns workspaces on the device (sized for u_rows x m and v_rows x n),
@@ -96,10 +103,12 @@ svd1_status svd1_update(svd1_plan_t plan, double* U, int64_t ldu, double* sigma,
                         double eps, svd1_report* rep);
 
 /* Row-sharded update, phase 1 (STEP 1 projections over the LOCAL rows):
- * proj (device, 5*m + n doubles) receives the partial sums
+ * proj (device, 5*m + n + 6 doubles) receives the partial sums
  *   proj[0:m]        = U_loc^T a_loc          (x_a = U^T a)
  *   proj[(1+k)m:...] = U_loc^T g_k,loc, k=0..3 (sign probes)
  *   proj[5m:5m+n]    = V_loc^T b_loc          (y_b = V^T b)
+ *   proj[5m+n+k]     = a_loc . g_k,loc (k<4), proj[5m+n+4] = a_loc.a_loc,
+ *   proj[5m+n+5]     = b_loc . b_loc          (alpha, beta of STEP 1)
  * with a_loc = a[u_row0 : u_row0+u_rows], b_loc = b[v_row0 : v_row0+v_rows]
  * (a, b are the FULL vectors).  Sum proj over ranks (e.g. NCCL all-reduce)
  * before phase 2. */

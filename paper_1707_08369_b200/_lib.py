@@ -29,14 +29,18 @@ class Config(C.Structure):
 class Report(C.Structure):
     _fields_ = [("t_ms", dbl * 8), ("n_active", i32 * 4), ("n_deflated", i32 * 4),
                 ("max_iter", i32 * 4), ("fmm_used", i32 * 4), ("p", i32), ("neg_clamped", i32),
-                ("sign_flips", i32), ("noop", i32), ("kernel_launches", i64)]
+                ("sign_flips", i32), ("noop", i32), ("kernel_launches", i64),
+                ("apply_ms", dbl * 4), ("apply_flops", dbl * 4), ("spectral_ms", dbl * 4),
+                ("fmm_levels", i32 * 4), ("fmm_max_near", i32 * 4)]
 
     def as_dict(self):
         return dict(t_ms=list(self.t_ms)[:5], n_active=list(self.n_active),
                     n_deflated=list(self.n_deflated), max_iter=list(self.max_iter),
                     fmm_used=list(self.fmm_used), p=self.p, neg_clamped=self.neg_clamped,
                     sign_flips=self.sign_flips, noop=self.noop,
-                    kernel_launches=self.kernel_launches)
+                    kernel_launches=self.kernel_launches, apply_ms=list(self.apply_ms),
+                    apply_flops=list(self.apply_flops), spectral_ms=list(self.spectral_ms),
+                    fmm_levels=list(self.fmm_levels), fmm_max_near=list(self.fmm_max_near))
 
 
 def _sig(name, args):

@@ -87,7 +87,9 @@ struct StepRecord {
   std::vector<double> da, mu, tau_h, cs_h;  // host copies (tree + sign folding)
   std::vector<int32_t> k_h;
   int max_iter = 0;
+  double spectral_ms = 0.0;
   void clear_host() {
+    spectral_ms = 0.0;
     N = na = 0;
     rho = 0.0;
     max_iter = 0;
@@ -132,6 +134,7 @@ struct svd1_plan_s {
   cudaEvent_t arena_ev = nullptr;
   bool arena_pending = false;
   FmmHost fmm_last;         // stats of the last FMM apply
+  cudaEvent_t ev[16] = {};  // timing events (spectral / apply phases)
 };
 
 namespace {
@@ -183,6 +186,19 @@ svd1_status arena_put(svd1_plan_t P, const void* src, size_t bytes, void* dev) {
   P->arena_pending = true;
   P->arena_used = off + bytes;
   return SVD1_OK;
+}
+
+svd1_status ev_record(svd1_plan_t P, int i) {
+  if (!P->ev[i]) SVD1_CUDA_TRY(cudaEventCreate(&P->ev[i]));
+  SVD1_CUDA_TRY(cudaEventRecord(P->ev[i], P->st));
+  return SVD1_OK;
+}
+
+double ev_ms(svd1_plan_t P, int a, int b) {
+  float ms = 0.f;
+  if (P->ev[a] && P->ev[b] && cudaEventElapsedTime(&ms, P->ev[a], P->ev[b]) == cudaSuccess) return ms;
+  cudaGetLastError();
+  return 0.0;
 }
 
 template <class T>
@@ -356,18 +372,21 @@ svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, 
                        const double* d_tau, const double* d_zhat, const double* d_cs,
                        const double* U_in, int64_t ld_in, const int32_t* d_src, double* U_out,
                        int64_t ld_out, const int32_t* d_dst, const std::vector<double>& da,
-                       const std::vector<double>& mu, int p, bool* used_fmm) {
+                       const std::vector<double>& mu, int p, bool* used_fmm,
+                       double* flops = nullptr) {
   const int minn = P->cfg.fmm_min_n > 0 ? P->cfg.fmm_min_n : 384;
   const int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2: s ~ 2p, capped by the tile
   bool fmm = (P->cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
   if (P->cfg.flags & SVD1_FORCE_DIRECT) fmm = false;
   if (leaf > kMaxLeaf) fmm = false;
   *used_fmm = fmm;
+  if (flops) *flops = 2.0 * double(rows) * double(na) * double(na);
   if (!fmm)
     return apply_direct(rows, na, d_da, d_k, d_tau, d_zhat, d_cs, U_in, ld_in, d_src, U_out, ld_out,
                         d_dst, P->st, &P->launches);
   FmmHost& F = P->fmm_last;
   fmm_build_host(F, na, leaf, p, da, mu);
+  if (flops) *flops = double(F.flops_per_row) * double(rows);
   FmmCell* dc;
   FmmOpDesc* dd;
   FmmTerm* dt;
@@ -418,7 +437,7 @@ svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, 
 // by buffer column; on return D and carries are indexed by output position.
 svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
                           const std::vector<double>& z, double rho,
-                          std::vector<std::vector<double>>& carries) {
+                          std::vector<std::vector<double>>& carries, int ev0) {
   const int N = int(D.size());
   S.clear_host();  // device buffers are kept (grow-only)
   S.N = N;
@@ -516,9 +535,11 @@ svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
     TRY(P->status.get<int32_t>(1, &dst));
     TRY(P->iters.get<int32_t>(na, &dit));
     SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
+    TRY(ev_record(P, ev0));
     TRY(secular(dda, dza, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
     TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, P->st, &P->launches));
     TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, P->st, &P->launches));
+    TRY(ev_record(P, ev0 + 1));
     // read back k, tau, cs, carried vectors, iterations, status
     S.k_h.resize(na);
     S.tau_h.resize(na);
@@ -535,6 +556,7 @@ svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
     SVD1_CUDA_TRY(cudaMemcpyAsync(&st_h, dst, sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
     SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
     for (int v : it_h) S.max_iter = std::max(S.max_iter, v);
+    S.spectral_ms = ev_ms(P, ev0, ev0 + 1);
     if (st_h & 1) return SVD1_E_NOCONV;
     if (st_h & 2) return SVD1_E_POLE;
     if (st_h & 4) return SVD1_E_ZEROCOL;
@@ -579,8 +601,11 @@ svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
 // Apply one recorded step: Householder (in place on U_in), Cauchy apply, passthrough.
 // out_col(q) = reverse ? (N - 1 - q) : q.
 svd1_status apply_step(svd1_plan_t P, StepRecord& S, int64_t rows, double* U_in, int64_t ld_in,
-                       double* U_out, int64_t ld_out, bool reverse, bool* used_fmm) {
+                       double* U_out, int64_t ld_out, bool reverse, bool* used_fmm, double* flops,
+                       int ev0) {
   *used_fmm = false;
+  *flops = 0.0;
+  TRY(ev_record(P, ev0));
   const int N = S.N;
   auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
   if (S.h_goff.size() > 1) {
@@ -607,7 +632,7 @@ svd1_status apply_step(svd1_plan_t P, StepRecord& S, int64_t rows, double* U_in,
     TRY(S.d_zhat.get<double>(S.na, &dzh));
     TRY(S.d_k.get<int32_t>(S.na, &dk));
     TRY(run_cauchy(P, rows, S.na, dda, dk, dtau, dzh, dcs, U_in, ld_in, dsrc, U_out, ld_out, ddst, S.da,
-                   S.mu, P->p, used_fmm));
+                   S.mu, P->p, used_fmm, flops));
   }
   if (!S.pass_src.empty()) {
     std::vector<int32_t> dst(S.pass_dst.size());
@@ -619,6 +644,7 @@ svd1_status apply_step(svd1_plan_t P, StepRecord& S, int64_t rows, double* U_in,
     TRY(upload(P, S.d_pass_scale, S.pass_scale, &sc));
     TRY(passthrough(rows, int(dst.size()), U_in, ld_in, ds, U_out, ld_out, dd, sc, P->st, &P->launches));
   }
+  TRY(ev_record(P, ev0 + 1));
   return SVD1_OK;
 }
 
@@ -672,6 +698,8 @@ svd1_status svd1_plan_destroy(svd1_plan_t P) {
   if (P->h_pin) cudaFreeHost(P->h_pin);
   if (P->arena) cudaFreeHost(P->arena);
   if (P->arena_ev) cudaEventDestroy(P->arena_ev);
+  for (auto& e : P->ev)
+    if (e) cudaEventDestroy(e);
   delete P;
   return SVD1_OK;
 }
@@ -754,18 +782,18 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   }
   // ---- spectral phase, all four eigen-updates, before any write to U or V
   const double t1 = now_ms();
-  TRY(spectral_step(P, P->steps[0], Du, z1, su.rho1, cu));       // STEP 4
+  TRY(spectral_step(P, P->steps[0], Du, z1, su.rho1, cu, 8));       // STEP 4
   {
     std::vector<double> z2 = cu[0];
     cu.erase(cu.begin());
-    TRY(spectral_step(P, P->steps[1], Du, z2, su.rho2, cu));     // STEP 5
+    TRY(spectral_step(P, P->steps[1], Du, z2, su.rho2, cu, 10));     // STEP 5
   }
   const double t2 = now_ms();
-  TRY(spectral_step(P, P->steps[2], Dv, z3, sv.rho1, cv));       // STEP 6
+  TRY(spectral_step(P, P->steps[2], Dv, z3, sv.rho1, cv, 12));       // STEP 6
   {
     std::vector<double> z4 = cv[0];
     cv.erase(cv.begin());
-    TRY(spectral_step(P, P->steps[3], Dv, z4, sv.rho2, cv));     // STEP 7
+    TRY(spectral_step(P, P->steps[3], Dv, z4, sv.rho2, cv, 14));     // STEP 7
   }
   const double t3 = now_ms();
   R.t_ms[1] = t2 - t1;
@@ -813,23 +841,32 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
   if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * n, &Wv));
   bool f;
-  if (c.u_rows) {
-    TRY(apply_step(P, P->steps[0], c.u_rows, U, ldu, Wu, m, false, &f));
-    R.fmm_used[0] = f;
-    TRY(apply_step(P, P->steps[1], c.u_rows, Wu, m, U, ldu, true, &f));
-    R.fmm_used[1] = f;
-  }
-  if (c.v_rows) {
-    TRY(apply_step(P, P->steps[2], c.v_rows, V, ldv, Wv, n, false, &f));
-    R.fmm_used[2] = f;
-    TRY(apply_step(P, P->steps[3], c.v_rows, Wv, n, V, ldv, true, &f));
-    R.fmm_used[3] = f;
+  for (int e = 0; e < 4; ++e) {
+    const bool uside = e < 2;
+    const int64_t rows = uside ? c.u_rows : c.v_rows;
+    if (!rows) continue;
+    double* in = uside ? (e == 0 ? U : Wu) : (e == 2 ? V : Wv);
+    double* out = uside ? (e == 0 ? Wu : U) : (e == 2 ? Wv : V);
+    const int64_t ldi = uside ? (e == 0 ? ldu : m) : (e == 2 ? ldv : n);
+    const int64_t ldo = uside ? (e == 0 ? m : ldu) : (e == 2 ? n : ldv);
+    TRY(apply_step(P, P->steps[e], rows, in, ldi, out, ldo, e == 1 || e == 3, &f, &R.apply_flops[e],
+                   2 * e));
+    R.fmm_used[e] = f;
+    if (f) {
+      R.fmm_levels[e] = P->fmm_last.L;
+      R.fmm_max_near[e] = P->fmm_last.max_near;
+    }
   }
   std::memcpy(h, sig_new.data(), size_t(m) * sizeof(double));
   SVD1_CUDA_TRY(cudaMemcpyAsync(sigma, h, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, P->st));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   SVD1_CUDA_TRY(cudaGetLastError());
   R.t_ms[3] = now_ms() - t3;
+  for (int e = 0; e < 4; ++e) {
+    const bool has = (e < 2 ? c.u_rows : c.v_rows) > 0;
+    R.apply_ms[e] = has ? ev_ms(P, 2 * e, 2 * e + 1) : 0.0;
+    R.spectral_ms[e] = P->steps[e].spectral_ms;
+  }
   R.t_ms[4] = now_ms() - t0;
   R.kernel_launches = P->launches - launches0;
   if (rep) *rep = R;
