@@ -152,6 +152,14 @@ svd1_status svd1_colnorms(svd1_plan_t plan, int64_t n, const double* d,
                           const int32_t* k, const double* tau, const double* zhat,
                           double* colnorm_out);
 
+/* Host-only introspection of the FMM plan the apply would build for the sorted
+ * sources d and roots mu_j = d[k_j] + tau_j (HOST pointers; no GPU needed).
+ * stats_out (8 int64): [0] tree depth L, [1] non-empty cells, [2] largest leaf,
+ * [3] largest near list (leaves), [4] near pairs, [5] M2L pairs,
+ * [6] algorithmic flops per row of U (2 * sum K*N), [7] GEMM tasks. */
+svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k,
+                                const double* tau, double eps, int64_t* stats_out);
+
 const char* svd1_status_string(svd1_status s);
 /* Library build identifier (for the bench/smoke evidence). */
 const char* svd1_version(void);

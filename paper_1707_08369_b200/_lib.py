@@ -61,6 +61,7 @@ svd1_cauchy_apply = _sig("svd1_cauchy_apply", [vp, i64, i64, vp, vp, vp, vp, vp,
 svd1_secular_solve = _sig("svd1_secular_solve", [vp, i64, vp, vp, dbl, vp, vp, C.POINTER(i32)])
 svd1_loewner = _sig("svd1_loewner", [vp, i64, vp, vp, vp, dbl, vp, vp])
 svd1_colnorms = _sig("svd1_colnorms", [vp, i64, vp, vp, vp, vp, vp])
+svd1_fmm_tree_stats = _sig("svd1_fmm_tree_stats", [i64, vp, vp, vp, dbl, vp])
 lib.svd1_status_string.argtypes = [status_t]
 lib.svd1_status_string.restype = C.c_char_p
 lib.svd1_version.argtypes = []
@@ -68,7 +69,7 @@ lib.svd1_version.restype = C.c_char_p
 
 EXPORTS = ["svd1_plan_create", "svd1_plan_destroy", "svd1_update", "svd1_project",
            "svd1_update_projected", "svd1_cauchy_apply", "svd1_secular_solve", "svd1_loewner",
-           "svd1_colnorms", "svd1_status_string", "svd1_version"]
+           "svd1_colnorms", "svd1_fmm_tree_stats", "svd1_status_string", "svd1_version"]
 
 FORCE_DIRECT = 0x1
 FORCE_FMM = 0x2
@@ -80,3 +81,18 @@ def status_string(code: int) -> str:
 
 def version() -> str:
     return lib.svd1_version().decode()
+
+
+def fmm_tree_stats(d, k, tau, eps=1e-10):
+    """Host-only FMM plan statistics (numpy inputs): dict of the 8 stats of svd1.h."""
+    import numpy as np
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    k = np.ascontiguousarray(k, dtype=np.int32)
+    tau = np.ascontiguousarray(tau, dtype=np.float64)
+    out = np.zeros(8, dtype=np.int64)
+    code = svd1_fmm_tree_stats(d.size, d.ctypes.data, k.ctypes.data, tau.ctypes.data, float(eps),
+                               out.ctypes.data)
+    if code:
+        raise RuntimeError(status_string(code))
+    keys = ["L", "cells", "max_leaf", "max_near", "near_pairs", "m2l_pairs", "flops_per_row", "tasks"]
+    return dict(zip(keys, (int(x) for x in out)))

@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
       switch (D.kind) {
         case OP_P2M: {  // Phi~_X[j] += zhat_i U_i / (t_j (x_i - c_X) - 3 r_X)
           const FmmCell X = cells[D.a];
-          const int s = X.lo + i;
+          const int s = X.slo + i;
           v = zhat[s] / (t[j] * (d[s] - X.c) - 3.0 * X.r);
           break;
         }
@@ -224,13 +224,13 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
         }
         case OP_L2P: {  // leaf Y (b): i = node, j = target
           const FmmCell Y = cells[D.b];
-          const int jt = Y.lo + j;
+          const int jt = Y.tlo + j;
           v = lagrange(t, w, p, i, ((d[k[jt]] - Y.c) + tau[jt]) / Y.r) * cs[jt];
           break;
         }
         default: {  // OP_P2P: source leaf X (a), target leaf Y (b)
           const FmmCell X = cells[D.a], Y = cells[D.b];
-          const int s = X.lo + i, jt = Y.lo + j;
+          const int s = X.slo + i, jt = Y.tlo + j;
           v = (zhat[s] * cs[jt]) / ((d[s] - d[k[jt]]) - tau[jt]);
           break;
         }
@@ -241,87 +241,138 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
 }
 
 // ------------------------------------------------------------------- K6-K10
-// out (64 rows x N<=32) = sum_t in_t (64 x K_t<=32) * op_t (K_t x N)
-constexpr int TBM = 64, TBK = 32, TBN = 32;
-constexpr int TLDA = TBK + 4, TLDB = TBN + 4;
+// One FMM pass = a batch of "gathered small GEMMs": for task T and a tile of BM rows,
+//   out[:, T.col0 : T.col0 + N] = sum_t in_t[:, col0_t : col0_t + K_t] * op_t (K_t x N).
+// in/out are U (columns through src/dst maps) or the expansion matrices Phi/Psi.
+// K is streamed in chunks of KC through a 2-stage cp.async pipeline; each warp owns a
+// 32 x 16 output tile (4 x 2 DMMA m8n8k4 fragments).  BN = 16: 8 warps down the rows
+// (BM = 256); BN = 32: 4 x 2 warps (BM = 128).
+constexpr int KC = 16;
+constexpr int ALD = KC + 4;  // 20 doubles: conflict-free A fragment loads
 
-__global__ void __launch_bounds__(128) fmm_task_kernel(
-    const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int64_t rows, int p,
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 8 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int WN = BN / 16;      // warps along N
+  static constexpr int WM = 8 / WN;       // warps along M
+  static constexpr int BM = 32 * WM;      // rows per CTA
+  static constexpr int BLD = BN + 4;      // B row stride (doubles)
+  static constexpr int A_ELEMS = BM * ALD;
+  static constexpr int B_ELEMS = KC * BLD;
+  static constexpr int SMEM = 2 * (A_ELEMS + B_ELEMS) * 8;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(256) fmm_gemm_kernel(
+    const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int64_t rows,
     const double* __restrict__ ops, const double* __restrict__ U_in, int64_t ld_in,
     const int32_t* __restrict__ src, double* __restrict__ U_out, int64_t ld_out,
-    const int32_t* __restrict__ dst, double* __restrict__ phi, double* __restrict__ psi) {
-  __shared__ double As[TBM * TLDA];
-  __shared__ double Bs[TBK * TLDB];
+    const int32_t* __restrict__ dst, double* __restrict__ phi, double* __restrict__ psi, int64_t ldE) {
+  using G = GemmCfg<BN>;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                        // [2][BM][ALD]
+  double* Bs = smem + 2 * G::A_ELEMS;       // [2][KC][BLD]
   const FmmTask T = tasks[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t row0 = int64_t(blockIdx.y) * TBM;
-  const int64_t nrow = (rows - row0 < TBM) ? (rows - row0) : int64_t(TBM);
-  double acc[2][4][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  for (int ti = T.t_begin; ti < T.t_end; ++ti) {
-    const FmmTerm R = terms[ti];
-    const int K = R.K, K4 = (K + 3) & ~3;
-    __syncthreads();
-    // A tile
-    if (R.in_kind == IO_U) {
-      for (int e = tid; e < TBM * TBK; e += 128) {
-        const int rr = e >> 5, kk = e & 31;
-        if (kk >= K4) continue;
-        double v = 0.0;
-        if (rr < nrow && kk < K) {
-          const int col = src ? src[R.in_idx + kk] : R.in_idx + kk;
-          v = __ldg(U_in + (row0 + rr) * ld_in + col);
-        }
-        As[rr * TLDA + kk] = v;
-      }
-    } else {
-      const double* base = (R.in_kind == IO_PHI ? phi : psi) + (int64_t(R.in_idx) * rows + row0) * p;
-      for (int e = tid; e < TBM * TBK; e += 128) {
-        const int rr = e >> 5, kk = e & 31;
-        if (kk >= K4) continue;
-        As[rr * TLDA + kk] = (rr < nrow && kk < K) ? base[int64_t(rr) * p + kk] : 0.0;
-      }
+  const int wm = warp % G::WM, wn = warp / G::WM;
+  const int64_t row0 = int64_t(blockIdx.y) * G::BM;
+  const int nrow = int(rows - row0 < G::BM ? rows - row0 : G::BM);
+
+  // stage iterator over (term, K-chunk)
+  int ti = T.t_begin, k0 = 0;
+  auto load_stage = [&](int buf, int term, int kk0) {
+    const FmmTerm R = terms[term];
+    double* a = As + buf * G::A_ELEMS;
+    double* b = Bs + buf * G::B_ELEMS;
+    const double* base = R.in_kind == IO_U ? U_in : (R.in_kind == IO_PHI ? phi : psi);
+    const int64_t ld = R.in_kind == IO_U ? ld_in : ldE;
+#pragma unroll 4
+    for (int e = tid; e < G::BM * KC; e += 256) {
+      const int rr = e / KC, kk = e % KC;
+      const int k = kk0 + kk;
+      const bool ok = rr < nrow && k < R.K;
+      int col = R.col0 + (ok ? k : 0);
+      if (R.in_kind == IO_U && src) col = src[ok ? col : R.col0];
+      cp_async8(a + rr * ALD + kk, base + (row0 + (ok ? rr : 0)) * ld + col, ok);
     }
-    // B = op (K x N, row-major, ld N)
-    const double* op = ops + R.op_off;
-    for (int e = tid; e < TBK * TBN; e += 128) {
-      const int kk = e >> 5, jj = e & 31;
-      if (kk >= K4) continue;
-      Bs[kk * TLDB + jj] = (kk < K && jj < T.N) ? __ldg(op + kk * T.N + jj) : 0.0;
+    for (int e = tid; e < KC * BN; e += 256) {
+      const int kk = e / BN, jj = e % BN;
+      const int k = kk0 + kk;
+      const bool ok = k < R.K && jj < T.N;
+      cp_async8(b + kk * G::BLD + jj, ops + R.op_off + (ok ? int64_t(k) * R.op_ld + T.op_col0 + jj : 0), ok);
     }
-    __syncthreads();
-    for (int kk = 0; kk < K4; kk += 4) {
-      double af[2], bf[4];
+  };
+  double acc[4][2][2];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) af[mt] = As[(warp * 16 + mt * 8 + (lane >> 2)) * TLDA + kk + (lane & 3)];
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(kk + (lane & 3)) * TLDB + nt * 8 + (lane >> 2)];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
-    }
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  if (ti < T.t_end) {
+    load_stage(0, ti, 0);
+    cp_async_commit();
   }
-  // store
+  int buf = 0;
+  while (ti < T.t_end) {
+    // next stage
+    int nti = ti, nk0 = k0 + KC;
+    if (nk0 >= terms[ti].K) {
+      ++nti;
+      nk0 = 0;
+    }
+    const bool more = nti < T.t_end;
+    if (more) {
+      load_stage(buf ^ 1, nti, nk0);
+      cp_async_commit();
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncthreads();
+    const double* a = As + buf * G::A_ELEMS;
+    const double* b = Bs + buf * G::B_ELEMS;
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
-    const int rr = warp * 16 + mt * 8 + (lane >> 2);
+    for (int kk = 0; kk < KC; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) af[mt] = a[(wm * 32 + mt * 8 + (lane >> 2)) * ALD + kk + (lane & 3)];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) bf[nt] = b[(kk + (lane & 3)) * G::BLD + wn * 16 + nt * 8 + (lane >> 2)];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+    }
+    __syncthreads();  // buffer `buf` is refilled by the next iteration's prefetch
+    ti = nti;
+    k0 = nk0;
+    buf ^= 1;
+  }
+  // epilogue
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int rr = wm * 32 + mt * 8 + (lane >> 2);
     if (rr >= nrow) continue;
     const int64_t r = row0 + rr;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
+    for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int jj = nt * 8 + (lane & 3) * 2 + h;
+        const int jj = wn * 16 + nt * 8 + (lane & 3) * 2 + h;
         if (jj >= T.N) continue;
+        const int col = T.col0 + jj;
         if (T.out_kind == IO_U) {
-          U_out[r * ld_out + (dst ? dst[T.out_idx + jj] : T.out_idx + jj)] = acc[mt][nt][h];
+          U_out[r * ld_out + (dst ? dst[col] : col)] = acc[mt][nt][h];
         } else {
-          double* base = (T.out_kind == IO_PHI ? phi : psi) + int64_t(T.out_idx) * rows * p;
-          base[r * p + jj] = acc[mt][nt][h];
+          (T.out_kind == IO_PHI ? phi : psi)[r * ldE + col] = acc[mt][nt][h];
         }
       }
     }
@@ -380,14 +431,33 @@ svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cell
   return SVD1_OK;
 }
 
-svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
-                          int p, const double* ops, const double* U_in, int64_t ld_in,
+template <int BN>
+svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
+                        const double* ops, const double* U_in, int64_t ld_in, const int32_t* src,
+                        double* U_out, int64_t ld_out, const int32_t* dst, double* phi, double* psi,
+                        int64_t ldE, cudaStream_t st) {
+  using G = GemmCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    SVD1_CUDA_TRY(cudaFuncSetAttribute(fmm_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+    attr = true;
+  }
+  dim3 grid(unsigned(n_tasks), unsigned((rows + G::BM - 1) / G::BM));
+  fmm_gemm_kernel<BN><<<grid, 256, G::SMEM, st>>>(tasks, terms, rows, ops, U_in, ld_in, src, U_out,
+                                                  ld_out, dst, phi, psi, ldE);
+  return SVD1_OK;
+}
+
+svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
+                          int64_t rows, const double* ops, const double* U_in, int64_t ld_in,
                           const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
-                          double* phi, double* psi, cudaStream_t st, int64_t* launches) {
+                          double* phi, double* psi, int64_t ldE, cudaStream_t st, int64_t* launches) {
   if (n_tasks <= 0 || rows <= 0) return SVD1_OK;
-  dim3 grid(unsigned(n_tasks), unsigned((rows + TBM - 1) / TBM));
-  fmm_task_kernel<<<grid, 128, 0, st>>>(tasks, terms, rows, p, ops, U_in, ld_in, src, U_out, ld_out,
-                                        dst, phi, psi);
+  svd1_status s = bn <= 16 ? launch_gemm<16>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, src, U_out,
+                                             ld_out, dst, phi, psi, ldE, st)
+                           : launch_gemm<32>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, src, U_out,
+                                             ld_out, dst, phi, psi, ldE, st);
+  if (s != SVD1_OK) return s;
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;

@@ -109,6 +109,7 @@ struct FmmHost {
   std::vector<FmmTerm> terms;
   std::vector<FmmTask> tasks;
   std::vector<int> pass_begin;  // task index where each pass starts (+ end sentinel)
+  std::vector<int> pass_bn;     // tile width (16 or 32) of each pass
   int64_t ops_elems = 0;
   int64_t flops_per_row = 0;    // algorithmic flops per row of U (2 * sum K*N over terms)
   int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
@@ -217,65 +218,157 @@ int choose_p(double eps) {
 }
 
 // ------------------------------------------------------------------ FMM tree
-// Count-balanced binary tree over active indices [0, na) (cells = index ranges,
-// geometry = hull of the sources d_i and targets mu_j in the range); interaction
-// lists by symmetric admissibility |c_X - c_Y| >= max(3 r_X + r_Y, r_X + 3 r_Y)
-// (reduces to the paper's |x0 - y0| > 4r at equal radii).
-void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<double>& da,
-                    const std::vector<double>& mu) {
-  F = FmmHost();
-  int L = 0;
-  while ((int64_t(na) + (int64_t(1) << L) - 1) / (int64_t(1) << L) > leaf) ++L;
+// Binary tree of depth L over the active indices [0, na) (cells = index ranges;
+// geometry = hull of the sources d_i and targets mu_j of the range).
+// Splits are count-balanced (the tree of P:706 generalised to non-uniform spectra),
+// except that a cell whose points have a gap of at least half its width is split
+// at that gap when the capacities allow (isolated outlier
+// eigenvalues, e.g. the large singular values a rank-1 update creates, would
+// otherwise blow one leaf up to the whole spectrum).  Leaves hold <= s points.
+// Interaction lists use the symmetric admissibility
+//   |c_X - c_Y| >= max(3 r_X + r_Y, r_X + 3 r_Y)
+// (the paper's |x0 - y0| > 4r at equal radii).
+namespace {
+
+// pts: the 2n merged points (sorted); is_src[q]; nsrc[q] = sources among pts[0, q).
+struct Merged {
+  std::vector<double> pts;
+  std::vector<int32_t> nsrc;
+};
+
+Merged merge_points(const std::vector<double>& da, const std::vector<double>& mu) {
+  const int n = int(da.size());
+  struct Pt {
+    double v;
+    int type, idx;  // type 0 = source, 1 = target
+  };
+  std::vector<Pt> all;
+  all.reserve(2 * n);
+  for (int i = 0; i < n; ++i) all.push_back({da[i], 0, i});
+  for (int j = 0; j < n; ++j) all.push_back({mu[j], 1, j});
+  std::sort(all.begin(), all.end(), [](const Pt& a, const Pt& b) {
+    if (a.v != b.v) return a.v < b.v;
+    if (a.type != b.type) return a.type < b.type;
+    return a.idx < b.idx;
+  });
+  Merged M;
+  M.pts.resize(2 * n);
+  M.nsrc.resize(2 * n + 1);
+  M.nsrc[0] = 0;
+  for (int q = 0; q < 2 * n; ++q) {
+    M.pts[q] = all[q].v;
+    M.nsrc[q + 1] = M.nsrc[q] + (all[q].type == 0);
+  }
+  return M;
+}
+
+bool fmm_cells(FmmHost& F, int s, int L, const Merged& M) {
+  const int np = int(M.pts.size());
+  const int64_t leafcap = 2 * int64_t(s);  // merged points per leaf (<= s+1 targets when interlaced)
   F.L = L;
   F.ncells = (1 << (L + 1)) - 1;
-  F.cells.resize(F.ncells);
+  F.cells.assign(F.ncells, FmmCell{0.0, 0.0, 0, 0, 0, 0, 0, 0});
   F.cells[0].lo = 0;
-  F.cells[0].hi = na;
-  for (int l = 0; l < L; ++l)
+  F.cells[0].hi = np;
+  const std::vector<double>& P = M.pts;
+  for (int l = 0; l < L; ++l) {
+    const int64_t cap = leafcap << (L - l - 1);  // capacity of each child
     for (int i = 0; i < (1 << l); ++i) {
       const int c = (1 << l) - 1 + i;
-      const int lo = F.cells[c].lo, hi = F.cells[c].hi, mid = lo + (hi - lo) / 2;
+      const int lo = F.cells[c].lo, hi = F.cells[c].hi, nc = hi - lo;
+      int t;
+      if (nc <= 1) {
+        t = hi;
+      } else {
+        const int tmin = int(std::max<int64_t>(lo + 1, hi - cap));
+        const int tmax = int(std::min<int64_t>(hi - 1, lo + cap));
+        if (tmin > tmax) return false;
+        t = std::min(std::max(lo + nc / 2, tmin), tmax);
+        const double width = P[hi - 1] - P[lo];
+        double best = -1.0;
+        int tb = t;
+        for (int u = tmin; u <= tmax; ++u) {
+          const double g = P[u] - P[u - 1];
+          if (g > best) {
+            best = g;
+            tb = u;
+          }
+        }
+        if (best >= 0.5 * width) t = tb;  // split isolated points off at a dominant gap
+      }
       F.cells[2 * c + 1].lo = lo;
-      F.cells[2 * c + 1].hi = mid;
-      F.cells[2 * c + 2].lo = mid;
+      F.cells[2 * c + 1].hi = t;
+      F.cells[2 * c + 2].lo = t;
       F.cells[2 * c + 2].hi = hi;
     }
+  }
+  for (int i = 0; i < (1 << L); ++i) {
+    const FmmCell& C = F.cells[(1 << L) - 1 + i];
+    if (C.hi - C.lo > leafcap) return false;
+  }
   for (int c = 0; c < F.ncells; ++c) {
     FmmCell& C = F.cells[c];
-    double a, b;
-    if (C.hi > C.lo) {
-      a = std::min(da[C.lo], mu[C.lo]);
-      b = std::max(da[C.hi - 1], mu[C.hi - 1]);
-    } else {
-      a = b = 0.0;
-    }
+    C.slo = M.nsrc[C.lo];
+    C.shi = M.nsrc[C.hi];
+    C.tlo = C.lo - C.slo;
+    C.thi = C.hi - C.shi;
+    if (C.hi <= C.lo) continue;
+    const double a = P[C.lo], b = P[C.hi - 1];
     C.c = 0.5 * (a + b);
     double r = std::max(C.c - a, b - C.c);
-    r = std::max(r, std::max(std::fabs(C.c) * 0x1.0p-50, 1e-300));
-    C.r = r;
+    C.r = std::max(r, std::max(std::fabs(C.c) * 0x1.0p-50, 1e-300));
   }
+  return true;
+}
+
+void fmm_lists(FmmHost& F, int p) {
+  const int L = F.L;
+  auto nonempty = [&](int c) { return F.cells[c].hi > F.cells[c].lo; };
+  auto has_src = [&](int c) { return F.cells[c].shi > F.cells[c].slo; };
+  auto has_tgt = [&](int c) { return F.cells[c].thi > F.cells[c].tlo; };
   auto adm = [&](int x, int y) {
     const FmmCell &X = F.cells[x], &Y = F.cells[y];
-    const double dist = std::fabs(X.c - Y.c);
-    return dist >= std::max(3.0 * X.r + Y.r, X.r + 3.0 * Y.r);
+    return std::fabs(X.c - Y.c) >= std::max(3.0 * X.r + Y.r, X.r + 3.0 * Y.r);
   };
+  // Dual-tree traversal (cells of different levels may interact): a pair is
+  // admissible -> M2L into the target cell; two leaves -> near field (P2P);
+  // otherwise split the larger cell.  Needed for graded spectra, where a wide
+  // target cell only separates from the narrow sources below it at a finer level.
   std::vector<std::vector<int>> near(F.ncells), m2l(F.ncells);
-  near[0].push_back(0);
-  for (int l = 1; l <= L; ++l)
-    for (int i = 0; i < (1 << l); ++i) {
-      const int y = (1 << l) - 1 + i, par = (y - 1) / 2;
-      for (int xp : near[par])
-        for (int x : {2 * xp + 1, 2 * xp + 2}) {
-          if (F.cells[x].hi <= F.cells[x].lo) continue;
-          if (x != y && adm(x, y)) m2l[y].push_back(x);
-          else near[y].push_back(x);
-        }
+  const int first_leaf = (1 << L) - 1;
+  auto is_leaf = [&](int c) { return c >= first_leaf; };
+  std::vector<std::pair<int, int>> stack;
+  stack.push_back({0, 0});
+  while (!stack.empty()) {
+    const auto [x, y] = stack.back();
+    stack.pop_back();
+    if (!has_src(x) || !has_tgt(y)) continue;
+    if (x != y && adm(x, y)) {
+      m2l[y].push_back(x);
+      continue;
     }
+    if (is_leaf(x) && is_leaf(y)) {
+      near[y].push_back(x);
+      continue;
+    }
+    const bool split_x = is_leaf(y) || (!is_leaf(x) && F.cells[x].r > F.cells[y].r);
+    if (split_x) {
+      stack.push_back({2 * x + 2, y});
+      stack.push_back({2 * x + 1, y});
+    } else {
+      stack.push_back({x, 2 * y + 2});
+      stack.push_back({x, 2 * y + 1});
+    }
+  }
+  for (int c = 0; c < F.ncells; ++c) {
+    std::sort(near[c].begin(), near[c].end());
+    std::sort(m2l[c].begin(), m2l[c].end());
+  }
   std::vector<char> has_psi(F.ncells, 0);
   for (int l = 1; l <= L; ++l)
     for (int i = 0; i < (1 << l); ++i) {
       const int y = (1 << l) - 1 + i;
-      has_psi[y] = !m2l[y].empty() || (l >= 2 && has_psi[(y - 1) / 2]);
+      has_psi[y] = has_tgt(y) && (!m2l[y].empty() || (l >= 2 && has_psi[(y - 1) / 2]));
     }
   auto add_op = [&](int kind, int a, int b, int rows, int cols) {
     FmmOpDesc D;
@@ -289,82 +382,144 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
     F.ops.push_back(D);
     return D.off;
   };
-  auto add_term = [&](int in_kind, int in_idx, int K, int64_t off, int N) {
+  auto add_term = [&](int in_kind, int col0, int K, int64_t off, int N) {
     FmmTerm t;
     t.in_kind = in_kind;
-    t.in_idx = in_idx;
+    t.col0 = col0;
     t.K = K;
-    t.pad = 0;
+    t.op_ld = N;
     t.op_off = off;
     F.terms.push_back(t);
     F.flops_per_row += 2ll * K * N;
   };
-  auto begin_task = [&](int out_kind, int out_idx, int N) {
-    FmmTask T;
-    T.out_kind = out_kind;
-    T.out_idx = out_idx;
-    T.N = N;
-    T.t_begin = int(F.terms.size());
-    T.t_end = T.t_begin;
-    T.pad = 0;
-    F.tasks.push_back(T);
+  int tb = 0;
+  auto begin_task = [&]() { tb = int(F.terms.size()); };
+  // tasks wider than 32 columns are split along N (they share their terms)
+  auto end_task = [&](int out_kind, int col0, int N) {
+    for (int c0 = 0; c0 < N; c0 += 32) {
+      FmmTask T;
+      T.out_kind = out_kind;
+      T.col0 = col0 + c0;
+      T.N = std::min(32, N - c0);
+      T.t_begin = tb;
+      T.t_end = int(F.terms.size());
+      T.op_col0 = c0;
+      F.tasks.push_back(T);
+    }
   };
-  auto end_task = [&]() { F.tasks.back().t_end = int(F.terms.size()); };
+  // consecutive partners -> one term over adjacent columns of U (sources) or Phi
+  auto add_runs = [&](const std::vector<int>& xs, int in_kind, int op_kind, int y, int N) {
+    size_t a = 0;
+    while (a < xs.size()) {
+      size_t b = a;
+      if (in_kind == IO_U) {
+        while (b + 1 < xs.size() && F.cells[xs[b + 1]].slo == F.cells[xs[b]].shi) ++b;
+      } else {
+        while (b + 1 < xs.size() && xs[b + 1] == xs[b] + 1) ++b;
+      }
+      int K = 0;
+      int64_t off0 = -1;
+      for (size_t q = a; q <= b; ++q) {
+        const int x = xs[q];
+        const int kx = in_kind == IO_U ? F.cells[x].shi - F.cells[x].slo : p;
+        const int64_t off = add_op(op_kind, x, y, kx, N);
+        if (off0 < 0) off0 = off;
+        K += kx;
+      }
+      add_term(in_kind, in_kind == IO_U ? F.cells[xs[a]].slo : xs[a] * p, K, off0, N);
+      a = b + 1;
+    }
+  };
   const int lf0 = (1 << L) - 1, nleaf = 1 << L;
   if (L >= 1) {
-    // P2M (STEP 5), scaled far field
+    // P2M (STEP 5) in the scaled far-field form
     F.pass_begin.push_back(int(F.tasks.size()));
+    F.pass_bn.push_back(p);
     for (int i = 0; i < nleaf; ++i) {
-      const int x = lf0 + i, sx = F.cells[x].hi - F.cells[x].lo;
-      if (sx <= 0) continue;
-      begin_task(IO_PHI, x, p);
-      add_term(IO_U, F.cells[x].lo, sx, add_op(OP_P2M, x, x, sx, p), p);
-      end_task();
+      const int x = lf0 + i;
+      if (!has_src(x)) continue;
+      const int sx = F.cells[x].shi - F.cells[x].slo;
+      begin_task();
+      add_term(IO_U, F.cells[x].slo, sx, add_op(OP_P2M, x, x, sx, p), p);
+      end_task(IO_PHI, x * p, p);
     }
-    // M2M (STEP 6), levels L-1 .. 1
+    // M2M (STEP 6), levels L-1 .. 1 (operator re-derived)
     for (int l = L - 1; l >= 1; --l) {
       F.pass_begin.push_back(int(F.tasks.size()));
+      F.pass_bn.push_back(p);
       for (int i = 0; i < (1 << l); ++i) {
         const int c = (1 << l) - 1 + i;
-        begin_task(IO_PHI, c, p);
-        for (int ch : {2 * c + 1, 2 * c + 2})
-          if (F.cells[ch].hi > F.cells[ch].lo) add_term(IO_PHI, ch, p, add_op(OP_M2M, ch, c, p, p), p);
-        end_task();
+        if (!has_src(c)) continue;
+        std::vector<int> ch;
+        for (int x : {2 * c + 1, 2 * c + 2})
+          if (has_src(x)) ch.push_back(x);
+        begin_task();
+        add_runs(ch, IO_PHI, OP_M2M, c, p);
+        end_task(IO_PHI, c * p, p);
       }
     }
-    // downward: L2L + M2L (STEP 8), levels 1 .. L
+    // downward: L2L + M2L (STEP 8), levels 1 .. L (M2L re-derived)
     for (int l = 1; l <= L; ++l) {
       F.pass_begin.push_back(int(F.tasks.size()));
+      F.pass_bn.push_back(p);
       for (int i = 0; i < (1 << l); ++i) {
         const int y = (1 << l) - 1 + i;
         if (!has_psi[y]) continue;
-        begin_task(IO_PSI, y, p);
+        begin_task();
         const int par = (y - 1) / 2;
-        if (l >= 2 && has_psi[par]) add_term(IO_PSI, par, p, add_op(OP_L2L, par, y, p, p), p);
-        for (int x : m2l[y]) {
-          add_term(IO_PHI, x, p, add_op(OP_M2L, x, y, p, p), p);
-          ++F.n_m2l_pairs;
-        }
-        end_task();
+        if (l >= 2 && has_psi[par]) add_term(IO_PSI, par * p, p, add_op(OP_L2L, par, y, p, p), p);
+        add_runs(m2l[y], IO_PHI, OP_M2L, y, p);
+        F.n_m2l_pairs += int(m2l[y].size());
+        end_task(IO_PSI, y * p, p);
       }
     }
   }
   // final: L2P (STEP 9) + P2P near field (STEP 10)
   F.pass_begin.push_back(int(F.tasks.size()));
+  int bn_final = 16;
   for (int i = 0; i < nleaf; ++i) {
-    const int y = lf0 + i, ty = F.cells[y].hi - F.cells[y].lo;
-    if (ty <= 0) continue;
-    begin_task(IO_U, F.cells[y].lo, ty);
-    if (has_psi[y]) add_term(IO_PSI, y, p, add_op(OP_L2P, y, y, p, ty), ty);
-    for (int x : near[y]) {
-      const int sx = F.cells[x].hi - F.cells[x].lo;
-      add_term(IO_U, F.cells[x].lo, sx, add_op(OP_P2P, x, y, sx, ty), ty);
-      ++F.n_near_pairs;
-    }
+    const int y = lf0 + i;
+    if (!has_tgt(y)) continue;
+    const int ty = F.cells[y].thi - F.cells[y].tlo;
+    bn_final = std::max(bn_final, std::min(ty, 32));
+    begin_task();
+    if (has_psi[y]) add_term(IO_PSI, y * p, p, add_op(OP_L2P, y, y, p, ty), ty);
+    add_runs(near[y], IO_U, OP_P2P, y, ty);
+    F.n_near_pairs += int(near[y].size());
     F.max_near = std::max<int>(F.max_near, int(near[y].size()));
-    end_task();
+    end_task(IO_U, F.cells[y].tlo, ty);
   }
+  F.pass_bn.push_back(bn_final);
   F.pass_begin.push_back(int(F.tasks.size()));
+  for (int& bn : F.pass_bn) bn = bn <= 16 ? 16 : 32;
+  (void)nonempty;
+}
+
+}  // namespace
+
+void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<double>& da,
+                    const std::vector<double>& mu) {
+  const Merged M = merge_points(da, mu);
+  int L0 = 0;
+  while ((2 * int64_t(na) + (int64_t(1) << L0) - 1) / (int64_t(1) << L0) > 2 * leaf) ++L0;
+  FmmHost best;
+  bool have = false;
+  for (int L = L0; L <= L0 + 2 && L <= 22; ++L) {
+    FmmHost F2;
+    if (!fmm_cells(F2, leaf, L, M)) {
+      if (std::getenv("SVD1_DEBUG")) fprintf(stderr, "[svd1] fmm L=%d infeasible\n", L);
+      continue;
+    }
+    fmm_lists(F2, p);
+    if (std::getenv("SVD1_DEBUG"))
+      fprintf(stderr, "[svd1] fmm L=%d flops/row=%lld max_near=%d m2l=%d near=%d\n", L,
+              (long long)F2.flops_per_row, F2.max_near, F2.n_m2l_pairs, F2.n_near_pairs);
+    if (!have || F2.flops_per_row < best.flops_per_row) {
+      best = std::move(F2);
+      have = true;
+    }
+  }
+  F = std::move(best);
 }
 
 // Cauchy apply of one step: U_out[:, dst[j]] = cs_j sum_i U_in[:, src[i]] zhat_i / ((d_i - d_kj) - tau_j)
@@ -397,7 +552,8 @@ svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, 
   TRY(upload(P, P->fmm_tasks, F.tasks, &dk));
   double *ops, *phi, *psi;
   TRY(P->ops.get<double>(size_t(F.ops_elems), &ops));
-  const size_t exp_elems = size_t(F.ncells) * size_t(rows) * size_t(p);
+  const int64_t ldE = int64_t(F.ncells) * p;
+  const size_t exp_elems = size_t(ldE) * size_t(rows);
   TRY(P->phi.get<double>(exp_elems, &phi));
   TRY(P->psi.get<double>(exp_elems, &psi));
   TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, ops, P->st,
@@ -406,12 +562,12 @@ svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, 
   if (dbg) {  // host-side validation of the task lists
     for (const FmmTask& T : F.tasks) {
       if (T.N < 1 || T.N > 32 || T.t_begin < 0 || T.t_end > int(F.terms.size()) || T.t_begin > T.t_end)
-        fprintf(stderr, "[svd1] bad task out=%d/%d N=%d terms=[%d,%d)\n", T.out_kind, T.out_idx, T.N,
+        fprintf(stderr, "[svd1] bad task out=%d/%d N=%d terms=[%d,%d)\n", T.out_kind, T.col0, T.N,
                 T.t_begin, T.t_end);
       for (int t = T.t_begin; t < T.t_end; ++t) {
         const FmmTerm& R = F.terms[t];
-        if (R.K < 1 || R.K > 32 || R.op_off < 0 || R.op_off + int64_t(R.K) * T.N > F.ops_elems)
-          fprintf(stderr, "[svd1] bad term %d: kind=%d idx=%d K=%d off=%lld\n", t, R.in_kind, R.in_idx,
+        if (R.K < 1 || R.op_ld != T.N || R.op_off < 0 || R.op_off + int64_t(R.K) * T.N > F.ops_elems)
+          fprintf(stderr, "[svd1] bad term %d: kind=%d col0=%d K=%d off=%lld\n", t, R.in_kind, R.col0,
                   R.K, (long long)R.op_off);
       }
     }
@@ -420,8 +576,8 @@ svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, 
   }
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
-    TRY(fmm_run_tasks(e - b, dk + b, dt, rows, p, ops, U_in, ld_in, d_src, U_out, ld_out, d_dst, phi,
-                      psi, P->st, &P->launches));
+    TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, ops, U_in, ld_in, d_src, U_out, ld_out,
+                      d_dst, phi, psi, ldE, P->st, &P->launches));
     if (dbg) {
       cudaError_t err = cudaStreamSynchronize(P->st);
       fprintf(stderr, "[svd1] pass %zu tasks [%d,%d): %s\n", s, b, e, cudaGetErrorString(err));
@@ -910,6 +1066,35 @@ svd1_status svd1_cauchy_apply(svd1_plan_t P, int64_t rows, int64_t n, const doub
                  nullptr, dh, mu, p, &used));
   if (fmm_used) *fmm_used = used ? 1 : 0;
   SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k, const double* tau,
+                                double eps, int64_t* st) {
+  if (n <= 0 || !d || !k || !tau || !st || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
+  const int p = choose_p(eps);
+  const int leaf = std::min(2 * p, kMaxLeaf);
+  std::vector<double> dh(d, d + n), mu(n);
+  for (int64_t j = 0; j < n; ++j) {
+    if (k[j] < 0 || k[j] >= n) return SVD1_E_INVALID;
+    mu[j] = dh[k[j]] + tau[j];
+  }
+  FmmHost F;
+  fmm_build_host(F, int(n), leaf, p, dh, mu);
+  int64_t nonempty = 0, max_leaf = 0;
+  for (int c = 0; c < F.ncells; ++c) nonempty += F.cells[c].hi > F.cells[c].lo;
+  for (int i = 0; i < (1 << F.L); ++i) {
+    const FmmCell& C = F.cells[(1 << F.L) - 1 + i];
+    max_leaf = std::max<int64_t>(max_leaf, std::max(C.shi - C.slo, C.thi - C.tlo));
+  }
+  st[0] = F.L;
+  st[1] = nonempty;
+  st[2] = max_leaf;
+  st[3] = F.max_near;
+  st[4] = F.n_near_pairs;
+  st[5] = F.n_m2l_pairs;
+  st[6] = F.flops_per_row;
+  st[7] = int64_t(F.tasks.size());
   return SVD1_OK;
 }
 

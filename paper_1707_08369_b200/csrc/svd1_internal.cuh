@@ -72,9 +72,12 @@ svd1_status passthrough(int64_t rows, int nq, const double* U_in, int64_t ld_in,
                         int64_t* launches);
 
 // ---------------------------------------------------------------- FMM
-struct FmmCell {      // geometry of one tree cell (index range over active points)
-  double c, r;        // centre and radius of the hull of {d_i, mu_j : i, j in [lo, hi)}
-  int32_t lo, hi;
+struct FmmCell {      // one tree cell: a contiguous range [lo, hi) of the merged sorted
+                      // sequence of sources d_i and targets mu_j (2 n points)
+  double c, r;        // centre and radius of the hull of its points
+  int32_t lo, hi;     // merged range
+  int32_t slo, shi;   // its sources  d_slo .. d_{shi-1}
+  int32_t tlo, thi;   // its targets mu_tlo .. mu_{thi-1}
 };
 enum FmmOpKind : int32_t { OP_P2M = 0, OP_M2M = 1, OP_M2L = 2, OP_L2L = 3, OP_L2P = 4, OP_P2P = 5 };
 struct FmmOpDesc {    // one operator matrix to build: rows x cols, row-major at ops + off
@@ -83,27 +86,31 @@ struct FmmOpDesc {    // one operator matrix to build: rows x cols, row-major at
   int64_t off;
 };
 enum FmmIoKind : int32_t { IO_U = 0, IO_PHI = 1, IO_PSI = 2 };
-struct FmmTerm {      // in (rows x K) * op (K x N)
-  int32_t in_kind;    // IO_U (gather src[lo..lo+K)) or IO_PHI/IO_PSI (cell block)
-  int32_t in_idx;     // cell id, or first active index for IO_U
+// Expansions are stored as row-major matrices Phi, Psi (rows x ldE, ldE = ncells * p):
+// cell c's p coefficients of row r at [r * ldE + c * p].  Adjacent cells are adjacent
+// columns, so consecutive interaction partners merge into one long-K term.
+struct FmmTerm {      // in[:, col0 : col0 + K] * op (K x N, row-major, leading dim op_ld)
+  int32_t in_kind;    // IO_U (columns mapped through src[]) or IO_PHI / IO_PSI
+  int32_t col0;
   int32_t K;
-  int32_t pad;
+  int32_t op_ld;
   int64_t op_off;
 };
-struct FmmTask {      // out (rows x N) = sum of terms
-  int32_t out_kind;   // IO_U (scatter dst[lo..lo+N)) or IO_PHI/IO_PSI
-  int32_t out_idx;
+struct FmmTask {      // out[:, col0 : col0 + N] = sum of terms
+  int32_t out_kind;   // IO_U (columns mapped through dst[]) or IO_PHI / IO_PSI
+  int32_t col0;
   int32_t N;
   int32_t t_begin, t_end;
-  int32_t pad;
+  int32_t op_col0;    // column offset into every term's op (tasks split along N)
 };
 svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cells, int p,
                           const double* d, const int32_t* k, const double* tau,
                           const double* zhat, const double* cs, double* ops, cudaStream_t st,
                           int64_t* launches);
-svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
-                          int p, const double* ops, const double* U_in, int64_t ld_in,
+// One pass: every task's output block for all rows.  bn = 16 or 32 (>= every task N).
+svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
+                          int64_t rows, const double* ops, const double* U_in, int64_t ld_in,
                           const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
-                          double* phi, double* psi, cudaStream_t st, int64_t* launches);
+                          double* phi, double* psi, int64_t ldE, cudaStream_t st, int64_t* launches);
 
 }  // namespace svd1

@@ -1,0 +1,45 @@
+"""Host-side FMM plan logic (no GPU): the tree and interaction lists the apply builds
+ stay O(n) in flops for the spectra of the BASELINE configs,
+including isolated outlier eigenvalues and graded spectra."""
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import interlaced_cauchy, random_secular
+from paper_1707_08369_b200._lib import fmm_tree_stats
+
+
+def _roots(d, z, rho):
+    return O.secular_roots_bisect(d, z, rho)
+
+
+@pytest.mark.parametrize("kind,rho", [("gaussian", 3.0), ("graded", 4096.0), ("uniform", -2.0),
+                                      ("graded", -0.5)])
+def test_flops_per_point_bounded(kind, rho):
+    rng = np.random.default_rng(5)
+    n = 2048
+    d, z, _ = random_secular(n, rng, kind=kind)
+    k, tau = _roots(d, z, rho)
+    st = fmm_tree_stats(d, k, tau, 1e-10)
+    assert st["max_leaf"] <= 33
+    assert st["max_near"] <= 24
+    assert st["flops_per_row"] / n <= 700, st      # direct product: 2n = 4096 per point
+
+
+def test_outliers_do_not_widen_leaves():
+    """A handful of eigenvalues 1e7 x above a graded bulk (what rank-1 updates of C3
+    create) must not make any leaf near-field to the whole spectrum."""
+    rng = np.random.default_rng(0)
+    n = 2048
+    d = np.sort(np.concatenate([10.0 ** (-12 * np.arange(n - 16) / n), 1.7e7 * (1 + rng.random(16))]))
+    z = rng.standard_normal(n)
+    k, tau = _roots(d, z, 1.0)
+    st = fmm_tree_stats(d, k, tau, 1e-10)
+    assert st["max_near"] <= 8 and st["flops_per_row"] / n <= 700, st
+
+
+@pytest.mark.parametrize("n", [40, 65, 777, 3000])
+def test_small_and_ragged(n):
+    d, k, tau, *_ = interlaced_cauchy(n, 1, n)
+    st = fmm_tree_stats(d, k, tau, 1e-10)
+    assert st["max_leaf"] <= 33 and st["tasks"] >= 1
