@@ -32,18 +32,26 @@ struct DevBuf {
   ~DevBuf() {
     if (p) cudaFree(p);
   }
+  // Grows geometrically; frees with the legacy (device-wide) semantics only on growth,
+  // which after the first calls of a stream of updates no longer happens.
   template <class T>
   svd1_status get(size_t count, T** out) {
     const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
     if (bytes > cap) {
+      const size_t want = std::max(bytes + bytes / 2, size_t(4096));
       if (p) cudaFree(p);
       p = nullptr;
       cap = 0;
-      if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      if (cudaMalloc(&p, want) != cudaSuccess) {
         cudaGetLastError();
-        return SVD1_E_NOMEM;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+          cudaGetLastError();
+          return SVD1_E_NOMEM;
+        }
+        cap = bytes;
+      } else {
+        cap = want;
       }
-      cap = bytes;
     }
     *out = static_cast<T*>(p);
     return SVD1_OK;
@@ -73,6 +81,29 @@ Split schur_split(double beta) {
   return s;
 }
 
+struct FmmHost {
+  int L = 0, ncells = 0;
+  std::vector<FmmCell> cells;
+  std::vector<FmmOpDesc> ops;
+  std::vector<FmmTerm> terms;
+  std::vector<FmmTask> tasks;
+  std::vector<int> pass_begin;  // task index where each pass starts (+ end sentinel)
+  std::vector<int> pass_bn;     // tile width (16 or 32) of each pass
+  int64_t ops_elems = 0;
+  int64_t flops_per_row = 0;    // algorithmic flops per row of U (2 * sum K*N over terms)
+  int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
+};
+
+struct CauchyPrep {
+  bool fmm = false;
+  int p = 16;
+  int na = 0;
+  int64_t rows = 0;
+  double flops = 0.0;
+  FmmHost F;
+  DevBuf d_cells, d_descs, d_terms, d_tasks, d_ops;
+};
+
 // Everything one RankOneUpdate (Alg 6.2) needs at apply time.
 struct StepRecord {
   int N = 0;                          // size of the eigenproblem (columns of the buffer)
@@ -88,6 +119,17 @@ struct StepRecord {
   std::vector<int32_t> k_h;
   int max_iter = 0;
   double spectral_ms = 0.0;
+  int ev0 = 0, nc = 0;
+  int64_t rows = 0;
+  std::vector<int32_t> perm;
+  std::vector<int> act, dfl;
+  std::vector<double> ds;
+  std::vector<std::vector<double>> cs_sorted;
+  double* rb = nullptr;  // pinned read-back
+  size_t rb_cap = 0;
+  ~StepRecord() {
+    if (rb) cudaFreeHost(rb);
+  }
   void clear_host() {
     spectral_ms = 0.0;
     N = na = 0;
@@ -99,21 +141,11 @@ struct StepRecord {
   }
   // device arrays
   DevBuf d_da, d_za, d_k, d_tau, d_zhat, d_cs, d_src, d_dst, d_pass_src, d_pass_dst, d_pass_scale,
-      d_goff, d_hcols, d_hv, d_carry, d_carry_out;
+      d_goff, d_hcols, d_hv, d_carry, d_carry_out, d_status, d_iters;
+  CauchyPrep cp;
 };
 
-struct FmmHost {
-  int L = 0, ncells = 0;
-  std::vector<FmmCell> cells;
-  std::vector<FmmOpDesc> ops;
-  std::vector<FmmTerm> terms;
-  std::vector<FmmTask> tasks;
-  std::vector<int> pass_begin;  // task index where each pass starts (+ end sentinel)
-  std::vector<int> pass_bn;     // tile width (16 or 32) of each pass
-  int64_t ops_elems = 0;
-  int64_t flops_per_row = 0;    // algorithmic flops per row of U (2 * sum K*N over terms)
-  int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
-};
+
 
 }  // namespace
 
@@ -134,7 +166,7 @@ struct svd1_plan_s {
   size_t arena_cap = 0, arena_used = 0;
   cudaEvent_t arena_ev = nullptr;
   bool arena_pending = false;
-  FmmHost fmm_last;         // stats of the last FMM apply
+  CauchyPrep standalone;    // plan of the standalone svd1_cauchy_apply
   cudaEvent_t ev[16] = {};  // timing events (spectral / apply phases)
 };
 
@@ -237,27 +269,17 @@ struct Merged {
 };
 
 Merged merge_points(const std::vector<double>& da, const std::vector<double>& mu) {
+  // two sorted sequences -> one (ties: source first), O(n)
   const int n = int(da.size());
-  struct Pt {
-    double v;
-    int type, idx;  // type 0 = source, 1 = target
-  };
-  std::vector<Pt> all;
-  all.reserve(2 * n);
-  for (int i = 0; i < n; ++i) all.push_back({da[i], 0, i});
-  for (int j = 0; j < n; ++j) all.push_back({mu[j], 1, j});
-  std::sort(all.begin(), all.end(), [](const Pt& a, const Pt& b) {
-    if (a.v != b.v) return a.v < b.v;
-    if (a.type != b.type) return a.type < b.type;
-    return a.idx < b.idx;
-  });
   Merged M;
   M.pts.resize(2 * n);
   M.nsrc.resize(2 * n + 1);
   M.nsrc[0] = 0;
+  int i = 0, j = 0;
   for (int q = 0; q < 2 * n; ++q) {
-    M.pts[q] = all[q].v;
-    M.nsrc[q + 1] = M.nsrc[q] + (all[q].type == 0);
+    const bool take_src = j >= n || (i < n && da[i] <= mu[j]);
+    M.pts[q] = take_src ? da[i++] : mu[j++];
+    M.nsrc[q + 1] = M.nsrc[q] + (take_src ? 1 : 0);
   }
   return M;
 }
@@ -505,6 +527,8 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
   FmmHost best;
   bool have = false;
   for (int L = L0; L <= L0 + 2 && L <= 22; ++L) {
+    // a deeper tree only pays when the shallower one has wide leaves (outliers)
+    if (have && best.max_near <= 8) break;
     FmmHost F2;
     if (!fmm_cells(F2, leaf, L, M)) {
       if (std::getenv("SVD1_DEBUG")) fprintf(stderr, "[svd1] fmm L=%d infeasible\n", L);
@@ -522,40 +546,63 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
   F = std::move(best);
 }
 
-// Cauchy apply of one step: U_out[:, dst[j]] = cs_j sum_i U_in[:, src[i]] zhat_i / ((d_i - d_kj) - tau_j)
-svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, const int32_t* d_k,
-                       const double* d_tau, const double* d_zhat, const double* d_cs,
-                       const double* U_in, int64_t ld_in, const int32_t* d_src, double* U_out,
-                       int64_t ld_out, const int32_t* d_dst, const std::vector<double>& da,
-                       const std::vector<double>& mu, int p, bool* used_fmm,
-                       double* flops = nullptr) {
+// Cauchy apply of one step, split in a host phase (decide FMM vs direct, build the
+// tree and task lists, stage their upload) and a launch phase (operators + passes).
+// U_out[:, dst[j]] = cs_j sum_i U_in[:, src[i]] zhat_i / ((d_i - d_kj) - tau_j)
+
+
+svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
+                           const std::vector<double>& da, const std::vector<double>& mu, int p) {
   const int minn = P->cfg.fmm_min_n > 0 ? P->cfg.fmm_min_n : 384;
   const int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2: s ~ 2p, capped by the tile
   bool fmm = (P->cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
   if (P->cfg.flags & SVD1_FORCE_DIRECT) fmm = false;
-  if (leaf > kMaxLeaf) fmm = false;
-  *used_fmm = fmm;
-  if (flops) *flops = 2.0 * double(rows) * double(na) * double(na);
-  if (!fmm)
-    return apply_direct(rows, na, d_da, d_k, d_tau, d_zhat, d_cs, U_in, ld_in, d_src, U_out, ld_out,
-                        d_dst, P->st, &P->launches);
-  FmmHost& F = P->fmm_last;
+  C.fmm = fmm;
+  C.p = p;
+  C.na = na;
+  C.rows = rows;
+  C.flops = 2.0 * double(rows) * double(na) * double(na);
+  if (!fmm) return SVD1_OK;
+  FmmHost& F = C.F;
   fmm_build_host(F, na, leaf, p, da, mu);
-  if (flops) *flops = double(F.flops_per_row) * double(rows);
+  C.flops = double(F.flops_per_row) * double(rows);
   FmmCell* dc;
   FmmOpDesc* dd;
   FmmTerm* dt;
   FmmTask* dk;
-  TRY(upload(P, P->fmm_cells, F.cells, &dc));
-  TRY(upload(P, P->fmm_descs, F.ops, &dd));
-  TRY(upload(P, P->fmm_terms, F.terms, &dt));
-  TRY(upload(P, P->fmm_tasks, F.tasks, &dk));
-  double *ops, *phi, *psi;
-  TRY(P->ops.get<double>(size_t(F.ops_elems), &ops));
-  const int64_t ldE = int64_t(F.ncells) * p;
-  const size_t exp_elems = size_t(ldE) * size_t(rows);
-  TRY(P->phi.get<double>(exp_elems, &phi));
+  TRY(upload(P, C.d_cells, F.cells, &dc));
+  TRY(upload(P, C.d_descs, F.ops, &dd));
+  TRY(upload(P, C.d_terms, F.terms, &dt));
+  TRY(upload(P, C.d_tasks, F.tasks, &dk));
+  double* ops;
+  TRY(C.d_ops.get<double>(size_t(F.ops_elems), &ops));
+  return SVD1_OK;
+}
+
+size_t cauchy_exp_elems(const CauchyPrep& C) {
+  return C.fmm ? size_t(C.F.ncells) * size_t(C.p) * size_t(C.rows) : 0;
+}
+
+svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, const int32_t* d_k,
+                          const double* d_tau, const double* d_zhat, const double* d_cs,
+                          const double* U_in, int64_t ld_in, const int32_t* d_src, double* U_out,
+                          int64_t ld_out, const int32_t* d_dst) {
+  const int64_t rows = C.rows;
+  if (!C.fmm)
+    return apply_direct(rows, C.na, d_da, d_k, d_tau, d_zhat, d_cs, U_in, ld_in, d_src, U_out, ld_out,
+                        d_dst, P->st, &P->launches);
+  FmmHost& F = C.F;
+  const int p = C.p;
+  double *phi, *psi;
+  const size_t exp_elems = cauchy_exp_elems(C);
+  TRY(P->phi.get<double>(exp_elems, &phi));  // sized beforehand by the caller (no realloc here)
   TRY(P->psi.get<double>(exp_elems, &psi));
+  const int64_t ldE = int64_t(F.ncells) * p;
+  auto* dc = static_cast<FmmCell*>(C.d_cells.p);
+  auto* dd = static_cast<FmmOpDesc*>(C.d_descs.p);
+  auto* dt = static_cast<FmmTerm*>(C.d_terms.p);
+  auto* dk = static_cast<FmmTask*>(C.d_tasks.p);
+  auto* ops = static_cast<double*>(C.d_ops.p);
   TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, ops, P->st,
                     &P->launches));
   const bool dbg = std::getenv("SVD1_DEBUG") != nullptr;
@@ -566,13 +613,14 @@ svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, 
                 T.t_begin, T.t_end);
       for (int t = T.t_begin; t < T.t_end; ++t) {
         const FmmTerm& R = F.terms[t];
-        if (R.K < 1 || R.op_ld != T.N || R.op_off < 0 || R.op_off + int64_t(R.K) * T.N > F.ops_elems)
+        if (R.K < 1 || R.op_off < 0 || R.op_off + int64_t(R.K - 1) * R.op_ld + T.op_col0 + T.N > F.ops_elems)
           fprintf(stderr, "[svd1] bad term %d: kind=%d col0=%d K=%d off=%lld\n", t, R.in_kind, R.col0,
                   R.K, (long long)R.op_off);
       }
     }
-    fprintf(stderr, "[svd1] fmm na=%d L=%d cells=%d tasks=%zu terms=%zu ops=%lld rows=%lld p=%d\n", na,
-            F.L, F.ncells, F.tasks.size(), F.terms.size(), (long long)F.ops_elems, (long long)rows, p);
+    fprintf(stderr, "[svd1] fmm na=%d L=%d cells=%d tasks=%zu terms=%zu ops=%lld rows=%lld p=%d\n",
+            C.na, F.L, F.ncells, F.tasks.size(), F.terms.size(), (long long)F.ops_elems,
+            (long long)rows, p);
   }
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
@@ -587,31 +635,44 @@ svd1_status run_cauchy(svd1_plan_t P, int64_t rows, int na, const double* d_da, 
   return SVD1_OK;
 }
 
+svd1_status ensure_expansions(svd1_plan_t P, size_t elems) {
+  double* x;
+  TRY(P->phi.get<double>(elems, &x));
+  TRY(P->psi.get<double>(elems, &x));
+  return SVD1_OK;
+}
+
 // --------------------------------------------------------- Alg 6.2 spectral
-// One RankOneUpdate on the small vectors: sort, deflate, secular solve,
-// Loewner, column norms, carried vectors X^T v, merge.  D, z and carries are indexed
-// by buffer column; on return D and carries are indexed by output position.
-svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
-                          const std::vector<double>& z, double rho,
-                          std::vector<std::vector<double>>& carries, int ev0) {
+// One RankOneUpdate on the small vectors, in two halves so that the U- and
+// V-side eigen-updates run on the GPU together and the host builds FMM trees meanwhile.
+// spectral_launch: sort (stable, ties by column), deflate, enqueue the
+// secular solve (STEP 2), Loewner, column norms and carried X^T v, and their read-back.
+svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<double>& D,
+                            const std::vector<double>& z, double rho,
+                            const std::vector<std::vector<double>>& carries, int ev0) {
   const int N = int(D.size());
   S.clear_host();  // device buffers are kept (grow-only)
   S.N = N;
   S.rho = rho;
-  // stable ascending sort of the eigenvalues (ties by column index)
-  std::vector<int32_t> perm(N);
+  S.ev0 = ev0;
+  std::vector<int32_t>& perm = S.perm;
+  perm.resize(N);
   std::iota(perm.begin(), perm.end(), 0);
   std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return D[a] < D[b]; });
-  std::vector<double> ds(N), zs(N);
+  std::vector<double>& ds = S.ds;
+  ds.resize(N);
+  std::vector<double> zs(N);
   for (int s = 0; s < N; ++s) {
     ds[s] = D[perm[s]];
     zs[s] = z[perm[s]];
   }
   const int nc = int(carries.size());
-  std::vector<std::vector<double>> cs_sorted(nc, std::vector<double>(N));
+  S.nc = nc;
+  auto& cs_sorted = S.cs_sorted;
+  cs_sorted.assign(nc, std::vector<double>(N));
   for (int q = 0; q < nc; ++q)
     for (int s = 0; s < N; ++s) cs_sorted[q][s] = carries[q][perm[s]];
-  // deflation (P:121-124; DESIGN.md §3.2 D1): (i) zero weights, (iii) exact repeats
+  // deflation (DESIGN.md §3.2 D1): (i) zero weights, (iii) exact repeats
   double zn2 = 0.0;
   for (double v : zs) zn2 += v * v;
   const double tol = 8.0 * kEps * std::sqrt(zn2);
@@ -661,72 +722,99 @@ svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
       t = u + 1;
     }
   }
-  std::vector<int> act, dfl;
-  for (int s = 0; s < N; ++s) (alive[s] ? act : dfl).push_back(s);
-  const int na = int(act.size());
+  S.act.clear();
+  S.dfl.clear();
+  for (int s = 0; s < N; ++s) (alive[s] ? S.act : S.dfl).push_back(s);
+  const int na = int(S.act.size());
   S.na = na;
   std::vector<double> za(na);
   S.da.resize(na);
   S.src_cols.resize(na);
   for (int i = 0; i < na; ++i) {
-    S.da[i] = ds[act[i]];
-    za[i] = zs[act[i]];
-    S.src_cols[i] = perm[act[i]];
+    S.da[i] = ds[S.act[i]];
+    za[i] = zs[S.act[i]];
+    S.src_cols[i] = perm[S.act[i]];
   }
+  if (na == 0) return SVD1_OK;
   std::vector<double> carry_act(size_t(nc) * na);
   for (int q = 0; q < nc; ++q)
-    for (int i = 0; i < na; ++i) carry_act[size_t(q) * na + i] = cs_sorted[q][act[i]];
-  std::vector<double> carry_out(size_t(nc) * na);
+    for (int i = 0; i < na; ++i) carry_act[size_t(q) * na + i] = cs_sorted[q][S.act[i]];
+  double *dda, *dza, *dtau, *dzh, *dcs, *dcar, *dco;
+  int32_t *dk, *dst, *dit;
+  TRY(upload(P, S.d_da, S.da, &dda));
+  TRY(upload(P, S.d_za, za, &dza));
+  TRY(upload(P, S.d_carry, carry_act, &dcar));
+  TRY(S.d_k.get<int32_t>(na, &dk));
+  TRY(S.d_tau.get<double>(na, &dtau));
+  TRY(S.d_zhat.get<double>(na, &dzh));
+  TRY(S.d_cs.get<double>(na, &dcs));
+  TRY(S.d_carry_out.get<double>(size_t(nc) * na, &dco));
+  TRY(S.d_status.get<int32_t>(1, &dst));
+  TRY(S.d_iters.get<int32_t>(na, &dit));
+  SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
+  TRY(ev_record(P, ev0));
+  TRY(secular(dda, dza, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
+  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, P->st, &P->launches));
+  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, P->st, &P->launches));
+  TRY(ev_record(P, ev0 + 1));
+  // read back into pinned memory: [k (as int32 pairs) | tau | cs | carry_out | iters | status]
+  const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
+  if (words * sizeof(double) > S.rb_cap) {
+    if (S.rb) cudaFreeHost(S.rb);
+    S.rb = nullptr;
+    S.rb_cap = 0;
+    if (cudaMallocHost(&S.rb, words * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return SVD1_E_NOMEM;
+    }
+    S.rb_cap = words * sizeof(double);
+  }
+  double* rb = S.rb;
+  SVD1_CUDA_TRY(cudaMemcpyAsync(rb, dk, na * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + na, dtau, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + 2 * na, dcs, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  if (nc)
+    SVD1_CUDA_TRY(cudaMemcpyAsync(rb + 3 * na, dco, size_t(nc) * na * sizeof(double),
+                                  cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + size_t(3 + nc) * na, dit, na * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + words - 1, dst, sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+  return SVD1_OK;
+}
+
+// spectral_finish (after a stream sync): status, mu, merge of mu with the deflated
+// eigenvalues (stable ascending, deflated first on ties), the new eigenvalues D and
+// carried vectors indexed by output position.
+svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
+                            std::vector<std::vector<double>>& carries) {
+  const int N = S.N, na = S.na, nc = S.nc;
+  const double* carry_out = nullptr;
   if (na > 0) {
-    double *dda, *dza, *dtau, *dzh, *dcs, *dcar, *dco;
-    int32_t *dk, *dst, *dit;
-    TRY(upload(P, S.d_da, S.da, &dda));
-    TRY(upload(P, S.d_za, za, &dza));
-    TRY(upload(P, S.d_carry, carry_act, &dcar));
-    TRY(S.d_k.get<int32_t>(na, &dk));
-    TRY(S.d_tau.get<double>(na, &dtau));
-    TRY(S.d_zhat.get<double>(na, &dzh));
-    TRY(S.d_cs.get<double>(na, &dcs));
-    TRY(S.d_carry_out.get<double>(size_t(nc) * na, &dco));
-    TRY(P->status.get<int32_t>(1, &dst));
-    TRY(P->iters.get<int32_t>(na, &dit));
-    SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
-    TRY(ev_record(P, ev0));
-    TRY(secular(dda, dza, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
-    TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, P->st, &P->launches));
-    TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, P->st, &P->launches));
-    TRY(ev_record(P, ev0 + 1));
-    // read back k, tau, cs, carried vectors, iterations, status
+    const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
+    const double* rb = S.rb;
+    int32_t st_h;
+    std::memcpy(&st_h, rb + words - 1, sizeof(int32_t));
     S.k_h.resize(na);
-    S.tau_h.resize(na);
-    S.cs_h.resize(na);
-    std::vector<int32_t> it_h(na);
-    int32_t st_h = 0;
-    SVD1_CUDA_TRY(cudaMemcpyAsync(S.k_h.data(), dk, na * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
-    SVD1_CUDA_TRY(cudaMemcpyAsync(S.tau_h.data(), dtau, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
-    SVD1_CUDA_TRY(cudaMemcpyAsync(S.cs_h.data(), dcs, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
-    SVD1_CUDA_TRY(cudaMemcpyAsync(it_h.data(), dit, na * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
-    if (nc)
-      SVD1_CUDA_TRY(cudaMemcpyAsync(carry_out.data(), dco, size_t(nc) * na * sizeof(double),
-                                    cudaMemcpyDeviceToHost, P->st));
-    SVD1_CUDA_TRY(cudaMemcpyAsync(&st_h, dst, sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
-    SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
-    for (int v : it_h) S.max_iter = std::max(S.max_iter, v);
-    S.spectral_ms = ev_ms(P, ev0, ev0 + 1);
+    std::memcpy(S.k_h.data(), rb, na * sizeof(int32_t));
+    S.tau_h.assign(rb + na, rb + 2 * na);
+    S.cs_h.assign(rb + 2 * na, rb + 3 * na);
+    carry_out = rb + 3 * na;
+    const int32_t* it = reinterpret_cast<const int32_t*>(rb + size_t(3 + nc) * na);
+    for (int j = 0; j < na; ++j) S.max_iter = std::max(S.max_iter, it[j]);
+    S.spectral_ms = ev_ms(P, S.ev0, S.ev0 + 1);
     if (st_h & 1) return SVD1_E_NOCONV;
     if (st_h & 2) return SVD1_E_POLE;
     if (st_h & 4) return SVD1_E_ZEROCOL;
   }
   S.mu.resize(na);
   for (int j = 0; j < na; ++j) S.mu[j] = S.da[S.k_h[j]] + S.tau_h[j];
-  // merge mu with the deflated eigenvalues: stable ascending, deflated first on ties
   struct Item {
     double v;
     int flag, pos;
   };
   std::vector<Item> items;
   items.reserve(N);
-  for (int s : dfl) items.push_back({ds[s], 0, s});
+  for (int s : S.dfl) items.push_back({S.ds[s], 0, s});
   for (int j = 0; j < na; ++j) items.push_back({S.mu[j], 1, j});
   std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
     if (a.v != b.v) return a.v < b.v;
@@ -740,10 +828,10 @@ svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
     const Item& it = items[q];
     Dn[q] = it.v;
     if (it.flag == 0) {
-      S.pass_src.push_back(perm[it.pos]);
+      S.pass_src.push_back(S.perm[it.pos]);
       S.pass_dst.push_back(q);
       S.pass_scale.push_back(1.0);
-      for (int qq = 0; qq < nc; ++qq) cn[qq][q] = cs_sorted[qq][it.pos];
+      for (int qq = 0; qq < nc; ++qq) cn[qq][q] = S.cs_sorted[qq][it.pos];
     } else {
       S.tgt_pos[it.pos] = q;
       for (int qq = 0; qq < nc; ++qq) cn[qq][q] = carry_out[size_t(qq) * na + it.pos];
@@ -754,24 +842,19 @@ svd1_status spectral_step(svd1_plan_t P, StepRecord& S, std::vector<double>& D,
   return SVD1_OK;
 }
 
-// Apply one recorded step: Householder (in place on U_in), Cauchy apply, passthrough.
+// Host half of one apply: column maps, Householder data, Cauchy plan; staged uploads.
 // out_col(q) = reverse ? (N - 1 - q) : q.
-svd1_status apply_step(svd1_plan_t P, StepRecord& S, int64_t rows, double* U_in, int64_t ld_in,
-                       double* U_out, int64_t ld_out, bool reverse, bool* used_fmm, double* flops,
-                       int ev0) {
-  *used_fmm = false;
-  *flops = 0.0;
-  TRY(ev_record(P, ev0));
+svd1_status apply_prepare(svd1_plan_t P, StepRecord& S, int64_t rows, bool reverse) {
   const int N = S.N;
+  S.rows = rows;
   auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
+  if (rows <= 0) return SVD1_OK;
   if (S.h_goff.size() > 1) {
     int32_t *goff, *cols;
     double* hv;
     TRY(upload(P, S.d_goff, S.h_goff, &goff));
     TRY(upload(P, S.d_hcols, S.h_cols, &cols));
     TRY(upload(P, S.d_hv, S.h_hv, &hv));
-    TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1, goff, cols, hv, P->st,
-                         &P->launches));
   }
   if (S.na > 0) {
     std::vector<int32_t> dst(S.na);
@@ -781,14 +864,7 @@ svd1_status apply_step(svd1_plan_t P, StepRecord& S, int64_t rows, double* U_in,
     TRY(upload(P, S.d_src, S.src_cols, &dsrc));
     TRY(upload(P, S.d_dst, dst, &ddst));
     TRY(upload(P, S.d_cs, S.cs_h, &dcs));  // cs_h may carry the sign alignment
-    double *dda, *dtau, *dzh;
-    int32_t* dk;
-    TRY(S.d_da.get<double>(S.na, &dda));
-    TRY(S.d_tau.get<double>(S.na, &dtau));
-    TRY(S.d_zhat.get<double>(S.na, &dzh));
-    TRY(S.d_k.get<int32_t>(S.na, &dk));
-    TRY(run_cauchy(P, rows, S.na, dda, dk, dtau, dzh, dcs, U_in, ld_in, dsrc, U_out, ld_out, ddst, S.da,
-                   S.mu, P->p, used_fmm, flops));
+    TRY(cauchy_prepare(P, S.cp, rows, S.na, S.da, S.mu, P->p));
   }
   if (!S.pass_src.empty()) {
     std::vector<int32_t> dst(S.pass_dst.size());
@@ -798,8 +874,29 @@ svd1_status apply_step(svd1_plan_t P, StepRecord& S, int64_t rows, double* U_in,
     TRY(upload(P, S.d_pass_src, S.pass_src, &ds));
     TRY(upload(P, S.d_pass_dst, dst, &dd));
     TRY(upload(P, S.d_pass_scale, S.pass_scale, &sc));
-    TRY(passthrough(rows, int(dst.size()), U_in, ld_in, ds, U_out, ld_out, dd, sc, P->st, &P->launches));
   }
+  return SVD1_OK;
+}
+
+// Device half: Householder (in place on U_in), Cauchy apply, passthrough.
+svd1_status apply_launch(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_in, double* U_out,
+                         int64_t ld_out, int ev0) {
+  const int64_t rows = S.rows;
+  if (rows <= 0) return SVD1_OK;
+  TRY(ev_record(P, ev0));
+  if (S.h_goff.size() > 1)
+    TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1,
+                         static_cast<int32_t*>(S.d_goff.p), static_cast<int32_t*>(S.d_hcols.p),
+                         static_cast<double*>(S.d_hv.p), P->st, &P->launches));
+  if (S.na > 0)
+    TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_da.p), static_cast<int32_t*>(S.d_k.p),
+                      static_cast<double*>(S.d_tau.p), static_cast<double*>(S.d_zhat.p),
+                      static_cast<double*>(S.d_cs.p), U_in, ld_in, static_cast<int32_t*>(S.d_src.p),
+                      U_out, ld_out, static_cast<int32_t*>(S.d_dst.p)));
+  if (!S.pass_src.empty())
+    TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, static_cast<int32_t*>(S.d_pass_src.p),
+                    U_out, ld_out, static_cast<int32_t*>(S.d_pass_dst.p),
+                    static_cast<double*>(S.d_pass_scale.p), P->st, &P->launches));
   TRY(ev_record(P, ev0 + 1));
   return SVD1_OK;
 }
@@ -914,7 +1011,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   const Split su = schur_split(beta), sv = schur_split(alpha);
   // small vectors in the U and V column bases (B7 identities):
   // U^T b~ = Sigma (V^T b)[:m],  V^T a~ = Sigma^T (U^T a)
-  std::vector<double> z1(m), w1(m), Du(m), z3(n), w3(n), Dv(n, 0.0);
+  std::vector<double> z1(m), Du(m), z3(n), Dv(n, 0.0);
   std::vector<std::vector<double>> cu, cv;
   cu.emplace_back(m);
   cv.emplace_back(n);
@@ -924,36 +1021,52 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   }
   for (int64_t i = 0; i < m; ++i) {
     const double sx = sig[i] * yb[i];
-    z1[i] = su.q00 * xa[i] + su.q10 * sx;   // U^T a1, [a b~] Q_u = [a1 b1]
+    z1[i] = su.q00 * xa[i] + su.q10 * sx;     // U^T a1, [a b~] Q_u = [a1 b1]
     cu[0][i] = su.q01 * xa[i] + su.q11 * sx;  // U^T b1
     Du[i] = sig[i] * sig[i];
     Dv[i] = Du[i];
   }
   for (int64_t i = 0; i < n; ++i) {
     const double sxa = i < m ? sig[i] * xa[i] : 0.0;
-    z3[i] = sv.q00 * yb[i] + sv.q10 * sxa;  // V^T a2, [b a~] Q_v = [a2 b2]
+    z3[i] = sv.q00 * yb[i] + sv.q10 * sxa;     // V^T a2, [b a~] Q_v = [a2 b2]
     cv[0][i] = sv.q01 * yb[i] + sv.q11 * sxa;  // V^T b2
-    for (int q = 0; q < kNumProbes; ++q)   // V^T A_hat^T g = Sigma^T U^T g + (V^T b)(a.g)
+    for (int q = 0; q < kNumProbes; ++q)       // V^T A_hat^T g = Sigma^T U^T g + (V^T b)(a.g)
       cv[1 + q][i] = (i < m ? sig[i] * xg[q * m + i] : 0.0) + yb[i] * ag[q];
   }
-  // ---- spectral phase, all four eigen-updates, before any write to U or V
+  // ---- spectral phase: all four eigen-updates before any write to U or V.
+  // Round 1: STEP 4 (U, rho1) and STEP 6 (V, rho3) together.
   const double t1 = now_ms();
-  TRY(spectral_step(P, P->steps[0], Du, z1, su.rho1, cu, 8));       // STEP 4
+  StepRecord* S = P->steps;
   {
-    std::vector<double> z2 = cu[0];
+    std::vector<double> zu = z1, zv = z3;
+    std::vector<std::vector<double>> cu1(cu.begin() + 1, cu.end()), cv1(cv.begin() + 1, cv.end());
+    // carry 0 = the chained vector U^T b1 / V^T b2, carries 1.. = probes
+    cu1.insert(cu1.begin(), cu[0]);
+    cv1.insert(cv1.begin(), cv[0]);
+    cu.swap(cu1);
+    cv.swap(cv1);
+    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8));
+    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12));
+  }
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  TRY(spectral_finish(P, S[0], Du, cu));
+  TRY(spectral_finish(P, S[2], Dv, cv));
+  // Round 2: STEP 5 (U, rho2, z2 = X1^T U^T b1) and STEP 7 (V, rho4)
+  {
+    std::vector<double> z2 = cu[0], z4 = cv[0];
     cu.erase(cu.begin());
-    TRY(spectral_step(P, P->steps[1], Du, z2, su.rho2, cu, 10));     // STEP 5
-  }
-  const double t2 = now_ms();
-  TRY(spectral_step(P, P->steps[2], Dv, z3, sv.rho1, cv, 12));       // STEP 6
-  {
-    std::vector<double> z4 = cv[0];
     cv.erase(cv.begin());
-    TRY(spectral_step(P, P->steps[3], Dv, z4, sv.rho2, cv, 14));     // STEP 7
+    TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10));
+    TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14));
   }
+  // host work overlapping round 2 on the GPU: Cauchy plans of the first applies
+  TRY(apply_prepare(P, S[0], c.u_rows, false));
+  TRY(apply_prepare(P, S[2], c.v_rows, false));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  TRY(spectral_finish(P, S[1], Du, cu));
+  TRY(spectral_finish(P, S[3], Dv, cv));
   const double t3 = now_ms();
-  R.t_ms[1] = t2 - t1;
-  R.t_ms[2] = t3 - t2;
+  R.t_ms[1] = t3 - t1;
   // ---- sign alignment: final column i = position N-1-i
   std::vector<double> sgn(m, 1.0);
   for (int64_t i = 0; i < m; ++i) {
@@ -965,20 +1078,18 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
         best = std::fabs(cu[q][qu]);
         kb = q;
       }
-    const double prod = cu[kb][qu] * cv[kb][qv];
-    if (prod < 0.0) {
+    if (cu[kb][qu] * cv[kb][qv] < 0.0) {
       sgn[i] = -1.0;
       ++R.sign_flips;
     }
   }
-  StepRecord& S4 = P->steps[3];
-  for (int j = 0; j < S4.na; ++j) {
-    const int64_t col = n - 1 - S4.tgt_pos[j];
-    if (col < m) S4.cs_h[j] *= sgn[col];
+  for (int j = 0; j < S[3].na; ++j) {
+    const int64_t col = n - 1 - S[3].tgt_pos[j];
+    if (col < m) S[3].cs_h[j] *= sgn[col];
   }
-  for (size_t q = 0; q < S4.pass_dst.size(); ++q) {
-    const int64_t col = n - 1 - S4.pass_dst[q];
-    if (col < m) S4.pass_scale[q] *= sgn[col];
+  for (size_t q = 0; q < S[3].pass_dst.size(); ++q) {
+    const int64_t col = n - 1 - S[3].pass_dst[q];
+    if (col < m) S[3].pass_scale[q] *= sgn[col];
   }
   // ---- STEP 8: sigma = sqrt(max(D, 0)), descending
   std::vector<double> sig_new(m);
@@ -988,40 +1099,51 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     sig_new[i] = std::sqrt(std::max(dv, 0.0));
   }
   for (int e = 0; e < 4; ++e) {
-    R.n_active[e] = P->steps[e].na;
-    R.n_deflated[e] = P->steps[e].N - P->steps[e].na;
-    R.max_iter[e] = P->steps[e].max_iter;
+    R.n_active[e] = S[e].na;
+    R.n_deflated[e] = S[e].N - S[e].na;
+    R.max_iter[e] = S[e].max_iter;
   }
-  // ---- applies (STEP 4-7 vector parts): U -> W_u -> U, V -> W_v -> V
+  // ---- applies (vector parts of STEPS 4-7): U -> W_u -> U, V -> W_v -> V.
+  // The first apply of each side was planned during round 2; launch both, then plan
+  // the second applies on the host while the GPU runs the first ones.
+  const double t4 = now_ms();
   double *Wu = nullptr, *Wv = nullptr;
   if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
   if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * n, &Wv));
-  bool f;
-  for (int e = 0; e < 4; ++e) {
-    const bool uside = e < 2;
-    const int64_t rows = uside ? c.u_rows : c.v_rows;
-    if (!rows) continue;
-    double* in = uside ? (e == 0 ? U : Wu) : (e == 2 ? V : Wv);
-    double* out = uside ? (e == 0 ? Wu : U) : (e == 2 ? Wv : V);
-    const int64_t ldi = uside ? (e == 0 ? ldu : m) : (e == 2 ? ldv : n);
-    const int64_t ldo = uside ? (e == 0 ? m : ldu) : (e == 2 ? n : ldv);
-    TRY(apply_step(P, P->steps[e], rows, in, ldi, out, ldo, e == 1 || e == 3, &f, &R.apply_flops[e],
-                   2 * e));
-    R.fmm_used[e] = f;
-    if (f) {
-      R.fmm_levels[e] = P->fmm_last.L;
-      R.fmm_max_near[e] = P->fmm_last.max_near;
-    }
+  // expansions are sized for all four applies up front (a mid-stream realloc would sync)
+  {
+    size_t exp_max = 0;
+    for (int e : {0, 2})
+      if (S[e].rows > 0 && S[e].na > 0) exp_max = std::max(exp_max, cauchy_exp_elems(S[e].cp));
+    const int64_t rows_max = std::max(c.u_rows, c.v_rows);
+    const size_t guess = size_t(rows_max) * size_t(P->p) * size_t(4 * std::max<int64_t>(n, 1) / std::max(P->leaf, 1) + 8);
+    TRY(ensure_expansions(P, std::max(exp_max, guess)));
   }
+  TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0));
+  TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4));
+  TRY(apply_prepare(P, S[1], c.u_rows, true));
+  TRY(apply_prepare(P, S[3], c.v_rows, true));
+  for (int e : {1, 3})
+    if (S[e].rows > 0 && S[e].na > 0 && cauchy_exp_elems(S[e].cp) > P->phi.cap / sizeof(double))
+      TRY(ensure_expansions(P, cauchy_exp_elems(S[e].cp)));  // rare: deeper tree than guessed
+  TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2));
+  TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6));
+  R.t_ms[2] = now_ms() - t4;
   std::memcpy(h, sig_new.data(), size_t(m) * sizeof(double));
   SVD1_CUDA_TRY(cudaMemcpyAsync(sigma, h, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, P->st));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   SVD1_CUDA_TRY(cudaGetLastError());
   R.t_ms[3] = now_ms() - t3;
   for (int e = 0; e < 4; ++e) {
-    const bool has = (e < 2 ? c.u_rows : c.v_rows) > 0;
+    const bool has = S[e].rows > 0;
     R.apply_ms[e] = has ? ev_ms(P, 2 * e, 2 * e + 1) : 0.0;
-    R.spectral_ms[e] = P->steps[e].spectral_ms;
+    R.apply_flops[e] = (has && S[e].na > 0) ? S[e].cp.flops : 0.0;
+    R.fmm_used[e] = (has && S[e].na > 0) ? S[e].cp.fmm : 0;
+    if (R.fmm_used[e]) {
+      R.fmm_levels[e] = S[e].cp.F.L;
+      R.fmm_max_near[e] = S[e].cp.F.max_near;
+    }
+    R.spectral_ms[e] = S[e].spectral_ms;
   }
   R.t_ms[4] = now_ms() - t0;
   R.kernel_launches = P->launches - launches0;
@@ -1062,8 +1184,13 @@ svd1_status svd1_cauchy_apply(svd1_plan_t P, int64_t rows, int64_t n, const doub
     mu[j] = dh[kh[j]] + th[j];
   }
   bool used = false;
-  TRY(run_cauchy(P, rows, int(n), d, k, tau, zhat, colscale, U_in, ld_in, nullptr, U_out, ld_out,
-                 nullptr, dh, mu, p, &used));
+  {
+    CauchyPrep& C = P->standalone;
+    TRY(cauchy_prepare(P, C, rows, int(n), dh, mu, p));
+    TRY(ensure_expansions(P, cauchy_exp_elems(C)));
+    TRY(cauchy_launch(P, C, d, k, tau, zhat, colscale, U_in, ld_in, nullptr, U_out, ld_out, nullptr));
+    used = C.fmm;
+  }
   if (fmm_used) *fmm_used = used ? 1 : 0;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
