@@ -163,26 +163,19 @@ def main():
     m, n = cfg["m"], cfg["n"]
     ab = [(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)) for a, b in inp["ab"]]
     U0, s0, V0 = inp["U"], inp["sigma"], inp["V"]
-    # row shards
-    ur = [(m * r) // world for r in range(world + 1)]
-    vr = [(n * r) // world for r in range(world + 1)]
-    u0, u1, v0, v1 = ur[rank], ur[rank + 1], vr[rank], vr[rank + 1]
+    # row shards (paper_1707_08369_b200.parallel: NCCL all-reduce of the projections)
+    from paper_1707_08369_b200.parallel import ShardedUpdater
+    stream = torch.cuda.current_stream()
+    upd = ShardedUpdater(m, n, rank, world, eps=cfg["eps"], stream=stream)
+    u0, u1, v0, v1 = upd.u_lo, upd.u_hi, upd.v_lo, upd.v_hi
     U = U0[u0:u1].clone()
     V = V0[v0:v1].clone()
     sig = s0.clone()
     Upr, Vpr, spr = U.clone(), V.clone(), sig.clone()
-    stream = torch.cuda.current_stream()
-    plan = P.Plan(m, n, eps=cfg["eps"], stream=stream, u_rows=u1 - u0, v_rows=v1 - v0,
-                  u_row0=u0, v_row0=v0)
-    proj = torch.empty(plan.proj_size(), dtype=torch.float64, device=dev)
 
     def step(t, a=None, b=None):
         a_t, b_t = ab[t % len(ab)] if a is None else (a, b)
-        if world == 1:
-            return plan.update(U, sig, V, a_t, b_t)
-        plan.project(U, V, a_t, b_t, proj)
-        dist.all_reduce(proj)  # N1: sum of the row-block partial projections (NCCL)
-        return plan.update_projected(U, sig, V, proj, a_t, b_t)
+        return upd.update(U, sig, V, a_t, b_t)
 
     def restore():
         U.copy_(Upr)
