@@ -70,7 +70,8 @@ typedef struct {
 typedef struct {
   double t_ms[8];        /* host wall times (ms): [0] projection read-back, [1] spectral
                             rounds, [2] apply planning + launch, [3] from the end of the
-                            spectral phase to the final sync, [4] total */
+                            spectral phase to the final sync, [4] total; [5] device time
+                            of the whole apply phase (U side and V side run concurrently) */
   int32_t n_active[4];   /* active sizes of the four eigen-updates */
   int32_t n_deflated[4]; /* deflated counts */
   int32_t max_iter[4];   /* max secular iterations per eigen-update */

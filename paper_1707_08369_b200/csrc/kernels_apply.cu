@@ -295,13 +295,20 @@ __global__ void __launch_bounds__(256) fmm_gemm_kernel(
     const double* base = R.in_kind == IO_U ? U_in : (R.in_kind == IO_PHI ? phi : psi);
     const int64_t ld = R.in_kind == IO_U ? ld_in : ldE;
 #pragma unroll 4
-    for (int e = tid; e < G::BM * KC; e += 256) {
-      const int rr = e / KC, kk = e % KC;
+    // 256 % KC == 0: every thread loads one fixed column kk of the chunk for
+    // rows rr0, rr0 + 256/KC, ... so the column map is read once per stage.
+    {
+      const int kk = tid % KC, rr0 = tid / KC;
       const int k = kk0 + kk;
-      const bool ok = rr < nrow && k < R.K;
-      int col = R.col0 + (ok ? k : 0);
-      if (R.in_kind == IO_U && src) col = src[ok ? col : R.col0];
-      cp_async8(a + rr * ALD + kk, base + (row0 + (ok ? rr : 0)) * ld + col, ok);
+      const bool kok = k < R.K;
+      int col = R.col0 + (kok ? k : 0);
+      if (R.in_kind == IO_U && src) col = src[col];
+      const double* colp = base + row0 * ld + col;
+#pragma unroll 4
+      for (int rr = rr0; rr < G::BM; rr += 256 / KC) {
+        const bool ok = kok && rr < nrow;
+        cp_async8(a + rr * ALD + kk, colp + (ok ? int64_t(rr) * ld : 0), ok);
+      }
     }
     for (int e = tid; e < KC * BN; e += 256) {
       const int kk = e / BN, jj = e % BN;

@@ -155,8 +155,11 @@ struct svd1_plan_s {
   int p = 16, leaf = 32;
   uint64_t probe_seed = 0x1707083691234567ull;
   int64_t launches = 0;
-  DevBuf W_u, W_v, proj, partial, status, iters, phi, psi, ops, fmm_cells, fmm_descs, fmm_terms,
+  DevBuf W_u, W_v, proj, partial, status, iters, ops, fmm_cells, fmm_descs, fmm_terms,
       fmm_tasks, scratch_i, scratch_d;
+  DevBuf phi[2], psi[2];         // FMM expansions per side (U applies, V applies)
+  cudaStream_t st2 = nullptr;    // V-side applies run here, concurrently with the U side
+  cudaEvent_t sync_ev[4] = {};
   StepRecord steps[4];
   double* h_pin = nullptr;  // pinned staging for read-backs
   size_t h_pin_cap = 0;
@@ -167,7 +170,7 @@ struct svd1_plan_s {
   cudaEvent_t arena_ev = nullptr;
   bool arena_pending = false;
   CauchyPrep standalone;    // plan of the standalone svd1_cauchy_apply
-  cudaEvent_t ev[16] = {};  // timing events (spectral / apply phases)
+  cudaEvent_t ev[18] = {};  // timing events (spectral / apply phases)
 };
 
 namespace {
@@ -221,9 +224,18 @@ svd1_status arena_put(svd1_plan_t P, const void* src, size_t bytes, void* dev) {
   return SVD1_OK;
 }
 
-svd1_status ev_record(svd1_plan_t P, int i) {
+svd1_status ev_record(svd1_plan_t P, int i, cudaStream_t st = nullptr) {
   if (!P->ev[i]) SVD1_CUDA_TRY(cudaEventCreate(&P->ev[i]));
-  SVD1_CUDA_TRY(cudaEventRecord(P->ev[i], P->st));
+  SVD1_CUDA_TRY(cudaEventRecord(P->ev[i], st ? st : P->st));
+  return SVD1_OK;
+}
+
+// `waiter` waits for everything enqueued on `signaller` so far.
+svd1_status stream_wait(svd1_plan_t P, int slot, cudaStream_t signaller, cudaStream_t waiter) {
+  if (!P->sync_ev[slot])
+    SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->sync_ev[slot], cudaEventDisableTiming));
+  SVD1_CUDA_TRY(cudaEventRecord(P->sync_ev[slot], signaller));
+  SVD1_CUDA_TRY(cudaStreamWaitEvent(waiter, P->sync_ev[slot], 0));
   return SVD1_OK;
 }
 
@@ -496,14 +508,16 @@ void fmm_lists(FmmHost& F, int p) {
       }
     }
   }
-  // final: L2P (STEP 9) + P2P near field (STEP 10)
+  // final: L2P (STEP 9) + P2P near field (STEP 10); two launches by
+  // output width (leaves with <= 16 targets use the 16-wide tile)
+  for (int wide = 0; wide < 2; ++wide) {
   F.pass_begin.push_back(int(F.tasks.size()));
-  int bn_final = 16;
+  F.pass_bn.push_back(wide ? 32 : 16);
   for (int i = 0; i < nleaf; ++i) {
     const int y = lf0 + i;
     if (!has_tgt(y)) continue;
     const int ty = F.cells[y].thi - F.cells[y].tlo;
-    bn_final = std::max(bn_final, std::min(ty, 32));
+    if ((ty > 16) != (wide == 1)) continue;
     begin_task();
     if (has_psi[y]) add_term(IO_PSI, y * p, p, add_op(OP_L2P, y, y, p, ty), ty);
     add_runs(near[y], IO_U, OP_P2P, y, ty);
@@ -511,7 +525,7 @@ void fmm_lists(FmmHost& F, int p) {
     F.max_near = std::max<int>(F.max_near, int(near[y].size()));
     end_task(IO_U, F.cells[y].tlo, ty);
   }
-  F.pass_bn.push_back(bn_final);
+  }
   F.pass_begin.push_back(int(F.tasks.size()));
   for (int& bn : F.pass_bn) bn = bn <= 16 ? 16 : 32;
   (void)nonempty;
@@ -586,24 +600,24 @@ size_t cauchy_exp_elems(const CauchyPrep& C) {
 svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, const int32_t* d_k,
                           const double* d_tau, const double* d_zhat, const double* d_cs,
                           const double* U_in, int64_t ld_in, const int32_t* d_src, double* U_out,
-                          int64_t ld_out, const int32_t* d_dst) {
+                          int64_t ld_out, const int32_t* d_dst, cudaStream_t st, int side) {
   const int64_t rows = C.rows;
   if (!C.fmm)
     return apply_direct(rows, C.na, d_da, d_k, d_tau, d_zhat, d_cs, U_in, ld_in, d_src, U_out, ld_out,
-                        d_dst, P->st, &P->launches);
+                        d_dst, st, &P->launches);
   FmmHost& F = C.F;
   const int p = C.p;
   double *phi, *psi;
   const size_t exp_elems = cauchy_exp_elems(C);
-  TRY(P->phi.get<double>(exp_elems, &phi));  // sized beforehand by the caller (no realloc here)
-  TRY(P->psi.get<double>(exp_elems, &psi));
+  TRY(P->phi[side].get<double>(exp_elems, &phi));  // sized beforehand (no realloc here)
+  TRY(P->psi[side].get<double>(exp_elems, &psi));
   const int64_t ldE = int64_t(F.ncells) * p;
   auto* dc = static_cast<FmmCell*>(C.d_cells.p);
   auto* dd = static_cast<FmmOpDesc*>(C.d_descs.p);
   auto* dt = static_cast<FmmTerm*>(C.d_terms.p);
   auto* dk = static_cast<FmmTask*>(C.d_tasks.p);
   auto* ops = static_cast<double*>(C.d_ops.p);
-  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, ops, P->st,
+  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, ops, st,
                     &P->launches));
   const bool dbg = std::getenv("SVD1_DEBUG") != nullptr;
   if (dbg) {  // host-side validation of the task lists
@@ -625,9 +639,9 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, ops, U_in, ld_in, d_src, U_out, ld_out,
-                      d_dst, phi, psi, ldE, P->st, &P->launches));
+                      d_dst, phi, psi, ldE, st, &P->launches));
     if (dbg) {
-      cudaError_t err = cudaStreamSynchronize(P->st);
+      cudaError_t err = cudaStreamSynchronize(st);
       fprintf(stderr, "[svd1] pass %zu tasks [%d,%d): %s\n", s, b, e, cudaGetErrorString(err));
       if (err != cudaSuccess) return SVD1_E_CUDA;
     }
@@ -635,10 +649,10 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   return SVD1_OK;
 }
 
-svd1_status ensure_expansions(svd1_plan_t P, size_t elems) {
+svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
   double* x;
-  TRY(P->phi.get<double>(elems, &x));
-  TRY(P->psi.get<double>(elems, &x));
+  TRY(P->phi[side].get<double>(elems, &x));
+  TRY(P->psi[side].get<double>(elems, &x));
   return SVD1_OK;
 }
 
@@ -880,24 +894,24 @@ svd1_status apply_prepare(svd1_plan_t P, StepRecord& S, int64_t rows, bool rever
 
 // Device half: Householder (in place on U_in), Cauchy apply, passthrough.
 svd1_status apply_launch(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_in, double* U_out,
-                         int64_t ld_out, int ev0) {
+                         int64_t ld_out, int ev0, cudaStream_t st, int side) {
   const int64_t rows = S.rows;
   if (rows <= 0) return SVD1_OK;
-  TRY(ev_record(P, ev0));
+  TRY(ev_record(P, ev0, st));
   if (S.h_goff.size() > 1)
     TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1,
                          static_cast<int32_t*>(S.d_goff.p), static_cast<int32_t*>(S.d_hcols.p),
-                         static_cast<double*>(S.d_hv.p), P->st, &P->launches));
+                         static_cast<double*>(S.d_hv.p), st, &P->launches));
   if (S.na > 0)
     TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_da.p), static_cast<int32_t*>(S.d_k.p),
                       static_cast<double*>(S.d_tau.p), static_cast<double*>(S.d_zhat.p),
                       static_cast<double*>(S.d_cs.p), U_in, ld_in, static_cast<int32_t*>(S.d_src.p),
-                      U_out, ld_out, static_cast<int32_t*>(S.d_dst.p)));
+                      U_out, ld_out, static_cast<int32_t*>(S.d_dst.p), st, side));
   if (!S.pass_src.empty())
     TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, static_cast<int32_t*>(S.d_pass_src.p),
                     U_out, ld_out, static_cast<int32_t*>(S.d_pass_dst.p),
-                    static_cast<double*>(S.d_pass_scale.p), P->st, &P->launches));
-  TRY(ev_record(P, ev0 + 1));
+                    static_cast<double*>(S.d_pass_scale.p), st, &P->launches));
+  TRY(ev_record(P, ev0 + 1, st));
   return SVD1_OK;
 }
 
@@ -953,6 +967,12 @@ svd1_status svd1_plan_destroy(svd1_plan_t P) {
   if (P->arena_ev) cudaEventDestroy(P->arena_ev);
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : P->sync_ev)
+    if (e) cudaEventDestroy(e);
+  if (P->st2) {
+    cudaStreamSynchronize(P->st2);
+    cudaStreamDestroy(P->st2);
+  }
   delete P;
   return SVD1_OK;
 }
@@ -1111,23 +1131,36 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
   if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * n, &Wv));
   // expansions are sized for all four applies up front (a mid-stream realloc would sync)
-  {
-    size_t exp_max = 0;
-    for (int e : {0, 2})
-      if (S[e].rows > 0 && S[e].na > 0) exp_max = std::max(exp_max, cauchy_exp_elems(S[e].cp));
-    const int64_t rows_max = std::max(c.u_rows, c.v_rows);
-    const size_t guess = size_t(rows_max) * size_t(P->p) * size_t(4 * std::max<int64_t>(n, 1) / std::max(P->leaf, 1) + 8);
-    TRY(ensure_expansions(P, std::max(exp_max, guess)));
+  const int64_t rows_max = std::max(c.u_rows, c.v_rows);
+  const size_t guess = size_t(rows_max) * size_t(P->p) *
+                       size_t(4 * std::max<int64_t>(n, 1) / std::max(P->leaf, 1) + 8);
+  for (int side = 0; side < 2; ++side) {
+    const int e = 2 * side;
+    size_t need = guess;
+    if (S[e].rows > 0 && S[e].na > 0) need = std::max(need, cauchy_exp_elems(S[e].cp));
+    TRY(ensure_expansions(P, side, need));
   }
-  TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0));
-  TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4));
+  if (!P->st2) SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->st2, cudaStreamNonBlocking));
+  // U side on the plan stream, V side on st2 (independent until the end of the update)
+  TRY(stream_wait(P, 0, P->st, P->st2));  // uploads of the first applies, W buffers
+  TRY(ev_record(P, 16, P->st));           // apply phase start (both sides)
+  TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
+  TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, P->st2, 1));
   TRY(apply_prepare(P, S[1], c.u_rows, true));
   TRY(apply_prepare(P, S[3], c.v_rows, true));
-  for (int e : {1, 3})
-    if (S[e].rows > 0 && S[e].na > 0 && cauchy_exp_elems(S[e].cp) > P->phi.cap / sizeof(double))
-      TRY(ensure_expansions(P, cauchy_exp_elems(S[e].cp)));  // rare: deeper tree than guessed
-  TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2));
-  TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6));
+  for (int e : {1, 3}) {
+    const int side = e / 2;
+    if (S[e].rows > 0 && S[e].na > 0 &&
+        cauchy_exp_elems(S[e].cp) > P->phi[side].cap / sizeof(double)) {
+      SVD1_CUDA_TRY(cudaDeviceSynchronize());  // rare: deeper tree than guessed
+      TRY(ensure_expansions(P, side, cauchy_exp_elems(S[e].cp)));
+    }
+  }
+  TRY(stream_wait(P, 1, P->st, P->st2));  // uploads of the V-side second apply
+  TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
+  TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, P->st2, 1));
+  TRY(stream_wait(P, 2, P->st2, P->st));  // join
+  TRY(ev_record(P, 17, P->st));           // apply phase end
   R.t_ms[2] = now_ms() - t4;
   std::memcpy(h, sig_new.data(), size_t(m) * sizeof(double));
   SVD1_CUDA_TRY(cudaMemcpyAsync(sigma, h, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, P->st));
@@ -1146,6 +1179,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     R.spectral_ms[e] = S[e].spectral_ms;
   }
   R.t_ms[4] = now_ms() - t0;
+  R.t_ms[5] = ev_ms(P, 16, 17);
   R.kernel_launches = P->launches - launches0;
   if (rep) *rep = R;
   return SVD1_OK;
@@ -1187,8 +1221,9 @@ svd1_status svd1_cauchy_apply(svd1_plan_t P, int64_t rows, int64_t n, const doub
   {
     CauchyPrep& C = P->standalone;
     TRY(cauchy_prepare(P, C, rows, int(n), dh, mu, p));
-    TRY(ensure_expansions(P, cauchy_exp_elems(C)));
-    TRY(cauchy_launch(P, C, d, k, tau, zhat, colscale, U_in, ld_in, nullptr, U_out, ld_out, nullptr));
+    TRY(ensure_expansions(P, 0, cauchy_exp_elems(C)));
+    TRY(cauchy_launch(P, C, d, k, tau, zhat, colscale, U_in, ld_in, nullptr, U_out, ld_out, nullptr,
+                      P->st, 0));
     used = C.fmm;
   }
   if (fmm_used) *fmm_used = used ? 1 : 0;
