@@ -292,7 +292,8 @@ def main():
                            "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
                 "cpu_baseline": cpu, "check": check,
-                "spectral_ms_per_step": sp_ms / args.steps, "apply_ms_per_step": ap_ms / args.steps}
+                "spectral_ms_per_step": sp_ms / args.steps, "apply_ms_per_step": ap_ms / args.steps,
+                "host_phase_ms": [sum(r["t_ms"][i] for r in reps) / args.steps for i in range(5)]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -312,85 +312,137 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
 }
 
 // ------------------------------------------------------------------ K3a
-// zhat_i^2 = |prod_j (mu_j - d_i)| / (|rho| prod_{j != i} |d_j - d_i|), evaluated as a
-// product of ratios (mu_j - d_i)/(d_j - d_i) with mantissa/exponent tracking.
-__global__ void __launch_bounds__(256) loewner_kernel(const double* __restrict__ d,
-                                                     const int32_t* __restrict__ k,
-                                                     const double* __restrict__ tau, double rho,
-                                                     const double* __restrict__ z, int n,
-                                                     double* __restrict__ zhat) {
-  const int lane = threadIdx.x & 31;
-  const int i = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
-  if (i >= n) return;
-  const double di = d[i];
-  double P = 1.0;
-  int E = 0, cnt = 0;
-  for (int j = lane; j < n; j += 32) {
-    const double num = (__ldg(d + __ldg(k + j)) - di) + __ldg(tau + j);
-    const double den = (j == i) ? 1.0 : (__ldg(d + j) - di);
-    P *= fabs(num / den);
-    if (++cnt == 8) {
-      int e;
-      P = frexp(P, &e);
-      E += e;
-      cnt = 0;
+// zhat_i^2 = |prod_j (mu_j - d_i)| / (|rho| prod_{j != i} |d_j - d_i|).  Thread per i,
+// the j range split over gridDim.y chunks staged in shared memory (broadcast reads);
+// numerator and denominator are separate running products (no division per term)
+// renormalised with frexp every 8 factors.  Partials (mantissa, exponent) per chunk are
+// combined in a fixed order by loewner_combine_kernel (deterministic).
+constexpr int kLT = 128;   // threads (i) per block
+constexpr int kLJ = 256;   // j per shared-memory tile
+
+__global__ void __launch_bounds__(kLT) loewner_partial_kernel(
+    const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau, int n,
+    int chunk, double* __restrict__ pm, int32_t* __restrict__ pe) {
+  __shared__ double s_d[kLJ], s_mu[kLJ], s_t[kLJ];
+  const int i = blockIdx.x * kLT + threadIdx.x;
+  const int j0 = blockIdx.y * chunk, j1 = min(n, j0 + chunk);
+  const double di = i < n ? d[i] : 0.0;
+  double Pn = 1.0, Pd = 1.0;
+  int E = 0;
+  for (int jb = j0; jb < j1; jb += kLJ) {
+    const int nj = min(kLJ, j1 - jb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nj; t += kLT) {
+      s_d[t] = d[jb + t];
+      s_mu[t] = d[k[jb + t]];
+      s_t[t] = tau[jb + t];
     }
+    __syncthreads();
+    int cnt = 0;
+    for (int t = 0; t < nj; ++t) {
+      const int j = jb + t;
+      Pn *= fabs((s_mu[t] - di) + s_t[t]);
+      Pd *= (j == i) ? 1.0 : fabs(s_d[t] - di);
+      if (++cnt == 8) {
+        int e1, e2;
+        Pn = frexp(Pn, &e1);
+        Pd = frexp(Pd, &e2);
+        E += e1 - e2;
+        cnt = 0;
+      }
+    }
+    int e1, e2;
+    Pn = frexp(Pn, &e1);
+    Pd = frexp(Pd, &e2);
+    E += e1 - e2;
   }
-  {
+  if (i < n) {
     int e;
-    P = frexp(P, &e);
-    E += e;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double Po = __shfl_xor_sync(0xffffffffu, P, o);
-    const int Eo = __shfl_xor_sync(0xffffffffu, E, o);
-    int e;
-    P = frexp(P * Po, &e);
-    E += Eo + e;
-  }
-  if (lane == 0) {
-    const double zh2 = ldexp(P, E) / fabs(rho);
-    zhat[i] = copysign(sqrt(zh2), z[i]);
+    const double m = frexp(Pn / Pd, &e);
+    pm[int64_t(blockIdx.y) * n + i] = m;
+    pe[int64_t(blockIdx.y) * n + i] = E + e;
   }
 }
 
+__global__ void loewner_combine_kernel(const double* __restrict__ pm, const int32_t* __restrict__ pe,
+                                       int nchunks, int n, double rho, const double* __restrict__ z,
+                                       double* __restrict__ zhat) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double P = 1.0;
+  int E = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    int e;
+    P = frexp(P * pm[int64_t(c) * n + i], &e);
+    E += e + pe[int64_t(c) * n + i];
+  }
+  const double zh2 = ldexp(P, E) / fabs(rho);
+  zhat[i] = copysign(sqrt(zh2), z[i]);
+}
+
 // ------------------------------------------------------------------ K3b/K12
-// For column j: y_i = zhat_i |tau_j| / ((d_i - d_kj) - tau_j)  (|y_i| <= |zhat_i| since the
+// For column j: y_i = zhat_i |tau_j| / ((d_i - d_kj) - tau_j)  (|y_i| <~ |zhat_i|: the
 // origin pole is the nearest), s = sum y^2, colscale_j = |tau_j| / sqrt(s) = 1/||c_j||,
 // carry_out[q][j] = (sum_i y_i carry_q[i]) / sqrt(s) = (X^T carry_q)_j.
+// Thread per column j; the i range is split over gridDim.y chunks staged in shared
+// memory; partial sums are reduced in chunk order by colnorm_combine_kernel.
+constexpr int kCT = 128;
+constexpr int kCI = 256;
+
 template <int NC>
-__global__ void __launch_bounds__(256) colnorm_carry_kernel(const double* __restrict__ d,
-                                                           const int32_t* __restrict__ k,
-                                                           const double* __restrict__ tau,
-                                                           const double* __restrict__ zhat, int n,
-                                                           const double* __restrict__ carry,
-                                                           double* __restrict__ colscale,
-                                                           double* __restrict__ carry_out,
-                                                           int32_t* __restrict__ status) {
-  const int lane = threadIdx.x & 31;
-  const int j = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
-  if (j >= n) return;
-  const double dk = d[k[j]], tj = tau[j], at = fabs(tj);
+__global__ void __launch_bounds__(kCT) colnorm_partial_kernel(
+    const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau,
+    const double* __restrict__ zhat, int n, int chunk, const double* __restrict__ carry,
+    double* __restrict__ part) {
+  __shared__ double s_d[kCI], s_z[kCI], s_c[NC > 0 ? NC : 1][kCI];
+  const int j = blockIdx.x * kCT + threadIdx.x;
+  const int i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
+  const bool ok = j < n;
+  const double dk = ok ? d[k[j]] : 0.0, tj = ok ? tau[j] : 1.0, at = fabs(tj);
   double s = 0.0, t[NC > 0 ? NC : 1];
 #pragma unroll
   for (int q = 0; q < NC; ++q) t[q] = 0.0;
-  for (int i = lane; i < n; i += 32) {
-    const double y = __ldg(zhat + i) * (at / ((__ldg(d + i) - dk) - tj));
-    s = fma(y, y, s);
+  for (int ib = i0; ib < i1; ib += kCI) {
+    const int ni = min(kCI, i1 - ib);
+    __syncthreads();
+    for (int u = threadIdx.x; u < ni; u += kCT) {
+      s_d[u] = d[ib + u];
+      s_z[u] = zhat[ib + u] * 1.0;
 #pragma unroll
-    for (int q = 0; q < NC; ++q) t[q] = fma(y, __ldg(carry + int64_t(q) * n + i), t[q]);
+      for (int q = 0; q < NC; ++q) s_c[q][u] = carry[int64_t(q) * n + ib + u];
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int u = 0; u < ni; ++u) {
+      const double y = s_z[u] * at * fast_rcp((s_d[u] - dk) - tj);
+      s = fma(y, y, s);
+#pragma unroll
+      for (int q = 0; q < NC; ++q) t[q] = fma(y, s_c[q][u], t[q]);
+    }
   }
-  s = warp_sum(s);
+  if (ok) {
+    const int64_t base = int64_t(blockIdx.y) * (NC + 1) * n;
+    part[base + j] = s;
 #pragma unroll
-  for (int q = 0; q < NC; ++q) t[q] = warp_sum(t[q]);
-  if (lane == 0) {
-    const double rs = sqrt(s);
-    const double cs = at / rs;
-    if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
-    colscale[j] = cs;
-#pragma unroll
-    for (int q = 0; q < NC; ++q) carry_out[int64_t(q) * n + j] = t[q] / rs;
+    for (int q = 0; q < NC; ++q) part[base + int64_t(q + 1) * n + j] = t[q];
+  }
+}
+
+__global__ void colnorm_combine_kernel(const double* __restrict__ part, int nchunks, int nc, int n,
+                                       const double* __restrict__ tau, double* __restrict__ colscale,
+                                       double* __restrict__ carry_out, int32_t* __restrict__ status) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[int64_t(c) * (nc + 1) * n + j];
+  const double rs = sqrt(s);
+  const double cs = fabs(tau[j]) / rs;
+  if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
+  colscale[j] = cs;
+  for (int q = 0; q < nc; ++q) {
+    double t = 0.0;
+    for (int c = 0; c < nchunks; ++c) t += part[int64_t(c) * (nc + 1) * n + int64_t(q + 1) * n + j];
+    carry_out[int64_t(q) * n + j] = t / rs;
   }
 }
 
@@ -449,32 +501,56 @@ svd1_status secular(const double* d, const double* z, double rho, int n, int32_t
   return SVD1_OK;
 }
 
+// chunks over the inner index: enough blocks to fill 148 SMs a few times over
+static int inner_chunks(int n, int threads) {
+  const int outer = (n + threads - 1) / threads;
+  int ch = (4 * 148 + outer - 1) / outer;
+  ch = std::max(1, std::min(ch, (n + 255) / 256));
+  return ch;
+}
+
+int64_t spectral_scratch_elems(int n, int ncarry) {
+  const int ch = std::max(inner_chunks(n, kLT), inner_chunks(n, kCT));
+  return int64_t(ch) * n * (ncarry + 2) + 16;
+}
+
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
-                    const double* z, int n, double* zhat, cudaStream_t st, int64_t* launches) {
+                    const double* z, int n, double* zhat, double* scratch, cudaStream_t st,
+                    int64_t* launches) {
   if (n <= 0) return SVD1_OK;
-  loewner_kernel<<<blocks_for_warps(n), 256, 0, st>>>(d, k, tau, rho, z, n, zhat);
-  *launches += 1;
+  const int ch = inner_chunks(n, kLT);
+  const int chunk = (n + ch - 1) / ch;
+  double* pm = scratch;
+  int32_t* pe = reinterpret_cast<int32_t*>(scratch + int64_t(ch) * n);
+  loewner_partial_kernel<<<dim3(unsigned((n + kLT - 1) / kLT), unsigned(ch)), kLT, 0, st>>>(d, k, tau, n,
+                                                                                       chunk, pm, pe);
+  loewner_combine_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(pm, pe, ch, n, rho, z, zhat);
+  *launches += 2;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }
 
 svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
                           const double* zhat, int n, const double* carry, int ncarry,
-                          double* colscale, double* carry_out, int32_t* status, cudaStream_t st,
-                          int64_t* launches) {
+                          double* colscale, double* carry_out, int32_t* status, double* scratch,
+                          cudaStream_t st, int64_t* launches) {
   if (n <= 0) return SVD1_OK;
-  const unsigned g = blocks_for_warps(n);
+  const int ch = inner_chunks(n, kCT);
+  const int chunk = (n + ch - 1) / ch;
+  const dim3 g(unsigned((n + kCT - 1) / kCT), unsigned(ch));
   switch (ncarry) {
-    case 0: colnorm_carry_kernel<0><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
-    case 1: colnorm_carry_kernel<1><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
-    case 2: colnorm_carry_kernel<2><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
-    case 3: colnorm_carry_kernel<3><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
-    case 4: colnorm_carry_kernel<4><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
-    case 5: colnorm_carry_kernel<5><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
-    case 6: colnorm_carry_kernel<6><<<g, 256, 0, st>>>(d, k, tau, zhat, n, carry, colscale, carry_out, status); break;
+    case 0: colnorm_partial_kernel<0><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
+    case 1: colnorm_partial_kernel<1><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
+    case 2: colnorm_partial_kernel<2><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
+    case 3: colnorm_partial_kernel<3><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
+    case 4: colnorm_partial_kernel<4><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
+    case 5: colnorm_partial_kernel<5><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
+    case 6: colnorm_partial_kernel<6><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
     default: return SVD1_E_INVALID;
   }
-  *launches += 1;
+  colnorm_combine_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(scratch, ch, ncarry, n, tau, colscale,
+                                                                     carry_out, status);
+  *launches += 2;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

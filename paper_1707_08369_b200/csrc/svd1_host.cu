@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "svd1_internal.cuh"
@@ -115,6 +116,7 @@ struct StepRecord {
   std::vector<int32_t> pass_src, pass_dst;  // deflated: input col -> output position
   std::vector<double> pass_scale;
   std::vector<int32_t> tgt_pos;       // active target j -> output position q
+  std::vector<int32_t> dst_cols, pass_dst_cols;  // output buffer columns
   std::vector<double> da, mu, tau_h, cs_h;  // host copies (tree + sign folding)
   std::vector<int32_t> k_h;
   int max_iter = 0;
@@ -141,7 +143,8 @@ struct StepRecord {
   }
   // device arrays
   DevBuf d_da, d_za, d_k, d_tau, d_zhat, d_cs, d_src, d_dst, d_pass_src, d_pass_dst, d_pass_scale,
-      d_goff, d_hcols, d_hv, d_carry, d_carry_out, d_status, d_iters;
+      d_goff, d_hcols, d_hv, d_carry, d_carry_out, d_status, d_iters, d_scratch, d_in, d_out;
+  std::vector<double> stage;
   CauchyPrep cp;
 };
 
@@ -565,21 +568,26 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
 // U_out[:, dst[j]] = cs_j sum_i U_in[:, src[i]] zhat_i / ((d_i - d_kj) - tau_j)
 
 
-svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
-                           const std::vector<double>& da, const std::vector<double>& mu, int p) {
-  const int minn = P->cfg.fmm_min_n > 0 ? P->cfg.fmm_min_n : 384;
+// host compute only (thread-safe: touches nothing but C)
+void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
+                 const std::vector<double>& da, const std::vector<double>& mu, int p) {
+  const int minn = cfg.fmm_min_n > 0 ? cfg.fmm_min_n : 384;
   const int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2: s ~ 2p, capped by the tile
-  bool fmm = (P->cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
-  if (P->cfg.flags & SVD1_FORCE_DIRECT) fmm = false;
+  bool fmm = (cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
+  if (cfg.flags & SVD1_FORCE_DIRECT) fmm = false;
   C.fmm = fmm;
   C.p = p;
   C.na = na;
   C.rows = rows;
   C.flops = 2.0 * double(rows) * double(na) * double(na);
-  if (!fmm) return SVD1_OK;
+  if (!fmm) return;
+  fmm_build_host(C.F, na, leaf, p, da, mu);
+  C.flops = double(C.F.flops_per_row) * double(rows);
+}
+
+svd1_status cauchy_upload(svd1_plan_t P, CauchyPrep& C) {
+  if (!C.fmm) return SVD1_OK;
   FmmHost& F = C.F;
-  fmm_build_host(F, na, leaf, p, da, mu);
-  C.flops = double(F.flops_per_row) * double(rows);
   FmmCell* dc;
   FmmOpDesc* dd;
   FmmTerm* dt;
@@ -591,6 +599,12 @@ svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
   double* ops;
   TRY(C.d_ops.get<double>(size_t(F.ops_elems), &ops));
   return SVD1_OK;
+}
+
+svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
+                           const std::vector<double>& da, const std::vector<double>& mu, int p) {
+  cauchy_plan(P->cfg, C, rows, na, da, mu, p);
+  return cauchy_upload(P, C);
 }
 
 size_t cauchy_exp_elems(const CauchyPrep& C) {
@@ -672,7 +686,20 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   std::vector<int32_t>& perm = S.perm;
   perm.resize(N);
   std::iota(perm.begin(), perm.end(), 0);
-  std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return D[a] < D[b]; });
+  // stable ascending order; D is usually already ascending (second eigen-update) or
+  // strictly descending (user's sigma order) -> O(n) fast paths
+  bool asc = true, desc_strict = true;
+  for (int q = 1; q < N; ++q) {
+    if (D[q] < D[q - 1]) asc = false;
+    if (!(D[q] < D[q - 1])) desc_strict = false;
+  }
+  if (!asc) {
+    if (desc_strict) {
+      std::reverse(perm.begin(), perm.end());
+    } else {
+      std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return D[a] < D[b]; });
+    }
+  }
   std::vector<double>& ds = S.ds;
   ds.resize(N);
   std::vector<double> zs(N);
@@ -753,26 +780,41 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   std::vector<double> carry_act(size_t(nc) * na);
   for (int q = 0; q < nc; ++q)
     for (int i = 0; i < na; ++i) carry_act[size_t(q) * na + i] = cs_sorted[q][S.act[i]];
-  double *dda, *dza, *dtau, *dzh, *dcs, *dcar, *dco;
-  int32_t *dk, *dst, *dit;
-  TRY(upload(P, S.d_da, S.da, &dda));
-  TRY(upload(P, S.d_za, za, &dza));
-  TRY(upload(P, S.d_carry, carry_act, &dcar));
-  TRY(S.d_k.get<int32_t>(na, &dk));
-  TRY(S.d_tau.get<double>(na, &dtau));
+  // one upload [d_a | z_a | carries] and one read-back
+  // [k (na words) | tau | cs | carry_out (nc*na) | iters (int32) | status]
+  const size_t in_words = size_t(na) * (2 + nc);
+  const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
+  double* din;
+  double* dout;
+  TRY(S.d_in.get<double>(in_words, &din));
+  TRY(S.d_out.get<double>(words, &dout));
+  {
+    std::vector<double>& stage = S.stage;
+    stage.resize(in_words);
+    std::memcpy(stage.data(), S.da.data(), na * sizeof(double));
+    std::memcpy(stage.data() + na, za.data(), na * sizeof(double));
+    std::memcpy(stage.data() + 2 * na, carry_act.data(), size_t(nc) * na * sizeof(double));
+    TRY(arena_put(P, stage.data(), in_words * sizeof(double), din));
+  }
+  double* dda = din;
+  double* dza = din + na;
+  double* dcar = din + 2 * na;
+  int32_t* dk = reinterpret_cast<int32_t*>(dout);
+  double* dtau = dout + na;
+  double* dcs = dout + 2 * na;
+  double* dco = dout + 3 * na;
+  int32_t* dit = reinterpret_cast<int32_t*>(dout + size_t(3 + nc) * na);
+  int32_t* dst = reinterpret_cast<int32_t*>(dout + words - 1);
+  double* dzh;
   TRY(S.d_zhat.get<double>(na, &dzh));
-  TRY(S.d_cs.get<double>(na, &dcs));
-  TRY(S.d_carry_out.get<double>(size_t(nc) * na, &dco));
-  TRY(S.d_status.get<int32_t>(1, &dst));
-  TRY(S.d_iters.get<int32_t>(na, &dit));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
   TRY(ev_record(P, ev0));
+  double* scr;
+  TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
   TRY(secular(dda, dza, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
-  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, P->st, &P->launches));
-  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, P->st, &P->launches));
+  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, P->st, &P->launches));
+  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, P->st, &P->launches));
   TRY(ev_record(P, ev0 + 1));
-  // read back into pinned memory: [k (as int32 pairs) | tau | cs | carry_out | iters | status]
-  const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
   if (words * sizeof(double) > S.rb_cap) {
     if (S.rb) cudaFreeHost(S.rb);
     S.rb = nullptr;
@@ -783,16 +825,7 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     }
     S.rb_cap = words * sizeof(double);
   }
-  double* rb = S.rb;
-  SVD1_CUDA_TRY(cudaMemcpyAsync(rb, dk, na * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + na, dtau, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + 2 * na, dcs, na * sizeof(double), cudaMemcpyDeviceToHost, P->st));
-  if (nc)
-    SVD1_CUDA_TRY(cudaMemcpyAsync(rb + 3 * na, dco, size_t(nc) * na * sizeof(double),
-                                  cudaMemcpyDeviceToHost, P->st));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + size_t(3 + nc) * na, dit, na * sizeof(int32_t),
-                                cudaMemcpyDeviceToHost, P->st));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(rb + words - 1, dst, sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(S.rb, dout, words * sizeof(double), cudaMemcpyDeviceToHost, P->st));
   return SVD1_OK;
 }
 
@@ -826,15 +859,34 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
     double v;
     int flag, pos;
   };
+  // both lists are ascending (deflated d in sorted order; roots interlace) -> O(n) merge
+  // (stable ascending, deflated first on ties); fall back to a sort if mu is not sorted
   std::vector<Item> items;
   items.reserve(N);
-  for (int s : S.dfl) items.push_back({S.ds[s], 0, s});
-  for (int j = 0; j < na; ++j) items.push_back({S.mu[j], 1, j});
-  std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
-    if (a.v != b.v) return a.v < b.v;
-    if (a.flag != b.flag) return a.flag < b.flag;
-    return a.pos < b.pos;
-  });
+  bool mu_sorted = true;
+  for (int j = 1; j < na; ++j)
+    if (S.mu[j] < S.mu[j - 1]) mu_sorted = false;
+  if (mu_sorted) {
+    size_t a = 0;
+    int j = 0;
+    while (a < S.dfl.size() || j < na) {
+      if (j >= na || (a < S.dfl.size() && S.ds[S.dfl[a]] <= S.mu[j])) {
+        items.push_back({S.ds[S.dfl[a]], 0, S.dfl[a]});
+        ++a;
+      } else {
+        items.push_back({S.mu[j], 1, j});
+        ++j;
+      }
+    }
+  } else {
+    for (int s : S.dfl) items.push_back({S.ds[s], 0, s});
+    for (int j = 0; j < na; ++j) items.push_back({S.mu[j], 1, j});
+    std::sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
+      if (a.v != b.v) return a.v < b.v;
+      if (a.flag != b.flag) return a.flag < b.flag;
+      return a.pos < b.pos;
+    });
+  }
   S.tgt_pos.assign(na, -1);
   std::vector<double> Dn(N);
   std::vector<std::vector<double>> cn(nc, std::vector<double>(N));
@@ -858,11 +910,23 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
 
 // Host half of one apply: column maps, Householder data, Cauchy plan; staged uploads.
 // out_col(q) = reverse ? (N - 1 - q) : q.
-svd1_status apply_prepare(svd1_plan_t P, StepRecord& S, int64_t rows, bool reverse) {
+// Host half of one apply, in two parts: apply_plan (pure host compute, thread-safe per
+// step: column maps and the Cauchy/FMM plan) and apply_upload (staged uploads).
+// out_col(q) = reverse ? (N - 1 - q) : q.
+void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool reverse) {
   const int N = S.N;
   S.rows = rows;
   auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
-  if (rows <= 0) return SVD1_OK;
+  if (rows <= 0) return;
+  S.dst_cols.resize(S.na);
+  for (int j = 0; j < S.na; ++j) S.dst_cols[j] = oc(S.tgt_pos[j]);
+  S.pass_dst_cols.resize(S.pass_dst.size());
+  for (size_t q = 0; q < S.pass_dst.size(); ++q) S.pass_dst_cols[q] = oc(S.pass_dst[q]);
+  if (S.na > 0) cauchy_plan(cfg, S.cp, rows, S.na, S.da, S.mu, p);
+}
+
+svd1_status apply_upload(svd1_plan_t P, StepRecord& S) {
+  if (S.rows <= 0) return SVD1_OK;
   if (S.h_goff.size() > 1) {
     int32_t *goff, *cols;
     double* hv;
@@ -871,24 +935,33 @@ svd1_status apply_prepare(svd1_plan_t P, StepRecord& S, int64_t rows, bool rever
     TRY(upload(P, S.d_hv, S.h_hv, &hv));
   }
   if (S.na > 0) {
-    std::vector<int32_t> dst(S.na);
-    for (int j = 0; j < S.na; ++j) dst[j] = oc(S.tgt_pos[j]);
     int32_t *dsrc, *ddst;
     double* dcs;
     TRY(upload(P, S.d_src, S.src_cols, &dsrc));
-    TRY(upload(P, S.d_dst, dst, &ddst));
+    TRY(upload(P, S.d_dst, S.dst_cols, &ddst));
     TRY(upload(P, S.d_cs, S.cs_h, &dcs));  // cs_h may carry the sign alignment
-    TRY(cauchy_prepare(P, S.cp, rows, S.na, S.da, S.mu, P->p));
+    TRY(cauchy_upload(P, S.cp));
   }
   if (!S.pass_src.empty()) {
-    std::vector<int32_t> dst(S.pass_dst.size());
-    for (size_t q = 0; q < dst.size(); ++q) dst[q] = oc(S.pass_dst[q]);
     int32_t *ds, *dd;
     double* sc;
     TRY(upload(P, S.d_pass_src, S.pass_src, &ds));
-    TRY(upload(P, S.d_pass_dst, dst, &dd));
+    TRY(upload(P, S.d_pass_dst, S.pass_dst_cols, &dd));
     TRY(upload(P, S.d_pass_scale, S.pass_scale, &sc));
   }
+  return SVD1_OK;
+}
+
+// Plan two steps concurrently (one worker thread), then stage their uploads.
+svd1_status apply_prepare2(svd1_plan_t P, StepRecord& A, int64_t rows_a, StepRecord& B,
+                           int64_t rows_b, bool reverse) {
+  const svd1_config cfg = P->cfg;
+  const int p = P->p;
+  std::thread worker([&] { apply_plan(cfg, p, B, rows_b, reverse); });
+  apply_plan(cfg, p, A, rows_a, reverse);
+  worker.join();
+  TRY(apply_upload(P, A));
+  TRY(apply_upload(P, B));
   return SVD1_OK;
 }
 
@@ -903,8 +976,8 @@ svd1_status apply_launch(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_
                          static_cast<int32_t*>(S.d_goff.p), static_cast<int32_t*>(S.d_hcols.p),
                          static_cast<double*>(S.d_hv.p), st, &P->launches));
   if (S.na > 0)
-    TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_da.p), static_cast<int32_t*>(S.d_k.p),
-                      static_cast<double*>(S.d_tau.p), static_cast<double*>(S.d_zhat.p),
+    TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
+                      static_cast<double*>(S.d_out.p) + S.na, static_cast<double*>(S.d_zhat.p),
                       static_cast<double*>(S.d_cs.p), U_in, ld_in, static_cast<int32_t*>(S.d_src.p),
                       U_out, ld_out, static_cast<int32_t*>(S.d_dst.p), st, side));
   if (!S.pass_src.empty())
@@ -1068,9 +1141,12 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8));
     TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12));
   }
+  const double tA = now_ms();
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  const double tB = now_ms();
   TRY(spectral_finish(P, S[0], Du, cu));
   TRY(spectral_finish(P, S[2], Dv, cv));
+  const double tC = now_ms();
   // Round 2: STEP 5 (U, rho2, z2 = X1^T U^T b1) and STEP 7 (V, rho4)
   {
     std::vector<double> z2 = cu[0], z4 = cv[0];
@@ -1080,11 +1156,16 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14));
   }
   // host work overlapping round 2 on the GPU: Cauchy plans of the first applies
-  TRY(apply_prepare(P, S[0], c.u_rows, false));
-  TRY(apply_prepare(P, S[2], c.v_rows, false));
+  const double tD = now_ms();
+  TRY(apply_prepare2(P, S[0], c.u_rows, S[2], c.v_rows, false));
+  const double tE = now_ms();
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  const double tF = now_ms();
   TRY(spectral_finish(P, S[1], Du, cu));
   TRY(spectral_finish(P, S[3], Dv, cv));
+  if (std::getenv("SVD1_TIMING"))
+    fprintf(stderr, "[svd1] launch1 %.3f wait1 %.3f finish1 %.3f launch2 %.3f plan %.3f wait2 %.3f finish2 %.3f\n",
+            tA - t1, tB - tA, tC - tB, tD - tC, tE - tD, tF - tE, now_ms() - tF);
   const double t3 = now_ms();
   R.t_ms[1] = t3 - t1;
   // ---- sign alignment: final column i = position N-1-i
@@ -1146,8 +1227,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   TRY(ev_record(P, 16, P->st));           // apply phase start (both sides)
   TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
   TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, P->st2, 1));
-  TRY(apply_prepare(P, S[1], c.u_rows, true));
-  TRY(apply_prepare(P, S[3], c.v_rows, true));
+  TRY(apply_prepare2(P, S[1], c.u_rows, S[3], c.v_rows, true));
   for (int e : {1, 3}) {
     const int side = e / 2;
     if (S[e].rows > 0 && S[e].na > 0 &&
@@ -1283,7 +1363,9 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
 svd1_status svd1_loewner(svd1_plan_t P, int64_t n, const double* d, const int32_t* k, const double* tau,
                          double rho, const double* z, double* zhat_out) {
   if (!P || n < 0 || !d || !k || !tau || !z || !zhat_out || rho == 0.0) return SVD1_E_INVALID;
-  TRY(loewner(d, k, tau, rho, z, int(n), zhat_out, P->st, &P->launches));
+  double* scr;
+  TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr));
+  TRY(loewner(d, k, tau, rho, z, int(n), zhat_out, scr, P->st, &P->launches));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   return SVD1_OK;
 }
@@ -1295,9 +1377,11 @@ svd1_status svd1_colnorms(svd1_plan_t P, int64_t n, const double* d, const int32
   int32_t* dst;
   double* cs;
   TRY(P->status.get<int32_t>(1, &dst));
-  TRY(P->scratch_d.get<double>(size_t(n), &cs));
+  TRY(P->scratch_i.get<double>(size_t(n), &cs));
+  double* scr;
+  TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
-  TRY(colnorm_carry(d, k, tau, zhat, int(n), nullptr, 0, cs, nullptr, dst, P->st, &P->launches));
+  TRY(colnorm_carry(d, k, tau, zhat, int(n), nullptr, 0, cs, nullptr, dst, scr, P->st, &P->launches));
   std::vector<double> h(n);
   SVD1_CUDA_TRY(cudaMemcpyAsync(h.data(), cs, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));

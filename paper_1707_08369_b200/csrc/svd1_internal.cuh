@@ -44,13 +44,17 @@ int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t
 svd1_status secular(const double* d, const double* z, double rho, int n, int32_t* k_out,
                     double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
                     int64_t* launches);
-// K3a: Loewner zhat (warp per i)
+// scratch (doubles) needed by loewner / colnorm_carry for size n and ncarry vectors
+int64_t spectral_scratch_elems(int n, int ncarry);
+// K3a: Loewner zhat (thread per i, split-j partial products + ordered combine)
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
-                    const double* z, int n, double* zhat, cudaStream_t st, int64_t* launches);
-// K3b + K12: colscale_j = 1/||c_j|| and carry_out[q][j] = (X^T carry_q)_j (warp per j).
+                    const double* z, int n, double* zhat, double* scratch, cudaStream_t st,
+                    int64_t* launches);
+// K3b + K12: colscale_j = 1/||c_j|| and carry_out[q][j] = (X^T carry_q)_j
+// (thread per j, split-i partial sums + ordered combine).
 svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
                           const double* zhat, int n, const double* carry, int ncarry,
-                          double* colscale, double* carry_out, int32_t* status,
+                          double* colscale, double* carry_out, int32_t* status, double* scratch,
                           cudaStream_t st, int64_t* launches);
 
 // K11: direct apply  U_out[r, dst[j]] = cs[j] * sum_i U_in[r, src[i]] zhat[i] / ((d_i - d_kj) - tau_j)
