@@ -270,7 +270,8 @@ def main():
         orth = max(float((U.T @ U - I).abs().max()), float((V.T @ V - I).abs().max()))
         check = {"residual": res, "orthogonality": orth, "updates": args.steps,
                  "n_active_last": reps[-1]["n_active"], "max_secular_iter": max(max(r["max_iter"]) for r in reps),
-                 "fmm_levels": reps[-1]["fmm_levels"], "fmm_max_near": reps[-1]["fmm_max_near"]}
+                 "fmm_levels": reps[-1]["fmm_levels"], "fmm_max_near": reps[-1]["fmm_max_near"],
+                 "mean_secular_evals": sum(sum(r["mean_iter"]) for r in reps) / (4 * len(reps))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -88,6 +88,7 @@ typedef struct {
   double spectral_ms[4]; /* device time of secular + Loewner + norms per eigen-update */
   int32_t fmm_levels[4]; /* tree depth L of each FMM apply (0 if direct) */
   int32_t fmm_max_near[4]; /* largest near-field list (leaves) of each FMM apply */
+  double mean_iter[4];   /* mean secular evaluations per root (incl. the midpoint one) */
 } svd1_report;
 
 /* Plan: owns workspaces on the device (sized for u_rows x m and v_rows x n),

@@ -143,40 +143,30 @@ struct SecAcc {
   double psi, phi, dpsi, dphi, eabs;
 };
 
-__device__ __forceinline__ double sd(const double* __restrict__ d, int i, int n, bool refl) {
-  return refl ? -__ldg(d + (n - 1 - i)) : __ldg(d + i);
-}
-__device__ __forceinline__ double sz2(const double* __restrict__ z, int i, int n, bool refl) {
-  const double v = refl ? __ldg(z + (n - 1 - i)) : __ldg(z + i);
-  return v * v;
-}
-
 // Sums of w in the gap form: delta_i = (d_i - d_k) - tau.
-// Left set i <= sp (psi), right set i > sp (phi).
-__device__ SecAcc sec_eval(const double* __restrict__ d, const double* __restrict__ z, int n,
-                           bool refl, double dk, double tau, int sp, int lane) {
+// d, z2 are the rho > 0 view (reflected by the host when rho < 0; z2 = z^2).  Left set
+// i <= sp (psi, all terms negative), right set i > sp (phi, one sign), so
+// sum |z_i^2/delta_i| = |psi| + |phi|.
+__device__ SecAcc sec_eval(const double* __restrict__ d, const double* __restrict__ z2, int n,
+                           double dk, double tau, int sp, int lane) {
   SecAcc a = {0, 0, 0, 0, 0};
   for (int i = lane; i <= sp; i += 32) {
-    const double delta = (sd(d, i, n, refl) - dk) - tau;
-    const double rr = fast_rcp(delta);
-    const double t = sz2(z, i, n, refl) * rr;
+    const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
+    const double t = __ldg(z2 + i) * rr;
     a.psi += t;
     a.dpsi = fma(t, rr, a.dpsi);
-    a.eabs += fabs(t);
   }
   for (int i = sp + 1 + lane; i < n; i += 32) {
-    const double delta = (sd(d, i, n, refl) - dk) - tau;
-    const double rr = fast_rcp(delta);
-    const double t = sz2(z, i, n, refl) * rr;
+    const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
+    const double t = __ldg(z2 + i) * rr;
     a.phi += t;
     a.dphi = fma(t, rr, a.dphi);
-    a.eabs += fabs(t);
   }
   a.psi = warp_sum(a.psi);
   a.phi = warp_sum(a.phi);
   a.dpsi = warp_sum(a.dpsi);
   a.dphi = warp_sum(a.dphi);
-  a.eabs = warp_sum(a.eabs);
+  a.eabs = fabs(a.psi) + fabs(a.phi);
   return a;
 }
 
@@ -223,8 +213,19 @@ __device__ __forceinline__ double sec_step(double w, const SecAcc& a, double r, 
 
 constexpr int kSecMaxIt = 100;
 
+// rho > 0 view of (d, z): reflected (-d reversed, z reversed) when rho < 0; z squared.
+__global__ void secular_orient_kernel(const double* __restrict__ d, const double* __restrict__ z,
+                                      double rho, int n, double* __restrict__ dr,
+                                      double* __restrict__ z2r) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int src = rho < 0.0 ? n - 1 - i : i;
+  dr[i] = rho < 0.0 ? -d[src] : d[src];
+  z2r[i] = z[src] * z[src];
+}
+
 __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__ d,
-                                                     const double* __restrict__ z, double rho, int n,
+                                                     const double* __restrict__ z2, double rho, int n,
                                                      int32_t* __restrict__ k_out,
                                                      double* __restrict__ tau_out,
                                                      int32_t* __restrict__ iters_out,
@@ -232,22 +233,21 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
   const int lane = threadIdx.x & 31;
   const int j = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
   if (j >= n) return;
-  const bool refl = rho < 0.0;  // solve (-d reversed, z reversed, -rho) and map back
+  const bool refl = rho < 0.0;  // d, z2 hold (-d reversed, z^2 reversed); map the roots back
   const double r = fabs(rho);
   int k = j, it = 0, stat = 0;
   double tau;
   if (n == 1) {
-    const double z0 = z[0];
-    tau = r * z0 * z0;  // mu = d + rho z^2
+    tau = r * z2[0];  // mu = d + rho z^2
   } else {
     const int sp = (j < n - 1) ? j : n - 2;
-    const double dsp = sd(d, sp, n, refl), dsp1 = sd(d, sp + 1, n, refl);
+    const double dsp = d[sp], dsp1 = d[sp + 1];
     double lo, hi;
     bool solved = false;
     if (j < n - 1) {
       // interlacing bracket (d_j, d_{j+1}); origin = nearer pole by the sign of w(mid)
       const double gap = dsp1 - dsp, mid = 0.5 * gap;
-      const SecAcc a = sec_eval(d, z, n, refl, dsp, mid, sp, lane);
+      const SecAcc a = sec_eval(d, z2, n, dsp, mid, sp, lane);
       const double w = 1.0 + r * (a.psi + a.phi);
       it = 1;
       if (w == 0.0) {  // the midpoint is the root
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
     } else {
       // last root in (d_{n-1}, d_{n-1} + rho ||z||^2]
       double s = 0.0;
-      for (int i = lane; i < n; i += 32) s += sz2(z, i, n, refl);
+      for (int i = lane; i < n; i += 32) s += z2[i];
       s = warp_sum(s);
       k = n - 1;
       lo = 0.0;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
       hi = hi * (1.0 + 4.0 * kEps);  // keep tau = r||z||^2 strictly inside
     }
     if (!solved) {
-      const double dk = sd(d, k, n, refl);
+      const double dk = d[k];
       const double p1 = dsp - dk, p2 = dsp1 - dk;  // pole offsets (one of them is 0)
       bool fin = false;
       for (;;) {
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
           stat |= 1;
           break;
         }
-        const SecAcc a = sec_eval(d, z, n, refl, dk, tau, sp, lane);
+        const SecAcc a = sec_eval(d, z2, n, dk, tau, sp, lane);
         const double w = 1.0 + r * (a.psi + a.phi);
         if (w == 0.0) break;
         if (w < 0.0) lo = tau; else hi = tau;
@@ -491,11 +491,11 @@ svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int
   return SVD1_OK;
 }
 
-svd1_status secular(const double* d, const double* z, double rho, int n, int32_t* k_out,
+svd1_status secular(const double* d, const double* z2, double rho, int n, int32_t* k_out,
                     double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
                     int64_t* launches) {
   if (n <= 0) return SVD1_OK;
-  secular_kernel<<<blocks_for_warps(n), 256, 0, st>>>(d, z, rho, n, k_out, tau_out, iters_out, status);
+  secular_kernel<<<blocks_for_warps(n), 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out, status);
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
@@ -512,6 +512,15 @@ static int inner_chunks(int n, int threads) {
 int64_t spectral_scratch_elems(int n, int ncarry) {
   const int ch = std::max(inner_chunks(n, kLT), inner_chunks(n, kCT));
   return int64_t(ch) * n * (ncarry + 2) + 16;
+}
+
+svd1_status secular_orient(const double* d, const double* z, double rho, int n, double* dr,
+                           double* z2r, cudaStream_t st, int64_t* launches) {
+  if (n <= 0) return SVD1_OK;
+  secular_orient_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(d, z, rho, n, dr, z2r);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
 }
 
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,

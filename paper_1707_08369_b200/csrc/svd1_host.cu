@@ -120,6 +120,7 @@ struct StepRecord {
   std::vector<double> da, mu, tau_h, cs_h;  // host copies (tree + sign folding)
   std::vector<int32_t> k_h;
   int max_iter = 0;
+  double mean_iter = 0.0;
   double spectral_ms = 0.0;
   int ev0 = 0, nc = 0;
   int64_t rows = 0;
@@ -782,7 +783,7 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     for (int i = 0; i < na; ++i) carry_act[size_t(q) * na + i] = cs_sorted[q][S.act[i]];
   // one upload [d_a | z_a | carries] and one read-back
   // [k (na words) | tau | cs | carry_out (nc*na) | iters (int32) | status]
-  const size_t in_words = size_t(na) * (2 + nc);
+  const size_t in_words = size_t(na) * (4 + nc);
   const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
   double* din;
   double* dout;
@@ -793,12 +794,22 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     stage.resize(in_words);
     std::memcpy(stage.data(), S.da.data(), na * sizeof(double));
     std::memcpy(stage.data() + na, za.data(), na * sizeof(double));
-    std::memcpy(stage.data() + 2 * na, carry_act.data(), size_t(nc) * na * sizeof(double));
+    // the secular solver's view: rho > 0 orientation (reflected for rho < 0), z squared
+    double* dr = stage.data() + 2 * na;
+    double* z2r = stage.data() + 3 * na;
+    for (int i = 0; i < na; ++i) {
+      const int src = rho < 0.0 ? na - 1 - i : i;
+      dr[i] = rho < 0.0 ? -S.da[src] : S.da[src];
+      z2r[i] = za[src] * za[src];
+    }
+    std::memcpy(stage.data() + 4 * na, carry_act.data(), size_t(nc) * na * sizeof(double));
     TRY(arena_put(P, stage.data(), in_words * sizeof(double), din));
   }
   double* dda = din;
   double* dza = din + na;
-  double* dcar = din + 2 * na;
+  double* ddr = din + 2 * na;
+  double* dz2r = din + 3 * na;
+  double* dcar = din + 4 * na;
   int32_t* dk = reinterpret_cast<int32_t*>(dout);
   double* dtau = dout + na;
   double* dcs = dout + 2 * na;
@@ -811,7 +822,7 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   TRY(ev_record(P, ev0));
   double* scr;
   TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
-  TRY(secular(dda, dza, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
+  TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
   TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, P->st, &P->launches));
   TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, P->st, &P->launches));
   TRY(ev_record(P, ev0 + 1));
@@ -847,7 +858,12 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
     S.cs_h.assign(rb + 2 * na, rb + 3 * na);
     carry_out = rb + 3 * na;
     const int32_t* it = reinterpret_cast<const int32_t*>(rb + size_t(3 + nc) * na);
-    for (int j = 0; j < na; ++j) S.max_iter = std::max(S.max_iter, it[j]);
+    double sum_it = 0.0;
+    for (int j = 0; j < na; ++j) {
+      S.max_iter = std::max(S.max_iter, it[j]);
+      sum_it += it[j];
+    }
+    S.mean_iter = sum_it / na;
     S.spectral_ms = ev_ms(P, S.ev0, S.ev0 + 1);
     if (st_h & 1) return SVD1_E_NOCONV;
     if (st_h & 2) return SVD1_E_POLE;
@@ -1257,6 +1273,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
       R.fmm_max_near[e] = S[e].cp.F.max_near;
     }
     R.spectral_ms[e] = S[e].spectral_ms;
+    R.mean_iter[e] = S[e].mean_iter;
   }
   R.t_ms[4] = now_ms() - t0;
   R.t_ms[5] = ev_ms(P, 16, 17);
@@ -1348,7 +1365,10 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
   TRY(P->status.get<int32_t>(1, &dst));
   TRY(P->iters.get<int32_t>(size_t(n), &dit));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
-  TRY(secular(d, z, rho, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
+  double* orient;
+  TRY(P->scratch_d.get<double>(size_t(2 * n), &orient));
+  TRY(secular_orient(d, z, rho, int(n), orient, orient + n, P->st, &P->launches));
+  TRY(secular(orient, orient + n, rho, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
   std::vector<int32_t> it(n);
   int32_t st_h = 0;
   SVD1_CUDA_TRY(cudaMemcpyAsync(it.data(), dit, n * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));

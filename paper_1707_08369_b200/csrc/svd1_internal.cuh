@@ -41,9 +41,13 @@ svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int
 int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t n);
 
 // K2: secular roots (warp per root).  status bit 1 = no convergence, 2 = pole.
-svd1_status secular(const double* d, const double* z, double rho, int n, int32_t* k_out,
+// d, z2: the rho > 0 view of the problem (for rho < 0: -d reversed, z^2 reversed);
+// outputs (k, tau) are in the original orientation.
+svd1_status secular(const double* d, const double* z2, double rho, int n, int32_t* k_out,
                     double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
                     int64_t* launches);
+svd1_status secular_orient(const double* d, const double* z, double rho, int n, double* dr,
+                           double* z2r, cudaStream_t st, int64_t* launches);
 // scratch (doubles) needed by loewner / colnorm_carry for size n and ncarry vectors
 int64_t spectral_scratch_elems(int n, int ncarry);
 // K3a: Loewner zhat (thread per i, split-j partial products + ordered combine)
