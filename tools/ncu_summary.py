@@ -41,7 +41,7 @@ def summary_csv(path):
             continue
         v = float(d["Metric Value"].replace(",", ""))
         u = d.get("Metric Unit", "")
-        v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1.0)
+        v = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6}.get(u, 1.0)
         name = re.sub(r"\(.*", "", d["Kernel Name"]).replace("svd1::", "").replace("<unnamed>::", "")
         if "svd1" not in d["Kernel Name"]:
             name = "[input generation / torch] " + name[:50]
