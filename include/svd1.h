@@ -89,6 +89,7 @@ typedef struct {
   int32_t fmm_levels[4]; /* tree depth L of each FMM apply (0 if direct) */
   int32_t fmm_max_near[4]; /* largest near-field list (leaves) of each FMM apply */
   double mean_iter[4];   /* mean secular evaluations per root (incl. the midpoint one) */
+  int32_t pair_rotations; /* repeated-sigma clusters paired by a k x k rotation (D5) */
 } svd1_report;
 
 /* Plan: owns workspaces on the device (sized for u_rows x m and v_rows x n),

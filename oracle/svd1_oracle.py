@@ -443,14 +443,35 @@ def svd_update(U, sigma, V, a, b, sign_rule="explicit", probes=None, rows=None):
     Vh, Dvh = Vh[:, ::-1], Dvh[::-1]
     neg = int(np.sum(Dh < 0))
     sig_hat = np.sqrt(np.maximum(Dh, 0.0))
-    # O7 / Q11 sign alignment of V_hat against U_hat
-    flips = 0
+    # O7 / Q11 pairing of V_hat with U_hat (D5): for each cluster of
+    # numerically equal final eigenvalues (consecutive gap <= 64 eps D_1; singletons
+    # are clusters of one), M = U_c^T A_hat V_c = sigma W with W orthogonal; W is
+    # orthonormalised (QR, positive diagonal) and V_c <- V_c W^T.  For a singleton
+    # this is the sign flip of u^T A_hat v < 0.
+    flips, rotations = 0, 0
+    tolc = 64 * EPS * max(Dh[0], 0.0)
+    clusters, i0 = [], 0
+    while i0 < m:
+        i1 = i0 + 1
+        while i1 < m and Dh[i1 - 1] - Dh[i1] <= tolc:
+            i1 += 1
+        clusters.append((i0, i1))
+        i0 = i1
     if sign_rule == "explicit" and not large:
         A_hat = (U * sigma[None, :]) @ V[:, :m].T + np.outer(a, b)
-        for i in range(m):
-            if sig_hat[i] > 0 and Uh[:, i] @ (A_hat @ Vh[:, i]) < 0:
-                Vh[:, i] = -Vh[:, i]
-                flips += 1
+        for (i0, i1) in clusters:
+            if sig_hat[i0] <= 0:
+                continue
+            if i1 - i0 == 1:
+                if Uh[:, i0] @ (A_hat @ Vh[:, i0]) < 0:
+                    Vh[:, i0] = -Vh[:, i0]
+                    flips += 1
+                continue
+            M = Uh[:, i0:i1].T @ (A_hat @ Vh[:, i0:i1])
+            q, r = np.linalg.qr(M / sig_hat[i0])
+            W = q * np.sign(np.diag(r))[None, :]
+            Vh[:, i0:i1] = Vh[:, i0:i1] @ W.T
+            rotations += 1
     elif sign_rule == "probe":
         P = np.stack([c[::-1] for c in cu])[:, :m]     # p_k in U_hat column order
         Qp = np.stack([c[::-1] for c in cv])[:, :m]    # q_k in V_hat column order
@@ -458,10 +479,21 @@ def svd_update(U, sigma, V, a, b, sign_rule="explicit", probes=None, rows=None):
         cols = np.arange(m)
         s = np.sign(Qp[kstar, cols] * P[kstar, cols])
         s[s == 0] = 1.0
+        for (i0, i1) in clusters:
+            k = i1 - i0
+            if k == 1 or k > P.shape[0] or sig_hat[i0] <= 0:
+                continue
+            Pc, Qc = P[:, i0:i1].T, Qp[:, i0:i1].T        # k x K:  Q_c = M^T P_c
+            Mt = Qc @ Pc.T @ np.linalg.inv(Pc @ Pc.T)
+            q, r = np.linalg.qr(Mt.T / sig_hat[i0])
+            W = q * np.sign(np.diag(r))[None, :]
+            Vh[:, i0:i1] = Vh[:, i0:i1] @ W.T
+            s[i0:i1] = 1.0
+            rotations += 1
         Vh[:, :m] = Vh[:, :m] * s[None, :]
         flips = int(np.sum(s < 0))
     info = dict(rho=(rho1, rho2, rho3, rho4), Qu=Qu, Qv=Qv, alpha=alpha, beta=beta,
-                neg_clamped=neg, flips=flips, Dv_hat=Dvh, D_hat=Dh,
+                neg_clamped=neg, flips=flips, rotations=rotations, Dv_hat=Dvh, D_hat=Dh,
                 updates=(i1, i2, i3, i4))
     return dict(U=Uh, sigma=sig_hat, V=Vh, info=info)
 

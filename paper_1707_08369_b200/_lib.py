@@ -31,7 +31,8 @@ class Report(C.Structure):
                 ("max_iter", i32 * 4), ("fmm_used", i32 * 4), ("p", i32), ("neg_clamped", i32),
                 ("sign_flips", i32), ("noop", i32), ("kernel_launches", i64),
                 ("apply_ms", dbl * 4), ("apply_flops", dbl * 4), ("spectral_ms", dbl * 4),
-                ("fmm_levels", i32 * 4), ("fmm_max_near", i32 * 4), ("mean_iter", dbl * 4)]
+                ("fmm_levels", i32 * 4), ("fmm_max_near", i32 * 4), ("mean_iter", dbl * 4),
+                ("pair_rotations", i32)]
 
     def as_dict(self):
         return dict(t_ms=list(self.t_ms)[:6], n_active=list(self.n_active),
@@ -41,7 +42,7 @@ class Report(C.Structure):
                     kernel_launches=self.kernel_launches, apply_ms=list(self.apply_ms),
                     apply_flops=list(self.apply_flops), spectral_ms=list(self.spectral_ms),
                     fmm_levels=list(self.fmm_levels), fmm_max_near=list(self.fmm_max_near),
-                    mean_iter=list(self.mean_iter))
+                    mean_iter=list(self.mean_iter), pair_rotations=self.pair_rotations)
 
 
 def _sig(name, args):

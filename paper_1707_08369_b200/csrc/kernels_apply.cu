@@ -149,6 +149,28 @@ __global__ void __launch_bounds__(256) householder_kernel(int64_t rows, double* 
   }
 }
 
+__global__ void col_rotate_kernel(int64_t rows, double* __restrict__ U, int64_t ld,
+                                  const int32_t* __restrict__ goff, const int32_t* __restrict__ cols,
+                                  const double* __restrict__ mats) {
+  const int g = blockIdx.y;
+  const int o0 = goff[g], k = goff[g + 1] - o0;
+  int64_t moff = 0;  // groups' matrices are stored back to back
+  for (int h = 0; h < g; ++h) {
+    const int kh = goff[h + 1] - goff[h];
+    moff += int64_t(kh) * kh;
+  }
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows || k > 8) return;
+  double v[8], o[8];
+  for (int a = 0; a < k; ++a) v[a] = U[r * ld + cols[o0 + a]];
+  for (int b = 0; b < k; ++b) {
+    double acc = 0.0;
+    for (int a = 0; a < k; ++a) acc = fma(v[a], mats[moff + a * k + b], acc);
+    o[b] = acc;
+  }
+  for (int b = 0; b < k; ++b) U[r * ld + cols[o0 + b]] = o[b];
+}
+
 __global__ void passthrough_kernel(int64_t rows, int nq, const double* __restrict__ U_in,
                                    int64_t ld_in, const int32_t* __restrict__ src,
                                    double* __restrict__ U_out, int64_t ld_out,
@@ -409,6 +431,16 @@ svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,
   if (rows <= 0 || ngroups <= 0) return SVD1_OK;
   dim3 grid(unsigned((rows + 31) / 32), unsigned(ngroups));
   householder_kernel<<<grid, 256, 0, st>>>(rows, U, ld, goff, cols, hv);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status col_rotate(int64_t rows, double* U, int64_t ld, int ngroups, const int32_t* goff,
+                       const int32_t* cols, const double* mats, cudaStream_t st, int64_t* launches) {
+  if (rows <= 0 || ngroups <= 0) return SVD1_OK;
+  dim3 grid(unsigned((rows + 255) / 256), unsigned(ngroups));
+  col_rotate_kernel<<<grid, 256, 0, st>>>(rows, U, ld, goff, cols, mats);
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;

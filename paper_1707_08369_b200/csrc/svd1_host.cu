@@ -174,6 +174,9 @@ struct svd1_plan_s {
   cudaEvent_t arena_ev = nullptr;
   bool arena_pending = false;
   CauchyPrep standalone;    // plan of the standalone svd1_cauchy_apply
+  std::vector<int32_t> rot_goff, rot_cols;  // pairing rotations of repeated sigma clusters
+  std::vector<double> rot_mats;
+  DevBuf d_rot_goff, d_rot_cols, d_rot_mats;
   cudaEvent_t ev[18] = {};  // timing events (spectral / apply phases)
 };
 
@@ -1200,6 +1203,99 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
       ++R.sign_flips;
     }
   }
+  // Exactly (or numerically) repeated final singular values: the U- and V-side bases
+  // of that singular subspace are computed independently, so the sign rule is
+  // generalised to a k x k pairing rotation (DESIGN.md §3.2 D5): with probes,
+  // q_c = M^T p_c for M = U_c^T A_hat V_c = sigma W, so M^T = Q P^T (P P^T)^-1 from the
+  // 4 probes, W = orthonormalised M / sigma, and V_c <- V_c W^T after the last apply.
+  P->rot_goff.assign(1, 0);
+  P->rot_cols.clear();
+  P->rot_mats.clear();
+  {
+    const double dmax = std::max(Du[m - 1], 0.0);
+    const double tolc = 64.0 * kEps * dmax;
+    int64_t i0 = 0;
+    while (i0 < m) {
+      int64_t i1 = i0 + 1;
+      while (i1 < m && Du[m - 1 - (i1 - 1)] - Du[m - 1 - i1] <= tolc) ++i1;
+      const int k = int(i1 - i0);
+      if (k >= 2 && k <= kNumProbes && Du[m - 1 - i0] > 0.0) {
+        // P (k x K), Q (k x K)
+        double Pm[kNumProbes][kNumProbes], Qm[kNumProbes][kNumProbes];
+        for (int a = 0; a < k; ++a)
+          for (int q = 0; q < kNumProbes; ++q) {
+            Pm[a][q] = cu[q][m - 1 - (i0 + a)];
+            Qm[a][q] = cv[q][n - 1 - (i0 + a)];
+          }
+        double G[kNumProbes][2 * kNumProbes], H[kNumProbes][kNumProbes];
+        for (int a = 0; a < k; ++a)
+          for (int b = 0; b < k; ++b) {
+            double g = 0.0, h = 0.0;
+            for (int q = 0; q < kNumProbes; ++q) {
+              g += Pm[a][q] * Pm[b][q];
+              h += Qm[a][q] * Pm[b][q];
+            }
+            G[a][b] = g;
+            G[a][k + b] = (a == b) ? 1.0 : 0.0;
+            H[a][b] = h;
+          }
+        // G^-1 by Gauss-Jordan with partial pivoting (k <= 4)
+        bool ok = true;
+        for (int c2 = 0; c2 < k && ok; ++c2) {
+          int piv = c2;
+          for (int r2 = c2 + 1; r2 < k; ++r2)
+            if (std::fabs(G[r2][c2]) > std::fabs(G[piv][c2])) piv = r2;
+          if (G[piv][c2] == 0.0) {
+            ok = false;
+            break;
+          }
+          if (piv != c2)
+            for (int t = 0; t < 2 * k; ++t) std::swap(G[piv][t], G[c2][t]);
+          const double inv = 1.0 / G[c2][c2];
+          for (int t = 0; t < 2 * k; ++t) G[c2][t] *= inv;
+          for (int r2 = 0; r2 < k; ++r2)
+            if (r2 != c2) {
+              const double f = G[r2][c2];
+              for (int t = 0; t < 2 * k; ++t) G[r2][t] -= f * G[c2][t];
+            }
+        }
+        if (ok) {
+          // M^T = H G^-1 ;  W = M / sigma  -> columns of W: W[:, b] = (M^T)[b, :]
+          double W[kNumProbes][kNumProbes];
+          const double sig_c = std::sqrt(Du[m - 1 - i0]);
+          for (int a = 0; a < k; ++a)
+            for (int b = 0; b < k; ++b) {
+              double mt = 0.0;  // (M^T)[a][b]
+              for (int t = 0; t < k; ++t) mt += H[a][t] * G[t][k + b];
+              W[b][a] = mt / sig_c;  // M[b][a]
+            }
+          // modified Gram-Schmidt on the columns of W (W ~ orthogonal)
+          for (int b = 0; b < k; ++b) {
+            for (int b2 = 0; b2 < b; ++b2) {
+              double dot = 0.0;
+              for (int a = 0; a < k; ++a) dot += W[a][b] * W[a][b2];
+              for (int a = 0; a < k; ++a) W[a][b] -= dot * W[a][b2];
+            }
+            double nr = 0.0;
+            for (int a = 0; a < k; ++a) nr += W[a][b] * W[a][b];
+            nr = std::sqrt(nr);
+            for (int a = 0; a < k; ++a) W[a][b] /= nr;
+          }
+          // V_c <- V_c W^T : new col b = sum_a old col a * W[b][a]; stored row-major
+          // as R[a][b] = W[b][a] (the kernel computes out[b] = sum_a in[a] R[a][b])
+          for (int a = 0; a < k; ++a) {
+            P->rot_cols.push_back(int32_t(i0 + a));
+            sgn[i0 + a] = 1.0;  // the rotation carries the sign
+          }
+          for (int a = 0; a < k; ++a)
+            for (int b = 0; b < k; ++b) P->rot_mats.push_back(W[b][a]);
+          P->rot_goff.push_back(int32_t(P->rot_cols.size()));
+          ++R.pair_rotations;
+        }
+      }
+      i0 = i1;
+    }
+  }
   for (int j = 0; j < S[3].na; ++j) {
     const int64_t col = n - 1 - S[3].tgt_pos[j];
     if (col < m) S[3].cs_h[j] *= sgn[col];
@@ -1208,6 +1304,8 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     const int64_t col = n - 1 - S[3].pass_dst[q];
     if (col < m) S[3].pass_scale[q] *= sgn[col];
   }
+  R.sign_flips = 0;
+  for (int64_t i = 0; i < m; ++i) R.sign_flips += sgn[i] < 0.0;
   // ---- STEP 8: sigma = sqrt(max(D, 0)), descending
   std::vector<double> sig_new(m);
   for (int64_t i = 0; i < m; ++i) {
@@ -1252,9 +1350,21 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
       TRY(ensure_expansions(P, side, cauchy_exp_elems(S[e].cp)));
     }
   }
+  const int nrot = int(P->rot_goff.size()) - 1;
+  if (nrot > 0 && c.v_rows > 0) {
+    int32_t *g, *cl;
+    double* mt;
+    TRY(upload(P, P->d_rot_goff, P->rot_goff, &g));
+    TRY(upload(P, P->d_rot_cols, P->rot_cols, &cl));
+    TRY(upload(P, P->d_rot_mats, P->rot_mats, &mt));
+  }
   TRY(stream_wait(P, 1, P->st, P->st2));  // uploads of the V-side second apply
   TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
   TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, P->st2, 1));
+  if (nrot > 0 && c.v_rows > 0)
+    TRY(col_rotate(c.v_rows, V, ldv, nrot, static_cast<int32_t*>(P->d_rot_goff.p),
+                   static_cast<int32_t*>(P->d_rot_cols.p), static_cast<double*>(P->d_rot_mats.p),
+                   P->st2, &P->launches));
   TRY(stream_wait(P, 2, P->st2, P->st));  // join
   TRY(ev_record(P, 17, P->st));           // apply phase end
   R.t_ms[2] = now_ms() - t4;

@@ -173,3 +173,20 @@ def test_update_stream_c3_small():
         At = T(A)
         res = float(torch.linalg.norm(At @ Vg - Ug * sg[None, :], dim=0).max() / sg[0])
         assert res <= 1e-10
+
+
+@pytest.mark.parametrize("n,flags", [(24, 0), (600, P.FORCE_FMM)])
+def test_repeated_sigma_pairing(n, flags):
+    """Multiplicity-4 singular value -> multiplicity 2 after the update: the GPU's
+    probe-based k x k pairing rotation (D5) gives a paired SVD (residual), and the
+    cluster's subspaces match the oracle's."""
+    rng = np.random.default_rng(n)
+    s = np.sort(rng.uniform(1, 10, n))[::-1].copy()
+    s[5:9] = s[5]
+    U = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    V = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    a, b = rng.standard_normal(n), rng.standard_normal(n)
+    r = _check_update(U, s, V, a, b, flags=flags)
+    assert r["rep"]["pair_rotations"] >= 1
+    assert r["res"] <= 1e-10 and r["orth"] <= 1e-10, r
+    assert r["U"]["cluster"] <= 1e-9 and r["V"]["cluster"] <= 1e-9, r

@@ -383,3 +383,26 @@ def test_large_mode_rows_match_full():
     assert np.max(np.abs(r2["sigma"] - r1["sigma"])) <= 1e-14 * r1["sigma"][0]
     assert np.max(np.abs(r2["U"] - r1["U"][ru])) <= 1e-12
     assert np.max(np.abs(r2["V"][:, :m] - r1["V"][rv][:, :m])) <= 1e-12
+
+
+@pytest.mark.parametrize("rule", ["explicit", "probe"])
+def test_repeated_singular_values_are_paired(rule):
+    """A singular value of multiplicity 4 in A keeps multiplicity 2 after the two
+    symmetric rank-1 updates of each side; the U and V bases of that subspace come
+    out independently, so a sign flip cannot pair them (D5): the k x k pairing
+    rotation must, or the residual is O(sigma).  Checked against the residual and a
+    brute-force Jacobi SVD."""
+    rng = np.random.default_rng(8)
+    m = n = 24
+    s = np.sort(rng.uniform(1, 10, n))[::-1].copy()
+    s[5:9] = s[5]  # multiplicity 4
+    U = np.linalg.qr(rng.standard_normal((m, m)))[0]
+    V = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    a, b = rng.standard_normal(m), rng.standard_normal(n)
+    r = O.svd_update(U, s, V, a, b, sign_rule=rule)
+    A_hat = (U * s) @ V.T + np.outer(a, b)
+    assert r["info"]["rotations"] >= 1
+    assert O.column_residual(A_hat, r["U"], r["sigma"], r["V"]) <= 1e-13
+    assert O.orth_defect(r["V"]) <= 1e-13
+    _, sj, _ = jacobi_svd(A_hat)
+    assert sigma_errors(r["sigma"], sj)["gram"] <= 1e-13
