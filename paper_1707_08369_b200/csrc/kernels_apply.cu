@@ -250,6 +250,22 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
           v = lagrange(t, w, p, i, ((d[k[jt]] - Y.c) + tau[jt]) / Y.r) * cs[jt];
           break;
         }
+        case OP_ID: {
+          v = (i == j) ? 1.0 : 0.0;
+          break;
+        }
+        case OP_L2P_FROM: {  // Psi of cell a (an ancestor) at the targets of leaf b
+          const FmmCell A = cells[D.a], Y = cells[D.b];
+          const int jt = Y.tlo + j;
+          v = lagrange(t, w, p, i, ((d[k[jt]] - A.c) + tau[jt]) / A.r) * cs[jt];
+          break;
+        }
+        case OP_P2L: {  // sources of X (a) -> local expansion of Y (b) at y_j = c_Y + r_Y t_j
+          const FmmCell X = cells[D.a], Y = cells[D.b];
+          const int s = X.slo + i;
+          v = zhat[s] / ((d[s] - Y.c) - Y.r * t[j]);
+          break;
+        }
         default: {  // OP_P2P: source leaf X (a), target leaf Y (b)
           const FmmCell X = cells[D.a], Y = cells[D.b];
           const int s = X.slo + i, jt = Y.tlo + j;
@@ -277,125 +293,143 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   const int n = valid ? 8 : 0;  // src-size 0 -> zero fill
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int WN = BN / 16;      // warps along N
-  static constexpr int WM = 8 / WN;       // warps along M
-  static constexpr int BM = 32 * WM;      // rows per CTA
+  // every warp owns 32 rows x BN columns (4 x BN/8 DMMA m8n8k4 fragments)
+  static constexpr int NWARP = BN <= 16 ? 8 : 4;
+  static constexpr int NTHR = 32 * NWARP;
+  static constexpr int NT = BN / 8;
+  static constexpr int BM = 32 * NWARP;   // rows per CTA
   static constexpr int BLD = BN + 4;      // B row stride (doubles)
+  static constexpr int STAGES = 2;        // cp.async pipeline depth
   static constexpr int A_ELEMS = BM * ALD;
   static constexpr int B_ELEMS = KC * BLD;
-  static constexpr int SMEM = 2 * (A_ELEMS + B_ELEMS) * 8;
+  static constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * 8;
 };
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int BN>
-__global__ void __launch_bounds__(256) fmm_gemm_kernel(
+__global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
     const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int64_t rows,
     const double* __restrict__ ops, const double* __restrict__ U_in, int64_t ld_in,
     const int32_t* __restrict__ src, double* __restrict__ U_out, int64_t ld_out,
     const int32_t* __restrict__ dst, double* __restrict__ phi, double* __restrict__ psi, int64_t ldE) {
   using G = GemmCfg<BN>;
+  constexpr int NT = G::NT;
   extern __shared__ __align__(16) double smem[];
-  double* As = smem;                        // [2][BM][ALD]
-  double* Bs = smem + 2 * G::A_ELEMS;       // [2][KC][BLD]
+  double* As = smem;                            // [STAGES][BM][ALD]
+  double* Bs = smem + G::STAGES * G::A_ELEMS;   // [STAGES][KC][BLD]
   const FmmTask T = tasks[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % G::WM, wn = warp / G::WM;
   const int64_t row0 = int64_t(blockIdx.y) * G::BM;
   const int nrow = int(rows - row0 < G::BM ? rows - row0 : G::BM);
 
-  // stage iterator over (term, K-chunk)
-  int ti = T.t_begin, k0 = 0;
   auto load_stage = [&](int buf, int term, int kk0) {
     const FmmTerm R = terms[term];
     double* a = As + buf * G::A_ELEMS;
     double* b = Bs + buf * G::B_ELEMS;
     const double* base = R.in_kind == IO_U ? U_in : (R.in_kind == IO_PHI ? phi : psi);
     const int64_t ld = R.in_kind == IO_U ? ld_in : ldE;
-#pragma unroll 4
-    // 256 % KC == 0: every thread loads one fixed column kk of the chunk for
-    // rows rr0, rr0 + 256/KC, ... so the column map is read once per stage.
+    // Every thread owns one fixed column pair (kp, kp+1) of the chunk for rows rr0,
+    // rr0 + 2*NTHR/KC, ...: the column map is read once per stage, and a pair of
+    // adjacent, 16-byte aligned source columns moves as one 16-byte cp.async.
     {
-      const int kk = tid % KC, rr0 = tid / KC;
-      const int k = kk0 + kk;
-      const bool kok = k < R.K;
-      int col = R.col0 + (kok ? k : 0);
-      if (R.in_kind == IO_U && src) col = src[col];
-      const double* colp = base + row0 * ld + col;
+      const int kp = (tid % (KC / 2)) * 2, rr0 = tid / (KC / 2);
+      const int k = kk0 + kp;
+      const bool ok0 = k < R.K, ok1 = k + 1 < R.K;
+      int c0 = R.col0 + (ok0 ? k : 0), c1 = R.col0 + (ok1 ? k + 1 : 0);
+      if (R.in_kind == IO_U && src) {
+        c0 = src[c0];
+        c1 = src[c1];
+      }
+      const bool vec = ok1 && c1 == c0 + 1 && !(c0 & 1) && !(ld & 1);
+      const double* p0 = base + row0 * ld + c0;
+      const double* p1 = base + row0 * ld + c1;
 #pragma unroll 4
-      for (int rr = rr0; rr < G::BM; rr += 256 / KC) {
-        const bool ok = kok && rr < nrow;
-        cp_async8(a + rr * ALD + kk, colp + (ok ? int64_t(rr) * ld : 0), ok);
+      for (int rr = rr0; rr < G::BM; rr += 2 * G::NTHR / KC) {
+        const bool rok = rr < nrow;
+        const int64_t ro = rok ? int64_t(rr) * ld : 0;
+        if (vec) {
+          cp_async16(a + rr * ALD + kp, p0 + ro, rok);
+        } else {
+          cp_async8(a + rr * ALD + kp, p0 + (ok0 ? ro : 0), ok0 && rok);
+          cp_async8(a + rr * ALD + kp + 1, p1 + (ok1 ? ro : 0), ok1 && rok);
+        }
       }
     }
-    for (int e = tid; e < KC * BN; e += 256) {
+    for (int e = tid; e < KC * BN; e += G::NTHR) {
       const int kk = e / BN, jj = e % BN;
       const int k = kk0 + kk;
       const bool ok = k < R.K && jj < T.N;
       cp_async8(b + kk * G::BLD + jj, ops + R.op_off + (ok ? int64_t(k) * R.op_ld + T.op_col0 + jj : 0), ok);
     }
   };
-  double acc[4][2][2];
+  double acc[4][NT][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  if (ti < T.t_end) {
-    load_stage(0, ti, 0);
+  // stage list = (term, K-chunk) pairs; a STAGES-deep cp.async ring
+  int nst = 0;
+  for (int t = T.t_begin; t < T.t_end; ++t) nst += (terms[t].K + KC - 1) / KC;
+  int lti = T.t_begin, lk0 = 0;
+  auto load_next = [&](int buf) {
+    load_stage(buf, lti, lk0);
+    lk0 += KC;
+    if (lk0 >= terms[lti].K) {
+      ++lti;
+      lk0 = 0;
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < G::STAGES - 1; ++q) {
+    if (q < nst) load_next(q);
     cp_async_commit();
   }
-  int buf = 0;
-  while (ti < T.t_end) {
-    // next stage
-    int nti = ti, nk0 = k0 + KC;
-    if (nk0 >= terms[ti].K) {
-      ++nti;
-      nk0 = 0;
-    }
-    const bool more = nti < T.t_end;
-    if (more) {
-      load_stage(buf ^ 1, nti, nk0);
-      cp_async_commit();
-      cp_async_wait1();
-    } else {
-      cp_async_wait0();
-    }
+  for (int it = 0; it < nst; ++it) {
+    const int buf = it % G::STAGES;
+    if (it + G::STAGES - 1 < nst) load_next((it + G::STAGES - 1) % G::STAGES);
+    cp_async_commit();
+    cp_async_wait<G::STAGES - 1>();
     __syncthreads();
     const double* a = As + buf * G::A_ELEMS;
     const double* b = Bs + buf * G::B_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
-      double af[4], bf[2];
+      double af[4], bf[NT];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = a[(wm * 32 + mt * 8 + (lane >> 2)) * ALD + kk + (lane & 3)];
+      for (int mt = 0; mt < 4; ++mt) af[mt] = a[(warp * 32 + mt * 8 + (lane >> 2)) * ALD + kk + (lane & 3)];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) bf[nt] = b[(kk + (lane & 3)) * G::BLD + wn * 16 + nt * 8 + (lane >> 2)];
+      for (int nt = 0; nt < NT; ++nt) bf[nt] = b[(kk + (lane & 3)) * G::BLD + nt * 8 + (lane >> 2)];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
     }
-    __syncthreads();  // buffer `buf` is refilled by the next iteration's prefetch
-    ti = nti;
-    k0 = nk0;
-    buf ^= 1;
+    __syncthreads();  // buffer `buf` is refilled by a later prefetch
   }
   // epilogue
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
-    const int rr = wm * 32 + mt * 8 + (lane >> 2);
+    const int rr = warp * 32 + mt * 8 + (lane >> 2);
     if (rr >= nrow) continue;
     const int64_t r = row0 + rr;
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
+    for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int jj = wn * 16 + nt * 8 + (lane & 3) * 2 + h;
+        const int jj = nt * 8 + (lane & 3) * 2 + h;
         if (jj >= T.N) continue;
         const int col = T.col0 + jj;
         if (T.out_kind == IO_U) {
@@ -482,7 +516,7 @@ svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms,
     attr = true;
   }
   dim3 grid(unsigned(n_tasks), unsigned((rows + G::BM - 1) / G::BM));
-  fmm_gemm_kernel<BN><<<grid, 256, G::SMEM, st>>>(tasks, terms, rows, ops, U_in, ld_in, src, U_out,
+  fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(tasks, terms, rows, ops, U_in, ld_in, src, U_out,
                                                   ld_out, dst, phi, psi, ldE);
   return SVD1_OK;
 }

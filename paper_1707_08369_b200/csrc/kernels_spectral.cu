@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(256) proj_partial_kernel(const double* __restr
                                                           int64_t rows, int64_t cols,
                                                           const double* __restrict__ x,
                                                           int64_t row0, int rows_per_chunk,
-                                                          uint64_t seed, double* __restrict__ part) {
+                                                          const double* __restrict__ probes,
+                                                          double* __restrict__ part) {
   __shared__ double vec[NV][64];
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t r_begin = int64_t(blockIdx.y) * rows_per_chunk;
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(256) proj_partial_kernel(const double* __restr
     __syncthreads();
     for (int t = threadIdx.x; t < nr * NV; t += blockDim.x) {
       const int rr = t % nr, v = t / nr;
-      vec[v][rr] = (v == 0) ? x[row0 + rb + rr] : probe_value(seed, v - 1, row0 + rb + rr);
+      vec[v][rr] = (v == 0) ? x[row0 + rb + rr] : probes[(v - 1) * rows + rb + rr];
     }
     __syncthreads();
     if (c < cols) {
@@ -107,20 +108,32 @@ __global__ void proj_reduce_kernel(const double* __restrict__ part, int nchunks,
   out[t] = s;
 }
 
+// probes g_k(row) for this process's rows, row-major [4][u_rows] (computed once per plan)
+__global__ void probe_fill_kernel(uint64_t seed, int64_t row0, int64_t rows, double* __restrict__ g) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= 4 * rows) return;
+  const int kq = int(t / rows);
+  const int64_t r = t % rows;
+  g[t] = probe_value(seed, kq, row0 + r);
+}
+
 // scalars: out[0..3] = a_loc . g_k,loc ; out[4] = a_loc . a_loc ; out[5] = b_loc . b_loc
+// block partials [gridDim.x][6], then proj_dots_final sums them in block order.
 __global__ void __launch_bounds__(256) proj_dots_kernel(const double* __restrict__ a, int64_t u_rows,
                                                        int64_t u_row0, const double* __restrict__ b,
-                                                       int64_t v_rows, int64_t v_row0, uint64_t seed,
-                                                       double* __restrict__ out) {
+                                                       int64_t v_rows, int64_t v_row0,
+                                                       const double* __restrict__ probes,
+                                                       double* __restrict__ part) {
   __shared__ double red[6][8];
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t r = threadIdx.x; r < u_rows; r += blockDim.x) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < u_rows; r += stride) {
     const double av = a[u_row0 + r];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = fma(av, probe_value(seed, q, u_row0 + r), acc[q]);
+    for (int q = 0; q < 4; ++q) acc[q] = fma(av, probes[q * u_rows + r], acc[q]);
     acc[4] = fma(av, av, acc[4]);
   }
-  for (int64_t r = threadIdx.x; r < v_rows; r += blockDim.x) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < v_rows; r += stride) {
     const double bv = b[v_row0 + r];
     acc[5] = fma(bv, bv, acc[5]);
   }
@@ -134,6 +147,14 @@ __global__ void __launch_bounds__(256) proj_dots_kernel(const double* __restrict
   if (threadIdx.x < 6) {
     double s = 0.0;
     for (int i = 0; i < 8; ++i) s += red[threadIdx.x][i];
+    part[blockIdx.x * 6 + threadIdx.x] = s;
+  }
+}
+
+__global__ void proj_dots_final(const double* __restrict__ part, int nblocks, double* __restrict__ out) {
+  if (threadIdx.x < 6) {
+    double s = 0.0;
+    for (int i = 0; i < nblocks; ++i) s += part[i * 6 + threadIdx.x];
     out[threadIdx.x] = s;
   }
 }
@@ -453,25 +474,36 @@ inline unsigned blocks_for_warps(int64_t nwarps, int threads = 256) {
 }  // namespace
 
 // ------------------------------------------------------------------ wrappers
+constexpr int kDotBlocks = 64;
+
 int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t n) {
   const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
   const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
-  return cu * 5 * m + cv * n;
+  return cu * 5 * m + cv * n + 6 * kDotBlocks;
+}
+
+svd1_status fill_probes(uint64_t seed, int64_t row0, int64_t rows, double* g, cudaStream_t st,
+                        int64_t* launches) {
+  if (rows <= 0) return SVD1_OK;
+  probe_fill_kernel<<<unsigned((4 * rows + 255) / 256), 256, 0, st>>>(seed, row0, rows, g);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
 }
 
 svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
                     const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0,
                     const double* a, const double* b, double* part, int64_t partial_cap,
-                    double* proj, uint64_t seed, cudaStream_t st, int64_t* launches) {
+                    double* proj, const double* probes, cudaStream_t st, int64_t* launches) {
   const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
   const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
-  if (cu * 5 * m + cv * n > partial_cap) return SVD1_E_NOMEM;
+  if (cu * 5 * m + cv * n + 6 * kDotBlocks > partial_cap) return SVD1_E_NOMEM;
   const int rpc_u = int((u_rows + cu - 1) / cu), rpc_v = int((v_rows + cv - 1) / cv);
   double* part_u = part;
   double* part_v = part + cu * 5 * m;
   if (u_rows > 0) {
     proj_partial_kernel<5><<<dim3(unsigned((m + 255) / 256), unsigned(cu)), 256, 0, st>>>(
-        U, ldu, u_rows, m, a, u_row0, rpc_u, seed, part_u);
+        U, ldu, u_rows, m, a, u_row0, rpc_u, probes, part_u);
     proj_reduce_kernel<<<unsigned((5 * m + 255) / 256), 256, 0, st>>>(part_u, int(cu), 5, m, proj);
     *launches += 2;
   } else {
@@ -479,14 +511,16 @@ svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int
   }
   if (v_rows > 0) {
     proj_partial_kernel<1><<<dim3(unsigned((n + 255) / 256), unsigned(cv)), 256, 0, st>>>(
-        V, ldv, v_rows, n, b, v_row0, rpc_v, seed, part_v);
+        V, ldv, v_rows, n, b, v_row0, rpc_v, nullptr, part_v);
     proj_reduce_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(part_v, int(cv), 1, n, proj + 5 * m);
     *launches += 2;
   } else {
     SVD1_CUDA_TRY(cudaMemsetAsync(proj + 5 * m, 0, sizeof(double) * n, st));
   }
-  proj_dots_kernel<<<1, 256, 0, st>>>(a, u_rows, u_row0, b, v_rows, v_row0, seed, proj + 5 * m + n);
-  *launches += 1;
+  double* part_d = part + cu * 5 * m + cv * n;
+  proj_dots_kernel<<<kDotBlocks, 256, 0, st>>>(a, u_rows, u_row0, b, v_rows, v_row0, probes, part_d);
+  proj_dots_final<<<1, 32, 0, st>>>(part_d, kDotBlocks, proj + 5 * m + n);
+  *launches += 2;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

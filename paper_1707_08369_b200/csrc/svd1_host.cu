@@ -162,6 +162,8 @@ struct svd1_plan_s {
   DevBuf W_u, W_v, proj, partial, status, iters, ops, fmm_cells, fmm_descs, fmm_terms,
       fmm_tasks, scratch_i, scratch_d;
   DevBuf phi[2], psi[2];         // FMM expansions per side (U applies, V applies)
+  DevBuf probes;                 // 4 x u_rows sign probes
+  bool probes_ready = false;
   cudaStream_t st2 = nullptr;    // V-side applies run here, concurrently with the U side
   cudaEvent_t sync_ev[4] = {};
   StepRecord steps[4];
@@ -499,34 +501,63 @@ void fmm_lists(FmmHost& F, int p) {
         end_task(IO_PHI, c * p, p);
       }
     }
-    // downward: L2L + M2L (STEP 8), levels 1 .. L (M2L re-derived)
-    for (int l = 1; l <= L; ++l) {
+    // downward (STEP 8; M2L re-derived), restructured:
+    // (a) one pass with the M2L (and P2L) contributions of EVERY cell, all levels at
+    //     once (no dependence between them: long coarse-level K chains run beside
+    //     the many short fine-level tasks);
+    // (b) the L2L chain for levels 2..L-1, accumulating in place
+    //     Psi_Y <- Psi_Y * I + Psi_parent * S_Y;
+    // (c) leaves take L2L from their parent folded into the final pass (evaluating
+    //     the parent's local polynomial at the targets is exactly L2L then L2P).
+    F.pass_begin.push_back(int(F.tasks.size()));
+    F.pass_bn.push_back(p);
+    for (int y = 1; y < F.ncells; ++y) {
+      if (m2l[y].empty() || !has_tgt(y)) continue;
+      begin_task();
+      // partners with fewer than p sources are cheaper as P2L (K = #sources < p)
+      std::vector<int> via_phi, via_src;
+      for (int x : m2l[y]) (F.cells[x].shi - F.cells[x].slo >= p ? via_phi : via_src).push_back(x);
+      add_runs(via_phi, IO_PHI, OP_M2L, y, p);
+      add_runs(via_src, IO_U, OP_P2L, y, p);
+      F.n_m2l_pairs += int(m2l[y].size());
+      end_task(IO_PSI, y * p, p);
+    }
+    for (int l = 2; l <= L - 1; ++l) {
       F.pass_begin.push_back(int(F.tasks.size()));
       F.pass_bn.push_back(p);
       for (int i = 0; i < (1 << l); ++i) {
-        const int y = (1 << l) - 1 + i;
-        if (!has_psi[y]) continue;
+        const int y = (1 << l) - 1 + i, par = (y - 1) / 2;
+        if (!has_psi[y] || !has_psi[par]) continue;
         begin_task();
-        const int par = (y - 1) / 2;
-        if (l >= 2 && has_psi[par]) add_term(IO_PSI, par * p, p, add_op(OP_L2L, par, y, p, p), p);
-        add_runs(m2l[y], IO_PHI, OP_M2L, y, p);
-        F.n_m2l_pairs += int(m2l[y].size());
+        if (!m2l[y].empty()) add_term(IO_PSI, y * p, p, add_op(OP_ID, y, y, p, p), p);
+        add_term(IO_PSI, par * p, p, add_op(OP_L2L, par, y, p, p), p);
         end_task(IO_PSI, y * p, p);
       }
     }
   }
   // final: L2P (STEP 9) + P2P near field (STEP 10); two launches by
   // output width (leaves with <= 16 targets use the 16-wide tile)
+  int n_narrow = 0, n_wide = 0;
+  for (int i = 0; i < nleaf; ++i) {
+    const int y = lf0 + i;
+    if (!has_tgt(y)) continue;
+    (F.cells[y].thi - F.cells[y].tlo > 16 ? n_wide : n_narrow)++;
+  }
+  // a separate 16-wide launch only pays when it carries a real share of the leaves
+  const bool split_narrow = n_narrow >= 16 || n_wide == 0;
   for (int wide = 0; wide < 2; ++wide) {
+  if (!split_narrow && wide == 0) continue;
   F.pass_begin.push_back(int(F.tasks.size()));
   F.pass_bn.push_back(wide ? 32 : 16);
   for (int i = 0; i < nleaf; ++i) {
     const int y = lf0 + i;
     if (!has_tgt(y)) continue;
     const int ty = F.cells[y].thi - F.cells[y].tlo;
-    if ((ty > 16) != (wide == 1)) continue;
+    if (split_narrow && (ty > 16) != (wide == 1)) continue;
     begin_task();
-    if (has_psi[y]) add_term(IO_PSI, y * p, p, add_op(OP_L2P, y, y, p, ty), ty);
+    const int par = (y - 1) / 2;
+    if (!m2l[y].empty()) add_term(IO_PSI, y * p, p, add_op(OP_L2P, y, y, p, ty), ty);
+    if (L >= 2 && has_psi[par]) add_term(IO_PSI, par * p, p, add_op(OP_L2P_FROM, par, y, p, ty), ty);
     add_runs(near[y], IO_U, OP_P2P, y, ty);
     F.n_near_pairs += int(near[y].size());
     F.max_near = std::max<int>(F.max_near, int(near[y].size()));
@@ -1077,8 +1108,14 @@ svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const doub
   double* part;
   const int64_t need = project_partial_elems(c.u_rows, c.m, c.v_rows, c.n);
   TRY(P->partial.get<double>(size_t(need), &part));
+  if (!P->probes_ready) {  // the probes depend only on (seed, global row): once per plan
+    double* g;
+    TRY(P->probes.get<double>(size_t(4 * std::max<int64_t>(c.u_rows, 1)), &g));
+    TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, g, P->st, &P->launches));
+    P->probes_ready = true;
+  }
   return project(U, ldu, c.u_rows, c.m, c.u_row0, V, ldv, c.v_rows, c.n, c.v_row0, a, b, part, need,
-                 proj, P->probe_seed, P->st, &P->launches);
+                 proj, static_cast<double*>(P->probes.p), P->st, &P->launches);
 }
 
 svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,

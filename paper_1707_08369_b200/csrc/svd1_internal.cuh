@@ -37,7 +37,10 @@ __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
 svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
                     const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0,
                     const double* a, const double* b, double* partial_ws, int64_t partial_cap,
-                    double* proj, uint64_t probe_seed, cudaStream_t st, int64_t* launches);
+                    double* proj, const double* probes, cudaStream_t st, int64_t* launches);
+// probes g_k(row0 + r), k < 4, r < rows, into g[k * rows + r] (splitmix64 + Box-Muller)
+svd1_status fill_probes(uint64_t seed, int64_t row0, int64_t rows, double* g, cudaStream_t st,
+                        int64_t* launches);
 int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t n);
 
 // K2: secular roots (warp per root).  status bit 1 = no convergence, 2 = pole.
@@ -91,7 +94,12 @@ struct FmmCell {      // one tree cell: a contiguous range [lo, hi) of the merge
   int32_t slo, shi;   // its sources  d_slo .. d_{shi-1}
   int32_t tlo, thi;   // its targets mu_tlo .. mu_{thi-1}
 };
-enum FmmOpKind : int32_t { OP_P2M = 0, OP_M2M = 1, OP_M2L = 2, OP_L2L = 3, OP_L2P = 4, OP_P2P = 5 };
+enum FmmOpKind : int32_t {
+  OP_P2M = 0, OP_M2M = 1, OP_M2L = 2, OP_L2L = 3, OP_L2P = 4, OP_P2P = 5,
+  OP_P2L = 6,       // sources of a cell with fewer than p points straight into a local expansion
+  OP_ID = 7,        // p x p identity (in-place accumulation of the L2L chain)
+  OP_L2P_FROM = 8   // local expansion of cell a evaluated at the targets of leaf b
+};
 struct FmmOpDesc {    // one operator matrix to build: rows x cols, row-major at ops + off
   int32_t kind, a, b; // cells (a = source side, b = target side; see kernel)
   int32_t rows, cols;
