@@ -31,8 +31,16 @@ import numpy as np  # noqa: E402
 METRIC = "rank-1 SVD updates/s (fp64, n=4096) and FMM Cauchy-apply % of FP64 roofline"
 UNIT = "updates/s"
 CFG_ID = 3
-WORKLOAD = ("C3: m=n=4096 fp64, A = Q1 diag(sigma) Q2^T, sigma_i = 10^(-6 i/n) (graded), "
-            "16-update stream a,b ~ N(0,1), eps=1e-10 (p=16)")
+WORKLOADS = {
+    1: "C1: m=n=64 fp64, A i.i.d. N(0,1), U,S,V from an SVD of A, update a,b ~ N(0,1) (repeated)",
+    2: "C2: m=n=1024 fp64, A i.i.d. N(0,1), update a,b ~ N(0,1)/sqrt(n) (repeated)",
+    3: ("C3: m=n=4096 fp64, A = Q1 diag(sigma) Q2^T, sigma_i = 10^(-6 i/n) (graded), "
+        "16-update stream a,b ~ N(0,1), eps=1e-10 (p=16)"),
+    4: "C4: m=2048, n=8192 fp64, A i.i.d. N(0,1), 64-update stream a,b ~ N(0,1)*1e-2",
+    5: ("C5: m=n=16384 fp64, A = Q1 diag(sigma) Q2^T, sigma ~ U[1,100] with 5% bitwise "
+        "duplicates, 8-update stream a,b ~ N(0,1)"),
+}
+WORKLOAD = WORKLOADS[3]
 FP64_PEAK_TFLOPS = 37.17  # measured DMMA m8n8k4 sustained on this pool's B200 (profiles/fp64_peak_r01.jsonl)
 HBM_PEAK_GBS = 6553.0
 
@@ -142,7 +150,13 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--config", type=int, default=CFG_ID, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default C3, the headline metric's workload)")
     args = ap.parse_args()
+    global WORKLOAD, METRIC
+    if args.config != CFG_ID:
+        WORKLOAD = WORKLOADS[args.config]
+        METRIC = f"rank-1 SVD updates/s (fp64, config C{args.config})"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -158,7 +172,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    inp = config_inputs(CFG_ID, device=dev)
+    inp = config_inputs(args.config, device=dev)
     cfg = inp["cfg"]
     m, n = cfg["m"], cfg["n"]
     ab = [(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)) for a, b in inp["ab"]]
@@ -260,21 +274,22 @@ def main():
     check = None
     if not args.no_check and world == 1:
         restore()
-        A = (U0 * s0[None, :]) @ V0.T
+        A = (U0 * s0[None, :]) @ V0[:, :m].T
         for t in range(args.steps):
             step(t)
             a_t, b_t = ab[t % len(ab)]
             A = A + torch.outer(a_t, b_t)
-        res = float(torch.linalg.norm(A @ V - U * sig[None, :], dim=0).max() / sig[0])
+        res = float(torch.linalg.norm(A @ V[:, :m] - U * sig[None, :], dim=0).max() / sig[0])
         I = torch.eye(m, dtype=torch.float64, device=dev)
-        orth = max(float((U.T @ U - I).abs().max()), float((V.T @ V - I).abs().max()))
+        In = torch.eye(n, dtype=torch.float64, device=dev)
+        orth = max(float((U.T @ U - I).abs().max()), float((V.T @ V - In).abs().max()))
         check = {"residual": res, "orthogonality": orth, "updates": args.steps,
                  "n_active_last": reps[-1]["n_active"], "max_secular_iter": max(max(r["max_iter"]) for r in reps),
                  "fmm_levels": reps[-1]["fmm_levels"], "fmm_max_near": reps[-1]["fmm_max_near"],
                  "mean_secular_evals": sum(sum(r["mean_iter"]) for r in reps) / (4 * len(reps))}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.config == CFG_ID:
         from synth import config_inputs as ci
         cin = ci(CFG_ID)
         t, nr = oracle_sample_time(cin, 1)
@@ -289,7 +304,9 @@ def main():
                 "data": "synthetic (seeded, BASELINE.json C3 recipe)",
                 "config": {"workload": WORKLOAD, "m": m, "n": n, "eps": cfg["eps"], "p": reps[-1]["p"],
                            "updates_in_stream": cfg["updates"],
-                           "l2": "inputs larger than L2 (U + V = 256 MiB > 126 MB)",
+                           "l2": (f"inputs larger than L2 (U + V = {8 * (m * m + n * n) / 2**20:.0f} MiB > 126 MB)"
+                                  if 8 * (m * m + n * n) > 126e6 else
+                                  f"inputs fit in L2 ({8 * (m * m + n * n) / 2**20:.1f} MiB); no flush"),
                            "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
                 "cpu_baseline": cpu, "check": check,
