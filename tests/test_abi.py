@@ -9,14 +9,23 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _build_module():
+    """build.py loaded by path (the package __init__ needs the built library)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_svd1_build", os.path.join(ROOT, "paper_1707_08369_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def _declared():
     src = open(os.path.join(ROOT, "include", "svd1.h")).read()
     return sorted(set(re.findall(r"\b(svd1_[a-z_]+)\s*\(", src)))
 
 
 def test_library_exports_header_symbols():
-    from paper_1707_08369_b200 import build
-    lib = build.build()
+    lib = _build_module().build()
     out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (svd1_\w+)", out))
     missing = [s for s in _declared() if s not in exported]
@@ -50,8 +59,7 @@ def test_plan_rejects_bad_config_without_gpu():
 
 def test_sass_has_fp64_tensor_ops():
     """The Cauchy-apply kernels lower to DMMA (fp64 tensor core) on sm_100a."""
-    from paper_1707_08369_b200 import build
-    lib = build.build()
+    lib = _build_module().build()
     r = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True)
     if r.returncode != 0:
         pytest.skip("cuobjdump unavailable")
