@@ -685,6 +685,25 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
             C.na, F.L, F.ncells, F.tasks.size(), F.terms.size(), (long long)F.ops_elems,
             (long long)rows, p);
   }
+  if (std::getenv("SVD1_PASSSTATS")) {  // per pass: tasks, algorithmic vs tile-padded flops
+    for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
+      const int b = F.pass_begin[s], e = F.pass_begin[s + 1], bn = F.pass_bn[s];
+      double fa = 0.0, fp = 0.0;
+      int64_t kmax = 0;
+      for (int t = b; t < e; ++t) {
+        const FmmTask& T = F.tasks[t];
+        int64_t ks = 0;
+        for (int q = T.t_begin; q < T.t_end; ++q) {
+          fa += 2.0 * F.terms[q].K * T.N;
+          fp += 2.0 * ((F.terms[q].K + 15) / 16 * 16) * bn;
+          ks += F.terms[q].K;
+        }
+        kmax = std::max(kmax, ks);
+      }
+      fprintf(stderr, "[svd1] pass %zu bn=%d tasks=%d flops=%.3e padded=%.3e (x%.2f) kmax=%lld\n", s, bn,
+              e - b, fa * rows, fp * rows, fa > 0 ? fp / fa : 0.0, (long long)kmax);
+    }
+  }
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, ops, U_in, ld_in, d_src, U_out, ld_out,

@@ -1,0 +1,25 @@
+"""Diagnostics for one C3 update (GPU): host phase timing (SVD1_TIMING) and per-pass
+FMM flops (SVD1_PASSSTATS) of the last update.  usage: python tools/diag_c3.py [cfg] [updates]"""
+import os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_1707_08369_b200 as P
+from synth import config_inputs
+
+cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+nup = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+dev = torch.device("cuda:0")
+inp = config_inputs(cfg_id, device=dev)
+c = inp["cfg"]
+U, s, V = inp["U"].clone(), inp["sigma"].clone(), inp["V"].clone()
+plan = P.Plan(c["m"], c["n"], eps=c["eps"])
+for t in range(nup):
+    if t == nup - 1:
+        os.environ["SVD1_TIMING"] = "1"
+        os.environ["SVD1_PASSSTATS"] = "1"
+        print(f"--- update {t}", file=sys.stderr, flush=True)
+    a, b = inp["ab"][t % len(inp["ab"])]
+    rep = plan.update(U, s, V, torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev))
+    torch.cuda.synchronize()
+print({k: rep[k] for k in ("t_ms", "apply_ms", "apply_flops", "spectral_ms", "fmm_levels", "n_active")})
