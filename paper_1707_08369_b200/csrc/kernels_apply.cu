@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
                                                      const double* __restrict__ tau,
                                                      const double* __restrict__ zhat,
                                                      const double* __restrict__ cs,
+                                                     const int32_t* __restrict__ col2src,
                                                      double* __restrict__ ops) {
   __shared__ double t[kMaxP], w[kMaxP];
   if (threadIdx.x < p) {
@@ -219,11 +220,17 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
       const int i = e / D.cols, j = e % D.cols;
       double v = 0.0;
+      // source kinds: row i holds input column c0 + i (zero unless an active source of
+      // the term's range [a, s_hi) sits there)
+      int s = -1;
+      if (D.kind == OP_P2M || D.kind == OP_P2L || D.kind == OP_P2P) {
+        s = col2src ? col2src[D.c0 + i] : D.c0 + i;
+        if (s < D.a || s >= D.s_hi) s = -1;
+      }
       switch (D.kind) {
-        case OP_P2M: {  // Phi~_X[j] += zhat_i U_i / (t_j (x_i - c_X) - 3 r_X)
-          const FmmCell X = cells[D.a];
-          const int s = X.slo + i;
-          v = zhat[s] / (t[j] * (d[s] - X.c) - 3.0 * X.r);
+        case OP_P2M: {  // Phi~_X[j] += zhat_s U_s / (t_j (x_s - c_X) - 3 r_X), X = b
+          const FmmCell X = cells[D.b];
+          if (s >= 0) v = zhat[s] / (t[j] * (d[s] - X.c) - 3.0 * X.r);
           break;
         }
         case OP_M2M: {  // child (a) -> parent (b): i = child node, j = parent node
@@ -260,184 +267,250 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
           v = lagrange(t, w, p, i, ((d[k[jt]] - A.c) + tau[jt]) / A.r) * cs[jt];
           break;
         }
-        case OP_P2L: {  // sources of X (a) -> local expansion of Y (b) at y_j = c_Y + r_Y t_j
-          const FmmCell X = cells[D.a], Y = cells[D.b];
-          const int s = X.slo + i;
-          v = zhat[s] / ((d[s] - Y.c) - Y.r * t[j]);
+        case OP_P2L: {  // source s -> local expansion of Y (b) at y_j = c_Y + r_Y t_j
+          const FmmCell Y = cells[D.b];
+          if (s >= 0) v = zhat[s] / ((d[s] - Y.c) - Y.r * t[j]);
           break;
         }
-        default: {  // OP_P2P: source leaf X (a), target leaf Y (b)
-          const FmmCell X = cells[D.a], Y = cells[D.b];
-          const int s = X.slo + i, jt = Y.tlo + j;
-          v = (zhat[s] * cs[jt]) / ((d[s] - d[k[jt]]) - tau[jt]);
+        default: {  // OP_P2P: source s, target leaf Y (b)
+          const FmmCell Y = cells[D.b];
+          const int jt = Y.tlo + j;
+          if (s >= 0) v = (zhat[s] * cs[jt]) / ((d[s] - d[k[jt]]) - tau[jt]);
           break;
         }
       }
-      out[e] = v;
+      out[int64_t(i) * D.ld + j] = v;
     }
   }
 }
 
 // ------------------------------------------------------------------- K6-K10
-// One FMM pass = a batch of "gathered small GEMMs": for task T and a tile of BM rows,
-//   out[:, T.col0 : T.col0 + N] = sum_t in_t[:, col0_t : col0_t + K_t] * op_t (K_t x N).
-// in/out are U (columns through src/dst maps) or the expansion matrices Phi/Psi.
-// K is streamed in chunks of KC through a 2-stage cp.async pipeline; each warp owns a
-// 32 x 16 output tile (4 x 2 DMMA m8n8k4 fragments).  BN = 16: 8 warps down the rows
-// (BM = 256); BN = 32: 4 x 2 warps (BM = 128).
+// One FMM pass = a batch of "gathered small GEMMs": for task T and every row,
+//   out[r, T.col0 : T.col0 + N] = sum_t in_t[r, col0_t : col0_t + K_t] * op_t (K_t x N).
+// in = U (physical column windows resolved on the host, so no column map is read here)
+// or the expansion matrices Phi/Psi; out = U (through dst[]) or Phi/Psi.
+// Persistent CTAs walk the pass's tiles (task, block of BM rows) with stride gridDim.x;
+// the host orders tasks by decreasing K, so the longest tiles start first.  One
+// continuous STAGES-deep cp.async ring runs across term, chunk and tile boundaries, so
+// a tile's first loads are in flight while the previous tile finishes.  K tails (terms
+// are not multiples of KC) are masked per 4-wide k-step; A reads past the term stay
+// inside the row (columns clamped to ld - 2) and B reads past the op inside the padded
+// ops buffer, and both only ever meet masked k-steps.  Each warp owns a 32 x BN tile
+// (4 x BN/8 DMMA m8n8k4 fragments); 4 warps -> BM = 128 rows per tile.
 constexpr int KC = 16;
 constexpr int ALD = KC + 4;  // 20 doubles: conflict-free A fragment loads
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int n = valid ? 8 : 0;  // src-size 0 -> zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
-template <int BN>
-struct GemmCfg {
-  // every warp owns 32 rows x BN columns (4 x BN/8 DMMA m8n8k4 fragments)
-  static constexpr int NWARP = BN <= 16 ? 8 : 4;
-  static constexpr int NTHR = 32 * NWARP;
-  static constexpr int NT = BN / 8;
-  static constexpr int BM = 32 * NWARP;   // rows per CTA
-  static constexpr int BLD = BN + 4;      // B row stride (doubles)
-  static constexpr int STAGES = 2;        // cp.async pipeline depth
-  static constexpr int A_ELEMS = BM * ALD;
-  static constexpr int B_ELEMS = KC * BLD;
-  static constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * 8;
-};
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int BN>
+struct GemmCfg {
+  static constexpr int NWARP = 4;
+  static constexpr int NTHR = 32 * NWARP;
+  static constexpr int NT = BN / 8;
+  static constexpr int BM = 32 * NWARP;   // rows per tile
+  static constexpr int BLD = BN + 4;      // B row stride (doubles): conflict-free fragments
+  static constexpr int STAGES = 3;        // cp.async ring depth
+  static constexpr int A_ELEMS = BM * ALD;
+  static constexpr int B_ELEMS = KC * BLD;
+  static constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * 8 + STAGES * 16;
+};
+
+struct StageInfo {   // written by the loader, read by the compute side of the same stage
+  int32_t rem;       // K - k0 of the chunk's term (k-steps beyond it are masked)
+  int32_t tile;      // tile the chunk belongs to
+  int32_t last;      // 1: last chunk of the tile (epilogue after it), -1: no chunk
+  int32_t pad;
+};
+
+template <int BN>
 __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
-    const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int64_t rows,
-    const double* __restrict__ ops, const double* __restrict__ U_in, int64_t ld_in,
-    const int32_t* __restrict__ src, double* __restrict__ U_out, int64_t ld_out,
-    const int32_t* __restrict__ dst, double* __restrict__ phi, double* __restrict__ psi, int64_t ldE) {
+    const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int ntiles, int nrb,
+    int64_t rows, const double* __restrict__ ops, const double* __restrict__ U_in, int64_t ld_in,
+    double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst,
+    double* __restrict__ phi, double* __restrict__ psi, int64_t ldE) {
   using G = GemmCfg<BN>;
   constexpr int NT = G::NT;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                            // [STAGES][BM][ALD]
   double* Bs = smem + G::STAGES * G::A_ELEMS;   // [STAGES][KC][BLD]
-  const FmmTask T = tasks[blockIdx.x];
+  StageInfo* info = reinterpret_cast<StageInfo*>(Bs + G::STAGES * G::B_ELEMS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t row0 = int64_t(blockIdx.y) * G::BM;
-  const int nrow = int(rows - row0 < G::BM ? rows - row0 : G::BM);
 
-  auto load_stage = [&](int buf, int term, int kk0) {
-    const FmmTerm R = terms[term];
-    double* a = As + buf * G::A_ELEMS;
-    double* b = Bs + buf * G::B_ELEMS;
-    const double* base = R.in_kind == IO_U ? U_in : (R.in_kind == IO_PHI ? phi : psi);
-    const int64_t ld = R.in_kind == IO_U ? ld_in : ldE;
-    // Every thread owns one fixed column pair (kp, kp+1) of the chunk for rows rr0,
-    // rr0 + 2*NTHR/KC, ...: the column map is read once per stage, and a pair of
-    // adjacent, 16-byte aligned source columns moves as one 16-byte cp.async.
-    {
-      const int kp = (tid % (KC / 2)) * 2, rr0 = tid / (KC / 2);
-      const int k = kk0 + kp;
-      const bool ok0 = k < R.K, ok1 = k + 1 < R.K;
-      int c0 = R.col0 + (ok0 ? k : 0), c1 = R.col0 + (ok1 ? k + 1 : 0);
-      if (R.in_kind == IO_U && src) {
-        c0 = src[c0];
-        c1 = src[c1];
-      }
-      const bool vec = ok1 && c1 == c0 + 1 && !(c0 & 1) && !(ld & 1);
-      const double* p0 = base + row0 * ld + c0;
-      const double* p1 = base + row0 * ld + c1;
-#pragma unroll 4
-      for (int rr = rr0; rr < G::BM; rr += 2 * G::NTHR / KC) {
-        const bool rok = rr < nrow;
-        const int64_t ro = rok ? int64_t(rr) * ld : 0;
-        if (vec) {
-          cp_async16(a + rr * ALD + kp, p0 + ro, rok);
-        } else {
-          cp_async8(a + rr * ALD + kp, p0 + (ok0 ? ro : 0), ok0 && rok);
-          cp_async8(a + rr * ALD + kp + 1, p1 + (ok1 ? ro : 0), ok1 && rok);
+  // ---- loader iterator (uniform across the CTA)
+  int l_tile = blockIdx.x, l_term = 0, l_tend = 0, l_k0 = 0, l_opc0 = 0;
+  int64_t l_row0 = 0;   // first row of the tile
+  bool l_full = true;   // the tile's rows are all < rows (no clamping)
+  FmmTerm R{};
+  auto l_start_tile = [&]() {
+    if (l_tile < ntiles) {
+      const int task = l_tile / nrb;
+      const FmmTask T = tasks[task];
+      l_row0 = int64_t(l_tile - task * nrb) * G::BM;
+      l_full = l_row0 + G::BM <= rows;
+      l_term = T.t_begin;
+      l_tend = T.t_end;
+      l_k0 = 0;
+      l_opc0 = T.op_col0;
+      R = terms[l_term];
+    }
+  };
+  l_start_tile();
+  // A: thread -> column pair kp (of KC/2), rows rr0 + 16 i (BM / 16 of them)
+  const int kp = (tid & (KC / 2 - 1)) * 2, rr0 = tid >> 3;
+  auto issue = [&](int buf) {
+    if (tid == 0) info[buf].last = -1;
+    if (l_tile >= ntiles) return;
+    const bool inU = R.in_kind == IO_U;
+    const double* base = inU ? U_in : (R.in_kind == IO_PHI ? phi : psi);
+    const int64_t ld = inU ? ld_in : ldE;
+    double* a = As + buf * G::A_ELEMS + rr0 * ALD + kp;
+    const int cu = R.col0 + l_k0 + kp;
+    if (!(ld & 1)) {  // pairs (c, c+1), c even: in the row whenever c <= ld - 2
+      const int c = min(cu, int(ld - 2));
+      if (l_full) {
+        const double* g = base + (l_row0 + rr0) * ld + c;
+        const int64_t step = 16 * ld;
+#pragma unroll
+        for (int i = 0; i < G::BM / 16; ++i) {
+          cp_async16(a + 16 * i * ALD, g);
+          g += step;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < G::BM / 16; ++i) {
+          const int64_t r = min(l_row0 + rr0 + 16 * i, rows - 1);
+          cp_async16(a + 16 * i * ALD, base + r * ld + c);
         }
       }
+    } else {  // odd leading dimension: rows are not 16-byte aligned; clamp per column
+      const int c0 = min(cu, int(ld - 1)), c1 = min(cu + 1, int(ld - 1));
+#pragma unroll
+      for (int i = 0; i < G::BM / 16; ++i) {
+        const int64_t r = min(l_row0 + rr0 + 16 * i, rows - 1);
+        cp_async8(a + 16 * i * ALD, base + r * ld + c0);
+        cp_async8(a + 16 * i * ALD + 1, base + r * ld + c1);
+      }
     }
-    for (int e = tid; e < KC * BN; e += G::NTHR) {
-      const int kk = e / BN, jj = e % BN;
-      const int k = kk0 + kk;
-      const bool ok = k < R.K && jj < T.N;
-      cp_async8(b + kk * G::BLD + jj, ops + R.op_off + (ok ? int64_t(k) * R.op_ld + T.op_col0 + jj : 0), ok);
+    // B: KC x BN block of the op (row stride op_ld even, 16-byte aligned rows)
+    double* b = Bs + buf * G::B_ELEMS;
+    const double* bsrc = ops + R.op_off + int64_t(l_k0) * R.op_ld + l_opc0;
+#pragma unroll
+    for (int e = tid; e < KC * BN / 2; e += G::NTHR) {
+      const int kk = e / (BN / 2), jj = (e % (BN / 2)) * 2;
+      cp_async16(b + kk * G::BLD + jj, bsrc + kk * R.op_ld + jj);
     }
+    const int rem = R.K - l_k0;
+    // advance
+    l_k0 += KC;
+    int last = 0;
+    const int tile = l_tile;
+    if (l_k0 >= R.K) {
+      l_k0 = 0;
+      if (++l_term == l_tend) {
+        last = 1;
+        l_tile += gridDim.x;
+        l_start_tile();
+      } else {
+        R = terms[l_term];
+      }
+    }
+    if (tid == 0) info[buf] = StageInfo{rem, tile, last, 0};
   };
+
   double acc[4][NT][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
 
-  // stage list = (term, K-chunk) pairs; a STAGES-deep cp.async ring
-  int nst = 0;
-  for (int t = T.t_begin; t < T.t_end; ++t) nst += (terms[t].K + KC - 1) / KC;
-  int lti = T.t_begin, lk0 = 0;
-  auto load_next = [&](int buf) {
-    load_stage(buf, lti, lk0);
-    lk0 += KC;
-    if (lk0 >= terms[lti].K) {
-      ++lti;
-      lk0 = 0;
-    }
-  };
 #pragma unroll
   for (int q = 0; q < G::STAGES - 1; ++q) {
-    if (q < nst) load_next(q);
+    issue(q);
     cp_async_commit();
   }
-  for (int it = 0; it < nst; ++it) {
+  const int a_off = (warp * 32 + (lane >> 2)) * ALD + (lane & 3);
+  const int b_off = (lane & 3) * G::BLD + (lane >> 2);
+  for (int it = 0;; ++it) {
     const int buf = it % G::STAGES;
-    if (it + G::STAGES - 1 < nst) load_next((it + G::STAGES - 1) % G::STAGES);
+    issue((it + G::STAGES - 1) % G::STAGES);
     cp_async_commit();
     cp_async_wait<G::STAGES - 1>();
     __syncthreads();
-    const double* a = As + buf * G::A_ELEMS;
-    const double* b = Bs + buf * G::B_ELEMS;
+    const StageInfo I = info[buf];
+    if (I.last < 0) break;
+    const double* a = As + buf * G::A_ELEMS + a_off;
+    const double* b = Bs + buf * G::B_ELEMS + b_off;
+    // fragments double-buffered in registers: k-step kk+1 loads while kk multiplies
+    double af[2][4], bf[2][NT];
 #pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
-      double af[4], bf[NT];
+    for (int mt = 0; mt < 4; ++mt) af[0][mt] = a[mt * 8 * ALD];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = a[(warp * 32 + mt * 8 + (lane >> 2)) * ALD + kk + (lane & 3)];
+    for (int nt = 0; nt < NT; ++nt) bf[0][nt] = b[nt * 8];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) bf[nt] = b[(kk + (lane & 3)) * G::BLD + nt * 8 + (lane >> 2)];
+    for (int q = 0; q < KC / 4; ++q) {
+      const int kk = 4 * q, cur = q & 1;
+      if (kk >= I.rem) break;
+      if (q + 1 < KC / 4) {
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[cur ^ 1][mt] = a[mt * 8 * ALD + kk + 4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bf[cur ^ 1][nt] = b[(kk + 4) * G::BLD + nt * 8];
+      }
+      if (kk + 4 > I.rem) {  // ragged K tail: zero both operands of the missing k
+        const bool ok = kk + (lane & 3) < I.rem;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) af[cur][mt] = ok ? af[cur][mt] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bf[cur][nt] = ok ? bf[cur][nt] : 0.0;
+      }
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt], bf[nt]);
+        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt], bf[cur][nt]);
     }
     __syncthreads();  // buffer `buf` is refilled by a later prefetch
-  }
-  // epilogue
+    if (I.last) {     // epilogue of tile I.tile (registers -> global only)
+      const FmmTask T = tasks[I.tile / nrb];
+      const int64_t row0 = int64_t(I.tile % nrb) * G::BM;
+      double* E = T.out_kind == IO_PHI ? phi : psi;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int rr = warp * 32 + mt * 8 + (lane >> 2);
-    if (rr >= nrow) continue;
-    const int64_t r = row0 + rr;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jj = nt * 8 + (lane & 3) * 2 + h;
+      for (int nt = 0; nt < NT; ++nt) {
+        const int jj = nt * 8 + (lane & 3) * 2;
         if (jj >= T.N) continue;
         const int col = T.col0 + jj;
         if (T.out_kind == IO_U) {
-          U_out[r * ld_out + (dst ? dst[col] : col)] = acc[mt][nt][h];
-        } else {
-          (T.out_kind == IO_PHI ? phi : psi)[r * ldE + col] = acc[mt][nt][h];
+          const int c0 = dst ? dst[col] : col;
+          const int c1 = (jj + 1 < T.N) ? (dst ? dst[col + 1] : col + 1) : -1;
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const int64_t r = row0 + warp * 32 + mt * 8 + (lane >> 2);
+            if (r >= rows) continue;
+            U_out[r * ld_out + c0] = acc[mt][nt][0];
+            if (c1 >= 0) U_out[r * ld_out + c1] = acc[mt][nt][1];
+          }
+        } else {  // expansions: N is a multiple of 4, col0 even -> 16-byte stores
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const int64_t r = row0 + warp * 32 + mt * 8 + (lane >> 2);
+            if (r >= rows) continue;
+            *reinterpret_cast<double2*>(E + r * ldE + col) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+          }
         }
       }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
     }
   }
 }
@@ -494,11 +567,11 @@ svd1_status passthrough(int64_t rows, int nq, const double* U_in, int64_t ld_in,
 
 svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cells, int p,
                           const double* d, const int32_t* k, const double* tau,
-                          const double* zhat, const double* cs, double* ops, cudaStream_t st,
-                          int64_t* launches) {
+                          const double* zhat, const double* cs, const int32_t* col2src,
+                          double* ops, cudaStream_t st, int64_t* launches) {
   if (n_ops <= 0) return SVD1_OK;
   const unsigned g = unsigned(std::min(n_ops, 148 * 16));
-  fmm_ops_kernel<<<g, 256, 0, st>>>(n_ops, descs, cells, p, d, k, tau, zhat, cs, ops);
+  fmm_ops_kernel<<<g, 256, 0, st>>>(n_ops, descs, cells, p, d, k, tau, zhat, cs, col2src, ops);
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
@@ -506,30 +579,37 @@ svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cell
 
 template <int BN>
 svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
-                        const double* ops, const double* U_in, int64_t ld_in, const int32_t* src,
-                        double* U_out, int64_t ld_out, const int32_t* dst, double* phi, double* psi,
-                        int64_t ldE, cudaStream_t st) {
+                        const double* ops, const double* U_in, int64_t ld_in, double* U_out,
+                        int64_t ld_out, const int32_t* dst, double* phi, double* psi, int64_t ldE,
+                        cudaStream_t st) {
   using G = GemmCfg<BN>;
-  static bool attr = false;
-  if (!attr) {
+  static int max_ctas = 0;  // resident CTAs on the whole device (persistent grid)
+  if (!max_ctas) {
     SVD1_CUDA_TRY(cudaFuncSetAttribute(fmm_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
-    attr = true;
+    int dev = 0, nsm = 0, per_sm = 0;
+    SVD1_CUDA_TRY(cudaGetDevice(&dev));
+    SVD1_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    SVD1_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fmm_gemm_kernel<BN>, G::NTHR, G::SMEM));
+    max_ctas = std::max(1, nsm * std::max(per_sm, 1));
   }
-  dim3 grid(unsigned(n_tasks), unsigned((rows + G::BM - 1) / G::BM));
-  fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(tasks, terms, rows, ops, U_in, ld_in, src, U_out,
-                                                  ld_out, dst, phi, psi, ldE);
+  const int64_t nrb = (rows + G::BM - 1) / G::BM;
+  const int64_t ntiles = nrb * n_tasks;
+  if (ntiles > (int64_t(1) << 30)) return SVD1_E_INVALID;
+  const int grid = int(std::min<int64_t>(ntiles, max_ctas));
+  fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(tasks, terms, int(ntiles), int(nrb), rows, ops, U_in,
+                                                       ld_in, U_out, ld_out, dst, phi, psi, ldE);
   return SVD1_OK;
 }
 
 svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
                           int64_t rows, const double* ops, const double* U_in, int64_t ld_in,
-                          const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
-                          double* phi, double* psi, int64_t ldE, cudaStream_t st, int64_t* launches) {
+                          double* U_out, int64_t ld_out, const int32_t* dst, double* phi,
+                          double* psi, int64_t ldE, cudaStream_t st, int64_t* launches) {
   if (n_tasks <= 0 || rows <= 0) return SVD1_OK;
-  svd1_status s = bn <= 16 ? launch_gemm<16>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, src, U_out,
-                                             ld_out, dst, phi, psi, ldE, st)
-                           : launch_gemm<32>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, src, U_out,
-                                             ld_out, dst, phi, psi, ldE, st);
+  svd1_status s = bn <= 16 ? launch_gemm<16>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, U_out, ld_out,
+                                             dst, phi, psi, ldE, st)
+                           : launch_gemm<32>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, U_out, ld_out,
+                                             dst, phi, psi, ldE, st);
   if (s != SVD1_OK) return s;
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());

@@ -102,7 +102,8 @@ struct CauchyPrep {
   int64_t rows = 0;
   double flops = 0.0;
   FmmHost F;
-  DevBuf d_cells, d_descs, d_terms, d_tasks, d_ops;
+  std::vector<int32_t> col2src;  // input column -> active source (-1: none); empty = identity
+  DevBuf d_cells, d_descs, d_terms, d_tasks, d_ops, d_col2src;
 };
 
 // Everything one RankOneUpdate (Alg 6.2) needs at apply time.
@@ -364,7 +365,7 @@ bool fmm_cells(FmmHost& F, int s, int L, const Merged& M) {
   return true;
 }
 
-void fmm_lists(FmmHost& F, int p) {
+void fmm_lists(FmmHost& F, int p, const int32_t* src) {
   const int L = F.L;
   auto nonempty = [&](int c) { return F.cells[c].hi > F.cells[c].lo; };
   auto has_src = [&](int c) { return F.cells[c].shi > F.cells[c].slo; };
@@ -413,6 +414,7 @@ void fmm_lists(FmmHost& F, int p) {
       const int y = (1 << l) - 1 + i;
       has_psi[y] = has_tgt(y) && (!m2l[y].empty() || (l >= 2 && has_psi[(y - 1) / 2]));
     }
+  // ops: even row stride and even offset (16-byte aligned rows for the GEMM's B copies)
   auto add_op = [&](int kind, int a, int b, int rows, int cols) {
     FmmOpDesc D;
     D.kind = kind;
@@ -420,20 +422,53 @@ void fmm_lists(FmmHost& F, int p) {
     D.b = b;
     D.rows = rows;
     D.cols = cols;
+    D.ld = (cols + 1) & ~1;
+    D.c0 = 0;
+    D.s_hi = 0;
+    F.ops_elems = (F.ops_elems + 1) & ~int64_t(1);
     D.off = F.ops_elems;
-    F.ops_elems += int64_t(rows) * cols;
+    F.ops_elems += int64_t(rows) * D.ld;
     F.ops.push_back(D);
     return D.off;
   };
-  auto add_term = [&](int in_kind, int col0, int K, int64_t off, int N) {
+  // kreal: rows that carry work (window rows of absent sources are zero): flop count
+  auto add_term = [&](int in_kind, int col0, int K, int64_t off, int op_ld, int kreal, int N) {
     FmmTerm t;
     t.in_kind = in_kind;
     t.col0 = col0;
     t.K = K;
-    t.op_ld = N;
+    t.op_ld = op_ld;
     t.op_off = off;
     F.terms.push_back(t);
-    F.flops_per_row += 2ll * K * N;
+    F.flops_per_row += 2ll * kreal * N;
+  };
+  // sources [s_lo, s_hi) (a contiguous range of the sorted active sources) read through
+  // their physical input columns src[s]: windows of nearby columns (gaps <= 8 are
+  // bridged by zero op rows), each window starting at an even column
+  std::vector<int> pc;
+  auto add_src = [&](int kind, int s_lo, int s_hi, int b, int N) {
+    pc.resize(s_hi - s_lo);
+    bool up = true, down = true;  // monotone maps (identity, reversal) need no sort
+    for (int s2 = s_lo; s2 < s_hi; ++s2) {
+      pc[s2 - s_lo] = src ? src[s2] : s2;
+      if (s2 > s_lo) {
+        up = up && pc[s2 - s_lo] > pc[s2 - s_lo - 1];
+        down = down && pc[s2 - s_lo] < pc[s2 - s_lo - 1];
+      }
+    }
+    if (down) std::reverse(pc.begin(), pc.end());
+    else if (!up) std::sort(pc.begin(), pc.end());
+    size_t a = 0;
+    while (a < pc.size()) {
+      size_t e = a;
+      while (e + 1 < pc.size() && pc[e + 1] - pc[e] <= 8) ++e;
+      const int c0 = pc[a] & ~1, len = pc[e] + 1 - c0;
+      const int64_t off = add_op(kind, s_lo, b, len, N);
+      F.ops.back().c0 = c0;
+      F.ops.back().s_hi = s_hi;
+      add_term(IO_U, c0, len, off, F.ops.back().ld, int(e - a + 1), N);
+      a = e + 1;
+    }
   };
   int tb = 0;
   auto begin_task = [&]() { tb = int(F.terms.size()); };
@@ -457,21 +492,32 @@ void fmm_lists(FmmHost& F, int p) {
       size_t b = a;
       if (in_kind == IO_U) {
         while (b + 1 < xs.size() && F.cells[xs[b + 1]].slo == F.cells[xs[b]].shi) ++b;
-      } else {
-        while (b + 1 < xs.size() && xs[b + 1] == xs[b] + 1) ++b;
+        add_src(op_kind, F.cells[xs[a]].slo, F.cells[xs[b]].shi, y, N);
+        a = b + 1;
+        continue;
       }
-      int K = 0;
+      while (b + 1 < xs.size() && xs[b + 1] == xs[b] + 1) ++b;
+      int K = 0, ld = 0;
       int64_t off0 = -1;
       for (size_t q = a; q <= b; ++q) {
-        const int x = xs[q];
-        const int kx = in_kind == IO_U ? F.cells[x].shi - F.cells[x].slo : p;
-        const int64_t off = add_op(op_kind, x, y, kx, N);
+        const int64_t off = add_op(op_kind, xs[q], y, p, N);
         if (off0 < 0) off0 = off;
-        K += kx;
+        ld = F.ops.back().ld;
+        K += p;
       }
-      add_term(in_kind, in_kind == IO_U ? F.cells[xs[a]].slo : xs[a] * p, K, off0, N);
+      add_term(in_kind, xs[a] * p, K, off0, ld, K, N);
       a = b + 1;
     }
+  };
+  // longest tasks first inside each pass (persistent CTAs take tiles in this order)
+  auto sort_pass = [&](int b) {
+    auto cost = [&](const FmmTask& T) {
+      int64_t k = 0;
+      for (int t = T.t_begin; t < T.t_end; ++t) k += F.terms[t].K;
+      return k;
+    };
+    std::stable_sort(F.tasks.begin() + b, F.tasks.end(),
+                     [&](const FmmTask& x, const FmmTask& y) { return cost(x) > cost(y); });
   };
   const int lf0 = (1 << L) - 1, nleaf = 1 << L;
   if (L >= 1) {
@@ -483,9 +529,11 @@ void fmm_lists(FmmHost& F, int p) {
       if (!has_src(x)) continue;
       const int sx = F.cells[x].shi - F.cells[x].slo;
       begin_task();
-      add_term(IO_U, F.cells[x].slo, sx, add_op(OP_P2M, x, x, sx, p), p);
+      add_src(OP_P2M, F.cells[x].slo, F.cells[x].shi, x, p);
       end_task(IO_PHI, x * p, p);
+      (void)sx;
     }
+    sort_pass(F.pass_begin.back());
     // M2M (STEP 6), levels L-1 .. 1 (operator re-derived)
     for (int l = L - 1; l >= 1; --l) {
       F.pass_begin.push_back(int(F.tasks.size()));
@@ -500,6 +548,7 @@ void fmm_lists(FmmHost& F, int p) {
         add_runs(ch, IO_PHI, OP_M2M, c, p);
         end_task(IO_PHI, c * p, p);
       }
+      sort_pass(F.pass_begin.back());
     }
     // downward (STEP 8; M2L re-derived), restructured:
     // (a) one pass with the M2L (and P2L) contributions of EVERY cell, all levels at
@@ -522,6 +571,7 @@ void fmm_lists(FmmHost& F, int p) {
       F.n_m2l_pairs += int(m2l[y].size());
       end_task(IO_PSI, y * p, p);
     }
+    sort_pass(F.pass_begin.back());
     for (int l = 2; l <= L - 1; ++l) {
       F.pass_begin.push_back(int(F.tasks.size()));
       F.pass_bn.push_back(p);
@@ -529,10 +579,15 @@ void fmm_lists(FmmHost& F, int p) {
         const int y = (1 << l) - 1 + i, par = (y - 1) / 2;
         if (!has_psi[y] || !has_psi[par]) continue;
         begin_task();
-        if (!m2l[y].empty()) add_term(IO_PSI, y * p, p, add_op(OP_ID, y, y, p, p), p);
-        add_term(IO_PSI, par * p, p, add_op(OP_L2L, par, y, p, p), p);
+        if (!m2l[y].empty()) {
+          const int64_t off = add_op(OP_ID, y, y, p, p);
+          add_term(IO_PSI, y * p, p, off, F.ops.back().ld, p, p);
+        }
+        const int64_t off = add_op(OP_L2L, par, y, p, p);
+        add_term(IO_PSI, par * p, p, off, F.ops.back().ld, p, p);
         end_task(IO_PSI, y * p, p);
       }
+      sort_pass(F.pass_begin.back());
     }
   }
   // final: L2P (STEP 9) + P2P near field (STEP 10); two launches by
@@ -556,13 +611,20 @@ void fmm_lists(FmmHost& F, int p) {
     if (split_narrow && (ty > 16) != (wide == 1)) continue;
     begin_task();
     const int par = (y - 1) / 2;
-    if (!m2l[y].empty()) add_term(IO_PSI, y * p, p, add_op(OP_L2P, y, y, p, ty), ty);
-    if (L >= 2 && has_psi[par]) add_term(IO_PSI, par * p, p, add_op(OP_L2P_FROM, par, y, p, ty), ty);
+    if (!m2l[y].empty()) {
+      const int64_t off = add_op(OP_L2P, y, y, p, ty);
+      add_term(IO_PSI, y * p, p, off, F.ops.back().ld, p, ty);
+    }
+    if (L >= 2 && has_psi[par]) {
+      const int64_t off = add_op(OP_L2P_FROM, par, y, p, ty);
+      add_term(IO_PSI, par * p, p, off, F.ops.back().ld, p, ty);
+    }
     add_runs(near[y], IO_U, OP_P2P, y, ty);
     F.n_near_pairs += int(near[y].size());
     F.max_near = std::max<int>(F.max_near, int(near[y].size()));
     end_task(IO_U, F.cells[y].tlo, ty);
   }
+  sort_pass(F.pass_begin.back());
   }
   F.pass_begin.push_back(int(F.tasks.size()));
   for (int& bn : F.pass_bn) bn = bn <= 16 ? 16 : 32;
@@ -572,7 +634,7 @@ void fmm_lists(FmmHost& F, int p) {
 }  // namespace
 
 void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<double>& da,
-                    const std::vector<double>& mu) {
+                    const std::vector<double>& mu, const int32_t* src) {
   const Merged M = merge_points(da, mu);
   int L0 = 0;
   while ((2 * int64_t(na) + (int64_t(1) << L0) - 1) / (int64_t(1) << L0) > 2 * leaf) ++L0;
@@ -586,10 +648,11 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
       if (std::getenv("SVD1_DEBUG")) fprintf(stderr, "[svd1] fmm L=%d infeasible\n", L);
       continue;
     }
-    fmm_lists(F2, p);
+    const double tl0 = now_ms();
+    fmm_lists(F2, p, src);
     if (std::getenv("SVD1_DEBUG"))
-      fprintf(stderr, "[svd1] fmm L=%d flops/row=%lld max_near=%d m2l=%d near=%d\n", L,
-              (long long)F2.flops_per_row, F2.max_near, F2.n_m2l_pairs, F2.n_near_pairs);
+      fprintf(stderr, "[svd1] fmm L=%d flops/row=%lld max_near=%d m2l=%d near=%d lists %.3f ms\n", L,
+              (long long)F2.flops_per_row, F2.max_near, F2.n_m2l_pairs, F2.n_near_pairs, now_ms() - tl0);
     if (!have || F2.flops_per_row < best.flops_per_row) {
       best = std::move(F2);
       have = true;
@@ -604,8 +667,10 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
 
 
 // host compute only (thread-safe: touches nothing but C)
+// src: active source i -> input column (nullptr: identity), n_in: input columns
 void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
-                 const std::vector<double>& da, const std::vector<double>& mu, int p) {
+                 const std::vector<double>& da, const std::vector<double>& mu, int p,
+                 const int32_t* src, int n_in) {
   const int minn = cfg.fmm_min_n > 0 ? cfg.fmm_min_n : 384;
   const int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2: s ~ 2p, capped by the tile
   bool fmm = (cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
@@ -616,8 +681,13 @@ void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
   C.rows = rows;
   C.flops = 2.0 * double(rows) * double(na) * double(na);
   if (!fmm) return;
-  fmm_build_host(C.F, na, leaf, p, da, mu);
+  fmm_build_host(C.F, na, leaf, p, da, mu, src);
   C.flops = double(C.F.flops_per_row) * double(rows);
+  C.col2src.clear();
+  if (src) {
+    C.col2src.assign(size_t(n_in), -1);
+    for (int i = 0; i < na; ++i) C.col2src[src[i]] = i;
+  }
 }
 
 svd1_status cauchy_upload(svd1_plan_t P, CauchyPrep& C) {
@@ -631,14 +701,18 @@ svd1_status cauchy_upload(svd1_plan_t P, CauchyPrep& C) {
   TRY(upload(P, C.d_descs, F.ops, &dd));
   TRY(upload(P, C.d_terms, F.terms, &dt));
   TRY(upload(P, C.d_tasks, F.tasks, &dk));
+  if (!C.col2src.empty()) {
+    int32_t* c2s;
+    TRY(upload(P, C.d_col2src, C.col2src, &c2s));
+  }
   double* ops;
-  TRY(C.d_ops.get<double>(size_t(F.ops_elems), &ops));
+  TRY(C.d_ops.get<double>(size_t(F.ops_elems + kOpsPad), &ops));
   return SVD1_OK;
 }
 
 svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
                            const std::vector<double>& da, const std::vector<double>& mu, int p) {
-  cauchy_plan(P->cfg, C, rows, na, da, mu, p);
+  cauchy_plan(P->cfg, C, rows, na, da, mu, p, nullptr, na);
   return cauchy_upload(P, C);
 }
 
@@ -666,7 +740,8 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   auto* dt = static_cast<FmmTerm*>(C.d_terms.p);
   auto* dk = static_cast<FmmTask*>(C.d_tasks.p);
   auto* ops = static_cast<double*>(C.d_ops.p);
-  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, ops, st,
+  const int32_t* c2s = C.col2src.empty() ? nullptr : static_cast<int32_t*>(C.d_col2src.p);
+  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, c2s, ops, st,
                     &P->launches));
   const bool dbg = std::getenv("SVD1_DEBUG") != nullptr;
   if (dbg) {  // host-side validation of the task lists
@@ -706,8 +781,8 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   }
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
-    TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, ops, U_in, ld_in, d_src, U_out, ld_out,
-                      d_dst, phi, psi, ldE, st, &P->launches));
+    TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, ops, U_in, ld_in, U_out, ld_out, d_dst,
+                      phi, psi, ldE, st, &P->launches));
     if (dbg) {
       cudaError_t err = cudaStreamSynchronize(st);
       fprintf(stderr, "[svd1] pass %zu tasks [%d,%d): %s\n", s, b, e, cudaGetErrorString(err));
@@ -991,7 +1066,7 @@ void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool
   for (int j = 0; j < S.na; ++j) S.dst_cols[j] = oc(S.tgt_pos[j]);
   S.pass_dst_cols.resize(S.pass_dst.size());
   for (size_t q = 0; q < S.pass_dst.size(); ++q) S.pass_dst_cols[q] = oc(S.pass_dst[q]);
-  if (S.na > 0) cauchy_plan(cfg, S.cp, rows, S.na, S.da, S.mu, p);
+  if (S.na > 0) cauchy_plan(cfg, S.cp, rows, S.na, S.da, S.mu, p, S.src_cols.data(), S.N);
 }
 
 svd1_status apply_upload(svd1_plan_t P, StepRecord& S) {
@@ -1505,7 +1580,7 @@ svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k, co
     mu[j] = dh[k[j]] + tau[j];
   }
   FmmHost F;
-  fmm_build_host(F, int(n), leaf, p, dh, mu);
+  fmm_build_host(F, int(n), leaf, p, dh, mu, nullptr);
   int64_t nonempty = 0, max_leaf = 0;
   for (int c = 0; c < F.ncells; ++c) nonempty += F.cells[c].hi > F.cells[c].lo;
   for (int i = 0; i < (1 << F.L); ++i) {

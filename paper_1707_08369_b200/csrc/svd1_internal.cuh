@@ -100,17 +100,20 @@ enum FmmOpKind : int32_t {
   OP_ID = 7,        // p x p identity (in-place accumulation of the L2L chain)
   OP_L2P_FROM = 8   // local expansion of cell a evaluated at the targets of leaf b
 };
-struct FmmOpDesc {    // one operator matrix to build: rows x cols, row-major at ops + off
-  int32_t kind, a, b; // cells (a = source side, b = target side; see kernel)
-  int32_t rows, cols;
-  int64_t off;
+struct FmmOpDesc {    // one operator matrix to build: rows x cols, row stride ld, at ops + off
+  int32_t kind, a, b; // a = source cell (expansion kinds) or first source index (source
+                      // kinds P2M/P2L/P2P); b = target-side cell
+  int32_t rows, cols, ld;
+  int64_t off;        // 16-byte aligned (even), ld even
+  int32_t c0, s_hi;   // source kinds: row q <-> input column c0 + q, holding active source
+                      // s = col2src[c0 + q]; rows with s outside [a, s_hi) are zero
 };
 enum FmmIoKind : int32_t { IO_U = 0, IO_PHI = 1, IO_PSI = 2 };
 // Expansions are stored as row-major matrices Phi, Psi (rows x ldE, ldE = ncells * p):
 // cell c's p coefficients of row r at [r * ldE + c * p].  Adjacent cells are adjacent
 // columns, so consecutive interaction partners merge into one long-K term.
 struct FmmTerm {      // in[:, col0 : col0 + K] * op (K x N, row-major, leading dim op_ld)
-  int32_t in_kind;    // IO_U (columns mapped through src[]) or IO_PHI / IO_PSI
+  int32_t in_kind;    // IO_U (physical columns of U_in, col0 even) or IO_PHI / IO_PSI
   int32_t col0;
   int32_t K;
   int32_t op_ld;
@@ -125,12 +128,15 @@ struct FmmTask {      // out[:, col0 : col0 + N] = sum of terms
 };
 svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cells, int p,
                           const double* d, const int32_t* k, const double* tau,
-                          const double* zhat, const double* cs, double* ops, cudaStream_t st,
-                          int64_t* launches);
+                          const double* zhat, const double* cs, const int32_t* col2src,
+                          double* ops, cudaStream_t st, int64_t* launches);
 // One pass: every task's output block for all rows.  bn = 16 or 32 (>= every task N).
+// Terms read physical column windows of U_in (col0 even) or of Phi/Psi; op rows are
+// 16-byte aligned with even op_ld; the ops buffer has kOpsPad doubles of slack.
 svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
                           int64_t rows, const double* ops, const double* U_in, int64_t ld_in,
-                          const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
-                          double* phi, double* psi, int64_t ldE, cudaStream_t st, int64_t* launches);
+                          double* U_out, int64_t ld_out, const int32_t* dst, double* phi,
+                          double* psi, int64_t ldE, cudaStream_t st, int64_t* launches);
+constexpr int64_t kOpsPad = 16 * 64;
 
 }  // namespace svd1

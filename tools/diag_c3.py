@@ -23,3 +23,18 @@ for t in range(nup):
     rep = plan.update(U, s, V, torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev))
     torch.cuda.synchronize()
 print({k: rep[k] for k in ("t_ms", "apply_ms", "apply_flops", "spectral_ms", "fmm_levels", "n_active")})
+
+# realistic spectrum for host-side planning benchmarks: the first eigen-update of the
+# next update (d = sigma^2 ascending, z = U^T a, rho ~ |b|^2), roots by the GPU solver
+import numpy as np
+a, b = inp["ab"][nup % len(inp["ab"])]
+sg = s.cpu().numpy()
+order = np.argsort(sg ** 2, kind="stable")
+d = np.ascontiguousarray((sg ** 2)[order])
+z = np.ascontiguousarray((U.T @ torch.from_numpy(a).to(dev)).cpu().numpy()[order])
+rho = float(b @ b)
+kk, tau, it = plan.secular_solve(torch.from_numpy(d).to(dev), torch.from_numpy(z).to(dev), rho)
+kk, tau = kk.cpu().numpy(), tau.cpu().numpy()
+if True:
+    np.savez(os.path.join(ROOT, "gpurun_out", f"spectrum_c{cfg_id}.npz"), d=d, z=z, rho=rho, k=kk, tau=tau)
+    print("saved spectrum", d.shape)
