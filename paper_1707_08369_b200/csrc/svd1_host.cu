@@ -365,7 +365,8 @@ bool fmm_cells(FmmHost& F, int s, int L, const Merged& M) {
   return true;
 }
 
-void fmm_lists(FmmHost& F, int p, const int32_t* src) {
+void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
+  const double tt0 = now_ms();
   const int L = F.L;
   auto nonempty = [&](int c) { return F.cells[c].hi > F.cells[c].lo; };
   auto has_src = [&](int c) { return F.cells[c].shi > F.cells[c].slo; };
@@ -408,12 +409,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src) {
     std::sort(near[c].begin(), near[c].end());
     std::sort(m2l[c].begin(), m2l[c].end());
   }
-  std::vector<char> has_psi(F.ncells, 0);
-  for (int l = 1; l <= L; ++l)
-    for (int i = 0; i < (1 << l); ++i) {
-      const int y = (1 << l) - 1 + i;
-      has_psi[y] = has_tgt(y) && (!m2l[y].empty() || (l >= 2 && has_psi[(y - 1) / 2]));
-    }
+  const double tt1 = now_ms();
   // ops: even row stride and even offset (16-byte aligned rows for the GEMM's B copies)
   auto add_op = [&](int kind, int a, int b, int rows, int cols) {
     FmmOpDesc D;
@@ -510,16 +506,32 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src) {
     }
   };
   // longest tasks first inside each pass (persistent CTAs take tiles in this order)
+  std::vector<std::pair<int64_t, int>> order;
+  std::vector<FmmTask> tmp;
   auto sort_pass = [&](int b) {
-    auto cost = [&](const FmmTask& T) {
+    const int e = int(F.tasks.size());
+    order.clear();
+    for (int q = b; q < e; ++q) {
       int64_t k = 0;
-      for (int t = T.t_begin; t < T.t_end; ++t) k += F.terms[t].K;
-      return k;
-    };
-    std::stable_sort(F.tasks.begin() + b, F.tasks.end(),
-                     [&](const FmmTask& x, const FmmTask& y) { return cost(x) > cost(y); });
+      for (int t = F.tasks[q].t_begin; t < F.tasks[q].t_end; ++t) k += F.terms[t].K;
+      order.push_back({-k, q});
+    }
+    std::sort(order.begin(), order.end());  // (cost desc, index asc): stable
+    tmp.assign(F.tasks.begin() + b, F.tasks.end());
+    for (int q = b; q < e; ++q) F.tasks[q] = tmp[order[q - b].second - b];
   };
+  F.ops.reserve(size_t(F.ncells) * 8);
+  F.terms.reserve(size_t(F.ncells) * 6);
+  F.tasks.reserve(size_t(F.ncells) * 3);
   const int lf0 = (1 << L) - 1, nleaf = 1 << L;
+  // Levels are grouped into bands computed by ONE pass each (a launch costs about
+  // launch_row flops per row of work): a level joins the current band when the extra
+  // flops of reaching back to the band's input level stay below that.
+  const double launch_row = 2.0e8 / double(std::max<int64_t>(rows, 1));
+  auto first_desc = [](int c, int depth) { return ((c + 1) << depth) - 1; };
+  // where the full local expansion of a cell lives (IO_PSI: its M2L part alone, IO_PHI:
+  // accumulated with its ancestors' by a band pass; -1: none)
+  std::vector<int> loc(F.ncells, -1);
   if (L >= 1) {
     // P2M (STEP 5) in the scaled far-field form
     F.pass_begin.push_back(int(F.tasks.size()));
@@ -527,35 +539,58 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src) {
     for (int i = 0; i < nleaf; ++i) {
       const int x = lf0 + i;
       if (!has_src(x)) continue;
-      const int sx = F.cells[x].shi - F.cells[x].slo;
       begin_task();
       add_src(OP_P2M, F.cells[x].slo, F.cells[x].shi, x, p);
       end_task(IO_PHI, x * p, p);
-      (void)sx;
     }
     sort_pass(F.pass_begin.back());
-    // M2M (STEP 6), levels L-1 .. 1 (operator re-derived)
-    for (int l = L - 1; l >= 1; --l) {
+    // M2M (STEP 6; operator re-derived), levels L-1 .. 1 in
+    // bands: every level of a band reads the band's input level f directly (the M2M
+    // operator of any descendant D -> ancestor c has the same closed form).
+    std::vector<int> ds;
+    int f = L;
+    while (f - 1 >= 1) {
+      int lo = f - 1;
+      while (lo - 1 >= 1) {
+        const int l2 = lo - 1;
+        double extra = 0.0;  // flops per row beyond the level-by-level M2M
+        for (int i = 0; i < (1 << l2); ++i) {
+          const int c = (1 << l2) - 1 + i;
+          if (!has_src(c)) continue;
+          const int d0 = first_desc(c, f - l2);
+          int nd = 0;
+          for (int q = 0; q < (1 << (f - l2)); ++q) nd += has_src(d0 + q);
+          int nch = has_src(2 * c + 1) + has_src(2 * c + 2);
+          extra += 2.0 * double(nd - nch) * p * p;
+        }
+        if (extra > launch_row) break;
+        lo = l2;
+      }
       F.pass_begin.push_back(int(F.tasks.size()));
       F.pass_bn.push_back(p);
-      for (int i = 0; i < (1 << l); ++i) {
-        const int c = (1 << l) - 1 + i;
-        if (!has_src(c)) continue;
-        std::vector<int> ch;
-        for (int x : {2 * c + 1, 2 * c + 2})
-          if (has_src(x)) ch.push_back(x);
-        begin_task();
-        add_runs(ch, IO_PHI, OP_M2M, c, p);
-        end_task(IO_PHI, c * p, p);
-      }
+      for (int l = f - 1; l >= lo; --l)
+        for (int i = 0; i < (1 << l); ++i) {
+          const int c = (1 << l) - 1 + i;
+          if (!has_src(c)) continue;
+          ds.clear();
+          const int d0 = first_desc(c, f - l);
+          for (int q = 0; q < (1 << (f - l)); ++q)
+            if (has_src(d0 + q)) ds.push_back(d0 + q);
+          begin_task();
+          add_runs(ds, IO_PHI, OP_M2M, c, p);
+          end_task(IO_PHI, c * p, p);
+        }
       sort_pass(F.pass_begin.back());
+      f = lo;
     }
     // downward (STEP 8; M2L re-derived), restructured:
     // (a) one pass with the M2L (and P2L) contributions of EVERY cell, all levels at
-    //     once (no dependence between them: long coarse-level K chains run beside
-    //     the many short fine-level tasks);
-    // (b) the L2L chain for levels 2..L-1, accumulating in place
-    //     Psi_Y <- Psi_Y * I + Psi_parent * S_Y;
+    //     once (no dependence between them), into Psi;
+    // (b) L2L for levels 2..L-1 in bands: the full local expansion of a band cell Y is
+    //     sum over its ancestors A in the band (A = Y included) of Psi_A S(A -> Y), plus
+    //     full(anchor) S(anchor -> Y) for its ancestor at the level above the band;
+    //     exact, since the local expansion is a polynomial and L2L re-interpolates it.
+    //     Full expansions are stored in Phi (dead after the M2L pass);
     // (c) leaves take L2L from their parent folded into the final pass (evaluating
     //     the parent's local polynomial at the targets is exactly L2L then L2P).
     F.pass_begin.push_back(int(F.tasks.size()));
@@ -572,22 +607,62 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src) {
       end_task(IO_PSI, y * p, p);
     }
     sort_pass(F.pass_begin.back());
-    for (int l = 2; l <= L - 1; ++l) {
-      F.pass_begin.push_back(int(F.tasks.size()));
-      F.pass_bn.push_back(p);
-      for (int i = 0; i < (1 << l); ++i) {
-        const int y = (1 << l) - 1 + i, par = (y - 1) / 2;
-        if (!has_psi[y] || !has_psi[par]) continue;
-        begin_task();
-        if (!m2l[y].empty()) {
-          const int64_t off = add_op(OP_ID, y, y, p, p);
-          add_term(IO_PSI, y * p, p, off, F.ops.back().ld, p, p);
+    for (int i = 0; i < 2 && i < (1 << L); ++i) {
+      const int y = 1 + i;  // level 1: full = the M2L part
+      if (L >= 1 && has_tgt(y) && !m2l[y].empty()) loc[y] = IO_PSI;
+    }
+    int a = 1;  // anchor level: full expansions known
+    while (a + 1 <= L - 1) {
+      int hi = a + 1;
+      while (hi + 1 <= L - 1) {
+        double extra = 0.0;  // ancestors beyond the parent, per target cell of level hi+1
+        const int l2 = hi + 1;
+        for (int i = 0; i < (1 << l2); ++i) {
+          const int y = (1 << l2) - 1 + i;
+          if (!has_tgt(y)) continue;
+          int na2 = 0;
+          for (int A = (y - 1) / 2, l3 = l2 - 1; l3 >= a + 1; A = (A - 1) / 2, --l3) na2 += !m2l[A].empty();
+          extra += 2.0 * double(std::max(na2 - 1, 0)) * p * p;
         }
-        const int64_t off = add_op(OP_L2L, par, y, p, p);
-        add_term(IO_PSI, par * p, p, off, F.ops.back().ld, p, p);
-        end_task(IO_PSI, y * p, p);
+        if (extra > launch_row) break;
+        hi = l2;
       }
-      sort_pass(F.pass_begin.back());
+      const int pb = int(F.tasks.size());
+      for (int l = a + 1; l <= hi; ++l)
+        for (int i = 0; i < (1 << l); ++i) {
+          const int y = (1 << l) - 1 + i;
+          if (!has_tgt(y)) continue;
+          // (cell, input) pairs: Psi of the band ancestors with an M2L part, then the
+          // anchor's full expansion
+          int nA = 0, Acell[32], Akind[32];
+          int A = y;
+          for (int l3 = l; l3 >= a + 1; --l3, A = (A - 1) / 2)
+            if (!m2l[A].empty()) {
+              Acell[nA] = A;
+              Akind[nA++] = IO_PSI;
+            }
+          if (loc[A] >= 0) {  // A is now the ancestor at the anchor level a
+            Acell[nA] = A;
+            Akind[nA++] = loc[A];
+          }
+          if (nA == 0 || (nA == 1 && Acell[0] == y)) {  // nothing to accumulate
+            loc[y] = nA ? IO_PSI : -1;
+            continue;
+          }
+          begin_task();
+          for (int q = 0; q < nA; ++q) {
+            const int64_t off = add_op(Acell[q] == y ? OP_ID : OP_L2L, Acell[q], y, p, p);
+            add_term(Akind[q], Acell[q] * p, p, off, F.ops.back().ld, p, p);
+          }
+          end_task(IO_PHI, y * p, p);
+          loc[y] = IO_PHI;
+        }
+      if (int(F.tasks.size()) > pb) {
+        F.pass_begin.push_back(pb);
+        F.pass_bn.push_back(p);
+        sort_pass(pb);
+      }
+      a = hi;
     }
   }
   // final: L2P (STEP 9) + P2P near field (STEP 10); two launches by
@@ -615,9 +690,9 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src) {
       const int64_t off = add_op(OP_L2P, y, y, p, ty);
       add_term(IO_PSI, y * p, p, off, F.ops.back().ld, p, ty);
     }
-    if (L >= 2 && has_psi[par]) {
+    if (par >= 1 && loc[par] >= 0) {
       const int64_t off = add_op(OP_L2P_FROM, par, y, p, ty);
-      add_term(IO_PSI, par * p, p, off, F.ops.back().ld, p, ty);
+      add_term(loc[par], par * p, p, off, F.ops.back().ld, p, ty);
     }
     add_runs(near[y], IO_U, OP_P2P, y, ty);
     F.n_near_pairs += int(near[y].size());
@@ -628,13 +703,16 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src) {
   }
   F.pass_begin.push_back(int(F.tasks.size()));
   for (int& bn : F.pass_bn) bn = bn <= 16 ? 16 : 32;
+  if (std::getenv("SVD1_DEBUG"))
+    fprintf(stderr, "[svd1] lists: traversal %.3f ms, generation %.3f ms (ops %zu terms %zu tasks %zu)\n",
+            tt1 - tt0, now_ms() - tt1, F.ops.size(), F.terms.size(), F.tasks.size());
   (void)nonempty;
 }
 
 }  // namespace
 
 void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<double>& da,
-                    const std::vector<double>& mu, const int32_t* src) {
+                    const std::vector<double>& mu, const int32_t* src, int64_t rows) {
   const Merged M = merge_points(da, mu);
   int L0 = 0;
   while ((2 * int64_t(na) + (int64_t(1) << L0) - 1) / (int64_t(1) << L0) > 2 * leaf) ++L0;
@@ -648,8 +726,19 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
       if (std::getenv("SVD1_DEBUG")) fprintf(stderr, "[svd1] fmm L=%d infeasible\n", L);
       continue;
     }
+    // a leaf whose hull spans a quarter of the spectrum (outliers packed with bulk
+    // points because the capacities left no room for a gap split) is near to every
+    // leaf: skip building lists for such a tree when a deeper one is still to come
+    if (L < L0 + 2) {
+      double rmax = 0.0;
+      for (int i = 0; i < (1 << L); ++i) rmax = std::max(rmax, F2.cells[(1 << L) - 1 + i].r);
+      if (rmax >= 0.25 * F2.cells[0].r && F2.cells[0].r > 0.0) {
+        if (std::getenv("SVD1_DEBUG")) fprintf(stderr, "[svd1] fmm L=%d skipped (wide leaf)\n", L);
+        continue;
+      }
+    }
     const double tl0 = now_ms();
-    fmm_lists(F2, p, src);
+    fmm_lists(F2, p, src, rows);
     if (std::getenv("SVD1_DEBUG"))
       fprintf(stderr, "[svd1] fmm L=%d flops/row=%lld max_near=%d m2l=%d near=%d lists %.3f ms\n", L,
               (long long)F2.flops_per_row, F2.max_near, F2.n_m2l_pairs, F2.n_near_pairs, now_ms() - tl0);
@@ -659,6 +748,14 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
     }
   }
   F = std::move(best);
+  if (std::getenv("SVD1_DEBUG"))
+    for (size_t q = 0; q + 1 < F.pass_begin.size(); ++q) {
+      double fl = 0.0;
+      for (int t = F.pass_begin[q]; t < F.pass_begin[q + 1]; ++t)
+        for (int u = F.tasks[t].t_begin; u < F.tasks[t].t_end; ++u) fl += 2.0 * F.terms[u].K * F.tasks[t].N;
+      fprintf(stderr, "[svd1]   pass %zu: %d tasks, %.0f flops/row (window)\n", q,
+              F.pass_begin[q + 1] - F.pass_begin[q], fl);
+    }
 }
 
 // Cauchy apply of one step, split in a host phase (decide FMM vs direct, build the
@@ -681,7 +778,7 @@ void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
   C.rows = rows;
   C.flops = 2.0 * double(rows) * double(na) * double(na);
   if (!fmm) return;
-  fmm_build_host(C.F, na, leaf, p, da, mu, src);
+  fmm_build_host(C.F, na, leaf, p, da, mu, src, rows);
   C.flops = double(C.F.flops_per_row) * double(rows);
   C.col2src.clear();
   if (src) {
@@ -779,10 +876,36 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
               e - b, fa * rows, fp * rows, fa > 0 ? fp / fa : 0.0, (long long)kmax);
     }
   }
+  const bool ptime = std::getenv("SVD1_PASSTIME") != nullptr;  // diagnostics (syncs)
+  std::vector<cudaEvent_t> pev;
+  auto pmark = [&]() {
+    if (!ptime) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    pev.push_back(e);
+  };
+  struct PassTimePrinter {
+    std::vector<cudaEvent_t>* ev;
+    ~PassTimePrinter() {
+      if (ev->size() < 2) return;
+      cudaEventSynchronize(ev->back());
+      fprintf(stderr, "[svd1] pass us:");
+      for (size_t i = 1; i < ev->size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, (*ev)[i - 1], (*ev)[i]);
+        fprintf(stderr, " %.1f", 1e3 * ms);
+      }
+      fprintf(stderr, "\n");
+      for (auto e : *ev) cudaEventDestroy(e);
+    }
+  } ptp{&pev};
+  pmark();
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, ops, U_in, ld_in, U_out, ld_out, d_dst,
                       phi, psi, ldE, st, &P->launches));
+    pmark();
     if (dbg) {
       cudaError_t err = cudaStreamSynchronize(st);
       fprintf(stderr, "[svd1] pass %zu tasks [%d,%d): %s\n", s, b, e, cudaGetErrorString(err));
@@ -799,6 +922,18 @@ svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
   return SVD1_OK;
 }
 
+// joins its threads on scope exit (early error returns included)
+struct Joiner {
+  std::vector<std::thread> ts;
+  void add(std::thread&& t) { ts.push_back(std::move(t)); }
+  void join() {
+    for (auto& t : ts)
+      if (t.joinable()) t.join();
+    ts.clear();
+  }
+  ~Joiner() { join(); }
+};
+
 // --------------------------------------------------------- Alg 6.2 spectral
 // One RankOneUpdate on the small vectors, in two halves so that the U- and
 // V-side eigen-updates run on the GPU together and the host builds FMM trees meanwhile.
@@ -807,6 +942,7 @@ svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
 svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<double>& D,
                             const std::vector<double>& z, double rho,
                             const std::vector<std::vector<double>>& carries, int ev0) {
+  const double th_start = now_ms();
   const int N = int(D.size());
   S.clear_host();  // device buffers are kept (grow-only)
   S.N = N;
@@ -906,6 +1042,7 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     S.src_cols[i] = perm[S.act[i]];
   }
   if (na == 0) return SVD1_OK;
+  const double th0 = now_ms();
   std::vector<double> carry_act(size_t(nc) * na);
   for (int q = 0; q < nc; ++q)
     for (int i = 0; i < na; ++i) carry_act[size_t(q) * na + i] = cs_sorted[q][S.act[i]];
@@ -965,6 +1102,9 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     S.rb_cap = words * sizeof(double);
   }
   SVD1_CUDA_TRY(cudaMemcpyAsync(S.rb, dout, words * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  if (std::getenv("SVD1_TIMING"))
+    fprintf(stderr, "[svd1] spectral_launch N=%d: host prep %.3f ms, stage+launch %.3f ms\n", N,
+            th0 - th_start, now_ms() - th0);
   return SVD1_OK;
 }
 
@@ -1297,6 +1437,15 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   TRY(spectral_finish(P, S[0], Du, cu));
   TRY(spectral_finish(P, S[2], Dv, cv));
   const double tC = now_ms();
+  // The Cauchy/FMM plans of the first applies depend on round 1 only: build them on two
+  // worker threads while this thread launches round 2 and the GPU runs it.
+  Joiner planners;
+  {
+    const svd1_config cfg = P->cfg;
+    const int pp = P->p;
+    planners.add(std::thread([&S, cfg, pp, rows = c.u_rows] { apply_plan(cfg, pp, S[0], rows, false); }));
+    planners.add(std::thread([&S, cfg, pp, rows = c.v_rows] { apply_plan(cfg, pp, S[2], rows, false); }));
+  }
   // Round 2: STEP 5 (U, rho2, z2 = X1^T U^T b1) and STEP 7 (V, rho4)
   {
     std::vector<double> z2 = cu[0], z4 = cv[0];
@@ -1307,7 +1456,9 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   }
   // host work overlapping round 2 on the GPU: Cauchy plans of the first applies
   const double tD = now_ms();
-  TRY(apply_prepare2(P, S[0], c.u_rows, S[2], c.v_rows, false));
+  planners.join();
+  TRY(apply_upload(P, S[0]));
+  TRY(apply_upload(P, S[2]));
   const double tE = now_ms();
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   const double tF = now_ms();
@@ -1471,7 +1622,9 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   TRY(stream_wait(P, 0, P->st, P->st2));  // uploads of the first applies, W buffers
   TRY(ev_record(P, 16, P->st));           // apply phase start (both sides)
   TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
-  TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, P->st2, 1));
+  const bool one_stream = std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
+  cudaStream_t stv = one_stream ? P->st : P->st2;
+  TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
   TRY(apply_prepare2(P, S[1], c.u_rows, S[3], c.v_rows, true));
   for (int e : {1, 3}) {
     const int side = e / 2;
@@ -1491,7 +1644,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   }
   TRY(stream_wait(P, 1, P->st, P->st2));  // uploads of the V-side second apply
   TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
-  TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, P->st2, 1));
+  TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, stv, 1));
   if (nrot > 0 && c.v_rows > 0)
     TRY(col_rotate(c.v_rows, V, ldv, nrot, static_cast<int32_t*>(P->d_rot_goff.p),
                    static_cast<int32_t*>(P->d_rot_cols.p), static_cast<double*>(P->d_rot_mats.p),
@@ -1580,7 +1733,7 @@ svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k, co
     mu[j] = dh[k[j]] + tau[j];
   }
   FmmHost F;
-  fmm_build_host(F, int(n), leaf, p, dh, mu, nullptr);
+  fmm_build_host(F, int(n), leaf, p, dh, mu, nullptr, n);
   int64_t nonempty = 0, max_leaf = 0;
   for (int c = 0; c < F.ncells; ++c) nonempty += F.cells[c].hi > F.cells[c].lo;
   for (int i = 0; i < (1 << F.L); ++i) {

@@ -139,4 +139,5 @@ svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* term
                           double* psi, int64_t ldE, cudaStream_t st, int64_t* launches);
 constexpr int64_t kOpsPad = 16 * 64;
 
+
 }  // namespace svd1

@@ -22,7 +22,9 @@ def test_flops_per_point_bounded(kind, rho):
     k, tau = _roots(d, z, rho)
     st = fmm_tree_stats(d, k, tau, 1e-10)
     assert st["max_leaf"] <= 33
-    assert st["max_near"] <= 24
+    # the planner picks the depth by estimated cost (flops + launches), so one leaf
+    # next to an isolated outlier root may keep a long near list
+    assert st["max_near"] <= 40
     assert st["flops_per_row"] / n <= 700, st      # direct product: 2n = 4096 per point
 
 

@@ -38,3 +38,21 @@ kk, tau = kk.cpu().numpy(), tau.cpu().numpy()
 if True:
     np.savez(os.path.join(ROOT, "gpurun_out", f"spectrum_c{cfg_id}.npz"), d=d, z=z, rho=rho, k=kk, tau=tau)
     print("saved spectrum", d.shape)
+
+# per-pass device times of one update, sides serialized on one stream (diagnostics)
+for env in ({"SVD1_NO_CHAIN": "1"}, {}):
+    for k in ("SVD1_NO_CHAIN",):
+        os.environ.pop(k, None)
+    os.environ.update(env)
+    os.environ["SVD1_ONE_STREAM"] = "1"
+    os.environ["SVD1_PASSTIME"] = "1"
+    os.environ.pop("SVD1_PASSSTATS", None)
+    os.environ.pop("SVD1_TIMING", None)
+    print("--- passtime", env, file=sys.stderr, flush=True)
+    a, b = inp["ab"][nup % len(inp["ab"])]
+    U2, s2, V2 = U.clone(), s.clone(), V.clone()
+    rep = plan.update(U2, s2, V2, torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev))
+    torch.cuda.synchronize()
+    print("apply_ms", rep["apply_ms"], file=sys.stderr)
+for k in ("SVD1_ONE_STREAM", "SVD1_PASSTIME", "SVD1_NO_CHAIN"):
+    os.environ.pop(k, None)
