@@ -83,13 +83,17 @@ typedef struct {
   int64_t kernel_launches; /* CUDA kernels launched by this call */
   double apply_ms[4];    /* device time of each Cauchy apply (CUDA events on the plan
                             stream; Householder + apply + passthrough) */
-  double apply_flops[4]; /* algorithmic flops of each apply: FMM 2*rows*sum(K*N) over the
-                            plan's P2M/M2M/M2L/L2L/L2P/P2P terms; direct 2*rows*n_a^2 */
+  double apply_flops[4]; /* algorithmic flops of each apply: FMM 2*rows*
+                            sum(K*N) over level-by-level P2M/M2M/M2L/L2L/L2P/P2P terms;
+                            direct 2*rows*n_a^2 */
   double spectral_ms[4]; /* device time of secular + Loewner + norms per eigen-update */
   int32_t fmm_levels[4]; /* tree depth L of each FMM apply (0 if direct) */
   int32_t fmm_max_near[4]; /* largest near-field list (leaves) of each FMM apply */
   double mean_iter[4];   /* mean secular evaluations per root (incl. the midpoint one) */
   int32_t pair_rotations; /* repeated-sigma clusters paired by a k x k rotation (D5) */
+  double apply_flops_exec[4]; /* flops each apply executes: as apply_flops, except that the
+                            coarse M2M / L2L levels run in bands, which
+                            trade a few flops for fewer launches */
 } svd1_report;
 
 /* Plan: owns workspaces on the device (sized for u_rows x m and v_rows x n),
@@ -158,9 +162,10 @@ svd1_status svd1_colnorms(svd1_plan_t plan, int64_t n, const double* d,
 
 /* Host-only introspection of the FMM plan the apply would build for the sorted
  * sources d and roots mu_j = d[k_j] + tau_j (HOST pointers; no GPU needed).
- * stats_out (8 int64): [0] tree depth L, [1] non-empty cells, [2] largest leaf,
+ * stats_out (9 int64): [0] tree depth L, [1] non-empty cells, [2] largest leaf,
  * [3] largest near list (leaves), [4] near pairs, [5] M2L pairs,
- * [6] algorithmic flops per row of U (2 * sum K*N), [7] GEMM tasks. */
+ * [6] algorithmic flops per row of U (2 * sum K*N, level by level), [7] GEMM tasks,
+ * [8] flops per row the plan executes (coarse levels in bands). */
 svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k,
                                 const double* tau, double eps, int64_t* stats_out);
 

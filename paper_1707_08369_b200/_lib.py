@@ -32,7 +32,7 @@ class Report(C.Structure):
                 ("sign_flips", i32), ("noop", i32), ("kernel_launches", i64),
                 ("apply_ms", dbl * 4), ("apply_flops", dbl * 4), ("spectral_ms", dbl * 4),
                 ("fmm_levels", i32 * 4), ("fmm_max_near", i32 * 4), ("mean_iter", dbl * 4),
-                ("pair_rotations", i32)]
+                ("pair_rotations", i32), ("apply_flops_exec", dbl * 4)]
 
     def as_dict(self):
         return dict(t_ms=list(self.t_ms)[:6], n_active=list(self.n_active),
@@ -42,7 +42,8 @@ class Report(C.Structure):
                     kernel_launches=self.kernel_launches, apply_ms=list(self.apply_ms),
                     apply_flops=list(self.apply_flops), spectral_ms=list(self.spectral_ms),
                     fmm_levels=list(self.fmm_levels), fmm_max_near=list(self.fmm_max_near),
-                    mean_iter=list(self.mean_iter), pair_rotations=self.pair_rotations)
+                    mean_iter=list(self.mean_iter), pair_rotations=self.pair_rotations,
+                    apply_flops_exec=list(self.apply_flops_exec))
 
 
 def _sig(name, args):
@@ -86,15 +87,16 @@ def version() -> str:
 
 
 def fmm_tree_stats(d, k, tau, eps=1e-10):
-    """Host-only FMM plan statistics (numpy inputs): dict of the 8 stats of svd1.h."""
+    """Host-only FMM plan statistics (numpy inputs): dict of the 9 stats of svd1.h."""
     import numpy as np
     d = np.ascontiguousarray(d, dtype=np.float64)
     k = np.ascontiguousarray(k, dtype=np.int32)
     tau = np.ascontiguousarray(tau, dtype=np.float64)
-    out = np.zeros(8, dtype=np.int64)
+    out = np.zeros(9, dtype=np.int64)
     code = svd1_fmm_tree_stats(d.size, d.ctypes.data, k.ctypes.data, tau.ctypes.data, float(eps),
                                out.ctypes.data)
     if code:
         raise RuntimeError(status_string(code))
-    keys = ["L", "cells", "max_leaf", "max_near", "near_pairs", "m2l_pairs", "flops_per_row", "tasks"]
+    keys = ["L", "cells", "max_leaf", "max_near", "near_pairs", "m2l_pairs", "flops_per_row", "tasks",
+            "flops_exec_per_row"]
     return dict(zip(keys, (int(x) for x in out)))

@@ -91,7 +91,8 @@ struct FmmHost {
   std::vector<int> pass_begin;  // task index where each pass starts (+ end sentinel)
   std::vector<int> pass_bn;     // tile width (16 or 32) of each pass
   int64_t ops_elems = 0;
-  int64_t flops_per_row = 0;    // algorithmic flops per row of U (2 * sum K*N over terms)
+  int64_t flops_per_row = 0;    // algorithmic flops per row (level by level)
+  int64_t flops_exec_per_row = 0;  // flops the plan executes per row (level bands included)
   int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
 };
 
@@ -100,7 +101,8 @@ struct CauchyPrep {
   int p = 16;
   int na = 0;
   int64_t rows = 0;
-  double flops = 0.0;
+  double flops = 0.0;       // algorithmic
+  double flops_exec = 0.0;  // executed by the plan
   FmmHost F;
   std::vector<int32_t> col2src;  // input column -> active source (-1: none); empty = identity
   DevBuf d_cells, d_descs, d_terms, d_tasks, d_ops, d_col2src;
@@ -436,8 +438,9 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     t.op_ld = op_ld;
     t.op_off = off;
     F.terms.push_back(t);
-    F.flops_per_row += 2ll * kreal * N;
+    F.flops_exec_per_row += 2ll * kreal * N;
   };
+  int64_t adj = 0;  // level-by-level M2M / L2L flops minus the banded ones
   // sources [s_lo, s_hi) (a contiguous range of the sorted active sources) read through
   // their physical input columns src[s]: windows of nearby columns (gaps <= 8 are
   // bridged by zero op rows), each window starting at an even column
@@ -576,6 +579,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
           const int d0 = first_desc(c, f - l);
           for (int q = 0; q < (1 << (f - l)); ++q)
             if (has_src(d0 + q)) ds.push_back(d0 + q);
+          adj += 2ll * p * p * (has_src(2 * c + 1) + has_src(2 * c + 2) - int(ds.size()));
           begin_task();
           add_runs(ds, IO_PHI, OP_M2M, c, p);
           end_task(IO_PHI, c * p, p);
@@ -645,6 +649,11 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
             Acell[nA] = A;
             Akind[nA++] = loc[A];
           }
+          {  // level by level: Psi_y = Psi_y I + full(parent) S when the parent has one
+            const int par = (y - 1) / 2;
+            if (loc[par] >= 0) adj += 2ll * p * p * ((m2l[y].empty() ? 0 : 1) + 1);
+            if (!(nA == 0 || (nA == 1 && Acell[0] == y))) adj -= 2ll * p * p * nA;
+          }
           if (nA == 0 || (nA == 1 && Acell[0] == y)) {  // nothing to accumulate
             loc[y] = nA ? IO_PSI : -1;
             continue;
@@ -703,6 +712,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   }
   F.pass_begin.push_back(int(F.tasks.size()));
   for (int& bn : F.pass_bn) bn = bn <= 16 ? 16 : 32;
+  F.flops_per_row = F.flops_exec_per_row + adj;
   if (std::getenv("SVD1_DEBUG"))
     fprintf(stderr, "[svd1] lists: traversal %.3f ms, generation %.3f ms (ops %zu terms %zu tasks %zu)\n",
             tt1 - tt0, now_ms() - tt1, F.ops.size(), F.terms.size(), F.tasks.size());
@@ -742,7 +752,11 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
     if (std::getenv("SVD1_DEBUG"))
       fprintf(stderr, "[svd1] fmm L=%d flops/row=%lld max_near=%d m2l=%d near=%d lists %.3f ms\n", L,
               (long long)F2.flops_per_row, F2.max_near, F2.n_m2l_pairs, F2.n_near_pairs, now_ms() - tl0);
-    if (!have || F2.flops_per_row < best.flops_per_row) {
+    // cost: executed flops plus one launch-equivalent per pass
+    auto cost = [rows](const FmmHost& H) {
+      return double(H.flops_exec_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
+    };
+    if (!have || cost(F2) < cost(best)) {
       best = std::move(F2);
       have = true;
     }
@@ -776,10 +790,11 @@ void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
   C.p = p;
   C.na = na;
   C.rows = rows;
-  C.flops = 2.0 * double(rows) * double(na) * double(na);
+  C.flops = C.flops_exec = 2.0 * double(rows) * double(na) * double(na);
   if (!fmm) return;
   fmm_build_host(C.F, na, leaf, p, da, mu, src, rows);
   C.flops = double(C.F.flops_per_row) * double(rows);
+  C.flops_exec = double(C.F.flops_exec_per_row) * double(rows);
   C.col2src.clear();
   if (src) {
     C.col2src.assign(size_t(n_in), -1);
@@ -1661,6 +1676,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     const bool has = S[e].rows > 0;
     R.apply_ms[e] = has ? ev_ms(P, 2 * e, 2 * e + 1) : 0.0;
     R.apply_flops[e] = (has && S[e].na > 0) ? S[e].cp.flops : 0.0;
+    R.apply_flops_exec[e] = (has && S[e].na > 0) ? S[e].cp.flops_exec : 0.0;
     R.fmm_used[e] = (has && S[e].na > 0) ? S[e].cp.fmm : 0;
     if (R.fmm_used[e]) {
       R.fmm_levels[e] = S[e].cp.F.L;
@@ -1747,6 +1763,7 @@ svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k, co
   st[4] = F.n_near_pairs;
   st[5] = F.n_m2l_pairs;
   st[6] = F.flops_per_row;
+  st[8] = F.flops_exec_per_row;
   st[7] = int64_t(F.tasks.size());
   return SVD1_OK;
 }
