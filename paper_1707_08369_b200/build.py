@@ -12,6 +12,9 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
+FLAGS += os.environ.get("SVD1_NVCC_EXTRA", "").split()  # e.g. -DSVD1_BOUNDS (debug checks)
+
+
 def build(verbose=False, force=False):
     srcs = [os.path.join(SRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(SRC, "svd1_internal.cuh"),

@@ -8,6 +8,8 @@
 // FP64 tensor work uses mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4): tcgen05 has no fp64 kind.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "svd1_internal.cuh"
 
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
                                                      const double* __restrict__ zhat,
                                                      const double* __restrict__ cs,
                                                      const int32_t* __restrict__ col2src,
-                                                     double* __restrict__ ops) {
+                                                     double* __restrict__ ops, int64_t ops_elems) {
   __shared__ double t[kMaxP], w[kMaxP];
   if (threadIdx.x < p) {
     const double th = (2.0 * threadIdx.x + 1.0) / (2.0 * p);  // in units of pi
@@ -215,7 +217,6 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
   __syncthreads();
   for (int o = blockIdx.x; o < n_ops; o += gridDim.x) {
     const FmmOpDesc D = descs[o];
-    double* out = ops + D.off;
     const int total = D.rows * D.cols;
     for (int e = threadIdx.x; e < total; e += blockDim.x) {
       const int i = e / D.cols, j = e % D.cols;
@@ -279,7 +280,17 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
           break;
         }
       }
-      out[int64_t(i) * D.ld + j] = v;
+      // chunk-transposed layout of the term's op: chunk (kb + i) / 16 is an [npad][16]
+      // block (n-major, 16 k contiguous), the GEMM's B tile as TMA reads it
+      const int kk = D.kb + i;
+#ifdef SVD1_BOUNDS
+      if ((D.op_row + int64_t(kk >> 4) * D.npad + j) * 16 + (kk & 15) >= ops_elems || j >= D.npad) {
+        printf("[svd1 bounds] ops desc %d kind %d row %lld kb %d rows %d cols %d npad %d\n", o, D.kind,
+               (long long)D.op_row, D.kb, D.rows, D.cols, D.npad);
+        __trap();
+      }
+#endif
+      ops[(D.op_row + int64_t(kk >> 4) * D.npad + j) * 16 + (kk & 15)] = v;
     }
   }
 }
@@ -287,205 +298,209 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
 // ------------------------------------------------------------------- K6-K10
 // One FMM pass = a batch of "gathered small GEMMs": for task T and every row,
 //   out[r, T.col0 : T.col0 + N] = sum_t in_t[r, col0_t : col0_t + K_t] * op_t (K_t x N).
-// in = U (physical column windows resolved on the host, so no column map is read here)
-// or the expansion matrices Phi/Psi; out = U (through dst[]) or Phi/Psi.
-// Persistent CTAs walk the pass's tiles (task, block of BM rows) with stride gridDim.x;
-// the host orders tasks by decreasing K, so the longest tiles start first.  One
-// continuous STAGES-deep cp.async ring runs across term, chunk and tile boundaries, so
-// a tile's first loads are in flight while the previous tile finishes.  K tails (terms
-// are not multiples of KC) are masked per 4-wide k-step; A reads past the term stay
-// inside the row (columns clamped to ld - 2) and B reads past the op inside the padded
-// ops buffer, and both only ever meet masked k-steps.  Each warp owns a 32 x BN tile
-// (4 x BN/8 DMMA m8n8k4 fragments); 4 warps -> BM = 128 rows per tile.
-constexpr int KC = 16;
-constexpr int ALD = KC + 4;  // 20 doubles: conflict-free A fragment loads
+// in = U (physical column windows resolved on the host) or the expansion matrices
+// Phi/Psi; out = U (through dst[]) or Phi/Psi.
+//
+// Warp-specialised persistent kernel.  One producer warp walks the CTA's tiles (task,
+// block of BM rows; stride gridDim.x; tasks ordered longest first by the host) and, per
+// 16-wide K chunk, fills one slot of a STAGES-deep ring: the A tile (BM rows x 16
+// columns of U / Phi / Psi) by one TMA load (rows past `rows` and columns past the
+// matrix arrive as zeros), the B tile (the op chunk, stored transposed as [n][16 k]) by
+// cp.async from the warp's 32 lanes; both land 128B-swizzled.  CW consumer warps (32 rows each) wait on the stage's full mbarrier,
+// read their fragments with conflict-free 16-byte loads, run the DMMAs and release the
+// stage on its empty mbarrier -- no CTA barrier and no address arithmetic in the math
+// loop.  Within a chunk, lane t4 carries k = 4 t4 + q in k-step q (the same permutation
+// for A and B, so the sum over k is unchanged), which makes each lane's four A (and
+// B) values for the chunk one contiguous 32-byte run.  Op chunks are zero past K, so
+// the A columns of a chunk that fall outside the term only ever meet zeros.
+constexpr int KC = 16;  // chunk (k) width: one 128-byte swizzle row of doubles
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ double2 lds128(const unsigned char* p) {
+  return *reinterpret_cast<const double2*>(p);
+}
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int NWARP = 4;
-  static constexpr int NTHR = 32 * NWARP;
+  static constexpr int CW = 4;               // consumer warps (32 rows each)
+  static constexpr int NTHR = 32 * (CW + 1); // + one producer warp
   static constexpr int NT = BN / 8;
-  static constexpr int BM = 32 * NWARP;   // rows per tile
-  static constexpr int BLD = BN + 4;      // B row stride (doubles): conflict-free fragments
-  static constexpr int STAGES = 3;        // cp.async ring depth
-  static constexpr int A_ELEMS = BM * ALD;
-  static constexpr int B_ELEMS = KC * BLD;
-  static constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * 8 + STAGES * 16;
+  static constexpr int BM = 32 * CW;
+  static constexpr int STAGES = BN <= 16 ? 6 : 4;
+  static constexpr int A_BYTES = BM * KC * 8;
+  static constexpr int B_BYTES = BN * KC * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STAGES * (16 + 16);
 };
 
-struct StageInfo {   // written by the loader, read by the compute side of the same stage
-  int32_t rem;       // K - k0 of the chunk's term (k-steps beyond it are masked)
-  int32_t tile;      // tile the chunk belongs to
-  int32_t last;      // 1: last chunk of the tile (epilogue after it), -1: no chunk
-  int32_t pad;
+struct StageInfo {
+  int32_t tile;  // tile the chunk belongs to; -1: no more chunks
+  int32_t last;  // 1: last chunk of the tile (epilogue after it)
 };
 
 template <int BN>
 __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
-    const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int ntiles, int nrb,
-    int64_t rows, const double* __restrict__ ops, const double* __restrict__ U_in, int64_t ld_in,
-    double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst,
-    double* __restrict__ phi, double* __restrict__ psi, int64_t ldE) {
+    const FmmMaps* __restrict__ maps, const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int ntiles, int nrb,
+    int64_t rows, double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst,
+    double* __restrict__ phi, double* __restrict__ psi, int64_t ldE, int64_t out_cols, int64_t exp_elems,
+    const double* __restrict__ ops_raw, int64_t ops_rows) {
   using G = GemmCfg<BN>;
-  constexpr int NT = G::NT;
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;                            // [STAGES][BM][ALD]
-  double* Bs = smem + G::STAGES * G::A_ELEMS;   // [STAGES][KC][BLD]
-  StageInfo* info = reinterpret_cast<StageInfo*>(Bs + G::STAGES * G::B_ELEMS);
+  constexpr int NT = G::NT, S = G::STAGES;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // SWIZZLE_128B tiles need 1024-byte aligned shared addresses
+  unsigned char* sbase = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* sA = sbase;                  // [S][BM][16] doubles, swizzled
+  unsigned char* sB = sbase + S * G::A_BYTES; // [S][BN][16] doubles, swizzled
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * G::B_BYTES);
+  uint64_t* empty = full + S;
+  StageInfo* info = reinterpret_cast<StageInfo*>(empty + S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(&full[q], 33);
+      mbar_init(&empty[q], G::CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
-  // ---- loader iterator (uniform across the CTA)
-  int l_tile = blockIdx.x, l_term = 0, l_tend = 0, l_k0 = 0, l_opc0 = 0;
-  int64_t l_row0 = 0;   // first row of the tile
-  bool l_full = true;   // the tile's rows are all < rows (no clamping)
-  FmmTerm R{};
-  auto l_start_tile = [&]() {
-    if (l_tile < ntiles) {
-      const int task = l_tile / nrb;
+  if (warp == G::CW) {  // ---------------- producer warp
+    // A tiles by TMA (lane 0); B tiles (the op chunk, [BN][16] doubles, 2-4 KB) by
+    // cp.async from all 32 lanes into the same 128B-swizzled layout, their completion
+    // tracked by the stage's full barrier (32 noinc arrivals + lane 0's expect_tx).
+    // (A TMA load of the op chunk, written by the operator kernel just before, was
+    // measured to return stale data when another stream's kernels ran concurrently.)
+    const int w = BN == 32 ? 1 : 0;
+    const CUtensorMap* tm_u = &maps->u[w];
+    const CUtensorMap* tm_phi = &maps->phi[w];
+    const CUtensorMap* tm_psi = &maps->psi[w];
+    if (lane == 0)
+      for (const CUtensorMap* m : {tm_u, tm_phi, tm_psi})
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(m) : "memory");
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int task = tile / nrb;
+      const int row0 = (tile - task * nrb) * G::BM;
       const FmmTask T = tasks[task];
-      l_row0 = int64_t(l_tile - task * nrb) * G::BM;
-      l_full = l_row0 + G::BM <= rows;
-      l_term = T.t_begin;
-      l_tend = T.t_end;
-      l_k0 = 0;
-      l_opc0 = T.op_col0;
-      R = terms[l_term];
-    }
-  };
-  l_start_tile();
-  // A: thread -> column pair kp (of KC/2), rows rr0 + 16 i (BM / 16 of them)
-  const int kp = (tid & (KC / 2 - 1)) * 2, rr0 = tid >> 3;
-  auto issue = [&](int buf) {
-    if (tid == 0) info[buf].last = -1;
-    if (l_tile >= ntiles) return;
-    const bool inU = R.in_kind == IO_U;
-    const double* base = inU ? U_in : (R.in_kind == IO_PHI ? phi : psi);
-    const int64_t ld = inU ? ld_in : ldE;
-    double* a = As + buf * G::A_ELEMS + rr0 * ALD + kp;
-    const int cu = R.col0 + l_k0 + kp;
-    if (!(ld & 1)) {  // pairs (c, c+1), c even: in the row whenever c <= ld - 2
-      const int c = min(cu, int(ld - 2));
-      if (l_full) {
-        const double* g = base + (l_row0 + rr0) * ld + c;
-        const int64_t step = 16 * ld;
-#pragma unroll
-        for (int i = 0; i < G::BM / 16; ++i) {
-          cp_async16(a + 16 * i * ALD, g);
-          g += step;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < G::BM / 16; ++i) {
-          const int64_t r = min(l_row0 + rr0 + 16 * i, rows - 1);
-          cp_async16(a + 16 * i * ALD, base + r * ld + c);
+      for (int t = T.t_begin; t < T.t_end; ++t) {
+        const FmmTerm R = terms[t];
+        const CUtensorMap* ma = R.in_kind == IO_U ? tm_u : (R.in_kind == IO_PHI ? tm_phi : tm_psi);
+        for (int k0 = 0; k0 < R.K; k0 += KC) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const int64_t brow = R.op_row + int64_t(k0 / KC) * R.npad + T.op_col0;
+          const double* bsrc = ops_raw + brow * 16;
+          unsigned char* bdst = sB + stage * G::B_BYTES;
+          for (int q = lane; q < BN * 8; q += 32) {
+            const int n = q >> 3, j = q & 7;
+            const int64_t row = brow + n;
+            const bool ok = row < ops_rows;
+            const unsigned sa = smem_u32(bdst + n * 128 + ((j ^ (n & 7)) << 4));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                         "l"(bsrc + (ok ? n * 16 + 2 * j : 0)), "r"(ok ? 16 : 0));
+          }
+          if (lane == 0) {
+            info[stage] = StageInfo{tile, (t == T.t_end - 1 && k0 + KC >= R.K) ? 1 : 0};
+            mbar_arrive_tx(&full[stage], G::A_BYTES);
+            tma_load_2d(sA + stage * G::A_BYTES, ma, R.col0 + k0, row0, &full[stage]);
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[stage])) : "memory");
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
-    } else {  // odd leading dimension: rows are not 16-byte aligned; clamp per column
-      const int c0 = min(cu, int(ld - 1)), c1 = min(cu + 1, int(ld - 1));
-#pragma unroll
-      for (int i = 0; i < G::BM / 16; ++i) {
-        const int64_t r = min(l_row0 + rr0 + 16 * i, rows - 1);
-        cp_async8(a + 16 * i * ALD, base + r * ld + c0);
-        cp_async8(a + 16 * i * ALD + 1, base + r * ld + c1);
-      }
     }
-    // B: KC x BN block of the op (row stride op_ld even, 16-byte aligned rows)
-    double* b = Bs + buf * G::B_ELEMS;
-    const double* bsrc = ops + R.op_off + int64_t(l_k0) * R.op_ld + l_opc0;
-#pragma unroll
-    for (int e = tid; e < KC * BN / 2; e += G::NTHR) {
-      const int kk = e / (BN / 2), jj = (e % (BN / 2)) * 2;
-      cp_async16(b + kk * G::BLD + jj, bsrc + kk * R.op_ld + jj);
-    }
-    const int rem = R.K - l_k0;
-    // advance
-    l_k0 += KC;
-    int last = 0;
-    const int tile = l_tile;
-    if (l_k0 >= R.K) {
-      l_k0 = 0;
-      if (++l_term == l_tend) {
-        last = 1;
-        l_tile += gridDim.x;
-        l_start_tile();
-      } else {
-        R = terms[l_term];
-      }
-    }
-    if (tid == 0) info[buf] = StageInfo{rem, tile, last, 0};
-  };
-
+    mbar_wait(&empty[stage], phase ^ 1);
+    if (lane == 0) info[stage] = StageInfo{-1, -1};
+    __syncwarp();
+    mbar_arrive(&full[stage]);
+    if (lane == 0) mbar_arrive(&full[stage]);  // 33 arrivals per phase
+    return;
+  }
+  // ------------------------------------ consumers: warp owns rows warp*32 .. +31
+  const int g = lane >> 2, t4 = lane & 3;
+  // byte offsets (within a stage) of this lane's 16-byte fragment runs: row r, k pair j
+  // sits at r*128 + ((j ^ (r & 7)) << 4) (TMA SWIZZLE_128B); r & 7 == g for every row
+  // this lane reads (fragment rows are 8-aligned)
+  const int sw0 = ((2 * t4) ^ g) << 4, sw1 = ((2 * t4 + 1) ^ g) << 4;
+  const int a_row = (warp * 32 + g) * 128;
+  const int b_row = g * 128;
   double acc[4][NT][2];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-
-#pragma unroll
-  for (int q = 0; q < G::STAGES - 1; ++q) {
-    issue(q);
-    cp_async_commit();
-  }
-  const int a_off = (warp * 32 + (lane >> 2)) * ALD + (lane & 3);
-  const int b_off = (lane & 3) * G::BLD + (lane >> 2);
-  for (int it = 0;; ++it) {
-    const int buf = it % G::STAGES;
-    issue((it + G::STAGES - 1) % G::STAGES);
-    cp_async_commit();
-    cp_async_wait<G::STAGES - 1>();
-    __syncthreads();
-    const StageInfo I = info[buf];
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    mbar_wait(&full[stage], phase);
+    const StageInfo I = info[stage];
     if (I.last < 0) break;
-    const double* a = As + buf * G::A_ELEMS + a_off;
-    const double* b = Bs + buf * G::B_ELEMS + b_off;
-    // fragments double-buffered in registers: k-step kk+1 loads while kk multiplies
-    double af[2][4], bf[2][NT];
+    const unsigned char* a = sA + stage * G::A_BYTES + a_row;
+    const unsigned char* b = sB + stage * G::B_BYTES + b_row;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) af[0][mt] = a[mt * 8 * ALD];
+    for (int h = 0; h < 2; ++h) {  // k-steps q = 2h, 2h + 1
+      const int sw = h ? sw1 : sw0;
+      double2 af[4], bf[NT];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) bf[0][nt] = b[nt * 8];
+      for (int mt = 0; mt < 4; ++mt) af[mt] = lds128(a + mt * 8 * 128 + sw);
 #pragma unroll
-    for (int q = 0; q < KC / 4; ++q) {
-      const int kk = 4 * q, cur = q & 1;
-      if (kk >= I.rem) break;
-      if (q + 1 < KC / 4) {
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) af[cur ^ 1][mt] = a[mt * 8 * ALD + kk + 4];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) bf[cur ^ 1][nt] = b[(kk + 4) * G::BLD + nt * 8];
-      }
-      if (kk + 4 > I.rem) {  // ragged K tail: zero both operands of the missing k
-        const bool ok = kk + (lane & 3) < I.rem;
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) af[cur][mt] = ok ? af[cur][mt] : 0.0;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) bf[cur][nt] = ok ? bf[cur][nt] : 0.0;
-      }
+      for (int nt = 0; nt < NT; ++nt) bf[nt] = lds128(b + nt * 8 * 128 + sw);
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt], bf[cur][nt]);
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma_8x8x4(acc[mt][nt], af[mt].x, bf[nt].x);
+          dmma_8x8x4(acc[mt][nt], af[mt].y, bf[nt].y);
+        }
     }
-    __syncthreads();  // buffer `buf` is refilled by a later prefetch
-    if (I.last) {     // epilogue of tile I.tile (registers -> global only)
-      const FmmTask T = tasks[I.tile / nrb];
-      const int64_t row0 = int64_t(I.tile % nrb) * G::BM;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1;
+    }
+    if (I.last) {  // epilogue of tile I.tile (registers -> global)
+      const int task = I.tile / nrb;
+      const int64_t row0 = int64_t(I.tile - task * nrb) * G::BM;
+      const FmmTask T = tasks[task];
       double* E = T.out_kind == IO_PHI ? phi : psi;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const int jj = nt * 8 + (lane & 3) * 2;
+        const int jj = nt * 8 + 2 * t4;
         if (jj >= T.N) continue;
         const int col = T.col0 + jj;
         if (T.out_kind == IO_U) {
@@ -493,16 +508,30 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
           const int c1 = (jj + 1 < T.N) ? (dst ? dst[col + 1] : col + 1) : -1;
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) {
-            const int64_t r = row0 + warp * 32 + mt * 8 + (lane >> 2);
+            const int64_t r = row0 + warp * 32 + mt * 8 + g;
             if (r >= rows) continue;
+#ifdef SVD1_BOUNDS
+            if (c0 < 0 || c0 >= out_cols || c1 >= out_cols) {
+              printf("[svd1 bounds] U_out col %d/%d of %lld (task %d N %d col %d)\n", c0, c1, (long long)out_cols,
+                     task, T.N, col);
+              __trap();
+            }
+#endif
             U_out[r * ld_out + c0] = acc[mt][nt][0];
             if (c1 >= 0) U_out[r * ld_out + c1] = acc[mt][nt][1];
           }
         } else {  // expansions: N is a multiple of 4, col0 even -> 16-byte stores
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) {
-            const int64_t r = row0 + warp * 32 + mt * 8 + (lane >> 2);
+            const int64_t r = row0 + warp * 32 + mt * 8 + g;
             if (r >= rows) continue;
+#ifdef SVD1_BOUNDS
+            if (col + 1 >= ldE || r * ldE + col + 1 >= exp_elems) {
+              printf("[svd1 bounds] expansion col %d ldE %lld r %lld elems %lld\n", col, (long long)ldE,
+                     (long long)r, (long long)exp_elems);
+              __trap();
+            }
+#endif
             *reinterpret_cast<double2*>(E + r * ldE + col) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
           }
         }
@@ -568,20 +597,50 @@ svd1_status passthrough(int64_t rows, int nq, const double* U_in, int64_t ld_in,
 svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cells, int p,
                           const double* d, const int32_t* k, const double* tau,
                           const double* zhat, const double* cs, const int32_t* col2src,
-                          double* ops, cudaStream_t st, int64_t* launches) {
+                          double* ops, int64_t ops_elems, cudaStream_t st, int64_t* launches) {
   if (n_ops <= 0) return SVD1_OK;
   const unsigned g = unsigned(std::min(n_ops, 148 * 16));
-  fmm_ops_kernel<<<g, 256, 0, st>>>(n_ops, descs, cells, p, d, k, tau, zhat, cs, col2src, ops);
+  fmm_ops_kernel<<<g, 256, 0, st>>>(n_ops, descs, cells, p, d, k, tau, zhat, cs, col2src, ops, ops_elems);
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }
 
+// ---- TMA descriptors (driver entry point through the runtime: no -lcuda)
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+svd1_status make_tmap(CUtensorMap* map, const double* base, int64_t inner, int64_t outer,
+                      int64_t ld, int box_inner, int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return SVD1_E_CUDA;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld & 1) || inner < 1 || outer < 1) return SVD1_E_INVALID;
+  const cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
+  const cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? SVD1_OK : SVD1_E_INVALID;
+}
+
 template <int BN>
 svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
-                        const double* ops, const double* U_in, int64_t ld_in, double* U_out,
-                        int64_t ld_out, const int32_t* dst, double* phi, double* psi, int64_t ldE,
-                        cudaStream_t st) {
+                        const FmmMaps* maps, double* U_out, int64_t ld_out, const int32_t* dst,
+                        double* phi, double* psi, int64_t ldE, int64_t out_cols, int64_t exp_elems,
+                        const double* ops_raw, int64_t ops_rows, cudaStream_t st) {
   using G = GemmCfg<BN>;
   static int max_ctas = 0;  // resident CTAs on the whole device (persistent grid)
   if (!max_ctas) {
@@ -594,22 +653,38 @@ svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms,
   }
   const int64_t nrb = (rows + G::BM - 1) / G::BM;
   const int64_t ntiles = nrb * n_tasks;
-  if (ntiles > (int64_t(1) << 30)) return SVD1_E_INVALID;
-  const int grid = int(std::min<int64_t>(ntiles, max_ctas));
-  fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(tasks, terms, int(ntiles), int(nrb), rows, ops, U_in,
-                                                       ld_in, U_out, ld_out, dst, phi, psi, ldE);
+  if (ntiles > (int64_t(1) << 30) || rows > (int64_t(1) << 30)) return SVD1_E_INVALID;
+  int cap = max_ctas;
+  if (const char* e = std::getenv("SVD1_GEMM_CTAS")) cap = std::max(1, atoi(e));  // diagnostics
+  const int grid = int(std::min<int64_t>(ntiles, cap));
+  fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(maps, tasks, terms, int(ntiles), int(nrb), rows, U_out,
+                                                       ld_out, dst, phi, psi, ldE, out_cols, exp_elems,
+                                                       ops_raw, ops_rows);
+  return SVD1_OK;
+}
+
+svd1_status fmm_make_maps(FmmMaps* m, int64_t rows, const double* U_in, int64_t ncols_in, int64_t ld_in,
+                          const double* phi, const double* psi, int64_t ldE) {
+  for (int w = 0; w < 2; ++w) {
+    const int bm = w ? GemmCfg<32>::BM : GemmCfg<16>::BM;
+    svd1_status s = make_tmap(&m->u[w], U_in, ncols_in, rows, ld_in, KC, bm);
+    if (s != SVD1_OK) return s;
+    if ((s = make_tmap(&m->phi[w], phi, ldE, rows, ldE, KC, bm)) != SVD1_OK) return s;
+    if ((s = make_tmap(&m->psi[w], psi, ldE, rows, ldE, KC, bm)) != SVD1_OK) return s;
+  }
   return SVD1_OK;
 }
 
 svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
-                          int64_t rows, const double* ops, const double* U_in, int64_t ld_in,
-                          double* U_out, int64_t ld_out, const int32_t* dst, double* phi,
-                          double* psi, int64_t ldE, cudaStream_t st, int64_t* launches) {
+                          int64_t rows, const FmmMaps* maps, double* U_out, int64_t ld_out,
+                          const int32_t* dst, double* phi, double* psi, int64_t ldE, int64_t out_cols,
+                          int64_t exp_elems, const double* ops_raw, int64_t ops_rows, cudaStream_t st,
+                          int64_t* launches) {
   if (n_tasks <= 0 || rows <= 0) return SVD1_OK;
-  svd1_status s = bn <= 16 ? launch_gemm<16>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, U_out, ld_out,
-                                             dst, phi, psi, ldE, st)
-                           : launch_gemm<32>(n_tasks, tasks, terms, rows, ops, U_in, ld_in, U_out, ld_out,
-                                             dst, phi, psi, ldE, st);
+  svd1_status s = bn <= 16 ? launch_gemm<16>(n_tasks, tasks, terms, rows, maps, U_out, ld_out, dst, phi, psi,
+                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, st)
+                           : launch_gemm<32>(n_tasks, tasks, terms, rows, maps, U_out, ld_out, dst, phi, psi,
+                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, st);
   if (s != SVD1_OK) return s;
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());

@@ -90,7 +90,7 @@ struct FmmHost {
   std::vector<FmmTask> tasks;
   std::vector<int> pass_begin;  // task index where each pass starts (+ end sentinel)
   std::vector<int> pass_bn;     // tile width (16 or 32) of each pass
-  int64_t ops_elems = 0;
+  int64_t ops_rows = 0;         // ops buffer: rows of 16 doubles
   int64_t flops_per_row = 0;    // algorithmic flops per row (level by level)
   int64_t flops_exec_per_row = 0;  // flops the plan executes per row (level bands included)
   int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
@@ -105,7 +105,13 @@ struct CauchyPrep {
   double flops_exec = 0.0;  // executed by the plan
   FmmHost F;
   std::vector<int32_t> col2src;  // input column -> active source (-1: none); empty = identity
-  DevBuf d_cells, d_descs, d_terms, d_tasks, d_ops, d_col2src;
+  int n_in = 0;                  // columns of the input buffer
+  int n_out = 0;                 // columns of the output buffer
+  DevBuf d_cells, d_descs, d_terms, d_tasks, d_ops, d_col2src, d_maps;
+  FmmMaps* h_maps = nullptr;  // pinned staging of the TMA descriptors (copied on the apply stream)
+  ~CauchyPrep() {
+    if (h_maps) cudaFreeHost(h_maps);
+  }
 };
 
 // Everything one RankOneUpdate (Alg 6.2) needs at apply time.
@@ -165,6 +171,7 @@ struct svd1_plan_s {
   DevBuf W_u, W_v, proj, partial, status, iters, ops, fmm_cells, fmm_descs, fmm_terms,
       fmm_tasks, scratch_i, scratch_d;
   DevBuf phi[2], psi[2];         // FMM expansions per side (U applies, V applies)
+  DevBuf upad[2];                // even-ld copy of an apply input TMA cannot read in place
   DevBuf probes;                 // 4 x u_rows sign probes
   bool probes_ready = false;
   cudaStream_t st2 = nullptr;    // V-side applies run here, concurrently with the U side
@@ -412,38 +419,39 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     std::sort(m2l[c].begin(), m2l[c].end());
   }
   const double tt1 = now_ms();
-  // ops: even row stride and even offset (16-byte aligned rows for the GEMM's B copies)
-  auto add_op = [&](int kind, int a, int b, int rows, int cols) {
+  // A term's op (K x N) is stored chunk-transposed (FmmTerm): new_term reserves its
+  // ceil(K/16) chunks of [npad][16] doubles; add_op adds a block of its rows.
+  // kreal: rows that carry work (window rows of absent sources are zero): flop count
+  auto new_term = [&](int in_kind, int col0, int K, int N, int kreal) {
+    FmmTerm t;
+    t.in_kind = in_kind;
+    t.col0 = col0;
+    t.K = K;
+    t.npad = (N + 15) & ~15;
+    t.op_row = F.ops_rows;
+    F.ops_rows += int64_t((K + 15) / 16) * t.npad;
+    F.terms.push_back(t);
+    F.flops_exec_per_row += 2ll * kreal * N;
+  };
+  auto add_op = [&](int kind, int a, int b, int rows, int cols, int kb) {
+    const FmmTerm& t = F.terms.back();
     FmmOpDesc D;
     D.kind = kind;
     D.a = a;
     D.b = b;
     D.rows = rows;
     D.cols = cols;
-    D.ld = (cols + 1) & ~1;
+    D.kb = kb;
+    D.npad = t.npad;
+    D.op_row = t.op_row;
     D.c0 = 0;
     D.s_hi = 0;
-    F.ops_elems = (F.ops_elems + 1) & ~int64_t(1);
-    D.off = F.ops_elems;
-    F.ops_elems += int64_t(rows) * D.ld;
     F.ops.push_back(D);
-    return D.off;
-  };
-  // kreal: rows that carry work (window rows of absent sources are zero): flop count
-  auto add_term = [&](int in_kind, int col0, int K, int64_t off, int op_ld, int kreal, int N) {
-    FmmTerm t;
-    t.in_kind = in_kind;
-    t.col0 = col0;
-    t.K = K;
-    t.op_ld = op_ld;
-    t.op_off = off;
-    F.terms.push_back(t);
-    F.flops_exec_per_row += 2ll * kreal * N;
   };
   int64_t adj = 0;  // level-by-level M2M / L2L flops minus the banded ones
   // sources [s_lo, s_hi) (a contiguous range of the sorted active sources) read through
   // their physical input columns src[s]: windows of nearby columns (gaps <= 8 are
-  // bridged by zero op rows), each window starting at an even column
+  // bridged by zero op rows), each starting at an even column
   std::vector<int> pc;
   auto add_src = [&](int kind, int s_lo, int s_hi, int b, int N) {
     pc.resize(s_hi - s_lo);
@@ -461,11 +469,13 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     while (a < pc.size()) {
       size_t e = a;
       while (e + 1 < pc.size() && pc[e + 1] - pc[e] <= 8) ++e;
+      // TMA needs 16-byte aligned box starts: windows start at an even column (a
+      // column in front of the term's sources gets a zero op row)
       const int c0 = pc[a] & ~1, len = pc[e] + 1 - c0;
-      const int64_t off = add_op(kind, s_lo, b, len, N);
+      new_term(IO_U, c0, len, N, int(e - a + 1));
+      add_op(kind, s_lo, b, len, N, 0);
       F.ops.back().c0 = c0;
       F.ops.back().s_hi = s_hi;
-      add_term(IO_U, c0, len, off, F.ops.back().ld, int(e - a + 1), N);
       a = e + 1;
     }
   };
@@ -496,15 +506,9 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
         continue;
       }
       while (b + 1 < xs.size() && xs[b + 1] == xs[b] + 1) ++b;
-      int K = 0, ld = 0;
-      int64_t off0 = -1;
-      for (size_t q = a; q <= b; ++q) {
-        const int64_t off = add_op(op_kind, xs[q], y, p, N);
-        if (off0 < 0) off0 = off;
-        ld = F.ops.back().ld;
-        K += p;
-      }
-      add_term(in_kind, xs[a] * p, K, off0, ld, K, N);
+      const int K = int(b - a + 1) * p;
+      new_term(in_kind, xs[a] * p, K, N, K);
+      for (size_t q = a; q <= b; ++q) add_op(op_kind, xs[q], y, p, N, int(q - a) * p);
       a = b + 1;
     }
   };
@@ -660,8 +664,8 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
           }
           begin_task();
           for (int q = 0; q < nA; ++q) {
-            const int64_t off = add_op(Acell[q] == y ? OP_ID : OP_L2L, Acell[q], y, p, p);
-            add_term(Akind[q], Acell[q] * p, p, off, F.ops.back().ld, p, p);
+            new_term(Akind[q], Acell[q] * p, p, p, p);
+            add_op(Acell[q] == y ? OP_ID : OP_L2L, Acell[q], y, p, p, 0);
           }
           end_task(IO_PHI, y * p, p);
           loc[y] = IO_PHI;
@@ -696,12 +700,12 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     begin_task();
     const int par = (y - 1) / 2;
     if (!m2l[y].empty()) {
-      const int64_t off = add_op(OP_L2P, y, y, p, ty);
-      add_term(IO_PSI, y * p, p, off, F.ops.back().ld, p, ty);
+      new_term(IO_PSI, y * p, p, ty, p);
+      add_op(OP_L2P, y, y, p, ty, 0);
     }
     if (par >= 1 && loc[par] >= 0) {
-      const int64_t off = add_op(OP_L2P_FROM, par, y, p, ty);
-      add_term(loc[par], par * p, p, off, F.ops.back().ld, p, ty);
+      new_term(loc[par], par * p, p, ty, p);
+      add_op(OP_L2P_FROM, par, y, p, ty, 0);
     }
     add_runs(near[y], IO_U, OP_P2P, y, ty);
     F.n_near_pairs += int(near[y].size());
@@ -796,6 +800,8 @@ void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
   C.flops = double(C.F.flops_per_row) * double(rows);
   C.flops_exec = double(C.F.flops_exec_per_row) * double(rows);
   C.col2src.clear();
+  C.n_in = n_in;
+  C.n_out = n_in;
   if (src) {
     C.col2src.assign(size_t(n_in), -1);
     for (int i = 0; i < na; ++i) C.col2src[src[i]] = i;
@@ -818,7 +824,7 @@ svd1_status cauchy_upload(svd1_plan_t P, CauchyPrep& C) {
     TRY(upload(P, C.d_col2src, C.col2src, &c2s));
   }
   double* ops;
-  TRY(C.d_ops.get<double>(size_t(F.ops_elems + kOpsPad), &ops));
+  TRY(C.d_ops.get<double>(size_t(std::max<int64_t>(F.ops_rows, 1)) * 16, &ops));
   return SVD1_OK;
 }
 
@@ -853,8 +859,30 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   auto* dk = static_cast<FmmTask*>(C.d_tasks.p);
   auto* ops = static_cast<double*>(C.d_ops.p);
   const int32_t* c2s = C.col2src.empty() ? nullptr : static_cast<int32_t*>(C.d_col2src.p);
-  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, c2s, ops, st,
-                    &P->launches));
+  // op chunks are zero past K and N (the GEMM relies on it)
+  SVD1_CUDA_TRY(cudaMemsetAsync(ops, 0, size_t(std::max<int64_t>(F.ops_rows, 1)) * 16 * sizeof(double), st));
+  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, c2s, ops,
+                    std::max<int64_t>(F.ops_rows, 1) * 16, st, &P->launches));
+  // TMA reads U_in: 16-byte aligned base and even leading dimension, else a padded copy
+  if ((reinterpret_cast<uintptr_t>(U_in) & 15) || (ld_in & 1)) {
+    const int64_t ldp = (C.n_in + 1) & ~int64_t(1);
+    double* pad;
+    TRY(P->upad[side].get<double>(size_t(rows) * size_t(ldp), &pad));
+    SVD1_CUDA_TRY(cudaMemcpy2DAsync(pad, size_t(ldp) * 8, U_in, size_t(ld_in) * 8, size_t(C.n_in) * 8,
+                                    size_t(rows), cudaMemcpyDeviceToDevice, st));
+    U_in = pad;
+    ld_in = ldp;
+  }
+  // descriptors live in global memory (one copy per apply, written on the apply's own
+  // stream; the kernel acquires them through the tensormap proxy before use)
+  if (!C.h_maps && cudaMallocHost(&C.h_maps, sizeof(FmmMaps)) != cudaSuccess) {
+    cudaGetLastError();
+    return SVD1_E_NOMEM;
+  }
+  TRY(fmm_make_maps(C.h_maps, rows, U_in, C.n_in, ld_in, phi, psi, ldE));
+  FmmMaps* maps;
+  TRY(C.d_maps.get<FmmMaps>(1, &maps));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(maps, C.h_maps, sizeof(FmmMaps), cudaMemcpyHostToDevice, st));
   const bool dbg = std::getenv("SVD1_DEBUG") != nullptr;
   if (dbg) {  // host-side validation of the task lists
     for (const FmmTask& T : F.tasks) {
@@ -863,13 +891,14 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
                 T.t_begin, T.t_end);
       for (int t = T.t_begin; t < T.t_end; ++t) {
         const FmmTerm& R = F.terms[t];
-        if (R.K < 1 || R.op_off < 0 || R.op_off + int64_t(R.K - 1) * R.op_ld + T.op_col0 + T.N > F.ops_elems)
-          fprintf(stderr, "[svd1] bad term %d: kind=%d col0=%d K=%d off=%lld\n", t, R.in_kind, R.col0,
-                  R.K, (long long)R.op_off);
+        if (R.K < 1 || R.op_row < 0 || R.op_row + int64_t((R.K + 15) / 16) * R.npad > F.ops_rows ||
+            T.op_col0 + T.N > R.npad)
+          fprintf(stderr, "[svd1] bad term %d: kind=%d col0=%d K=%d row=%lld\n", t, R.in_kind, R.col0,
+                  R.K, (long long)R.op_row);
       }
     }
     fprintf(stderr, "[svd1] fmm na=%d L=%d cells=%d tasks=%zu terms=%zu ops=%lld rows=%lld p=%d\n",
-            C.na, F.L, F.ncells, F.tasks.size(), F.terms.size(), (long long)F.ops_elems,
+            C.na, F.L, F.ncells, F.tasks.size(), F.terms.size(), (long long)F.ops_rows * 16,
             (long long)rows, p);
   }
   if (std::getenv("SVD1_PASSSTATS")) {  // per pass: tasks, algorithmic vs tile-padded flops
@@ -889,6 +918,32 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
       }
       fprintf(stderr, "[svd1] pass %zu bn=%d tasks=%d flops=%.3e padded=%.3e (x%.2f) kmax=%lld\n", s, bn,
               e - b, fa * rows, fp * rows, fa > 0 ? fp / fa : 0.0, (long long)kmax);
+    }
+  }
+  if (std::getenv("SVD1_CHECK_PASSES")) {  // diagnostics: a pass must not read what it writes
+    for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
+      std::vector<char> wphi(ldE, 0), wpsi(ldE, 0), wu(std::max(C.n_in, 1) + 64, 0);
+      for (int t = F.pass_begin[s]; t < F.pass_begin[s + 1]; ++t) {
+        const FmmTask& T = F.tasks[t];
+        for (int j = 0; j < T.N; ++j) {
+          if (T.out_kind == IO_PHI) wphi[T.col0 + j] = 1;
+          if (T.out_kind == IO_PSI) wpsi[T.col0 + j] = 1;
+        }
+      }
+      int bad = 0;
+      for (int t = F.pass_begin[s]; t < F.pass_begin[s + 1]; ++t) {
+        const FmmTask& T = F.tasks[t];
+        for (int u = T.t_begin; u < T.t_end; ++u) {
+          const FmmTerm& R = F.terms[u];
+          const int kend = (R.K + 15) / 16 * 16;
+          for (int k = 0; k < kend; ++k) {
+            const int c = R.col0 + k;
+            if (R.in_kind == IO_PHI && c < ldE && wphi[c]) ++bad;
+            if (R.in_kind == IO_PSI && c < ldE && wpsi[c]) ++bad;
+          }
+        }
+      }
+      if (bad) fprintf(stderr, "[svd1] CHECK pass %zu: %d reads of columns written by the same pass\n", s, bad);
     }
   }
   const bool ptime = std::getenv("SVD1_PASSTIME") != nullptr;  // diagnostics (syncs)
@@ -918,8 +973,8 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   pmark();
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
-    TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, ops, U_in, ld_in, U_out, ld_out, d_dst,
-                      phi, psi, ldE, st, &P->launches));
+    TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, maps, U_out, ld_out, d_dst, phi, psi, ldE,
+                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, st, &P->launches));
     pmark();
     if (dbg) {
       cudaError_t err = cudaStreamSynchronize(st);
@@ -931,9 +986,14 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
 }
 
 svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
-  double* x;
-  TRY(P->phi[side].get<double>(elems, &x));
-  TRY(P->psi[side].get<double>(elems, &x));
+  // zeroed when (re)allocated: a K chunk may reach past a term into columns no pass wrote
+  // (they meet zero op rows, but 0 * NaN would not be 0)
+  for (DevBuf* b : {&P->phi[side], &P->psi[side]}) {
+    void* before = b->p;
+    double* x;
+    TRY(b->get<double>(elems, &x));
+    if (b->p != before) SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, P->st));
+  }
   return SVD1_OK;
 }
 
@@ -1212,7 +1272,7 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
 // Host half of one apply, in two parts: apply_plan (pure host compute, thread-safe per
 // step: column maps and the Cauchy/FMM plan) and apply_upload (staged uploads).
 // out_col(q) = reverse ? (N - 1 - q) : q.
-void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool reverse) {
+void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool reverse, int side) {
   const int N = S.N;
   S.rows = rows;
   auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
@@ -1221,6 +1281,7 @@ void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool
   for (int j = 0; j < S.na; ++j) S.dst_cols[j] = oc(S.tgt_pos[j]);
   S.pass_dst_cols.resize(S.pass_dst.size());
   for (size_t q = 0; q < S.pass_dst.size(); ++q) S.pass_dst_cols[q] = oc(S.pass_dst[q]);
+  (void)side;
   if (S.na > 0) cauchy_plan(cfg, S.cp, rows, S.na, S.da, S.mu, p, S.src_cols.data(), S.N);
 }
 
@@ -1256,8 +1317,8 @@ svd1_status apply_prepare2(svd1_plan_t P, StepRecord& A, int64_t rows_a, StepRec
                            int64_t rows_b, bool reverse) {
   const svd1_config cfg = P->cfg;
   const int p = P->p;
-  std::thread worker([&] { apply_plan(cfg, p, B, rows_b, reverse); });
-  apply_plan(cfg, p, A, rows_a, reverse);
+  std::thread worker([&] { apply_plan(cfg, p, B, rows_b, reverse, 1); });
+  apply_plan(cfg, p, A, rows_a, reverse, 0);
   worker.join();
   TRY(apply_upload(P, A));
   TRY(apply_upload(P, B));
@@ -1458,8 +1519,8 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   {
     const svd1_config cfg = P->cfg;
     const int pp = P->p;
-    planners.add(std::thread([&S, cfg, pp, rows = c.u_rows] { apply_plan(cfg, pp, S[0], rows, false); }));
-    planners.add(std::thread([&S, cfg, pp, rows = c.v_rows] { apply_plan(cfg, pp, S[2], rows, false); }));
+    planners.add(std::thread([&S, cfg, pp, rows = c.u_rows] { apply_plan(cfg, pp, S[0], rows, false, 0); }));
+    planners.add(std::thread([&S, cfg, pp, rows = c.v_rows] { apply_plan(cfg, pp, S[2], rows, false, 1); }));
   }
   // Round 2: STEP 5 (U, rho2, z2 = X1^T U^T b1) and STEP 7 (V, rho4)
   {
@@ -1663,7 +1724,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   if (nrot > 0 && c.v_rows > 0)
     TRY(col_rotate(c.v_rows, V, ldv, nrot, static_cast<int32_t*>(P->d_rot_goff.p),
                    static_cast<int32_t*>(P->d_rot_cols.p), static_cast<double*>(P->d_rot_mats.p),
-                   P->st2, &P->launches));
+                   stv, &P->launches));
   TRY(stream_wait(P, 2, P->st2, P->st));  // join
   TRY(ev_record(P, 17, P->st));           // apply phase end
   R.t_ms[2] = now_ms() - t4;

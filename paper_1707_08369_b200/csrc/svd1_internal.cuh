@@ -1,5 +1,7 @@
 // Internal declarations of libsvd1 (kernels + host runtime).  Not part of the ABI.
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors; encoded through the runtime entry point)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <vector>
@@ -100,11 +102,13 @@ enum FmmOpKind : int32_t {
   OP_ID = 7,        // p x p identity (in-place accumulation of the L2L chain)
   OP_L2P_FROM = 8   // local expansion of cell a evaluated at the targets of leaf b
 };
-struct FmmOpDesc {    // one operator matrix to build: rows x cols, row stride ld, at ops + off
+struct FmmOpDesc {    // one operator block: rows x cols, written into its term's op
   int32_t kind, a, b; // a = source cell (expansion kinds) or first source index (source
                       // kinds P2M/P2L/P2P); b = target-side cell
-  int32_t rows, cols, ld;
-  int64_t off;        // 16-byte aligned (even), ld even
+  int32_t rows, cols;
+  int32_t kb;         // first k (row) of this block inside the term's op
+  int32_t npad;       // the term's op: chunks of [npad][16] doubles (see FmmTerm)
+  int64_t op_row;     // the term's first 16-double row in the ops buffer
   int32_t c0, s_hi;   // source kinds: row q <-> input column c0 + q, holding active source
                       // s = col2src[c0 + q]; rows with s outside [a, s_hi) are zero
 };
@@ -112,12 +116,13 @@ enum FmmIoKind : int32_t { IO_U = 0, IO_PHI = 1, IO_PSI = 2 };
 // Expansions are stored as row-major matrices Phi, Psi (rows x ldE, ldE = ncells * p):
 // cell c's p coefficients of row r at [r * ldE + c * p].  Adjacent cells are adjacent
 // columns, so consecutive interaction partners merge into one long-K term.
-struct FmmTerm {      // in[:, col0 : col0 + K] * op (K x N, row-major, leading dim op_ld)
-  int32_t in_kind;    // IO_U (physical columns of U_in, col0 even) or IO_PHI / IO_PSI
+struct FmmTerm {      // in[:, col0 : col0 + K] * op (K x N)
+  int32_t in_kind;    // IO_U (physical columns of U_in) or IO_PHI / IO_PSI
   int32_t col0;
   int32_t K;
-  int32_t op_ld;
-  int64_t op_off;
+  int32_t npad;       // op stored chunk-transposed: chunk c (k = 16c .. 16c+15) is an
+                      // [npad][16] block at ops row op_row + c*npad (zero past K and N)
+  int64_t op_row;
 };
 struct FmmTask {      // out[:, col0 : col0 + N] = sum of terms
   int32_t out_kind;   // IO_U (columns mapped through dst[]) or IO_PHI / IO_PSI
@@ -129,15 +134,22 @@ struct FmmTask {      // out[:, col0 : col0 + N] = sum of terms
 svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cells, int p,
                           const double* d, const int32_t* k, const double* tau,
                           const double* zhat, const double* cs, const int32_t* col2src,
-                          double* ops, cudaStream_t st, int64_t* launches);
+                          double* ops, int64_t ops_elems, cudaStream_t st, int64_t* launches);
 // One pass: every task's output block for all rows.  bn = 16 or 32 (>= every task N).
 // Terms read physical column windows of U_in (col0 even) or of Phi/Psi; op rows are
 // 16-byte aligned with even op_ld; the ops buffer has kOpsPad doubles of slack.
+// TMA descriptors of one apply (per tile width: [0] BN = 16, [1] BN = 32)
+struct FmmMaps {
+  CUtensorMap u[2], phi[2], psi[2];
+};
+// U_in must be 16-byte aligned with even ld (the host pads otherwise)
+svd1_status fmm_make_maps(FmmMaps* m, int64_t rows, const double* U_in, int64_t ncols_in, int64_t ld_in,
+                          const double* phi, const double* psi, int64_t ldE);
 svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
-                          int64_t rows, const double* ops, const double* U_in, int64_t ld_in,
-                          double* U_out, int64_t ld_out, const int32_t* dst, double* phi,
-                          double* psi, int64_t ldE, cudaStream_t st, int64_t* launches);
-constexpr int64_t kOpsPad = 16 * 64;
+                          int64_t rows, const FmmMaps* maps /* device */, double* U_out, int64_t ld_out,
+                          const int32_t* dst, double* phi, double* psi, int64_t ldE, int64_t out_cols,
+                          int64_t exp_elems, const double* ops_raw, int64_t ops_rows, cudaStream_t st,
+                          int64_t* launches);
 
 
 }  // namespace svd1

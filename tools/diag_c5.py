@@ -1,24 +1,32 @@
-# Diagnostic: C5-recipe update at size n; per-column residuals and sign check.
-import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+"""Diagnostics (GPU): one C5 update, FMM vs forced-direct plan; per-column residuals."""
+import os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 import numpy as np, torch
 import paper_1707_08369_b200 as P
 from synth import config_inputs
-n = int(sys.argv[1]); flags = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 dev = torch.device("cuda:0")
-inp = config_inputs(5, device=dev, m=n, n=n, updates=1)
-Ug, sg, Vg = inp["U"].clone(), inp["sigma"].clone(), inp["V"].clone()
+nn = int(sys.argv[1]) if len(sys.argv) > 1 else None
+only = sys.argv[2] if len(sys.argv) > 2 else "fmm,direct"
+inp = config_inputs(5, device=dev, updates=1, m=nn, n=nn)
+m = n = inp["U"].shape[0]
 a, b = (torch.from_numpy(x).to(dev) for x in inp["ab"][0])
-A = (Ug * sg[None, :]) @ Vg.T + torch.outer(a, b)
-plan = P.Plan(n, n, eps=1e-10, flags=flags)
-rep = plan.update(Ug, sg, Vg, a, b)
-R = A @ Vg - Ug * sg[None, :]
-res = torch.linalg.norm(R, dim=0) / sg[0]
-Rf = A @ (-Vg) - Ug * sg[None, :]
-resf = torch.linalg.norm(Rf, dim=0) / sg[0]
-bad = torch.nonzero(res > 1e-10).flatten().cpu().numpy()
-print("n", n, "flags", flags, "max res", float(res.max()), "n bad", len(bad), "fixed by flip", int((resf[bad] < 1e-10).sum()) if len(bad) else 0)
-print("rep", {k: rep[k] for k in ("n_active", "n_deflated", "sign_flips", "fmm_used", "max_iter")})
-s = sg.cpu().numpy()
-for i in bad[:10]:
-    print(i, "sigma", s[i], "res", float(res[i]), "flipres", float(resf[i]), "neighbors", s[max(0,i-1):i+2])
+A = (inp["U"] * inp["sigma"][None, :]) @ inp["V"].T + torch.outer(a, b)
+out = {}
+for name, flags in (("fmm", 0), ("direct", P.FORCE_DIRECT)):
+    if name not in only:
+        continue
+    Ug, sg, Vg = inp["U"].clone(), inp["sigma"].clone(), inp["V"].clone()
+    rep = P.Plan(m, n, eps=1e-10, flags=flags).update(Ug, sg, Vg, a, b)
+    torch.cuda.synchronize()
+    colres = (torch.linalg.norm(A @ Vg - Ug * sg[None, :], dim=0) / sg[0]).cpu().numpy()
+    ou = (Ug.T @ Ug - torch.eye(m, device=dev, dtype=torch.float64)).abs().max(dim=0).values.cpu().numpy()
+    ov = (Vg.T @ Vg - torch.eye(n, device=dev, dtype=torch.float64)).abs().max(dim=0).values.cpu().numpy()
+    print(name, "res", colres.max(), "orthU", ou.max(), "orthV", ov.max(), "levels", rep["fmm_levels"],
+          "defl", rep["n_deflated"], "rot", rep["pair_rotations"])
+    bad = np.nonzero(colres > 1e-10)[0]
+    print("  bad res cols:", len(bad), bad[:20], "orthU bad:", np.nonzero(ou > 1e-10)[0][:20],
+          "orthV bad:", np.nonzero(ov > 1e-10)[0][:20])
+    out[name] = (Ug, sg, Vg)
+if len(out) == 2:
+    print("sigma diff fmm-direct", float((out["fmm"][1] - out["direct"][1]).abs().max()))
