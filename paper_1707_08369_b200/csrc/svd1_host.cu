@@ -139,8 +139,11 @@ struct StepRecord {
   std::vector<std::vector<double>> cs_sorted;
   double* rb = nullptr;  // pinned read-back
   size_t rb_cap = 0;
+  cudaEvent_t done_ev = nullptr;  // recorded after the read-back copy
+  bool pending = false;           // spectral work in flight (wait on done_ev)
   ~StepRecord() {
     if (rb) cudaFreeHost(rb);
+    if (done_ev) cudaEventDestroy(done_ev);
   }
   void clear_host() {
     spectral_ms = 0.0;
@@ -1177,6 +1180,9 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     S.rb_cap = words * sizeof(double);
   }
   SVD1_CUDA_TRY(cudaMemcpyAsync(S.rb, dout, words * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  if (!S.done_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&S.done_ev, cudaEventDisableTiming));
+  SVD1_CUDA_TRY(cudaEventRecord(S.done_ev, P->st));
+  S.pending = true;
   if (std::getenv("SVD1_TIMING"))
     fprintf(stderr, "[svd1] spectral_launch N=%d: host prep %.3f ms, stage+launch %.3f ms\n", N,
             th0 - th_start, now_ms() - th0);
@@ -1190,6 +1196,10 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
                             std::vector<std::vector<double>>& carries) {
   const int N = S.N, na = S.na, nc = S.nc;
   const double* carry_out = nullptr;
+  if (S.pending) {  // this step's kernels and read-back only (the other side may still run)
+    SVD1_CUDA_TRY(cudaEventSynchronize(S.done_ev));
+    S.pending = false;
+  }
   if (na > 0) {
     const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
     const double* rb = S.rb;
@@ -1507,42 +1517,43 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8));
     TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12));
   }
+  // The two sides' chains are interleaved: each side's host step (finish one
+  // eigen-update, launch the next) runs while the GPU works on the other side's, so the
+  // stream stays busy.  The Cauchy/FMM plan of each first apply depends on that side's
+  // round 1 only and is built on a worker thread meanwhile.
   const double tA = now_ms();
-  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
-  const double tB = now_ms();
-  TRY(spectral_finish(P, S[0], Du, cu));
-  TRY(spectral_finish(P, S[2], Dv, cv));
-  const double tC = now_ms();
-  // The Cauchy/FMM plans of the first applies depend on round 1 only: build them on two
-  // worker threads while this thread launches round 2 and the GPU runs it.
   Joiner planners;
+  const svd1_config pcfg = P->cfg;
+  const int pp = P->p;
+  // U: finish STEP 4, launch STEP 5 (rho2, z2 = X1^T U^T b1)
+  TRY(spectral_finish(P, S[0], Du, cu));
+  planners.add(std::thread([&S, pcfg, pp, rows = c.u_rows] { apply_plan(pcfg, pp, S[0], rows, false, 0); }));
   {
-    const svd1_config cfg = P->cfg;
-    const int pp = P->p;
-    planners.add(std::thread([&S, cfg, pp, rows = c.u_rows] { apply_plan(cfg, pp, S[0], rows, false, 0); }));
-    planners.add(std::thread([&S, cfg, pp, rows = c.v_rows] { apply_plan(cfg, pp, S[2], rows, false, 1); }));
-  }
-  // Round 2: STEP 5 (U, rho2, z2 = X1^T U^T b1) and STEP 7 (V, rho4)
-  {
-    std::vector<double> z2 = cu[0], z4 = cv[0];
+    std::vector<double> z2 = cu[0];
     cu.erase(cu.begin());
-    cv.erase(cv.begin());
     TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10));
+  }
+  const double tB = now_ms();
+  // V: finish STEP 6, launch STEP 7 (rho4)
+  TRY(spectral_finish(P, S[2], Dv, cv));
+  planners.add(std::thread([&S, pcfg, pp, rows = c.v_rows] { apply_plan(pcfg, pp, S[2], rows, false, 1); }));
+  {
+    std::vector<double> z4 = cv[0];
+    cv.erase(cv.begin());
     TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14));
   }
-  // host work overlapping round 2 on the GPU: Cauchy plans of the first applies
-  const double tD = now_ms();
+  const double tC = now_ms();
   planners.join();
   TRY(apply_upload(P, S[0]));
   TRY(apply_upload(P, S[2]));
-  const double tE = now_ms();
-  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
-  const double tF = now_ms();
+  const double tD = now_ms();
   TRY(spectral_finish(P, S[1], Du, cu));
+  const double tE = now_ms();
   TRY(spectral_finish(P, S[3], Dv, cv));
+  const double tF = now_ms();
   if (std::getenv("SVD1_TIMING"))
-    fprintf(stderr, "[svd1] launch1 %.3f wait1 %.3f finish1 %.3f launch2 %.3f plan %.3f wait2 %.3f finish2 %.3f\n",
-            tA - t1, tB - tA, tC - tB, tD - tC, tE - tD, tF - tE, now_ms() - tF);
+    fprintf(stderr, "[svd1] launch1 %.3f U1->U2 %.3f V1->V2 %.3f plans+uploads %.3f finish U2 %.3f finish V2 %.3f\n",
+            tA - t1, tB - tA, tC - tB, tD - tC, tE - tD, tF - tE);
   const double t3 = now_ms();
   R.t_ms[1] = t3 - t1;
   // ---- sign alignment: final column i = position N-1-i
