@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 SOURCES = ["kernels_spectral.cu", "kernels_apply.cu", "svd1_host.cu"]
-LIB = os.path.join(HERE, "libsvd1.so")
+LIB = os.environ.get("SVD1_LIB_OUT") or os.path.join(HERE, "libsvd1.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -314,6 +314,12 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
 // B) values for the chunk one contiguous 32-byte run.  Op chunks are zero past K, so
 // the A columns of a chunk that fall outside the term only ever meet zeros.
 constexpr int KC = 16;  // chunk (k) width: one 128-byte swizzle row of doubles
+#ifndef SVD1_STAGES16
+#define SVD1_STAGES16 4   // ring depth of the 16-wide passes (3 CTAs / SM; measured best)
+#endif
+#ifndef SVD1_STAGES32
+#define SVD1_STAGES32 3   // ring depth of the 32-wide passes (3 CTAs / SM; measured best)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -357,7 +363,7 @@ struct GemmCfg {
   static constexpr int NTHR = 32 * (CW + 1); // + one producer warp
   static constexpr int NT = BN / 8;
   static constexpr int BM = 32 * CW;
-  static constexpr int STAGES = BN <= 16 ? 6 : 4;
+  static constexpr int STAGES = BN <= 16 ? SVD1_STAGES16 : SVD1_STAGES32;
   static constexpr int A_BYTES = BM * KC * 8;
   static constexpr int B_BYTES = BN * KC * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
