@@ -230,8 +230,17 @@ def main():
     n_apply = sum(sum(1 for x in r["apply_ms"] if x > 0) for r in reps)
     achieved = ap_fl / (ap_ms / 1e3) / 1e12 if ap_ms > 0 else 0.0
     launches = sum(r["kernel_launches"] for r in reps)
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per apply from the committed ncu capture of this workload
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+            tj = json.load(f)
+        if args.config == CFG_ID:
+            traffic, traffic_src = tj["traffic_bytes_per_apply"], "profiles/ncu_traffic_r01.json: " + tj["label"]
+    except Exception:
+        pass
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes_per_apply": 16.0 * (m * m + n * n) / 2.0,
             "kernel": "FMM Cauchy apply (K5 ops + K6-K10 task passes + K4/passthrough), per apply",
             "flops_per_apply": ap_fl / max(n_apply, 1), "ms_per_apply": ap_ms / max(n_apply, 1),
             "flops_exec_per_apply": ap_fx / max(n_apply, 1),

@@ -186,17 +186,14 @@ __global__ void passthrough_kernel(int64_t rows, int nq, const double* __restric
 // ------------------------------------------------------------------- K5
 // Chebyshev nodes t_k = cos((2k+1) pi / 2p) (k 0-based) and barycentric weights
 // w_k = (-1)^k sin((2k+1) pi / 2p); u_k(t) = [w_k/(t - t_k)] / sum_m w_m/(t - t_m).
-__device__ double lagrange(const double* __restrict__ t, const double* __restrict__ w, int p,
-                           int kk, double x) {
-  double den = 0.0, num = 0.0;
-  for (int m = 0; m < p; ++m) {
-    const double dx = x - t[m];
-    if (dx == 0.0) return (m == kk) ? 1.0 : 0.0;
-    const double q = w[m] / dx;
-    den += q;
-    if (m == kk) num = q;
-  }
-  return num / den;
+
+// blockIdx.y = 1: expansion kinds (M2M, M2L, L2L, L2P, L2P_FROM), a warp per operator
+// block: they are Lagrange bases evaluated at a point that depends only on the column
+// j, so lane j forms the barycentric denominator once and then the p rows (2p divisions
+// per column instead of p per element).  blockIdx.y = 0: source kinds (P2M, P2L, P2P)
+// and ID, a block per operator, one division per element.
+__device__ __forceinline__ bool is_lagrange(int kind) {
+  return kind == OP_M2M || kind == OP_M2L || kind == OP_L2L || kind == OP_L2P || kind == OP_L2P_FROM;
 }
 
 __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc* __restrict__ descs,
@@ -215,73 +212,17 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
     w[threadIdx.x] = ((threadIdx.x & 1) ? -1.0 : 1.0) * sinpi(th);
   }
   __syncthreads();
-  for (int o = blockIdx.x; o < n_ops; o += gridDim.x) {
+  const bool lag_mode = blockIdx.y == 1;
+  const int lane = threadIdx.x & 31;
+  const int nunits = lag_mode ? gridDim.x * (blockDim.x >> 5) : gridDim.x;  // warps | blocks
+  const int unit = lag_mode ? blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) : blockIdx.x;
+  const int ustride = lag_mode ? 32 : blockDim.x, uid = lag_mode ? lane : threadIdx.x;
+  for (int o = unit; o < n_ops; o += nunits) {
     const FmmOpDesc D = descs[o];
-    const int total = D.rows * D.cols;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int i = e / D.cols, j = e % D.cols;
-      double v = 0.0;
-      // source kinds: row i holds input column c0 + i (zero unless an active source of
-      // the term's range [a, s_hi) sits there)
-      int s = -1;
-      if (D.kind == OP_P2M || D.kind == OP_P2L || D.kind == OP_P2P) {
-        s = col2src ? col2src[D.c0 + i] : D.c0 + i;
-        if (s < D.a || s >= D.s_hi) s = -1;
-      }
-      switch (D.kind) {
-        case OP_P2M: {  // Phi~_X[j] += zhat_s U_s / (t_j (x_s - c_X) - 3 r_X), X = b
-          const FmmCell X = cells[D.b];
-          if (s >= 0) v = zhat[s] / (t[j] * (d[s] - X.c) - 3.0 * X.r);
-          break;
-        }
-        case OP_M2M: {  // child (a) -> parent (b): i = child node, j = parent node
-          const FmmCell C = cells[D.a], P = cells[D.b];
-          const double den = 3.0 * P.r + t[j] * (P.c - C.c);
-          const double tc = 3.0 * C.r * t[j] / den;
-          v = (3.0 * C.r / den) * lagrange(t, w, p, i, tc);
-          break;
-        }
-        case OP_M2L: {  // source X (a) -> target Y (b): i = X node, j = Y node
-          const FmmCell X = cells[D.a], Y = cells[D.b];
-          const double tx = 3.0 * X.r / ((Y.c - X.c) + Y.r * t[j]);
-          v = tx * lagrange(t, w, p, i, tx);
-          break;
-        }
-        case OP_L2L: {  // parent (a) -> child (b): i = parent node, j = child node
-          const FmmCell P = cells[D.a], C = cells[D.b];
-          v = lagrange(t, w, p, i, ((C.c - P.c) + C.r * t[j]) / P.r);
-          break;
-        }
-        case OP_L2P: {  // leaf Y (b): i = node, j = target
-          const FmmCell Y = cells[D.b];
-          const int jt = Y.tlo + j;
-          v = lagrange(t, w, p, i, ((d[k[jt]] - Y.c) + tau[jt]) / Y.r) * cs[jt];
-          break;
-        }
-        case OP_ID: {
-          v = (i == j) ? 1.0 : 0.0;
-          break;
-        }
-        case OP_L2P_FROM: {  // Psi of cell a (an ancestor) at the targets of leaf b
-          const FmmCell A = cells[D.a], Y = cells[D.b];
-          const int jt = Y.tlo + j;
-          v = lagrange(t, w, p, i, ((d[k[jt]] - A.c) + tau[jt]) / A.r) * cs[jt];
-          break;
-        }
-        case OP_P2L: {  // source s -> local expansion of Y (b) at y_j = c_Y + r_Y t_j
-          const FmmCell Y = cells[D.b];
-          if (s >= 0) v = zhat[s] / ((d[s] - Y.c) - Y.r * t[j]);
-          break;
-        }
-        default: {  // OP_P2P: source s, target leaf Y (b)
-          const FmmCell Y = cells[D.b];
-          const int jt = Y.tlo + j;
-          if (s >= 0) v = (zhat[s] * cs[jt]) / ((d[s] - d[k[jt]]) - tau[jt]);
-          break;
-        }
-      }
-      // chunk-transposed layout of the term's op: chunk (kb + i) / 16 is an [npad][16]
-      // block (n-major, 16 k contiguous), the GEMM's B tile as TMA reads it
+    if (is_lagrange(D.kind) != lag_mode) continue;
+    // chunk-transposed layout of the term's op: chunk (kb + i) / 16 is an [npad][16]
+    // block (n-major, 16 k contiguous), the GEMM's B tile
+    auto store = [&](int i, int j, double v) {
       const int kk = D.kb + i;
 #ifdef SVD1_BOUNDS
       if ((D.op_row + int64_t(kk >> 4) * D.npad + j) * 16 + (kk & 15) >= ops_elems || j >= D.npad) {
@@ -291,6 +232,87 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
       }
 #endif
       ops[(D.op_row + int64_t(kk >> 4) * D.npad + j) * 16 + (kk & 15)] = v;
+    };
+    if (is_lagrange(D.kind)) {
+      for (int j = lane; j < D.cols; j += 32) {
+        double x, f = 1.0;  // u_i(x) * f for rows i < p
+        switch (D.kind) {
+          case OP_M2M: {  // child (a) -> ancestor (b): i = child node, j = parent node
+            const FmmCell C = cells[D.a], P = cells[D.b];
+            const double den = 3.0 * P.r + t[j] * (P.c - C.c);
+            x = 3.0 * C.r * t[j] / den;
+            f = 3.0 * C.r / den;
+            break;
+          }
+          case OP_M2L: {  // source X (a) -> target Y (b): i = X node, j = Y node
+            const FmmCell X = cells[D.a], Y = cells[D.b];
+            x = 3.0 * X.r / ((Y.c - X.c) + Y.r * t[j]);
+            f = x;
+            break;
+          }
+          case OP_L2L: {  // ancestor (a) -> cell (b): i = ancestor node, j = cell node
+            const FmmCell P = cells[D.a], C = cells[D.b];
+            x = ((C.c - P.c) + C.r * t[j]) / P.r;
+            break;
+          }
+          case OP_L2P: {  // leaf Y (b): i = node, j = target
+            const FmmCell Y = cells[D.b];
+            const int jt = Y.tlo + j;
+            x = ((d[k[jt]] - Y.c) + tau[jt]) / Y.r;
+            f = cs[jt];
+            break;
+          }
+          default: {  // OP_L2P_FROM: expansion of cell a (an ancestor) at the targets of leaf b
+            const FmmCell A = cells[D.a], Y = cells[D.b];
+            const int jt = Y.tlo + j;
+            x = ((d[k[jt]] - A.c) + tau[jt]) / A.r;
+            f = cs[jt];
+            break;
+          }
+        }
+        // barycentric form u_i(x) = (w_i / (x - t_i)) / sum_m w_m / (x - t_m)
+        double den = 0.0;
+        int hit = -1;
+        for (int m = 0; m < p; ++m) {
+          const double dx = x - t[m];
+          if (dx == 0.0) hit = m;
+          else den += w[m] / dx;
+        }
+        for (int i = 0; i < D.rows; ++i) {
+          const double v = hit >= 0 ? (i == hit ? f : 0.0) : f * (w[i] / (x - t[i])) / den;
+          store(i, j, v);
+        }
+      }
+      continue;
+    }
+    const int total = D.rows * D.cols;
+    for (int e = uid; e < total; e += ustride) {
+      const int i = e / D.cols, j = e % D.cols;
+      double v = 0.0;
+      switch (D.kind) {
+        case OP_ID: {
+          v = (i == j) ? 1.0 : 0.0;
+          break;
+        }
+        default: {  // source kinds: row i holds input column c0 + i (zero unless an active
+                    // source of the term's range [a, s_hi) sits there)
+          int s = col2src ? col2src[D.c0 + i] : D.c0 + i;
+          if (s < D.a || s >= D.s_hi) break;
+          if (D.kind == OP_P2M) {  // Phi~_X[j] += zhat_s U_s / (t_j (x_s - c_X) - 3 r_X), X = b
+            const FmmCell X = cells[D.b];
+            v = zhat[s] / (t[j] * (d[s] - X.c) - 3.0 * X.r);
+          } else if (D.kind == OP_P2L) {  // source s -> local expansion of Y (b) at c_Y + r_Y t_j
+            const FmmCell Y = cells[D.b];
+            v = zhat[s] / ((d[s] - Y.c) - Y.r * t[j]);
+          } else {  // OP_P2P: source s, target leaf Y (b)
+            const FmmCell Y = cells[D.b];
+            const int jt = Y.tlo + j;
+            v = (zhat[s] * cs[jt]) / ((d[s] - d[k[jt]]) - tau[jt]);
+          }
+          break;
+        }
+      }
+      store(i, j, v);
     }
   }
 }
@@ -605,8 +627,9 @@ svd1_status fmm_build_ops(int n_ops, const FmmOpDesc* descs, const FmmCell* cell
                           const double* zhat, const double* cs, const int32_t* col2src,
                           double* ops, int64_t ops_elems, cudaStream_t st, int64_t* launches) {
   if (n_ops <= 0) return SVD1_OK;
-  const unsigned g = unsigned(std::min(n_ops, 148 * 16));
-  fmm_ops_kernel<<<g, 256, 0, st>>>(n_ops, descs, cells, p, d, k, tau, zhat, cs, col2src, ops, ops_elems);
+  const unsigned g = unsigned(std::min(n_ops, 148 * 8));
+  fmm_ops_kernel<<<dim3(g, 2), 256, 0, st>>>(n_ops, descs, cells, p, d, k, tau, zhat, cs, col2src, ops,
+                                             ops_elems);
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;

@@ -171,12 +171,14 @@ struct SecAcc {
 __device__ SecAcc sec_eval(const double* __restrict__ d, const double* __restrict__ z2, int n,
                            double dk, double tau, int sp, int lane) {
   SecAcc a = {0, 0, 0, 0, 0};
+#pragma unroll 4
   for (int i = lane; i <= sp; i += 32) {
     const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
     const double t = __ldg(z2 + i) * rr;
     a.psi += t;
     a.dpsi = fma(t, rr, a.dpsi);
   }
+#pragma unroll 4
   for (int i = sp + 1 + lane; i < n; i += 32) {
     const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
     const double t = __ldg(z2 + i) * rr;
@@ -359,23 +361,38 @@ __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
       s_t[t] = tau[jb + t];
     }
     __syncthreads();
-    int cnt = 0;
-    for (int t = 0; t < nj; ++t) {
+    // two independent product chains (even / odd t) for ILP, renormalised every 8
+    // factors each; merged below
+    double Qn = 1.0, Qd = 1.0;
+    int cnt = 0, t = 0;
+    for (; t + 1 < nj; t += 2) {
       const int j = jb + t;
       Pn *= fabs((s_mu[t] - di) + s_t[t]);
       Pd *= (j == i) ? 1.0 : fabs(s_d[t] - di);
+      Qn *= fabs((s_mu[t + 1] - di) + s_t[t + 1]);
+      Qd *= (j + 1 == i) ? 1.0 : fabs(s_d[t + 1] - di);
       if (++cnt == 8) {
-        int e1, e2;
+        int e1, e2, e3, e4;
         Pn = frexp(Pn, &e1);
         Pd = frexp(Pd, &e2);
-        E += e1 - e2;
+        Qn = frexp(Qn, &e3);
+        Qd = frexp(Qd, &e4);
+        E += (e1 - e2) + (e3 - e4);
         cnt = 0;
       }
     }
-    int e1, e2;
+    if (t < nj) {
+      Pn *= fabs((s_mu[t] - di) + s_t[t]);
+      Pd *= (jb + t == i) ? 1.0 : fabs(s_d[t] - di);
+    }
+    int e1, e2, e3, e4;
     Pn = frexp(Pn, &e1);
     Pd = frexp(Pd, &e2);
-    E += e1 - e2;
+    Qn = frexp(Qn, &e3);
+    Qd = frexp(Qd, &e4);
+    E += (e1 - e2) + (e3 - e4);
+    Pn *= Qn;
+    Pd *= Qd;
   }
   if (i < n) {
     int e;
@@ -392,6 +409,7 @@ __global__ void loewner_combine_kernel(const double* __restrict__ pm, const int3
   if (i >= n) return;
   double P = 1.0;
   int E = 0;
+#pragma unroll 8
   for (int c = 0; c < nchunks; ++c) {
     int e;
     P = frexp(P * pm[int64_t(c) * n + i], &e);
@@ -449,22 +467,28 @@ __global__ void __launch_bounds__(kCT) colnorm_partial_kernel(
   }
 }
 
+// thread per (j, q): q = 0 -> colscale_j (and the status check), q >= 1 -> carried
+// vector q-1 (which also needs ||y||: recomputed, the partials are L2-resident)
 __global__ void colnorm_combine_kernel(const double* __restrict__ part, int nchunks, int nc, int n,
                                        const double* __restrict__ tau, double* __restrict__ colscale,
                                        double* __restrict__ carry_out, int32_t* __restrict__ status) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, q = blockIdx.y;
   if (j >= n) return;
+  const int64_t cstride = int64_t(nc + 1) * n;
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) s += part[int64_t(c) * (nc + 1) * n + j];
+#pragma unroll 8
+  for (int c = 0; c < nchunks; ++c) s += part[int64_t(c) * cstride + j];
   const double rs = sqrt(s);
-  const double cs = fabs(tau[j]) / rs;
-  if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
-  colscale[j] = cs;
-  for (int q = 0; q < nc; ++q) {
-    double t = 0.0;
-    for (int c = 0; c < nchunks; ++c) t += part[int64_t(c) * (nc + 1) * n + int64_t(q + 1) * n + j];
-    carry_out[int64_t(q) * n + j] = t / rs;
+  if (q == 0) {
+    const double cs = fabs(tau[j]) / rs;
+    if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
+    colscale[j] = cs;
+    return;
   }
+  double t = 0.0;
+#pragma unroll 8
+  for (int c = 0; c < nchunks; ++c) t += part[int64_t(c) * cstride + int64_t(q) * n + j];
+  carry_out[int64_t(q - 1) * n + j] = t / rs;
 }
 
 inline unsigned blocks_for_warps(int64_t nwarps, int threads = 256) {
@@ -591,8 +615,8 @@ svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
     case 6: colnorm_partial_kernel<6><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
     default: return SVD1_E_INVALID;
   }
-  colnorm_combine_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(scratch, ch, ncarry, n, tau, colscale,
-                                                                     carry_out, status);
+  colnorm_combine_kernel<<<dim3(unsigned((n + 127) / 128), unsigned(ncarry + 1)), 128, 0, st>>>(
+      scratch, ch, ncarry, n, tau, colscale, carry_out, status);
   *launches += 2;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;

@@ -107,7 +107,13 @@ struct CauchyPrep {
   std::vector<int32_t> col2src;  // input column -> active source (-1: none); empty = identity
   int n_in = 0;                  // columns of the input buffer
   int n_out = 0;                 // columns of the output buffer
-  DevBuf d_cells, d_descs, d_terms, d_tasks, d_ops, d_col2src, d_maps;
+  DevBuf blob, d_ops, d_maps;  // blob: cells, descs, terms, tasks, col2src (one copy)
+  FmmCell* dcells = nullptr;
+  FmmOpDesc* ddescs = nullptr;
+  FmmTerm* dterms = nullptr;
+  FmmTask* dtasks = nullptr;
+  int32_t* dcol2src = nullptr;
+  size_t o_cells = 0, o_descs = 0, o_terms = 0, o_tasks = 0, o_c2s = 0;
   FmmMaps* h_maps = nullptr;  // pinned staging of the TMA descriptors (copied on the apply stream)
   ~CauchyPrep() {
     if (h_maps) cudaFreeHost(h_maps);
@@ -140,6 +146,7 @@ struct StepRecord {
   double* rb = nullptr;  // pinned read-back
   size_t rb_cap = 0;
   cudaEvent_t done_ev = nullptr;  // recorded after the read-back copy
+  double plan_ms = 0.0;           // host time of the last apply_plan (diagnostics)
   bool pending = false;           // spectral work in flight (wait on done_ev)
   ~StepRecord() {
     if (rb) cudaFreeHost(rb);
@@ -155,8 +162,11 @@ struct StepRecord {
     tau_h.clear(); cs_h.clear(); k_h.clear();
   }
   // device arrays
-  DevBuf d_da, d_za, d_k, d_tau, d_zhat, d_cs, d_src, d_dst, d_pass_src, d_pass_dst, d_pass_scale,
-      d_goff, d_hcols, d_hv, d_carry, d_carry_out, d_status, d_iters, d_scratch, d_in, d_out;
+  DevBuf d_zhat, d_scratch, d_in, d_out;
+  DevBuf blob;  // apply data (Householder groups, column maps, scales, FMM plan): one copy
+  int32_t *dgoff = nullptr, *dhcols = nullptr, *dsrc = nullptr, *ddst = nullptr, *dpsrc = nullptr,
+          *dpdst = nullptr;
+  double *dhv = nullptr, *dcs = nullptr, *dpscale = nullptr;
   std::vector<double> stage;
   CauchyPrep cp;
 };
@@ -243,6 +253,53 @@ svd1_status arena_put(svd1_plan_t P, const void* src, size_t bytes, void* dev) {
   SVD1_CUDA_TRY(cudaEventRecord(P->arena_ev, P->st));
   P->arena_pending = true;
   P->arena_used = off + bytes;
+  return SVD1_OK;
+}
+
+// Several host arrays staged as ONE pinned-arena region and ONE host->device copy into
+// a grow-only device blob (instead of one copy per array).
+struct BlobBuilder {
+  struct Part {
+    const void* p;
+    size_t bytes, off;
+  };
+  std::vector<Part> parts;
+  size_t total = 0;
+  template <class T>
+  size_t add(const std::vector<T>& v) {
+    const size_t off = (total + 255) & ~size_t(255);
+    parts.push_back({v.data(), v.size() * sizeof(T), off});
+    total = off + v.size() * sizeof(T);
+    return off;
+  }
+};
+
+svd1_status arena_put_blob(svd1_plan_t P, const BlobBuilder& B, DevBuf& dev, char** out) {
+  TRY(dev.get<char>(std::max<size_t>(B.total, 1), out));
+  if (B.total == 0) return SVD1_OK;
+  if (!P->arena_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->arena_ev, cudaEventDisableTiming));
+  size_t off = (P->arena_used + 255) & ~size_t(255);
+  if (off + B.total > P->arena_cap) {
+    TRY(arena_reset(P));
+    if (B.total > P->arena_cap) {
+      if (P->arena) cudaFreeHost(P->arena);
+      P->arena = nullptr;
+      P->arena_cap = 0;
+      const size_t cap = std::max<size_t>(B.total * 2, size_t(4) << 20);
+      if (cudaMallocHost(&P->arena, cap) != cudaSuccess) {
+        cudaGetLastError();
+        return SVD1_E_NOMEM;
+      }
+      P->arena_cap = cap;
+    }
+    off = 0;
+  }
+  for (const auto& q : B.parts)
+    if (q.bytes) std::memcpy(P->arena + off + q.off, q.p, q.bytes);
+  SVD1_CUDA_TRY(cudaMemcpyAsync(*out, P->arena + off, B.total, cudaMemcpyHostToDevice, P->st));
+  SVD1_CUDA_TRY(cudaEventRecord(P->arena_ev, P->st));
+  P->arena_pending = true;
+  P->arena_used = off + B.total;
   return SVD1_OK;
 }
 
@@ -377,6 +434,30 @@ bool fmm_cells(FmmHost& F, int s, int L, const Merged& M) {
   return true;
 }
 
+// sorted CSR of (row, value) pairs: row r's values in [off[r], off[r+1])
+struct Csr {
+  std::vector<int> off, val;
+  struct Row {
+    const int* b;
+    const int* e;
+    const int* begin() const { return b; }
+    const int* end() const { return e; }
+    size_t size() const { return size_t(e - b); }
+    bool empty() const { return b == e; }
+    int operator[](size_t i) const { return b[i]; }
+  };
+  Csr(std::vector<std::pair<int, int>>& pairs, int rows) : off(rows + 1, 0) {
+    std::sort(pairs.begin(), pairs.end());
+    val.resize(pairs.size());
+    for (size_t q = 0; q < pairs.size(); ++q) {
+      ++off[pairs[q].first + 1];
+      val[q] = pairs[q].second;
+    }
+    for (int r = 0; r < rows; ++r) off[r + 1] += off[r];
+  }
+  Row operator[](int r) const { return Row{val.data() + off[r], val.data() + off[r + 1]}; }
+};
+
 void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   const double tt0 = now_ms();
   const int L = F.L;
@@ -391,7 +472,11 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   // admissible -> M2L into the target cell; two leaves -> near field (P2P);
   // otherwise split the larger cell.  Needed for graded spectra, where a wide
   // target cell only separates from the narrow sources below it at a finer level.
-  std::vector<std::vector<int>> near(F.ncells), m2l(F.ncells);
+  // interaction lists as CSR (target cell -> sorted partner cells), built from the
+  // traversal's pairs with one sort (no per-cell allocations)
+  std::vector<std::pair<int, int>> near_pairs, m2l_pairs;
+  near_pairs.reserve(size_t(F.ncells) * 4);
+  m2l_pairs.reserve(size_t(F.ncells) * 4);
   const int first_leaf = (1 << L) - 1;
   auto is_leaf = [&](int c) { return c >= first_leaf; };
   std::vector<std::pair<int, int>> stack;
@@ -401,11 +486,11 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     stack.pop_back();
     if (!has_src(x) || !has_tgt(y)) continue;
     if (x != y && adm(x, y)) {
-      m2l[y].push_back(x);
+      m2l_pairs.push_back({y, x});
       continue;
     }
     if (is_leaf(x) && is_leaf(y)) {
-      near[y].push_back(x);
+      near_pairs.push_back({y, x});
       continue;
     }
     const bool split_x = is_leaf(y) || (!is_leaf(x) && F.cells[x].r > F.cells[y].r);
@@ -417,10 +502,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       stack.push_back({x, 2 * y + 1});
     }
   }
-  for (int c = 0; c < F.ncells; ++c) {
-    std::sort(near[c].begin(), near[c].end());
-    std::sort(m2l[c].begin(), m2l[c].end());
-  }
+  const Csr near(near_pairs, F.ncells), m2l(m2l_pairs, F.ncells);
   const double tt1 = now_ms();
   // A term's op (K x N) is stored chunk-transposed (FmmTerm): new_term reserves its
   // ceil(K/16) chunks of [npad][16] doubles; add_op adds a block of its rows.
@@ -498,7 +580,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     }
   };
   // consecutive partners -> one term over adjacent columns of U (sources) or Phi
-  auto add_runs = [&](const std::vector<int>& xs, int in_kind, int op_kind, int y, int N) {
+  auto add_runs = [&](const auto& xs, int in_kind, int op_kind, int y, int N) {
     size_t a = 0;
     while (a < xs.size()) {
       size_t b = a;
@@ -606,11 +688,13 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     //     the parent's local polynomial at the targets is exactly L2L then L2P).
     F.pass_begin.push_back(int(F.tasks.size()));
     F.pass_bn.push_back(p);
+    std::vector<int> via_phi, via_src;
     for (int y = 1; y < F.ncells; ++y) {
       if (m2l[y].empty() || !has_tgt(y)) continue;
       begin_task();
       // partners with fewer than p sources are cheaper as P2L (K = #sources < p)
-      std::vector<int> via_phi, via_src;
+      via_phi.clear();
+      via_src.clear();
       for (int x : m2l[y]) (F.cells[x].shi - F.cells[x].slo >= p ? via_phi : via_src).push_back(x);
       add_runs(via_phi, IO_PHI, OP_M2L, y, p);
       add_runs(via_src, IO_U, OP_P2L, y, p);
@@ -811,24 +895,35 @@ void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
   }
 }
 
+// the FMM plan's device arrays as parts of a blob (cauchy_bind sets the pointers)
+void cauchy_stage(CauchyPrep& C, BlobBuilder& B) {
+  if (!C.fmm) return;
+  C.o_cells = B.add(C.F.cells);
+  C.o_descs = B.add(C.F.ops);
+  C.o_terms = B.add(C.F.terms);
+  C.o_tasks = B.add(C.F.tasks);
+  C.o_c2s = B.add(C.col2src);
+}
+
+svd1_status cauchy_bind(CauchyPrep& C, char* base) {
+  if (!C.fmm) return SVD1_OK;
+  C.dcells = reinterpret_cast<FmmCell*>(base + C.o_cells);
+  C.ddescs = reinterpret_cast<FmmOpDesc*>(base + C.o_descs);
+  C.dterms = reinterpret_cast<FmmTerm*>(base + C.o_terms);
+  C.dtasks = reinterpret_cast<FmmTask*>(base + C.o_tasks);
+  C.dcol2src = C.col2src.empty() ? nullptr : reinterpret_cast<int32_t*>(base + C.o_c2s);
+  double* ops;
+  TRY(C.d_ops.get<double>(size_t(std::max<int64_t>(C.F.ops_rows, 1)) * 16, &ops));
+  return SVD1_OK;
+}
+
 svd1_status cauchy_upload(svd1_plan_t P, CauchyPrep& C) {
   if (!C.fmm) return SVD1_OK;
-  FmmHost& F = C.F;
-  FmmCell* dc;
-  FmmOpDesc* dd;
-  FmmTerm* dt;
-  FmmTask* dk;
-  TRY(upload(P, C.d_cells, F.cells, &dc));
-  TRY(upload(P, C.d_descs, F.ops, &dd));
-  TRY(upload(P, C.d_terms, F.terms, &dt));
-  TRY(upload(P, C.d_tasks, F.tasks, &dk));
-  if (!C.col2src.empty()) {
-    int32_t* c2s;
-    TRY(upload(P, C.d_col2src, C.col2src, &c2s));
-  }
-  double* ops;
-  TRY(C.d_ops.get<double>(size_t(std::max<int64_t>(F.ops_rows, 1)) * 16, &ops));
-  return SVD1_OK;
+  BlobBuilder B;
+  cauchy_stage(C, B);
+  char* base;
+  TRY(arena_put_blob(P, B, C.blob, &base));
+  return cauchy_bind(C, base);
 }
 
 svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
@@ -856,12 +951,12 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   TRY(P->phi[side].get<double>(exp_elems, &phi));  // sized beforehand (no realloc here)
   TRY(P->psi[side].get<double>(exp_elems, &psi));
   const int64_t ldE = int64_t(F.ncells) * p;
-  auto* dc = static_cast<FmmCell*>(C.d_cells.p);
-  auto* dd = static_cast<FmmOpDesc*>(C.d_descs.p);
-  auto* dt = static_cast<FmmTerm*>(C.d_terms.p);
-  auto* dk = static_cast<FmmTask*>(C.d_tasks.p);
+  FmmCell* dc = C.dcells;
+  FmmOpDesc* dd = C.ddescs;
+  FmmTerm* dt = C.dterms;
+  FmmTask* dk = C.dtasks;
   auto* ops = static_cast<double*>(C.d_ops.p);
-  const int32_t* c2s = C.col2src.empty() ? nullptr : static_cast<int32_t*>(C.d_col2src.p);
+  const int32_t* c2s = C.dcol2src;
   // op chunks are zero past K and N (the GEMM relies on it)
   SVD1_CUDA_TRY(cudaMemsetAsync(ops, 0, size_t(std::max<int64_t>(F.ops_rows, 1)) * 16 * sizeof(double), st));
   TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, c2s, ops,
@@ -1283,6 +1378,12 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
 // step: column maps and the Cauchy/FMM plan) and apply_upload (staged uploads).
 // out_col(q) = reverse ? (N - 1 - q) : q.
 void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool reverse, int side) {
+  const double t0 = now_ms();
+  struct Stamp {
+    StepRecord& S;
+    double t0;
+    ~Stamp() { S.plan_ms = now_ms() - t0; }
+  } stamp{S, t0};
   const int N = S.N;
   S.rows = rows;
   auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
@@ -1297,28 +1398,24 @@ void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool
 
 svd1_status apply_upload(svd1_plan_t P, StepRecord& S) {
   if (S.rows <= 0) return SVD1_OK;
-  if (S.h_goff.size() > 1) {
-    int32_t *goff, *cols;
-    double* hv;
-    TRY(upload(P, S.d_goff, S.h_goff, &goff));
-    TRY(upload(P, S.d_hcols, S.h_cols, &cols));
-    TRY(upload(P, S.d_hv, S.h_hv, &hv));
-  }
-  if (S.na > 0) {
-    int32_t *dsrc, *ddst;
-    double* dcs;
-    TRY(upload(P, S.d_src, S.src_cols, &dsrc));
-    TRY(upload(P, S.d_dst, S.dst_cols, &ddst));
-    TRY(upload(P, S.d_cs, S.cs_h, &dcs));  // cs_h may carry the sign alignment
-    TRY(cauchy_upload(P, S.cp));
-  }
-  if (!S.pass_src.empty()) {
-    int32_t *ds, *dd;
-    double* sc;
-    TRY(upload(P, S.d_pass_src, S.pass_src, &ds));
-    TRY(upload(P, S.d_pass_dst, S.pass_dst_cols, &dd));
-    TRY(upload(P, S.d_pass_scale, S.pass_scale, &sc));
-  }
+  BlobBuilder B;
+  const size_t o_goff = B.add(S.h_goff), o_hcols = B.add(S.h_cols), o_hv = B.add(S.h_hv);
+  const size_t o_src = B.add(S.src_cols), o_dst = B.add(S.dst_cols);
+  const size_t o_cs = B.add(S.cs_h);  // cs_h may carry the sign alignment
+  const size_t o_ps = B.add(S.pass_src), o_pd = B.add(S.pass_dst_cols), o_pc = B.add(S.pass_scale);
+  if (S.na > 0) cauchy_stage(S.cp, B);
+  char* base;
+  TRY(arena_put_blob(P, B, S.blob, &base));
+  S.dgoff = reinterpret_cast<int32_t*>(base + o_goff);
+  S.dhcols = reinterpret_cast<int32_t*>(base + o_hcols);
+  S.dhv = reinterpret_cast<double*>(base + o_hv);
+  S.dsrc = reinterpret_cast<int32_t*>(base + o_src);
+  S.ddst = reinterpret_cast<int32_t*>(base + o_dst);
+  S.dcs = reinterpret_cast<double*>(base + o_cs);
+  S.dpsrc = reinterpret_cast<int32_t*>(base + o_ps);
+  S.dpdst = reinterpret_cast<int32_t*>(base + o_pd);
+  S.dpscale = reinterpret_cast<double*>(base + o_pc);
+  if (S.na > 0) TRY(cauchy_bind(S.cp, base));
   return SVD1_OK;
 }
 
@@ -1342,18 +1439,15 @@ svd1_status apply_launch(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_
   if (rows <= 0) return SVD1_OK;
   TRY(ev_record(P, ev0, st));
   if (S.h_goff.size() > 1)
-    TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1,
-                         static_cast<int32_t*>(S.d_goff.p), static_cast<int32_t*>(S.d_hcols.p),
-                         static_cast<double*>(S.d_hv.p), st, &P->launches));
+    TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, st,
+                         &P->launches));
   if (S.na > 0)
     TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
-                      static_cast<double*>(S.d_out.p) + S.na, static_cast<double*>(S.d_zhat.p),
-                      static_cast<double*>(S.d_cs.p), U_in, ld_in, static_cast<int32_t*>(S.d_src.p),
-                      U_out, ld_out, static_cast<int32_t*>(S.d_dst.p), st, side));
+                      static_cast<double*>(S.d_out.p) + S.na, static_cast<double*>(S.d_zhat.p), S.dcs,
+                      U_in, ld_in, S.dsrc, U_out, ld_out, S.ddst, st, side));
   if (!S.pass_src.empty())
-    TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, static_cast<int32_t*>(S.d_pass_src.p),
-                    U_out, ld_out, static_cast<int32_t*>(S.d_pass_dst.p),
-                    static_cast<double*>(S.d_pass_scale.p), st, &P->launches));
+    TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, S.dpsrc, U_out, ld_out, S.dpdst, S.dpscale,
+                    st, &P->launches));
   TRY(ev_record(P, ev0 + 1, st));
   return SVD1_OK;
 }
@@ -1522,12 +1616,12 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   // stream stays busy.  The Cauchy/FMM plan of each first apply depends on that side's
   // round 1 only and is built on a worker thread meanwhile.
   const double tA = now_ms();
-  Joiner planners;
+  Joiner plan_u, plan_v;
   const svd1_config pcfg = P->cfg;
   const int pp = P->p;
   // U: finish STEP 4, launch STEP 5 (rho2, z2 = X1^T U^T b1)
   TRY(spectral_finish(P, S[0], Du, cu));
-  planners.add(std::thread([&S, pcfg, pp, rows = c.u_rows] { apply_plan(pcfg, pp, S[0], rows, false, 0); }));
+  plan_u.add(std::thread([&S, pcfg, pp, rows = c.u_rows] { apply_plan(pcfg, pp, S[0], rows, false, 0); }));
   {
     std::vector<double> z2 = cu[0];
     cu.erase(cu.begin());
@@ -1536,24 +1630,27 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   const double tB = now_ms();
   // V: finish STEP 6, launch STEP 7 (rho4)
   TRY(spectral_finish(P, S[2], Dv, cv));
-  planners.add(std::thread([&S, pcfg, pp, rows = c.v_rows] { apply_plan(pcfg, pp, S[2], rows, false, 1); }));
+  plan_v.add(std::thread([&S, pcfg, pp, rows = c.v_rows] { apply_plan(pcfg, pp, S[2], rows, false, 1); }));
   {
     std::vector<double> z4 = cv[0];
     cv.erase(cv.begin());
     TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14));
   }
+  // whatever finishes first goes first: U's plan and round 2, then V's
   const double tC = now_ms();
-  planners.join();
+  plan_u.join();
   TRY(apply_upload(P, S[0]));
-  TRY(apply_upload(P, S[2]));
-  const double tD = now_ms();
+  const double tC2 = now_ms();
   TRY(spectral_finish(P, S[1], Du, cu));
+  const double tD = now_ms();
+  plan_v.join();
+  TRY(apply_upload(P, S[2]));
   const double tE = now_ms();
   TRY(spectral_finish(P, S[3], Dv, cv));
   const double tF = now_ms();
   if (std::getenv("SVD1_TIMING"))
-    fprintf(stderr, "[svd1] launch1 %.3f U1->U2 %.3f V1->V2 %.3f plans+uploads %.3f finish U2 %.3f finish V2 %.3f\n",
-            tA - t1, tB - tA, tC - tB, tD - tC, tE - tD, tF - tE);
+    fprintf(stderr, "[svd1] launch1 %.3f U1->U2 %.3f V1->V2 %.3f U plan+upload %.3f finish U2 %.3f V plan+upload %.3f finish V2 %.3f (plans %.3f %.3f)\n",
+            tA - t1, tB - tA, tC - tB, tC2 - tC, tD - tC2, tE - tD, tF - tE, S[0].plan_ms, S[2].plan_ms);
   const double t3 = now_ms();
   R.t_ms[1] = t3 - t1;
   // ---- sign alignment: final column i = position N-1-i
