@@ -874,7 +874,8 @@ void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
                  const std::vector<double>& da, const std::vector<double>& mu, int p,
                  const int32_t* src, int n_in) {
   const int minn = cfg.fmm_min_n > 0 ? cfg.fmm_min_n : 384;
-  const int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2: s ~ 2p, capped by the tile
+  int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2: s ~ 2p, capped by the tile
+  if (const char* e = std::getenv("SVD1_LEAF")) leaf = std::max(4, std::min(kMaxLeaf, atoi(e)));  // tuning
   bool fmm = (cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
   if (cfg.flags & SVD1_FORCE_DIRECT) fmm = false;
   C.fmm = fmm;
