@@ -94,6 +94,9 @@ typedef struct {
   double apply_flops_exec[4]; /* flops each apply executes: as apply_flops, except that the
                             coarse M2M / L2L levels run in bands, which
                             trade a few flops for fewer launches */
+  double gemm_ms[4];     /* device time of each apply's FMM GEMM passes (CUDA events around
+                            every pass launch on its stream) when the environment variable
+                            SVD1_GEMM_EVENTS is set (diagnostics), else 0 */
 } svd1_report;
 
 /* Plan: owns workspaces on the device (sized for u_rows x m and v_rows x n),

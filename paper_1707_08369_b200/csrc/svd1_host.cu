@@ -115,8 +115,21 @@ struct CauchyPrep {
   int32_t* dcol2src = nullptr;
   size_t o_cells = 0, o_descs = 0, o_terms = 0, o_tasks = 0, o_c2s = 0;
   FmmMaps* h_maps = nullptr;  // pinned staging of the TMA descriptors (copied on the apply stream)
+  std::vector<cudaEvent_t> gev;  // events around each GEMM pass of the last launch
+  int ngev = 0;
   ~CauchyPrep() {
     if (h_maps) cudaFreeHost(h_maps);
+    for (auto e : gev) cudaEventDestroy(e);
+  }
+  // device time of the GEMM passes of the last launch (after it completed)
+  double gemm_ms() const {
+    double t = 0.0;
+    for (int i = 0; i + 1 < ngev; i += 2) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, gev[i], gev[i + 1]) == cudaSuccess) t += ms;
+      else cudaGetLastError();
+    }
+    return t;
   }
 };
 
@@ -192,17 +205,20 @@ struct svd1_plan_s {
   StepRecord steps[4];
   double* h_pin = nullptr;  // pinned staging for read-backs
   size_t h_pin_cap = 0;
-  // pinned upload arena: every host->device upload is copied here first, so the DMA
-  // never reads pageable or short-lived host memory; reset only after `arena_ev`.
-  char* arena = nullptr;
-  size_t arena_cap = 0, arena_used = 0;
-  cudaEvent_t arena_ev = nullptr;
-  bool arena_pending = false;
+  // pinned upload arenas, one per side stream (U side: st, V side: st2): every
+  // host->device upload is copied here first, so the DMA never reads pageable or
+  // short-lived host memory; an arena is rewound only after its last copy (`ev`).
+  struct Arena {
+    char* buf = nullptr;
+    size_t cap = 0, used = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  } arena[2];
   CauchyPrep standalone;    // plan of the standalone svd1_cauchy_apply
   std::vector<int32_t> rot_goff, rot_cols;  // pairing rotations of repeated sigma clusters
   std::vector<double> rot_mats;
   DevBuf d_rot_goff, d_rot_cols, d_rot_mats;
-  cudaEvent_t ev[18] = {};  // timing events (spectral / apply phases)
+  cudaEvent_t ev[20] = {};  // timing events (spectral / apply phases)
 };
 
 namespace {
@@ -222,38 +238,66 @@ svd1_status pinned(svd1_plan_t P, size_t doubles, double** out) {
   return SVD1_OK;
 }
 
-// Wait for the uploads in flight and rewind the arena (called at API entry points).
-svd1_status arena_reset(svd1_plan_t P) {
-  if (P->arena_pending) SVD1_CUDA_TRY(cudaEventSynchronize(P->arena_ev));
-  P->arena_pending = false;
-  P->arena_used = 0;
+svd1_status ensure_st2(svd1_plan_t P) {
+  if (!P->st2) SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->st2, cudaStreamNonBlocking));
   return SVD1_OK;
 }
+// side 0 (U) works on the plan stream, side 1 (V) on st2
+cudaStream_t side_stream(svd1_plan_t P, int side) { return side ? P->st2 : P->st; }
 
-svd1_status arena_put(svd1_plan_t P, const void* src, size_t bytes, void* dev) {
-  if (!P->arena_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->arena_ev, cudaEventDisableTiming));
-  const size_t off = (P->arena_used + 255) & ~size_t(255);
-  if (off + bytes > P->arena_cap) {
-    TRY(arena_reset(P));  // everything staged so far has been consumed
-    if (bytes > P->arena_cap) {
-      if (P->arena) cudaFreeHost(P->arena);
-      P->arena = nullptr;
-      P->arena_cap = 0;
+// Wait for the uploads in flight and rewind the arenas (called at API entry points).
+svd1_status arena_reset(svd1_plan_t P, int side) {
+  auto& A = P->arena[side];
+  if (A.pending) SVD1_CUDA_TRY(cudaEventSynchronize(A.ev));
+  A.pending = false;
+  A.used = 0;
+  return SVD1_OK;
+}
+svd1_status arena_reset(svd1_plan_t P) {
+  TRY(arena_reset(P, 0));
+  return arena_reset(P, 1);
+}
+
+// reserve `bytes` of side's arena (rewinding or growing it when full): offset
+svd1_status arena_reserve(svd1_plan_t P, int side, size_t bytes, size_t* off_out) {
+  auto& A = P->arena[side];
+  if (!A.ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&A.ev, cudaEventDisableTiming));
+  size_t off = (A.used + 255) & ~size_t(255);
+  if (off + bytes > A.cap) {
+    TRY(arena_reset(P, side));  // everything staged so far has been consumed
+    if (bytes > A.cap) {
+      if (A.buf) cudaFreeHost(A.buf);
+      A.buf = nullptr;
+      A.cap = 0;
       const size_t cap = std::max<size_t>(bytes * 2, size_t(4) << 20);
-      if (cudaMallocHost(&P->arena, cap) != cudaSuccess) {
+      if (cudaMallocHost(&A.buf, cap) != cudaSuccess) {
         cudaGetLastError();
         return SVD1_E_NOMEM;
       }
-      P->arena_cap = cap;
+      A.cap = cap;
     }
-    return arena_put(P, src, bytes, dev);
+    off = 0;
   }
-  std::memcpy(P->arena + off, src, bytes);
-  SVD1_CUDA_TRY(cudaMemcpyAsync(dev, P->arena + off, bytes, cudaMemcpyHostToDevice, P->st));
-  SVD1_CUDA_TRY(cudaEventRecord(P->arena_ev, P->st));
-  P->arena_pending = true;
-  P->arena_used = off + bytes;
+  *off_out = off;
   return SVD1_OK;
+}
+
+svd1_status arena_commit(svd1_plan_t P, int side, size_t off, size_t bytes, void* dev) {
+  auto& A = P->arena[side];
+  const cudaStream_t st = side_stream(P, side);
+  SVD1_CUDA_TRY(cudaMemcpyAsync(dev, A.buf + off, bytes, cudaMemcpyHostToDevice, st));
+  SVD1_CUDA_TRY(cudaEventRecord(A.ev, st));
+  A.pending = true;
+  A.used = off + bytes;
+  return SVD1_OK;
+}
+
+svd1_status arena_put(svd1_plan_t P, const void* src, size_t bytes, void* dev, int side = 0) {
+  if (side) TRY(ensure_st2(P));
+  size_t off;
+  TRY(arena_reserve(P, side, bytes, &off));
+  std::memcpy(P->arena[side].buf + off, src, bytes);
+  return arena_commit(P, side, off, bytes, dev);
 }
 
 // Several host arrays staged as ONE pinned-arena region and ONE host->device copy into
@@ -274,33 +318,15 @@ struct BlobBuilder {
   }
 };
 
-svd1_status arena_put_blob(svd1_plan_t P, const BlobBuilder& B, DevBuf& dev, char** out) {
+svd1_status arena_put_blob(svd1_plan_t P, const BlobBuilder& B, DevBuf& dev, char** out, int side = 0) {
+  if (side) TRY(ensure_st2(P));
   TRY(dev.get<char>(std::max<size_t>(B.total, 1), out));
   if (B.total == 0) return SVD1_OK;
-  if (!P->arena_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->arena_ev, cudaEventDisableTiming));
-  size_t off = (P->arena_used + 255) & ~size_t(255);
-  if (off + B.total > P->arena_cap) {
-    TRY(arena_reset(P));
-    if (B.total > P->arena_cap) {
-      if (P->arena) cudaFreeHost(P->arena);
-      P->arena = nullptr;
-      P->arena_cap = 0;
-      const size_t cap = std::max<size_t>(B.total * 2, size_t(4) << 20);
-      if (cudaMallocHost(&P->arena, cap) != cudaSuccess) {
-        cudaGetLastError();
-        return SVD1_E_NOMEM;
-      }
-      P->arena_cap = cap;
-    }
-    off = 0;
-  }
+  size_t off;
+  TRY(arena_reserve(P, side, B.total, &off));
   for (const auto& q : B.parts)
-    if (q.bytes) std::memcpy(P->arena + off + q.off, q.p, q.bytes);
-  SVD1_CUDA_TRY(cudaMemcpyAsync(*out, P->arena + off, B.total, cudaMemcpyHostToDevice, P->st));
-  SVD1_CUDA_TRY(cudaEventRecord(P->arena_ev, P->st));
-  P->arena_pending = true;
-  P->arena_used = off + B.total;
-  return SVD1_OK;
+    if (q.bytes) std::memcpy(P->arena[side].buf + off + q.off, q.p, q.bytes);
+  return arena_commit(P, side, off, B.total, *out);
 }
 
 svd1_status ev_record(svd1_plan_t P, int i, cudaStream_t st = nullptr) {
@@ -326,9 +352,9 @@ double ev_ms(svd1_plan_t P, int a, int b) {
 }
 
 template <class T>
-svd1_status upload(svd1_plan_t P, DevBuf& buf, const std::vector<T>& v, T** out) {
+svd1_status upload(svd1_plan_t P, DevBuf& buf, const std::vector<T>& v, T** out, int side = 0) {
   TRY(buf.get<T>(v.size(), out));
-  if (!v.empty()) TRY(arena_put(P, v.data(), v.size() * sizeof(T), *out));
+  if (!v.empty()) TRY(arena_put(P, v.data(), v.size() * sizeof(T), *out, side));
   return SVD1_OK;
 }
 
@@ -461,7 +487,6 @@ struct Csr {
 void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   const double tt0 = now_ms();
   const int L = F.L;
-  auto nonempty = [&](int c) { return F.cells[c].hi > F.cells[c].lo; };
   auto has_src = [&](int c) { return F.cells[c].shi > F.cells[c].slo; };
   auto has_tgt = [&](int c) { return F.cells[c].thi > F.cells[c].tlo; };
   auto adm = [&](int x, int y) {
@@ -807,7 +832,6 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   if (std::getenv("SVD1_DEBUG"))
     fprintf(stderr, "[svd1] lists: traversal %.3f ms, generation %.3f ms (ops %zu terms %zu tasks %zu)\n",
             tt1 - tt0, now_ms() - tt1, F.ops.size(), F.terms.size(), F.tasks.size());
-  (void)nonempty;
 }
 
 }  // namespace
@@ -1070,10 +1094,25 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
     }
   } ptp{&pev};
   pmark();
+  C.ngev = 0;
+  const bool gtime = std::getenv("SVD1_GEMM_EVENTS") != nullptr;  // diagnostics (host cost)
+  auto gmark = [&]() -> svd1_status {  // events bracketing each GEMM pass
+    if (!gtime) return SVD1_OK;
+    if (C.ngev == int(C.gev.size())) {
+      cudaEvent_t e;
+      SVD1_CUDA_TRY(cudaEventCreate(&e));
+      C.gev.push_back(e);
+    }
+    SVD1_CUDA_TRY(cudaEventRecord(C.gev[C.ngev++], st));
+    return SVD1_OK;
+  };
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
+    if (e <= b) continue;
+    TRY(gmark());
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, maps, U_out, ld_out, d_dst, phi, psi, ldE,
                       C.n_out, int64_t(exp_elems), ops, F.ops_rows, st, &P->launches));
+    TRY(gmark());
     pmark();
     if (dbg) {
       cudaError_t err = cudaStreamSynchronize(st);
@@ -1091,7 +1130,7 @@ svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
     void* before = b->p;
     double* x;
     TRY(b->get<double>(elems, &x));
-    if (b->p != before) SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, P->st));
+    if (b->p != before) SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, side_stream(P, side)));
   }
   return SVD1_OK;
 }
@@ -1115,7 +1154,9 @@ struct Joiner {
 // secular solve (STEP 2), Loewner, column norms and carried X^T v, and their read-back.
 svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<double>& D,
                             const std::vector<double>& z, double rho,
-                            const std::vector<std::vector<double>>& carries, int ev0) {
+                            const std::vector<std::vector<double>>& carries, int ev0, int side) {
+  if (side) TRY(ensure_st2(P));
+  const cudaStream_t st = side_stream(P, side);
   const double th_start = now_ms();
   const int N = int(D.size());
   S.clear_host();  // device buffers are kept (grow-only)
@@ -1242,7 +1283,7 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
       z2r[i] = za[src] * za[src];
     }
     std::memcpy(stage.data() + 4 * na, carry_act.data(), size_t(nc) * na * sizeof(double));
-    TRY(arena_put(P, stage.data(), in_words * sizeof(double), din));
+    TRY(arena_put(P, stage.data(), in_words * sizeof(double), din, side));
   }
   double* dda = din;
   double* dza = din + na;
@@ -1257,14 +1298,14 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   int32_t* dst = reinterpret_cast<int32_t*>(dout + words - 1);
   double* dzh;
   TRY(S.d_zhat.get<double>(na, &dzh));
-  SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
-  TRY(ev_record(P, ev0));
+  SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), st));
+  TRY(ev_record(P, ev0, st));
   double* scr;
   TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
-  TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, P->st, &P->launches));   // STEP 2
-  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, P->st, &P->launches));
-  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, P->st, &P->launches));
-  TRY(ev_record(P, ev0 + 1));
+  TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, st, &P->launches));   // STEP 2
+  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, st, &P->launches));
+  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, st, &P->launches));
+  TRY(ev_record(P, ev0 + 1, st));
   if (words * sizeof(double) > S.rb_cap) {
     if (S.rb) cudaFreeHost(S.rb);
     S.rb = nullptr;
@@ -1275,9 +1316,9 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     }
     S.rb_cap = words * sizeof(double);
   }
-  SVD1_CUDA_TRY(cudaMemcpyAsync(S.rb, dout, words * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(S.rb, dout, words * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (!S.done_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&S.done_ev, cudaEventDisableTiming));
-  SVD1_CUDA_TRY(cudaEventRecord(S.done_ev, P->st));
+  SVD1_CUDA_TRY(cudaEventRecord(S.done_ev, st));
   S.pending = true;
   if (std::getenv("SVD1_TIMING"))
     fprintf(stderr, "[svd1] spectral_launch N=%d: host prep %.3f ms, stage+launch %.3f ms\n", N,
@@ -1397,7 +1438,7 @@ void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool
   if (S.na > 0) cauchy_plan(cfg, S.cp, rows, S.na, S.da, S.mu, p, S.src_cols.data(), S.N);
 }
 
-svd1_status apply_upload(svd1_plan_t P, StepRecord& S) {
+svd1_status apply_upload(svd1_plan_t P, StepRecord& S, int side) {
   if (S.rows <= 0) return SVD1_OK;
   BlobBuilder B;
   const size_t o_goff = B.add(S.h_goff), o_hcols = B.add(S.h_cols), o_hv = B.add(S.h_hv);
@@ -1406,7 +1447,7 @@ svd1_status apply_upload(svd1_plan_t P, StepRecord& S) {
   const size_t o_ps = B.add(S.pass_src), o_pd = B.add(S.pass_dst_cols), o_pc = B.add(S.pass_scale);
   if (S.na > 0) cauchy_stage(S.cp, B);
   char* base;
-  TRY(arena_put_blob(P, B, S.blob, &base));
+  TRY(arena_put_blob(P, B, S.blob, &base, side));
   S.dgoff = reinterpret_cast<int32_t*>(base + o_goff);
   S.dhcols = reinterpret_cast<int32_t*>(base + o_hcols);
   S.dhv = reinterpret_cast<double*>(base + o_hv);
@@ -1417,19 +1458,6 @@ svd1_status apply_upload(svd1_plan_t P, StepRecord& S) {
   S.dpdst = reinterpret_cast<int32_t*>(base + o_pd);
   S.dpscale = reinterpret_cast<double*>(base + o_pc);
   if (S.na > 0) TRY(cauchy_bind(S.cp, base));
-  return SVD1_OK;
-}
-
-// Plan two steps concurrently (one worker thread), then stage their uploads.
-svd1_status apply_prepare2(svd1_plan_t P, StepRecord& A, int64_t rows_a, StepRecord& B,
-                           int64_t rows_b, bool reverse) {
-  const svd1_config cfg = P->cfg;
-  const int p = P->p;
-  std::thread worker([&] { apply_plan(cfg, p, B, rows_b, reverse, 1); });
-  apply_plan(cfg, p, A, rows_a, reverse, 0);
-  worker.join();
-  TRY(apply_upload(P, A));
-  TRY(apply_upload(P, B));
   return SVD1_OK;
 }
 
@@ -1500,9 +1528,12 @@ svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out) {
 svd1_status svd1_plan_destroy(svd1_plan_t P) {
   if (!P) return SVD1_E_INVALID;
   cudaStreamSynchronize(P->st);
+  if (P->st2) cudaStreamSynchronize(P->st2);
   if (P->h_pin) cudaFreeHost(P->h_pin);
-  if (P->arena) cudaFreeHost(P->arena);
-  if (P->arena_ev) cudaEventDestroy(P->arena_ev);
+  for (auto& A : P->arena) {
+    if (A.buf) cudaFreeHost(A.buf);
+    if (A.ev) cudaEventDestroy(A.ev);
+  }
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : P->sync_ev)
@@ -1597,8 +1628,27 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     for (int q = 0; q < kNumProbes; ++q)       // V^T A_hat^T g = Sigma^T U^T g + (V^T b)(a.g)
       cv[1 + q][i] = (i < m ? sig[i] * xg[q * m + i] : 0.0) + yb[i] * ag[q];
   }
-  // ---- spectral phase: all four eigen-updates before any write to U or V.
-  // Round 1: STEP 4 (U, rho1) and STEP 6 (V, rho3) together.
+  // ---- workspaces for the applies (sized up front: a mid-stream realloc would sync)
+  TRY(ensure_st2(P));
+  double *Wu = nullptr, *Wv = nullptr;
+  if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
+  if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * n, &Wv));
+  {
+    const int64_t rows_max = std::max(c.u_rows, c.v_rows);
+    const size_t guess = size_t(rows_max) * size_t(P->p) *
+                         size_t(4 * std::max<int64_t>(n, 1) / std::max(P->leaf, 1) + 8);
+    for (int side = 0; side < 2; ++side) TRY(ensure_expansions(P, side, guess));
+  }
+  const bool one_stream = std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
+  cudaStream_t stv = one_stream ? P->st : P->st2;
+  // ---- spectral phase.  Each side is a chain on its own stream (U: the plan stream,
+  // V: st2): STEP 4 -> STEP 5 and STEP 6 -> STEP 7.  The chains are
+  // interleaved on the host, so each side's host step (finish one eigen-update, launch
+  // the next) overlaps the other side's GPU work; the FMM plan of each apply is built on
+  // a worker thread as soon as its eigen-update is known, and a first apply whose input
+  // is not transformed in place (no Householder group) starts as soon as it is planned:
+  // it writes only the workspace W, so U, Sigma and V stay untouched until every
+  // eigen-update has succeeded.
   const double t1 = now_ms();
   StepRecord* S = P->steps;
   {
@@ -1609,15 +1659,11 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     cv1.insert(cv1.begin(), cv[0]);
     cu.swap(cu1);
     cv.swap(cv1);
-    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8));
-    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12));
+    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8, 0));
+    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, one_stream ? 0 : 1));
   }
-  // The two sides' chains are interleaved: each side's host step (finish one
-  // eigen-update, launch the next) runs while the GPU works on the other side's, so the
-  // stream stays busy.  The Cauchy/FMM plan of each first apply depends on that side's
-  // round 1 only and is built on a worker thread meanwhile.
   const double tA = now_ms();
-  Joiner plan_u, plan_v;
+  Joiner plan_u, plan_v, plan_u2, plan_v2;
   const svd1_config pcfg = P->cfg;
   const int pp = P->p;
   // U: finish STEP 4, launch STEP 5 (rho2, z2 = X1^T U^T b1)
@@ -1626,7 +1672,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   {
     std::vector<double> z2 = cu[0];
     cu.erase(cu.begin());
-    TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10));
+    TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, 0));
   }
   const double tB = now_ms();
   // V: finish STEP 6, launch STEP 7 (rho4)
@@ -1635,19 +1681,40 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   {
     std::vector<double> z4 = cv[0];
     cv.erase(cv.begin());
-    TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14));
+    TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, one_stream ? 0 : 1));
   }
-  // whatever finishes first goes first: U's plan and round 2, then V's
   const double tC = now_ms();
+  auto rare_grow = [&](int e, int side) -> svd1_status {  // deeper tree than guessed
+    if (S[e].rows > 0 && S[e].na > 0 && cauchy_exp_elems(S[e].cp) > P->phi[side].cap / sizeof(double)) {
+      SVD1_CUDA_TRY(cudaDeviceSynchronize());
+      TRY(ensure_expansions(P, side, cauchy_exp_elems(S[e].cp)));
+    }
+    return SVD1_OK;
+  };
+  bool launched_u1 = false, launched_v1 = false;
   plan_u.join();
-  TRY(apply_upload(P, S[0]));
+  TRY(rare_grow(0, 0));
+  TRY(apply_upload(P, S[0], 0));
+  if (S[0].h_goff.size() <= 1) {  // nothing in place: start now
+    TRY(ev_record(P, 16, P->st));
+    TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
+    launched_u1 = true;
+  }
   const double tC2 = now_ms();
   TRY(spectral_finish(P, S[1], Du, cu));
+  plan_u2.add(std::thread([&S, pcfg, pp, rows = c.u_rows] { apply_plan(pcfg, pp, S[1], rows, true, 0); }));
   const double tD = now_ms();
   plan_v.join();
-  TRY(apply_upload(P, S[2]));
+  TRY(rare_grow(2, 1));
+  TRY(apply_upload(P, S[2], one_stream ? 0 : 1));
+  if (S[2].h_goff.size() <= 1) {
+    TRY(ev_record(P, 18, stv));
+    TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
+    launched_v1 = true;
+  }
   const double tE = now_ms();
   TRY(spectral_finish(P, S[3], Dv, cv));
+  plan_v2.add(std::thread([&S, pcfg, pp, rows = c.v_rows] { apply_plan(pcfg, pp, S[3], rows, true, 1); }));
   const double tF = now_ms();
   if (std::getenv("SVD1_TIMING"))
     fprintf(stderr, "[svd1] launch1 %.3f U1->U2 %.3f V1->V2 %.3f U plan+upload %.3f finish U2 %.3f V plan+upload %.3f finish V2 %.3f (plans %.3f %.3f)\n",
@@ -1785,50 +1852,34 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     R.n_deflated[e] = S[e].N - S[e].na;
     R.max_iter[e] = S[e].max_iter;
   }
-  // ---- applies (vector parts of STEPS 4-7): U -> W_u -> U, V -> W_v -> V.
-  // The first apply of each side was planned during round 2; launch both, then plan
-  // the second applies on the host while the GPU runs the first ones.
+  // ---- applies (vector parts of STEPS 4-7): U -> W_u -> U, V -> W_v -> V.  Every
+  // eigen-update succeeded: the first applies that transform their input in place can
+  // start now; the second applies follow as soon as their plans are uploaded.
   const double t4 = now_ms();
-  double *Wu = nullptr, *Wv = nullptr;
-  if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
-  if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * n, &Wv));
-  // expansions are sized for all four applies up front (a mid-stream realloc would sync)
-  const int64_t rows_max = std::max(c.u_rows, c.v_rows);
-  const size_t guess = size_t(rows_max) * size_t(P->p) *
-                       size_t(4 * std::max<int64_t>(n, 1) / std::max(P->leaf, 1) + 8);
-  for (int side = 0; side < 2; ++side) {
-    const int e = 2 * side;
-    size_t need = guess;
-    if (S[e].rows > 0 && S[e].na > 0) need = std::max(need, cauchy_exp_elems(S[e].cp));
-    TRY(ensure_expansions(P, side, need));
+  if (!launched_u1) {
+    TRY(ev_record(P, 16, P->st));
+    TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
   }
-  if (!P->st2) SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->st2, cudaStreamNonBlocking));
-  // U side on the plan stream, V side on st2 (independent until the end of the update)
-  TRY(stream_wait(P, 0, P->st, P->st2));  // uploads of the first applies, W buffers
-  TRY(ev_record(P, 16, P->st));           // apply phase start (both sides)
-  TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
-  const bool one_stream = std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
-  cudaStream_t stv = one_stream ? P->st : P->st2;
-  TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
-  TRY(apply_prepare2(P, S[1], c.u_rows, S[3], c.v_rows, true));
-  for (int e : {1, 3}) {
-    const int side = e / 2;
-    if (S[e].rows > 0 && S[e].na > 0 &&
-        cauchy_exp_elems(S[e].cp) > P->phi[side].cap / sizeof(double)) {
-      SVD1_CUDA_TRY(cudaDeviceSynchronize());  // rare: deeper tree than guessed
-      TRY(ensure_expansions(P, side, cauchy_exp_elems(S[e].cp)));
-    }
+  if (!launched_v1) {
+    TRY(ev_record(P, 18, stv));
+    TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
   }
+  plan_u2.join();
+  TRY(rare_grow(1, 0));
+  TRY(apply_upload(P, S[1], 0));
+  TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
+  plan_v2.join();
+  TRY(rare_grow(3, 1));
+  TRY(apply_upload(P, S[3], one_stream ? 0 : 1));  // carries the sign alignment
   const int nrot = int(P->rot_goff.size()) - 1;
   if (nrot > 0 && c.v_rows > 0) {
     int32_t *g, *cl;
     double* mt;
-    TRY(upload(P, P->d_rot_goff, P->rot_goff, &g));
-    TRY(upload(P, P->d_rot_cols, P->rot_cols, &cl));
-    TRY(upload(P, P->d_rot_mats, P->rot_mats, &mt));
+    const int sd = one_stream ? 0 : 1;
+    TRY(upload(P, P->d_rot_goff, P->rot_goff, &g, sd));
+    TRY(upload(P, P->d_rot_cols, P->rot_cols, &cl, sd));
+    TRY(upload(P, P->d_rot_mats, P->rot_mats, &mt, sd));
   }
-  TRY(stream_wait(P, 1, P->st, P->st2));  // uploads of the V-side second apply
-  TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
   TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, stv, 1));
   if (nrot > 0 && c.v_rows > 0)
     TRY(col_rotate(c.v_rows, V, ldv, nrot, static_cast<int32_t*>(P->d_rot_goff.p),
@@ -1847,6 +1898,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     R.apply_ms[e] = has ? ev_ms(P, 2 * e, 2 * e + 1) : 0.0;
     R.apply_flops[e] = (has && S[e].na > 0) ? S[e].cp.flops : 0.0;
     R.apply_flops_exec[e] = (has && S[e].na > 0) ? S[e].cp.flops_exec : 0.0;
+    R.gemm_ms[e] = (has && S[e].na > 0 && S[e].cp.fmm) ? S[e].cp.gemm_ms() : 0.0;
     R.fmm_used[e] = (has && S[e].na > 0) ? S[e].cp.fmm : 0;
     if (R.fmm_used[e]) {
       R.fmm_levels[e] = S[e].cp.F.L;
@@ -1856,7 +1908,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     R.mean_iter[e] = S[e].mean_iter;
   }
   R.t_ms[4] = now_ms() - t0;
-  R.t_ms[5] = ev_ms(P, 16, 17);
+  R.t_ms[5] = std::max(ev_ms(P, 16, 17), ev_ms(P, 18, 17));  // both sides' applies
   R.kernel_launches = P->launches - launches0;
   if (rep) *rep = R;
   return SVD1_OK;
