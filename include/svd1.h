@@ -53,6 +53,10 @@ typedef enum {
 /* flags */
 #define SVD1_FORCE_DIRECT 0x1u /* always use the direct Cauchy-on-the-fly apply */
 #define SVD1_FORCE_FMM 0x2u    /* use the FMM apply whenever n_active >= 2 leaves */
+#define SVD1_SECULAR_FMM 0x4u  /* secular solve with the FMM far field for
+                                  every size above 64 (default: from 6144 roots, or the
+                                  environment variable SVD1_SEC_FMM_MIN) */
+#define SVD1_SECULAR_DIRECT 0x8u /* secular solve with the direct O(n) sums only */
 
 typedef struct {
   int64_t m, n;      /* global sizes, 1 <= m <= n */

@@ -76,6 +76,8 @@ EXPORTS = ["svd1_plan_create", "svd1_plan_destroy", "svd1_update", "svd1_project
 
 FORCE_DIRECT = 0x1
 FORCE_FMM = 0x2
+SECULAR_FMM = 0x4     # secular solve with the FMM far field at every size > 64
+SECULAR_DIRECT = 0x8  # secular solve with direct sums only
 
 
 def status_string(code: int) -> str:

@@ -168,27 +168,73 @@ struct SecAcc {
 // d, z2 are the rho > 0 view (reflected by the host when rho < 0; z2 = z^2).  Left set
 // i <= sp (psi, all terms negative), right set i > sp (phi, one sign), so
 // sum |z_i^2/delta_i| = |psi| + |phi|.
+// Reduction groups: one warp per root, or one block per root (the FMM path's few
+// direct roots, so they do not set the kernel's tail).
+struct WarpGrp {
+  int tid;
+  static constexpr int size = 32;
+  __device__ double sum(double v) const { return warp_sum(v); }
+  __device__ void sum4(double& a, double& b, double& c, double& d) const {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    d = warp_sum(d);
+  }
+};
+struct BlockGrp {  // all threads of the block call sum() together (uniform control flow)
+  int tid, size;
+  double* sm;      // 4 * 8 doubles (blockDim.x <= 256)
+  __device__ double sum(double v) const {
+    v = warp_sum(v);
+    __syncthreads();
+    if ((tid & 31) == 0) sm[tid >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int q = 0; q < (size >> 5); ++q) s += sm[q];
+    return s;
+  }
+  __device__ void sum4(double& a, double& b, double& c, double& d) const {  // sm: 4 * 8 doubles
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    d = warp_sum(d);
+    __syncthreads();
+    if ((tid & 31) == 0) {
+      sm[tid >> 5] = a;
+      sm[8 + (tid >> 5)] = b;
+      sm[16 + (tid >> 5)] = c;
+      sm[24 + (tid >> 5)] = d;
+    }
+    __syncthreads();
+    a = b = c = d = 0.0;
+    for (int q = 0; q < (size >> 5); ++q) {
+      a += sm[q];
+      b += sm[8 + q];
+      c += sm[16 + q];
+      d += sm[24 + q];
+    }
+  }
+};
+
+template <class G>
 __device__ SecAcc sec_eval(const double* __restrict__ d, const double* __restrict__ z2, int n,
-                           double dk, double tau, int sp, int lane) {
+                           double dk, double tau, int sp, const G& g) {
   SecAcc a = {0, 0, 0, 0, 0};
 #pragma unroll 4
-  for (int i = lane; i <= sp; i += 32) {
+  for (int i = g.tid; i <= sp; i += g.size) {
     const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
     const double t = __ldg(z2 + i) * rr;
     a.psi += t;
     a.dpsi = fma(t, rr, a.dpsi);
   }
 #pragma unroll 4
-  for (int i = sp + 1 + lane; i < n; i += 32) {
+  for (int i = sp + 1 + g.tid; i < n; i += g.size) {
     const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
     const double t = __ldg(z2 + i) * rr;
     a.phi += t;
     a.dphi = fma(t, rr, a.dphi);
   }
-  a.psi = warp_sum(a.psi);
-  a.phi = warp_sum(a.phi);
-  a.dpsi = warp_sum(a.dpsi);
-  a.dphi = warp_sum(a.dphi);
+  g.sum4(a.psi, a.phi, a.dpsi, a.dphi);
   a.eabs = fabs(a.psi) + fabs(a.phi);
   return a;
 }
@@ -231,7 +277,8 @@ __device__ __forceinline__ double sec_step(double w, const SecAcc& a, double r, 
     if (tn == tau) return tau;               // step below the resolution of tau: converged
     if (tn > lo && tn < hi) return tn;
   }
-  return 0.5 * (lo + hi);                    // bisection safeguard
+  // bisection safeguard (geometric across a bracket spanning many binades)
+  return (lo > 0.0 && hi > 64.0 * lo) ? sqrt(lo) * sqrt(hi) : 0.5 * (lo + hi);
 }
 
 constexpr int kSecMaxIt = 100;
@@ -247,15 +294,75 @@ __global__ void secular_orient_kernel(const double* __restrict__ d, const double
   z2r[i] = z[src] * z[src];
 }
 
-__global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__ d,
-                                                     const double* __restrict__ z2, double rho, int n,
-                                                     int32_t* __restrict__ k_out,
-                                                     double* __restrict__ tau_out,
-                                                     int32_t* __restrict__ iters_out,
-                                                     int32_t* __restrict__ status) {
-  const int lane = threadIdx.x & 31;
-  const int j = int((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
-  if (j >= n) return;
+// far-field evaluation of the secular sums for a root of leaf q (FMM path): near-leaf
+// sources directly (exact left/right split at sp), far field from the leaf's two local
+// expansions at t = ((d_k - c_t) + tau) / r_t (barycentric value and t-derivative)
+struct FarEval {
+  const SecFmmDev* F;
+  int q;         // leaf of the root
+  double tk, wk; // this lane's Chebyshev node and barycentric weight (lane < kSecP)
+  __device__ SecAcc operator()(const double* __restrict__ d, const double* __restrict__ z2,
+                               double dk, double tau, int sp, int lane) const {
+    SecAcc a = {0, 0, 0, 0, 0};
+    for (int g = F->near_off[q]; g < F->near_off[q + 1]; ++g) {
+      const int lo = F->near_lo[g], hi = F->near_hi[g];
+      for (int i = lo + lane; i < hi; i += 32) {
+        const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
+        const double t = __ldg(z2 + i) * rr;
+        if (i <= sp) {
+          a.psi += t;
+          a.dpsi = fma(t, rr, a.dpsi);
+        } else {
+          a.phi += t;
+          a.dphi = fma(t, rr, a.dphi);
+        }
+      }
+    }
+    const int cell = F->leaf_cell[q];
+    const SecFmmCell C = F->cells[cell];
+    double t = ((dk - C.ct) + tau) / C.rt;
+    double nl = 0.0, nr = 0.0, den = 0.0, dnl = 0.0, dnr = 0.0, dden = 0.0;
+    if (lane < kSecP) {
+      double dx = t - tk;
+      if (dx == 0.0) dx = 0x1.0p-50 * (1.0 + fabs(t));  // exact node: an ulp-scale nudge
+      const double qk = wk / dx, pl = F->psiL[cell * kSecP + lane], pr = F->psiR[cell * kSecP + lane];
+      den = qk;
+      nl = pl * qk;
+      nr = pr * qk;
+      dden = -qk / dx;
+      dnl = -nl / dx;
+      dnr = -nr / dx;
+    }
+    a.psi = warp_sum(a.psi);
+    a.phi = warp_sum(a.phi);
+    a.dpsi = warp_sum(a.dpsi);
+    a.dphi = warp_sum(a.dphi);
+    nl = warp_sum(nl);
+    nr = warp_sum(nr);
+    den = warp_sum(den);
+    dnl = warp_sum(dnl);
+    dnr = warp_sum(dnr);
+    dden = warp_sum(dden);
+    const double id = 1.0 / den;
+    a.psi += nl * id;
+    a.phi += nr * id;
+    a.dpsi += (dnl * den - nl * dden) * id * id / C.rt;
+    a.dphi += (dnr * den - nr * dden) * id * id / C.rt;
+    a.eabs = fabs(a.psi) + fabs(a.phi);
+    return a;
+  }
+};
+
+// Solve root j (0-based, rho > 0 view) with the group g; eval(dk, tau, sp) returns the
+// group-reduced sums.  All threads of g run the same control flow.
+template <class G, class E>
+__device__ void solve_root(int j, const double* __restrict__ d, const double* __restrict__ z2,
+                           double rho, int n, const G& g, const E& eval, int32_t* __restrict__ k_out,
+                           double* __restrict__ tau_out, int32_t* __restrict__ iters_out,
+                           int32_t* __restrict__ status) {
+#ifdef SVD1_SECPROF
+  const long long clk0 = clock64();
+#endif
   const bool refl = rho < 0.0;  // d, z2 hold (-d reversed, z^2 reversed); map the roots back
   const double r = fabs(rho);
   int k = j, it = 0, stat = 0;
@@ -270,7 +377,7 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
     if (j < n - 1) {
       // interlacing bracket (d_j, d_{j+1}); origin = nearer pole by the sign of w(mid)
       const double gap = dsp1 - dsp, mid = 0.5 * gap;
-      const SecAcc a = sec_eval(d, z2, n, dsp, mid, sp, lane);
+      const SecAcc a = eval(dsp, mid, sp);
       const double w = 1.0 + r * (a.psi + a.phi);
       it = 1;
       if (w == 0.0) {  // the midpoint is the root
@@ -293,13 +400,28 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
     } else {
       // last root in (d_{n-1}, d_{n-1} + rho ||z||^2]
       double s = 0.0;
-      for (int i = lane; i < n; i += 32) s += z2[i];
-      s = warp_sum(s);
+      for (int i = g.tid; i < n; i += g.size) s += z2[i];
+      s = g.sum(s);
       k = n - 1;
       lo = 0.0;
       hi = r * s;
       tau = hi;
       hi = hi * (1.0 + 4.0 * kEps);  // keep tau = r||z||^2 strictly inside
+      // probe at the scale of the last gap: a root near d_{n-1} (the reflected view of a
+      // rank-one downdate of a nearly singular Gram matrix) gets a bracket of its own
+      // scale instead of (0, rho ||z||^2], where bisection would need ~50 halvings
+      const double t0 = fmin(dsp1 - dsp, 0.5 * tau);
+      if (t0 > 0.0) {
+        const SecAcc a = eval(dsp1, t0, sp);
+        ++it;
+        const double w = 1.0 + r * (a.psi + a.phi);
+        if (w >= 0.0) {
+          hi = t0;
+          tau = t0;
+        } else {
+          lo = t0;
+        }
+      }
     }
     if (!solved) {
       const double dk = d[k];
@@ -310,7 +432,7 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
           stat |= 1;
           break;
         }
-        const SecAcc a = sec_eval(d, z2, n, dk, tau, sp, lane);
+        const SecAcc a = eval(dk, tau, sp);
         const double w = 1.0 + r * (a.psi + a.phi);
         if (w == 0.0) break;
         if (w < 0.0) lo = tau; else hi = tau;
@@ -325,12 +447,186 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
     }
   }
   if (tau == 0.0) stat |= 2;
-  if (lane == 0) {
+  if (g.tid == 0) {
     const int jo = refl ? n - 1 - j : j;
     k_out[jo] = refl ? n - 1 - k : k;
     tau_out[jo] = refl ? -tau : tau;
+#ifdef SVD1_SECPROF
+    if (iters_out) iters_out[jo] = int(((clock64() - clk0) >> 10) << 8) | min(it, 255);
+#else
     if (iters_out) iters_out[jo] = it;
+#endif
     if (stat) atomicOr(status, stat);
+  }
+}
+
+// One warp per root.  FMM = false: every evaluation sums all n terms (sec_eval), the
+// last root (widest bracket) on a block of its own.  FMM = true: roots 0..n-2 use
+// FarEval (their leaf's near sources + two local expansions); the last root and the
+// roots bracketed by outlier gaps (outside every target interval, listed in F.direct)
+// take one block each, ahead of the nfar warp blocks, with the direct sum.
+template <bool FMM>
+__global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__ d,
+                                                     const double* __restrict__ z2, double rho, int n,
+                                                     int32_t* __restrict__ k_out,
+                                                     double* __restrict__ tau_out,
+                                                     int32_t* __restrict__ iters_out,
+                                                     int32_t* __restrict__ status, SecFmmDev F,
+                                                     int nfar) {
+  const int lane = threadIdx.x & 31;
+  // direct blocks first (they are the longest-running), then the nfar warp blocks
+  // (the direct solver's one such root is the last, with the widest bracket)
+  const int ndir = FMM ? F.ndirect : 1;
+  if (int(blockIdx.x) < ndir) {
+    __shared__ double red[32];
+    const BlockGrp g{int(threadIdx.x), int(blockDim.x), red};
+    const int j = FMM ? F.direct[blockIdx.x] : n - 1;
+    solve_root(j, d, z2, rho, n, g,
+               [&](double dk, double tau, int sp) { return sec_eval(d, z2, n, dk, tau, sp, g); },
+               k_out, tau_out, iters_out, status);
+    return;
+  }
+  const int j = int((int64_t(blockIdx.x - ndir) * blockDim.x + threadIdx.x) >> 5);
+  if (j >= n) return;
+  const WarpGrp g{lane};
+  if (j == n - 1) return;   // a direct block's
+  if (!FMM) {
+    solve_root(j, d, z2, rho, n, g,
+               [&](double dk, double tau, int sp) { return sec_eval(d, z2, n, dk, tau, sp, g); },
+               k_out, tau_out, iters_out, status);
+    return;
+  }
+  FarEval fe{&F, 0, 0.0, 0.0};
+  int lo = 0, hi = F.nleaf;  // leaf q with leaf_lo[q] <= j < leaf_lo[q + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (F.leaf_lo[mid] <= j) lo = mid;
+    else hi = mid;
+  }
+  fe.q = lo;
+  // the root bracketed by an outlier gap lies outside its leaf's target interval
+  if (F.cells[F.leaf_cell[lo]].pad && j == F.leaf_lo[lo + 1] - 1) return;  // a direct block's
+  if (lane < kSecP) {
+    const double th = (2.0 * lane + 1.0) / (2.0 * kSecP);
+    fe.tk = cospi(th);
+    fe.wk = ((lane & 1) ? -1.0 : 1.0) * sinpi(th);
+  }
+  solve_root(j, d, z2, rho, n, g,
+             [&](double dk, double tau, int sp) { return fe(d, z2, dk, tau, sp, lane); }, k_out,
+             tau_out, iters_out, status);
+}
+
+// ------------------------------------------------------------------ K2' build
+// Far field of the secular sums on the source tree (one right-hand side, the charges
+// z_i^2).  Operators as the apply's (scaled far field), each target
+// cell's interval [d_lo, d_next] as its local-expansion box, evaluated on the fly.
+__device__ __forceinline__ double bary(const double* __restrict__ t, const double* __restrict__ w,
+                                       const double* __restrict__ f, double x) {
+  // sum_i f_i u_i(x), barycentric Lagrange on the kSecP Chebyshev nodes
+  // (unrolled: kSecP independent loads and reciprocals in flight; an exact node is
+  // nudged by an ulp-scale step, whose interpolation error is below rounding)
+  double num = 0.0, den = 0.0;
+#pragma unroll
+  for (int i = 0; i < kSecP; ++i) {
+    double dx = x - t[i];
+    if (dx == 0.0) dx = 0x1.0p-50;
+    const double q = w[i] * fast_rcp(dx);
+    num = fma(q, f[i], num);
+    den += q;
+  }
+  return num * fast_rcp(den);
+}
+
+// Four launches, no level-by-level chain: phase 0 P2M (leaves); phase 1 M2M of every
+// non-leaf cell directly from its leaf descendants (the M2M operator of any descendant
+// has the same closed form, and is better conditioned than a chain); phase 2 M2L / P2L
+// into the left / right expansions of every cell; phase 3 L2L into every leaf directly
+// from all its ancestors (a local expansion is a polynomial: re-interpolation is
+// exact), accumulated in place (leaves are nobody's ancestors).  Items are (cell, node).
+__global__ void __launch_bounds__(256) secfmm_phase_kernel(SecFmmDev F, const double* __restrict__ d,
+                                                          const double* __restrict__ z2, int phase) {
+  __shared__ double t[kSecP], w[kSecP];
+  if (threadIdx.x < kSecP) {
+    const double th = (2.0 * threadIdx.x + 1.0) / (2.0 * kSecP);
+    t[threadIdx.x] = cospi(th);
+    w[threadIdx.x] = ((threadIdx.x & 1) ? -1.0 : 1.0) * sinpi(th);
+  }
+  __syncthreads();
+  const int L = F.L, first_leaf = (1 << L) - 1;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (phase == 0) {  // P2M: Phi~_X[i] = sum_s z_s^2 / (t_i (d_s - c_X) - 3 r_X)
+    if (e >= (1 << L) * kSecP) return;
+    const int c = first_leaf + e / kSecP, i = e % kSecP;
+    const SecFmmCell C = F.cells[c];
+    double v = 0.0;
+    for (int s = C.lo; s < C.hi; ++s) v += z2[s] * fast_rcp(t[i] * (d[s] - C.c) - 3.0 * C.r);
+    F.phi[c * kSecP + i] = v;
+  } else if (phase == 1) {  // M2M: Phi_P[i] = sum_leaves D (3 r_D / den) Phi_D(tc); warp per item
+    const int e32 = e >> 5, lane = threadIdx.x & 31;
+    if (e32 >= first_leaf * kSecP) return;
+    const int c = e32 / kSecP, i = e32 % kSecP;
+    const SecFmmCell P = F.cells[c];
+    double v = 0.0;
+    if (P.hi > P.lo) {
+      int l = 0;
+      while ((2 << l) - 1 <= c) ++l;                 // level of c
+      const int dep = L - l, d0 = ((c + 1) << dep) - 1;
+      for (int q = lane; q < (1 << dep); q += 32) {
+        const int dc = d0 + q;
+        const SecFmmCell D = F.cells[dc];
+        if (D.hi <= D.lo) continue;
+        const double rden = fast_rcp(3.0 * P.r + t[i] * (P.c - D.c));
+        v += (3.0 * D.r * rden) * bary(t, w, F.phi + dc * kSecP, 3.0 * D.r * t[i] * rden);
+      }
+    }
+    v = warp_sum(v);
+    if (lane == 0) F.phi[c * kSecP + i] = v;
+  } else if (phase == 2) {  // M2L / P2L into the left / right local expansions; warp per item
+    const int e32 = e >> 5, lane = threadIdx.x & 31;
+    if (e32 >= F.ncells * kSecP) return;
+    const int c = e32 / kSecP, i = e32 % kSecP;
+    const SecFmmCell Y = F.cells[c];
+    const double y = Y.rt * t[i];  // node offset from c_t
+    double vl = 0.0, vr = 0.0;
+    for (int g = Y.m2l_off + lane; g < F.cells[c + 1].m2l_off; g += 32) {  // lane per partner
+      const SecFmmPart X = F.parts[g];
+      const SecFmmCell C = F.cells[X.cell];
+      double v = 0.0;
+      if (X.flags & 2) {  // P2L: sources of X at the node c_t + r_t t_i
+        for (int s = C.lo; s < C.hi; ++s) v += z2[s] * fast_rcp((d[s] - Y.ct) - y);
+      } else {  // M2L: t_X = 3 r_X / ((c_t - c_X) + r_t t_i), value t_X Phi_X(t_X)
+        const double tx = 3.0 * C.r * fast_rcp((Y.ct - C.c) + y);
+        v = tx * bary(t, w, F.phi + X.cell * kSecP, tx);
+      }
+      if (X.flags & 1) vr += v;
+      else vl += v;
+    }
+    vl = warp_sum(vl);
+    vr = warp_sum(vr);
+    if (lane == 0) {
+      F.psiL[c * kSecP + i] = vl;
+      F.psiR[c * kSecP + i] = vr;
+    }
+  } else {  // L2L: Psi_Y[i] += sum_{ancestors A} Psi_A(((c_Yt - c_At) + r_Yt t_i) / r_At); warp
+    // per item, lane 2 a' + s evaluates side s of the a'-th ancestor
+    const int e32 = e >> 5, lane = threadIdx.x & 31;
+    if (e32 >= (1 << L) * kSecP) return;
+    const int c = first_leaf + e32 / kSecP, i = e32 % kSecP;
+    const SecFmmCell Y = F.cells[c];
+    if (Y.hi <= Y.lo) return;
+    double v = 0.0;
+    if (lane < 2 * L) {
+      int a = c;
+      for (int q = 0; q <= (lane >> 1); ++q) a = (a - 1) / 2;
+      const SecFmmCell A = F.cells[a];
+      const double x = ((Y.ct - A.ct) + Y.rt * t[i]) * fast_rcp(A.rt);
+      v = bary(t, w, ((lane & 1) ? F.psiR : F.psiL) + a * kSecP, x);
+    }
+    const double vl = warp_sum((lane & 1) ? 0.0 : v), vr = warp_sum((lane & 1) ? v : 0.0);
+    if (lane == 0) {
+      F.psiL[c * kSecP + i] += vl;
+      F.psiR[c * kSecP + i] += vr;
+    }
   }
 }
 
@@ -553,8 +849,27 @@ svd1_status secular(const double* d, const double* z2, double rho, int n, int32_
                     double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
                     int64_t* launches) {
   if (n <= 0) return SVD1_OK;
-  secular_kernel<<<blocks_for_warps(n), 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out, status);
+  secular_kernel<false><<<1 + blocks_for_warps(n), 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out,
+                                                                   status, SecFmmDev{}, 0);
   *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, const SecFmmDev& F,
+                        int32_t* k_out, double* tau_out, int32_t* iters_out, int32_t* status,
+                        cudaStream_t st, int64_t* launches) {
+  if (n <= 0) return SVD1_OK;
+  auto grid = [](int items) { return unsigned(std::max(1, (items + 255) / 256)); };
+  const int L = F.L;
+  secfmm_phase_kernel<<<grid((1 << L) * kSecP), 256, 0, st>>>(F, d, z2, 0);
+  secfmm_phase_kernel<<<grid(((1 << L) - 1) * kSecP * 32), 256, 0, st>>>(F, d, z2, 1);
+  secfmm_phase_kernel<<<grid(F.ncells * kSecP * 32), 256, 0, st>>>(F, d, z2, 2);
+  secfmm_phase_kernel<<<grid((1 << L) * kSecP * 32), 256, 0, st>>>(F, d, z2, 3);
+  const int nfar = blocks_for_warps(n);
+  secular_kernel<true><<<nfar + F.ndirect, 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out, status, F,
+                                                          nfar);
+  *launches += 5;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

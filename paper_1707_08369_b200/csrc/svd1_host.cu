@@ -96,6 +96,15 @@ struct FmmHost {
   int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
 };
 
+// secular FMM plan (host side; see secfmm_plan)
+struct SecPlanHost {
+  int L = 0, ncells = 0, nleaf = 0;
+  std::vector<SecFmmCell> cells;  // ncells + 1 (sentinel carries the partner count)
+  std::vector<SecFmmPart> parts;
+  std::vector<int32_t> leaf_lo, leaf_cell, near_off, near_lo, near_hi;
+  std::vector<int32_t> direct;  // roots outside every target interval (direct sum)
+};
+
 struct CauchyPrep {
   bool fmm = false;
   int p = 16;
@@ -182,6 +191,9 @@ struct StepRecord {
   double *dhv = nullptr, *dcs = nullptr, *dpscale = nullptr;
   std::vector<double> stage;
   CauchyPrep cp;
+  SecPlanHost sec;          // secular FMM plan (large active sizes)
+  DevBuf sec_blob, sec_scr;
+  int sec_fmm_used = 0;
 };
 
 
@@ -458,6 +470,163 @@ bool fmm_cells(FmmHost& F, int s, int L, const Merged& M) {
     C.r = std::max(r, std::max(std::fabs(C.c) * 0x1.0p-50, 1e-300));
   }
   return true;
+}
+
+// ---- secular FMM plan: tree over the oriented sources d (ascending),
+// target interval of a cell = [d_lo, d_next] (the brackets of its roots), dual traversal
+// with the symmetric admissibility of the apply's tree; far partners -> M2L (P2L when
+// the partner holds fewer than kSecP sources) into the left or right expansion, leaf
+// pairs -> near ranges evaluated directly by each root.
+void secfmm_plan(const double* d, int n, SecPlanHost& S) {
+  Merged M;
+  M.pts.assign(d, d + n);
+  M.nsrc.resize(n + 1);
+  for (int q = 0; q <= n; ++q) M.nsrc[q] = q;
+  const int s = 16;  // leaves of <= 2 s = 32 sources
+  int L0 = 0;
+  while ((int64_t(n) + (int64_t(1) << L0) - 1) / (int64_t(1) << L0) > 2 * s) ++L0;
+  FmmHost F;
+  for (int L = L0; L <= L0 + 2; ++L) {
+    FmmHost F2;
+    if (!fmm_cells(F2, s, L, M)) continue;
+    double rmax = 0.0;
+    for (int i = 0; i < (1 << L); ++i) rmax = std::max(rmax, F2.cells[(1 << L) - 1 + i].r);
+    F = std::move(F2);
+    if (!(rmax >= 0.25 * F.cells[0].r && F.cells[0].r > 0.0)) break;  // no outlier-wide leaf
+  }
+  const int L = F.L, nc = F.ncells;
+  S.L = L;
+  S.ncells = nc;
+  S.cells.assign(nc + 1, SecFmmCell{0, 0, 0, 0, 0.0, 0.0, 0.0, 0.0});
+  // Target intervals bottom-up.  A leaf's is [d_lo, d_hi] (the brackets of its roots)
+  // unless the gap to the next leaf is wider than its own hull (an outlier gap): then it
+  // is the hull [d_lo, d_{hi-1}] and the one root bracketed by the gap sums directly
+  // (pad = 1), so no leaf is near-field to a whole side of the spectrum.  A parent's
+  // interval is the hull of its children's, so every expansion contains its descendants'.
+  std::vector<double> tlo(nc, 0.0), thi(nc, -1.0);
+  const int first_leaf0 = (1 << L) - 1;
+  for (int c = nc - 1; c >= 0; --c) {
+    const FmmCell& C = F.cells[c];
+    SecFmmCell& X = S.cells[c];
+    X.lo = C.lo;
+    X.hi = C.hi;
+    X.c = C.c;
+    X.r = C.r;
+    X.pad = 0;
+    if (C.hi <= C.lo) continue;
+    if (c >= first_leaf0) {
+      const double a = d[C.lo], h = d[C.hi - 1], b = d[std::min(C.hi, n - 1)];
+      tlo[c] = a;
+      thi[c] = b;
+      if (C.hi < n && b - h > h - a) {
+        thi[c] = h;
+        X.pad = 1;
+      }
+    } else {
+      bool any = false;
+      for (int ch = 2 * c + 1; ch <= 2 * c + 2; ++ch) {
+        if (thi[ch] < tlo[ch]) continue;
+        tlo[c] = any ? std::min(tlo[c], tlo[ch]) : tlo[ch];
+        thi[c] = any ? std::max(thi[c], thi[ch]) : thi[ch];
+        any = true;
+      }
+    }
+    X.ct = 0.5 * (tlo[c] + thi[c]);
+    X.rt = std::max(std::max(X.ct - tlo[c], thi[c] - X.ct), std::max(std::fabs(X.ct) * 0x1.0p-50, 1e-300));
+  }
+  auto has_src = [&](int c) { return S.cells[c].hi > S.cells[c].lo; };
+  auto has_tgt = [&](int c) { return S.cells[c].hi > S.cells[c].lo && S.cells[c].lo <= n - 2; };
+  auto adm = [&](int x, int y) {
+    const SecFmmCell &X = S.cells[x], &Y = S.cells[y];
+    return std::fabs(X.c - Y.ct) >= std::max(3.0 * X.r + Y.rt, X.r + 3.0 * Y.rt);
+  };
+  const int first_leaf = (1 << L) - 1;
+  auto is_leaf = [&](int c) { return c >= first_leaf; };
+  std::vector<std::pair<int, int>> m2l_pairs, near_pairs;
+  std::vector<std::pair<int, int>> stack{{0, 0}};
+  while (!stack.empty()) {
+    const auto [x, y] = stack.back();
+    stack.pop_back();
+    if (!has_src(x) || !has_tgt(y)) continue;
+    if (x != y && adm(x, y)) {
+      m2l_pairs.push_back({y, x});
+      continue;
+    }
+    if (is_leaf(x) && is_leaf(y)) {
+      near_pairs.push_back({y, x});
+      continue;
+    }
+    const bool split_x = is_leaf(y) || (!is_leaf(x) && S.cells[x].r > S.cells[y].rt);
+    if (split_x) {
+      stack.push_back({2 * x + 2, y});
+      stack.push_back({2 * x + 1, y});
+    } else {
+      stack.push_back({x, 2 * y + 2});
+      stack.push_back({x, 2 * y + 1});
+    }
+  }
+  std::sort(m2l_pairs.begin(), m2l_pairs.end());
+  S.parts.clear();
+  size_t q = 0;
+  for (int c = 0; c < nc; ++c) {
+    S.cells[c].m2l_off = int32_t(S.parts.size());
+    for (; q < m2l_pairs.size() && m2l_pairs[q].first == c; ++q) {
+      const int x = m2l_pairs[q].second;
+      const SecFmmCell& X = S.cells[x];
+      int32_t fl = X.c > S.cells[c].ct ? 1 : 0;
+      if (X.hi - X.lo < kSecP) fl |= 2;
+      S.parts.push_back(SecFmmPart{x, fl});
+    }
+  }
+  S.cells[nc].m2l_off = int32_t(S.parts.size());
+  // leaves (non-empty, in index order) and their near source ranges
+  S.leaf_lo.clear();
+  S.leaf_cell.clear();
+  std::vector<int> leaf_of_cell(nc, -1);
+  for (int i = 0; i < (1 << L); ++i) {
+    const int c = first_leaf + i;
+    if (!has_src(c)) continue;
+    leaf_of_cell[c] = int(S.leaf_cell.size());
+    S.leaf_lo.push_back(S.cells[c].lo);
+    S.leaf_cell.push_back(c);
+  }
+  S.nleaf = int(S.leaf_cell.size());
+  S.leaf_lo.push_back(n);
+  S.direct.clear();
+  for (int q = 0; q < S.nleaf; ++q)
+    if (S.cells[S.leaf_cell[q]].pad) S.direct.push_back(S.leaf_lo[q + 1] - 1);
+  S.direct.push_back(n - 1);
+  std::sort(near_pairs.begin(), near_pairs.end());
+  S.near_off.assign(S.nleaf + 1, 0);
+  S.near_lo.clear();
+  S.near_hi.clear();
+  size_t r = 0;
+  for (int lf = 0; lf < S.nleaf; ++lf) {
+    const int c = S.leaf_cell[lf];
+    S.near_off[lf] = int32_t(S.near_lo.size());
+    while (r < near_pairs.size() && near_pairs[r].first < c) ++r;
+    for (; r < near_pairs.size() && near_pairs[r].first == c; ++r) {
+      const SecFmmCell& X = S.cells[near_pairs[r].second];
+      if (!S.near_hi.empty() && S.near_off[lf] < int32_t(S.near_lo.size()) && S.near_hi.back() == X.lo)
+        S.near_hi.back() = X.hi;  // merge adjacent ranges
+      else {
+        S.near_lo.push_back(X.lo);
+        S.near_hi.push_back(X.hi);
+      }
+    }
+  }
+  S.near_off[S.nleaf] = int32_t(S.near_lo.size());
+  if (std::getenv("SVD1_DEBUG")) {
+    int64_t tot = 0, mx = 0;
+    for (int lf = 0; lf < S.nleaf; ++lf) {
+      int64_t k = 0;
+      for (int g = S.near_off[lf]; g < S.near_off[lf + 1]; ++g) k += S.near_hi[g] - S.near_lo[g];
+      tot += k * (S.leaf_lo[lf + 1] - S.leaf_lo[lf]);
+      mx = std::max(mx, k);
+    }
+    fprintf(stderr, "[svd1] secfmm n=%d L=%d cells=%d leaves=%d m2l parts=%zu near terms/root mean %.1f max %lld\n",
+            n, L, nc, S.nleaf, S.parts.size(), double(tot) / n, (long long)mx);
+  }
 }
 
 // sorted CSR of (row, value) pairs: row r's values in [off[r], off[r+1])
@@ -1135,6 +1304,72 @@ svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
   return SVD1_OK;
 }
 
+// Secular FMM: plan from the oriented sources (host), one-copy upload, device view.
+int sec_fmm_min() {
+  static const int v = [] {
+    const char* e = std::getenv("SVD1_SEC_FMM_MIN");
+    return e ? std::max(64, atoi(e)) : 6144;
+  }();
+  return v;
+}
+
+bool use_sec_fmm(uint32_t flags, int n) {
+  if (flags & SVD1_SECULAR_DIRECT) return false;
+  if (flags & SVD1_SECULAR_FMM) return n > 64;
+  return n >= sec_fmm_min();
+}
+
+svd1_status secfmm_prepare(svd1_plan_t P, SecPlanHost& H, DevBuf& blob, DevBuf& scr, const double* dr,
+                           int n, int side, SecFmmDev* out) {
+  static const bool report = std::getenv("SVD1_SECTIME") != nullptr;
+  const double t0 = now_ms();
+  secfmm_plan(dr, n, H);
+  if (report) {
+    int64_t mx = 0, tot = 0;
+    int npad = 0, mxleaf = 0;
+    for (int q = 0; q < H.nleaf; ++q) {
+      int64_t s = 0;
+      for (int g = H.near_off[q]; g < H.near_off[q + 1]; ++g) s += H.near_hi[g] - H.near_lo[g];
+      const int cnt = H.leaf_lo[q + 1] - H.leaf_lo[q];
+      tot += s * cnt;
+      mx = std::max(mx, s);
+      mxleaf = std::max(mxleaf, cnt);
+      npad += H.cells[H.leaf_cell[q]].pad;
+    }
+    std::fprintf(stderr,
+                 "secfmm_plan n=%d L=%d cells=%d leaves=%d parts=%zu near=%zu max_near_terms=%lld "
+                 "mean=%.1f max_leaf=%d pad=%d: %.3f ms\n",
+                 n, H.L, H.ncells, H.nleaf, H.parts.size(), H.near_lo.size(), (long long)mx,
+                 double(tot) / n, mxleaf, npad, now_ms() - t0);
+  }
+  BlobBuilder B;
+  const size_t o_cells = B.add(H.cells), o_parts = B.add(H.parts), o_llo = B.add(H.leaf_lo),
+               o_lc = B.add(H.leaf_cell), o_no = B.add(H.near_off), o_nlo = B.add(H.near_lo),
+               o_nhi = B.add(H.near_hi), o_dir = B.add(H.direct);
+  char* base;
+  TRY(arena_put_blob(P, B, blob, &base, side));
+  double* sc;
+  TRY(scr.get<double>(size_t(3) * H.ncells * kSecP, &sc));
+  SecFmmDev F;
+  F.L = H.L;
+  F.ncells = H.ncells;
+  F.nleaf = H.nleaf;
+  F.ndirect = int(H.direct.size());
+  F.direct = reinterpret_cast<const int32_t*>(base + o_dir);
+  F.cells = reinterpret_cast<const SecFmmCell*>(base + o_cells);
+  F.parts = reinterpret_cast<const SecFmmPart*>(base + o_parts);
+  F.leaf_lo = reinterpret_cast<const int32_t*>(base + o_llo);
+  F.leaf_cell = reinterpret_cast<const int32_t*>(base + o_lc);
+  F.near_off = reinterpret_cast<const int32_t*>(base + o_no);
+  F.near_lo = reinterpret_cast<const int32_t*>(base + o_nlo);
+  F.near_hi = reinterpret_cast<const int32_t*>(base + o_nhi);
+  F.phi = sc;
+  F.psiL = sc + size_t(H.ncells) * kSecP;
+  F.psiR = sc + size_t(2) * H.ncells * kSecP;
+  *out = F;
+  return SVD1_OK;
+}
+
 // joins its threads on scope exit (early error returns included)
 struct Joiner {
   std::vector<std::thread> ts;
@@ -1302,7 +1537,14 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   TRY(ev_record(P, ev0, st));
   double* scr;
   TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
-  TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, st, &P->launches));   // STEP 2
+  S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na);
+  if (S.sec_fmm_used) {  // STEP 2 with the far field by FMM
+    SecFmmDev F;
+    TRY(secfmm_prepare(P, S.sec, S.sec_blob, S.sec_scr, S.stage.data() + 2 * na, na, side, &F));
+    TRY(secular_fmm(ddr, dz2r, rho, na, F, dk, dtau, dit, dst, st, &P->launches));
+  } else {
+    TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, st, &P->launches));   // STEP 2
+  }
   TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, st, &P->launches));
   TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, st, &P->launches));
   TRY(ev_record(P, ev0 + 1, st));
@@ -1354,6 +1596,21 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
       sum_it += it[j];
     }
     S.mean_iter = sum_it / na;
+#ifdef SVD1_SECPROF  // iters hold per-root kilocycles: print the slowest roots
+    {
+      std::vector<int> ord(na);
+      std::iota(ord.begin(), ord.end(), 0);
+      std::partial_sort(ord.begin(), ord.begin() + std::min(na, 6), ord.end(),
+                        [&](int x, int y) { return it[x] > it[y]; });
+      std::fprintf(stderr, "secprof na=%d fmm=%d:", na, int(S.sec_fmm_used));
+      for (int q = 0; q < std::min(na, 6); ++q)
+        std::fprintf(stderr, " j%d=%dk/%dit", ord[q], it[ord[q]] >> 8, it[ord[q]] & 255);
+      std::vector<int> v(it, it + na);
+      std::nth_element(v.begin(), v.begin() + na / 2, v.end());
+      std::fprintf(stderr, " median=%dk rho=%.3e dk=%.3e tau=%.3e\n", v[na / 2] >> 8, S.rho,
+                   S.da[S.k_h[ord[0]]], S.tau_h[ord[0]]);
+    }
+#endif
     S.spectral_ms = ev_ms(P, S.ev0, S.ev0 + 1);
     if (st_h & 1) return SVD1_E_NOCONV;
     if (st_h & 2) return SVD1_E_POLE;
@@ -2001,7 +2258,17 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
   double* orient;
   TRY(P->scratch_d.get<double>(size_t(2 * n), &orient));
   TRY(secular_orient(d, z, rho, int(n), orient, orient + n, P->st, &P->launches));
-  TRY(secular(orient, orient + n, rho, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
+  if (use_sec_fmm(P->cfg.flags, int(n))) {  // plan from the oriented sources (host copy)
+    std::vector<double> dr(n);
+    SVD1_CUDA_TRY(cudaMemcpyAsync(dr.data(), orient, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+    SecFmmDev F;
+    TRY(arena_reset(P));
+    TRY(secfmm_prepare(P, P->steps[0].sec, P->steps[0].sec_blob, P->steps[0].sec_scr, dr.data(), int(n), 0, &F));
+    TRY(secular_fmm(orient, orient + n, rho, int(n), F, k_out, tau_out, dit, dst, P->st, &P->launches));
+  } else {
+    TRY(secular(orient, orient + n, rho, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
+  }
   std::vector<int32_t> it(n);
   int32_t st_h = 0;
   SVD1_CUDA_TRY(cudaMemcpyAsync(it.data(), dit, n * sizeof(int32_t), cudaMemcpyDeviceToHost, P->st));

@@ -55,6 +55,40 @@ svd1_status secular_orient(const double* d, const double* z, double rho, int n, 
                            double* z2r, cudaStream_t st, int64_t* launches);
 // scratch (doubles) needed by loewner / colnorm_carry for size n and ncarry vectors
 int64_t spectral_scratch_elems(int n, int ncarry);
+// K2': FMM-accelerated secular evaluation.  Tree over
+// the (oriented) sources; each target cell Y carries local expansions of the far field of
+// the sources left (psiL) and right (psiR) of its target interval [d_lo, d_next]; a root
+// in leaf Y sums its near-leaf sources directly (exact left/right split) and evaluates
+// the two polynomials, so an evaluation costs O(near + p) instead of O(n).
+constexpr int kSecP = 20;  // Chebyshev order of the secular far field
+struct SecFmmCell {        // heap-ordered; empty cells have lo == hi
+  int32_t lo, hi;          // source index range
+  int32_t m2l_off;         // partners m2l[m2l_off .. next cell's m2l_off)
+  int32_t pad;             // leaf: 1 = its last root (outlier-gap bracket) sums directly
+  double c, r;             // source hull
+  double ct, rt;           // target interval (centre, radius); see secfmm_plan
+};
+struct SecFmmPart {        // M2L partner of a target cell
+  int32_t cell, flags;     // flags bit 0: right of the target (phi), bit 1: P2L (few sources)
+};
+struct SecFmmDev {         // device view of one plan
+  int L, ncells, nleaf, ndirect;
+  const int32_t* direct;    // ndirect roots solved with the direct sum (one block each)
+  const SecFmmCell* cells;
+  const SecFmmPart* parts;  // size cells[ncells].m2l_off (sentinel entry)
+  const int32_t* leaf_lo;   // nleaf + 1: source ranges of the leaves (non-empty, in order)
+  const int32_t* leaf_cell; // heap index of leaf q
+  const int32_t* near_off;  // nleaf + 1 into near_lo / near_hi
+  const int32_t* near_lo;   // near source index ranges [near_lo, near_hi) of leaf q
+  const int32_t* near_hi;
+  double* phi;              // ncells * kSecP far-field coefficients (scaled, as the apply's)
+  double* psiL;             // ncells * kSecP local expansions: sources left of the interval
+  double* psiR;             //                                 and right of it
+};
+svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, const SecFmmDev& F,
+                        int32_t* k_out, double* tau_out, int32_t* iters_out, int32_t* status,
+                        cudaStream_t st, int64_t* launches);
+
 // K3a: Loewner zhat (thread per i, split-j partial products + ordered combine)
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
                     const double* z, int n, double* zhat, double* scratch, cudaStream_t st,

@@ -190,3 +190,42 @@ def test_repeated_sigma_pairing(n, flags):
     assert r["rep"]["pair_rotations"] >= 1
     assert r["res"] <= 1e-10 and r["orth"] <= 1e-10, r
     assert r["U"]["cluster"] <= 1e-9 and r["V"]["cluster"] <= 1e-9, r
+
+
+# ------------------------------------------------------- FMM secular solve (§8(f) #2)
+@pytest.fixture(scope="module")
+def plan_secfmm():
+    p = P.Plan(4096, 4096, eps=1e-10, flags=P.SECULAR_FMM)
+    yield p
+    p.close()
+
+
+@pytest.mark.parametrize("n,kind,sgn", [(n, k, s) for n in (97, 700, 3000) for k in ("gaussian", "graded", "uniform")
+                                         for s in (1.0, -1.0)])
+def test_secular_fmm_parity(plan_secfmm, n, kind, sgn):
+    """Roots with the far field of w from the secular FMM (near sources direct) agree with
+    the bisection oracle as the direct solver does, and lie in w's rounding band."""
+    rng = np.random.default_rng(n * 11 + len(kind))
+    d, z, rho = random_secular(n, rng, kind=kind)
+    rho = sgn * abs(rho)
+    dfl = O.deflate(d, z, rho)
+    d, z = dfl.d[dfl.active], dfl.z[dfl.active]
+    n = d.size
+    ko, to = O.secular_roots_bisect(d, z, rho)
+    kg, tg, iters = plan_secfmm.secular_solve(T(d), T(z), rho)
+    kg, tg = N(kg).astype(np.int64), N(tg)
+    diff = ((d[kg] - d[ko]) + tg) - to
+    scale = np.minimum(np.abs(to), np.abs(tg))
+    assert np.max(np.abs(diff) / scale) <= 2e-12, (np.max(np.abs(diff) / scale), iters)
+    w = O.secular_w(d, z, rho, kg, tg)
+    terms = np.abs(z[None, :] ** 2 / ((d[None, :] - d[kg][:, None]) - tg[:, None]))
+    assert np.all(np.abs(w) <= 64 * n * O.EPS * (1 + abs(rho) * terms.sum(axis=1)))
+    assert iters <= 40
+
+
+@pytest.mark.parametrize("cfg,m,n", [(3, 512, 512), (5, 600, 600), (4, 256, 1024)])
+def test_update_parity_secular_fmm(cfg, m, n):
+    """Whole updates with every secular solve on the FMM path (D2-D4 tolerances)."""
+    inp = config_inputs(cfg, m=m, n=n, updates=1)
+    a, b = inp["ab"][0]
+    _check_update(inp["U"], inp["sigma"], inp["V"], a, b, flags=P.SECULAR_FMM)
