@@ -3,6 +3,7 @@
 // / interaction lists.  Every O(n^2) and O(rows*n)
 // step runs in the CUDA kernels of kernels_spectral.cu / kernels_apply.cu.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -1920,27 +1921,10 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, one_stream ? 0 : 1));
   }
   const double tA = now_ms();
+  std::atomic<bool> planned[4] = {false, false, false, false};  // outlives the Joiners
   Joiner plan_u, plan_v, plan_u2, plan_v2;
   const svd1_config pcfg = P->cfg;
   const int pp = P->p;
-  // U: finish STEP 4, launch STEP 5 (rho2, z2 = X1^T U^T b1)
-  TRY(spectral_finish(P, S[0], Du, cu));
-  plan_u.add(std::thread([&S, pcfg, pp, rows = c.u_rows] { apply_plan(pcfg, pp, S[0], rows, false, 0); }));
-  {
-    std::vector<double> z2 = cu[0];
-    cu.erase(cu.begin());
-    TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, 0));
-  }
-  const double tB = now_ms();
-  // V: finish STEP 6, launch STEP 7 (rho4)
-  TRY(spectral_finish(P, S[2], Dv, cv));
-  plan_v.add(std::thread([&S, pcfg, pp, rows = c.v_rows] { apply_plan(pcfg, pp, S[2], rows, false, 1); }));
-  {
-    std::vector<double> z4 = cv[0];
-    cv.erase(cv.begin());
-    TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, one_stream ? 0 : 1));
-  }
-  const double tC = now_ms();
   auto rare_grow = [&](int e, int side) -> svd1_status {  // deeper tree than guessed
     if (S[e].rows > 0 && S[e].na > 0 && cauchy_exp_elems(S[e].cp) > P->phi[side].cap / sizeof(double)) {
       SVD1_CUDA_TRY(cudaDeviceSynchronize());
@@ -1948,34 +1932,107 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     }
     return SVD1_OK;
   };
-  bool launched_u1 = false, launched_v1 = false;
-  plan_u.join();
-  TRY(rare_grow(0, 0));
-  TRY(apply_upload(P, S[0], 0));
-  if (S[0].h_goff.size() <= 1) {  // nothing in place: start now
-    TRY(ev_record(P, 16, P->st));
-    TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
-    launched_u1 = true;
+  // Host scheduler of the two chains: each round takes the first ready action in
+  // priority order — launch a planned first apply (GPU work as early as possible), then
+  // finish an eigen-update whose read-back has landed (and launch its successor / start
+  // its plan on a worker thread).  Readiness is polled (cudaEventQuery, atomic flags),
+  // so neither side's host step waits behind the other side's GPU work.
+  auto spawn_plan = [&](Joiner& J, int e, bool reverse, int side, int64_t rows) {
+    J.add(std::thread([&S, &planned, pcfg, pp, e, reverse, side, rows] {
+      apply_plan(pcfg, pp, S[e], rows, reverse, side);
+      planned[e].store(true, std::memory_order_release);
+    }));
+  };
+  auto landed = [&](int e) {
+    if (!S[e].pending) return true;
+    const cudaError_t q = cudaEventQuery(S[e].done_ev);
+    if (q == cudaErrorNotReady) return false;
+    return true;  // success, or an error that spectral_finish reports
+  };
+  bool fin[4] = {false, false, false, false};
+  bool launched_u1 = false, launched_v1 = false, uploaded_u1 = false, uploaded_v1 = false;
+  double t_fin[4] = {0, 0, 0, 0}, t_dbg[4] = {0, 0, 0, 0};
+  auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
+    const int side = e == 0 ? 0 : 1;
+    TRY(rare_grow(e, side));
+    TRY(apply_upload(P, S[e], one_stream ? 0 : side));
+    if (S[e].h_goff.size() <= 1) {  // nothing transformed in place: start now
+      if (e == 0) {
+        TRY(ev_record(P, 16, P->st));
+        TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
+        launched_u1 = true;
+      } else {
+        TRY(ev_record(P, 18, stv));
+        TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
+        launched_v1 = true;
+      }
+    }
+    return SVD1_OK;
+  };
+  while (!(fin[0] && fin[1] && fin[2] && fin[3])) {
+    if (fin[0] && !uploaded_u1 && planned[0].load(std::memory_order_acquire)) {
+      plan_u.join();
+      TRY(first_apply(0));
+      uploaded_u1 = true;
+      continue;
+    }
+    if (fin[2] && !uploaded_v1 && planned[2].load(std::memory_order_acquire)) {
+      plan_v.join();
+      TRY(first_apply(2));
+      uploaded_v1 = true;
+      continue;
+    }
+    if (!fin[0] && landed(0)) {  // U: finish STEP 4, launch STEP 5 (rho2, z2 = X1^T U^T b1)
+      t_dbg[0] = now_ms();
+      TRY(spectral_finish(P, S[0], Du, cu));
+      fin[0] = true;
+      t_dbg[1] = now_ms();
+      spawn_plan(plan_u, 0, false, 0, c.u_rows);
+      t_dbg[2] = now_ms();
+      std::vector<double> z2 = cu[0];
+      cu.erase(cu.begin());
+      TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, 0));
+      t_fin[0] = now_ms();
+      continue;
+    }
+    if (!fin[2] && landed(2)) {  // V: finish STEP 6, launch STEP 7 (rho4)
+      TRY(spectral_finish(P, S[2], Dv, cv));
+      fin[2] = true;
+      spawn_plan(plan_v, 2, false, 1, c.v_rows);
+      std::vector<double> z4 = cv[0];
+      cv.erase(cv.begin());
+      TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, one_stream ? 0 : 1));
+      t_fin[2] = now_ms();
+      continue;
+    }
+    if (fin[0] && !fin[1] && landed(1)) {
+      TRY(spectral_finish(P, S[1], Du, cu));
+      fin[1] = true;
+      spawn_plan(plan_u2, 1, true, 0, c.u_rows);
+      t_fin[1] = now_ms();
+      continue;
+    }
+    if (fin[2] && !fin[3] && landed(3)) {
+      TRY(spectral_finish(P, S[3], Dv, cv));
+      fin[3] = true;
+      spawn_plan(plan_v2, 3, true, 1, c.v_rows);
+      t_fin[3] = now_ms();
+      continue;
+    }
+    std::this_thread::yield();
   }
-  const double tC2 = now_ms();
-  TRY(spectral_finish(P, S[1], Du, cu));
-  plan_u2.add(std::thread([&S, pcfg, pp, rows = c.u_rows] { apply_plan(pcfg, pp, S[1], rows, true, 0); }));
-  const double tD = now_ms();
-  plan_v.join();
-  TRY(rare_grow(2, 1));
-  TRY(apply_upload(P, S[2], one_stream ? 0 : 1));
-  if (S[2].h_goff.size() <= 1) {
-    TRY(ev_record(P, 18, stv));
-    TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
-    launched_v1 = true;
+  if (!uploaded_u1) {
+    plan_u.join();
+    TRY(first_apply(0));
   }
-  const double tE = now_ms();
-  TRY(spectral_finish(P, S[3], Dv, cv));
-  plan_v2.add(std::thread([&S, pcfg, pp, rows = c.v_rows] { apply_plan(pcfg, pp, S[3], rows, true, 1); }));
-  const double tF = now_ms();
+  if (!uploaded_v1) {
+    plan_v.join();
+    TRY(first_apply(2));
+  }
   if (std::getenv("SVD1_TIMING"))
-    fprintf(stderr, "[svd1] launch1 %.3f U1->U2 %.3f V1->V2 %.3f U plan+upload %.3f finish U2 %.3f V plan+upload %.3f finish V2 %.3f (plans %.3f %.3f)\n",
-            tA - t1, tB - tA, tC - tB, tC2 - tC, tD - tC2, tE - tD, tF - tE, S[0].plan_ms, S[2].plan_ms);
+    fprintf(stderr, "[svd1] host: launch1 %.3f finished U1 %.3f U2 %.3f V1 %.3f V2 %.3f (plans %.3f %.3f) U1 landed %.3f finish %.3f spawn %.3f\n",
+            tA - t1, t_fin[0] - t1, t_fin[1] - t1, t_fin[2] - t1, t_fin[3] - t1, S[0].plan_ms, S[2].plan_ms,
+            t_dbg[0] - t1, t_dbg[1] - t1, t_dbg[2] - t1);
   const double t3 = now_ms();
   R.t_ms[1] = t3 - t1;
   // ---- sign alignment: final column i = position N-1-i
@@ -2166,6 +2223,14 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   }
   R.t_ms[4] = now_ms() - t0;
   R.t_ms[5] = std::max(ev_ms(P, 16, 17), ev_ms(P, 18, 17));  // both sides' applies
+  if (std::getenv("SVD1_TIMING")) {  // device timeline relative to the first spectral launch
+    const char* nm[4] = {"U1", "U2", "V1", "V2"};
+    for (int e = 0; e < 4; ++e)
+      fprintf(stderr, "[svd1] dev %s spectral %.3f..%.3f apply %.3f..%.3f\n", nm[e],
+              ev_ms(P, 8, 8 + 2 * e), ev_ms(P, 8, 9 + 2 * e), ev_ms(P, 8, 2 * e), ev_ms(P, 8, 2 * e + 1));
+    fprintf(stderr, "[svd1] dev end %.3f; host: spectral rounds %.3f, t4 %.3f, end %.3f\n", ev_ms(P, 8, 17),
+            t3 - t1, t4 - t1, now_ms() - t1);
+  }
   R.kernel_launches = P->launches - launches0;
   if (rep) *rep = R;
   return SVD1_OK;
