@@ -117,6 +117,23 @@ svd1_status svd1_update(svd1_plan_t plan, double* U, int64_t ldu, double* sigma,
                         double* V, int64_t ldv, const double* a, const double* b,
                         double eps, svd1_report* rep);
 
+/* A stream of K rank-1 updates A_t = A_{t-1} + a_t b_t^T, t = 0..K-1, applied in order
+ * on one GPU (single process: u_rows = m, v_rows = n).  Results are those of K calls
+ * of svd1_update (same algorithm, same tolerances), but the updates are pipelined
+ * (DESIGN.md §4.9): every update's projections U_t^T a_t, U_t^T g, V_t^T b_t are
+ * carried as a few extra rows through the previous updates' transforms (the rows of U
+ * and of a projection transform alike, U_{t+1}^T a = X^T U_t^T a), so the spectral phase
+ * of update t+1 runs while the applies of update t are still on the GPU.
+ * A (device): a_t at A + t*lda (m doubles, lda >= m); B (device): b_t at B + t*ldb
+ * (n doubles, ldb >= n).  U, sigma, V as for svd1_update (in place).  reps: K host
+ * reports or NULL (their device-time fields apply_ms, gemm_ms, t_ms[5] are 0 in this
+ * mode).  On an error at update t the factors hold the result of updates 0..t-1 and
+ * the error is returned.  K <= 28 per call (longer streams: call repeatedly). */
+svd1_status svd1_update_batch(svd1_plan_t plan, double* U, int64_t ldu, double* sigma,
+                              double* V, int64_t ldv, const double* A, int64_t lda,
+                              const double* B, int64_t ldb, int64_t K, double eps,
+                              svd1_report* reps);
+
 /* Row-sharded update, phase 1 (STEP 1 projections over the LOCAL rows):
  * proj (device, 5*m + n + 6 doubles) receives the partial sums
  *   proj[0:m]        = U_loc^T a_loc          (x_a = U^T a)

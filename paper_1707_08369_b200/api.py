@@ -82,6 +82,19 @@ class Plan:
                              float(eps), C.byref(rep)), "svd1_update")
         return rep.as_dict()
 
+    def update_batch(self, U, sigma, V, A, B, eps=-1.0):
+        """K in-place rank-1 updates in order: A (K x m), B (K x n) row-major, row t = a_t, b_t.
+        Pipelined; returns the K reports."""
+        K = A.shape[0]
+        if A.dim() != 2 or B.dim() != 2 or B.shape[0] != K:
+            raise ValueError("A, B must be K x m and K x n")
+        reps = (L.Report * max(K, 1))()
+        _check(L.svd1_update_batch(self._h, _ptr(U, name="U"), _ld(U), _ptr(sigma, name="sigma"),
+                                   _ptr(V, name="V"), _ld(V), _ptr(A, name="A"), _ld(A),
+                                   _ptr(B, name="B"), _ld(B), int(K), float(eps), reps),
+               "svd1_update_batch")
+        return [reps[t].as_dict() for t in range(K)]
+
     def proj_size(self):
         return 5 * self.m + self.n + 6
 

@@ -83,8 +83,10 @@ __global__ void __launch_bounds__(256) apply_direct_kernel(
     for (int e = 0; e < 4; ++e) {
       const int idx = tid + e * 256;
       const int kk = idx >> 6, jj = idx & 63;
+      // padded sources (i >= n) and targets (j >= n) get exact zeros: a padding d_i = 0
+      // meets a root mu_j = 0 (the null-space root of a rank-deficient side) as 0 / 0
       const double del = (s_di[kk] - s_dk[jj]) - s_tau[jj];
-      Bs[kk * DLDB + jj] = (s_zi[kk] * s_cs[jj]) / del;
+      Bs[kk * DLDB + jj] = (i0 + kk < n && j0 + jj < n) ? (s_zi[kk] * s_cs[jj]) / del : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -585,6 +587,88 @@ svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
   apply_direct_kernel<<<grid, 256, 0, st>>>(rows, n, d, k, tau, zhat, cs, U_in, ld_in, src, U_out,
                                             ld_out, dst);
   *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+// ------------------------------------------------------------------ K11' few rows
+// part[s][r][j] = sum_{i in split s} U_in[r, src_i] zhat_i / ((d_i - d_kj) - tau_j): thread
+// per target j (128 per block), the split's sources staged 32 at a time with their rows;
+// RB = rows rounded up (registers).  Then U_out[r, dst_j] = cs_j sum_s part[s][r][j].
+constexpr int kFewSplitChunk = 512;  // sources per split
+template <int RB>
+__global__ void __launch_bounds__(128) few_rows_partial_kernel(
+    int rows, int n, const double* __restrict__ d, const int32_t* __restrict__ k,
+    const double* __restrict__ tau, const double* __restrict__ zhat, const double* __restrict__ U_in,
+    int64_t ld_in, const int32_t* __restrict__ src, double* __restrict__ part) {
+  __shared__ double s_u[RB][32];
+  __shared__ double s_d[32], s_z[32];
+  const int j = blockIdx.x * 128 + threadIdx.x;
+  const int i_lo = blockIdx.y * kFewSplitChunk, i_hi = min(n, i_lo + kFewSplitChunk);
+  const double dk = j < n ? d[k[j]] : 0.0, tj = j < n ? tau[j] : 1.0;
+  double acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+  for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * 32; e += 128) {
+      const int r = e >> 5, ii = e & 31, i = i0 + ii;
+      s_u[r][ii] = (r < rows && i < i_hi) ? U_in[int64_t(r) * ld_in + (src ? src[i] : i)] : 0.0;
+    }
+    if (threadIdx.x < 32) {
+      const int i = i0 + threadIdx.x;
+      s_d[threadIdx.x] = i < i_hi ? d[i] : 0.0;
+      s_z[threadIdx.x] = i < i_hi ? zhat[i] : 0.0;
+    }
+    __syncthreads();
+    const int cnt = min(32, i_hi - i0);
+    for (int ii = 0; ii < cnt; ++ii) {
+      const double c = s_z[ii] / ((s_d[ii] - dk) - tj);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[r] = fma(c, s_u[r][ii], acc[r]);
+    }
+  }
+  if (j < n) {
+    const int64_t base = int64_t(blockIdx.y) * rows * n;
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (r < rows) part[base + int64_t(r) * n + j] = acc[r];
+  }
+}
+
+__global__ void few_rows_combine_kernel(int rows, int n, int nsplit, const double* __restrict__ part,
+                                        const double* __restrict__ cs, double* __restrict__ U_out,
+                                        int64_t ld_out, const int32_t* __restrict__ dst) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= int64_t(rows) * n) return;
+  const int r = int(e / n), j = int(e % n);
+  double s = 0.0;
+  for (int q = 0; q < nsplit; ++q) s += part[(int64_t(q) * rows + r) * n + j];
+  U_out[int64_t(r) * ld_out + (dst ? dst[j] : j)] = cs[j] * s;
+}
+
+int64_t few_rows_scratch_elems(int rows, int n) {
+  const int64_t nsplit = (int64_t(n) + kFewSplitChunk - 1) / kFewSplitChunk;
+  return std::max<int64_t>(1, nsplit * rows * n);
+}
+
+svd1_status apply_few_rows(int rows, int n, const double* d, const int32_t* k, const double* tau,
+                           const double* zhat, const double* cs, const double* U_in, int64_t ld_in,
+                           const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
+                           double* scratch, cudaStream_t st, int64_t* launches) {
+  if (rows <= 0 || n <= 0) return SVD1_OK;
+  if (rows > 32) return SVD1_E_INVALID;
+  const int nsplit = (n + kFewSplitChunk - 1) / kFewSplitChunk;
+  const dim3 grid(unsigned((n + 127) / 128), unsigned(nsplit));
+  if (rows <= 8)
+    few_rows_partial_kernel<8><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
+  else if (rows <= 16)
+    few_rows_partial_kernel<16><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
+  else
+    few_rows_partial_kernel<32><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
+  few_rows_combine_kernel<<<unsigned((int64_t(rows) * n + 255) / 256), 256, 0, st>>>(rows, n, nsplit, scratch,
+                                                                                      cs, U_out, ld_out, dst);
+  *launches += 2;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

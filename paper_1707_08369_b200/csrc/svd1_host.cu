@@ -195,6 +195,7 @@ struct StepRecord {
   SecPlanHost sec;          // secular FMM plan (large active sizes)
   DevBuf sec_blob, sec_scr;
   int sec_fmm_used = 0;
+  DevBuf rot_goff, rot_cols, rot_mats;  // pairing rotations (the V2 step's record)
 };
 
 
@@ -214,8 +215,17 @@ struct svd1_plan_s {
   DevBuf probes;                 // 4 x u_rows sign probes
   bool probes_ready = false;
   cudaStream_t st2 = nullptr;    // V-side applies run here, concurrently with the U side
+  cudaStream_t sp[2] = {};       // batch mode: spectral + carried-row streams (U, V side)
   cudaEvent_t sync_ev[4] = {};
   StepRecord steps[4];
+  // batch mode (svd1_update_batch): step records per update parity (the
+  // next update's spectral phase runs while this one's applies are in flight), carried
+  // projection rows (ping-pong per side), and the events marking each parity's applies done
+  StepRecord bsteps[2][4];
+  DevBuf RU[2], RV[2], few_scr[2], bproj;
+  cudaEvent_t bdone[2][2] = {};  // [parity][side]
+  bool bdone_rec[2] = {false, false};
+  cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
   double* h_pin = nullptr;  // pinned staging for read-backs
   size_t h_pin_cap = 0;
   // pinned upload arenas, one per side stream (U side: st, V side: st2): every
@@ -226,7 +236,7 @@ struct svd1_plan_s {
     size_t cap = 0, used = 0;
     cudaEvent_t ev = nullptr;
     bool pending = false;
-  } arena[2];
+  } arena[4];  // sides 0, 1: apply streams; 2, 3: batch spectral streams
   CauchyPrep standalone;    // plan of the standalone svd1_cauchy_apply
   std::vector<int32_t> rot_goff, rot_cols;  // pairing rotations of repeated sigma clusters
   std::vector<double> rot_mats;
@@ -255,8 +265,17 @@ svd1_status ensure_st2(svd1_plan_t P) {
   if (!P->st2) SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->st2, cudaStreamNonBlocking));
   return SVD1_OK;
 }
+svd1_status ensure_side(svd1_plan_t P, int side) {
+  if (side == 1) return ensure_st2(P);
+  if (side >= 2 && !P->sp[side - 2])
+    SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->sp[side - 2], cudaStreamNonBlocking));
+  return SVD1_OK;
+}
 // side 0 (U) works on the plan stream, side 1 (V) on st2
-cudaStream_t side_stream(svd1_plan_t P, int side) { return side ? P->st2 : P->st; }
+// side 2 (U) and 3 (V): the batch mode's spectral streams
+cudaStream_t side_stream(svd1_plan_t P, int side) {
+  return side == 0 ? P->st : side == 1 ? P->st2 : P->sp[side - 2];
+}
 
 // Wait for the uploads in flight and rewind the arenas (called at API entry points).
 svd1_status arena_reset(svd1_plan_t P, int side) {
@@ -267,8 +286,8 @@ svd1_status arena_reset(svd1_plan_t P, int side) {
   return SVD1_OK;
 }
 svd1_status arena_reset(svd1_plan_t P) {
-  TRY(arena_reset(P, 0));
-  return arena_reset(P, 1);
+  for (int side = 0; side < 4; ++side) TRY(arena_reset(P, side));
+  return SVD1_OK;
 }
 
 // reserve `bytes` of side's arena (rewinding or growing it when full): offset
@@ -306,7 +325,7 @@ svd1_status arena_commit(svd1_plan_t P, int side, size_t off, size_t bytes, void
 }
 
 svd1_status arena_put(svd1_plan_t P, const void* src, size_t bytes, void* dev, int side = 0) {
-  if (side) TRY(ensure_st2(P));
+  TRY(ensure_side(P, side));
   size_t off;
   TRY(arena_reserve(P, side, bytes, &off));
   std::memcpy(P->arena[side].buf + off, src, bytes);
@@ -332,7 +351,7 @@ struct BlobBuilder {
 };
 
 svd1_status arena_put_blob(svd1_plan_t P, const BlobBuilder& B, DevBuf& dev, char** out, int side = 0) {
-  if (side) TRY(ensure_st2(P));
+  TRY(ensure_side(P, side));
   TRY(dev.get<char>(std::max<size_t>(B.total, 1), out));
   if (B.total == 0) return SVD1_OK;
   size_t off;
@@ -1391,7 +1410,7 @@ struct Joiner {
 svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<double>& D,
                             const std::vector<double>& z, double rho,
                             const std::vector<std::vector<double>>& carries, int ev0, int side) {
-  if (side) TRY(ensure_st2(P));
+  TRY(ensure_side(P, side));
   const cudaStream_t st = side_stream(P, side);
   const double th_start = now_ms();
   const int N = int(D.size());
@@ -1736,6 +1755,48 @@ svd1_status apply_launch(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_
     TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, S.dpsrc, U_out, ld_out, S.dpdst, S.dpscale,
                     st, &P->launches));
   TRY(ev_record(P, ev0 + 1, st));
+  if (std::getenv("SVD1_NANCHECK")) {  // diagnostics: first non-finite output column
+    SVD1_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<double> hb(size_t(rows) * ld_out);
+    SVD1_CUDA_TRY(cudaMemcpy(hb.data(), U_out, hb.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    int64_t bad = -1, nbad = 0;
+    for (int64_t r = 0; r < rows; ++r)
+      for (int64_t c2 = 0; c2 < S.N; ++c2)
+        if (!std::isfinite(hb[r * ld_out + c2])) {
+          ++nbad;
+          if (bad < 0) bad = c2;
+        }
+    double csmin = 1e300, csmax = 0.0;
+    for (double v : S.cs_h) {
+      csmin = std::min(csmin, std::fabs(v));
+      csmax = std::max(csmax, std::fabs(v));
+    }
+    fprintf(stderr, "[svd1] apply ev%d N=%d na=%d hh_groups=%zu pass=%zu: non-finite %lld (first col %lld) cs [%.3e, %.3e]\n",
+            ev0, S.N, S.na, S.h_goff.size() - 1, S.pass_src.size(), (long long)nbad, (long long)bad, csmin, csmax);
+    int ncs = 0, ntau = 0;
+    for (double v : S.cs_h) ncs += !std::isfinite(v);
+    for (double v : S.tau_h) ntau += !std::isfinite(v);
+    std::vector<double> zh(S.na);
+    cudaMemcpy(zh.data(), S.d_zhat.p, S.na * sizeof(double), cudaMemcpyDeviceToHost);
+    int nzh = 0;
+    for (double v : zh) nzh += !std::isfinite(v);
+    if (bad >= 0) {
+      int wj = -1, wq = -1, nw = 0;
+      for (int j = 0; j < S.na; ++j)
+        if (S.dst_cols[j] == bad) wj = j, ++nw;
+      for (size_t q = 0; q < S.pass_dst_cols.size(); ++q)
+        if (S.pass_dst_cols[q] == bad) wq = int(q), ++nw;
+      std::vector<double> inb(size_t(rows) * ld_in);
+      cudaMemcpy(inb.data(), U_in, inb.size() * sizeof(double), cudaMemcpyDeviceToHost);
+      int64_t nin = 0;
+      for (double v : inb) nin += !std::isfinite(v);
+      fprintf(stderr, "   col %lld written by j %d q %d (%d writers); non-finite in U_in %lld; pass_scale %g\n", (long long)bad, wj, wq, nw,
+              (long long)nin, wq >= 0 ? S.pass_scale[wq] : 0.0);
+      if (wj >= 0) fprintf(stderr, "   j %d: k %d tau %.17g cs %g\n", wj, S.k_h[wj], S.tau_h[wj], S.cs_h[wj]);
+    }
+    fprintf(stderr, "   nonfinite cs %d tau %d zhat %d; j0: k %d tau %.17g cs %.6g mu %.6g d0 %.17g d1 %.6g zhat0 %.6g dst0 %d\n", ncs, ntau, nzh,
+            S.k_h[0], S.tau_h[0], S.cs_h[0], S.mu[0], S.da[0], S.na > 1 ? S.da[1] : 0.0, zh[0], S.dst_cols[0]);
+  }
   return SVD1_OK;
 }
 
@@ -1787,7 +1848,14 @@ svd1_status svd1_plan_destroy(svd1_plan_t P) {
   if (!P) return SVD1_E_INVALID;
   cudaStreamSynchronize(P->st);
   if (P->st2) cudaStreamSynchronize(P->st2);
+  for (auto& q : P->sp)
+    if (q) cudaStreamSynchronize(q);
   if (P->h_pin) cudaFreeHost(P->h_pin);
+  for (auto& pe : P->bdone)
+    for (auto& e : pe)
+      if (e) cudaEventDestroy(e);
+  for (auto& e : P->rb_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& A : P->arena) {
     if (A.buf) cudaFreeHost(A.buf);
     if (A.ev) cudaEventDestroy(A.ev);
@@ -1800,6 +1868,8 @@ svd1_status svd1_plan_destroy(svd1_plan_t P) {
     cudaStreamSynchronize(P->st2);
     cudaStreamDestroy(P->st2);
   }
+  for (auto& q : P->sp)
+    if (q) cudaStreamDestroy(q);
   delete P;
   return SVD1_OK;
 }
@@ -1822,12 +1892,42 @@ svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const doub
                  proj, static_cast<double*>(P->probes.p), P->st, &P->launches);
 }
 
-svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,
-                                  int64_t ldv, const double* proj, const double* a, const double* b,
-                                  double eps, svd1_report* rep) {
-  (void)a;
-  (void)b;
-  if (!P || !sigma || !proj) return SVD1_E_INVALID;
+}  // extern "C"
+
+namespace {
+// Batch mode context of one update (svd1_update_batch).
+struct BatchCtx {
+  int parity = 0;
+  const double* h_proj = nullptr;   // host: [x_a | x_g (4) | y_b | dots] of this update
+  std::vector<double>* sig = nullptr;  // in: sigma_t (descending), out: sigma_{t+1}
+  int ru_rows = 0, rv_rows = 0;     // carried rows to transform (U: m wide, V: n wide)
+  double* h_next = nullptr;         // pinned: read-back of the next update's x_a | x_g | y_b
+  int ru_next = -1, rv_next = -1;   // carried row index of the next update's a / b (-1: none)
+};
+
+// carried rows through one step's transform: Householder (in place on `in`), Cauchy
+// product of the few rows, passthrough of the deflated columns
+svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, int64_t ld, int rows,
+                       cudaStream_t st, int side) {
+  if (rows <= 0) return SVD1_OK;
+  if (S.h_goff.size() > 1)
+    TRY(householder_cols(rows, in, ld, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, st, &P->launches));
+  if (S.na > 0) {
+    double* scr;
+    TRY(P->few_scr[side].get<double>(size_t(few_rows_scratch_elems(rows, S.na)), &scr));
+    TRY(apply_few_rows(rows, S.na, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
+                       static_cast<double*>(S.d_out.p) + S.na, static_cast<double*>(S.d_zhat.p), S.dcs, in, ld,
+                       S.dsrc, out, ld, S.ddst, scr, st, &P->launches));
+  }
+  if (!S.pass_src.empty())
+    TRY(passthrough(rows, int(S.pass_src.size()), in, ld, S.dpsrc, out, ld, S.dpdst, S.dpscale, st,
+                    &P->launches));
+  return SVD1_OK;
+}
+
+svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                        const double* proj, double eps, svd1_report* rep, BatchCtx* B) {
+  if (!P || (!B && (!sigma || !proj)) || (B && (!B->h_proj || !B->sig))) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
   const int64_t m = c.m, n = c.n;
   if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < n))) return SVD1_E_INVALID;
@@ -1839,20 +1939,25 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   std::memset(&R, 0, sizeof(R));
   P->p = choose_p(eps > 0.0 ? eps : c.eps);
   R.p = P->p;
-  // ---- read back the projections and sigma (one sync)
+  // ---- read back the projections and sigma (one sync); batch mode: given on the host
   const size_t nproj = size_t(5 * m + n + 6);
   double* h;
-  TRY(pinned(P, nproj + size_t(m), &h));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(h, proj, nproj * sizeof(double), cudaMemcpyDeviceToHost, P->st));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(h + nproj, sigma, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost, P->st));
-  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
-  if (!all_finite(h, nproj + size_t(m))) return SVD1_E_NONFINITE;
+  if (B) {
+    h = const_cast<double*>(B->h_proj);
+    if (!all_finite(h, nproj) || !all_finite(B->sig->data(), size_t(m))) return SVD1_E_NONFINITE;
+  } else {
+    TRY(pinned(P, nproj + size_t(m), &h));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(h, proj, nproj * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(h + nproj, sigma, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+    SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+    if (!all_finite(h, nproj + size_t(m))) return SVD1_E_NONFINITE;
+  }
   const double* xa = h;
   const double* xg = h + m;
   const double* yb = h + 5 * m;
   const double* ag = h + 5 * m + n;
   const double alpha = ag[4], beta = ag[5];
-  std::vector<double> sig(h + nproj, h + nproj + m);
+  std::vector<double> sig = B ? *B->sig : std::vector<double>(h + nproj, h + nproj + m);
   R.t_ms[0] = now_ms() - t0;
   if (alpha == 0.0 || beta == 0.0) {  // A_hat = A
     R.noop = 1;
@@ -1897,7 +2002,15 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
                          size_t(4 * std::max<int64_t>(n, 1) / std::max(P->leaf, 1) + 8);
     for (int side = 0; side < 2; ++side) TRY(ensure_expansions(P, side, guess));
   }
-  const bool one_stream = std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
+  const bool one_stream = !B && std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
+  // spectral work and uploads: the apply streams' sides (0, 1), or in batch mode the
+  // spectral streams (2, 3), so the next update's spectral phase is not queued behind
+  // this update's applies
+  const int sp0 = B ? 2 : 0, sp1 = B ? 3 : (one_stream ? 0 : 1);
+  if (B) {
+    TRY(ensure_side(P, 2));
+    TRY(ensure_side(P, 3));
+  }
   cudaStream_t stv = one_stream ? P->st : P->st2;
   // ---- spectral phase.  Each side is a chain on its own stream (U: the plan stream,
   // V: st2): STEP 4 -> STEP 5 and STEP 6 -> STEP 7.  The chains are
@@ -1908,7 +2021,12 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   // it writes only the workspace W, so U, Sigma and V stay untouched until every
   // eigen-update has succeeded.
   const double t1 = now_ms();
-  StepRecord* S = P->steps;
+  StepRecord* S = B ? P->bsteps[B->parity] : P->steps;
+  if (B && P->bdone_rec[B->parity]) {  // the applies that last used these records are done
+    SVD1_CUDA_TRY(cudaEventSynchronize(P->bdone[B->parity][0]));
+    SVD1_CUDA_TRY(cudaEventSynchronize(P->bdone[B->parity][1]));
+    P->bdone_rec[B->parity] = false;
+  }
   {
     std::vector<double> zu = z1, zv = z3;
     std::vector<std::vector<double>> cu1(cu.begin() + 1, cu.end()), cv1(cv.begin() + 1, cv.end());
@@ -1917,8 +2035,8 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
     cv1.insert(cv1.begin(), cv[0]);
     cu.swap(cu1);
     cv.swap(cv1);
-    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8, 0));
-    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, one_stream ? 0 : 1));
+    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8, sp0));
+    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, sp1));
   }
   const double tA = now_ms();
   std::atomic<bool> planned[4] = {false, false, false, false};  // outlives the Joiners
@@ -1952,10 +2070,56 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   bool fin[4] = {false, false, false, false};
   bool launched_u1 = false, launched_v1 = false, uploaded_u1 = false, uploaded_v1 = false;
   double t_fin[4] = {0, 0, 0, 0}, t_dbg[4] = {0, 0, 0, 0};
+  auto nrot_v = [&]() { return c.v_rows > 0 ? int(P->rot_goff.size()) - 1 : 0; };
+  auto upload_rot = [&](int us) -> svd1_status {  // pairing rotations (set before step 3's upload)
+    if (nrot_v() <= 0) return SVD1_OK;
+    int32_t *g, *cl;
+    double* mt;
+    TRY(upload(P, S[3].rot_goff, P->rot_goff, &g, us));
+    TRY(upload(P, S[3].rot_cols, P->rot_cols, &cl, us));
+    TRY(upload(P, S[3].rot_mats, P->rot_mats, &mt, us));
+    return SVD1_OK;
+  };
+  // upload step e's apply data; in batch mode on its spectral stream, which then carries
+  // the projection rows of later updates through the same transform (apply_rows), and
+  // the apply stream waits for the upload only
+  auto upload_step = [&](int e) -> svd1_status {
+    const int side = e < 2 ? 0 : 1;
+    const int us = B ? side + 2 : (one_stream ? 0 : side);
+    TRY(apply_upload(P, S[e], us));
+    if (!B) return SVD1_OK;
+    const cudaStream_t ss = side_stream(P, us), as = side_stream(P, side);
+    if (e == 3) TRY(upload_rot(us));
+    TRY(stream_wait(P, e, ss, as));
+    DevBuf* R = side ? P->RV : P->RU;
+    const int rows = side ? B->rv_rows : B->ru_rows;
+    const int64_t ld = side ? n : m;
+    const bool second = e == 1 || e == 3;  // R[0] -> R[1] (first step), R[1] -> R[0]
+    double* rin = static_cast<double*>(R[second ? 1 : 0].p);
+    double* rout = static_cast<double*>(R[second ? 0 : 1].p);
+    TRY(apply_rows(P, S[e], rin, rout, ld, rows, ss, side));
+    if (e == 3 && rows > 0 && nrot_v() > 0)
+      TRY(col_rotate(rows, rout, ld, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
+                     static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), ss,
+                     &P->launches));
+    if (second) {  // read back the next update's rows: x_a | x_g (U side), y_b (V side)
+      if (!P->rb_ev[side]) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->rb_ev[side], cudaEventDisableTiming));
+      if (side == 0 && B->ru_next >= 0) {
+        SVD1_CUDA_TRY(cudaMemcpyAsync(B->h_next, rout + int64_t(B->ru_next) * m, m * sizeof(double),
+                                      cudaMemcpyDeviceToHost, ss));
+        SVD1_CUDA_TRY(cudaMemcpyAsync(B->h_next + m, rout, 4 * m * sizeof(double), cudaMemcpyDeviceToHost, ss));
+      }
+      if (side == 1 && B->rv_next >= 0)
+        SVD1_CUDA_TRY(cudaMemcpyAsync(B->h_next + 5 * m, rout + int64_t(B->rv_next) * n, n * sizeof(double),
+                                      cudaMemcpyDeviceToHost, ss));
+      SVD1_CUDA_TRY(cudaEventRecord(P->rb_ev[side], ss));
+    }
+    return SVD1_OK;
+  };
   auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
     const int side = e == 0 ? 0 : 1;
     TRY(rare_grow(e, side));
-    TRY(apply_upload(P, S[e], one_stream ? 0 : side));
+    TRY(upload_step(e));
     if (S[e].h_goff.size() <= 1) {  // nothing transformed in place: start now
       if (e == 0) {
         TRY(ev_record(P, 16, P->st));
@@ -1991,7 +2155,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
       t_dbg[2] = now_ms();
       std::vector<double> z2 = cu[0];
       cu.erase(cu.begin());
-      TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, 0));
+      TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, sp0));
       t_fin[0] = now_ms();
       continue;
     }
@@ -2001,7 +2165,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
       spawn_plan(plan_v, 2, false, 1, c.v_rows);
       std::vector<double> z4 = cv[0];
       cv.erase(cv.begin());
-      TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, one_stream ? 0 : 1));
+      TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, sp1));
       t_fin[2] = now_ms();
       continue;
     }
@@ -2180,25 +2344,43 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   }
   plan_u2.join();
   TRY(rare_grow(1, 0));
-  TRY(apply_upload(P, S[1], 0));
+  TRY(upload_step(1));
   TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
   plan_v2.join();
   TRY(rare_grow(3, 1));
-  TRY(apply_upload(P, S[3], one_stream ? 0 : 1));  // carries the sign alignment
-  const int nrot = int(P->rot_goff.size()) - 1;
-  if (nrot > 0 && c.v_rows > 0) {
-    int32_t *g, *cl;
-    double* mt;
-    const int sd = one_stream ? 0 : 1;
-    TRY(upload(P, P->d_rot_goff, P->rot_goff, &g, sd));
-    TRY(upload(P, P->d_rot_cols, P->rot_cols, &cl, sd));
-    TRY(upload(P, P->d_rot_mats, P->rot_mats, &mt, sd));
-  }
+  TRY(upload_step(3));  // carries the sign alignment
+  if (!B) TRY(upload_rot(one_stream ? 0 : 1));
   TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, stv, 1));
-  if (nrot > 0 && c.v_rows > 0)
-    TRY(col_rotate(c.v_rows, V, ldv, nrot, static_cast<int32_t*>(P->d_rot_goff.p),
-                   static_cast<int32_t*>(P->d_rot_cols.p), static_cast<double*>(P->d_rot_mats.p),
-                   stv, &P->launches));
+  if (nrot_v() > 0)
+    TRY(col_rotate(c.v_rows, V, ldv, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
+                   static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
+                   &P->launches));
+  if (B) {  // no join, no sync: the next update's spectral phase overlaps these applies
+    for (int sd = 0; sd < 2; ++sd) {
+      if (!P->bdone[B->parity][sd])
+        SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][sd], cudaEventDisableTiming));
+      SVD1_CUDA_TRY(cudaEventRecord(P->bdone[B->parity][sd], side_stream(P, sd)));
+    }
+    P->bdone_rec[B->parity] = true;
+    R.t_ms[2] = now_ms() - t4;
+    *B->sig = sig_new;
+    for (int e = 0; e < 4; ++e) {
+      const bool has = S[e].rows > 0 && S[e].na > 0;
+      R.apply_flops[e] = has ? S[e].cp.flops : 0.0;
+      R.apply_flops_exec[e] = has ? S[e].cp.flops_exec : 0.0;
+      R.fmm_used[e] = has ? S[e].cp.fmm : 0;
+      if (R.fmm_used[e]) {
+        R.fmm_levels[e] = S[e].cp.F.L;
+        R.fmm_max_near[e] = S[e].cp.F.max_near;
+      }
+      R.spectral_ms[e] = S[e].spectral_ms;
+      R.mean_iter[e] = S[e].mean_iter;
+    }
+    R.t_ms[4] = now_ms() - t0;
+    R.kernel_launches = P->launches - launches0;
+    if (rep) *rep = R;
+    return SVD1_OK;
+  }
   TRY(stream_wait(P, 2, P->st2, P->st));  // join
   TRY(ev_record(P, 17, P->st));           // apply phase end
   R.t_ms[2] = now_ms() - t4;
@@ -2234,6 +2416,104 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   R.kernel_launches = P->launches - launches0;
   if (rep) *rep = R;
   return SVD1_OK;
+}
+}  // namespace
+
+extern "C" {
+
+svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,
+                                  int64_t ldv, const double* proj, const double* a, const double* b,
+                                  double eps, svd1_report* rep) {
+  (void)a;
+  (void)b;
+  return update_impl(P, U, ldu, sigma, V, ldv, proj, eps, rep, nullptr);
+}
+
+svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                              const double* A, int64_t lda, const double* Bv, int64_t ldb, int64_t K,
+                              double eps, svd1_report* reps) {
+  if (!P || !U || !V || !sigma || (K > 0 && (!A || !Bv)) || K < 0 || K > 28) return SVD1_E_INVALID;
+  const svd1_config& c = P->cfg;
+  const int64_t m = c.m, n = c.n;
+  if (c.u_rows != m || c.v_rows != n || ldu < m || ldv < n || lda < m || ldb < n) return SVD1_E_INVALID;
+  if (K == 0) return SVD1_OK;
+  const int k = int(K);
+  TRY(arena_reset(P));
+  TRY(ensure_st2(P));
+  TRY(ensure_side(P, 2));
+  TRY(ensure_side(P, 3));
+  // every update's STEP-1 projections against the initial factors
+  const size_t nproj = size_t(5 * m + n + 6);
+  double* pj;
+  TRY(P->bproj.get<double>(size_t(k) * nproj, &pj));
+  for (int t = 0; t < k; ++t)
+    TRY(svd1_project(P, U, ldu, V, ldv, A + int64_t(t) * lda, Bv + int64_t(t) * ldb, pj + size_t(t) * nproj));
+  // carried rows (row-major, m resp. n wide): U side [x_g (4) | x_a(K-1) .. x_a(1)],
+  // V side [y_b(K-1) .. y_b(1)]; update t transforms the rows of updates t+1.. only
+  const int ru_max = 4 + (k - 1), rv_max = std::max(k - 1, 1);
+  double *ru0, *ru1, *rv0, *rv1;
+  TRY(P->RU[0].get<double>(size_t(ru_max) * m, &ru0));
+  TRY(P->RU[1].get<double>(size_t(ru_max) * m, &ru1));
+  TRY(P->RV[0].get<double>(size_t(rv_max) * n, &rv0));
+  TRY(P->RV[1].get<double>(size_t(rv_max) * n, &rv1));
+  double* scr;  // few-rows scratch at its largest up front (no reallocation mid-batch)
+  TRY(P->few_scr[0].get<double>(size_t(few_rows_scratch_elems(ru_max, int(m))), &scr));
+  TRY(P->few_scr[1].get<double>(size_t(few_rows_scratch_elems(rv_max, int(n))), &scr));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(ru0, pj + m, 4 * m * sizeof(double), cudaMemcpyDeviceToDevice, P->st));
+  for (int s = 1; s < k; ++s) {
+    SVD1_CUDA_TRY(cudaMemcpyAsync(ru0 + int64_t(4 + (k - 1 - s)) * m, pj + size_t(s) * nproj, m * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, P->st));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(rv0 + int64_t(k - 1 - s) * n, pj + size_t(s) * nproj + 5 * m,
+                                  n * sizeof(double), cudaMemcpyDeviceToDevice, P->st));
+  }
+  // host copies of the projections (dots of every update; x's of update 0) and sigma
+  double* h;
+  TRY(pinned(P, size_t(k) * nproj + size_t(m) + size_t(5 * m + n), &h));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(h, pj, size_t(k) * nproj * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(h + size_t(k) * nproj, sigma, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost,
+                                P->st));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));  // also orders the copies before the V stream
+  double* hn = h + size_t(k) * nproj + m;  // next update's x_a | x_g | y_b (read back)
+  std::vector<double> sig(h + size_t(k) * nproj, h + size_t(k) * nproj + m);
+  std::vector<double> hp(h, h + nproj);
+  svd1_status st = SVD1_OK;
+  for (int t = 0; t < k && st == SVD1_OK; ++t) {
+    if (t > 0) {  // x's from the carried rows, dots from update t's projection
+      std::memcpy(hp.data(), hn, size_t(5 * m + n) * sizeof(double));
+      std::memcpy(hp.data() + 5 * m + n, h + size_t(t) * nproj + 5 * m + n, 6 * sizeof(double));
+    }
+    BatchCtx b;
+    b.parity = t & 1;
+    b.h_proj = hp.data();
+    b.sig = &sig;
+    b.ru_rows = t + 1 < k ? 4 + (k - 1 - t) : 0;
+    b.rv_rows = t + 1 < k ? k - 1 - t : 0;
+    b.ru_next = t + 1 < k ? 4 + (k - 2 - t) : -1;
+    b.rv_next = t + 1 < k ? k - 2 - t : -1;
+    b.h_next = hn;
+    svd1_report R;
+    st = update_impl(P, U, ldu, sigma, V, ldv, nullptr, eps, &R, &b);
+    if (reps) reps[t] = R;
+    if (st != SVD1_OK || t + 1 >= k) break;
+    if (R.noop) {  // nothing transformed: the next rows are where they were
+      SVD1_CUDA_TRY(cudaDeviceSynchronize());
+      SVD1_CUDA_TRY(cudaMemcpy(hn, ru0 + int64_t(b.ru_next) * m, m * sizeof(double), cudaMemcpyDeviceToHost));
+      SVD1_CUDA_TRY(cudaMemcpy(hn + m, ru0, 4 * m * sizeof(double), cudaMemcpyDeviceToHost));
+      SVD1_CUDA_TRY(cudaMemcpy(hn + 5 * m, rv0 + int64_t(b.rv_next) * n, n * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+    } else {
+      SVD1_CUDA_TRY(cudaEventSynchronize(P->rb_ev[0]));
+      SVD1_CUDA_TRY(cudaEventSynchronize(P->rb_ev[1]));
+    }
+  }
+  // drain every stream; the factors now hold updates 0..t; sigma of the last success
+  for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1]}) SVD1_CUDA_TRY(cudaStreamSynchronize(q));
+  P->bdone_rec[0] = P->bdone_rec[1] = false;
+  std::memcpy(h + size_t(k) * nproj, sig.data(), size_t(m) * sizeof(double));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(sigma, h + size_t(k) * nproj, size_t(m) * sizeof(double), cudaMemcpyHostToDevice,
+                                P->st));
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  return st;
 }
 
 svd1_status svd1_update(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,

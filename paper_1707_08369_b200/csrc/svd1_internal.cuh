@@ -107,6 +107,15 @@ svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
                          double* U_out, int64_t ld_out, const int32_t* dst,
                          cudaStream_t st, int64_t* launches);
 
+// K11': the same product for a few rows (rows <= 32: the carried projection rows of a
+// batch): thread per target j, sources split over blocks (partials in
+// `scratch`, at least few_rows_scratch_elems doubles), ordered combine (deterministic).
+int64_t few_rows_scratch_elems(int rows, int n);
+svd1_status apply_few_rows(int rows, int n, const double* d, const int32_t* k, const double* tau,
+                           const double* zhat, const double* cs, const double* U_in, int64_t ld_in,
+                           const int32_t* src, double* U_out, int64_t ld_out, const int32_t* dst,
+                           double* scratch, cudaStream_t st, int64_t* launches);
+
 // K4: Householder column groups, in place: for each group g, cols idx[off_g..off_g+len_g)
 // U[:, idx] <- U[:, idx] (I - 2 v v^T / v^T v), v = hv[off_g..].
 svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,

@@ -1,0 +1,115 @@
+"""Batched (pipelined) update stream, svd1_update_batch, through the
+C ABI: the same K updates as K svd1_update calls, with the projections carried as extra
+rows through each update's transforms.  Checked against the sequential GPU path, and
+against the oracle's invariants (singular values of the explicitly accumulated matrix,
+residual, orthogonality)."""
+import numpy as np
+import pytest
+
+from synth import config_inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1707_08369_b200 as P  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV, torch.float64)
+
+
+def _stream(inp, K, flags, batch):
+    U, s, V = T(inp["U"]), T(inp["sigma"]), T(inp["V"])
+    m, n = U.shape[0], V.shape[0]
+    plan = P.Plan(m, n, flags=flags)
+    ab = inp["ab"][:K]
+    if batch:
+        A = T(np.stack([a for a, _ in ab]))
+        B = T(np.stack([b for _, b in ab]))
+        reps = plan.update_batch(U, s, V, A, B)
+    else:
+        reps = [plan.update(U, s, V, T(a), T(b)) for a, b in ab]
+    torch.cuda.synchronize()
+    plan.close()
+    return U, s, V, reps
+
+
+def _invariants(inp, K, U, s, V):
+    m = U.shape[0]
+    A = (inp["U"] * inp["sigma"][None, :]) @ inp["V"][:, :m].T
+    for a, b in inp["ab"][:K]:
+        A = A + np.outer(a, b)
+    At = T(A)
+    res = float(torch.linalg.norm(At @ V[:, :m] - U * s[None, :], dim=0).max() / s[0])
+    orth = max(float((U.T @ U - torch.eye(m, dtype=torch.float64, device=DEV)).abs().max()),
+               float((V.T @ V - torch.eye(V.shape[0], dtype=torch.float64, device=DEV)).abs().max()))
+    sv = np.linalg.svd(A, compute_uv=False)
+    sig_err = float(np.max(np.abs(s.cpu().numpy() - sv)) / sv[0])
+    return res, orth, sig_err
+
+
+@pytest.mark.parametrize("cfg,m,n,K,flags,exact", [
+    (1, None, None, 3, 0, True),            # C1 full size, direct path
+    (2, 300, 300, 3, P.FORCE_DIRECT, True),
+    (3, 256, 256, 6, P.FORCE_FMM, True),    # C3 recipe (graded, near-deflation)
+    (4, 64, 256, 5, 0, True),               # C4 recipe: rectangular, null-space Householder
+    (5, 200, 200, 4, P.FORCE_FMM, False),   # C5 recipe: duplicated sigma (pairing rotations)
+])
+def test_batch_matches_sequential(cfg, m, n, K, flags, exact):
+    inp = config_inputs(cfg, m=m, n=n, updates=K)
+    Ub, sb, Vb, rb = _stream(inp, K, flags, batch=True)
+    Us, ss, Vs, rs = _stream(inp, K, flags, batch=False)
+    sbn, ssn = sb.cpu().numpy(), ss.cpu().numpy()
+    assert np.max(np.abs(sbn - ssn)) <= 1e-12 * ssn[0]
+    for Z in ((Ub, sb, Vb), (Us, ss, Vs)):
+        res, orth, sig_err = _invariants(inp, K, *Z)
+        assert res <= 1e-10 and orth <= 1e-10 and sig_err <= 1e-12, (res, orth, sig_err)
+    if exact:  # isolated singular values: same vectors (signs included) up to rounding
+        m_ = Ub.shape[0]
+        assert float((Ub - Us).abs().max()) <= 1e-8
+        assert float((Vb[:, :m_] - Vs[:, :m_]).abs().max()) <= 1e-8
+    assert [r["n_active"] for r in rb] == [r["n_active"] for r in rs]
+
+
+def test_batch_noop_and_error():
+    inp = config_inputs(3, m=128, n=128, updates=5)
+    ab = list(inp["ab"][:5])
+    ab[1] = (np.zeros(128), ab[1][1])          # A_hat = A: a no-op inside the stream
+    inp2 = dict(inp, ab=ab)
+    Ub, sb, Vb, rb = _stream(inp2, 5, P.FORCE_FMM, batch=True)
+    Us, ss, Vs, rs = _stream(inp2, 5, P.FORCE_FMM, batch=False)
+    assert rb[1]["noop"] == 1
+    assert float((Ub - Us).abs().max()) <= 1e-8 and float((sb - ss).abs().max()) <= 1e-12 * float(ss[0])
+    # a non-finite b at update 3: error, factors hold updates 0..2
+    ab3 = list(inp["ab"][:5])
+    bad = ab3[3][1].copy()
+    bad[7] = np.nan
+    ab3[3] = (ab3[3][0], bad)
+    inp3 = dict(inp, ab=ab3)
+    U, s, V = T(inp["U"]), T(inp["sigma"]), T(inp["V"])
+    plan = P.Plan(128, 128, flags=P.FORCE_FMM)
+    with pytest.raises(P.SVD1Error) as e:
+        plan.update_batch(U, s, V, T(np.stack([a for a, _ in ab3])), T(np.stack([b for _, b in ab3])))
+    assert e.value.code == 2
+    Us3, ss3, Vs3, _ = _stream(inp3, 3, P.FORCE_FMM, batch=False)
+    assert float((U - Us3).abs().max()) <= 1e-8 and float((s - ss3).abs().max()) <= 1e-12 * float(ss3[0])
+
+
+def test_batch_c3_full_size():
+    """C3 at full size (m = n = 4096, FMM applies), 4 pipelined updates."""
+    inp = config_inputs(3, updates=4)
+    Ub, sb, Vb, rb = _stream(inp, 4, 0, batch=True)
+    m = 4096
+    assert all(r["fmm_used"][0] for r in rb)
+    orth = max(float((Ub.T @ Ub - torch.eye(m, dtype=torch.float64, device=DEV)).abs().max()),
+               float((Vb.T @ Vb - torch.eye(m, dtype=torch.float64, device=DEV)).abs().max()))
+    A = T(inp["U"]) * T(inp["sigma"])[None, :] @ T(inp["V"]).T
+    for a, b in inp["ab"][:4]:
+        A = A + torch.outer(T(a), T(b))
+    res = float(torch.linalg.norm(A @ Vb - Ub * sb[None, :], dim=0).max() / sb[0])
+    assert res <= 1e-10 and orth <= 1e-10, (res, orth)

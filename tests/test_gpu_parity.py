@@ -229,3 +229,18 @@ def test_update_parity_secular_fmm(cfg, m, n):
     inp = config_inputs(cfg, m=m, n=n, updates=1)
     a, b = inp["ab"][0]
     _check_update(inp["U"], inp["sigma"], inp["V"], a, b, flags=P.SECULAR_FMM)
+
+
+def test_rectangular_stream_null_root():
+    """C4 recipe (m < n), five chained updates: the V side's null-space root lands on
+    mu = 0 exactly, where a padded source of the direct apply (d = 0) once gave 0/0."""
+    inp = config_inputs(4, m=64, n=256, updates=5)
+    Ug, sg, Vg = T(inp["U"]), T(inp["sigma"]), T(inp["V"])
+    plan = P.Plan(64, 256)
+    A = (inp["U"] * inp["sigma"][None, :]) @ inp["V"][:, :64].T
+    for a, b in inp["ab"]:
+        plan.update(Ug, sg, Vg, T(a), T(b))
+        A = A + np.outer(a, b)
+    assert bool(torch.isfinite(Vg).all()) and bool(torch.isfinite(Ug).all())
+    res = float(torch.linalg.norm(T(A) @ Vg[:, :64] - Ug * sg[None, :], dim=0).max() / sg[0])
+    assert res <= 1e-10
