@@ -150,6 +150,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--sequential", action="store_true",
+                    help="time the per-update API (svd1_update) instead of svd1_update_batch")
     ap.add_argument("--config", type=int, default=CFG_ID, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default C3, the headline metric's workload)")
     args = ap.parse_args()
@@ -191,6 +193,30 @@ def main():
         a_t, b_t = ab[t % len(ab)] if a is None else (a, b)
         return upd.update(U, sig, V, a_t, b_t)
 
+    # one GPU: the stream of updates goes through svd1_update_batch (pipelined: update
+    # t+1's spectral phase overlaps update t's applies); row-sharded
+    # runs use the per-update path (projections all-reduced every update)
+    batch = world == 1 and not args.sequential
+    A_all = torch.stack([a for a, _ in ab])
+    B_all = torch.stack([b for _, b in ab])
+
+    def run(t0, K, A_src=None, B_src=None):
+        """updates t0 .. t0+K-1 of the stream; returns their reports"""
+        if not batch:
+            return [step(t) for t in range(t0, t0 + K)]
+        out = []
+        t = t0
+        while t < t0 + K:
+            kc = min(28, t0 + K - t)
+            idx = [(t + q) % len(ab) for q in range(kc)]
+            if A_src is None:
+                Ab, Bb = A_all[idx], B_all[idx]
+            else:
+                Ab, Bb = A_src[[q - t0 for q in range(t, t + kc)]], B_src[[q - t0 for q in range(t, t + kc)]]
+            out += upd.plan.update_batch(U, sig, V, Ab, Bb)
+            t += kc
+        return out
+
     def restore():
         U.copy_(Upr)
         V.copy_(Vpr)
@@ -200,8 +226,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    for t in range(args.warmup):
-        step(t)
+    run(0, args.warmup)
     restore()
     torch.cuda.synchronize()
     reps = []
@@ -210,8 +235,7 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for t in range(args.steps):
-            reps.append(step(t))
+        reps = run(0, args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -221,13 +245,26 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     value = args.steps / (ms / 1e3)
+    seq = None
+    if batch:  # the per-update API on the same stream, for reference (not the headline)
+        restore()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for t in range(args.steps):
+            step(t)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        sms = g0.elapsed_time(g1)
+        seq = {"api": "svd1_update (one call per update)", "value": args.steps / (sms / 1e3),
+               "ms_per_step": sms / args.steps}
 
     # roofline of the dominant kernel (the FMM Cauchy apply), from live CUDA events
     ap_ms = sum(r["t_ms"][5] for r in reps)  # apply phase (U and V sides concurrent)
     ap_fl = sum(sum(r["apply_flops"]) for r in reps)
     ap_fx = sum(sum(r["apply_flops_exec"]) for r in reps)
     sp_ms = sum(sum(r["spectral_ms"]) for r in reps)
-    n_apply = sum(sum(1 for x in r["apply_ms"] if x > 0) for r in reps)
+    n_apply = sum(sum(1 for x in r["apply_flops"] if x > 0) for r in reps)
     # dominant kernel: the FMM Cauchy apply (its GEMM passes carry every algorithmic
     # flop).  The U- and V-side applies run concurrently on two streams (and may overlap
     # the other side's last spectral step), so per-kernel durations overlap; the
@@ -255,6 +292,9 @@ def main():
                           "P2M/M2M/M2L/L2L/L2P/P2P from the plan); the plan executes "
                           "flops_exec_per_apply (coarse levels in bands, DESIGN.md §4.4)",
             "timing": ("CUDA events on the launching streams around the apply phase of every update in "
+                       "the timed region (svd1_update_batch: each update's window = its first apply start "
+                       "-> its last apply end; windows of consecutive updates may overlap, which only "
+                       "lowers achieved); "
                        "the timed region (both sides' applies; window includes any overlap with the "
                        "other side's last spectral step)"),
             "apply_share_of_step": ap_ms / ms if ms else None,
@@ -273,12 +313,23 @@ def main():
         torch.cuda.synchronize()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if batch:
+            A_h = torch.stack([a_h[t % len(ab)] for t in range(args.steps)]).pin_memory()
+            B_h = torch.stack([b_h[t % len(ab)] for t in range(args.steps)]).pin_memory()
+            A_d, B_d = torch.empty_like(A_h, device=dev), torch.empty_like(B_h, device=dev)
+            torch.cuda.synchronize()
         f0.record(stream)
-        for t in range(args.steps):
-            a_d.copy_(a_h[t % len(ab)], non_blocking=True)
-            b_d.copy_(b_h[t % len(ab)], non_blocking=True)
-            step(t, a_d, b_d)
+        if batch:  # every step's a, b copied from pinned host memory; sigma read back
+            A_d.copy_(A_h, non_blocking=True)
+            B_d.copy_(B_h, non_blocking=True)
+            run(0, args.steps, A_d, B_d)
             s_h.copy_(sig, non_blocking=True)
+        else:
+            for t in range(args.steps):
+                a_d.copy_(a_h[t % len(ab)], non_blocking=True)
+                b_d.copy_(b_h[t % len(ab)], non_blocking=True)
+                step(t, a_d, b_d)
+                s_h.copy_(sig, non_blocking=True)
         f1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -288,9 +339,12 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
         e2e = {"value": args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * (m + n),
-               "d2h_bytes_per_step": 8 * m,
-               "note": "factors stay resident (streaming update); a, b copied from pinned host "
-                       "memory and sigma read back every step through the public API"}
+               "d2h_bytes_per_step": (8 * m * -(-args.steps // 28)) / args.steps if batch else 8 * m,
+               "note": ("factors stay resident (streaming update); every step's a, b copied from pinned "
+                        "host memory inside the timed region, svd1_update_batch over the stream (chunks "
+                        "of <= 28), sigma read back after it" if batch else
+                        "factors stay resident (streaming update); a, b copied from pinned host "
+                        "memory and sigma read back every step through the public API")}
 
     # correctness check of the timed stream (outside the timed region): residual and
     # orthogonality against the explicitly accumulated A_hat (verification only)
@@ -298,8 +352,8 @@ def main():
     if not args.no_check and world == 1:
         restore()
         A = (U0 * s0[None, :]) @ V0[:, :m].T
+        run(0, args.steps)
         for t in range(args.steps):
-            step(t)
             a_t, b_t = ab[t % len(ab)]
             A = A + torch.outer(a_t, b_t)
         res = float(torch.linalg.norm(A @ V[:, :m] - U * sig[None, :], dim=0).max() / sig[0])
@@ -330,7 +384,9 @@ def main():
                            "l2": (f"inputs larger than L2 (U + V = {8 * (m * m + n * n) / 2**20:.0f} MiB > 126 MB)"
                                   if 8 * (m * m + n * n) > 126e6 else
                                   f"inputs fit in L2 ({8 * (m * m + n * n) / 2**20:.1f} MiB); no flush"),
-                           "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU"},
+                           "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
+                           "api": "svd1_update_batch (pipelined stream)" if batch else "svd1_update"},
+                "sequential_api": seq,
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
                 "cpu_baseline": cpu, "check": check,
                 "spectral_ms_per_step": sp_ms / args.steps, "apply_ms_per_step": ap_ms / args.steps,

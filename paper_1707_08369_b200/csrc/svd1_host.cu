@@ -226,6 +226,7 @@ struct svd1_plan_s {
   cudaEvent_t bdone[2][2] = {};  // [parity][side]
   bool bdone_rec[2] = {false, false};
   cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
+  cudaEvent_t bwin[2][4] = {};   // [parity]: apply start U, V; apply end U, V (timing)
   double* h_pin = nullptr;  // pinned staging for read-backs
   size_t h_pin_cap = 0;
   // pinned upload arenas, one per side stream (U side: st, V side: st2): every
@@ -267,8 +268,14 @@ svd1_status ensure_st2(svd1_plan_t P) {
 }
 svd1_status ensure_side(svd1_plan_t P, int side) {
   if (side == 1) return ensure_st2(P);
-  if (side >= 2 && !P->sp[side - 2])
-    SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->sp[side - 2], cudaStreamNonBlocking));
+  if (side >= 2 && !P->sp[side - 2]) {
+    // batch mode's spectral streams run at the highest priority: their short kernels
+    // gate the next update, the applies they share the GPU with fill in behind them
+    int lo = 0, hi = 0;
+    SVD1_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    static const bool flat = std::getenv("SVD1_FLAT_PRIORITY") != nullptr;  // experiments
+    SVD1_CUDA_TRY(cudaStreamCreateWithPriority(&P->sp[side - 2], cudaStreamNonBlocking, flat ? lo : hi));
+  }
   return SVD1_OK;
 }
 // side 0 (U) works on the plan stream, side 1 (V) on st2
@@ -374,6 +381,26 @@ svd1_status stream_wait(svd1_plan_t P, int slot, cudaStream_t signaller, cudaStr
   SVD1_CUDA_TRY(cudaEventRecord(P->sync_ev[slot], signaller));
   SVD1_CUDA_TRY(cudaStreamWaitEvent(waiter, P->sync_ev[slot], 0));
   return SVD1_OK;
+}
+
+// batch mode: record apply-window event q (0/1: start U/V, 2/3: end U/V) of a parity
+svd1_status bwin_record(svd1_plan_t P, int par, int q, cudaStream_t st) {
+  if (!P->bwin[par][q]) SVD1_CUDA_TRY(cudaEventCreate(&P->bwin[par][q]));
+  SVD1_CUDA_TRY(cudaEventRecord(P->bwin[par][q], st));
+  return SVD1_OK;
+}
+// first apply start -> last apply end of the update with that parity (after it completed)
+double bwin_ms(svd1_plan_t P, int par) {
+  auto el = [&](int a, int b) {
+    float ms = 0.f;
+    if (!P->bwin[par][a] || !P->bwin[par][b] ||
+        cudaEventElapsedTime(&ms, P->bwin[par][a], P->bwin[par][b]) != cudaSuccess) {
+      cudaGetLastError();
+      return 0.0;
+    }
+    return double(ms);
+  };
+  return std::max(el(0, 2), el(0, 3)) - std::min(0.0, el(0, 1));
 }
 
 double ev_ms(svd1_plan_t P, int a, int b) {
@@ -1902,6 +1929,7 @@ struct BatchCtx {
   std::vector<double>* sig = nullptr;  // in: sigma_t (descending), out: sigma_{t+1}
   int ru_rows = 0, rv_rows = 0;     // carried rows to transform (U: m wide, V: n wide)
   double* h_next = nullptr;         // pinned: read-back of the next update's x_a | x_g | y_b
+  double* prev_win = nullptr;       // receives the apply window (ms) of the update two back
   int ru_next = -1, rv_next = -1;   // carried row index of the next update's a / b (-1: none)
 };
 
@@ -2026,6 +2054,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     SVD1_CUDA_TRY(cudaEventSynchronize(P->bdone[B->parity][0]));
     SVD1_CUDA_TRY(cudaEventSynchronize(P->bdone[B->parity][1]));
     P->bdone_rec[B->parity] = false;
+    if (B->prev_win) *B->prev_win = bwin_ms(P, B->parity);
   }
   {
     std::vector<double> zu = z1, zv = z3;
@@ -2123,10 +2152,12 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     if (S[e].h_goff.size() <= 1) {  // nothing transformed in place: start now
       if (e == 0) {
         TRY(ev_record(P, 16, P->st));
+        if (B) TRY(bwin_record(P, B->parity, 0, P->st));
         TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
         launched_u1 = true;
       } else {
         TRY(ev_record(P, 18, stv));
+        if (B) TRY(bwin_record(P, B->parity, 1, stv));
         TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
         launched_v1 = true;
       }
@@ -2336,10 +2367,12 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   const double t4 = now_ms();
   if (!launched_u1) {
     TRY(ev_record(P, 16, P->st));
+    if (B) TRY(bwin_record(P, B->parity, 0, P->st));
     TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
   }
   if (!launched_v1) {
     TRY(ev_record(P, 18, stv));
+    if (B) TRY(bwin_record(P, B->parity, 1, stv));
     TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
   }
   plan_u2.join();
@@ -2356,6 +2389,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
                    static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
                    &P->launches));
   if (B) {  // no join, no sync: the next update's spectral phase overlaps these applies
+    TRY(bwin_record(P, B->parity, 2, P->st));
+    TRY(bwin_record(P, B->parity, 3, stv));
     for (int sd = 0; sd < 2; ++sd) {
       if (!P->bdone[B->parity][sd])
         SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][sd], cudaEventDisableTiming));
@@ -2443,14 +2478,17 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   TRY(ensure_side(P, 2));
   TRY(ensure_side(P, 3));
   // every update's STEP-1 projections against the initial factors
+  // buffers sized for the largest batch (28) whatever K is: no reallocation (and its
+  // implicit device synchronisation) between batches of different lengths
+  constexpr int kMaxBatch = 28;
   const size_t nproj = size_t(5 * m + n + 6);
   double* pj;
-  TRY(P->bproj.get<double>(size_t(k) * nproj, &pj));
+  TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj));
   for (int t = 0; t < k; ++t)
     TRY(svd1_project(P, U, ldu, V, ldv, A + int64_t(t) * lda, Bv + int64_t(t) * ldb, pj + size_t(t) * nproj));
   // carried rows (row-major, m resp. n wide): U side [x_g (4) | x_a(K-1) .. x_a(1)],
   // V side [y_b(K-1) .. y_b(1)]; update t transforms the rows of updates t+1.. only
-  const int ru_max = 4 + (k - 1), rv_max = std::max(k - 1, 1);
+  const int ru_max = 4 + (kMaxBatch - 1), rv_max = kMaxBatch - 1;
   double *ru0, *ru1, *rv0, *rv1;
   TRY(P->RU[0].get<double>(size_t(ru_max) * m, &ru0));
   TRY(P->RU[1].get<double>(size_t(ru_max) * m, &ru1));
@@ -2468,7 +2506,7 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   }
   // host copies of the projections (dots of every update; x's of update 0) and sigma
   double* h;
-  TRY(pinned(P, size_t(k) * nproj + size_t(m) + size_t(5 * m + n), &h));
+  TRY(pinned(P, size_t(kMaxBatch) * nproj + size_t(m) + size_t(5 * m + n), &h));
   SVD1_CUDA_TRY(cudaMemcpyAsync(h, pj, size_t(k) * nproj * sizeof(double), cudaMemcpyDeviceToHost, P->st));
   SVD1_CUDA_TRY(cudaMemcpyAsync(h + size_t(k) * nproj, sigma, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost,
                                 P->st));
@@ -2491,6 +2529,7 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
     b.ru_next = t + 1 < k ? 4 + (k - 2 - t) : -1;
     b.rv_next = t + 1 < k ? k - 2 - t : -1;
     b.h_next = hn;
+    b.prev_win = (reps && t >= 2) ? &reps[t - 2].t_ms[5] : nullptr;
     svd1_report R;
     st = update_impl(P, U, ldu, sigma, V, ldv, nullptr, eps, &R, &b);
     if (reps) reps[t] = R;
@@ -2508,6 +2547,9 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   }
   // drain every stream; the factors now hold updates 0..t; sigma of the last success
   for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1]}) SVD1_CUDA_TRY(cudaStreamSynchronize(q));
+  if (reps && st == SVD1_OK)  // apply windows of the last two updates
+    for (int t = std::max(0, k - 2); t < k; ++t)
+      if (P->bdone_rec[t & 1]) reps[t].t_ms[5] = bwin_ms(P, t & 1);
   P->bdone_rec[0] = P->bdone_rec[1] = false;
   std::memcpy(h + size_t(k) * nproj, sig.data(), size_t(m) * sizeof(double));
   SVD1_CUDA_TRY(cudaMemcpyAsync(sigma, h + size_t(k) * nproj, size_t(m) * sizeof(double), cudaMemcpyHostToDevice,
