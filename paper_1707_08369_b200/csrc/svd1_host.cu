@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -227,6 +228,11 @@ struct svd1_plan_s {
   bool bdone_rec[2] = {false, false};
   cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
   cudaEvent_t bwin[2][4] = {};   // [parity]: apply start U, V; apply end U, V (timing)
+  // SVD1_TIMELINE diagnostics (batch mode): labelled device events and host stamps
+  std::vector<std::pair<std::string, cudaEvent_t>> tl_dev;
+  std::vector<std::pair<std::string, double>> tl_host;
+  double tl_t0 = 0.0;
+  bool tl_on = false;
   double* h_pin = nullptr;  // pinned staging for read-backs
   size_t h_pin_cap = 0;
   // pinned upload arenas, one per side stream (U side: st, V side: st2): every
@@ -401,6 +407,18 @@ double bwin_ms(svd1_plan_t P, int par) {
     return double(ms);
   };
   return std::max(el(0, 2), el(0, 3)) - std::min(0.0, el(0, 1));
+}
+
+void tl_mark(svd1_plan_t P, const std::string& label, cudaStream_t st, bool dev = true) {  // diagnostics
+  if (!P->tl_on) return;
+  P->tl_host.push_back({label, now_ms() - P->tl_t0});
+  if (dev) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) == cudaSuccess) {
+      cudaEventRecord(e, st);
+      P->tl_dev.push_back({label, e});
+    }
+  }
 }
 
 double ev_ms(svd1_plan_t P, int a, int b) {
@@ -1723,23 +1741,57 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
 // Host half of one apply, in two parts: apply_plan (pure host compute, thread-safe per
 // step: column maps and the Cauchy/FMM plan) and apply_upload (staged uploads).
 // out_col(q) = reverse ? (N - 1 - q) : q.
-void apply_plan(const svd1_config& cfg, int p, StepRecord& S, int64_t rows, bool reverse, int side) {
+// output buffer columns of the step (main thread, before its plan is spawned)
+void set_out_cols(StepRecord& S, int64_t rows, bool reverse) {
+  const int N = S.N;
+  S.rows = rows;
+  auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
+  S.dst_cols.resize(S.na);
+  for (int j = 0; j < S.na; ++j) S.dst_cols[j] = oc(S.tgt_pos[j]);
+  S.pass_dst_cols.resize(S.pass_dst.size());
+  for (size_t q = 0; q < S.pass_dst.size(); ++q) S.pass_dst_cols[q] = oc(S.pass_dst[q]);
+}
+
+// the step's Cauchy/FMM plan (worker thread: touches S.cp and S.plan_ms only)
+void apply_plan(const svd1_config& cfg, int p, StepRecord& S) {
   const double t0 = now_ms();
   struct Stamp {
     StepRecord& S;
     double t0;
     ~Stamp() { S.plan_ms = now_ms() - t0; }
   } stamp{S, t0};
-  const int N = S.N;
-  S.rows = rows;
-  auto oc = [&](int q) { return reverse ? N - 1 - q : q; };
-  if (rows <= 0) return;
-  S.dst_cols.resize(S.na);
-  for (int j = 0; j < S.na; ++j) S.dst_cols[j] = oc(S.tgt_pos[j]);
-  S.pass_dst_cols.resize(S.pass_dst.size());
-  for (size_t q = 0; q < S.pass_dst.size(); ++q) S.pass_dst_cols[q] = oc(S.pass_dst[q]);
-  (void)side;
-  if (S.na > 0) cauchy_plan(cfg, S.cp, rows, S.na, S.da, S.mu, p, S.src_cols.data(), S.N);
+  if (S.rows <= 0) return;
+  if (S.na > 0) cauchy_plan(cfg, S.cp, S.rows, S.na, S.da, S.mu, p, S.src_cols.data(), S.N);
+}
+
+// batch mode: the column maps, Householder groups and scales alone (what the carried
+// rows need; no plan), and the FMM plan separately once it is built
+svd1_status upload_maps(svd1_plan_t P, StepRecord& S, int side) {
+  BlobBuilder B;
+  const size_t o_goff = B.add(S.h_goff), o_hcols = B.add(S.h_cols), o_hv = B.add(S.h_hv);
+  const size_t o_src = B.add(S.src_cols), o_dst = B.add(S.dst_cols);
+  const size_t o_cs = B.add(S.cs_h);
+  const size_t o_ps = B.add(S.pass_src), o_pd = B.add(S.pass_dst_cols), o_pc = B.add(S.pass_scale);
+  char* base;
+  TRY(arena_put_blob(P, B, S.blob, &base, side));
+  S.dgoff = reinterpret_cast<int32_t*>(base + o_goff);
+  S.dhcols = reinterpret_cast<int32_t*>(base + o_hcols);
+  S.dhv = reinterpret_cast<double*>(base + o_hv);
+  S.dsrc = reinterpret_cast<int32_t*>(base + o_src);
+  S.ddst = reinterpret_cast<int32_t*>(base + o_dst);
+  S.dcs = reinterpret_cast<double*>(base + o_cs);
+  S.dpsrc = reinterpret_cast<int32_t*>(base + o_ps);
+  S.dpdst = reinterpret_cast<int32_t*>(base + o_pd);
+  S.dpscale = reinterpret_cast<double*>(base + o_pc);
+  return SVD1_OK;
+}
+svd1_status upload_fmm(svd1_plan_t P, StepRecord& S, int side) {
+  if (S.rows <= 0 || S.na <= 0 || !S.cp.fmm) return SVD1_OK;
+  BlobBuilder B;
+  cauchy_stage(S.cp, B);
+  char* base;
+  TRY(arena_put_blob(P, B, S.cp.blob, &base, side));
+  return cauchy_bind(S.cp, base);
 }
 
 svd1_status apply_upload(svd1_plan_t P, StepRecord& S, int side) {
@@ -1924,7 +1976,7 @@ svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const doub
 namespace {
 // Batch mode context of one update (svd1_update_batch).
 struct BatchCtx {
-  int parity = 0;
+  int parity = 0, t = 0;
   const double* h_proj = nullptr;   // host: [x_a | x_g (4) | y_b | dots] of this update
   std::vector<double>* sig = nullptr;  // in: sigma_t (descending), out: sigma_{t+1}
   int ru_rows = 0, rv_rows = 0;     // carried rows to transform (U: m wide, V: n wide)
@@ -2064,7 +2116,10 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     cv1.insert(cv1.begin(), cv[0]);
     cu.swap(cu1);
     cv.swap(cv1);
+    const std::string ut = B ? "u" + std::to_string(B->t) + " " : "";
+    tl_mark(P, ut + "U1 spectral", side_stream(P, sp0));
     TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8, sp0));
+    tl_mark(P, ut + "V1 spectral", side_stream(P, sp1));
     TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, sp1));
   }
   const double tA = now_ms();
@@ -2085,8 +2140,10 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // its plan on a worker thread).  Readiness is polled (cudaEventQuery, atomic flags),
   // so neither side's host step waits behind the other side's GPU work.
   auto spawn_plan = [&](Joiner& J, int e, bool reverse, int side, int64_t rows) {
-    J.add(std::thread([&S, &planned, pcfg, pp, e, reverse, side, rows] {
-      apply_plan(pcfg, pp, S[e], rows, reverse, side);
+    (void)side;
+    set_out_cols(S[e], rows, reverse);
+    J.add(std::thread([&S, &planned, pcfg, pp, e] {
+      apply_plan(pcfg, pp, S[e]);
       planned[e].store(true, std::memory_order_release);
     }));
   };
@@ -2109,17 +2166,17 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     TRY(upload(P, S[3].rot_mats, P->rot_mats, &mt, us));
     return SVD1_OK;
   };
-  // upload step e's apply data; in batch mode on its spectral stream, which then carries
-  // the projection rows of later updates through the same transform (apply_rows), and
-  // the apply stream waits for the upload only
-  auto upload_step = [&](int e) -> svd1_status {
+  // batch mode, as soon as step e's eigen-update is known (no plan needed): its column
+  // maps on its spectral stream, and the carried projection rows of later updates
+  // through the step's transform there (apply_rows); after the second step of a side
+  // the next update's rows are read back, so the next update can start while this
+  // one's applies are still being planned and launched
+  auto rows_step = [&](int e) -> svd1_status {
     const int side = e < 2 ? 0 : 1;
-    const int us = B ? side + 2 : (one_stream ? 0 : side);
-    TRY(apply_upload(P, S[e], us));
-    if (!B) return SVD1_OK;
-    const cudaStream_t ss = side_stream(P, us), as = side_stream(P, side);
+    const int us = side + 2;
+    const cudaStream_t ss = side_stream(P, us);
+    TRY(upload_maps(P, S[e], us));
     if (e == 3) TRY(upload_rot(us));
-    TRY(stream_wait(P, e, ss, as));
     DevBuf* R = side ? P->RV : P->RU;
     const int rows = side ? B->rv_rows : B->ru_rows;
     const int64_t ld = side ? n : m;
@@ -2145,6 +2202,15 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     }
     return SVD1_OK;
   };
+  // upload step e's apply data (batch mode: its FMM plan, on its spectral stream after
+  // the maps; the apply stream waits for both)
+  auto upload_step = [&](int e) -> svd1_status {
+    const int side = e < 2 ? 0 : 1;
+    if (!B) return apply_upload(P, S[e], one_stream ? 0 : side);
+    const int us = side + 2;
+    TRY(upload_fmm(P, S[e], us));
+    return stream_wait(P, e, side_stream(P, us), side_stream(P, side));
+  };
   auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
     const int side = e == 0 ? 0 : 1;
     TRY(rare_grow(e, side));
@@ -2153,11 +2219,13 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       if (e == 0) {
         TRY(ev_record(P, 16, P->st));
         if (B) TRY(bwin_record(P, B->parity, 0, P->st));
+        tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U1 apply", P->st);
         TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
         launched_u1 = true;
       } else {
         TRY(ev_record(P, 18, stv));
         if (B) TRY(bwin_record(P, B->parity, 1, stv));
+        tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V1 apply", stv);
         TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
         launched_v1 = true;
       }
@@ -2183,9 +2251,11 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       fin[0] = true;
       t_dbg[1] = now_ms();
       spawn_plan(plan_u, 0, false, 0, c.u_rows);
+      if (B) TRY(rows_step(0));
       t_dbg[2] = now_ms();
       std::vector<double> z2 = cu[0];
       cu.erase(cu.begin());
+      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U1 finished; U2 spectral", side_stream(P, sp0));
       TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, sp0));
       t_fin[0] = now_ms();
       continue;
@@ -2194,8 +2264,10 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       TRY(spectral_finish(P, S[2], Dv, cv));
       fin[2] = true;
       spawn_plan(plan_v, 2, false, 1, c.v_rows);
+      if (B) TRY(rows_step(2));
       std::vector<double> z4 = cv[0];
       cv.erase(cv.begin());
+      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V1 finished; V2 spectral", side_stream(P, sp1));
       TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, sp1));
       t_fin[2] = now_ms();
       continue;
@@ -2203,13 +2275,16 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     if (fin[0] && !fin[1] && landed(1)) {
       TRY(spectral_finish(P, S[1], Du, cu));
       fin[1] = true;
+      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U2 finished", nullptr, false);
       spawn_plan(plan_u2, 1, true, 0, c.u_rows);
+      if (B) TRY(rows_step(1));
       t_fin[1] = now_ms();
       continue;
     }
     if (fin[2] && !fin[3] && landed(3)) {
       TRY(spectral_finish(P, S[3], Dv, cv));
       fin[3] = true;
+      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V2 finished", nullptr, false);
       spawn_plan(plan_v2, 3, true, 1, c.v_rows);
       t_fin[3] = now_ms();
       continue;
@@ -2349,6 +2424,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   }
   R.sign_flips = 0;
   for (int64_t i = 0; i < m; ++i) R.sign_flips += sgn[i] < 0.0;
+  if (B) TRY(rows_step(3));  // V2 maps carry the sign alignment and pairing rotations
   // ---- STEP 8: sigma = sqrt(max(D, 0)), descending
   std::vector<double> sig_new(m);
   for (int64_t i = 0; i < m; ++i) {
@@ -2378,17 +2454,21 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   plan_u2.join();
   TRY(rare_grow(1, 0));
   TRY(upload_step(1));
+  tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U2 apply", P->st);
   TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
   plan_v2.join();
   TRY(rare_grow(3, 1));
   TRY(upload_step(3));  // carries the sign alignment
   if (!B) TRY(upload_rot(one_stream ? 0 : 1));
+  tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V2 apply", stv);
   TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, stv, 1));
   if (nrot_v() > 0)
     TRY(col_rotate(c.v_rows, V, ldv, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                    static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
                    &P->launches));
   if (B) {  // no join, no sync: the next update's spectral phase overlaps these applies
+    tl_mark(P, "u" + std::to_string(B->t) + " U2 end", P->st);
+    tl_mark(P, "u" + std::to_string(B->t) + " V2 end", stv);
     TRY(bwin_record(P, B->parity, 2, P->st));
     TRY(bwin_record(P, B->parity, 3, stv));
     for (int sd = 0; sd < 2; ++sd) {
@@ -2515,6 +2595,9 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   std::vector<double> sig(h + size_t(k) * nproj, h + size_t(k) * nproj + m);
   std::vector<double> hp(h, h + nproj);
   svd1_status st = SVD1_OK;
+  P->tl_on = std::getenv("SVD1_TIMELINE") != nullptr;
+  P->tl_t0 = now_ms();
+  tl_mark(P, "batch start", P->st);
   for (int t = 0; t < k && st == SVD1_OK; ++t) {
     if (t > 0) {  // x's from the carried rows, dots from update t's projection
       std::memcpy(hp.data(), hn, size_t(5 * m + n) * sizeof(double));
@@ -2522,6 +2605,7 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
     }
     BatchCtx b;
     b.parity = t & 1;
+    b.t = t;
     b.h_proj = hp.data();
     b.sig = &sig;
     b.ru_rows = t + 1 < k ? 4 + (k - 1 - t) : 0;
@@ -2547,6 +2631,19 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   }
   // drain every stream; the factors now hold updates 0..t; sigma of the last success
   for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1]}) SVD1_CUDA_TRY(cudaStreamSynchronize(q));
+  if (P->tl_on) {  // host stamps and device times (ms from the batch start)
+    cudaEvent_t base = P->tl_dev.empty() ? nullptr : P->tl_dev.front().second;
+    for (size_t q = 0; q < P->tl_host.size(); ++q) fprintf(stderr, "[tl] host %8.3f %s\n", P->tl_host[q].second, P->tl_host[q].first.c_str());
+    for (auto& pr : P->tl_dev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, base, pr.second);
+      fprintf(stderr, "[tl] dev  %8.3f %s\n", ms, pr.first.c_str());
+    }
+    for (auto& pr : P->tl_dev) cudaEventDestroy(pr.second);
+    P->tl_dev.clear();
+    P->tl_host.clear();
+    P->tl_on = false;
+  }
   if (reps && st == SVD1_OK)  // apply windows of the last two updates
     for (int t = std::max(0, k - 2); t < k; ++t)
       if (P->bdone_rec[t & 1]) reps[t].t_ms[5] = bwin_ms(P, t & 1);
