@@ -227,6 +227,7 @@ struct svd1_plan_s {
   cudaEvent_t bdone[2][2] = {};  // [parity][side]
   bool bdone_rec[2] = {false, false};
   cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
+  cudaEvent_t maps_ev[4] = {};   // step e's column maps uploaded (spectral stream)
   cudaEvent_t bwin[2][4] = {};   // [parity]: apply start U, V; apply end U, V (timing)
   // SVD1_TIMELINE diagnostics (batch mode): labelled device events and host stamps
   std::vector<std::pair<std::string, cudaEvent_t>> tl_dev;
@@ -1600,6 +1601,7 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   TRY(S.d_zhat.get<double>(na, &dzh));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), st));
   TRY(ev_record(P, ev0, st));
+  tl_mark(P, "  ev" + std::to_string(ev0) + " uploaded", st);
   double* scr;
   TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
   S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na);
@@ -1610,8 +1612,11 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   } else {
     TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, st, &P->launches));   // STEP 2
   }
+  tl_mark(P, "  ev" + std::to_string(ev0) + " secular done", st);
   TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, st, &P->launches));
+  tl_mark(P, "  ev" + std::to_string(ev0) + " loewner done", st);
   TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, st, &P->launches));
+  tl_mark(P, "  ev" + std::to_string(ev0) + " colnorm done", st);
   TRY(ev_record(P, ev0 + 1, st));
   if (words * sizeof(double) > S.rb_cap) {
     if (S.rb) cudaFreeHost(S.rb);
@@ -2014,7 +2019,13 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if (m > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
   const int64_t launches0 = P->launches;
   const double t0 = now_ms();
-  TRY(arena_reset(P));
+  if (B) {  // the apply streams' arenas rewind only when full (their copies queue behind
+            // the previous update's applies)
+    TRY(arena_reset(P, 2));
+    TRY(arena_reset(P, 3));
+  } else {
+    TRY(arena_reset(P));
+  }
   svd1_report R;
   std::memset(&R, 0, sizeof(R));
   P->p = choose_p(eps > 0.0 ? eps : c.eps);
@@ -2177,6 +2188,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     const cudaStream_t ss = side_stream(P, us);
     TRY(upload_maps(P, S[e], us));
     if (e == 3) TRY(upload_rot(us));
+    if (!P->maps_ev[e]) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->maps_ev[e], cudaEventDisableTiming));
+    SVD1_CUDA_TRY(cudaEventRecord(P->maps_ev[e], ss));
     DevBuf* R = side ? P->RV : P->RU;
     const int rows = side ? B->rv_rows : B->ru_rows;
     const int64_t ld = side ? n : m;
@@ -2202,14 +2215,13 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     }
     return SVD1_OK;
   };
-  // upload step e's apply data (batch mode: its FMM plan, on its spectral stream after
-  // the maps; the apply stream waits for both)
+  // upload step e's apply data (batch mode: its FMM plan, on the apply stream itself,
+  // which waits for the step's maps only, not for the spectral work queued after them)
   auto upload_step = [&](int e) -> svd1_status {
     const int side = e < 2 ? 0 : 1;
     if (!B) return apply_upload(P, S[e], one_stream ? 0 : side);
-    const int us = side + 2;
-    TRY(upload_fmm(P, S[e], us));
-    return stream_wait(P, e, side_stream(P, us), side_stream(P, side));
+    SVD1_CUDA_TRY(cudaStreamWaitEvent(side_stream(P, side), P->maps_ev[e], 0));
+    return upload_fmm(P, S[e], side);
   };
   auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
     const int side = e == 0 ? 0 : 1;
