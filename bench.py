@@ -251,13 +251,16 @@ def main():
         torch.cuda.synchronize()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        for t in range(args.steps):
-            step(t)
+        seqreps = [step(t) for t in range(args.steps)]
         g1.record(stream)
         torch.cuda.synchronize()
         sms = g0.elapsed_time(g1)
+        sreps = seqreps
+        s_ap = sum(r["t_ms"][5] for r in sreps)
+        s_fl = sum(sum(r["apply_flops"]) for r in sreps)
         seq = {"api": "svd1_update (one call per update)", "value": args.steps / (sms / 1e3),
-               "ms_per_step": sms / args.steps}
+               "ms_per_step": sms / args.steps,
+               "apply_achieved_tflops": s_fl / (s_ap / 1e3) / 1e12 if s_ap > 0 else None}
 
     # roofline of the dominant kernel (the FMM Cauchy apply), from live CUDA events
     ap_ms = sum(r["t_ms"][5] for r in reps)  # apply phase (U and V sides concurrent)
@@ -298,6 +301,11 @@ def main():
                        "the timed region (both sides' applies; window includes any overlap with the "
                        "other side's last spectral step)"),
             "apply_share_of_step": ap_ms / ms if ms else None,
+            "achieved_isolated": (seq or {}).get("apply_achieved_tflops"),
+            "frac_isolated": ((seq or {}).get("apply_achieved_tflops") or 0.0) / FP64_PEAK_TFLOPS or None,
+            "isolated_note": ("the same applies timed in the per-update API run (sequential_api) of the "
+                              "same stream: there the next update's spectral kernels do not share the GPU "
+                              "with them") if batch else None,
             "spectral_share_of_step": sp_ms / ms if ms else None,
             "peak_source": "measured fp64 DMMA sustained (profiles/fp64_peak_r01.jsonl); "
                            "MEASURED_PEAKS.json has no fp64 entry"}

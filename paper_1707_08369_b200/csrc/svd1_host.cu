@@ -1987,6 +1987,7 @@ struct BatchCtx {
   int ru_rows = 0, rv_rows = 0;     // carried rows to transform (U: m wide, V: n wide)
   double* h_next = nullptr;         // pinned: read-back of the next update's x_a | x_g | y_b
   double* prev_win = nullptr;       // receives the apply window (ms) of the update two back
+  double* prev_gemm = nullptr;      // and its GEMM pass times (4; SVD1_GEMM_EVENTS)
   int ru_next = -1, rv_next = -1;   // carried row index of the next update's a / b (-1: none)
 };
 
@@ -2118,6 +2119,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     SVD1_CUDA_TRY(cudaEventSynchronize(P->bdone[B->parity][1]));
     P->bdone_rec[B->parity] = false;
     if (B->prev_win) *B->prev_win = bwin_ms(P, B->parity);
+    if (B->prev_gemm)
+      for (int e = 0; e < 4; ++e)
+        B->prev_gemm[e] = (S[e].rows > 0 && S[e].na > 0 && S[e].cp.fmm) ? S[e].cp.gemm_ms() : 0.0;
   }
   {
     std::vector<double> zu = z1, zv = z3;
@@ -2626,6 +2630,7 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
     b.rv_next = t + 1 < k ? k - 2 - t : -1;
     b.h_next = hn;
     b.prev_win = (reps && t >= 2) ? &reps[t - 2].t_ms[5] : nullptr;
+    b.prev_gemm = (reps && t >= 2) ? reps[t - 2].gemm_ms : nullptr;
     svd1_report R;
     st = update_impl(P, U, ldu, sigma, V, ldv, nullptr, eps, &R, &b);
     if (reps) reps[t] = R;
@@ -2658,7 +2663,13 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   }
   if (reps && st == SVD1_OK)  // apply windows of the last two updates
     for (int t = std::max(0, k - 2); t < k; ++t)
-      if (P->bdone_rec[t & 1]) reps[t].t_ms[5] = bwin_ms(P, t & 1);
+      if (P->bdone_rec[t & 1]) {
+        reps[t].t_ms[5] = bwin_ms(P, t & 1);
+        for (int e = 0; e < 4; ++e) {
+          StepRecord& Se = P->bsteps[t & 1][e];
+          reps[t].gemm_ms[e] = (Se.rows > 0 && Se.na > 0 && Se.cp.fmm) ? Se.cp.gemm_ms() : 0.0;
+        }
+      }
   P->bdone_rec[0] = P->bdone_rec[1] = false;
   std::memcpy(h + size_t(k) * nproj, sig.data(), size_t(m) * sizeof(double));
   SVD1_CUDA_TRY(cudaMemcpyAsync(sigma, h + size_t(k) * nproj, size_t(m) * sizeof(double), cudaMemcpyHostToDevice,
