@@ -595,7 +595,16 @@ svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
 // part[s][r][j] = sum_{i in split s} U_in[r, src_i] zhat_i / ((d_i - d_kj) - tau_j): thread
 // per target j (128 per block), the split's sources staged 32 at a time with their rows;
 // RB = rows rounded up (registers).  Then U_out[r, dst_j] = cs_j sum_s part[s][r][j].
-constexpr int kFewSplitChunk = 512;  // sources per split
+constexpr int kFewSplitChunk = 128;  // sources per split (many blocks: latency-bound work)
+
+__device__ __forceinline__ double few_rcp(double x) {  // 1/x to ~1 ulp: MUFU seed + 2 Newton steps
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
 template <int RB>
 __global__ void __launch_bounds__(128) few_rows_partial_kernel(
     int rows, int n, const double* __restrict__ d, const int32_t* __restrict__ k,
@@ -621,9 +630,12 @@ __global__ void __launch_bounds__(128) few_rows_partial_kernel(
       s_z[threadIdx.x] = i < i_hi ? zhat[i] : 0.0;
     }
     __syncthreads();
+    // padded sources (ii >= cnt) are skipped, not weighted by zero: d = 0 meets a root
+    // mu_j = 0 as 0 / 0 (see apply_direct_kernel)
     const int cnt = min(32, i_hi - i0);
-    for (int ii = 0; ii < cnt; ++ii) {
-      const double c = s_z[ii] / ((s_d[ii] - dk) - tj);
+#pragma unroll 4
+    for (int ii = 0; ii < 32; ++ii) {
+      const double c = ii < cnt ? s_z[ii] * few_rcp((s_d[ii] - dk) - tj) : 0.0;
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[r] = fma(c, s_u[r][ii], acc[r]);
     }
