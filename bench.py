@@ -248,6 +248,9 @@ def main():
     seq = None
     if batch:  # the per-update API on the same stream, for reference (not the headline)
         restore()
+        for t in range(args.warmup):  # its own buffers warm too
+            step(t)
+        restore()
         torch.cuda.synchronize()
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)

@@ -216,7 +216,8 @@ struct svd1_plan_s {
   DevBuf probes;                 // 4 x u_rows sign probes
   bool probes_ready = false;
   cudaStream_t st2 = nullptr;    // V-side applies run here, concurrently with the U side
-  cudaStream_t sp[2] = {};       // batch mode: spectral + carried-row streams (U, V side)
+  cudaStream_t sp[4] = {};       // batch mode: spectral + carried-row streams (U, V side),
+                                 // then upload streams for the FMM plans (U, V side)
   cudaEvent_t sync_ev[4] = {};
   StepRecord steps[4];
   // batch mode (svd1_update_batch): step records per update parity (the
@@ -244,7 +245,7 @@ struct svd1_plan_s {
     size_t cap = 0, used = 0;
     cudaEvent_t ev = nullptr;
     bool pending = false;
-  } arena[4];  // sides 0, 1: apply streams; 2, 3: batch spectral streams
+  } arena[6];  // sides 0, 1: apply streams; 2, 3: batch spectral streams; 4, 5: uploads
   CauchyPrep standalone;    // plan of the standalone svd1_cauchy_apply
   std::vector<int32_t> rot_goff, rot_cols;  // pairing rotations of repeated sigma clusters
   std::vector<double> rot_mats;
@@ -275,7 +276,9 @@ svd1_status ensure_st2(svd1_plan_t P) {
 }
 svd1_status ensure_side(svd1_plan_t P, int side) {
   if (side == 1) return ensure_st2(P);
-  if (side >= 2 && !P->sp[side - 2]) {
+  if (side >= 4 && !P->sp[side - 2]) {
+    SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->sp[side - 2], cudaStreamNonBlocking));
+  } else if (side >= 2 && !P->sp[side - 2]) {
     // batch mode's spectral streams run at the highest priority: their short kernels
     // gate the next update, the applies they share the GPU with fill in behind them
     int lo = 0, hi = 0;
@@ -300,7 +303,7 @@ svd1_status arena_reset(svd1_plan_t P, int side) {
   return SVD1_OK;
 }
 svd1_status arena_reset(svd1_plan_t P) {
-  for (int side = 0; side < 4; ++side) TRY(arena_reset(P, side));
+  for (int side = 0; side < 6; ++side) TRY(arena_reset(P, side));
   return SVD1_OK;
 }
 
@@ -2020,10 +2023,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if (m > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
   const int64_t launches0 = P->launches;
   const double t0 = now_ms();
-  if (B) {  // the apply streams' arenas rewind only when full (their copies queue behind
-            // the previous update's applies)
-    TRY(arena_reset(P, 2));
-    TRY(arena_reset(P, 3));
+  if (B) {  // the apply streams' arenas are unused in this mode
+    for (int sd = 2; sd < 6; ++sd) TRY(arena_reset(P, sd));
   } else {
     TRY(arena_reset(P));
   }
@@ -2219,13 +2220,17 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     }
     return SVD1_OK;
   };
-  // upload step e's apply data (batch mode: its FMM plan, on the apply stream itself,
-  // which waits for the step's maps only, not for the spectral work queued after them)
+  // upload step e's apply data (batch mode: its FMM plan on the side's upload stream,
+  // which never queues behind compute; the apply stream waits for that copy and for the
+  // step's maps, not for the spectral work queued after them)
   auto upload_step = [&](int e) -> svd1_status {
     const int side = e < 2 ? 0 : 1;
     if (!B) return apply_upload(P, S[e], one_stream ? 0 : side);
-    SVD1_CUDA_TRY(cudaStreamWaitEvent(side_stream(P, side), P->maps_ev[e], 0));
-    return upload_fmm(P, S[e], side);
+    TRY(ensure_side(P, side + 4));
+    const cudaStream_t as = side_stream(P, side);
+    SVD1_CUDA_TRY(cudaStreamWaitEvent(as, P->maps_ev[e], 0));
+    TRY(upload_fmm(P, S[e], side + 4));
+    return stream_wait(P, e, side_stream(P, side + 4), as);
   };
   auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
     const int side = e == 0 ? 0 : 1;
@@ -2647,7 +2652,8 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
     }
   }
   // drain every stream; the factors now hold updates 0..t; sigma of the last success
-  for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1]}) SVD1_CUDA_TRY(cudaStreamSynchronize(q));
+  for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1], P->sp[2], P->sp[3]})
+    if (q || q == P->st) SVD1_CUDA_TRY(cudaStreamSynchronize(q));
   if (P->tl_on) {  // host stamps and device times (ms from the batch start)
     cudaEvent_t base = P->tl_dev.empty() ? nullptr : P->tl_dev.front().second;
     for (size_t q = 0; q < P->tl_host.size(); ++q) fprintf(stderr, "[tl] host %8.3f %s\n", P->tl_host[q].second, P->tl_host[q].first.c_str());
