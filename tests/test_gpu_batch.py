@@ -59,6 +59,7 @@ def _invariants(inp, K, U, s, V):
     (3, 256, 256, 6, P.FORCE_FMM, True),    # C3 recipe (graded, near-deflation)
     (4, 64, 256, 5, 0, True),               # C4 recipe: rectangular, null-space Householder
     (5, 200, 200, 4, P.FORCE_FMM, False),   # C5 recipe: duplicated sigma (pairing rotations)
+    (3, 512, 512, 4, P.FORCE_FMM | P.SECULAR_FMM, True),  # FMM secular solve inside the stream
 ])
 def test_batch_matches_sequential(cfg, m, n, K, flags, exact):
     inp = config_inputs(cfg, m=m, n=n, updates=K)
