@@ -167,6 +167,8 @@ struct StepRecord {
   std::vector<int> act, dfl;
   std::vector<double> ds;
   std::vector<std::vector<double>> cs_sorted;
+  std::vector<double> Dn;              // next eigenvalues / carries (recycled storage)
+  std::vector<std::vector<double>> cn;
   double* rb = nullptr;  // pinned read-back
   size_t rb_cap = 0;
   cudaEvent_t done_ev = nullptr;  // recorded after the read-back copy
@@ -1493,10 +1495,14 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   }
   const int nc = int(carries.size());
   S.nc = nc;
-  auto& cs_sorted = S.cs_sorted;
-  cs_sorted.assign(nc, std::vector<double>(N));
-  for (int q = 0; q < nc; ++q)
-    for (int s = 0; s < N; ++s) cs_sorted[q][s] = carries[q][perm[s]];
+  auto& cs_sorted = S.cs_sorted;  // capacity kept across steps
+  cs_sorted.resize(nc);
+  for (int q = 0; q < nc; ++q) {
+    cs_sorted[q].resize(N);
+    double* dstq = cs_sorted[q].data();
+    const double* srcq = carries[q].data();
+    for (int s = 0; s < N; ++s) dstq[s] = srcq[perm[s]];
+  }
   // deflation (DESIGN.md §3.2 D1): (i) zero weights, (iii) exact repeats
   double zn2 = 0.0;
   for (double v : zs) zn2 += v * v;
@@ -1562,9 +1568,6 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   }
   if (na == 0) return SVD1_OK;
   const double th0 = now_ms();
-  std::vector<double> carry_act(size_t(nc) * na);
-  for (int q = 0; q < nc; ++q)
-    for (int i = 0; i < na; ++i) carry_act[size_t(q) * na + i] = cs_sorted[q][S.act[i]];
   // one upload [d_a | z_a | carries] and one read-back
   // [k (na words) | tau | cs | carry_out (nc*na) | iters (int32) | status]
   const size_t in_words = size_t(na) * (4 + nc);
@@ -1573,21 +1576,28 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   double* dout;
   TRY(S.d_in.get<double>(in_words, &din));
   TRY(S.d_out.get<double>(words, &dout));
+  double* stage;  // built in place in the pinned arena (no intermediate copies)
+  size_t stage_off;
   {
-    std::vector<double>& stage = S.stage;
-    stage.resize(in_words);
-    std::memcpy(stage.data(), S.da.data(), na * sizeof(double));
-    std::memcpy(stage.data() + na, za.data(), na * sizeof(double));
+    TRY(ensure_side(P, side));
+    TRY(arena_reserve(P, side, in_words * sizeof(double), &stage_off));
+    stage = reinterpret_cast<double*>(P->arena[side].buf + stage_off);
+    std::memcpy(stage, S.da.data(), na * sizeof(double));
+    std::memcpy(stage + na, za.data(), na * sizeof(double));
     // the secular solver's view: rho > 0 orientation (reflected for rho < 0), z squared
-    double* dr = stage.data() + 2 * na;
-    double* z2r = stage.data() + 3 * na;
+    double* dr = stage + 2 * na;
+    double* z2r = stage + 3 * na;
     for (int i = 0; i < na; ++i) {
       const int src = rho < 0.0 ? na - 1 - i : i;
       dr[i] = rho < 0.0 ? -S.da[src] : S.da[src];
       z2r[i] = za[src] * za[src];
     }
-    std::memcpy(stage.data() + 4 * na, carry_act.data(), size_t(nc) * na * sizeof(double));
-    TRY(arena_put(P, stage.data(), in_words * sizeof(double), din, side));
+    for (int q = 0; q < nc; ++q) {
+      double* cq = stage + size_t(4 + q) * na;
+      const double* src = cs_sorted[q].data();
+      for (int i = 0; i < na; ++i) cq[i] = src[S.act[i]];
+    }
+    TRY(arena_commit(P, side, stage_off, in_words * sizeof(double), din));
   }
   double* dda = din;
   double* dza = din + na;
@@ -1610,7 +1620,8 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na);
   if (S.sec_fmm_used) {  // STEP 2 with the far field by FMM
     SecFmmDev F;
-    TRY(secfmm_prepare(P, S.sec, S.sec_blob, S.sec_scr, S.stage.data() + 2 * na, na, side, &F));
+    // (reads the oriented sources from the staging region before its own upload)
+    TRY(secfmm_prepare(P, S.sec, S.sec_blob, S.sec_scr, stage + 2 * na, na, side, &F));
     TRY(secular_fmm(ddr, dz2r, rho, na, F, dk, dtau, dit, dst, st, &P->launches));
   } else {
     TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, st, &P->launches));   // STEP 2
@@ -1697,7 +1708,7 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
   };
   // both lists are ascending (deflated d in sorted order; roots interlace) -> O(n) merge
   // (stable ascending, deflated first on ties); fall back to a sort if mu is not sorted
-  std::vector<Item> items;
+  std::vector<Item> items;  // (local: spectral_finish runs on the main thread only)
   items.reserve(N);
   bool mu_sorted = true;
   for (int j = 1; j < na; ++j)
@@ -1724,8 +1735,11 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
     });
   }
   S.tgt_pos.assign(na, -1);
-  std::vector<double> Dn(N);
-  std::vector<std::vector<double>> cn(nc, std::vector<double>(N));
+  std::vector<double>& Dn = S.Dn;  // swapped with D / carries below: storage recycles
+  std::vector<std::vector<double>>& cn = S.cn;
+  Dn.resize(N);
+  cn.resize(nc);
+  for (auto& v : cn) v.resize(N);
   for (int q = 0; q < N; ++q) {
     const Item& it = items[q];
     Dn[q] = it.v;
