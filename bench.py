@@ -193,10 +193,10 @@ def main():
         a_t, b_t = ab[t % len(ab)] if a is None else (a, b)
         return upd.update(U, sig, V, a_t, b_t)
 
-    # one GPU: the stream of updates goes through svd1_update_batch (pipelined: update
-    # t+1's spectral phase overlaps update t's applies); row-sharded
-    # runs use the per-update path (projections all-reduced every update)
-    batch = world == 1 and not args.sequential
+    # the stream of updates goes through svd1_update_batch (pipelined: update t+1's
+    # spectral phase overlaps update t's applies); row-sharded: the K
+    # projection vectors of a chunk are all-reduced once, then svd1_update_batch_projected
+    batch = not args.sequential
     A_all = torch.stack([a for a, _ in ab])
     B_all = torch.stack([b for _, b in ab])
 
@@ -213,7 +213,7 @@ def main():
                 Ab, Bb = A_all[idx], B_all[idx]
             else:
                 Ab, Bb = A_src[[q - t0 for q in range(t, t + kc)]], B_src[[q - t0 for q in range(t, t + kc)]]
-            out += upd.plan.update_batch(U, sig, V, Ab, Bb)
+            out += upd.update_batch(U, sig, V, Ab, Bb)
             t += kc
         return out
 

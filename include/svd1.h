@@ -135,6 +135,17 @@ svd1_status svd1_update_batch(svd1_plan_t plan, double* U, int64_t ldu, double* 
                               const double* B, int64_t ldb, int64_t K, double eps,
                               svd1_report* reps);
 
+/* Row-sharded stream: svd1_update_batch after the projections.  proj (device): K
+ * consecutive all-reduced svd1_project outputs (5*m + n + 6 doubles each, update t at
+ * proj + t*(5*m + n + 6)), every one computed against the factors at the START of the
+ * stream; sigma full, replicated; U_loc, V_loc this rank's row blocks.  Every rank runs
+ * the same spectral phases and carried-row transforms (deterministic) on its own GPU;
+ * no collective inside.  K <= 28. */
+svd1_status svd1_update_batch_projected(svd1_plan_t plan, double* U_loc, int64_t ldu,
+                                        double* sigma, double* V_loc, int64_t ldv,
+                                        const double* proj, int64_t K, double eps,
+                                        svd1_report* reps);
+
 /* Row-sharded update, phase 1 (STEP 1 projections over the LOCAL rows):
  * proj (device, 5*m + n + 6 doubles) receives the partial sums
  *   proj[0:m]        = U_loc^T a_loc          (x_a = U^T a)

@@ -58,6 +58,8 @@ svd1_plan_destroy = _sig("svd1_plan_destroy", [vp])
 svd1_update = _sig("svd1_update", [vp, vp, i64, vp, vp, i64, vp, vp, dbl, C.POINTER(Report)])
 svd1_update_batch = _sig("svd1_update_batch", [vp, vp, i64, vp, vp, i64, vp, i64, vp, i64, i64, dbl,
                                                C.POINTER(Report)])
+svd1_update_batch_projected = _sig("svd1_update_batch_projected", [vp, vp, i64, vp, vp, i64, vp, i64, dbl,
+                                                                   C.POINTER(Report)])
 svd1_project = _sig("svd1_project", [vp, vp, i64, vp, i64, vp, vp, vp])
 svd1_update_projected = _sig("svd1_update_projected",
                              [vp, vp, i64, vp, vp, i64, vp, vp, vp, dbl, C.POINTER(Report)])
@@ -72,7 +74,7 @@ lib.svd1_status_string.restype = C.c_char_p
 lib.svd1_version.argtypes = []
 lib.svd1_version.restype = C.c_char_p
 
-EXPORTS = ["svd1_plan_create", "svd1_plan_destroy", "svd1_update", "svd1_update_batch", "svd1_project",
+EXPORTS = ["svd1_plan_create", "svd1_plan_destroy", "svd1_update", "svd1_update_batch", "svd1_update_batch_projected", "svd1_project",
            "svd1_update_projected", "svd1_cauchy_apply", "svd1_secular_solve", "svd1_loewner",
            "svd1_colnorms", "svd1_fmm_tree_stats", "svd1_status_string", "svd1_version"]
 

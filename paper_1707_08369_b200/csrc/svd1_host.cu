@@ -2579,28 +2579,42 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   return update_impl(P, U, ldu, sigma, V, ldv, proj, eps, rep, nullptr);
 }
 
+constexpr int kMaxBatch = 28;  // buffers are sized for this many updates per call
+
 svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
                               const double* A, int64_t lda, const double* Bv, int64_t ldb, int64_t K,
                               double eps, svd1_report* reps) {
-  if (!P || !U || !V || !sigma || (K > 0 && (!A || !Bv)) || K < 0 || K > 28) return SVD1_E_INVALID;
+  if (!P || !U || !V || !sigma || (K > 0 && (!A || !Bv)) || K < 0 || K > kMaxBatch) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
   const int64_t m = c.m, n = c.n;
   if (c.u_rows != m || c.v_rows != n || ldu < m || ldv < n || lda < m || ldb < n) return SVD1_E_INVALID;
+  if (K == 0) return SVD1_OK;
+  // every update's STEP-1 projections against the initial factors (P:336-337)
+  const size_t nproj = size_t(5 * m + n + 6);
+  double* pj;
+  TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj));
+  for (int t = 0; t < int(K); ++t)
+    TRY(svd1_project(P, U, ldu, V, ldv, A + int64_t(t) * lda, Bv + int64_t(t) * ldb, pj + size_t(t) * nproj));
+  return svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, K, eps, reps);
+}
+
+svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,
+                                        int64_t ldv, const double* proj, int64_t K, double eps,
+                                        svd1_report* reps) {
+  if (!P || !sigma || (K > 0 && !proj) || K < 0 || K > kMaxBatch) return SVD1_E_INVALID;
+  const svd1_config& c = P->cfg;
+  const int64_t m = c.m, n = c.n;
+  if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < n))) return SVD1_E_INVALID;
   if (K == 0) return SVD1_OK;
   const int k = int(K);
   TRY(arena_reset(P));
   TRY(ensure_st2(P));
   TRY(ensure_side(P, 2));
   TRY(ensure_side(P, 3));
-  // every update's STEP-1 projections against the initial factors (P:336-337)
-  // buffers sized for the largest batch (28) whatever K is: no reallocation (and its
+  // buffers sized for the largest batch whatever K is: no reallocation (and its
   // implicit device synchronisation) between batches of different lengths
-  constexpr int kMaxBatch = 28;
   const size_t nproj = size_t(5 * m + n + 6);
-  double* pj;
-  TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj));
-  for (int t = 0; t < k; ++t)
-    TRY(svd1_project(P, U, ldu, V, ldv, A + int64_t(t) * lda, Bv + int64_t(t) * ldb, pj + size_t(t) * nproj));
+  const double* pj = proj;
   // carried rows (row-major, m resp. n wide): U side [x_g (4) | x_a(K-1) .. x_a(1)],
   // V side [y_b(K-1) .. y_b(1)]; update t transforms the rows of updates t+1.. only
   const int ru_max = 4 + (kMaxBatch - 1), rv_max = kMaxBatch - 1;

@@ -47,6 +47,20 @@ class ShardedUpdater:
                          v_rows=self.v_hi - self.v_lo, u_row0=self.u_lo, v_row0=self.v_lo, **kw)
         self.proj = torch.empty(proj_size(m, n), dtype=torch.float64, device="cuda")
 
+    def update_batch(self, U_loc, sigma, V_loc, A, B):
+        """A stream of K updates (A: K x m, B: K x n): every update's projections against
+        the current factors, ONE all-reduce of the K projection vectors, then the
+        pipelined stream on this rank's rows (svd1_update_batch_projected)."""
+        import torch
+        if self.world == 1:
+            return self.plan.update_batch(U_loc, sigma, V_loc, A, B)
+        K = A.shape[0]
+        projs = torch.empty((K, proj_size(self.m, self.n)), dtype=torch.float64, device=A.device)
+        for t in range(K):
+            self.plan.project(U_loc, V_loc, A[t], B[t], projs[t])
+        allreduce_projection(projs, self.group)
+        return self.plan.update_batch_projected(U_loc, sigma, V_loc, projs)
+
     def update(self, U_loc, sigma, V_loc, a, b):
         if self.world == 1:
             return self.plan.update(U_loc, sigma, V_loc, a, b)

@@ -114,3 +114,38 @@ def test_batch_c3_full_size():
         A = A + torch.outer(T(a), T(b))
     res = float(torch.linalg.norm(A @ Vb - Ub * sb[None, :], dim=0).max() / sb[0])
     assert res <= 1e-10 and orth <= 1e-10, (res, orth)
+
+
+@pytest.mark.parametrize("cfg,m,n,K,flags", [(3, 256, 256, 5, P.FORCE_FMM), (4, 64, 256, 4, 0)])
+def test_sharded_batch_two_ranks(cfg, m, n, K, flags):
+    """The row-sharded stream (svd1_update_batch_projected) for world size 2, the two
+    ranks run one after the other on this GPU (no collective inside the stream: the
+    projections are summed here as the all-reduce would): the concatenated row blocks
+    equal the single-process stream's factors."""
+    from paper_1707_08369_b200.parallel import row_block
+    inp = config_inputs(cfg, m=m, n=n, updates=K)
+    Ub, sb, Vb, _ = _stream(inp, K, flags, batch=True)
+    ab = inp["ab"][:K]
+    A = T(np.stack([a for a, _ in ab]))
+    B = T(np.stack([b for _, b in ab]))
+    world, parts = 2, []
+    for r in range(world):
+        u0, u1 = row_block(m, r, world)
+        v0, v1 = row_block(n, r, world)
+        plan = P.Plan(m, n, flags=flags, u_rows=u1 - u0, v_rows=v1 - v0, u_row0=u0, v_row0=v0)
+        Ul, Vl = T(inp["U"][u0:u1]), T(inp["V"][v0:v1])
+        projs = torch.empty((K, plan.proj_size()), dtype=torch.float64, device=DEV)
+        for t in range(K):
+            plan.project(Ul, Vl, A[t], B[t], projs[t])
+        parts.append(dict(plan=plan, U=Ul, V=Vl, s=T(inp["sigma"]), projs=projs))
+    total = sum(p_["projs"] for p_ in parts)  # the all-reduce
+    for p_ in parts:
+        p_["plan"].update_batch_projected(p_["U"], p_["s"], p_["V"], total)
+        torch.cuda.synchronize()
+    Us = torch.cat([p_["U"] for p_ in parts])
+    Vs = torch.cat([p_["V"] for p_ in parts])
+    assert torch.equal(parts[0]["s"], parts[1]["s"])
+    assert float((parts[0]["s"] - sb).abs().max()) <= 1e-12 * float(sb[0])
+    assert float((Us - Ub).abs().max()) <= 1e-8 and float((Vs[:, :m] - Vb[:, :m]).abs().max()) <= 1e-8
+    for p_ in parts:
+        p_["plan"].close()

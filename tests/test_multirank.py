@@ -82,3 +82,41 @@ def test_row_block_partition():
             assert all(blocks[i][1] == blocks[i + 1][0] for i in range(world - 1))
             sizes = [h - l for l, h in blocks]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _batch_worker(rank, world, port, m, n, K, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)
+    U = torch.from_numpy(rng.standard_normal((m, m)))
+    V = torch.from_numpy(rng.standard_normal((n, n)))
+    A, B = torch.from_numpy(rng.standard_normal((K, m))), torch.from_numpy(rng.standard_normal((K, n)))
+    g = torch.from_numpy(rng.standard_normal((4, m)))
+    u_lo, u_hi = row_block(m, rank, world)
+    v_lo, v_hi = row_block(n, rank, world)
+    # the batched stream's one exchange: K projection vectors in one (K x proj) all-reduce
+    projs = torch.stack([_partial(U, V, A[t], B[t], g, u_lo, u_hi, v_lo, v_hi) for t in range(K)])
+    allreduce_projection(projs)
+    full = torch.stack([_partial(U, V, A[t], B[t], g, 0, m, 0, n) for t in range(K)])
+    q.put((rank, float((projs - full).abs().max()), float(full.abs().max()), projs.numpy().tobytes()))
+    dist.destroy_process_group()
+
+
+def test_sharded_batch_projection_allreduce():
+    """ShardedUpdater.update_batch's exchange (world size 2, gloo): one all-reduce of
+    the K stacked projection vectors gives every rank the single-process projections,
+    bitwise identical across ranks."""
+    world, m, n, K = 2, 11, 17, 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, m, n, K, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for _, err, scale, _ in res:
+        assert err <= 1e-13 * scale
+    assert res[0][3] == res[1][3]
