@@ -150,6 +150,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--thin", action="store_true",
+                    help="thin right factor (SVD1_THIN_V) for m < n configs (C4)")
     ap.add_argument("--sequential", action="store_true",
                     help="time the per-update API (svd1_update) instead of svd1_update_batch")
     ap.add_argument("--config", type=int, default=CFG_ID, choices=[1, 2, 3, 4, 5],
@@ -182,10 +184,15 @@ def main():
     # row shards (paper_1707_08369_b200.parallel: NCCL all-reduce of the projections)
     from paper_1707_08369_b200.parallel import ShardedUpdater
     stream = torch.cuda.current_stream()
-    upd = ShardedUpdater(m, n, rank, world, eps=cfg["eps"], stream=stream)
+    thin = args.thin and m < n
+    upd = ShardedUpdater(m, n, rank, world, eps=cfg["eps"], stream=stream, flags=P.THIN_V if thin else 0)
     u0, u1, v0, v1 = upd.u_lo, upd.u_hi, upd.v_lo, upd.v_hi
     U = U0[u0:u1].clone()
-    V = V0[v0:v1].clone()
+    if thin:  # V[:, :m] plus one workspace column (SVD1_THIN_V)
+        V = torch.zeros((v1 - v0, m + 1), dtype=torch.float64, device=dev)
+        V[:, :m] = V0[v0:v1, :m]
+    else:
+        V = V0[v0:v1].clone()
     sig = s0.clone()
     Upr, Vpr, spr = U.clone(), V.clone(), sig.clone()
 
@@ -196,7 +203,7 @@ def main():
     # the stream of updates goes through svd1_update_batch (pipelined: update t+1's
     # spectral phase overlaps update t's applies); row-sharded: the K
     # projection vectors of a chunk are all-reduced once, then svd1_update_batch_projected
-    batch = not args.sequential
+    batch = not args.sequential and not thin  # (the stream API keeps the full V)
     A_all = torch.stack([a for a, _ in ab])
     B_all = torch.stack([b for _, b in ab])
 
@@ -369,8 +376,9 @@ def main():
             A = A + torch.outer(a_t, b_t)
         res = float(torch.linalg.norm(A @ V[:, :m] - U * sig[None, :], dim=0).max() / sig[0])
         I = torch.eye(m, dtype=torch.float64, device=dev)
-        In = torch.eye(n, dtype=torch.float64, device=dev)
-        orth = max(float((U.T @ U - I).abs().max()), float((V.T @ V - In).abs().max()))
+        Vc = V[:, :m] if thin else V
+        In = torch.eye(Vc.shape[1], dtype=torch.float64, device=dev)
+        orth = max(float((U.T @ U - I).abs().max()), float((Vc.T @ Vc - In).abs().max()))
         check = {"residual": res, "orthogonality": orth, "updates": args.steps,
                  "n_active_last": reps[-1]["n_active"], "max_secular_iter": max(max(r["max_iter"]) for r in reps),
                  "fmm_levels": reps[-1]["fmm_levels"], "fmm_max_near": reps[-1]["fmm_max_near"],
@@ -396,7 +404,8 @@ def main():
                                   if 8 * (m * m + n * n) > 126e6 else
                                   f"inputs fit in L2 ({8 * (m * m + n * n) / 2**20:.1f} MiB); no flush"),
                            "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
-                           "api": "svd1_update_batch (pipelined stream)" if batch else "svd1_update"},
+                           "api": "svd1_update_batch (pipelined stream)" if batch else "svd1_update",
+                           "thin_v": thin},
                 "sequential_api": seq,
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
                 "cpu_baseline": cpu, "check": check,

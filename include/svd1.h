@@ -57,6 +57,11 @@ typedef enum {
                                   every size above 64 (default: from 6144 roots, or the
                                   environment variable SVD1_SEC_FMM_MIN) */
 #define SVD1_SECULAR_DIRECT 0x8u /* secular solve with the direct O(n) sums only */
+#define SVD1_THIN_V 0x10u        /* thin right factor (m < n):
+                                    V is n x (m+1), ldv >= m+1; columns 0..m-1 hold V[:, :m],
+                                    column m is workspace (the direction of b outside span(V),
+                                    overwritten by every update).  The null space of A^T is
+                                    never stored. */
 
 typedef struct {
   int64_t m, n;      /* global sizes, 1 <= m <= n */

@@ -82,6 +82,7 @@ FORCE_DIRECT = 0x1
 FORCE_FMM = 0x2
 SECULAR_FMM = 0x4     # secular solve with the FMM far field at every size > 64
 SECULAR_DIRECT = 0x8  # secular solve with direct sums only
+THIN_V = 0x10         # thin right factor: V is n x (m+1), column m workspace (svd1.h)
 
 
 def status_string(code: int) -> str:

@@ -814,7 +814,11 @@ svd1_status fill_probes(uint64_t seed, int64_t row0, int64_t rows, double* g, cu
 svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
                     const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0,
                     const double* a, const double* b, double* part, int64_t partial_cap,
-                    double* proj, const double* probes, cudaStream_t st, int64_t* launches) {
+                    double* proj, const double* probes, cudaStream_t st, int64_t* launches,
+                    int64_t vcols) {
+  // vcols < n (thin V): only the first vcols entries of V^T b are formed, the rest of the
+  // n-wide block is zero (the layout stays 5m + n + 6)
+  if (vcols < 0) vcols = n;
   const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
   const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
   if (cu * 5 * m + cv * n + 6 * kDotBlocks > partial_cap) return SVD1_E_NOMEM;
@@ -830,9 +834,10 @@ svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int
     SVD1_CUDA_TRY(cudaMemsetAsync(proj, 0, sizeof(double) * 5 * m, st));
   }
   if (v_rows > 0) {
-    proj_partial_kernel<1><<<dim3(unsigned((n + 255) / 256), unsigned(cv)), 256, 0, st>>>(
-        V, ldv, v_rows, n, b, v_row0, rpc_v, nullptr, part_v);
-    proj_reduce_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(part_v, int(cv), 1, n, proj + 5 * m);
+    proj_partial_kernel<1><<<dim3(unsigned((vcols + 255) / 256), unsigned(cv)), 256, 0, st>>>(
+        V, ldv, v_rows, vcols, b, v_row0, rpc_v, nullptr, part_v);
+    proj_reduce_kernel<<<unsigned((vcols + 255) / 256), 256, 0, st>>>(part_v, int(cv), 1, vcols, proj + 5 * m);
+    if (vcols < n) SVD1_CUDA_TRY(cudaMemsetAsync(proj + 5 * m + vcols, 0, sizeof(double) * (n - vcols), st));
     *launches += 2;
   } else {
     SVD1_CUDA_TRY(cudaMemsetAsync(proj + 5 * m, 0, sizeof(double) * n, st));
@@ -841,6 +846,30 @@ svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int
   proj_dots_kernel<<<kDotBlocks, 256, 0, st>>>(a, u_rows, u_row0, b, v_rows, v_row0, probes, part_d);
   proj_dots_final<<<1, 32, 0, st>>>(part_d, kDotBlocks, proj + 5 * m + n);
   *launches += 2;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+// warp per row: q = (b_r - V_r . y) / beta into column m
+__global__ void null_direction_kernel(int64_t rows, double* __restrict__ V, int64_t ldv, int64_t m,
+                                      const double* __restrict__ b, const double* __restrict__ y,
+                                      double inv_beta) {
+  const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const double* row = V + r * ldv;
+  double s = 0.0;
+  for (int64_t c = lane; c < m; c += 32) s = fma(row[c], y[c], s);
+  s = warp_sum(s);
+  if (lane == 0) V[r * ldv + m] = (b[r] - s) * inv_beta;
+}
+
+svd1_status null_direction(int64_t rows, double* V, int64_t ldv, int64_t m, const double* b, int64_t row0,
+                           const double* y, double inv_beta, cudaStream_t st, int64_t* launches) {
+  if (rows <= 0) return SVD1_OK;
+  null_direction_kernel<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(rows, V, ldv, m, b + row0, y,
+                                                                           inv_beta);
+  *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

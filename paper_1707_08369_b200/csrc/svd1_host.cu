@@ -1979,7 +1979,9 @@ svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const doub
                          const double* a, const double* b, double* proj) {
   if (!P || !proj || !a || !b) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
-  if ((c.u_rows && (!U || ldu < c.m)) || (c.v_rows && (!V || ldv < c.n))) return SVD1_E_INVALID;
+  const bool thin = (c.flags & SVD1_THIN_V) != 0;
+  if ((c.u_rows && (!U || ldu < c.m)) || (c.v_rows && (!V || ldv < (thin ? c.m + 1 : c.n))))
+    return SVD1_E_INVALID;
   double* part;
   const int64_t need = project_partial_elems(c.u_rows, c.m, c.v_rows, c.n);
   TRY(P->partial.get<double>(size_t(need), &part));
@@ -1990,7 +1992,7 @@ svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const doub
     P->probes_ready = true;
   }
   return project(U, ldu, c.u_rows, c.m, c.u_row0, V, ldv, c.v_rows, c.n, c.v_row0, a, b, part, need,
-                 proj, static_cast<double*>(P->probes.p), P->st, &P->launches);
+                 proj, static_cast<double*>(P->probes.p), P->st, &P->launches, thin ? c.m : c.n);
 }
 
 }  // extern "C"
@@ -2029,11 +2031,17 @@ svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, in
 }
 
 svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
-                        const double* proj, double eps, svd1_report* rep, BatchCtx* B) {
+                        const double* proj, double eps, svd1_report* rep, BatchCtx* B,
+                        const double* b_dev = nullptr) {
   if (!P || (!B && (!sigma || !proj)) || (B && (!B->h_proj || !B->sig))) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
   const int64_t m = c.m, n = c.n;
-  if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < n))) return SVD1_E_INVALID;
+  // thin right factor: the V side works in the basis [V[:, :m], q] of
+  // size nv = m + 1, q = the unit direction of b outside span(V) (column m of V)
+  const bool thin = (c.flags & SVD1_THIN_V) != 0;
+  const int64_t nv = thin ? m + 1 : n;
+  if (thin && (B || (c.v_rows && !b_dev))) return SVD1_E_INVALID;
+  if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < nv))) return SVD1_E_INVALID;
   if (m > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
   const int64_t launches0 = P->launches;
   const double t0 = now_ms();
@@ -2076,13 +2084,13 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   const Split su = schur_split(beta), sv = schur_split(alpha);
   // small vectors in the U and V column bases (B7 identities):
   // U^T b~ = Sigma (V^T b)[:m],  V^T a~ = Sigma^T (U^T a)
-  std::vector<double> z1(m), Du(m), z3(n), Dv(n, 0.0);
+  std::vector<double> z1(m), Du(m), z3(nv), Dv(nv, 0.0);
   std::vector<std::vector<double>> cu, cv;
   cu.emplace_back(m);
-  cv.emplace_back(n);
+  cv.emplace_back(nv);
   for (int q = 0; q < kNumProbes; ++q) {
     cu.emplace_back(xg + q * m, xg + (q + 1) * m);
-    cv.emplace_back(n, 0.0);
+    cv.emplace_back(nv, 0.0);
   }
   for (int64_t i = 0; i < m; ++i) {
     const double sx = sig[i] * yb[i];
@@ -2091,22 +2099,31 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     Du[i] = sig[i] * sig[i];
     Dv[i] = Du[i];
   }
-  for (int64_t i = 0; i < n; ++i) {
+  // thin: the coordinate of b along q is beta_perp = ||b - V V^T b|| (a~ = A^T a has none)
+  double beta_perp = 0.0;
+  if (thin) {
+    double yy = 0.0;
+    for (int64_t i = 0; i < m; ++i) yy += yb[i] * yb[i];
+    const double r2 = beta - yy;
+    beta_perp = r2 > 64.0 * kEps * beta ? std::sqrt(r2) : 0.0;  // b in span(V): no null part
+  }
+  for (int64_t i = 0; i < nv; ++i) {
     const double sxa = i < m ? sig[i] * xa[i] : 0.0;
-    z3[i] = sv.q00 * yb[i] + sv.q10 * sxa;     // V^T a2, [b a~] Q_v = [a2 b2]
-    cv[0][i] = sv.q01 * yb[i] + sv.q11 * sxa;  // V^T b2
-    for (int q = 0; q < kNumProbes; ++q)       // V^T A_hat^T g = Sigma^T U^T g + (V^T b)(a.g)
-      cv[1 + q][i] = (i < m ? sig[i] * xg[q * m + i] : 0.0) + yb[i] * ag[q];
+    const double ybi = thin && i == m ? beta_perp : yb[i];
+    z3[i] = sv.q00 * ybi + sv.q10 * sxa;     // V^T a2, [b a~] Q_v = [a2 b2]
+    cv[0][i] = sv.q01 * ybi + sv.q11 * sxa;  // V^T b2
+    for (int q = 0; q < kNumProbes; ++q)     // V^T A_hat^T g = Sigma^T U^T g + (V^T b)(a.g)
+      cv[1 + q][i] = (i < m ? sig[i] * xg[q * m + i] : 0.0) + ybi * ag[q];
   }
   // ---- workspaces for the applies (sized up front: a mid-stream realloc would sync)
   TRY(ensure_st2(P));
   double *Wu = nullptr, *Wv = nullptr;
   if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
-  if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * n, &Wv));
+  if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * nv, &Wv));
   {
     const int64_t rows_max = std::max(c.u_rows, c.v_rows);
     const size_t guess = size_t(rows_max) * size_t(P->p) *
-                         size_t(4 * std::max<int64_t>(n, 1) / std::max(P->leaf, 1) + 8);
+                         size_t(4 * std::max<int64_t>(nv, 1) / std::max(P->leaf, 1) + 8);
     for (int side = 0; side < 2; ++side) TRY(ensure_expansions(P, side, guess));
   }
   const bool one_stream = !B && std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
@@ -2246,6 +2263,12 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     TRY(upload_fmm(P, S[e], side + 4));
     return stream_wait(P, e, side_stream(P, side + 4), as);
   };
+  // thin V: column m of V <- q before the first V apply reads it (V side's apply stream)
+  auto null_dir = [&]() -> svd1_status {
+    if (!thin || !c.v_rows) return SVD1_OK;
+    return null_direction(c.v_rows, V, ldv, m, b_dev, c.v_row0, proj + 5 * m,
+                          beta_perp > 0.0 ? 1.0 / beta_perp : 0.0, stv, &P->launches);
+  };
   auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
     const int side = e == 0 ? 0 : 1;
     TRY(rare_grow(e, side));
@@ -2261,7 +2284,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
         TRY(ev_record(P, 18, stv));
         if (B) TRY(bwin_record(P, B->parity, 1, stv));
         tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V1 apply", stv);
-        TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
+        TRY(null_dir());
+        TRY(apply_launch(P, S[2], V, ldv, Wv, nv, 4, stv, 1));
         launched_v1 = true;
       }
     }
@@ -2343,7 +2367,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // ---- sign alignment: final column i = position N-1-i
   std::vector<double> sgn(m, 1.0);
   for (int64_t i = 0; i < m; ++i) {
-    const int64_t qu = m - 1 - i, qv = n - 1 - i;
+    const int64_t qu = m - 1 - i, qv = nv - 1 - i;
     int kb = 0;
     double best = -1.0;
     for (int q = 0; q < kNumProbes; ++q)
@@ -2378,7 +2402,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
         for (int a = 0; a < k; ++a)
           for (int q = 0; q < kNumProbes; ++q) {
             Pm[a][q] = cu[q][m - 1 - (i0 + a)];
-            Qm[a][q] = cv[q][n - 1 - (i0 + a)];
+            Qm[a][q] = cv[q][nv - 1 - (i0 + a)];
           }
         double G[kNumProbes][2 * kNumProbes], H[kNumProbes][kNumProbes];
         for (int a = 0; a < k; ++a)
@@ -2450,11 +2474,11 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     }
   }
   for (int j = 0; j < S[3].na; ++j) {
-    const int64_t col = n - 1 - S[3].tgt_pos[j];
+    const int64_t col = nv - 1 - S[3].tgt_pos[j];
     if (col < m) S[3].cs_h[j] *= sgn[col];
   }
   for (size_t q = 0; q < S[3].pass_dst.size(); ++q) {
-    const int64_t col = n - 1 - S[3].pass_dst[q];
+    const int64_t col = nv - 1 - S[3].pass_dst[q];
     if (col < m) S[3].pass_scale[q] *= sgn[col];
   }
   R.sign_flips = 0;
@@ -2484,7 +2508,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if (!launched_v1) {
     TRY(ev_record(P, 18, stv));
     if (B) TRY(bwin_record(P, B->parity, 1, stv));
-    TRY(apply_launch(P, S[2], V, ldv, Wv, n, 4, stv, 1));
+    TRY(null_dir());
+    TRY(apply_launch(P, S[2], V, ldv, Wv, nv, 4, stv, 1));
   }
   plan_u2.join();
   TRY(rare_grow(1, 0));
@@ -2496,7 +2521,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   TRY(upload_step(3));  // carries the sign alignment
   if (!B) TRY(upload_rot(one_stream ? 0 : 1));
   tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V2 apply", stv);
-  TRY(apply_launch(P, S[3], Wv, n, V, ldv, 6, stv, 1));
+  TRY(apply_launch(P, S[3], Wv, nv, V, ldv, 6, stv, 1));
   if (nrot_v() > 0)
     TRY(col_rotate(c.v_rows, V, ldv, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                    static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
@@ -2575,8 +2600,7 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
                                   int64_t ldv, const double* proj, const double* a, const double* b,
                                   double eps, svd1_report* rep) {
   (void)a;
-  (void)b;
-  return update_impl(P, U, ldu, sigma, V, ldv, proj, eps, rep, nullptr);
+  return update_impl(P, U, ldu, sigma, V, ldv, proj, eps, rep, nullptr, b);
 }
 
 constexpr int kMaxBatch = 28;  // buffers are sized for this many updates per call

@@ -39,7 +39,8 @@ __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
 svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
                     const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0,
                     const double* a, const double* b, double* partial_ws, int64_t partial_cap,
-                    double* proj, const double* probes, cudaStream_t st, int64_t* launches);
+                    double* proj, const double* probes, cudaStream_t st, int64_t* launches,
+                    int64_t vcols = -1);
 // probes g_k(row0 + r), k < 4, r < rows, into g[k * rows + r] (splitmix64 + Box-Muller)
 svd1_status fill_probes(uint64_t seed, int64_t row0, int64_t rows, double* g, cudaStream_t st,
                         int64_t* launches);
@@ -106,6 +107,11 @@ svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
                          const double* U_in, int64_t ld_in, const int32_t* src,
                          double* U_out, int64_t ld_out, const int32_t* dst,
                          cudaStream_t st, int64_t* launches);
+
+// thin right factor: q[r] = (b[row0 + r] - sum_{c<m} V[r, c] y[c]) * inv_beta written into
+// column m of V (the direction of b outside span(V); SVD1_THIN_V)
+svd1_status null_direction(int64_t rows, double* V, int64_t ldv, int64_t m, const double* b, int64_t row0,
+                           const double* y, double inv_beta, cudaStream_t st, int64_t* launches);
 
 // K11': the same product for a few rows (rows <= 32: the carried projection rows of a
 // batch): thread per target j, sources split over blocks (partials in
