@@ -150,8 +150,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-check", action="store_true")
-    ap.add_argument("--thin", action="store_true",
-                    help="thin right factor (SVD1_THIN_V) for m < n configs (C4)")
+    ap.add_argument("--full-v", action="store_true",
+                    help="keep the full n x n right factor for m < n configs (default: thin V, "
+                         "SVD1_THIN_V, DESIGN.md §4.10)")
     ap.add_argument("--sequential", action="store_true",
                     help="time the per-update API (svd1_update) instead of svd1_update_batch")
     ap.add_argument("--config", type=int, default=CFG_ID, choices=[1, 2, 3, 4, 5],
@@ -184,7 +185,7 @@ def main():
     # row shards (paper_1707_08369_b200.parallel: NCCL all-reduce of the projections)
     from paper_1707_08369_b200.parallel import ShardedUpdater
     stream = torch.cuda.current_stream()
-    thin = args.thin and m < n
+    thin = m < n and not args.full_v
     upd = ShardedUpdater(m, n, rank, world, eps=cfg["eps"], stream=stream, flags=P.THIN_V if thin else 0)
     u0, u1, v0, v1 = upd.u_lo, upd.u_hi, upd.v_lo, upd.v_hi
     U = U0[u0:u1].clone()
@@ -203,7 +204,7 @@ def main():
     # the stream of updates goes through svd1_update_batch (pipelined: update t+1's
     # spectral phase overlaps update t's applies); row-sharded: the K
     # projection vectors of a chunk are all-reduced once, then svd1_update_batch_projected
-    batch = not args.sequential and not thin  # (the stream API keeps the full V)
+    batch = not args.sequential and not (thin and world > 1)  # (sharded thin: per update)
     A_all = torch.stack([a for a, _ in ab])
     B_all = torch.stack([b for _, b in ab])
 

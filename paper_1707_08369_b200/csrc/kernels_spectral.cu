@@ -874,6 +874,59 @@ svd1_status null_direction(int64_t rows, double* V, int64_t ldv, int64_t m, cons
   return SVD1_OK;
 }
 
+__global__ void thin_carry_kernel(int rows, double* __restrict__ rv, int64_t ld, int64_t m,
+                                  const double* __restrict__ yt, const double* __restrict__ gram, int t,
+                                  int K, double inv_beta) {
+  const int j = blockIdx.x;  // block per carried row
+  if (j >= rows) return;
+  const double* ys = rv + int64_t(j) * ld;
+  double s = 0.0;
+  for (int64_t c = threadIdx.x; c < m; c += blockDim.x) s = fma(yt[c], ys[c], s);
+  __shared__ double red[8];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int q = 0; q < int(blockDim.x >> 5); ++q) acc += red[q];
+    rv[int64_t(j) * ld + m] = (gram[int64_t(t) * K + (K - 1 - j)] - acc) * inv_beta;
+  }
+}
+
+svd1_status thin_carry(int rows, double* rv, int64_t ld, int64_t m, const double* yt, const double* gram, int t,
+                       int K, double inv_beta, cudaStream_t st, int64_t* launches) {
+  if (rows <= 0) return SVD1_OK;
+  thin_carry_kernel<<<rows, 256, 0, st>>>(rows, rv, ld, m, yt, gram, t, K, inv_beta);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+__global__ void gram_rows_kernel(int K, const double* __restrict__ B, int64_t ldb, int64_t n,
+                                 double* __restrict__ gram) {
+  const int t = blockIdx.x / K, s2 = blockIdx.x % K;
+  double s = 0.0;
+  for (int64_t c = threadIdx.x; c < n; c += blockDim.x) s = fma(B[int64_t(t) * ldb + c], B[int64_t(s2) * ldb + c], s);
+  __shared__ double red[8];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+    for (int q = 0; q < int(blockDim.x >> 5); ++q) u += red[q];
+    gram[int64_t(t) * K + s2] = u;
+  }
+}
+
+svd1_status gram_rows(int K, const double* B, int64_t ldb, int64_t n, double* gram, cudaStream_t st,
+                      int64_t* launches) {
+  if (K <= 0) return SVD1_OK;
+  gram_rows_kernel<<<K * K, 256, 0, st>>>(K, B, ldb, n, gram);
+  *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
 svd1_status secular(const double* d, const double* z2, double rho, int n, int32_t* k_out,
                     double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
                     int64_t* launches) {

@@ -226,7 +226,9 @@ struct svd1_plan_s {
   // next update's spectral phase runs while this one's applies are in flight), carried
   // projection rows (ping-pong per side), and the events marking each parity's applies done
   StepRecord bsteps[2][4];
-  DevBuf RU[2], RV[2], few_scr[2], bproj;
+  DevBuf RU[2], RV[2], few_scr[2], bproj, bgram;
+  const double* batch_b = nullptr;  // svd1_update_batch's b's during the call (thin V)
+  int64_t batch_ldb = 0;
   cudaEvent_t bdone[2][2] = {};  // [parity][side]
   bool bdone_rec[2] = {false, false};
   cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
@@ -2007,6 +2009,12 @@ struct BatchCtx {
   double* h_next = nullptr;         // pinned: read-back of the next update's x_a | x_g | y_b
   double* prev_win = nullptr;       // receives the apply window (ms) of the update two back
   double* prev_gemm = nullptr;      // and its GEMM pass times (4; SVD1_GEMM_EVENTS)
+  // thin V (SVD1_THIN_V): b_t (device), y_t = V_t^T b_t (device, first m entries), the
+  // Gram matrix of the batch's b's (device, K x K)
+  const double* b_dev = nullptr;
+  const double* y_dev = nullptr;
+  const double* gram = nullptr;
+  int K = 0;
   int ru_next = -1, rv_next = -1;   // carried row index of the next update's a / b (-1: none)
 };
 
@@ -2040,7 +2048,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // size nv = m + 1, q = the unit direction of b outside span(V) (column m of V)
   const bool thin = (c.flags & SVD1_THIN_V) != 0;
   const int64_t nv = thin ? m + 1 : n;
-  if (thin && (B || (c.v_rows && !b_dev))) return SVD1_E_INVALID;
+  if (B) b_dev = B->b_dev;
+  if (thin && ((c.v_rows && !b_dev) || (B && (!B->y_dev || !B->gram)))) return SVD1_E_INVALID;
   if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < nv))) return SVD1_E_INVALID;
   if (m > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
   const int64_t launches0 = P->launches;
@@ -2228,10 +2237,13 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     SVD1_CUDA_TRY(cudaEventRecord(P->maps_ev[e], ss));
     DevBuf* R = side ? P->RV : P->RU;
     const int rows = side ? B->rv_rows : B->ru_rows;
-    const int64_t ld = side ? n : m;
+    const int64_t ld = side ? nv : m;
     const bool second = e == 1 || e == 3;  // R[0] -> R[1] (first step), R[1] -> R[0]
     double* rin = static_cast<double*>(R[second ? 1 : 0].p);
     double* rout = static_cast<double*>(R[second ? 0 : 1].p);
+    if (thin && e == 2)  // the later b's coordinates along this update's q
+      TRY(thin_carry(rows, rin, ld, m, B->y_dev, B->gram, B->t, B->K, beta_perp > 0.0 ? 1.0 / beta_perp : 0.0,
+                     ss, &P->launches));
     TRY(apply_rows(P, S[e], rin, rout, ld, rows, ss, side));
     if (e == 3 && rows > 0 && nrot_v() > 0)
       TRY(col_rotate(rows, rout, ld, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
@@ -2244,9 +2256,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
                                       cudaMemcpyDeviceToHost, ss));
         SVD1_CUDA_TRY(cudaMemcpyAsync(B->h_next + m, rout, 4 * m * sizeof(double), cudaMemcpyDeviceToHost, ss));
       }
-      if (side == 1 && B->rv_next >= 0)
-        SVD1_CUDA_TRY(cudaMemcpyAsync(B->h_next + 5 * m, rout + int64_t(B->rv_next) * n, n * sizeof(double),
-                                      cudaMemcpyDeviceToHost, ss));
+      if (side == 1 && B->rv_next >= 0)  // (thin: the first m entries; the rest stays 0)
+        SVD1_CUDA_TRY(cudaMemcpyAsync(B->h_next + 5 * m, rout + int64_t(B->rv_next) * ld,
+                                      (thin ? m : n) * sizeof(double), cudaMemcpyDeviceToHost, ss));
       SVD1_CUDA_TRY(cudaEventRecord(P->rb_ev[side], ss));
     }
     return SVD1_OK;
@@ -2266,7 +2278,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // thin V: column m of V <- q before the first V apply reads it (V side's apply stream)
   auto null_dir = [&]() -> svd1_status {
     if (!thin || !c.v_rows) return SVD1_OK;
-    return null_direction(c.v_rows, V, ldv, m, b_dev, c.v_row0, proj + 5 * m,
+    return null_direction(c.v_rows, V, ldv, m, b_dev, c.v_row0, B ? B->y_dev : proj + 5 * m,
                           beta_perp > 0.0 ? 1.0 / beta_perp : 0.0, stv, &P->launches);
   };
   auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
@@ -2611,7 +2623,9 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   if (!P || !U || !V || !sigma || (K > 0 && (!A || !Bv)) || K < 0 || K > kMaxBatch) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
   const int64_t m = c.m, n = c.n;
-  if (c.u_rows != m || c.v_rows != n || ldu < m || ldv < n || lda < m || ldb < n) return SVD1_E_INVALID;
+  const bool thin = (c.flags & SVD1_THIN_V) != 0;
+  if (c.u_rows != m || c.v_rows != n || ldu < m || ldv < (thin ? m + 1 : n) || lda < m || ldb < n)
+    return SVD1_E_INVALID;
   if (K == 0) return SVD1_OK;
   // every update's STEP-1 projections against the initial factors
   const size_t nproj = size_t(5 * m + n + 6);
@@ -2619,7 +2633,11 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj));
   for (int t = 0; t < int(K); ++t)
     TRY(svd1_project(P, U, ldu, V, ldv, A + int64_t(t) * lda, Bv + int64_t(t) * ldb, pj + size_t(t) * nproj));
-  return svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, K, eps, reps);
+  P->batch_b = Bv;  // thin V needs the b's themselves (null directions, Gram matrix)
+  P->batch_ldb = ldb;
+  const svd1_status st = svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, K, eps, reps);
+  P->batch_b = nullptr;
+  return st;
 }
 
 svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,
@@ -2628,7 +2646,11 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   if (!P || !sigma || (K > 0 && !proj) || K < 0 || K > kMaxBatch) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
   const int64_t m = c.m, n = c.n;
-  if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < n))) return SVD1_E_INVALID;
+  const bool thin = (c.flags & SVD1_THIN_V) != 0;
+  const int64_t nv = thin ? m + 1 : n;  // width of the carried V rows
+  // (thin V: only through svd1_update_batch, which has the b's)
+  if (thin && !P->batch_b) return SVD1_E_INVALID;
+  if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < nv))) return SVD1_E_INVALID;
   if (K == 0) return SVD1_OK;
   const int k = int(K);
   TRY(arena_reset(P));
@@ -2654,8 +2676,13 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   for (int s = 1; s < k; ++s) {
     SVD1_CUDA_TRY(cudaMemcpyAsync(ru0 + int64_t(4 + (k - 1 - s)) * m, pj + size_t(s) * nproj, m * sizeof(double),
                                   cudaMemcpyDeviceToDevice, P->st));
-    SVD1_CUDA_TRY(cudaMemcpyAsync(rv0 + int64_t(k - 1 - s) * n, pj + size_t(s) * nproj + 5 * m,
-                                  n * sizeof(double), cudaMemcpyDeviceToDevice, P->st));
+    SVD1_CUDA_TRY(cudaMemcpyAsync(rv0 + int64_t(k - 1 - s) * nv, pj + size_t(s) * nproj + 5 * m,
+                                  (thin ? m : n) * sizeof(double), cudaMemcpyDeviceToDevice, P->st));
+  }
+  double* gram = nullptr;  // thin: b_t . b_s
+  if (thin) {
+    TRY(P->bgram.get<double>(size_t(kMaxBatch) * kMaxBatch, &gram));
+    TRY(gram_rows(k, P->batch_b, P->batch_ldb, n, gram, P->st, &P->launches));
   }
   // host copies of the projections (dots of every update; x's of update 0) and sigma
   double* h;
@@ -2665,6 +2692,7 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
                                 P->st));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));  // also orders the copies before the V stream
   double* hn = h + size_t(k) * nproj + m;  // next update's x_a | x_g | y_b (read back)
+  std::memset(hn, 0, size_t(5 * m + n) * sizeof(double));  // (thin: y_b past m stays 0)
   std::vector<double> sig(h + size_t(k) * nproj, h + size_t(k) * nproj + m);
   std::vector<double> hp(h, h + nproj);
   svd1_status st = SVD1_OK;
@@ -2688,6 +2716,12 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
     b.h_next = hn;
     b.prev_win = (reps && t >= 2) ? &reps[t - 2].t_ms[5] : nullptr;
     b.prev_gemm = (reps && t >= 2) ? reps[t - 2].gemm_ms : nullptr;
+    if (thin) {
+      b.b_dev = P->batch_b + int64_t(t) * P->batch_ldb;
+      b.y_dev = t == 0 ? pj + 5 * m : rv0 + int64_t(k - 1 - t) * nv;
+      b.gram = gram;
+      b.K = k;
+    }
     svd1_report R;
     st = update_impl(P, U, ldu, sigma, V, ldv, nullptr, eps, &R, &b);
     if (reps) reps[t] = R;
@@ -2696,7 +2730,7 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
       SVD1_CUDA_TRY(cudaDeviceSynchronize());
       SVD1_CUDA_TRY(cudaMemcpy(hn, ru0 + int64_t(b.ru_next) * m, m * sizeof(double), cudaMemcpyDeviceToHost));
       SVD1_CUDA_TRY(cudaMemcpy(hn + m, ru0, 4 * m * sizeof(double), cudaMemcpyDeviceToHost));
-      SVD1_CUDA_TRY(cudaMemcpy(hn + 5 * m, rv0 + int64_t(b.rv_next) * n, n * sizeof(double),
+      SVD1_CUDA_TRY(cudaMemcpy(hn + 5 * m, rv0 + int64_t(b.rv_next) * nv, (thin ? m : n) * sizeof(double),
                                cudaMemcpyDeviceToHost));
     } else {
       SVD1_CUDA_TRY(cudaEventSynchronize(P->rb_ev[0]));

@@ -113,6 +113,15 @@ svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
 svd1_status null_direction(int64_t rows, double* V, int64_t ldv, int64_t m, const double* b, int64_t row0,
                            const double* y, double inv_beta, cudaStream_t st, int64_t* launches);
 
+// thin V in a batch: the carried rows of later updates s get their coordinate along this
+// update's q: rv[j][m] = (b_t . b_s - yt[:m] . rv[j][:m]) * inv_beta for j < rows, row j
+// holding update s = K-1-j, b_t . b_s = gram[t K + s]; rv row-major with ld; yt = V_t^T b_t
+svd1_status thin_carry(int rows, double* rv, int64_t ld, int64_t m, const double* yt, const double* gram, int t,
+                       int K, double inv_beta, cudaStream_t st, int64_t* launches);
+// gram[t * K + s] = b_t . b_s for t, s < K (rows of B, ld)
+svd1_status gram_rows(int K, const double* B, int64_t ldb, int64_t n, double* gram, cudaStream_t st,
+                      int64_t* launches);
+
 // K11': the same product for a few rows (rows <= 32: the carried projection rows of a
 // batch): thread per target j, sources split over blocks (partials in
 // `scratch`, at least few_rows_scratch_elems doubles), ordered combine (deterministic).

@@ -65,3 +65,21 @@ def test_thin_stream_matches_full(m, n, K):
     assert float((sf - st).abs().max()) <= 1e-12 * float(sf[0])
     assert float((Uf - Ut).abs().max()) <= 1e-8
     assert float((Vf[:, :m] - Vt[:, :m]).abs().max()) <= 1e-8
+
+
+@pytest.mark.parametrize("m,n,K", [(64, 256, 6), (300, 1200, 5)])
+def test_thin_batch_matches_sequential(m, n, K):
+    """Thin V through the pipelined stream: the later b's get their coordinate along each
+    update's q from the Gram matrix of the b's and the carried rows."""
+    inp = config_inputs(4, m=m, n=n, updates=K)
+    Ub, sb, Vb = T(inp["U"]), T(inp["sigma"]), _thin(inp["V"], m)
+    Us, ss, Vs = T(inp["U"]), T(inp["sigma"]), _thin(inp["V"], m)
+    pb, ps = P.Plan(m, n, flags=P.THIN_V), P.Plan(m, n, flags=P.THIN_V)
+    ab = inp["ab"][:K]
+    pb.update_batch(Ub, sb, Vb, T(np.stack([a for a, _ in ab])), T(np.stack([b for _, b in ab])))
+    for a, b in ab:
+        ps.update(Us, ss, Vs, T(a), T(b))
+    torch.cuda.synchronize()
+    assert float((sb - ss).abs().max()) <= 1e-12 * float(ss[0])
+    assert float((Ub - Us).abs().max()) <= 1e-8
+    assert float((Vb[:, :m] - Vs[:, :m]).abs().max()) <= 1e-8
