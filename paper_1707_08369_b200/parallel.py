@@ -52,8 +52,11 @@ class ShardedUpdater:
         the current factors, ONE all-reduce of the K projection vectors, then the
         pipelined stream on this rank's rows (svd1_update_batch_projected)."""
         import torch
+        from ._lib import THIN_V
         if self.world == 1:
             return self.plan.update_batch(U_loc, sigma, V_loc, A, B)
+        if self.plan.cfg.flags & THIN_V:  # sharded thin streams: one update at a time
+            return [self.update(U_loc, sigma, V_loc, A[t], B[t]) for t in range(A.shape[0])]
         K = A.shape[0]
         projs = torch.empty((K, proj_size(self.m, self.n)), dtype=torch.float64, device=A.device)
         for t in range(K):
