@@ -132,8 +132,9 @@ svd1_status svd1_update(svd1_plan_t plan, double* U, int64_t ldu, double* sigma,
  * A (device): a_t at A + t*lda (m doubles, lda >= m); B (device): b_t at B + t*ldb
  * (n doubles, ldb >= n).  U, sigma, V as for svd1_update (in place).  reps: K host
  * reports or NULL; in this mode apply_ms is 0, t_ms[5] is the update's apply window
- * (first apply start -> last apply end; windows of consecutive updates may overlap)
- * and gemm_ms is filled under SVD1_GEMM_EVENTS.  On an error at update t the factors hold the result of updates 0..t-1 and
+ * (first apply start -> last apply end; windows of consecutive updates may overlap),
+ * reps[K-1].t_ms[6] the whole batch's apply span (first apply start of update 0 ->
+ * last apply end of update K-1), and gemm_ms is filled under SVD1_GEMM_EVENTS.  On an error at update t the factors hold the result of updates 0..t-1 and
  * the error is returned.  K <= 28 per call (longer streams: call repeatedly). */
 svd1_status svd1_update_batch(svd1_plan_t plan, double* U, int64_t ldu, double* sigma,
                               double* V, int64_t ldv, const double* A, int64_t lda,

@@ -35,7 +35,7 @@ class Report(C.Structure):
                 ("pair_rotations", i32), ("apply_flops_exec", dbl * 4), ("gemm_ms", dbl * 4)]
 
     def as_dict(self):
-        return dict(t_ms=list(self.t_ms)[:6], n_active=list(self.n_active),
+        return dict(t_ms=list(self.t_ms)[:7], n_active=list(self.n_active),
                     n_deflated=list(self.n_deflated), max_iter=list(self.max_iter),
                     fmm_used=list(self.fmm_used), p=self.p, neg_clamped=self.neg_clamped,
                     sign_flips=self.sign_flips, noop=self.noop,

@@ -234,6 +234,7 @@ struct svd1_plan_s {
   cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
   cudaEvent_t maps_ev[4] = {};   // step e's column maps uploaded (spectral stream)
   cudaEvent_t bwin[2][4] = {};   // [parity]: apply start U, V; apply end U, V (timing)
+  cudaEvent_t bspan[4] = {};     // the batch's first apply start U, V; last apply end U, V
   // SVD1_TIMELINE diagnostics (batch mode): labelled device events and host stamps
   std::vector<std::pair<std::string, cudaEvent_t>> tl_dev;
   std::vector<std::pair<std::string, double>> tl_host;
@@ -403,6 +404,24 @@ svd1_status bwin_record(svd1_plan_t P, int par, int q, cudaStream_t st) {
   SVD1_CUDA_TRY(cudaEventRecord(P->bwin[par][q], st));
   return SVD1_OK;
 }
+// first / last apply of a whole batch (q as for bwin)
+svd1_status bspan_record(svd1_plan_t P, int q, cudaStream_t st) {
+  if (!P->bspan[q]) SVD1_CUDA_TRY(cudaEventCreate(&P->bspan[q]));
+  SVD1_CUDA_TRY(cudaEventRecord(P->bspan[q], st));
+  return SVD1_OK;
+}
+double bspan_ms(svd1_plan_t P) {
+  auto el = [&](int a, int b) {
+    float ms = 0.f;
+    if (!P->bspan[a] || !P->bspan[b] || cudaEventElapsedTime(&ms, P->bspan[a], P->bspan[b]) != cudaSuccess) {
+      cudaGetLastError();
+      return 0.0;
+    }
+    return double(ms);
+  };
+  return std::max(el(0, 2), el(0, 3)) - std::min(0.0, el(0, 1));
+}
+
 // first apply start -> last apply end of the update with that parity (after it completed)
 double bwin_ms(svd1_plan_t P, int par) {
   auto el = [&](int a, int b) {
@@ -2289,12 +2308,14 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       if (e == 0) {
         TRY(ev_record(P, 16, P->st));
         if (B) TRY(bwin_record(P, B->parity, 0, P->st));
+        if (B && B->t == 0) TRY(bspan_record(P, 0, P->st));
         tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U1 apply", P->st);
         TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
         launched_u1 = true;
       } else {
         TRY(ev_record(P, 18, stv));
         if (B) TRY(bwin_record(P, B->parity, 1, stv));
+        if (B && B->t == 0) TRY(bspan_record(P, 1, stv));
         tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V1 apply", stv);
         TRY(null_dir());
         TRY(apply_launch(P, S[2], V, ldv, Wv, nv, 4, stv, 1));
@@ -2515,11 +2536,13 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if (!launched_u1) {
     TRY(ev_record(P, 16, P->st));
     if (B) TRY(bwin_record(P, B->parity, 0, P->st));
+    if (B && B->t == 0) TRY(bspan_record(P, 0, P->st));
     TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
   }
   if (!launched_v1) {
     TRY(ev_record(P, 18, stv));
     if (B) TRY(bwin_record(P, B->parity, 1, stv));
+    if (B && B->t == 0) TRY(bspan_record(P, 1, stv));
     TRY(null_dir());
     TRY(apply_launch(P, S[2], V, ldv, Wv, nv, 4, stv, 1));
   }
@@ -2737,6 +2760,11 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
       SVD1_CUDA_TRY(cudaEventSynchronize(P->rb_ev[1]));
     }
   }
+  const bool span_ok = st == SVD1_OK;
+  if (span_ok) {
+    TRY(bspan_record(P, 2, P->st));
+    TRY(bspan_record(P, 3, P->st2));
+  }
   // drain every stream; the factors now hold updates 0..t; sigma of the last success
   for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1], P->sp[2], P->sp[3]})
     if (q || q == P->st) SVD1_CUDA_TRY(cudaStreamSynchronize(q));
@@ -2753,6 +2781,7 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
     P->tl_host.clear();
     P->tl_on = false;
   }
+  if (reps && span_ok) reps[k - 1].t_ms[6] = bspan_ms(P);  // whole batch's apply span
   if (reps && st == SVD1_OK)  // apply windows of the last two updates
     for (int t = std::max(0, k - 2); t < k; ++t)
       if (P->bdone_rec[t & 1]) {
