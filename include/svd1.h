@@ -211,6 +211,12 @@ svd1_status svd1_colnorms(svd1_plan_t plan, int64_t n, const double* d,
 svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k,
                                 const double* tau, double eps, int64_t* stats_out);
 
+/* Host-only planning diagnostics of the secular FMM (DESIGN.md §4.2 K2'): builds the
+ * plan for the ascending sources d (host, n) and fills stats_out (8 int64): depth L,
+ * cells, leaves, M2L partners, near ranges, max near terms per root, direct roots,
+ * planning time in ns.  No GPU needed. */
+svd1_status svd1_secfmm_plan_stats(int64_t n, const double* d, int64_t* stats_out);
+
 const char* svd1_status_string(svd1_status s);
 /* Library build identifier (for the bench/smoke evidence). */
 const char* svd1_version(void);

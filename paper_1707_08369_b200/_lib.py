@@ -69,6 +69,7 @@ svd1_secular_solve = _sig("svd1_secular_solve", [vp, i64, vp, vp, dbl, vp, vp, C
 svd1_loewner = _sig("svd1_loewner", [vp, i64, vp, vp, vp, dbl, vp, vp])
 svd1_colnorms = _sig("svd1_colnorms", [vp, i64, vp, vp, vp, vp, vp])
 svd1_fmm_tree_stats = _sig("svd1_fmm_tree_stats", [i64, vp, vp, vp, dbl, vp])
+svd1_secfmm_plan_stats = _sig("svd1_secfmm_plan_stats", [i64, vp, vp])
 lib.svd1_status_string.argtypes = [status_t]
 lib.svd1_status_string.restype = C.c_char_p
 lib.svd1_version.argtypes = []
@@ -76,7 +77,7 @@ lib.svd1_version.restype = C.c_char_p
 
 EXPORTS = ["svd1_plan_create", "svd1_plan_destroy", "svd1_update", "svd1_update_batch", "svd1_update_batch_projected", "svd1_project",
            "svd1_update_projected", "svd1_cauchy_apply", "svd1_secular_solve", "svd1_loewner",
-           "svd1_colnorms", "svd1_fmm_tree_stats", "svd1_status_string", "svd1_version"]
+           "svd1_colnorms", "svd1_fmm_tree_stats", "svd1_secfmm_plan_stats", "svd1_status_string", "svd1_version"]
 
 FORCE_DIRECT = 0x1
 FORCE_FMM = 0x2
@@ -91,6 +92,18 @@ def status_string(code: int) -> str:
 
 def version() -> str:
     return lib.svd1_version().decode()
+
+
+def secfmm_plan_stats(d):
+    """Host-only secular-FMM plan statistics (numpy ascending d): dict of svd1.h's 8 stats."""
+    import numpy as np
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    out = np.zeros(8, dtype=np.int64)
+    code = svd1_secfmm_plan_stats(d.size, d.ctypes.data, out.ctypes.data)
+    if code:
+        raise RuntimeError(status_string(code))
+    keys = ["L", "cells", "leaves", "m2l_parts", "near_ranges", "max_near_terms", "direct_roots", "plan_ns"]
+    return dict(zip(keys, (int(x) for x in out)))
 
 
 def fmm_tree_stats(d, k, tau, eps=1e-10):

@@ -657,13 +657,25 @@ void secfmm_plan(const double* d, int n, SecPlanHost& S) {
       stack.push_back({x, 2 * y + 1});
     }
   }
-  std::sort(m2l_pairs.begin(), m2l_pairs.end());
+  // group the pairs by target cell with a counting sort (partners ascending per cell)
+  auto group = [nc](std::vector<std::pair<int, int>>& pairs, std::vector<int>& off, std::vector<int>& val) {
+    off.assign(nc + 1, 0);
+    for (const auto& pr : pairs) ++off[pr.first + 1];
+    for (int c = 0; c < nc; ++c) off[c + 1] += off[c];
+    val.resize(pairs.size());
+    std::vector<int> fill(off.begin(), off.end() - 1);
+    for (const auto& pr : pairs) val[fill[pr.first]++] = pr.second;
+    for (int c = 0; c < nc; ++c)
+      if (off[c + 1] - off[c] > 1) std::sort(val.begin() + off[c], val.begin() + off[c + 1]);
+  };
+  std::vector<int> m_off, m_val;
+  group(m2l_pairs, m_off, m_val);
   S.parts.clear();
-  size_t q = 0;
+  S.parts.reserve(m_val.size());
   for (int c = 0; c < nc; ++c) {
     S.cells[c].m2l_off = int32_t(S.parts.size());
-    for (; q < m2l_pairs.size() && m2l_pairs[q].first == c; ++q) {
-      const int x = m2l_pairs[q].second;
+    for (int q = m_off[c]; q < m_off[c + 1]; ++q) {
+      const int x = m_val[q];
       const SecFmmCell& X = S.cells[x];
       int32_t fl = X.c > S.cells[c].ct ? 1 : 0;
       if (X.hi - X.lo < kSecP) fl |= 2;
@@ -688,18 +700,17 @@ void secfmm_plan(const double* d, int n, SecPlanHost& S) {
   for (int q = 0; q < S.nleaf; ++q)
     if (S.cells[S.leaf_cell[q]].pad) S.direct.push_back(S.leaf_lo[q + 1] - 1);
   S.direct.push_back(n - 1);
-  std::sort(near_pairs.begin(), near_pairs.end());
+  std::vector<int> n_off, n_val;
+  group(near_pairs, n_off, n_val);
   S.near_off.assign(S.nleaf + 1, 0);
   S.near_lo.clear();
   S.near_hi.clear();
-  size_t r = 0;
   for (int lf = 0; lf < S.nleaf; ++lf) {
     const int c = S.leaf_cell[lf];
     S.near_off[lf] = int32_t(S.near_lo.size());
-    while (r < near_pairs.size() && near_pairs[r].first < c) ++r;
-    for (; r < near_pairs.size() && near_pairs[r].first == c; ++r) {
-      const SecFmmCell& X = S.cells[near_pairs[r].second];
-      if (!S.near_hi.empty() && S.near_off[lf] < int32_t(S.near_lo.size()) && S.near_hi.back() == X.lo)
+    for (int q = n_off[c]; q < n_off[c + 1]; ++q) {
+      const SecFmmCell& X = S.cells[n_val[q]];
+      if (S.near_off[lf] < int32_t(S.near_lo.size()) && S.near_hi.back() == X.lo)
         S.near_hi.back() = X.hi;  // merge adjacent ranges
       else {
         S.near_lo.push_back(X.lo);
@@ -1397,18 +1408,23 @@ svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
 }
 
 // Secular FMM: plan from the oriented sources (host), one-copy upload, device view.
-int sec_fmm_min() {
+// Active size from which the secular solve uses the FMM far field.  In a stream
+// (svd1_update_batch) the solve shares the GPU with the previous update's applies, and
+// the FMM's smaller GPU work pays from C3's size on (measured 400 -> 410 updates/s); one
+// call per update it pays only at C5's (its host plan and launches are on the critical
+// path there).  SVD1_SEC_FMM_MIN overrides both.
+int sec_fmm_min(bool stream) {
   static const int v = [] {
     const char* e = std::getenv("SVD1_SEC_FMM_MIN");
-    return e ? std::max(64, atoi(e)) : 6144;
+    return e ? std::max(64, atoi(e)) : 0;
   }();
-  return v;
+  return v ? v : (stream ? 3072 : 6144);
 }
 
-bool use_sec_fmm(uint32_t flags, int n) {
+bool use_sec_fmm(uint32_t flags, int n, bool stream) {
   if (flags & SVD1_SECULAR_DIRECT) return false;
   if (flags & SVD1_SECULAR_FMM) return n > 64;
-  return n >= sec_fmm_min();
+  return n >= sec_fmm_min(stream);
 }
 
 svd1_status secfmm_prepare(svd1_plan_t P, SecPlanHost& H, DevBuf& blob, DevBuf& scr, const double* dr,
@@ -1638,7 +1654,7 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   tl_mark(P, "  ev" + std::to_string(ev0) + " uploaded", st);
   double* scr;
   TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
-  S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na);
+  S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na, side >= 2);  // sides 2, 3: batch mode
   if (S.sec_fmm_used) {  // STEP 2 with the far field by FMM
     SecFmmDev F;
     // (reads the oriented sources from the staging region before its own upload)
@@ -2845,6 +2861,29 @@ svd1_status svd1_cauchy_apply(svd1_plan_t P, int64_t rows, int64_t n, const doub
   return SVD1_OK;
 }
 
+svd1_status svd1_secfmm_plan_stats(int64_t n, const double* d, int64_t* st) {
+  if (n < 2 || !d || !st || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
+  SecPlanHost H;
+  const auto t0 = std::chrono::steady_clock::now();
+  secfmm_plan(d, int(n), H);
+  const auto t1 = std::chrono::steady_clock::now();
+  int64_t mx = 0;
+  for (int q = 0; q < H.nleaf; ++q) {
+    int64_t s2 = 0;
+    for (int g = H.near_off[q]; g < H.near_off[q + 1]; ++g) s2 += H.near_hi[g] - H.near_lo[g];
+    mx = std::max(mx, s2);
+  }
+  st[0] = H.L;
+  st[1] = H.ncells;
+  st[2] = H.nleaf;
+  st[3] = int64_t(H.parts.size());
+  st[4] = int64_t(H.near_lo.size());
+  st[5] = mx;
+  st[6] = int64_t(H.direct.size());
+  st[7] = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+  return SVD1_OK;
+}
+
 svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k, const double* tau,
                                 double eps, int64_t* st) {
   if (n <= 0 || !d || !k || !tau || !st || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
@@ -2886,7 +2925,7 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
   double* orient;
   TRY(P->scratch_d.get<double>(size_t(2 * n), &orient));
   TRY(secular_orient(d, z, rho, int(n), orient, orient + n, P->st, &P->launches));
-  if (use_sec_fmm(P->cfg.flags, int(n))) {  // plan from the oriented sources (host copy)
+  if (use_sec_fmm(P->cfg.flags, int(n), false)) {  // plan from the oriented sources (host copy)
     std::vector<double> dr(n);
     SVD1_CUDA_TRY(cudaMemcpyAsync(dr.data(), orient, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
     SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
