@@ -45,3 +45,30 @@ def test_small_and_ragged(n):
     d, k, tau, *_ = interlaced_cauchy(n, 1, n)
     st = fmm_tree_stats(d, k, tau, 1e-10)
     assert st["max_leaf"] <= 33 and st["tasks"] >= 1
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "graded", "uniform"])
+def test_secular_fmm_plan_bounded(kind):
+    """The secular FMM plan (K2'): every root's near field stays a small
+    fraction of n (a few leaves; the sparse tails of a Gaussian spectrum give the widest
+    lists, 24 leaves of 32 at n = 4096), and the directly-summed roots are the last one
+    plus the outlier-gap ones."""
+    from paper_1707_08369_b200._lib import secfmm_plan_stats
+    rng = np.random.default_rng(3)
+    n = 4096
+    d, _, _ = random_secular(n, rng, kind=kind)
+    st = secfmm_plan_stats(np.sort(d))
+    assert st["max_near_terms"] <= n // 4, st
+    assert 1 <= st["direct_roots"] <= 8, st
+    assert st["leaves"] * 32 >= n
+
+
+def test_secular_fmm_plan_outliers():
+    """Outliers far above a graded bulk (C3 after updates): the outlier gap does not make
+    any leaf near-field to the whole spectrum; the gap roots are summed directly."""
+    from paper_1707_08369_b200._lib import secfmm_plan_stats
+    rng = np.random.default_rng(0)
+    n = 4096
+    d = np.sort(np.concatenate([10.0 ** (-12 * np.arange(n - 16) / n), 1.7e7 * (1 + rng.random(16))]))
+    st = secfmm_plan_stats(d)
+    assert st["max_near_terms"] <= 6 * 32 and st["direct_roots"] >= 2, st
