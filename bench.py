@@ -204,9 +204,8 @@ def main():
     # the stream of updates goes through svd1_update_batch (pipelined: update t+1's
     # spectral phase overlaps update t's applies); row-sharded: the K
     # projection vectors of a chunk are all-reduced once, then svd1_update_batch_projected
-    # (sharded thin streams: per update; C1/C2 are launch-bound, where the per-update API
-    # is the faster of the two)
-    batch = not args.sequential and not (thin and world > 1) and m * n > 1024 * 1024
+    # (C1/C2 are launch-bound, where the per-update API is the faster of the two)
+    batch = not args.sequential and m * n > 1024 * 1024
     A_all = torch.stack([a for a, _ in ab])
     B_all = torch.stack([b for _, b in ab])
 

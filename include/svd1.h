@@ -144,13 +144,14 @@ svd1_status svd1_update_batch(svd1_plan_t plan, double* U, int64_t ldu, double* 
 /* Row-sharded stream: svd1_update_batch after the projections.  proj (device): K
  * consecutive all-reduced svd1_project outputs (5*m + n + 6 doubles each, update t at
  * proj + t*(5*m + n + 6)), every one computed against the factors at the START of the
- * stream; sigma full, replicated; U_loc, V_loc this rank's row blocks.  Every rank runs
- * the same spectral phases and carried-row transforms (deterministic) on its own GPU;
- * no collective inside.  K <= 28. */
+ * stream; sigma full, replicated; U_loc, V_loc this rank's row blocks.  B (device, the
+ * FULL b_t at B + t*ldb, ldb >= n) is needed with SVD1_THIN_V only (else NULL).  Every
+ * rank runs the same spectral phases and carried-row transforms (deterministic) on its
+ * own GPU; no collective inside.  K <= 28. */
 svd1_status svd1_update_batch_projected(svd1_plan_t plan, double* U_loc, int64_t ldu,
                                         double* sigma, double* V_loc, int64_t ldv,
-                                        const double* proj, int64_t K, double eps,
-                                        svd1_report* reps);
+                                        const double* proj, const double* B, int64_t ldb,
+                                        int64_t K, double eps, svd1_report* reps);
 
 /* Row-sharded update, phase 1 (STEP 1 projections over the LOCAL rows):
  * proj (device, 5*m + n + 6 doubles) receives the partial sums

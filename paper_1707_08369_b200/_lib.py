@@ -58,8 +58,8 @@ svd1_plan_destroy = _sig("svd1_plan_destroy", [vp])
 svd1_update = _sig("svd1_update", [vp, vp, i64, vp, vp, i64, vp, vp, dbl, C.POINTER(Report)])
 svd1_update_batch = _sig("svd1_update_batch", [vp, vp, i64, vp, vp, i64, vp, i64, vp, i64, i64, dbl,
                                                C.POINTER(Report)])
-svd1_update_batch_projected = _sig("svd1_update_batch_projected", [vp, vp, i64, vp, vp, i64, vp, i64, dbl,
-                                                                   C.POINTER(Report)])
+svd1_update_batch_projected = _sig("svd1_update_batch_projected", [vp, vp, i64, vp, vp, i64, vp, vp, i64, i64,
+                                                                   dbl, C.POINTER(Report)])
 svd1_project = _sig("svd1_project", [vp, vp, i64, vp, i64, vp, vp, vp])
 svd1_update_projected = _sig("svd1_update_projected",
                              [vp, vp, i64, vp, vp, i64, vp, vp, vp, dbl, C.POINTER(Report)])

@@ -95,14 +95,17 @@ class Plan:
                "svd1_update_batch")
         return [reps[t].as_dict() for t in range(K)]
 
-    def update_batch_projected(self, U, sigma, V, projs, eps=-1.0):
-        """Row-sharded stream after the projections: projs (K x proj_size) all-reduced."""
+    def update_batch_projected(self, U, sigma, V, projs, B=None, eps=-1.0):
+        """Row-sharded stream after the projections: projs (K x proj_size) all-reduced;
+        B (K x n, the full b's) only with THIN_V."""
         K = projs.shape[0]
         reps = (L.Report * max(K, 1))()
         _check(L.svd1_update_batch_projected(
             self._h, _ptr(U, name="U") if U is not None else None, _ld(U) if U is not None else 0,
             _ptr(sigma, name="sigma"), _ptr(V, name="V") if V is not None else None,
-            _ld(V) if V is not None else 0, _ptr(projs, name="projs"), int(K), float(eps), reps),
+            _ld(V) if V is not None else 0, _ptr(projs, name="projs"),
+            _ptr(B, name="B") if B is not None else None, _ld(B) if B is not None else 0,
+            int(K), float(eps), reps),
             "svd1_update_batch_projected")
         return [reps[t].as_dict() for t in range(K)]
 

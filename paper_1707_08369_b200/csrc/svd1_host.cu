@@ -2672,23 +2672,25 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj));
   for (int t = 0; t < int(K); ++t)
     TRY(svd1_project(P, U, ldu, V, ldv, A + int64_t(t) * lda, Bv + int64_t(t) * ldb, pj + size_t(t) * nproj));
-  P->batch_b = Bv;  // thin V needs the b's themselves (null directions, Gram matrix)
-  P->batch_ldb = ldb;
-  const svd1_status st = svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, K, eps, reps);
-  P->batch_b = nullptr;
-  return st;
+  return svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, Bv, ldb, K, eps, reps);
 }
 
 svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,
-                                        int64_t ldv, const double* proj, int64_t K, double eps,
-                                        svd1_report* reps) {
+                                        int64_t ldv, const double* proj, const double* Bv, int64_t ldb,
+                                        int64_t K, double eps, svd1_report* reps) {
   if (!P || !sigma || (K > 0 && !proj) || K < 0 || K > kMaxBatch) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
   const int64_t m = c.m, n = c.n;
   const bool thin = (c.flags & SVD1_THIN_V) != 0;
   const int64_t nv = thin ? m + 1 : n;  // width of the carried V rows
-  // (thin V: only through svd1_update_batch, which has the b's)
-  if (thin && !P->batch_b) return SVD1_E_INVALID;
+  // thin V needs the b's themselves (null directions, Gram matrix)
+  if (thin && (!Bv || ldb < n)) return SVD1_E_INVALID;
+  P->batch_b = thin ? Bv : nullptr;
+  P->batch_ldb = ldb;
+  struct ResetB {
+    svd1_plan_t P;
+    ~ResetB() { P->batch_b = nullptr; }
+  } reset_b{P};
   if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < nv))) return SVD1_E_INVALID;
   if (K == 0) return SVD1_OK;
   const int k = int(K);

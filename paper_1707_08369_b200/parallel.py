@@ -55,14 +55,13 @@ class ShardedUpdater:
         from ._lib import THIN_V
         if self.world == 1:
             return self.plan.update_batch(U_loc, sigma, V_loc, A, B)
-        if self.plan.cfg.flags & THIN_V:  # sharded thin streams: one update at a time
-            return [self.update(U_loc, sigma, V_loc, A[t], B[t]) for t in range(A.shape[0])]
+        thin = bool(self.plan.cfg.flags & THIN_V)
         K = A.shape[0]
         projs = torch.empty((K, proj_size(self.m, self.n)), dtype=torch.float64, device=A.device)
         for t in range(K):
             self.plan.project(U_loc, V_loc, A[t], B[t], projs[t])
         allreduce_projection(projs, self.group)
-        return self.plan.update_batch_projected(U_loc, sigma, V_loc, projs)
+        return self.plan.update_batch_projected(U_loc, sigma, V_loc, projs, B if thin else None)
 
     def update(self, U_loc, sigma, V_loc, a, b):
         if self.world == 1:

@@ -116,7 +116,8 @@ def test_batch_c3_full_size():
     assert res <= 1e-10 and orth <= 1e-10, (res, orth)
 
 
-@pytest.mark.parametrize("cfg,m,n,K,flags", [(3, 256, 256, 5, P.FORCE_FMM), (4, 64, 256, 4, 0)])
+@pytest.mark.parametrize("cfg,m,n,K,flags", [(3, 256, 256, 5, P.FORCE_FMM), (4, 64, 256, 4, 0),
+                                             (4, 64, 256, 4, P.THIN_V)])
 def test_sharded_batch_two_ranks(cfg, m, n, K, flags):
     """The row-sharded stream (svd1_update_batch_projected) for world size 2, the two
     ranks run one after the other on this GPU (no collective inside the stream: the
@@ -124,7 +125,16 @@ def test_sharded_batch_two_ranks(cfg, m, n, K, flags):
     equal the single-process stream's factors."""
     from paper_1707_08369_b200.parallel import row_block
     inp = config_inputs(cfg, m=m, n=n, updates=K)
-    Ub, sb, Vb, _ = _stream(inp, K, flags, batch=True)
+    thin = bool(flags & P.THIN_V)
+    if thin:  # reference: the single-process thin stream
+        Ub, sb, Vb = T(inp["U"]), T(inp["sigma"]), torch.zeros((n, m + 1), dtype=torch.float64, device=DEV)
+        Vb[:, :m] = T(inp["V"][:, :m])
+        pr = P.Plan(m, n, flags=flags)
+        pr.update_batch(Ub, sb, Vb, T(np.stack([a for a, _ in inp["ab"][:K]])),
+                        T(np.stack([b for _, b in inp["ab"][:K]])))
+        torch.cuda.synchronize()
+    else:
+        Ub, sb, Vb, _ = _stream(inp, K, flags, batch=True)
     ab = inp["ab"][:K]
     A = T(np.stack([a for a, _ in ab]))
     B = T(np.stack([b for _, b in ab]))
@@ -133,14 +143,19 @@ def test_sharded_batch_two_ranks(cfg, m, n, K, flags):
         u0, u1 = row_block(m, r, world)
         v0, v1 = row_block(n, r, world)
         plan = P.Plan(m, n, flags=flags, u_rows=u1 - u0, v_rows=v1 - v0, u_row0=u0, v_row0=v0)
-        Ul, Vl = T(inp["U"][u0:u1]), T(inp["V"][v0:v1])
+        Ul = T(inp["U"][u0:u1])
+        if thin:
+            Vl = torch.zeros((v1 - v0, m + 1), dtype=torch.float64, device=DEV)
+            Vl[:, :m] = T(inp["V"][v0:v1, :m])
+        else:
+            Vl = T(inp["V"][v0:v1])
         projs = torch.empty((K, plan.proj_size()), dtype=torch.float64, device=DEV)
         for t in range(K):
             plan.project(Ul, Vl, A[t], B[t], projs[t])
         parts.append(dict(plan=plan, U=Ul, V=Vl, s=T(inp["sigma"]), projs=projs))
     total = sum(p_["projs"] for p_ in parts)  # the all-reduce
     for p_ in parts:
-        p_["plan"].update_batch_projected(p_["U"], p_["s"], p_["V"], total)
+        p_["plan"].update_batch_projected(p_["U"], p_["s"], p_["V"], total, B if thin else None)
         torch.cuda.synchronize()
     Us = torch.cat([p_["U"] for p_ in parts])
     Vs = torch.cat([p_["V"] for p_ in parts])
