@@ -164,3 +164,26 @@ def test_sharded_batch_two_ranks(cfg, m, n, K, flags):
     assert float((Us - Ub).abs().max()) <= 1e-8 and float((Vs[:, :m] - Vb[:, :m]).abs().max()) <= 1e-8
     for p_ in parts:
         p_["plan"].close()
+
+
+@pytest.mark.parametrize("K", [1, 2, 28])
+def test_batch_lengths(K):
+    """Edge lengths: one update (no carried rows), two, and the maximum 28 (31 carried
+    U rows: the widest few-rows kernel)."""
+    inp = config_inputs(3, m=128, n=128, updates=K)
+    Ub, sb, Vb, rb = _stream(inp, K, P.FORCE_FMM, batch=True)
+    Us, ss, Vs, rs = _stream(inp, K, P.FORCE_FMM, batch=False)
+    assert len(rb) == K
+    assert float((sb - ss).abs().max()) <= 1e-12 * float(ss[0])
+    assert float((Ub - Us).abs().max()) <= 1e-8 and float((Vb - Vs).abs().max()) <= 1e-8
+    res, orth, sig_err = _invariants(inp, K, Ub, sb, Vb)
+    assert res <= 1e-10 and orth <= 1e-10 and sig_err <= 1e-12, (res, orth, sig_err)
+
+
+def test_batch_too_long():
+    inp = config_inputs(3, m=64, n=64, updates=29)
+    U, s, V = T(inp["U"]), T(inp["sigma"]), T(inp["V"])
+    plan = P.Plan(64, 64)
+    with pytest.raises(P.SVD1Error) as e:
+        plan.update_batch(U, s, V, T(np.stack([a for a, _ in inp["ab"]])), T(np.stack([b for _, b in inp["ab"]])))
+    assert e.value.code == 1
