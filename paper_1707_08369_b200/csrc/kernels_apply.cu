@@ -679,6 +679,8 @@ svd1_status apply_few_rows(int rows, int n, const double* d, const int32_t* k, c
     few_rows_partial_kernel<8><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
   else if (rows <= 16)
     few_rows_partial_kernel<16><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
+  else if (rows <= 24)
+    few_rows_partial_kernel<24><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
   else
     few_rows_partial_kernel<32><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
   few_rows_combine_kernel<<<unsigned((int64_t(rows) * n + 255) / 256), 256, 0, st>>>(rows, n, nsplit, scratch,
