@@ -639,9 +639,22 @@ __global__ void __launch_bounds__(256) secfmm_phase_kernel(SecFmmDev F, const do
 constexpr int kLT = 128;   // threads (i) per block
 constexpr int kLJ = 256;   // j per shared-memory tile
 
+// The last block of each column of the grid (counted on ctr[blockIdx.x], which it
+// resets) combines the chunks' partials in chunk order: deterministic, one launch.
+__device__ __forceinline__ bool last_block_of_column(int* ctr) {
+  __shared__ bool last;
+  __threadfence();  // this block's partials are visible before it is counted
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ctr + blockIdx.x, 1) == int(gridDim.y) - 1;
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
 __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
     const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau, int n,
-    int chunk, double* __restrict__ pm, int32_t* __restrict__ pe) {
+    int chunk, double* __restrict__ pm, int32_t* __restrict__ pe, int* __restrict__ ctr, double rho,
+    const double* __restrict__ z, double* __restrict__ zhat) {
   __shared__ double s_d[kLJ], s_mu[kLJ], s_t[kLJ];
   const int i = blockIdx.x * kLT + threadIdx.x;
   const int j0 = blockIdx.y * chunk, j1 = min(n, j0 + chunk);
@@ -696,24 +709,21 @@ __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
     pm[int64_t(blockIdx.y) * n + i] = m;
     pe[int64_t(blockIdx.y) * n + i] = E + e;
   }
+  if (!last_block_of_column(ctr)) return;
+  if (i < n) {  // combine (the partials of other blocks: L2, not this SM's L1)
+    double P = 1.0;
+    int Et = 0;
+    for (int c = 0; c < int(gridDim.y); ++c) {
+      int e;
+      P = frexp(P * __ldcg(pm + int64_t(c) * n + i), &e);
+      Et += e + __ldcg(pe + int64_t(c) * n + i);
+    }
+    const double zh2 = ldexp(P, Et) / fabs(rho);
+    zhat[i] = copysign(sqrt(zh2), z[i]);
+  }
+  if (threadIdx.x == 0) ctr[blockIdx.x] = 0;
 }
 
-__global__ void loewner_combine_kernel(const double* __restrict__ pm, const int32_t* __restrict__ pe,
-                                       int nchunks, int n, double rho, const double* __restrict__ z,
-                                       double* __restrict__ zhat) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double P = 1.0;
-  int E = 0;
-#pragma unroll 8
-  for (int c = 0; c < nchunks; ++c) {
-    int e;
-    P = frexp(P * pm[int64_t(c) * n + i], &e);
-    E += e + pe[int64_t(c) * n + i];
-  }
-  const double zh2 = ldexp(P, E) / fabs(rho);
-  zhat[i] = copysign(sqrt(zh2), z[i]);
-}
 
 // ------------------------------------------------------------------ K3b/K12
 // For column j: y_i = zhat_i |tau_j| / ((d_i - d_kj) - tau_j)  (|y_i| <~ |zhat_i|: the
@@ -728,7 +738,8 @@ template <int NC>
 __global__ void __launch_bounds__(kCT) colnorm_partial_kernel(
     const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau,
     const double* __restrict__ zhat, int n, int chunk, const double* __restrict__ carry,
-    double* __restrict__ part) {
+    double* __restrict__ part, int* __restrict__ ctr, double* __restrict__ colscale,
+    double* __restrict__ carry_out, int32_t* __restrict__ status) {
   __shared__ double s_d[kCI], s_z[kCI], s_c[NC > 0 ? NC : 1][kCI];
   const int j = blockIdx.x * kCT + threadIdx.x;
   const int i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
@@ -761,31 +772,27 @@ __global__ void __launch_bounds__(kCT) colnorm_partial_kernel(
 #pragma unroll
     for (int q = 0; q < NC; ++q) part[base + int64_t(q + 1) * n + j] = t[q];
   }
+  if (!last_block_of_column(ctr)) return;
+  if (ok) {  // combine in chunk order
+    const int64_t cstride = int64_t(NC + 1) * n;
+    double ss = 0.0;
+    for (int c = 0; c < int(gridDim.y); ++c) ss += __ldcg(part + int64_t(c) * cstride + j);
+    const double rs = sqrt(ss);
+    const double cs = fabs(tj) / rs;
+    if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
+    colscale[j] = cs;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      double tt = 0.0;
+      for (int c = 0; c < int(gridDim.y); ++c) tt += __ldcg(part + int64_t(c) * cstride + int64_t(q + 1) * n + j);
+      carry_out[int64_t(q) * n + j] = tt / rs;
+    }
+  }
+  if (threadIdx.x == 0) ctr[blockIdx.x] = 0;
 }
 
 // thread per (j, q): q = 0 -> colscale_j (and the status check), q >= 1 -> carried
 // vector q-1 (which also needs ||y||: recomputed, the partials are L2-resident)
-__global__ void colnorm_combine_kernel(const double* __restrict__ part, int nchunks, int nc, int n,
-                                       const double* __restrict__ tau, double* __restrict__ colscale,
-                                       double* __restrict__ carry_out, int32_t* __restrict__ status) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x, q = blockIdx.y;
-  if (j >= n) return;
-  const int64_t cstride = int64_t(nc + 1) * n;
-  double s = 0.0;
-#pragma unroll 8
-  for (int c = 0; c < nchunks; ++c) s += part[int64_t(c) * cstride + j];
-  const double rs = sqrt(s);
-  if (q == 0) {
-    const double cs = fabs(tau[j]) / rs;
-    if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
-    colscale[j] = cs;
-    return;
-  }
-  double t = 0.0;
-#pragma unroll 8
-  for (int c = 0; c < nchunks; ++c) t += part[int64_t(c) * cstride + int64_t(q) * n + j];
-  carry_out[int64_t(q - 1) * n + j] = t / rs;
-}
 
 inline unsigned blocks_for_warps(int64_t nwarps, int threads = 256) {
   return unsigned((nwarps * 32 + threads - 1) / threads);
@@ -964,9 +971,20 @@ static int inner_chunks(int n, int threads) {
   return ch;
 }
 
-int64_t spectral_scratch_elems(int n, int ncarry) {
+// the last-block counters at the end of a spectral scratch buffer
+int64_t spectral_counter_offset(int n, int ncarry) {
   const int ch = std::max(inner_chunks(n, kLT), inner_chunks(n, kCT));
   return int64_t(ch) * n * (ncarry + 2) + 16;
+}
+int* spectral_counters(double* scratch, int n, int ncarry) {
+  return reinterpret_cast<int*>(scratch + spectral_counter_offset(n, ncarry));
+}
+
+
+int64_t spectral_scratch_elems(int n, int ncarry) {
+  const int ch = std::max(inner_chunks(n, kLT), inner_chunks(n, kCT));
+  // partials, then the last-block counters (one int per column block; zero between uses)
+  return int64_t(ch) * n * (ncarry + 2) + 16 + (n + 63) / 64 + 16;
 }
 
 svd1_status secular_orient(const double* d, const double* z, double rho, int n, double* dr,
@@ -979,7 +997,7 @@ svd1_status secular_orient(const double* d, const double* z, double rho, int n, 
 }
 
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
-                    const double* z, int n, double* zhat, double* scratch, cudaStream_t st,
+                    const double* z, int n, double* zhat, double* scratch, int* ctr, cudaStream_t st,
                     int64_t* launches) {
   if (n <= 0) return SVD1_OK;
   const int ch = inner_chunks(n, kLT);
@@ -987,34 +1005,32 @@ svd1_status loewner(const double* d, const int32_t* k, const double* tau, double
   double* pm = scratch;
   int32_t* pe = reinterpret_cast<int32_t*>(scratch + int64_t(ch) * n);
   loewner_partial_kernel<<<dim3(unsigned((n + kLT - 1) / kLT), unsigned(ch)), kLT, 0, st>>>(d, k, tau, n,
-                                                                                       chunk, pm, pe);
-  loewner_combine_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(pm, pe, ch, n, rho, z, zhat);
-  *launches += 2;
+                                                                                       chunk, pm, pe, ctr, rho,
+                                                                                       z, zhat);
+  *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }
 
 svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
                           const double* zhat, int n, const double* carry, int ncarry,
-                          double* colscale, double* carry_out, int32_t* status, double* scratch,
+                          double* colscale, double* carry_out, int32_t* status, double* scratch, int* ctr,
                           cudaStream_t st, int64_t* launches) {
   if (n <= 0) return SVD1_OK;
   const int ch = inner_chunks(n, kCT);
   const int chunk = (n + ch - 1) / ch;
   const dim3 g(unsigned((n + kCT - 1) / kCT), unsigned(ch));
   switch (ncarry) {
-    case 0: colnorm_partial_kernel<0><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
-    case 1: colnorm_partial_kernel<1><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
-    case 2: colnorm_partial_kernel<2><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
-    case 3: colnorm_partial_kernel<3><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
-    case 4: colnorm_partial_kernel<4><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
-    case 5: colnorm_partial_kernel<5><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
-    case 6: colnorm_partial_kernel<6><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch); break;
+    case 0: colnorm_partial_kernel<0><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
+    case 1: colnorm_partial_kernel<1><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
+    case 2: colnorm_partial_kernel<2><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
+    case 3: colnorm_partial_kernel<3><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
+    case 4: colnorm_partial_kernel<4><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
+    case 5: colnorm_partial_kernel<5><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
+    case 6: colnorm_partial_kernel<6><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
     default: return SVD1_E_INVALID;
   }
-  colnorm_combine_kernel<<<dim3(unsigned((n + 127) / 128), unsigned(ncarry + 1)), 128, 0, st>>>(
-      scratch, ch, ncarry, n, tau, colscale, carry_out, status);
-  *launches += 2;
+  *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

@@ -189,6 +189,7 @@ struct StepRecord {
   }
   // device arrays
   DevBuf d_zhat, d_scratch, d_in, d_out;
+  DevBuf d_ctr;  // last-block counters of the Loewner / norm kernels (kept zero)
   DevBuf blob;  // apply data (Householder groups, column maps, scales, FMM plan): one copy
   int32_t *dgoff = nullptr, *dhcols = nullptr, *dsrc = nullptr, *ddst = nullptr, *dpsrc = nullptr,
           *dpdst = nullptr;
@@ -211,6 +212,7 @@ struct svd1_plan_s {
   int p = 16, leaf = 32;
   uint64_t probe_seed = 0x1707083691234567ull;
   int64_t launches = 0;
+  DevBuf ctr;  // last-block counters for the test hooks (kept zero)
   DevBuf W_u, W_v, proj, partial, status, iters, ops, fmm_cells, fmm_descs, fmm_terms,
       fmm_tasks, scratch_i, scratch_d;
   DevBuf phi[2], psi[2];         // FMM expansions per side (U applies, V applies)
@@ -272,6 +274,16 @@ svd1_status pinned(svd1_plan_t P, size_t doubles, double** out) {
     P->h_pin_cap = doubles * sizeof(double);
   }
   *out = P->h_pin;
+  return SVD1_OK;
+}
+
+// counters for the last-block combines: one int per 64-column block, zeroed when the
+// buffer is (re)allocated; the kernels leave them zero
+svd1_status counters(DevBuf& b, int n, cudaStream_t st, int** out) {
+  const void* before = b.p;
+  const size_t cap0 = b.cap;
+  TRY(b.get<int>(size_t(n / 64 + 16), out));
+  if (b.p != before || b.cap != cap0) SVD1_CUDA_TRY(cudaMemsetAsync(b.p, 0, b.cap, st));
   return SVD1_OK;
 }
 
@@ -1399,10 +1411,11 @@ svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
   // zeroed when (re)allocated: a K chunk may reach past a term into columns no pass wrote
   // (they meet zero op rows, but 0 * NaN would not be 0)
   for (DevBuf* b : {&P->phi[side], &P->psi[side]}) {
-    void* before = b->p;
+    const void* before = b->p;
+    const size_t cap0 = b->cap;  // (a new allocation may reuse the old address)
     double* x;
     TRY(b->get<double>(elems, &x));
-    if (b->p != before) SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, side_stream(P, side)));
+    if (b->p != before || b->cap != cap0) SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, side_stream(P, side)));
   }
   return SVD1_OK;
 }
@@ -1654,6 +1667,8 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   tl_mark(P, "  ev" + std::to_string(ev0) + " uploaded", st);
   double* scr;
   TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
+  int* ctr;
+  TRY(counters(S.d_ctr, na, st, &ctr));
   S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na, side >= 2);  // sides 2, 3: batch mode
   if (S.sec_fmm_used) {  // STEP 2 with the far field by FMM
     SecFmmDev F;
@@ -1664,9 +1679,9 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, st, &P->launches));   // STEP 2
   }
   tl_mark(P, "  ev" + std::to_string(ev0) + " secular done", st);
-  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, st, &P->launches));
+  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, ctr, st, &P->launches));
   tl_mark(P, "  ev" + std::to_string(ev0) + " loewner done", st);
-  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, st, &P->launches));
+  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, ctr, st, &P->launches));
   tl_mark(P, "  ev" + std::to_string(ev0) + " colnorm done", st);
   TRY(ev_record(P, ev0 + 1, st));
   if (words * sizeof(double) > S.rb_cap) {
@@ -2954,7 +2969,9 @@ svd1_status svd1_loewner(svd1_plan_t P, int64_t n, const double* d, const int32_
   if (!P || n < 0 || !d || !k || !tau || !z || !zhat_out || rho == 0.0) return SVD1_E_INVALID;
   double* scr;
   TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr));
-  TRY(loewner(d, k, tau, rho, z, int(n), zhat_out, scr, P->st, &P->launches));
+  int* ctr;
+  TRY(counters(P->ctr, int(n), P->st, &ctr));
+  TRY(loewner(d, k, tau, rho, z, int(n), zhat_out, scr, ctr, P->st, &P->launches));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   return SVD1_OK;
 }
@@ -2970,7 +2987,9 @@ svd1_status svd1_colnorms(svd1_plan_t P, int64_t n, const double* d, const int32
   double* scr;
   TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
-  TRY(colnorm_carry(d, k, tau, zhat, int(n), nullptr, 0, cs, nullptr, dst, scr, P->st, &P->launches));
+  int* ctr;
+  TRY(counters(P->ctr, int(n), P->st, &ctr));
+  TRY(colnorm_carry(d, k, tau, zhat, int(n), nullptr, 0, cs, nullptr, dst, scr, ctr, P->st, &P->launches));
   std::vector<double> h(n);
   SVD1_CUDA_TRY(cudaMemcpyAsync(h.data(), cs, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));

@@ -56,6 +56,10 @@ svd1_status secular_orient(const double* d, const double* z, double rho, int n, 
                            double* z2r, cudaStream_t st, int64_t* launches);
 // scratch (doubles) needed by loewner / colnorm_carry for size n and ncarry vectors
 int64_t spectral_scratch_elems(int n, int ncarry);
+// last-block counters inside that scratch (zero them once when the buffer is allocated;
+// the kernels leave them zero)
+int64_t spectral_counter_offset(int n, int ncarry);
+int* spectral_counters(double* scratch, int n, int ncarry);
 // K2': FMM-accelerated secular evaluation.  Tree over
 // the (oriented) sources; each target cell Y carries local expansions of the far field of
 // the sources left (psiL) and right (psiR) of its target interval [d_lo, d_next]; a root
@@ -92,13 +96,13 @@ svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, co
 
 // K3a: Loewner zhat (thread per i, split-j partial products + ordered combine)
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
-                    const double* z, int n, double* zhat, double* scratch, cudaStream_t st,
+                    const double* z, int n, double* zhat, double* scratch, int* ctr, cudaStream_t st,
                     int64_t* launches);
 // K3b + K12: colscale_j = 1/||c_j|| and carry_out[q][j] = (X^T carry_q)_j
 // (thread per j, split-i partial sums + ordered combine).
 svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
                           const double* zhat, int n, const double* carry, int ncarry,
-                          double* colscale, double* carry_out, int32_t* status, double* scratch,
+                          double* colscale, double* carry_out, int32_t* status, double* scratch, int* ctr,
                           cudaStream_t st, int64_t* launches);
 
 // K11: direct apply  U_out[r, dst[j]] = cs[j] * sum_i U_in[r, src[i]] zhat[i] / ((d_i - d_kj) - tau_j)
