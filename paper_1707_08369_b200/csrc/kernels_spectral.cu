@@ -99,6 +99,52 @@ __global__ void __launch_bounds__(256) proj_partial_kernel(const double* __restr
 }
 
 // out[v*cols + c] = sum over chunks in order (deterministic)
+// M^T x_v for up to MV vectors x_v = X[v * ldx + row0 + r] (a stream's a's or b's): the
+// same row-chunked partial sums as proj_partial_kernel, one pass over M for all of them
+constexpr int kMV = 8;
+__global__ void __launch_bounds__(256) proj_multi_kernel(const double* __restrict__ M, int64_t ld,
+                                                        int64_t rows, int64_t cols,
+                                                        const double* __restrict__ X, int64_t ldx, int nv,
+                                                        int64_t row0, int rows_per_chunk,
+                                                        double* __restrict__ part) {
+  __shared__ double vec[kMV][64];
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r_begin = int64_t(blockIdx.y) * rows_per_chunk;
+  const int64_t r_end = min(rows, r_begin + rows_per_chunk);
+  double acc[kMV];
+#pragma unroll
+  for (int v = 0; v < kMV; ++v) acc[v] = 0.0;
+  for (int64_t rb = r_begin; rb < r_end; rb += 64) {
+    const int nr = int((r_end - rb < 64) ? (r_end - rb) : 64);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nr * kMV; t += blockDim.x) {
+      const int rr = t % nr, v = t / nr;
+      vec[v][rr] = v < nv ? X[int64_t(v) * ldx + row0 + rb + rr] : 0.0;
+    }
+    __syncthreads();
+    if (c < cols) {
+      const double* p = M + rb * ld + c;
+      for (int rr = 0; rr < nr; ++rr, p += ld) {
+        const double m0 = __ldg(p);
+#pragma unroll
+        for (int v = 0; v < kMV; ++v) acc[v] = fma(m0, vec[v][rr], acc[v]);
+      }
+    }
+  }
+  if (c < cols)
+    for (int v = 0; v < nv; ++v) part[(int64_t(blockIdx.y) * nv + v) * cols + c] = acc[v];
+}
+
+// out[v * ostride + c] = sum over chunks (fixed order)
+__global__ void proj_reduce_strided_kernel(const double* __restrict__ part, int nchunks, int nv, int64_t cols,
+                                           double* __restrict__ out, int64_t ostride) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nv * cols) return;
+  double s = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) s += part[int64_t(ch) * nv * cols + t];
+  out[(t / cols) * ostride + t % cols] = s;
+}
+
 __global__ void proj_reduce_kernel(const double* __restrict__ part, int nchunks, int nv,
                                    int64_t cols, double* __restrict__ out) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -806,7 +852,8 @@ constexpr int kDotBlocks = 64;
 int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t n) {
   const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
   const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
-  return cu * 5 * m + cv * n + 6 * kDotBlocks;
+  // (also enough for project_many's 8-vector passes)
+  return std::max(cu * 5 * m + cv * n, std::max(cu * 8 * m, cv * 8 * n)) + 6 * kDotBlocks;
 }
 
 svd1_status fill_probes(uint64_t seed, int64_t row0, int64_t rows, double* g, cudaStream_t st,
@@ -930,6 +977,48 @@ svd1_status gram_rows(int K, const double* B, int64_t ldb, int64_t n, double* gr
   if (K <= 0) return SVD1_OK;
   gram_rows_kernel<<<K * K, 256, 0, st>>>(K, B, ldb, n, gram);
   *launches += 1;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+svd1_status project_many(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
+                         const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0, int64_t vcols,
+                         const double* A, int64_t lda, const double* B, int64_t ldb, int K, const double* probes,
+                         double* part, int64_t partial_cap, double* proj, int64_t nproj, cudaStream_t st,
+                         int64_t* launches) {
+  if (K <= 0) return SVD1_OK;
+  const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
+  const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
+  if (std::max(cu * kMV * m, cv * kMV * n) + 6 * kDotBlocks > partial_cap) return SVD1_E_NOMEM;
+  const int rpc_u = int((u_rows + cu - 1) / cu), rpc_v = int((v_rows + cv - 1) / cv);
+  for (int t0 = 0; t0 < K; t0 += kMV) {
+    const int nv = std::min(kMV, K - t0);
+    if (u_rows > 0) {
+      proj_multi_kernel<<<dim3(unsigned((m + 255) / 256), unsigned(cu)), 256, 0, st>>>(
+          U, ldu, u_rows, m, A + int64_t(t0) * lda, lda, nv, u_row0, rpc_u, part);
+      proj_reduce_strided_kernel<<<unsigned((nv * m + 255) / 256), 256, 0, st>>>(part, int(cu), nv, m,
+                                                                                 proj + int64_t(t0) * nproj, nproj);
+    }
+    if (v_rows > 0) {
+      proj_multi_kernel<<<dim3(unsigned((vcols + 255) / 256), unsigned(cv)), 256, 0, st>>>(
+          V, ldv, v_rows, vcols, B + int64_t(t0) * ldb, ldb, nv, v_row0, rpc_v, part);
+      proj_reduce_strided_kernel<<<unsigned((nv * vcols + 255) / 256), 256, 0, st>>>(
+          part, int(cv), nv, vcols, proj + int64_t(t0) * nproj + 5 * m, nproj);
+    }
+    *launches += 4;
+  }
+  double* part_d = part + std::max(cu * kMV * m, cv * kMV * n);
+  for (int t = 0; t < K; ++t) {  // the dots of every update (and zeros where nothing is projected)
+    double* pt = proj + int64_t(t) * nproj;
+    if (u_rows <= 0) SVD1_CUDA_TRY(cudaMemsetAsync(pt, 0, sizeof(double) * m, st));
+    if (v_rows <= 0 || vcols < n)
+      SVD1_CUDA_TRY(cudaMemsetAsync(pt + 5 * m + (v_rows > 0 ? vcols : 0), 0,
+                                    sizeof(double) * (n - (v_rows > 0 ? vcols : 0)), st));
+    proj_dots_kernel<<<kDotBlocks, 256, 0, st>>>(A + int64_t(t) * lda, u_rows, u_row0, B + int64_t(t) * ldb,
+                                                 v_rows, v_row0, probes, part_d);
+    proj_dots_final<<<1, 32, 0, st>>>(part_d, kDotBlocks, pt + 5 * m + n);
+    *launches += 2;
+  }
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

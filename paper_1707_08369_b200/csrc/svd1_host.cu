@@ -2685,8 +2685,17 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   const size_t nproj = size_t(5 * m + n + 6);
   double* pj;
   TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj));
-  for (int t = 0; t < int(K); ++t)
-    TRY(svd1_project(P, U, ldu, V, ldv, A + int64_t(t) * lda, Bv + int64_t(t) * ldb, pj + size_t(t) * nproj));
+  // update 0 in full (its probe block too), updates 1.. with one pass over U and V per
+  // 8 of them (only their x_a, y_b and dots are used: the probes are carried)
+  TRY(svd1_project(P, U, ldu, V, ldv, A, Bv, pj));
+  if (K > 1) {
+    double* part;
+    const int64_t need = project_partial_elems(c.u_rows, m, c.v_rows, n);
+    TRY(P->partial.get<double>(size_t(need), &part));
+    TRY(project_many(U, ldu, c.u_rows, m, c.u_row0, V, ldv, c.v_rows, n, c.v_row0, thin ? m : n, A + lda, lda,
+                     Bv + ldb, ldb, int(K) - 1, static_cast<double*>(P->probes.p), part, need, pj + nproj,
+                     int64_t(nproj), P->st, &P->launches));
+  }
   return svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, Bv, ldb, K, eps, reps);
 }
 

@@ -36,6 +36,14 @@ __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
 // ---------------------------------------------------------------- kernels
 // K1: partial projections over row chunks.  out layout (length 5m + n + 6):
 // [x_a (m)][x_g0..3 (4m)][y_b (n)][a.g0..3 (4)][a.a][b.b]
+// the projections of K updates (a_t at A + t*lda, b_t at B + t*ldb) against the same
+// factors into proj + t*nproj (svd1_project's layout; the probe block is NOT written):
+// one pass over U (and V) per 8 updates
+svd1_status project_many(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
+                         const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0, int64_t vcols,
+                         const double* A, int64_t lda, const double* B, int64_t ldb, int K, const double* probes,
+                         double* part, int64_t partial_cap, double* proj, int64_t nproj, cudaStream_t st,
+                         int64_t* launches);
 svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
                     const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0,
                     const double* a, const double* b, double* partial_ws, int64_t partial_cap,
