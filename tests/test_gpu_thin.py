@@ -83,3 +83,22 @@ def test_thin_batch_matches_sequential(m, n, K):
     assert float((sb - ss).abs().max()) <= 1e-12 * float(ss[0])
     assert float((Ub - Us).abs().max()) <= 1e-8
     assert float((Vb[:, :m] - Vs[:, :m]).abs().max()) <= 1e-8
+
+
+def test_thin_b_in_span():
+    """b inside span(V[:, :m]): no null-space component (beta_perp = 0), the extra
+    coordinate has zero weight and deflates; same result as the full-V path."""
+    m, n = 48, 160
+    inp = config_inputs(4, m=m, n=n, updates=1)
+    U, s, V = inp["U"], inp["sigma"], inp["V"]
+    a, _ = inp["ab"][0]
+    b = V[:, :m] @ np.random.default_rng(5).standard_normal(m)
+    Uf, sf, Vf = T(U), T(s), T(V)
+    P.Plan(m, n).update(Uf, sf, Vf, T(a), T(b))
+    Ut, st, Vt = T(U), T(s), _thin(V, m)
+    rep = P.Plan(m, n, flags=P.THIN_V).update(Ut, st, Vt, T(a), T(b))
+    torch.cuda.synchronize()
+    assert rep["n_deflated"][2] >= 1
+    assert bool(torch.isfinite(Vt).all())
+    assert float((sf - st).abs().max()) <= 1e-12 * float(sf[0])
+    assert float((Uf - Ut).abs().max()) <= 1e-8 and float((Vf[:, :m] - Vt[:, :m]).abs().max()) <= 1e-8
