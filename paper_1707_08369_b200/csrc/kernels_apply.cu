@@ -384,9 +384,12 @@ __device__ __forceinline__ double2 lds128(const unsigned char* p) {
 #ifndef SVD1_CW16
 #define SVD1_CW16 4  // consumer warps of the 16-wide passes (experiments)
 #endif
+#ifndef SVD1_CW32
+#define SVD1_CW32 4  // consumer warps of the 32-wide passes (experiments)
+#endif
 template <int BN>
 struct GemmCfg {
-  static constexpr int CW = BN <= 16 ? SVD1_CW16 : 4;  // consumer warps (32 rows each)
+  static constexpr int CW = BN <= 16 ? SVD1_CW16 : SVD1_CW32;  // consumer warps (32 rows each)
   static constexpr int NTHR = 32 * (CW + 1); // + one producer warp
   static constexpr int NT = BN / 8;
   static constexpr int BM = 32 * CW;

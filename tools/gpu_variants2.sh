@@ -1,7 +1,7 @@
 #!/bin/bash
 # build variants of the GEMM kernel config and bench each (experiments)
 cd "$(dirname "$0")/.."
-for v in "" "-DSVD1_CW16=8 -DSVD1_STAGES16=3" "-DSVD1_CW16=8 -DSVD1_STAGES16=2" "-DSVD1_CW16=2 -DSVD1_STAGES16=6"; do
+for v in ${VARIANTS:-""}; do
   rm -f paper_1707_08369_b200/libsvd1.so
   SVD1_NVCC_EXTRA="$v" python paper_1707_08369_b200/build.py > gpurun_out/build_v.log 2>&1 || { echo "build failed $v"; continue; }
   for i in 1 2; do
