@@ -1060,20 +1060,20 @@ static int inner_chunks(int n, int threads) {
   return ch;
 }
 
-// the last-block counters at the end of a spectral scratch buffer
-int64_t spectral_counter_offset(int n, int ncarry) {
-  const int ch = std::max(inner_chunks(n, kLT), inner_chunks(n, kCT));
-  return int64_t(ch) * n * (ncarry + 2) + 16;
+// the Loewner kernel is latency-bound (a running product with renormalisation): more
+// j chunks, so more warps per SM, than the norm kernel
+static int loewner_chunks(int n) {
+  const int outer = (n + kLT - 1) / kLT;
+  int ch = (16 * 148 + outer - 1) / outer;
+  return std::max(1, std::min(ch, (n + 63) / 64));
 }
-int* spectral_counters(double* scratch, int n, int ncarry) {
-  return reinterpret_cast<int*>(scratch + spectral_counter_offset(n, ncarry));
-}
+
+
 
 
 int64_t spectral_scratch_elems(int n, int ncarry) {
-  const int ch = std::max(inner_chunks(n, kLT), inner_chunks(n, kCT));
-  // partials, then the last-block counters (one int per column block; zero between uses)
-  return int64_t(ch) * n * (ncarry + 2) + 16 + (n + 63) / 64 + 16;
+  const int ch = std::max(loewner_chunks(n), inner_chunks(n, kCT));
+  return int64_t(ch) * n * (ncarry + 2) + 16;
 }
 
 svd1_status secular_orient(const double* d, const double* z, double rho, int n, double* dr,
@@ -1089,7 +1089,7 @@ svd1_status loewner(const double* d, const int32_t* k, const double* tau, double
                     const double* z, int n, double* zhat, double* scratch, int* ctr, cudaStream_t st,
                     int64_t* launches) {
   if (n <= 0) return SVD1_OK;
-  const int ch = inner_chunks(n, kLT);
+  const int ch = loewner_chunks(n);
   const int chunk = (n + ch - 1) / ch;
   double* pm = scratch;
   int32_t* pe = reinterpret_cast<int32_t*>(scratch + int64_t(ch) * n);

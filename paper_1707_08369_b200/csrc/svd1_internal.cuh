@@ -64,10 +64,6 @@ svd1_status secular_orient(const double* d, const double* z, double rho, int n, 
                            double* z2r, cudaStream_t st, int64_t* launches);
 // scratch (doubles) needed by loewner / colnorm_carry for size n and ncarry vectors
 int64_t spectral_scratch_elems(int n, int ncarry);
-// last-block counters inside that scratch (zero them once when the buffer is allocated;
-// the kernels leave them zero)
-int64_t spectral_counter_offset(int n, int ncarry);
-int* spectral_counters(double* scratch, int n, int ncarry);
 // K2': FMM-accelerated secular evaluation.  Tree over
 // the (oriented) sources; each target cell Y carries local expansions of the far field of
 // the sources left (psiL) and right (psiR) of its target interval [d_lo, d_next]; a root
