@@ -601,7 +601,10 @@ svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,
 // part[s][r][j] = sum_{i in split s} U_in[r, src_i] zhat_i / ((d_i - d_kj) - tau_j): thread
 // per target j (128 per block), the split's sources staged 32 at a time with their rows;
 // RB = rows rounded up (registers).  Then U_out[r, dst_j] = cs_j sum_s part[s][r][j].
-constexpr int kFewSplitChunk = 128;  // sources per split (many blocks: latency-bound work)
+#ifndef SVD1_FEW_CHUNK
+#define SVD1_FEW_CHUNK 256
+#endif
+constexpr int kFewSplitChunk = SVD1_FEW_CHUNK;  // sources per split (many blocks: latency-bound work)
 
 __device__ __forceinline__ double few_rcp(double x) {  // 1/x to ~1 ulp: MUFU seed + 2 Newton steps
   double y;
