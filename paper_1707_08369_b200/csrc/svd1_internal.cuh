@@ -69,7 +69,10 @@ int64_t spectral_scratch_elems(int n, int ncarry);
 // the sources left (psiL) and right (psiR) of its target interval [d_lo, d_next]; a root
 // in leaf Y sums its near-leaf sources directly (exact left/right split) and evaluates
 // the two polynomials, so an evaluation costs O(near + p) instead of O(n).
-constexpr int kSecP = 20;  // Chebyshev order of the secular far field
+#ifndef SVD1_SECP
+#define SVD1_SECP 20
+#endif
+constexpr int kSecP = SVD1_SECP;  // Chebyshev order of the secular far field
 struct SecFmmCell {        // heap-ordered; empty cells have lo == hi
   int32_t lo, hi;          // source index range
   int32_t m2l_off;         // partners m2l[m2l_off .. next cell's m2l_off)
