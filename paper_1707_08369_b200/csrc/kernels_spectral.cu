@@ -366,18 +366,20 @@ struct FarEval {
     }
     const int cell = F->leaf_cell[q];
     const SecFmmCell C = F->cells[cell];
-    double t = ((dk - C.ct) + tau) / C.rt;
+    const double irt = fast_rcp(C.rt);  // (MUFU + Newton: no IEEE division in the loop)
+    double t = ((dk - C.ct) + tau) * irt;
     double nl = 0.0, nr = 0.0, den = 0.0, dnl = 0.0, dnr = 0.0, dden = 0.0;
     if (lane < kSecP) {
       double dx = t - tk;
       if (dx == 0.0) dx = 0x1.0p-50 * (1.0 + fabs(t));  // exact node: an ulp-scale nudge
-      const double qk = wk / dx, pl = F->psiL[cell * kSecP + lane], pr = F->psiR[cell * kSecP + lane];
+      const double idx = fast_rcp(dx);
+      const double qk = wk * idx, pl = F->psiL[cell * kSecP + lane], pr = F->psiR[cell * kSecP + lane];
       den = qk;
       nl = pl * qk;
       nr = pr * qk;
-      dden = -qk / dx;
-      dnl = -nl / dx;
-      dnr = -nr / dx;
+      dden = -qk * idx;
+      dnl = -nl * idx;
+      dnr = -nr * idx;
     }
     a.psi = warp_sum(a.psi);
     a.phi = warp_sum(a.phi);
@@ -389,11 +391,11 @@ struct FarEval {
     dnl = warp_sum(dnl);
     dnr = warp_sum(dnr);
     dden = warp_sum(dden);
-    const double id = 1.0 / den;
+    const double id = fast_rcp(den);
     a.psi += nl * id;
     a.phi += nr * id;
-    a.dpsi += (dnl * den - nl * dden) * id * id / C.rt;
-    a.dphi += (dnr * den - nr * dden) * id * id / C.rt;
+    a.dpsi += (dnl * den - nl * dden) * id * id * irt;
+    a.dphi += (dnr * den - nr * dden) * id * id * irt;
     a.eabs = fabs(a.psi) + fabs(a.phi);
     return a;
   }
