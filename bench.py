@@ -447,6 +447,7 @@ def main():
                            "thin_v": thin},
                 "sequential_api": seq,
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+                "allocations_in_timed_region": sum(r.get("allocations", 0) for r in reps),
                 "cpu_baseline": cpu, "check": check,
                 "spectral_ms_per_step": sp_ms / args.steps, "apply_ms_per_step": ap_ms / args.steps,
                 "host_phase_ms": [sum(r["t_ms"][i] for r in reps) / args.steps for i in range(5)]}

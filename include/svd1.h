@@ -106,10 +106,20 @@ typedef struct {
   double gemm_ms[4];     /* device time of each apply's FMM GEMM passes (CUDA events around
                             every pass launch on its stream) when the environment variable
                             SVD1_GEMM_EVENTS is set (diagnostics), else 0 */
+  int64_t allocations;   /* device / pinned-host allocations the library made during this
+                            update (0 in steady state: every workspace is sized by
+                            svd1_plan_create; a buffer that depends on the FMM tree and
+                            outgrows its create-time estimate grows once, stream-ordered) */
 } svd1_report;
 
-/* Plan: owns workspaces on the device (sized for u_rows x m and v_rows x n),
- * host scratch and the probe seed.  Returns SVD1_E_INVALID for bad sizes. */
+/* Plan: owns every workspace, allocated HERE (FMM STEPS 1-2 fix p, s and
+ * the tree depth up front): W (u_rows x m, v_rows x n), the FMM expansions
+ * Phi/Psi of both sides for the deepest tree the planner can choose at this eps
+ * (rows x cells x p), the batch mode's carried rows and projections, the step records'
+ * spectral buffers, pinned read-back and upload staging.  Updates allocate nothing
+ * (svd1_report.allocations; stream-ordered growth only if a call's eps is smaller than
+ * the plan's or a tree-dependent estimate is exceeded).  Returns SVD1_E_INVALID for bad
+ * sizes, SVD1_E_NOMEM if the workspaces do not fit. */
 svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out);
 svd1_status svd1_plan_destroy(svd1_plan_t plan);
 

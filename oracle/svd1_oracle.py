@@ -16,14 +16,21 @@ every function here has at least one (DESIGN.md §3.3 lists them).
 """
 from __future__ import annotations
 
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 import math
+import os
 
 import numpy as np
 
 EPS = 2.0 ** -52  # fp64 unit roundoff x2 (machine epsilon)
 
 _CHUNK_ELEMS = 1 << 22  # bound the n x n temporaries of the vectorised loops
+# Independent roots are evaluated in parallel threads (numpy releases the GIL inside its
+# loops).  Each root's sum is formed by the same numpy reduction over the same row
+# whatever the chunking, so the results are bitwise those of one thread
+# (tests/test_oracle_pins.py::test_threaded_evaluation_is_bitwise_serial).
+THREADS = max(1, int(os.environ.get("SVD1_ORACLE_THREADS", os.cpu_count() or 1)))
 
 
 # --------------------------------------------------------------------------- 2x2
@@ -167,10 +174,21 @@ def deflate(d, z, rho):
 
 
 # ----------------------------------------------------------- secular equation
-def _chunks(n_rows, n_cols):
-    step = max(1, _CHUNK_ELEMS // max(1, n_cols))
+def _chunks(n_rows, n_cols, parts=1):
+    step = max(1, min(_CHUNK_ELEMS // max(1, n_cols), -(-n_rows // parts)))
     for s in range(0, n_rows, step):
         yield slice(s, min(n_rows, s + step))
+
+
+def _for_chunks(fn, n_rows, n_cols):
+    """fn(slice) for row chunks of an n_rows x n_cols evaluation, on THREADS threads."""
+    chunks = list(_chunks(n_rows, n_cols, THREADS))
+    if THREADS == 1 or len(chunks) == 1:
+        for sl in chunks:
+            fn(sl)
+        return
+    with ThreadPoolExecutor(THREADS) as ex:
+        list(ex.map(fn, chunks))
 
 
 def secular_w(d, z, rho, k, tau):
@@ -182,10 +200,12 @@ def secular_w(d, z, rho, k, tau):
     k = np.asarray(k)
     tau = np.asarray(tau, np.float64)
     out = np.empty(tau.size)
-    for sl in _chunks(tau.size, d.size):
+
+    def chunk(sl):
         delta = (d[None, :] - d[k[sl]][:, None]) - tau[sl, None]
         with np.errstate(divide="ignore", invalid="ignore"):
             out[sl] = 1.0 + rho * np.sum(z2[None, :] / delta, axis=1)
+    _for_chunks(chunk, tau.size, d.size)
     return out
 
 

@@ -32,7 +32,8 @@ class Report(C.Structure):
                 ("sign_flips", i32), ("noop", i32), ("kernel_launches", i64),
                 ("apply_ms", dbl * 4), ("apply_flops", dbl * 4), ("spectral_ms", dbl * 4),
                 ("fmm_levels", i32 * 4), ("fmm_max_near", i32 * 4), ("mean_iter", dbl * 4),
-                ("pair_rotations", i32), ("apply_flops_exec", dbl * 4), ("gemm_ms", dbl * 4)]
+                ("pair_rotations", i32), ("apply_flops_exec", dbl * 4), ("gemm_ms", dbl * 4),
+                ("allocations", i64)]
 
     def as_dict(self):
         return dict(t_ms=list(self.t_ms)[:7], n_active=list(self.n_active),
@@ -43,7 +44,8 @@ class Report(C.Structure):
                     apply_flops=list(self.apply_flops), spectral_ms=list(self.spectral_ms),
                     fmm_levels=list(self.fmm_levels), fmm_max_near=list(self.fmm_max_near),
                     mean_iter=list(self.mean_iter), pair_rotations=self.pair_rotations,
-                    apply_flops_exec=list(self.apply_flops_exec), gemm_ms=list(self.gemm_ms))
+                    apply_flops_exec=list(self.apply_flops_exec), gemm_ms=list(self.gemm_ms),
+                    allocations=self.allocations)
 
 
 def _sig(name, args):

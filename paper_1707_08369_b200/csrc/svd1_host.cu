@@ -25,41 +25,102 @@ double now_ms() {
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
+// Allocations made by the library (device, stream-ordered pool, pinned host) since the
+// process started: svd1_report.allocations is the difference over one call.  The plan
+// sizes its workspaces at creation (svd1_plan_create), so an update allocates only if its
+// FMM plan outgrows the create-time estimate of a plan-dependent buffer.
+std::atomic<int64_t> g_allocs{0};
+
 // grow-only device buffer
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool pooled = false;  // from cudaMallocAsync (stream-ordered pool)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, nullptr);
+      else cudaFree(p);
+    }
   }
-  // Grows geometrically; frees with the legacy (device-wide) semantics only on growth,
-  // which after the first calls of a stream of updates no longer happens.
+  // Create-time sizing (and the test hooks): cudaMalloc of exactly `count` elements.
   template <class T>
-  svd1_status get(size_t count, T** out) {
+  svd1_status reserve(size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (bytes <= cap) return SVD1_OK;
+    release();
+    ++g_allocs;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      return SVD1_E_NOMEM;
+    }
+    cap = bytes;
+    return SVD1_OK;
+  }
+  void release() {
+    if (p) {
+      if (pooled) cudaFreeAsync(p, nullptr);
+      else cudaFree(p);
+    }
+    p = nullptr;
+    cap = 0;
+    pooled = false;
+  }
+  // Inside an update: a buffer that outgrows its create-time size grows geometrically
+  // in stream order on `st` (the stream of its first use; cudaFreeAsync / cudaMallocAsync
+  // from the device's pool): no device-wide synchronisation.
+  template <class T>
+  svd1_status get(size_t count, T** out, cudaStream_t st) {
     const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
     if (bytes > cap) {
       const size_t want = std::max(bytes + bytes / 2, size_t(4096));
-      if (p) cudaFree(p);
+      if (p) {
+        if (pooled) cudaFreeAsync(p, st);
+        else cudaFree(p);  // (a create-time buffer that was too small: one-off)
+      }
       p = nullptr;
       cap = 0;
-      if (cudaMalloc(&p, want) != cudaSuccess) {
+      ++g_allocs;
+      if (cudaMallocAsync(&p, want, st) != cudaSuccess) {
         cudaGetLastError();
-        if (cudaMalloc(&p, bytes) != cudaSuccess) {
-          cudaGetLastError();
-          return SVD1_E_NOMEM;
-        }
-        cap = bytes;
-      } else {
-        cap = want;
+        p = nullptr;
+        return SVD1_E_NOMEM;
       }
+      pooled = true;
+      cap = want;
     }
     *out = static_cast<T*>(p);
     return SVD1_OK;
   }
+  // sized at creation: never grows
+  template <class T>
+  svd1_status get_fixed(size_t count, T** out) {
+    if (std::max<size_t>(count, 1) * sizeof(T) > cap) return SVD1_E_NOMEM;
+    *out = static_cast<T*>(p);
+    return SVD1_OK;
+  }
 };
+
+// pinned host buffer sized at creation (grows, counted, only if an estimate was short)
+svd1_status pinned_reserve(void** buf, size_t* cap, size_t bytes) {
+  if (bytes <= *cap) return SVD1_OK;
+  if (*buf) cudaFreeHost(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  ++g_allocs;
+  if (cudaMallocHost(buf, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    *buf = nullptr;
+    return SVD1_E_NOMEM;
+  }
+  *cap = bytes;
+  return SVD1_OK;
+}
+
+constexpr int kMaxBatch = 28;  // svd1_update_batch: buffers are sized for this many updates per call
 
 #define TRY(expr)                       \
   do {                                  \
@@ -126,6 +187,7 @@ struct CauchyPrep {
   int32_t* dcol2src = nullptr;
   size_t o_cells = 0, o_descs = 0, o_terms = 0, o_tasks = 0, o_c2s = 0;
   FmmMaps* h_maps = nullptr;  // pinned staging of the TMA descriptors (copied on the apply stream)
+  size_t h_maps_cap = 0;
   std::vector<cudaEvent_t> gev;  // events around each GEMM pass of the last launch
   int ngev = 0;
   ~CauchyPrep() {
@@ -263,16 +325,9 @@ struct svd1_plan_s {
 namespace {
 
 svd1_status pinned(svd1_plan_t P, size_t doubles, double** out) {
-  if (doubles * sizeof(double) > P->h_pin_cap) {
-    if (P->h_pin) cudaFreeHost(P->h_pin);
-    P->h_pin = nullptr;
-    P->h_pin_cap = 0;
-    if (cudaMallocHost(&P->h_pin, doubles * sizeof(double)) != cudaSuccess) {
-      cudaGetLastError();
-      return SVD1_E_NOMEM;
-    }
-    P->h_pin_cap = doubles * sizeof(double);
-  }
+  void* b = P->h_pin;
+  TRY(pinned_reserve(&b, &P->h_pin_cap, doubles * sizeof(double)));  // sized at creation
+  P->h_pin = static_cast<double*>(b);
   *out = P->h_pin;
   return SVD1_OK;
 }
@@ -282,7 +337,7 @@ svd1_status pinned(svd1_plan_t P, size_t doubles, double** out) {
 svd1_status counters(DevBuf& b, int n, cudaStream_t st, int** out) {
   const void* before = b.p;
   const size_t cap0 = b.cap;
-  TRY(b.get<int>(size_t(n / 64 + 16), out));
+  TRY(b.get<int>(size_t(n / 64 + 16), out, st));
   if (b.p != before || b.cap != cap0) SVD1_CUDA_TRY(cudaMemsetAsync(b.p, 0, b.cap, st));
   return SVD1_OK;
 }
@@ -331,16 +386,10 @@ svd1_status arena_reserve(svd1_plan_t P, int side, size_t bytes, size_t* off_out
   size_t off = (A.used + 255) & ~size_t(255);
   if (off + bytes > A.cap) {
     TRY(arena_reset(P, side));  // everything staged so far has been consumed
-    if (bytes > A.cap) {
-      if (A.buf) cudaFreeHost(A.buf);
-      A.buf = nullptr;
-      A.cap = 0;
-      const size_t cap = std::max<size_t>(bytes * 2, size_t(4) << 20);
-      if (cudaMallocHost(&A.buf, cap) != cudaSuccess) {
-        cudaGetLastError();
-        return SVD1_E_NOMEM;
-      }
-      A.cap = cap;
+    if (bytes > A.cap) {  // sized at creation; an outgrown estimate reallocates (counted)
+      void* b = A.buf;
+      TRY(pinned_reserve(&b, &A.cap, std::max<size_t>(bytes * 2, size_t(4) << 20)));
+      A.buf = static_cast<char*>(b);
     }
     off = 0;
   }
@@ -386,7 +435,7 @@ struct BlobBuilder {
 
 svd1_status arena_put_blob(svd1_plan_t P, const BlobBuilder& B, DevBuf& dev, char** out, int side = 0) {
   TRY(ensure_side(P, side));
-  TRY(dev.get<char>(std::max<size_t>(B.total, 1), out));
+  TRY(dev.get<char>(std::max<size_t>(B.total, 1), out, side_stream(P, side)));
   if (B.total == 0) return SVD1_OK;
   size_t off;
   TRY(arena_reserve(P, side, B.total, &off));
@@ -469,7 +518,8 @@ double ev_ms(svd1_plan_t P, int a, int b) {
 
 template <class T>
 svd1_status upload(svd1_plan_t P, DevBuf& buf, const std::vector<T>& v, T** out, int side = 0) {
-  TRY(buf.get<T>(v.size(), out));
+  TRY(ensure_side(P, side));
+  TRY(buf.get<T>(v.size(), out, side_stream(P, side)));
   if (!v.empty()) TRY(arena_put(P, v.data(), v.size() * sizeof(T), *out, side));
   return SVD1_OK;
 }
@@ -1171,6 +1221,26 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
     }
 }
 
+int apply_leaf(int p) {
+  int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2 (P:706): s ~ 2p, capped by the tile
+  if (const char* e = std::getenv("SVD1_LEAF")) leaf = std::max(4, std::min(kMaxLeaf, atoi(e)));  // tuning
+  return leaf;
+}
+
+// Cells of the deepest tree fmm_build_host can choose for na <= N active points: depth
+// L0 + 2, L0 the smallest depth with <= 2 leaf merged points per leaf (STEP 2).
+int64_t max_cells(int64_t N, int leaf) {
+  int L0 = 0;
+  while ((2 * std::max<int64_t>(N, 1) + (int64_t(1) << L0) - 1) / (int64_t(1) << L0) > 2 * leaf) ++L0;
+  const int L = std::min(L0 + 2, 22);
+  return (int64_t(1) << (L + 1)) - 1;
+}
+
+// Expansion workspace (Phi or Psi) of one side: rows x (cells * p) doubles
+size_t expansion_elems(int64_t rows, int64_t N, int p) {
+  return size_t(std::max<int64_t>(rows, 1)) * size_t(max_cells(N, apply_leaf(p))) * size_t(p);
+}
+
 // Cauchy apply of one step, split in a host phase (decide FMM vs direct, build the
 // tree and task lists, stage their upload) and a launch phase (operators + passes).
 // U_out[:, dst[j]] = cs_j sum_i U_in[:, src[i]] zhat_i / ((d_i - d_kj) - tau_j)
@@ -1182,8 +1252,7 @@ void cauchy_plan(const svd1_config& cfg, CauchyPrep& C, int64_t rows, int na,
                  const std::vector<double>& da, const std::vector<double>& mu, int p,
                  const int32_t* src, int n_in) {
   const int minn = cfg.fmm_min_n > 0 ? cfg.fmm_min_n : 384;
-  int leaf = std::min(2 * p, kMaxLeaf);  // STEP 2 (P:706): s ~ 2p, capped by the tile
-  if (const char* e = std::getenv("SVD1_LEAF")) leaf = std::max(4, std::min(kMaxLeaf, atoi(e)));  // tuning
+  const int leaf = apply_leaf(p);
   bool fmm = (cfg.flags & SVD1_FORCE_FMM) ? (na > leaf) : (na >= minn);
   if (cfg.flags & SVD1_FORCE_DIRECT) fmm = false;
   C.fmm = fmm;
@@ -1214,7 +1283,7 @@ void cauchy_stage(CauchyPrep& C, BlobBuilder& B) {
   C.o_c2s = B.add(C.col2src);
 }
 
-svd1_status cauchy_bind(CauchyPrep& C, char* base) {
+svd1_status cauchy_bind(CauchyPrep& C, char* base, cudaStream_t st) {
   if (!C.fmm) return SVD1_OK;
   C.dcells = reinterpret_cast<FmmCell*>(base + C.o_cells);
   C.ddescs = reinterpret_cast<FmmOpDesc*>(base + C.o_descs);
@@ -1222,7 +1291,7 @@ svd1_status cauchy_bind(CauchyPrep& C, char* base) {
   C.dtasks = reinterpret_cast<FmmTask*>(base + C.o_tasks);
   C.dcol2src = C.col2src.empty() ? nullptr : reinterpret_cast<int32_t*>(base + C.o_c2s);
   double* ops;
-  TRY(C.d_ops.get<double>(size_t(std::max<int64_t>(C.F.ops_rows, 1)) * 16, &ops));
+  TRY(C.d_ops.get<double>(size_t(std::max<int64_t>(C.F.ops_rows, 1)) * 16, &ops, st));
   return SVD1_OK;
 }
 
@@ -1232,7 +1301,7 @@ svd1_status cauchy_upload(svd1_plan_t P, CauchyPrep& C) {
   cauchy_stage(C, B);
   char* base;
   TRY(arena_put_blob(P, B, C.blob, &base));
-  return cauchy_bind(C, base);
+  return cauchy_bind(C, base, P->st);
 }
 
 svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
@@ -1257,8 +1326,8 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   const int p = C.p;
   double *phi, *psi;
   const size_t exp_elems = cauchy_exp_elems(C);
-  TRY(P->phi[side].get<double>(exp_elems, &phi));  // sized beforehand (no realloc here)
-  TRY(P->psi[side].get<double>(exp_elems, &psi));
+  TRY(P->phi[side].get<double>(exp_elems, &phi, st));  // sized at creation (no growth here)
+  TRY(P->psi[side].get<double>(exp_elems, &psi, st));
   const int64_t ldE = int64_t(F.ncells) * p;
   FmmCell* dc = C.dcells;
   FmmOpDesc* dd = C.ddescs;
@@ -1274,7 +1343,7 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   if ((reinterpret_cast<uintptr_t>(U_in) & 15) || (ld_in & 1)) {
     const int64_t ldp = (C.n_in + 1) & ~int64_t(1);
     double* pad;
-    TRY(P->upad[side].get<double>(size_t(rows) * size_t(ldp), &pad));
+    TRY(P->upad[side].get<double>(size_t(rows) * size_t(ldp), &pad, st));
     SVD1_CUDA_TRY(cudaMemcpy2DAsync(pad, size_t(ldp) * 8, U_in, size_t(ld_in) * 8, size_t(C.n_in) * 8,
                                     size_t(rows), cudaMemcpyDeviceToDevice, st));
     U_in = pad;
@@ -1282,13 +1351,14 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   }
   // descriptors live in global memory (one copy per apply, written on the apply's own
   // stream; the kernel acquires them through the tensormap proxy before use)
-  if (!C.h_maps && cudaMallocHost(&C.h_maps, sizeof(FmmMaps)) != cudaSuccess) {
-    cudaGetLastError();
-    return SVD1_E_NOMEM;
+  {
+    void* hm = C.h_maps;  // sized at creation
+    TRY(pinned_reserve(&hm, &C.h_maps_cap, sizeof(FmmMaps)));
+    C.h_maps = static_cast<FmmMaps*>(hm);
   }
   TRY(fmm_make_maps(C.h_maps, rows, U_in, C.n_in, ld_in, phi, psi, ldE));
   FmmMaps* maps;
-  TRY(C.d_maps.get<FmmMaps>(1, &maps));
+  TRY(C.d_maps.get<FmmMaps>(1, &maps, st));
   SVD1_CUDA_TRY(cudaMemcpyAsync(maps, C.h_maps, sizeof(FmmMaps), cudaMemcpyHostToDevice, st));
   const bool dbg = std::getenv("SVD1_DEBUG") != nullptr;
   if (dbg) {  // host-side validation of the task lists
@@ -1409,13 +1479,16 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
 
 svd1_status ensure_expansions(svd1_plan_t P, int side, size_t elems) {
   // zeroed when (re)allocated: a K chunk may reach past a term into columns no pass wrote
-  // (they meet zero op rows, but 0 * NaN would not be 0)
+  // (they meet zero op rows, but 0 * NaN would not be 0).  Sized for the deepest tree at
+  // creation; growth (a smaller eps than the plan's, or the standalone apply's sizes) is
+  // stream-ordered on the side's apply stream, behind the applies that used the old buffer.
+  const cudaStream_t st = side_stream(P, side);
   for (DevBuf* b : {&P->phi[side], &P->psi[side]}) {
     const void* before = b->p;
     const size_t cap0 = b->cap;  // (a new allocation may reuse the old address)
     double* x;
-    TRY(b->get<double>(elems, &x));
-    if (b->p != before || b->cap != cap0) SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, side_stream(P, side)));
+    TRY(b->get<double>(elems, &x, st));
+    if (b->p != before || b->cap != cap0) SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, st));
   }
   return SVD1_OK;
 }
@@ -1470,7 +1543,7 @@ svd1_status secfmm_prepare(svd1_plan_t P, SecPlanHost& H, DevBuf& blob, DevBuf& 
   char* base;
   TRY(arena_put_blob(P, B, blob, &base, side));
   double* sc;
-  TRY(scr.get<double>(size_t(3) * H.ncells * kSecP, &sc));
+  TRY(scr.get<double>(size_t(3) * H.ncells * kSecP, &sc, side_stream(P, side)));
   SecFmmDev F;
   F.L = H.L;
   F.ncells = H.ncells;
@@ -1624,8 +1697,8 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
   double* din;
   double* dout;
-  TRY(S.d_in.get<double>(in_words, &din));
-  TRY(S.d_out.get<double>(words, &dout));
+  TRY(S.d_in.get<double>(in_words, &din, st));
+  TRY(S.d_out.get<double>(words, &dout, st));
   double* stage;  // built in place in the pinned arena (no intermediate copies)
   size_t stage_off;
   {
@@ -1661,12 +1734,12 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   int32_t* dit = reinterpret_cast<int32_t*>(dout + size_t(3 + nc) * na);
   int32_t* dst = reinterpret_cast<int32_t*>(dout + words - 1);
   double* dzh;
-  TRY(S.d_zhat.get<double>(na, &dzh));
+  TRY(S.d_zhat.get<double>(na, &dzh, st));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), st));
   TRY(ev_record(P, ev0, st));
   tl_mark(P, "  ev" + std::to_string(ev0) + " uploaded", st);
   double* scr;
-  TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr));
+  TRY(S.d_scratch.get<double>(size_t(spectral_scratch_elems(na, nc)), &scr, st));
   int* ctr;
   TRY(counters(S.d_ctr, na, st, &ctr));
   S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na, side >= 2);  // sides 2, 3: batch mode
@@ -1684,15 +1757,10 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, ctr, st, &P->launches));
   tl_mark(P, "  ev" + std::to_string(ev0) + " colnorm done", st);
   TRY(ev_record(P, ev0 + 1, st));
-  if (words * sizeof(double) > S.rb_cap) {
-    if (S.rb) cudaFreeHost(S.rb);
-    S.rb = nullptr;
-    S.rb_cap = 0;
-    if (cudaMallocHost(&S.rb, words * sizeof(double)) != cudaSuccess) {
-      cudaGetLastError();
-      return SVD1_E_NOMEM;
-    }
-    S.rb_cap = words * sizeof(double);
+  {
+    void* rb = S.rb;  // sized at creation
+    TRY(pinned_reserve(&rb, &S.rb_cap, words * sizeof(double)));
+    S.rb = static_cast<double*>(rb);
   }
   SVD1_CUDA_TRY(cudaMemcpyAsync(S.rb, dout, words * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (!S.done_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&S.done_ev, cudaEventDisableTiming));
@@ -1865,7 +1933,7 @@ svd1_status upload_fmm(svd1_plan_t P, StepRecord& S, int side) {
   cauchy_stage(S.cp, B);
   char* base;
   TRY(arena_put_blob(P, B, S.cp.blob, &base, side));
-  return cauchy_bind(S.cp, base);
+  return cauchy_bind(S.cp, base, side_stream(P, side));
 }
 
 svd1_status apply_upload(svd1_plan_t P, StepRecord& S, int side) {
@@ -1887,7 +1955,7 @@ svd1_status apply_upload(svd1_plan_t P, StepRecord& S, int side) {
   S.dpsrc = reinterpret_cast<int32_t*>(base + o_ps);
   S.dpdst = reinterpret_cast<int32_t*>(base + o_pd);
   S.dpscale = reinterpret_cast<double*>(base + o_pc);
-  if (S.na > 0) TRY(cauchy_bind(S.cp, base));
+  if (S.na > 0) TRY(cauchy_bind(S.cp, base, side_stream(P, side)));
   return SVD1_OK;
 }
 
@@ -1959,6 +2027,120 @@ bool all_finite(const double* x, size_t n) {
   return true;
 }
 
+// ---- create-time workspaces ("the plan owns its workspace, sized at create
+// time").  Sizes depend on (m, n, row blocks, p) only; the FMM plan's own arrays (operator
+// blocks, interaction lists) depend on the tree and get a generous estimate here: an
+// update that outgrows one grows it in stream order (no device synchronisation) and
+// reports it in svd1_report.allocations.
+size_t fmm_blob_estimate(int64_t N, int p) {
+  const int64_t cells = max_cells(N, apply_leaf(p));
+  return size_t(cells) * 2048 + size_t(N) * 8 + (size_t(64) << 10);
+}
+size_t ops_estimate(int64_t N) { return size_t(std::max<int64_t>(N, 64)) * 1024 + (size_t(64) << 10); }
+size_t maps_blob_bytes(int64_t N) { return size_t(N + 1) * 48 + 4096; }  // upload_maps / apply_upload
+
+svd1_status reserve_step(StepRecord& S, int64_t N, int p) {
+  const int nc = kMaxCarry;
+  TRY(S.d_in.reserve<double>(size_t(N) * (4 + nc)));
+  TRY(S.d_out.reserve<double>(size_t(N) * (3 + nc) + size_t(N + 1) / 2 + 2));
+  TRY(S.d_zhat.reserve<double>(size_t(N)));
+  TRY(S.d_scratch.reserve<double>(size_t(spectral_scratch_elems(int(N), nc))));
+  TRY(S.d_ctr.reserve<int>(size_t(N / 64 + 16)));
+  SVD1_CUDA_TRY(cudaMemset(S.d_ctr.p, 0, S.d_ctr.cap));
+  {
+    void* rb = S.rb;
+    TRY(pinned_reserve(&rb, &S.rb_cap, (size_t(N) * (3 + nc) + size_t(N + 1) / 2 + 2) * sizeof(double)));
+    S.rb = static_cast<double*>(rb);
+  }
+  TRY(S.blob.reserve<char>(maps_blob_bytes(N) + fmm_blob_estimate(N, p)));
+  TRY(S.cp.blob.reserve<char>(fmm_blob_estimate(N, p)));
+  TRY(S.cp.d_ops.reserve<double>(ops_estimate(N)));
+  TRY(S.cp.d_maps.reserve<FmmMaps>(1));
+  {
+    void* hm = S.cp.h_maps;
+    TRY(pinned_reserve(&hm, &S.cp.h_maps_cap, sizeof(FmmMaps)));
+    S.cp.h_maps = static_cast<FmmMaps*>(hm);
+  }
+  TRY(S.sec_blob.reserve<char>(size_t(N) * 64 + (size_t(64) << 10)));
+  TRY(S.sec_scr.reserve<double>(size_t(3) * size_t(N + 64) * kSecP));
+  TRY(S.rot_goff.reserve<int32_t>(size_t(N / 2 + 2)));
+  TRY(S.rot_cols.reserve<int32_t>(size_t(N + 1)));
+  TRY(S.rot_mats.reserve<double>(size_t(N) * kNumProbes + 16));
+  return SVD1_OK;
+}
+
+svd1_status plan_reserve(svd1_plan_t P) {
+  const svd1_config& c = P->cfg;
+  const int64_t m = c.m, n = c.n;
+  const bool thin = (c.flags & SVD1_THIN_V) != 0;
+  const int64_t nv = thin ? m + 1 : n;
+  const int p = P->p;
+  // stream-ordered growth keeps its memory in the pool (no release at synchronisations)
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    SVD1_CUDA_TRY(cudaGetDevice(&dev));
+    SVD1_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~uint64_t(0);
+    SVD1_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  TRY(ensure_st2(P));
+  for (int sd = 2; sd < 6; ++sd) TRY(ensure_side(P, sd));
+  const size_t nproj = size_t(5 * m + n + 6);
+  TRY(P->W_u.reserve<double>(size_t(c.u_rows) * m));
+  TRY(P->W_v.reserve<double>(size_t(c.v_rows) * nv));
+  TRY(P->proj.reserve<double>(nproj));
+  TRY(P->partial.reserve<double>(size_t(project_partial_elems(c.u_rows, m, c.v_rows, n))));
+  TRY(P->probes.reserve<double>(size_t(4 * std::max<int64_t>(c.u_rows, 1))));
+  TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, static_cast<double*>(P->probes.p), P->st, &P->launches));
+  P->probes_ready = true;
+  // Phi, Psi of both sides for the deepest tree (zeroed: see ensure_expansions)
+  for (int side = 0; side < 2; ++side) {
+    const size_t e = expansion_elems(side ? c.v_rows : c.u_rows, side ? nv : m, p);
+    for (DevBuf* b : {&P->phi[side], &P->psi[side]}) {
+      TRY(b->reserve<double>(e));
+      SVD1_CUDA_TRY(cudaMemsetAsync(b->p, 0, b->cap, P->st));
+    }
+  }
+  // step records: per-update (steps) and the batch mode's two parities (bsteps)
+  for (int e = 0; e < 4; ++e) {
+    const int64_t N = e < 2 ? m : nv;
+    TRY(reserve_step(P->steps[e], N, p));
+    TRY(reserve_step(P->bsteps[0][e], N, p));
+    TRY(reserve_step(P->bsteps[1][e], N, p));
+  }
+  // batch mode (svd1_update_batch): projections, carried rows, few-rows scratch, Gram
+  const int ru_max = 4 + (kMaxBatch - 1), rv_max = kMaxBatch - 1;
+  TRY(P->bproj.reserve<double>(size_t(kMaxBatch) * nproj));
+  for (int q = 0; q < 2; ++q) {
+    TRY(P->RU[q].reserve<double>(size_t(ru_max) * m));
+    TRY(P->RV[q].reserve<double>(size_t(rv_max) * n));
+  }
+  TRY(P->few_scr[0].reserve<double>(size_t(few_rows_scratch_elems(ru_max, int(m)))));
+  TRY(P->few_scr[1].reserve<double>(size_t(few_rows_scratch_elems(rv_max, int(nv)))));
+  TRY(P->bgram.reserve<double>(size_t(kMaxBatch) * kMaxBatch));
+  TRY(P->d_rot_goff.reserve<int32_t>(size_t(m / 2 + 2)));
+  // pinned host: read-backs and the upload arenas
+  {
+    void* b = P->h_pin;
+    TRY(pinned_reserve(&b, &P->h_pin_cap,
+                       (std::max(nproj + size_t(m), size_t(kMaxBatch) * nproj + size_t(m) + size_t(5 * m + n))) *
+                           sizeof(double)));
+    P->h_pin = static_cast<double*>(b);
+  }
+  const int64_t Nmax = std::max(m, nv);
+  const size_t arena_bytes = std::max<size_t>(size_t(4) << 20, 2 * (size_t(Nmax) * (8 * (4 + kMaxCarry) + 64) +
+                                                                   fmm_blob_estimate(Nmax, p) + maps_blob_bytes(Nmax)));
+  for (auto& A : P->arena) {
+    void* b = A.buf;
+    TRY(pinned_reserve(&b, &A.cap, arena_bytes));
+    A.buf = static_cast<char*>(b);
+    if (!A.ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&A.ev, cudaEventDisableTiming));
+  }
+  SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
+  return SVD1_OK;
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -1993,6 +2175,11 @@ svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out) {
   P->st = static_cast<cudaStream_t>(cfg->stream);
   P->p = choose_p(cfg->eps);
   P->leaf = 2 * P->p;
+  const svd1_status st = plan_reserve(P);
+  if (st != SVD1_OK) {
+    svd1_plan_destroy(P);
+    return st;
+  }
   *out = P;
   return SVD1_OK;
 }
@@ -2036,10 +2223,10 @@ svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const doub
     return SVD1_E_INVALID;
   double* part;
   const int64_t need = project_partial_elems(c.u_rows, c.m, c.v_rows, c.n);
-  TRY(P->partial.get<double>(size_t(need), &part));
+  TRY(P->partial.get<double>(size_t(need), &part, P->st));
   if (!P->probes_ready) {  // the probes depend only on (seed, global row): once per plan
     double* g;
-    TRY(P->probes.get<double>(size_t(4 * std::max<int64_t>(c.u_rows, 1)), &g));
+    TRY(P->probes.get<double>(size_t(4 * std::max<int64_t>(c.u_rows, 1)), &g, P->st));
     TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, g, P->st, &P->launches));
     P->probes_ready = true;
   }
@@ -2077,7 +2264,7 @@ svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, in
     TRY(householder_cols(rows, in, ld, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, st, &P->launches));
   if (S.na > 0) {
     double* scr;
-    TRY(P->few_scr[side].get<double>(size_t(few_rows_scratch_elems(rows, S.na)), &scr));
+    TRY(P->few_scr[side].get<double>(size_t(few_rows_scratch_elems(rows, S.na)), &scr, st));
     TRY(apply_few_rows(rows, S.na, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
                        static_cast<double*>(S.d_out.p) + S.na, static_cast<double*>(S.d_zhat.p), S.dcs, in, ld,
                        S.dsrc, out, ld, S.ddst, scr, st, &P->launches));
@@ -2103,6 +2290,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < nv))) return SVD1_E_INVALID;
   if (m > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
   const int64_t launches0 = P->launches;
+  const int64_t allocs0 = g_allocs.load();
   const double t0 = now_ms();
   if (B) {  // the apply streams' arenas are unused in this mode
     for (int sd = 2; sd < 6; ++sd) TRY(arena_reset(P, sd));
@@ -2136,6 +2324,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if (alpha == 0.0 || beta == 0.0) {  // A_hat = A
     R.noop = 1;
     R.kernel_launches = P->launches - launches0;
+    R.allocations = g_allocs.load() - allocs0;
     if (rep) *rep = R;
     return SVD1_OK;
   }
@@ -2177,14 +2366,12 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // ---- workspaces for the applies (sized up front: a mid-stream realloc would sync)
   TRY(ensure_st2(P));
   double *Wu = nullptr, *Wv = nullptr;
-  if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu));
-  if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * nv, &Wv));
-  {
-    const int64_t rows_max = std::max(c.u_rows, c.v_rows);
-    const size_t guess = size_t(rows_max) * size_t(P->p) *
-                         size_t(4 * std::max<int64_t>(nv, 1) / std::max(P->leaf, 1) + 8);
-    for (int side = 0; side < 2; ++side) TRY(ensure_expansions(P, side, guess));
-  }
+  if (c.u_rows) TRY(P->W_u.get<double>(size_t(c.u_rows) * m, &Wu, P->st));  // sized at creation
+  if (c.v_rows) TRY(P->W_v.get<double>(size_t(c.v_rows) * nv, &Wv, P->st2));
+  // expansions for the deepest tree the planner can choose at this p (sized at creation
+  // for the plan's eps; a smaller eps per call grows them once, stream-ordered)
+  TRY(ensure_expansions(P, 0, expansion_elems(c.u_rows, m, P->p)));
+  TRY(ensure_expansions(P, 1, expansion_elems(c.v_rows, nv, P->p)));
   const bool one_stream = !B && std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
   // spectral work and uploads: the apply streams' sides (0, 1), or in batch mode the
   // spectral streams (2, 3), so the next update's spectral phase is not queued behind
@@ -2233,11 +2420,12 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   Joiner plan_u, plan_v, plan_u2, plan_v2;
   const svd1_config pcfg = P->cfg;
   const int pp = P->p;
-  auto rare_grow = [&](int e, int side) -> svd1_status {  // deeper tree than guessed
-    if (S[e].rows > 0 && S[e].na > 0 && cauchy_exp_elems(S[e].cp) > P->phi[side].cap / sizeof(double)) {
-      SVD1_CUDA_TRY(cudaDeviceSynchronize());
+  // expansions are sized at creation for the deepest tree; this only grows them (stream-
+  // ordered on the side's apply stream, no device synchronisation) if the call's eps is
+  // smaller than the plan's
+  auto rare_grow = [&](int e, int side) -> svd1_status {
+    if (S[e].rows > 0 && S[e].na > 0 && cauchy_exp_elems(S[e].cp) > P->phi[side].cap / sizeof(double))
       TRY(ensure_expansions(P, side, cauchy_exp_elems(S[e].cp)));
-    }
     return SVD1_OK;
   };
   // Host scheduler of the two chains: each round takes the first ready action in
@@ -2619,6 +2807,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     }
     R.t_ms[4] = now_ms() - t0;
     R.kernel_launches = P->launches - launches0;
+    R.allocations = g_allocs.load() - allocs0;
     if (rep) *rep = R;
     return SVD1_OK;
   }
@@ -2655,6 +2844,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
             t3 - t1, t4 - t1, now_ms() - t1);
   }
   R.kernel_launches = P->launches - launches0;
+  R.allocations = g_allocs.load() - allocs0;
   if (rep) *rep = R;
   return SVD1_OK;
 }
@@ -2669,8 +2859,6 @@ svd1_status svd1_update_projected(svd1_plan_t P, double* U, int64_t ldu, double*
   return update_impl(P, U, ldu, sigma, V, ldv, proj, eps, rep, nullptr, b);
 }
 
-constexpr int kMaxBatch = 28;  // buffers are sized for this many updates per call
-
 svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
                               const double* A, int64_t lda, const double* Bv, int64_t ldb, int64_t K,
                               double eps, svd1_report* reps) {
@@ -2684,14 +2872,14 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   // every update's STEP-1 projections against the initial factors
   const size_t nproj = size_t(5 * m + n + 6);
   double* pj;
-  TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj));
+  TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj, P->st));
   // update 0 in full (its probe block too), updates 1.. with one pass over U and V per
   // 8 of them (only their x_a, y_b and dots are used: the probes are carried)
   TRY(svd1_project(P, U, ldu, V, ldv, A, Bv, pj));
   if (K > 1) {
     double* part;
     const int64_t need = project_partial_elems(c.u_rows, m, c.v_rows, n);
-    TRY(P->partial.get<double>(size_t(need), &part));
+    TRY(P->partial.get<double>(size_t(need), &part, P->st));
     TRY(project_many(U, ldu, c.u_rows, m, c.u_row0, V, ldv, c.v_rows, n, c.v_row0, thin ? m : n, A + lda, lda,
                      Bv + ldb, ldb, int(K) - 1, static_cast<double*>(P->probes.p), part, need, pj + nproj,
                      int64_t(nproj), P->st, &P->launches));
@@ -2730,13 +2918,13 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   // V side [y_b(K-1) .. y_b(1)]; update t transforms the rows of updates t+1.. only
   const int ru_max = 4 + (kMaxBatch - 1), rv_max = kMaxBatch - 1;
   double *ru0, *ru1, *rv0, *rv1;
-  TRY(P->RU[0].get<double>(size_t(ru_max) * m, &ru0));
-  TRY(P->RU[1].get<double>(size_t(ru_max) * m, &ru1));
-  TRY(P->RV[0].get<double>(size_t(rv_max) * n, &rv0));
-  TRY(P->RV[1].get<double>(size_t(rv_max) * n, &rv1));
-  double* scr;  // few-rows scratch at its largest up front (no reallocation mid-batch)
-  TRY(P->few_scr[0].get<double>(size_t(few_rows_scratch_elems(ru_max, int(m))), &scr));
-  TRY(P->few_scr[1].get<double>(size_t(few_rows_scratch_elems(rv_max, int(n))), &scr));
+  TRY(P->RU[0].get<double>(size_t(ru_max) * m, &ru0, P->st));  // all sized at creation
+  TRY(P->RU[1].get<double>(size_t(ru_max) * m, &ru1, P->st));
+  TRY(P->RV[0].get<double>(size_t(rv_max) * n, &rv0, P->st));
+  TRY(P->RV[1].get<double>(size_t(rv_max) * n, &rv1, P->st));
+  double* scr;  // few-rows scratch at its largest
+  TRY(P->few_scr[0].get<double>(size_t(few_rows_scratch_elems(ru_max, int(m))), &scr, P->st));
+  TRY(P->few_scr[1].get<double>(size_t(few_rows_scratch_elems(rv_max, int(nv))), &scr, P->st));
   SVD1_CUDA_TRY(cudaMemcpyAsync(ru0, pj + m, 4 * m * sizeof(double), cudaMemcpyDeviceToDevice, P->st));
   for (int s = 1; s < k; ++s) {
     SVD1_CUDA_TRY(cudaMemcpyAsync(ru0 + int64_t(4 + (k - 1 - s)) * m, pj + size_t(s) * nproj, m * sizeof(double),
@@ -2746,7 +2934,7 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   }
   double* gram = nullptr;  // thin: b_t . b_s
   if (thin) {
-    TRY(P->bgram.get<double>(size_t(kMaxBatch) * kMaxBatch, &gram));
+    TRY(P->bgram.get<double>(size_t(kMaxBatch) * kMaxBatch, &gram, P->st));
     TRY(gram_rows(k, P->batch_b, P->batch_ldb, n, gram, P->st, &P->launches));
   }
   // host copies of the projections (dots of every update; x's of update 0) and sigma
@@ -2847,7 +3035,7 @@ svd1_status svd1_update(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   const svd1_config& c = P->cfg;
   if (c.u_rows != c.m || c.v_rows != c.n) return SVD1_E_INVALID;  // single process only
   double* proj;
-  TRY(P->proj.get<double>(size_t(5 * c.m + c.n + 6), &proj));
+  TRY(P->proj.get<double>(size_t(5 * c.m + c.n + 6), &proj, P->st));
   TRY(svd1_project(P, U, ldu, V, ldv, a, b, proj));
   return svd1_update_projected(P, U, ldu, sigma, V, ldv, proj, a, b, eps, rep);
 }
@@ -2945,11 +3133,11 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
   if (!P || n < 0 || !d || !z || !k_out || !tau_out || rho == 0.0) return SVD1_E_INVALID;
   if (n == 0) return SVD1_OK;
   int32_t *dst, *dit;
-  TRY(P->status.get<int32_t>(1, &dst));
-  TRY(P->iters.get<int32_t>(size_t(n), &dit));
+  TRY(P->status.get<int32_t>(1, &dst, P->st));
+  TRY(P->iters.get<int32_t>(size_t(n), &dit, P->st));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
   double* orient;
-  TRY(P->scratch_d.get<double>(size_t(2 * n), &orient));
+  TRY(P->scratch_d.get<double>(size_t(2 * n), &orient, P->st));
   TRY(secular_orient(d, z, rho, int(n), orient, orient + n, P->st, &P->launches));
   if (use_sec_fmm(P->cfg.flags, int(n), false)) {  // plan from the oriented sources (host copy)
     std::vector<double> dr(n);
@@ -2977,7 +3165,7 @@ svd1_status svd1_loewner(svd1_plan_t P, int64_t n, const double* d, const int32_
                          double rho, const double* z, double* zhat_out) {
   if (!P || n < 0 || !d || !k || !tau || !z || !zhat_out || rho == 0.0) return SVD1_E_INVALID;
   double* scr;
-  TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr));
+  TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr, P->st));
   int* ctr;
   TRY(counters(P->ctr, int(n), P->st, &ctr));
   TRY(loewner(d, k, tau, rho, z, int(n), zhat_out, scr, ctr, P->st, &P->launches));
@@ -2991,10 +3179,10 @@ svd1_status svd1_colnorms(svd1_plan_t P, int64_t n, const double* d, const int32
   if (n == 0) return SVD1_OK;
   int32_t* dst;
   double* cs;
-  TRY(P->status.get<int32_t>(1, &dst));
-  TRY(P->scratch_i.get<double>(size_t(n), &cs));
+  TRY(P->status.get<int32_t>(1, &dst, P->st));
+  TRY(P->scratch_i.get<double>(size_t(n), &cs, P->st));
   double* scr;
-  TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr));
+  TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr, P->st));
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
   int* ctr;
   TRY(counters(P->ctr, int(n), P->st, &ctr));

@@ -187,3 +187,23 @@ def test_batch_too_long():
     with pytest.raises(P.SVD1Error) as e:
         plan.update_batch(U, s, V, T(np.stack([a for a, _ in inp["ab"]])), T(np.stack([b for _, b in inp["ab"]])))
     assert e.value.code == 1
+
+
+def test_no_allocation_inside_updates():
+    """Every workspace is sized by svd1_plan_create: the updates of
+    the full-size C3 stream -- 20 of them, past the 16-update stream as bench.py's timed
+    region goes, where the trees deepen -- allocate nothing (svd1_report.allocations),
+    through the batch API and the per-update API alike."""
+    inp = config_inputs(3, device=DEV, updates=16)
+    m = 4096
+    A = torch.stack([torch.from_numpy(a) for a, _ in inp["ab"]]).to(DEV)
+    B = torch.stack([torch.from_numpy(b) for _, b in inp["ab"]]).to(DEV)
+    U, s, V = inp["U"].clone(), inp["sigma"].clone(), inp["V"].clone()
+    plan = P.Plan(m, m, eps=1e-10)
+    reps = plan.update_batch(U, s, V, A, B) + plan.update_batch(U, s, V, A[:4], B[:4])
+    assert [r["allocations"] for r in reps] == [0] * 20, [r["allocations"] for r in reps]
+    assert max(max(r["fmm_levels"]) for r in reps) >= 8
+    reps2 = [plan.update(U, s, V, A[t], B[t]) for t in range(3)]
+    assert [r["allocations"] for r in reps2] == [0] * 3
+    torch.cuda.synchronize()
+    plan.close()

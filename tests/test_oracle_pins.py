@@ -406,3 +406,57 @@ def test_repeated_singular_values_are_paired(rule):
     assert O.orth_defect(r["V"]) <= 1e-13
     _, sj, _ = jacobi_svd(A_hat)
     assert sigma_errors(r["sigma"], sj)["gram"] <= 1e-13
+
+
+# ------------------------------------------------------------------ metrics
+def test_paper_error_hand_cases():
+    """paper_error (Q24: the denominator is the largest singular value of A_hat)
+    on hand-computed 2x2 / 2x3 cases: a transposed V, a Frobenius-norm denominator or a
+    sum instead of a max would each change one of these values."""
+    A = np.array([[3.0, 0.0], [0.0, 4.0]])      # ||A||_2 = 4 (Frobenius 5)
+    Us = np.array([[0.0, 1.0], [1.0, 0.0]])     # u1 = e2, u2 = e1
+    assert O.paper_error(A, Us, np.array([4.0, 3.0]), Us) == 0.0
+    # sigma_2 off by 0.5 -> residual 0.5 at entry (0, 0): error 0.5 / 4
+    assert O.paper_error(A, Us, np.array([4.0, 2.5]), Us) == pytest.approx(0.125, rel=1e-15)
+    # both off: max (not sum) of |R| = 0.5, not 0.5 + 0.25
+    assert O.paper_error(A, Us, np.array([3.75, 2.5]), Us) == pytest.approx(0.125, rel=1e-15)
+    # rectangular m = 2 < n = 3: A_hat = 5 e1 e3^T, sigma = (5, 0), u1 = e1, v1 = e3
+    A = np.array([[0.0, 0.0, 5.0], [0.0, 0.0, 0.0]])
+    V = np.array([[0.0, 1.0, 0.0], [0.0, 0.0, 1.0], [1.0, 0.0, 0.0]])   # columns e3, e1, e2
+    assert O.paper_error(A, np.eye(2), np.array([5.0, 0.0]), V) == 0.0
+    assert O.paper_error(A, np.eye(2), np.array([5.0, 0.0]), V.T) == pytest.approx(1.0)  # wrong V
+    assert O.paper_error(A, np.eye(2), np.array([5.0, 0.0]), V, sigma_max=2.5) == 0.0
+
+
+def test_column_residual_hand_cases():
+    """column_residual (Q28): max_i ||A_hat v_i - sigma_i u_i||_2 / sigma_1, i < m."""
+    A = np.array([[5.0, 0.3], [0.0, 1.4]])
+    I = np.eye(2)
+    # column 0 exact; column 1: (0.3, 1.4) - (0, 1) = (0.3, 0.4), 2-norm 0.5 (max-abs 0.4)
+    assert O.column_residual(A, I, np.array([5.0, 1.0]), I) == pytest.approx(0.1, rel=1e-15)
+    # A_hat^T instead of A_hat would give max(0.3, 0.4) / 5 = 0.08
+    assert O.column_residual(A.T, I, np.array([5.0, 1.0]), I) == pytest.approx(0.08, rel=1e-15)
+    # rectangular: only the m columns of V paired with U count
+    A = np.array([[0.0, 0.0, 5.0], [0.0, 0.0, 0.0]])
+    V = np.array([[0.0, 1.0, 0.0], [0.0, 0.0, 1.0], [1.0, 0.0, 0.0]])
+    assert O.column_residual(A, np.eye(2), np.array([5.0, 0.0]), V) == 0.0
+    V2 = V.copy()
+    V2[:, 2] = 7.0  # the (n - m)-th column is not used
+    assert O.column_residual(A, np.eye(2), np.array([5.0, 0.0]), V2) == 0.0
+    # sigma_1 scales the result
+    assert O.column_residual(A, np.eye(2), np.array([4.0, 0.0]), V) == pytest.approx(1.0 / 4.0)
+
+
+def test_threaded_evaluation_is_bitwise_serial(monkeypatch):
+    """The oracle evaluates independent roots on several threads; every root's sum is the
+    same numpy reduction of the same row, so roots and w are bitwise the one-thread ones."""
+    import oracle.svd1_oracle as M
+    rng = np.random.default_rng(5)
+    d, z, rho = random_secular(700, rng, kind="graded")
+    monkeypatch.setattr(M, "THREADS", 1)
+    k1, t1 = O.secular_roots_bisect(d, z, rho)
+    w1 = O.secular_w(d, z, rho, k1, t1)
+    monkeypatch.setattr(M, "THREADS", 7)
+    k7, t7 = O.secular_roots_bisect(d, z, rho)
+    w7 = O.secular_w(d, z, rho, k7, t7)
+    assert np.array_equal(k1, k7) and np.array_equal(t1, t7) and np.array_equal(w1, w7)
