@@ -7,8 +7,10 @@ the FMM Cauchy-apply fraction of the FP64 (DMMA) roofline.
 One step = one svd1_update (Alg 6.1) of the C3 stream
 (m = n = 4096, sigma_i = 10^(-6 i/n), a, b ~ N(0,1)); the K timed steps are updates
 1..K of that stream (indices wrap at 16), applied in place to device-resident
-factors.  N > 1: torchrun, rows of U and V sharded across ranks, the STEP-1
-projections all-reduced over NCCL (the path's only exchange), time = max over ranks.
+factors.  N > 1: one process per GPU (torchrun; `--gpus N` without torchrun relaunches
+itself under torch.distributed.run), rows of U and V sharded across ranks, the STEP-1
+projections all-reduced over NCCL and every eigen-update's spectral phase sliced across
+the ranks and all-gathered inside libsvd1; time = max over ranks.
 `--impl reference` times the CPU oracle (oracle/, the base contract's reference arm
 for this tier) on bounded samples of the same workload.
 Prints ONE JSON line on rank 0.
@@ -195,6 +197,21 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.gpus != world:
+        if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+            # one process per GPU: relaunch this command under torch.distributed.run
+            import socket
+            import subprocess
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            sys.exit(subprocess.call(cmd))
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: run one process per GPU"}),
+              flush=True)
+        sys.exit(2)
 
     import torch
     import torch.distributed as dist

@@ -47,7 +47,8 @@ typedef enum {
   SVD1_E_POLE = 4,      /* a root coincides with a pole: tau == 0 */
   SVD1_E_ZEROCOL = 5,   /* ||c_j|| underflow/overflow */
   SVD1_E_CUDA = 6,      /* CUDA runtime error */
-  SVD1_E_NOMEM = 7      /* device or host allocation failed */
+  SVD1_E_NOMEM = 7,     /* device or host allocation failed */
+  SVD1_E_NCCL = 8       /* NCCL unavailable or a collective failed (world > 1) */
 } svd1_status;
 
 /* flags */
@@ -62,6 +63,12 @@ typedef enum {
                                     column m is workspace (the direction of b outside span(V),
                                     overwritten by every update).  The null space of A^T is
                                     never stored. */
+#define SVD1_EMULATE_RANKS 0x20u /* world > 1 without NCCL (test mode): this
+                                    process computes EVERY rank's slice of the spectral phase,
+                                    so the all-gathers are concatenations in place; the rows
+                                    are this process's as usual (normally all of them) */
+#define SVD1_FORCE_NCCL 0x40u    /* use the NCCL all-gathers even with world == 1 (test mode:
+                                    exercises the communicator path on one GPU; nccl_id needed) */
 
 typedef struct {
   int64_t m, n;      /* global sizes, 1 <= m <= n */
@@ -74,6 +81,20 @@ typedef struct {
   void* stream;      /* cudaStream_t */
   uint32_t flags;    /* SVD1_FORCE_* */
   int32_t fmm_min_n; /* active size from which the FMM apply is used (0 = 384) */
+  /* Ranks (one process per GPU).  Rows of U and V are split by
+   * the caller (u_row0/u_rows, v_row0/v_rows above).  With world > 1 the O(n^2) spectral phase
+   * of every eigen-update (P:363 STEP 2 and the Loewner / column-norm sums) is SLICED: rank r
+   * solves roots, Loewner weights and column norms of the index range [r c, r c + c),
+   * c = ceil(n_active / world), and the plan all-gathers them over NCCL (NVLink); decisions
+   * made on the host (deflation, merge, trees) see bitwise-identical data on every rank.
+   * Slices are computed by the same code as the whole range, so results are bitwise those of
+   * world == 1 (given the same all-reduced projections). */
+  int32_t rank;        /* 0 <= rank < world */
+  int32_t world;       /* number of ranks; 0 or 1 = one process */
+  const void* nccl_id; /* world > 1 (or SVD1_FORCE_NCCL): 128-byte ncclUniqueId from
+                          svd1_nccl_unique_id on rank 0, given to every rank by the caller;
+                          svd1_plan_create is then collective (all ranks call it).  NULL with
+                          SVD1_EMULATE_RANKS. */
 } svd1_config;
 
 typedef struct {
@@ -227,6 +248,11 @@ svd1_status svd1_fmm_tree_stats(int64_t n, const double* d, const int32_t* k,
  * cells, leaves, M2L partners, near ranges, max near terms per root, direct roots,
  * planning time in ns.  No GPU needed. */
 svd1_status svd1_secfmm_plan_stats(int64_t n, const double* d, int64_t* stats_out);
+
+/* A fresh 128-byte ncclUniqueId (out: host buffer of 128 bytes) for svd1_config.nccl_id:
+ * call on rank 0 and broadcast (e.g. torch.distributed.broadcast_object_list).
+ * SVD1_E_NCCL if libnccl.so.2 cannot be opened. */
+svd1_status svd1_nccl_unique_id(void* out);
 
 const char* svd1_status_string(svd1_status s);
 /* Library build identifier (for the bench/smoke evidence). */

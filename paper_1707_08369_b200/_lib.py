@@ -23,7 +23,8 @@ status_t = C.c_int
 
 class Config(C.Structure):
     _fields_ = [("m", i64), ("n", i64), ("u_rows", i64), ("v_rows", i64), ("u_row0", i64),
-                ("v_row0", i64), ("eps", dbl), ("stream", vp), ("flags", u32), ("fmm_min_n", i32)]
+                ("v_row0", i64), ("eps", dbl), ("stream", vp), ("flags", u32), ("fmm_min_n", i32),
+                ("rank", i32), ("world", i32), ("nccl_id", vp)]
 
 
 class Report(C.Structure):
@@ -72,6 +73,7 @@ svd1_loewner = _sig("svd1_loewner", [vp, i64, vp, vp, vp, dbl, vp, vp])
 svd1_colnorms = _sig("svd1_colnorms", [vp, i64, vp, vp, vp, vp, vp])
 svd1_fmm_tree_stats = _sig("svd1_fmm_tree_stats", [i64, vp, vp, vp, dbl, vp])
 svd1_secfmm_plan_stats = _sig("svd1_secfmm_plan_stats", [i64, vp, vp])
+svd1_nccl_unique_id = _sig("svd1_nccl_unique_id", [vp])
 lib.svd1_status_string.argtypes = [status_t]
 lib.svd1_status_string.restype = C.c_char_p
 lib.svd1_version.argtypes = []
@@ -79,13 +81,25 @@ lib.svd1_version.restype = C.c_char_p
 
 EXPORTS = ["svd1_plan_create", "svd1_plan_destroy", "svd1_update", "svd1_update_batch", "svd1_update_batch_projected", "svd1_project",
            "svd1_update_projected", "svd1_cauchy_apply", "svd1_secular_solve", "svd1_loewner",
-           "svd1_colnorms", "svd1_fmm_tree_stats", "svd1_secfmm_plan_stats", "svd1_status_string", "svd1_version"]
+           "svd1_colnorms", "svd1_fmm_tree_stats", "svd1_secfmm_plan_stats", "svd1_nccl_unique_id",
+           "svd1_status_string", "svd1_version"]
 
 FORCE_DIRECT = 0x1
 FORCE_FMM = 0x2
 SECULAR_FMM = 0x4     # secular solve with the FMM far field at every size > 64
 SECULAR_DIRECT = 0x8  # secular solve with direct sums only
 THIN_V = 0x10         # thin right factor: V is n x (m+1), column m workspace (svd1.h)
+EMULATE_RANKS = 0x20  # world > 1 in one process: every rank's spectral slice computed here (tests)
+FORCE_NCCL = 0x40     # NCCL all-gathers even at world 1 (tests the communicator path on one GPU)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for svd1_config.nccl_id (call on rank 0, broadcast to the others)."""
+    buf = C.create_string_buffer(128)
+    code = svd1_nccl_unique_id(C.cast(buf, vp))
+    if code:
+        raise RuntimeError(f"svd1_nccl_unique_id: {status_string(code)}")
+    return buf.raw
 
 
 def status_string(code: int) -> str:

@@ -47,16 +47,20 @@ class Plan:
     the whole matrices on one GPU)."""
 
     def __init__(self, m, n, eps=1e-10, stream=None, flags=0, fmm_min_n=0,
-                 u_rows=None, v_rows=None, u_row0=0, v_row0=0):
+                 u_rows=None, v_rows=None, u_row0=0, v_row0=0, rank=0, world=1, nccl_id=None):
+        """rank/world/nccl_id: one process per GPU (svd1.h); nccl_id = the 128 bytes of
+        nccl_unique_id() from rank 0 (creation is then collective over the ranks)."""
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream
         self.m, self.n = int(m), int(n)
+        self._id = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
         cfg = L.Config(m=self.m, n=self.n, u_rows=self.m if u_rows is None else int(u_rows),
                        v_rows=self.n if v_rows is None else int(v_rows), u_row0=int(u_row0),
                        v_row0=int(v_row0), eps=float(eps),
                        stream=C.c_void_p(stream.cuda_stream), flags=int(flags),
-                       fmm_min_n=int(fmm_min_n))
+                       fmm_min_n=int(fmm_min_n), rank=int(rank), world=int(world),
+                       nccl_id=None if self._id is None else C.cast(self._id, C.c_void_p))
         self.cfg = cfg
         h = C.c_void_p()
         _check(L.svd1_plan_create(C.byref(cfg), C.byref(h)), "svd1_plan_create")

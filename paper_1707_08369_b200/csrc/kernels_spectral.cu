@@ -520,22 +520,25 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
                                                      double* __restrict__ tau_out,
                                                      int32_t* __restrict__ iters_out,
                                                      int32_t* __restrict__ status, SecFmmDev F,
-                                                     int nfar) {
+                                                     int j0, int j1) {
   const int lane = threadIdx.x & 31;
-  // direct blocks first (they are the longest-running), then the nfar warp blocks
+  // Roots j0 <= j < j1 of the rho > 0 view (a rank's slice; every root is
+  // solved by the same code whatever the slice, so slices concatenate bitwise).
+  // direct blocks first (they are the longest-running), then the warp blocks
   // (the direct solver's one such root is the last, with the widest bracket)
   const int ndir = FMM ? F.ndirect : 1;
   if (int(blockIdx.x) < ndir) {
     __shared__ double red[32];
     const BlockGrp g{int(threadIdx.x), int(blockDim.x), red};
     const int j = FMM ? F.direct[blockIdx.x] : n - 1;
+    if (j < j0 || j >= j1) return;  // another rank's root
     solve_root(j, d, z2, rho, n, g,
                [&](double dk, double tau, int sp) { return sec_eval(d, z2, n, dk, tau, sp, g); },
                k_out, tau_out, iters_out, status);
     return;
   }
-  const int j = int((int64_t(blockIdx.x - ndir) * blockDim.x + threadIdx.x) >> 5);
-  if (j >= n) return;
+  const int j = j0 + int((int64_t(blockIdx.x - ndir) * blockDim.x + threadIdx.x) >> 5);
+  if (j >= j1) return;
   const WarpGrp g{lane};
   if (j == n - 1) return;   // a direct block's
   if (!FMM) {
@@ -702,11 +705,12 @@ __device__ __forceinline__ bool last_block_of_column(int* ctr) {
 __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
     const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau, int n,
     int chunk, double* __restrict__ pm, int32_t* __restrict__ pe, int* __restrict__ ctr, double rho,
-    const double* __restrict__ z, double* __restrict__ zhat) {
+    const double* __restrict__ z, double* __restrict__ zhat, int i_lo, int i_hi) {
   __shared__ double s_d[kLJ], s_mu[kLJ], s_t[kLJ];
-  const int i = blockIdx.x * kLT + threadIdx.x;
+  // i_lo <= i < i_hi: a rank's slice; the j chunks depend on n only (bitwise slices)
+  const int i = i_lo + blockIdx.x * kLT + threadIdx.x;
   const int j0 = blockIdx.y * chunk, j1 = min(n, j0 + chunk);
-  const double di = i < n ? d[i] : 0.0;
+  const double di = i < i_hi ? d[i] : 0.0;
   double Pn = 1.0, Pd = 1.0;
   int E = 0;
   for (int jb = j0; jb < j1; jb += kLJ) {
@@ -751,14 +755,14 @@ __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
     Pn *= Qn;
     Pd *= Qd;
   }
-  if (i < n) {
+  if (i < i_hi) {
     int e;
     const double m = frexp(Pn / Pd, &e);
     pm[int64_t(blockIdx.y) * n + i] = m;
     pe[int64_t(blockIdx.y) * n + i] = E + e;
   }
   if (!last_block_of_column(ctr)) return;
-  if (i < n) {  // combine (the partials of other blocks: L2, not this SM's L1)
+  if (i < i_hi) {  // combine (the partials of other blocks: L2, not this SM's L1)
     double P = 1.0;
     int Et = 0;
     for (int c = 0; c < int(gridDim.y); ++c) {
@@ -787,11 +791,13 @@ __global__ void __launch_bounds__(kCT) colnorm_partial_kernel(
     const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau,
     const double* __restrict__ zhat, int n, int chunk, const double* __restrict__ carry,
     double* __restrict__ part, int* __restrict__ ctr, double* __restrict__ colscale,
-    double* __restrict__ carry_out, int32_t* __restrict__ status) {
+    double* __restrict__ carry_out, int32_t* __restrict__ status, int j_lo, int j_hi, int64_t ldc) {
   __shared__ double s_d[kCI], s_z[kCI], s_c[NC > 0 ? NC : 1][kCI];
-  const int j = blockIdx.x * kCT + threadIdx.x;
+  // j_lo <= j < j_hi: a rank's slice; the i chunks depend on n only (bitwise slices);
+  // carry_out[q] at carry_out + q * ldc
+  const int j = j_lo + blockIdx.x * kCT + threadIdx.x;
   const int i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
-  const bool ok = j < n;
+  const bool ok = j < j_hi;
   const double dk = ok ? d[k[j]] : 0.0, tj = ok ? tau[j] : 1.0, at = fabs(tj);
   double s = 0.0, t[NC > 0 ? NC : 1];
 #pragma unroll
@@ -833,7 +839,7 @@ __global__ void __launch_bounds__(kCT) colnorm_partial_kernel(
     for (int q = 0; q < NC; ++q) {
       double tt = 0.0;
       for (int c = 0; c < int(gridDim.y); ++c) tt += __ldcg(part + int64_t(c) * cstride + int64_t(q + 1) * n + j);
-      carry_out[int64_t(q) * n + j] = tt / rs;
+      carry_out[int64_t(q) * ldc + j] = tt / rs;
     }
   }
   if (threadIdx.x == 0) ctr[blockIdx.x] = 0;
@@ -1025,30 +1031,30 @@ svd1_status project_many(const double* U, int64_t ldu, int64_t u_rows, int64_t m
   return SVD1_OK;
 }
 
-svd1_status secular(const double* d, const double* z2, double rho, int n, int32_t* k_out,
+svd1_status secular(const double* d, const double* z2, double rho, int n, int j0, int j1, int32_t* k_out,
                     double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
                     int64_t* launches) {
-  if (n <= 0) return SVD1_OK;
-  secular_kernel<false><<<1 + blocks_for_warps(n), 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out,
-                                                                   status, SecFmmDev{}, 0);
+  if (n <= 0 || j1 <= j0) return SVD1_OK;
+  secular_kernel<false><<<1 + blocks_for_warps(j1 - j0), 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out,
+                                                                         status, SecFmmDev{}, j0, j1);
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }
 
-svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, const SecFmmDev& F,
-                        int32_t* k_out, double* tau_out, int32_t* iters_out, int32_t* status,
-                        cudaStream_t st, int64_t* launches) {
-  if (n <= 0) return SVD1_OK;
+svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, int j0, int j1,
+                        const SecFmmDev& F, int32_t* k_out, double* tau_out, int32_t* iters_out,
+                        int32_t* status, cudaStream_t st, int64_t* launches) {
+  if (n <= 0 || j1 <= j0) return SVD1_OK;
   auto grid = [](int items) { return unsigned(std::max(1, (items + 255) / 256)); };
   const int L = F.L;
   secfmm_phase_kernel<<<grid((1 << L) * kSecP), 256, 0, st>>>(F, d, z2, 0);
   secfmm_phase_kernel<<<grid(((1 << L) - 1) * kSecP * 32), 256, 0, st>>>(F, d, z2, 1);
   secfmm_phase_kernel<<<grid(F.ncells * kSecP * 32), 256, 0, st>>>(F, d, z2, 2);
   secfmm_phase_kernel<<<grid((1 << L) * kSecP * 32), 256, 0, st>>>(F, d, z2, 3);
-  const int nfar = blocks_for_warps(n);
+  const int nfar = blocks_for_warps(j1 - j0);
   secular_kernel<true><<<nfar + F.ndirect, 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out, status, F,
-                                                          nfar);
+                                                          j0, j1);
   *launches += 5;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
@@ -1088,37 +1094,36 @@ svd1_status secular_orient(const double* d, const double* z, double rho, int n, 
 }
 
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
-                    const double* z, int n, double* zhat, double* scratch, int* ctr, cudaStream_t st,
-                    int64_t* launches) {
-  if (n <= 0) return SVD1_OK;
+                    const double* z, int n, int i0, int i1, double* zhat, double* scratch, int* ctr,
+                    cudaStream_t st, int64_t* launches) {
+  if (n <= 0 || i1 <= i0) return SVD1_OK;
   const int ch = loewner_chunks(n);
   const int chunk = (n + ch - 1) / ch;
   double* pm = scratch;
   int32_t* pe = reinterpret_cast<int32_t*>(scratch + int64_t(ch) * n);
-  loewner_partial_kernel<<<dim3(unsigned((n + kLT - 1) / kLT), unsigned(ch)), kLT, 0, st>>>(d, k, tau, n,
-                                                                                       chunk, pm, pe, ctr, rho,
-                                                                                       z, zhat);
+  loewner_partial_kernel<<<dim3(unsigned((i1 - i0 + kLT - 1) / kLT), unsigned(ch)), kLT, 0, st>>>(
+      d, k, tau, n, chunk, pm, pe, ctr, rho, z, zhat, i0, i1);
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }
 
 svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
-                          const double* zhat, int n, const double* carry, int ncarry,
-                          double* colscale, double* carry_out, int32_t* status, double* scratch, int* ctr,
-                          cudaStream_t st, int64_t* launches) {
-  if (n <= 0) return SVD1_OK;
+                          const double* zhat, int n, int j0, int j1, const double* carry, int ncarry,
+                          double* colscale, double* carry_out, int64_t ldc, int32_t* status, double* scratch,
+                          int* ctr, cudaStream_t st, int64_t* launches) {
+  if (n <= 0 || j1 <= j0) return SVD1_OK;
   const int ch = inner_chunks(n, kCT);
   const int chunk = (n + ch - 1) / ch;
-  const dim3 g(unsigned((n + kCT - 1) / kCT), unsigned(ch));
+  const dim3 g(unsigned((j1 - j0 + kCT - 1) / kCT), unsigned(ch));
   switch (ncarry) {
-    case 0: colnorm_partial_kernel<0><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
-    case 1: colnorm_partial_kernel<1><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
-    case 2: colnorm_partial_kernel<2><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
-    case 3: colnorm_partial_kernel<3><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
-    case 4: colnorm_partial_kernel<4><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
-    case 5: colnorm_partial_kernel<5><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
-    case 6: colnorm_partial_kernel<6><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status); break;
+    case 0: colnorm_partial_kernel<0><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status, j0, j1, ldc); break;
+    case 1: colnorm_partial_kernel<1><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status, j0, j1, ldc); break;
+    case 2: colnorm_partial_kernel<2><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status, j0, j1, ldc); break;
+    case 3: colnorm_partial_kernel<3><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status, j0, j1, ldc); break;
+    case 4: colnorm_partial_kernel<4><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status, j0, j1, ldc); break;
+    case 5: colnorm_partial_kernel<5><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status, j0, j1, ldc); break;
+    case 6: colnorm_partial_kernel<6><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, ctr, colscale, carry_out, status, j0, j1, ldc); break;
     default: return SVD1_E_INVALID;
   }
   *launches += 1;

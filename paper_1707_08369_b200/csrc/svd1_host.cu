@@ -2,6 +2,9 @@
 // decision logic of Alg 6.2 (sorting, deflation, merge), and the FMM tree
 // / interaction lists.  Every O(n^2) and O(rows*n)
 // step runs in the CUDA kernels of kernels_spectral.cu / kernels_apply.cu.
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is opened at run time when a plan spans ranks
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -122,6 +125,64 @@ svd1_status pinned_reserve(void** buf, size_t* cap, size_t bytes) {
 
 constexpr int kMaxBatch = 28;  // svd1_update_batch: buffers are sized for this many updates per call
 
+// ---- NCCL, opened at run time (no link-time dependency; in a process that already
+// loaded torch's libnccl.so.2 the same library is reused)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    auto sym = [h](const char* nm) { return dlsym(h, nm); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(sym("ncclCommSplit"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommSplit && a.AllGather && a.GroupStart && a.GroupEnd &&
+           a.CommDestroy && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
+svd1_status nccl_fail(ncclResult_t r, const char* what) {
+  const NcclApi& A = nccl_api();
+  std::fprintf(stderr, "[svd1] NCCL error %d (%s) in %s\n", int(r), A.GetErrorString ? A.GetErrorString(r) : "?",
+               what);
+  return SVD1_E_NCCL;
+}
+#define NCCL_TRY(expr)                                  \
+  do {                                                  \
+    ncclResult_t _r = (expr);                           \
+    if (_r != ncclSuccess) return nccl_fail(_r, #expr); \
+  } while (0)
+
+// Rank r's slice [lo, hi) of n indices: contiguous blocks of c = ceil(n / G), so rank r's
+// results sit at [r c, r c + c) of a G c buffer -- the in-place all-gather layout.
+struct Slice {
+  int c, lo, hi;
+};
+inline Slice slice_of(int n, int G, int r) {
+  const int c = (n + G - 1) / G;
+  const int lo = std::min(n, r * c);
+  return Slice{c, lo, std::min(n, lo + c)};
+}
+
 #define TRY(expr)                       \
   do {                                  \
     svd1_status _s = (expr);            \
@@ -210,6 +271,7 @@ struct CauchyPrep {
 struct StepRecord {
   int N = 0;                          // size of the eigenproblem (columns of the buffer)
   int na = 0;                         // active (secular) size
+  int nap = 0;                        // na padded to world * slice (all-gather layout)
   double rho = 0.0;
   std::vector<int32_t> h_goff, h_cols;  // Householder groups (buffer columns)
   std::vector<double> h_hv;
@@ -272,6 +334,14 @@ struct svd1_plan_s {
   svd1_config cfg{};
   cudaStream_t st = nullptr;
   int p = 16, leaf = 32;
+  // ranks: the spectral phase of every eigen-update is sliced -- roots,
+  // Loewner weights and column norms of rank r's index range -- and all-gathered over NCCL,
+  // one communicator per side chain (U: 0, V: 1), so each chain's collectives are issued
+  // in the same order on every rank whatever the host scheduler interleaves
+  int world = 1, rank = 0;
+  bool use_nccl = false;  // world > 1, or SVD1_FORCE_NCCL
+  bool emulate = false;   // SVD1_EMULATE_RANKS: this process computes every rank's slices
+  ncclComm_t comm[2] = {nullptr, nullptr};
   uint64_t probe_seed = 0x1707083691234567ull;
   int64_t launches = 0;
   DevBuf ctr;  // last-block counters for the test hooks (kept zero)
@@ -1576,6 +1646,37 @@ struct Joiner {
   ~Joiner() { join(); }
 };
 
+// read-back words of one eigen-update's spectral results (see spectral_launch)
+size_t spectral_words(int nap, int nc, int G) {
+  return size_t(nap) * (3 + nc) + size_t(nap + 1) / 2 + size_t(G + 1) / 2 + 1;
+}
+
+// In-place all-gather of every rank's slice [r c, r c + c) of each part, one NCCL group on
+// the chain's communicator and stream (no-op on one process or in the emulation mode,
+// where every slice was computed here).
+struct GatherPart {
+  void* base;
+  int count;  // c: elements per rank
+  ncclDataType_t type;
+  int elem;   // bytes per element
+};
+svd1_status exchange(svd1_plan_t P, int chain, cudaStream_t st, const std::vector<GatherPart>& parts) {
+  if (!P->use_nccl) return SVD1_OK;
+  const NcclApi& A = nccl_api();
+  NCCL_TRY(A.GroupStart());
+  for (const GatherPart& g : parts) {
+    char* base = static_cast<char*>(g.base);
+    const ncclResult_t r = A.AllGather(base + size_t(P->rank) * g.count * g.elem, base, size_t(g.count), g.type,
+                                       P->comm[chain], st);
+    if (r != ncclSuccess) {
+      A.GroupEnd();
+      return nccl_fail(r, "ncclAllGather");
+    }
+  }
+  NCCL_TRY(A.GroupEnd());
+  return SVD1_OK;
+}
+
 // --------------------------------------------------------- Alg 6.2 spectral
 // One RankOneUpdate on the small vectors, in two halves so that the U- and
 // V-side eigen-updates run on the GPU together and the host builds FMM trees meanwhile.
@@ -1583,7 +1684,7 @@ struct Joiner {
 // secular solve (STEP 2), Loewner, column norms and carried X^T v, and their read-back.
 svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<double>& D,
                             const std::vector<double>& z, double rho,
-                            const std::vector<std::vector<double>>& carries, int ev0, int side) {
+                            const std::vector<std::vector<double>>& carries, int ev0, int side, int chain) {
   TRY(ensure_side(P, side));
   const cudaStream_t st = side_stream(P, side);
   const double th_start = now_ms();
@@ -1692,9 +1793,14 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   if (na == 0) return SVD1_OK;
   const double th0 = now_ms();
   // one upload [d_a | z_a | carries] and one read-back
-  // [k (na words) | tau | cs | carry_out (nc*na) | iters (int32) | status]
+  // [k (nap words) | tau | cs | carry_out (nc*nap) | iters (int32) | status (G int32)]
+  // (nap = G c >= na: every rank's slice of c indices, the in-place all-gather layout)
+  const int G = P->world;
+  const int c_sl = slice_of(na, G, 0).c;
+  const int nap = G * c_sl;
+  S.nap = nap;
   const size_t in_words = size_t(na) * (4 + nc);
-  const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
+  const size_t words = spectral_words(nap, nc, G);
   double* din;
   double* dout;
   TRY(S.d_in.get<double>(in_words, &din, st));
@@ -1728,14 +1834,14 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   double* dz2r = din + 3 * na;
   double* dcar = din + 4 * na;
   int32_t* dk = reinterpret_cast<int32_t*>(dout);
-  double* dtau = dout + na;
-  double* dcs = dout + 2 * na;
-  double* dco = dout + 3 * na;
-  int32_t* dit = reinterpret_cast<int32_t*>(dout + size_t(3 + nc) * na);
-  int32_t* dst = reinterpret_cast<int32_t*>(dout + words - 1);
+  double* dtau = dout + nap;
+  double* dcs = dout + 2 * nap;
+  double* dco = dout + 3 * nap;
+  int32_t* dit = reinterpret_cast<int32_t*>(dout + size_t(3 + nc) * nap);
+  int32_t* dst = reinterpret_cast<int32_t*>(dout + size_t(3 + nc) * nap + size_t(nap + 1) / 2);
   double* dzh;
-  TRY(S.d_zhat.get<double>(na, &dzh, st));
-  SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), st));
+  TRY(S.d_zhat.get<double>(nap, &dzh, st));
+  SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t) * G, st));
   TRY(ev_record(P, ev0, st));
   tl_mark(P, "  ev" + std::to_string(ev0) + " uploaded", st);
   double* scr;
@@ -1743,18 +1849,39 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
   int* ctr;
   TRY(counters(S.d_ctr, na, st, &ctr));
   S.sec_fmm_used = use_sec_fmm(P->cfg.flags, na, side >= 2);  // sides 2, 3: batch mode
-  if (S.sec_fmm_used) {  // STEP 2 with the far field by FMM
-    SecFmmDev F;
-    // (reads the oriented sources from the staging region before its own upload)
+  // this process's ranks: its own, or every rank's slice in the emulation test mode
+  const int r_lo = P->emulate ? 0 : P->rank, r_hi = P->emulate ? G : P->rank + 1;
+  SecFmmDev F;
+  if (S.sec_fmm_used)  // (reads the oriented sources from the staging region before its own upload)
     TRY(secfmm_prepare(P, S.sec, S.sec_blob, S.sec_scr, stage + 2 * na, na, side, &F));
-    TRY(secular_fmm(ddr, dz2r, rho, na, F, dk, dtau, dit, dst, st, &P->launches));
-  } else {
-    TRY(secular(ddr, dz2r, rho, na, dk, dtau, dit, dst, st, &P->launches));   // STEP 2
+  for (int r = r_lo; r < r_hi; ++r) {  // STEP 2 on the roots of rank r's slice
+    const Slice sl = slice_of(na, G, r);
+    // output index range [lo, hi); the solver works in the rho > 0 view (reflected for rho < 0)
+    const int j0 = rho < 0.0 ? na - sl.hi : sl.lo, j1 = rho < 0.0 ? na - sl.lo : sl.hi;
+    if (S.sec_fmm_used)  // with the far field by FMM
+      TRY(secular_fmm(ddr, dz2r, rho, na, j0, j1, F, dk, dtau, dit, dst + r, st, &P->launches));
+    else
+      TRY(secular(ddr, dz2r, rho, na, j0, j1, dk, dtau, dit, dst + r, st, &P->launches));
   }
+  TRY(exchange(P, chain, st, {{dk, c_sl, ncclInt32, 4}, {dtau, c_sl, ncclFloat64, 8}, {dit, c_sl, ncclInt32, 4},
+                              {dst, 1, ncclInt32, 4}}));
   tl_mark(P, "  ev" + std::to_string(ev0) + " secular done", st);
-  TRY(loewner(dda, dk, dtau, rho, dza, na, dzh, scr, ctr, st, &P->launches));
+  for (int r = r_lo; r < r_hi; ++r) {
+    const Slice sl = slice_of(na, G, r);
+    TRY(loewner(dda, dk, dtau, rho, dza, na, sl.lo, sl.hi, dzh, scr, ctr, st, &P->launches));
+  }
+  TRY(exchange(P, chain, st, {{dzh, c_sl, ncclFloat64, 8}}));
   tl_mark(P, "  ev" + std::to_string(ev0) + " loewner done", st);
-  TRY(colnorm_carry(dda, dk, dtau, dzh, na, dcar, nc, dcs, dco, dst, scr, ctr, st, &P->launches));
+  for (int r = r_lo; r < r_hi; ++r) {
+    const Slice sl = slice_of(na, G, r);
+    TRY(colnorm_carry(dda, dk, dtau, dzh, na, sl.lo, sl.hi, dcar, nc, dcs, dco, nap, dst + r, scr, ctr, st,
+                      &P->launches));
+  }
+  {
+    std::vector<GatherPart> parts{{dcs, c_sl, ncclFloat64, 8}, {dst, 1, ncclInt32, 4}};
+    for (int q = 0; q < nc; ++q) parts.push_back({dco + size_t(q) * nap, c_sl, ncclFloat64, 8});
+    TRY(exchange(P, chain, st, parts));
+  }
   tl_mark(P, "  ev" + std::to_string(ev0) + " colnorm done", st);
   TRY(ev_record(P, ev0 + 1, st));
   {
@@ -1783,17 +1910,20 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
     SVD1_CUDA_TRY(cudaEventSynchronize(S.done_ev));
     S.pending = false;
   }
+  const int nap = S.nap;
   if (na > 0) {
-    const size_t words = size_t(na) * (3 + nc) + size_t(na + 1) / 2 + 2;
     const double* rb = S.rb;
-    int32_t st_h;
-    std::memcpy(&st_h, rb + words - 1, sizeof(int32_t));
+    int32_t st_h = 0;  // every rank's status word
+    {
+      const int32_t* sw = reinterpret_cast<const int32_t*>(rb + size_t(3 + nc) * nap + size_t(nap + 1) / 2);
+      for (int r = 0; r < P->world; ++r) st_h |= sw[r];
+    }
     S.k_h.resize(na);
     std::memcpy(S.k_h.data(), rb, na * sizeof(int32_t));
-    S.tau_h.assign(rb + na, rb + 2 * na);
-    S.cs_h.assign(rb + 2 * na, rb + 3 * na);
-    carry_out = rb + 3 * na;
-    const int32_t* it = reinterpret_cast<const int32_t*>(rb + size_t(3 + nc) * na);
+    S.tau_h.assign(rb + nap, rb + nap + na);
+    S.cs_h.assign(rb + 2 * nap, rb + 2 * nap + na);
+    carry_out = rb + 3 * nap;
+    const int32_t* it = reinterpret_cast<const int32_t*>(rb + size_t(3 + nc) * nap);
     double sum_it = 0.0;
     for (int j = 0; j < na; ++j) {
       S.max_iter = std::max(S.max_iter, it[j]);
@@ -1870,7 +2000,7 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
       for (int qq = 0; qq < nc; ++qq) cn[qq][q] = S.cs_sorted[qq][it.pos];
     } else {
       S.tgt_pos[it.pos] = q;
-      for (int qq = 0; qq < nc; ++qq) cn[qq][q] = carry_out[size_t(qq) * na + it.pos];
+      for (int qq = 0; qq < nc; ++qq) cn[qq][q] = carry_out[size_t(qq) * nap + it.pos];
     }
   }
   D.swap(Dn);
@@ -1970,7 +2100,7 @@ svd1_status apply_launch(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_
                          &P->launches));
   if (S.na > 0)
     TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
-                      static_cast<double*>(S.d_out.p) + S.na, static_cast<double*>(S.d_zhat.p), S.dcs,
+                      static_cast<double*>(S.d_out.p) + S.nap, static_cast<double*>(S.d_zhat.p), S.dcs,
                       U_in, ld_in, S.dsrc, U_out, ld_out, S.ddst, st, side));
   if (!S.pass_src.empty())
     TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, S.dpsrc, U_out, ld_out, S.dpdst, S.dpscale,
@@ -2039,17 +2169,18 @@ size_t fmm_blob_estimate(int64_t N, int p) {
 size_t ops_estimate(int64_t N) { return size_t(std::max<int64_t>(N, 64)) * 1024 + (size_t(64) << 10); }
 size_t maps_blob_bytes(int64_t N) { return size_t(N + 1) * 48 + 4096; }  // upload_maps / apply_upload
 
-svd1_status reserve_step(StepRecord& S, int64_t N, int p) {
+svd1_status reserve_step(StepRecord& S, int64_t N, int p, int G) {
   const int nc = kMaxCarry;
+  const int nap = G * slice_of(int(N), G, 0).c;
   TRY(S.d_in.reserve<double>(size_t(N) * (4 + nc)));
-  TRY(S.d_out.reserve<double>(size_t(N) * (3 + nc) + size_t(N + 1) / 2 + 2));
-  TRY(S.d_zhat.reserve<double>(size_t(N)));
+  TRY(S.d_out.reserve<double>(spectral_words(nap, nc, G)));
+  TRY(S.d_zhat.reserve<double>(size_t(nap)));
   TRY(S.d_scratch.reserve<double>(size_t(spectral_scratch_elems(int(N), nc))));
   TRY(S.d_ctr.reserve<int>(size_t(N / 64 + 16)));
   SVD1_CUDA_TRY(cudaMemset(S.d_ctr.p, 0, S.d_ctr.cap));
   {
     void* rb = S.rb;
-    TRY(pinned_reserve(&rb, &S.rb_cap, (size_t(N) * (3 + nc) + size_t(N + 1) / 2 + 2) * sizeof(double)));
+    TRY(pinned_reserve(&rb, &S.rb_cap, spectral_words(nap, nc, G) * sizeof(double)));
     S.rb = static_cast<double*>(rb);
   }
   TRY(S.blob.reserve<char>(maps_blob_bytes(N) + fmm_blob_estimate(N, p)));
@@ -2105,9 +2236,9 @@ svd1_status plan_reserve(svd1_plan_t P) {
   // step records: per-update (steps) and the batch mode's two parities (bsteps)
   for (int e = 0; e < 4; ++e) {
     const int64_t N = e < 2 ? m : nv;
-    TRY(reserve_step(P->steps[e], N, p));
-    TRY(reserve_step(P->bsteps[0][e], N, p));
-    TRY(reserve_step(P->bsteps[1][e], N, p));
+    TRY(reserve_step(P->steps[e], N, p, P->world));
+    TRY(reserve_step(P->bsteps[0][e], N, p, P->world));
+    TRY(reserve_step(P->bsteps[1][e], N, p, P->world));
   }
   // batch mode (svd1_update_batch): projections, carried rows, few-rows scratch, Gram
   const int ru_max = 4 + (kMaxBatch - 1), rv_max = kMaxBatch - 1;
@@ -2156,11 +2287,23 @@ const char* svd1_status_string(svd1_status s) {
     case SVD1_E_ZEROCOL: return "zero or non-finite column norm";
     case SVD1_E_CUDA: return "CUDA error";
     case SVD1_E_NOMEM: return "out of memory";
+    case SVD1_E_NCCL: return "NCCL error";
   }
   return "unknown status";
 }
 
-const char* svd1_version(void) { return "svd1 0.1 (sm_100a, fp64 DMMA)"; }
+const char* svd1_version(void) { return "svd1 0.2 (sm_100a, fp64 DMMA)"; }
+
+svd1_status svd1_nccl_unique_id(void* out) {
+  if (!out) return SVD1_E_INVALID;
+  const NcclApi& A = nccl_api();
+  if (!A.ok) return SVD1_E_NCCL;
+  ncclUniqueId id;
+  NCCL_TRY(A.GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out, &id, sizeof(id));
+  return SVD1_OK;
+}
 
 svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out) {
   if (!cfg || !out) return SVD1_E_INVALID;
@@ -2169,12 +2312,37 @@ svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out) {
       cfg->v_row0 + cfg->v_rows > cfg->n)
     return SVD1_E_INVALID;
   if (!(cfg->eps > 0.0 && cfg->eps < 1.0)) return SVD1_E_INVALID;
+  const int world = std::max(1, int(cfg->world));
+  if (cfg->rank < 0 || cfg->rank >= world) return SVD1_E_INVALID;
+  const bool emulate = (cfg->flags & SVD1_EMULATE_RANKS) != 0;
+  const bool use_nccl = !emulate && (world > 1 || (cfg->flags & SVD1_FORCE_NCCL));
+  if (use_nccl && !cfg->nccl_id) return SVD1_E_INVALID;
   svd1_plan_t P = new (std::nothrow) svd1_plan_s();
   if (!P) return SVD1_E_NOMEM;
   P->cfg = *cfg;
   P->st = static_cast<cudaStream_t>(cfg->stream);
   P->p = choose_p(cfg->eps);
   P->leaf = 2 * P->p;
+  P->world = world;
+  P->rank = emulate ? 0 : int(cfg->rank);
+  P->emulate = emulate && world > 1;
+  P->use_nccl = use_nccl;
+  if (use_nccl) {  // collective: every rank creates its plan
+    const NcclApi& A = nccl_api();
+    if (!A.ok) {
+      delete P;
+      return SVD1_E_NCCL;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof(id));
+    ncclResult_t r = A.CommInitRank(&P->comm[0], world, id, int(cfg->rank));
+    if (r == ncclSuccess) r = A.CommSplit(P->comm[0], 0, int(cfg->rank), &P->comm[1], nullptr);
+    if (r != ncclSuccess) {
+      nccl_fail(r, "communicator creation");
+      svd1_plan_destroy(P);
+      return SVD1_E_NCCL;
+    }
+  }
   const svd1_status st = plan_reserve(P);
   if (st != SVD1_OK) {
     svd1_plan_destroy(P);
@@ -2210,6 +2378,8 @@ svd1_status svd1_plan_destroy(svd1_plan_t P) {
   }
   for (auto& q : P->sp)
     if (q) cudaStreamDestroy(q);
+  for (auto& cm : P->comm)
+    if (cm) nccl_api().CommDestroy(cm);
   delete P;
   return SVD1_OK;
 }
@@ -2266,7 +2436,7 @@ svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, in
     double* scr;
     TRY(P->few_scr[side].get<double>(size_t(few_rows_scratch_elems(rows, S.na)), &scr, st));
     TRY(apply_few_rows(rows, S.na, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
-                       static_cast<double*>(S.d_out.p) + S.na, static_cast<double*>(S.d_zhat.p), S.dcs, in, ld,
+                       static_cast<double*>(S.d_out.p) + S.nap, static_cast<double*>(S.d_zhat.p), S.dcs, in, ld,
                        S.dsrc, out, ld, S.ddst, scr, st, &P->launches));
   }
   if (!S.pass_src.empty())
@@ -2411,9 +2581,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     cv.swap(cv1);
     const std::string ut = B ? "u" + std::to_string(B->t) + " " : "";
     tl_mark(P, ut + "U1 spectral", side_stream(P, sp0));
-    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8, sp0));
+    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8, sp0, 0));
     tl_mark(P, ut + "V1 spectral", side_stream(P, sp1));
-    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, sp1));
+    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, sp1, 1));
   }
   const double tA = now_ms();
   std::atomic<bool> planned[4] = {false, false, false, false};  // outlives the Joiners
@@ -2567,7 +2737,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       std::vector<double> z2 = cu[0];
       cu.erase(cu.begin());
       tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U1 finished; U2 spectral", side_stream(P, sp0));
-      TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, sp0));
+      TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, sp0, 0));
       t_fin[0] = now_ms();
       continue;
     }
@@ -2579,7 +2749,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       std::vector<double> z4 = cv[0];
       cv.erase(cv.begin());
       tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V1 finished; V2 spectral", side_stream(P, sp1));
-      TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, sp1));
+      TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, sp1, 1));
       t_fin[2] = now_ms();
       continue;
     }
@@ -3146,9 +3316,9 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
     SecFmmDev F;
     TRY(arena_reset(P));
     TRY(secfmm_prepare(P, P->steps[0].sec, P->steps[0].sec_blob, P->steps[0].sec_scr, dr.data(), int(n), 0, &F));
-    TRY(secular_fmm(orient, orient + n, rho, int(n), F, k_out, tau_out, dit, dst, P->st, &P->launches));
+    TRY(secular_fmm(orient, orient + n, rho, int(n), 0, int(n), F, k_out, tau_out, dit, dst, P->st, &P->launches));
   } else {
-    TRY(secular(orient, orient + n, rho, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
+    TRY(secular(orient, orient + n, rho, int(n), 0, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
   }
   std::vector<int32_t> it(n);
   int32_t st_h = 0;
@@ -3168,7 +3338,7 @@ svd1_status svd1_loewner(svd1_plan_t P, int64_t n, const double* d, const int32_
   TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr, P->st));
   int* ctr;
   TRY(counters(P->ctr, int(n), P->st, &ctr));
-  TRY(loewner(d, k, tau, rho, z, int(n), zhat_out, scr, ctr, P->st, &P->launches));
+  TRY(loewner(d, k, tau, rho, z, int(n), 0, int(n), zhat_out, scr, ctr, P->st, &P->launches));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   return SVD1_OK;
 }
@@ -3186,7 +3356,8 @@ svd1_status svd1_colnorms(svd1_plan_t P, int64_t n, const double* d, const int32
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
   int* ctr;
   TRY(counters(P->ctr, int(n), P->st, &ctr));
-  TRY(colnorm_carry(d, k, tau, zhat, int(n), nullptr, 0, cs, nullptr, dst, scr, ctr, P->st, &P->launches));
+  TRY(colnorm_carry(d, k, tau, zhat, int(n), 0, int(n), nullptr, 0, cs, nullptr, n, dst, scr, ctr, P->st,
+                    &P->launches));
   std::vector<double> h(n);
   SVD1_CUDA_TRY(cudaMemcpyAsync(h.data(), cs, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));

@@ -57,7 +57,8 @@ int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t
 // K2: secular roots (warp per root).  status bit 1 = no convergence, 2 = pole.
 // d, z2: the rho > 0 view of the problem (for rho < 0: -d reversed, z^2 reversed);
 // outputs (k, tau) are in the original orientation.
-svd1_status secular(const double* d, const double* z2, double rho, int n, int32_t* k_out,
+// roots j0 <= j < j1 of the rho > 0 view (a rank's slice; 0, n: all)
+svd1_status secular(const double* d, const double* z2, double rho, int n, int j0, int j1, int32_t* k_out,
                     double* tau_out, int32_t* iters_out, int32_t* status, cudaStream_t st,
                     int64_t* launches);
 svd1_status secular_orient(const double* d, const double* z, double rho, int n, double* dr,
@@ -97,20 +98,22 @@ struct SecFmmDev {         // device view of one plan
   double* psiL;             // ncells * kSecP local expansions: sources left of the interval
   double* psiR;             //                                 and right of it
 };
-svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, const SecFmmDev& F,
-                        int32_t* k_out, double* tau_out, int32_t* iters_out, int32_t* status,
-                        cudaStream_t st, int64_t* launches);
+svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, int j0, int j1,
+                        const SecFmmDev& F, int32_t* k_out, double* tau_out, int32_t* iters_out,
+                        int32_t* status, cudaStream_t st, int64_t* launches);
 
 // K3a: Loewner zhat (thread per i, split-j partial products + ordered combine)
+// (zhat_i for i0 <= i < i1: a rank's slice)
 svd1_status loewner(const double* d, const int32_t* k, const double* tau, double rho,
-                    const double* z, int n, double* zhat, double* scratch, int* ctr, cudaStream_t st,
-                    int64_t* launches);
+                    const double* z, int n, int i0, int i1, double* zhat, double* scratch, int* ctr,
+                    cudaStream_t st, int64_t* launches);
 // K3b + K12: colscale_j = 1/||c_j|| and carry_out[q][j] = (X^T carry_q)_j
 // (thread per j, split-i partial sums + ordered combine).
+// (columns j0 <= j < j1: a rank's slice; carry_out[q] at carry_out + q * ldc)
 svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
-                          const double* zhat, int n, const double* carry, int ncarry,
-                          double* colscale, double* carry_out, int32_t* status, double* scratch, int* ctr,
-                          cudaStream_t st, int64_t* launches);
+                          const double* zhat, int n, int j0, int j1, const double* carry, int ncarry,
+                          double* colscale, double* carry_out, int64_t ldc, int32_t* status, double* scratch,
+                          int* ctr, cudaStream_t st, int64_t* launches);
 
 // K11: direct apply  U_out[r, dst[j]] = cs[j] * sum_i U_in[r, src[i]] zhat[i] / ((d_i - d_kj) - tau_j)
 svd1_status apply_direct(int64_t rows, int n, const double* d, const int32_t* k,

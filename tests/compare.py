@@ -9,7 +9,31 @@ Readings:
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
+
+EPS = 2.0 ** -52
+
+
+def log_parity(name, **metrics):
+    """Append one JSON line of measured parity metrics to $SVD1_PARITY_LOG (if set): the
+    evidence behind the asserted bounds (profiles/parity_r02.jsonl)."""
+    path = os.environ.get("SVD1_PARITY_LOG")
+    if not path:
+        return
+
+    def clean(x):
+        if isinstance(x, dict):
+            return {k: clean(v) for k, v in x.items() if not k.startswith("_")}
+        if isinstance(x, (list, tuple)):
+            return [clean(v) for v in x]
+        if isinstance(x, (np.floating, np.integer)):
+            return x.item()
+        return x
+    with open(path, "a") as f:
+        f.write(json.dumps({"test": name, **clean(metrics)}) + "\n")
 
 
 def sigma_errors(s, s_ref):
@@ -18,14 +42,28 @@ def sigma_errors(s, s_ref):
     Gram matrices (STEP 8 P:350), whose rounding-level sensitivity is
     eps * sigma_1^2 in sigma^2.  Returns dict(gram = max|s^2 - s*^2| / s*_1^2,
     rel_top = max relative error over s*_i >= 0.1 s*_1, rel = max relative error
-    over all s*_i > 0)."""
+    over all s*_i > 0).
+    Also the strict per-sigma error against its rounding sensitivity: a
+    Gram eigenvalue perturbed by eps sigma_1^2 moves sigma_i by eps (sigma_1/sigma_i)^2 / 2
+    relative, so rel_sens = max_i rel_i / (eps (sigma_1/sigma_i)^2 / 2) is the strict error
+    in units of that bound (D2's gram <= 1e-12 implies rel_sens <= 1e-12 / eps ~ 4.5e3),
+    with the sigma_i where it is attained (sens_at)."""
     s = np.asarray(s, np.float64)
     s_ref = np.asarray(s_ref, np.float64)
     s1 = float(np.max(np.abs(s_ref)))
     gram = float(np.max(np.abs(s * s - s_ref * s_ref)) / max(s1 * s1, 1e-300))
     rel = np.abs(s - s_ref) / np.maximum(s_ref, 1e-300)
     top = s_ref >= 0.1 * s1
-    return dict(gram=gram, rel_top=float(np.max(rel[top])), rel=float(np.max(rel[s_ref > 0])) if np.any(s_ref > 0) else 0.0)
+    pos = s_ref > 0
+    out = dict(gram=gram, rel_top=float(np.max(rel[top])), rel=float(np.max(rel[pos])) if np.any(pos) else 0.0,
+               rel_sens=0.0, sens_at=None)
+    if np.any(pos):
+        sens = EPS * (s1 / s_ref[pos]) ** 2 / 2.0
+        r = rel[pos] / sens
+        i = int(np.argmax(r))
+        out["rel_sens"] = float(r[i])
+        out["sens_at"] = float(s_ref[pos][i] / s1)
+    return out
 
 
 def clusters(eigs, gap_tol=1e-3):
@@ -74,3 +112,22 @@ def vector_error_rows(Qr, Qr_ref, eigs_ref, gap_tol=1e-3, cols=None):
     sign on the sampled entries; clusters through the projector restricted to the
     sampled rows, sum_c q_rc q_r'c."""
     return vector_error(Qr, Qr_ref, eigs_ref, gap_tol, cols)
+
+
+def assert_parity(name, r, vec_tol=1e-9, res_tol=1e-10, orth_tol=1e-10, **extra):
+    """The north star's tolerances with readings D2-D4 on a result dict
+    r = dict(sigma=sigma_errors(...), U=vector_error(...), V=..., res=..., orth=...)
+    (U, V, res, orth optional); logs the measured values first (log_parity)."""
+    log_parity(name, **{k: v for k, v in r.items() if k in ("sigma", "U", "V", "res", "orth")}, **extra)
+    se = r["sigma"]
+    assert se["gram"] <= 1e-12 and se["rel_top"] <= 1e-12, (name, se)
+    # strict per-sigma error within its rounding sensitivity (implied by gram; asserted so
+    # that the reported figure is checked too)
+    assert se["rel_sens"] <= 1e4, (name, se)
+    for side in ("U", "V"):
+        if r.get(side) is not None:
+            assert r[side]["isolated"] <= vec_tol and r[side]["cluster"] <= vec_tol, (name, side, r[side])
+    if r.get("res") is not None:
+        assert r["res"] <= res_tol, (name, r["res"])
+    if r.get("orth") is not None:
+        assert r["orth"] <= orth_tol, (name, r["orth"])

@@ -6,6 +6,7 @@ residual, orthogonality)."""
 import numpy as np
 import pytest
 
+from compare import log_parity, vector_error
 from synth import config_inputs
 
 pytestmark = pytest.mark.gpu
@@ -70,10 +71,19 @@ def test_batch_matches_sequential(cfg, m, n, K, flags, exact):
     for Z in ((Ub, sb, Vb), (Us, ss, Vs)):
         res, orth, sig_err = _invariants(inp, K, *Z)
         assert res <= 1e-10 and orth <= 1e-10 and sig_err <= 1e-12, (res, orth, sig_err)
-    if exact:  # isolated singular values: same vectors (signs included) up to rounding
-        m_ = Ub.shape[0]
-        assert float((Ub - Us).abs().max()) <= 1e-8
-        assert float((Vb[:, :m_] - Vs[:, :m_]).abs().max()) <= 1e-8
+    m_ = Ub.shape[0]
+    du, dv = float((Ub - Us).abs().max()), float((Vb[:, :m_] - Vs[:, :m_]).abs().max())
+    # gap-aware (Q27) difference: columns up to sign where the relative eigengap >= 1e-3,
+    # cluster projectors elsewhere -- the same reading as the oracle parity
+    gu = vector_error(Ub.cpu().numpy(), Us.cpu().numpy(), ssn ** 2)
+    gv = vector_error(Vb[:, :m_].cpu().numpy(), Vs[:, :m_].cpu().numpy(), ssn ** 2)
+    log_parity(f"batch vs sequential C{cfg} {m}x{n} K={K} flags={flags}", max_abs_U=du, max_abs_V=dv, gap_U=gu,
+               gap_V=gv, sigma_rel=float(np.max(np.abs(sbn - ssn)) / ssn[0]))
+    assert max(gu["isolated"], gu["cluster"], gv["isolated"], gv["cluster"]) <= 1e-10, (gu, gv)
+    if exact:  # elementwise, signs included: the graded C3 recipe's near-degenerate columns
+        # (relative gap < 1e-3, determined only to eps sigma_1^2 / gap) differ by up to ~1e-10
+        # (measured 9.3e-11, profiles/parity_r02.jsonl); column/cluster-wise <= 2e-13
+        assert du <= 1e-9 and dv <= 1e-9, (du, dv)
     assert [r["n_active"] for r in rb] == [r["n_active"] for r in rs]
 
 

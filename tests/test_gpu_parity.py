@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from compare import sigma_errors, vector_error
+from compare import assert_parity, sigma_errors, vector_error
 from synth import config_inputs, interlaced_cauchy, random_secular
 
 pytestmark = pytest.mark.gpu
@@ -137,10 +137,7 @@ def test_update_parity(cfg, m, n, flags):
     inp = config_inputs(cfg, m=m, n=n, updates=1)
     a, b = inp["ab"][0]
     r = _check_update(inp["U"], inp["sigma"], inp["V"], a, b, flags=flags)
-    assert r["sigma"]["gram"] <= 1e-12 and r["sigma"]["rel_top"] <= 1e-12, r
-    assert r["U"]["isolated"] <= 1e-9 and r["U"]["cluster"] <= 1e-9, r
-    assert r["V"]["isolated"] <= 1e-9 and r["V"]["cluster"] <= 1e-9, r
-    assert r["res"] <= 1e-10 and r["orth"] <= 1e-10, r
+    assert_parity(f"update_parity C{cfg} {m}x{n} flags={flags}", r)
 
 
 def test_update_noop_and_errors():
@@ -169,10 +166,11 @@ def test_update_stream_c3_small():
         plan.update(Ug, sg, Vg, T(a), T(b))
         A = A + np.outer(a, b)
         e = sigma_errors(N(sg), ref["sigma"])
-        assert e["gram"] <= 1e-12 and e["rel_top"] <= 1e-12
         At = T(A)
         res = float(torch.linalg.norm(At @ Vg - Ug * sg[None, :], dim=0).max() / sg[0])
-        assert res <= 1e-10
+        eu = vector_error(N(Ug), ref["U"], ref["sigma"] ** 2)
+        ev = vector_error(N(Vg), ref["V"], ref["info"]["Dv_hat"])
+        assert_parity("stream_c3_small step", dict(sigma=e, U=eu, V=ev, res=res))
 
 
 @pytest.mark.parametrize("n,flags", [(24, 0), (600, P.FORCE_FMM)])
@@ -228,7 +226,9 @@ def test_update_parity_secular_fmm(cfg, m, n):
     """Whole updates with every secular solve on the FMM path (D2-D4 tolerances)."""
     inp = config_inputs(cfg, m=m, n=n, updates=1)
     a, b = inp["ab"][0]
-    _check_update(inp["U"], inp["sigma"], inp["V"], a, b, flags=P.SECULAR_FMM)
+    r = _check_update(inp["U"], inp["sigma"], inp["V"], a, b, flags=P.SECULAR_FMM)
+    assert r["rep"]["n_active"][0] > 64  # the FMM secular solve ran (sizes > 64)
+    assert_parity(f"update_parity_secular_fmm C{cfg} {m}x{n}", r)
 
 
 def test_rectangular_stream_null_root():

@@ -120,3 +120,50 @@ def test_sharded_batch_projection_allreduce():
     for _, err, scale, _ in res:
         assert err <= 1e-13 * scale
     assert res[0][3] == res[1][3]
+
+
+def _slice_worker(rank, world, port, n, q):
+    """One rank of the sliced spectral exchange: the NCCL id from rank 0,
+    then this rank's slice of per-root results gathered in place into the padded G*c
+    buffer the library uses (gloo stands in for NCCL's in-place all-gather here)."""
+    import oracle as O
+    from paper_1707_08369_b200.parallel import shared_nccl_id, spectral_slice
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nid = shared_nccl_id(rank, world)
+    rng = np.random.default_rng(3)
+    d = np.sort(rng.standard_normal(n))
+    z = rng.standard_normal(n)
+    rho = 0.7
+    k, tau = O.secular_roots_bisect(d, z, rho)          # (replicated inputs of the slice stage)
+    lo, hi = spectral_slice(n, rank, world)
+    c = -(-n // world)
+    mine = torch.zeros(c, dtype=torch.float64)
+    mine[:hi - lo] = torch.from_numpy(O.secular_w(d, z, rho, k[lo:hi], tau[lo:hi]))
+    buf = torch.zeros(world * c, dtype=torch.float64)
+    dist.all_gather_into_tensor(buf, mine)
+    full = O.secular_w(d, z, rho, k, tau)
+    q.put((rank, nid, bool(np.array_equal(buf.numpy()[:n], full)), lo, hi))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 101), (3, 100), (3, 2)])
+def test_sliced_spectral_exchange(world, n):
+    """World-size 2-3 (gloo): every rank receives rank 0's 128-byte NCCL id; the slices
+    tile [0, n) (ragged last slice, empty slices when n < world) and their in-place gather
+    reproduces the one-process per-root results bitwise."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slice_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    ids = {r[1] for r in res}
+    assert len(ids) == 1 and len(next(iter(ids))) == 128
+    assert all(r[2] for r in res)
+    assert res[0][3] == 0 and res[-1][4] == n
+    assert all(res[i][4] == res[i + 1][3] for i in range(world - 1))
