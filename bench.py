@@ -104,69 +104,81 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def oracle_sample_time(inp, steps, rows_sample=256):
-    """Time the CPU oracle on one C3 update per step (full spectral phase; the explicit
-    O(rows n^2) products on `rows_sample` sampled rows of U and V, O8)."""
+def cpu_info():
+    """Host description for the CPU numbers: logical CPUs and model."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def oracle_update_times(inp, steps, threads=None):
+    """The CPU oracle (oracle/, as it stands) running WHOLE C3 updates of the stream in
+    order (each on the previous step's output): Alg 6.1 with the literal STEP-1 products,
+    bisection over every root, Loewner, X and the explicit O(n^3) products on ALL rows of
+    U and V (no sampling, nothing extrapolated); sign rule by probes (pinned equal to the
+    explicit rule).  threads: oracle threads and BLAS threads (None = all host cores).
+    Returns the per-step times (s)."""
     import oracle as O
+    import oracle.svd1_oracle as OM
     U, s, V = inp["U"], inp["sigma"], inp["V"]
     if not isinstance(U, np.ndarray):
         U, s, V = U.cpu().numpy(), s.cpu().numpy(), V.cpu().numpy()
-    m = U.shape[0]
-    rows = (np.arange(0, m, max(1, m // rows_sample)), np.arange(0, V.shape[0], max(1, V.shape[0] // rows_sample)))
+    from contextlib import nullcontext
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    old = OM.THREADS
     t = []
-    for k in range(steps):
-        a, b = inp["ab"][k % len(inp["ab"])]
-        t0 = time.perf_counter()
-        O.svd_update(U, s, V, a, b, sign_rule="probe", rows=rows)
-        t.append(time.perf_counter() - t0)
-    return t, len(rows[0])
-
-
-def oracle_eigen_update_time(inp, steps, rows_sample=256):
-    """The reference arm's bounded step: ONE of an update's four symmetric eigen-updates
-    (Alg 6.2 RankOneUpdate: the U side's first, rho1 > 0) run by the oracle as it stands --
-    bisection over all n roots, Loewner, X, the explicit product on `rows_sample` sampled
-    rows -- for the stream's update k (inputs formed outside the timed call)."""
-    import oracle as O
-    U, s, V = inp["U"], inp["sigma"], inp["V"]
-    if not isinstance(U, np.ndarray):
-        U, s, V = U.cpu().numpy(), s.cpu().numpy(), V.cpu().numpy()
-    m = U.shape[0]
-    rows = np.arange(0, m, max(1, m // rows_sample))
-    t = []
-    for k in range(steps):
-        a, b = inp["ab"][k % len(inp["ab"])]
-        ing = O.prepare_update(U, s, V, a, b)
-        rho1, _, Qu = O.schur_update_2x2(ing["beta"])
-        a1 = Qu[0, 0] * a + Qu[1, 0] * ing["b_tilde"]
-        z1 = U.T @ a1
-        t0 = time.perf_counter()
-        O.rank_one_update(U[rows], s * s, rho1, z=z1)
-        t.append(time.perf_counter() - t0)
-    return t, len(rows)
+    cm = threadpool_limits(limits=threads) if (threads and threadpool_limits) else nullcontext()
+    try:
+        if threads:
+            OM.THREADS = threads
+        with cm:
+            for k in range(steps):
+                a, b = inp["ab"][k % len(inp["ab"])]
+                t0 = time.perf_counter()
+                r = O.svd_update(U, s, V, a, b, sign_rule="probe")
+                t.append(time.perf_counter() - t0)
+                U, s, V = r["U"], r["sigma"], r["V"]
+    finally:
+        OM.THREADS = old
+    return t
 
 
 def run_reference(args, rank, world):
+    """The reference arm for this tier: the CPU oracle on the same workload and metric
+    (C3 updates/s), each step one whole C3 update of the stream (all rows, full explicit
+    products), on all host cores; rank 0 alone (the others exit without work)."""
     if rank != 0:
         return
     from synth import config_inputs
     inp = config_inputs(CFG_ID)
-    # each step = one of the four eigen-updates of an update (the bounded sample that
-    # keeps --steps K --warmup W within minutes); an update is four of them
-    _, _ = oracle_eigen_update_time(inp, args.warmup)
-    t, nr = oracle_eigen_update_time(inp, args.steps)
+    oracle_update_times(inp, args.warmup)
+    t0 = time.perf_counter()
+    t = oracle_update_times(inp, args.steps)
+    wall = time.perf_counter() - t0
     total = sum(t)
-    val = args.steps / (4.0 * total)
-    cores = os.cpu_count()
-    sample = (f"per step: one of the C3 update's four symmetric eigen-updates by the oracle (secular "
-              f"bisection over all 4096 roots, Loewner, X, explicit product on {nr} sampled rows of U); "
-              f"updates/s = steps / (4 x time)")
+    val = args.steps / total
+    import oracle.svd1_oracle as OM
+    sample = ("per step: one whole C3 update of the 16-update stream (m = n = 4096) by the oracle: literal "
+              "STEP-1 products, bisection over all 4096 roots of each of the 4 eigen-updates, Loewner, X, explicit "
+              "products on all 4096 rows of U and V; nothing sampled or extrapolated")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 4e3 * total / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "m": 4096, "n": 4096},
-            "ms_per_eigen_update": 1e3 * total / args.steps,
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "data": "synthetic (seeded, BASELINE.json C3 recipe)",
+            "config": {"workload": WORKLOAD, "m": 4096, "n": 4096, "eps": 1e-10},
+            "timed_wall_s": wall,
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": OM.THREADS, "kind": "oracle", "sample": sample,
+                             **cpu_info()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -443,11 +455,17 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == CFG_ID:
         from synth import config_inputs as ci
+        import oracle.svd1_oracle as OM
         cin = ci(CFG_ID)
-        t, nr = oracle_sample_time(cin, 1)
-        cpu = {"value": 1.0 / t[0], "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"one C3 update: full spectral phase (bisection, Loewner, norms) + explicit "
-                         f"Cauchy products on {nr} sampled rows of U and V (of 4096); numpy fp64"}
+        t_all = oracle_update_times(cin, 2)          # two whole updates, all host cores
+        t_one = oracle_update_times(cin, 1, threads=1)  # one whole update, one core
+        cpu = {"value": len(t_all) / sum(t_all), "unit": UNIT, "cores": OM.THREADS, "kind": "oracle",
+               "sample": ("updates 0-1 of the C3 stream, each a whole update by the oracle (literal STEP-1 "
+                          "products, bisection over all roots, Loewner, explicit products on all 4096 rows of U "
+                          "and V; numpy fp64, oracle and BLAS threads on every host core); nothing sampled"),
+               "seconds_per_update": t_all, "one_core": {"value": 1.0 / t_one[0], "unit": UNIT, "cores": 1,
+                                                          "seconds_per_update": t_one[0]},
+               **cpu_info()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "svd1_internal.cuh"
 
@@ -400,14 +401,29 @@ struct GemmCfg {
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STAGES * (16 + 16);
 };
 
+// Tile -> (task, row block).  Task-major (default): consecutive CTAs take the same task's
+// row blocks (its operator chunks stay hot, the A windows stream down the rows).
+// Row-block-major (SVD1_TILE_ORDER=rb): the CTAs in flight cover a few row blocks and every
+// task, so shared input rows are re-read from L2 -- measured at C3: DRAM per apply 1.26 ->
+// 1.10 GB, but 481 -> 505 us (the passes are not DRAM-bound), hence not the default.
+__device__ __forceinline__ int tile_task(int tile, int nrb, int ntask, int rb_major) {
+  return rb_major ? tile % ntask : tile / nrb;
+}
+__device__ __forceinline__ int tile_rb(int tile, int nrb, int ntask, int rb_major) {
+  return rb_major ? tile / ntask : tile % nrb;
+}
+
 struct StageInfo {
-  int32_t tile;  // tile the chunk belongs to; -1: no more chunks
-  int32_t last;  // 1: last chunk of the tile (epilogue after it)
+  int32_t tile;   // tile the chunk belongs to; -1: no more chunks
+  int32_t last;   // 1: last chunk of the tile (epilogue after it)
+  int32_t kindN;  // the tile's task: out_kind << 8 | N (read by the epilogue from shared
+  int32_t col0;   //   memory, not from global memory)
 };
 
 template <int BN>
 __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
     const FmmMaps* __restrict__ maps, const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int ntiles, int nrb,
+    int ntask, int rb_major,
     int64_t rows, double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst,
     double* __restrict__ phi, double* __restrict__ psi, int64_t ldE, int64_t out_cols, int64_t exp_elems,
     const double* __restrict__ ops_raw, int64_t ops_rows) {
@@ -437,6 +453,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
     // tracked by the stage's full barrier (32 noinc arrivals + lane 0's expect_tx).
     // (A TMA load of the op chunk, written by the operator kernel just before, was
     // measured to return stale data when another stream's kernels ran concurrently.)
+    // Descriptors: the next tile's task is loaded while this tile's chunks are issued, and
+    // a task's terms are loaded once, one per lane (no global round trip per term).
     const int w = BN == 32 ? 1 : 0;
     const CUtensorMap* tm_u = &maps->u[w];
     const CUtensorMap* tm_phi = &maps->phi[w];
@@ -446,41 +464,58 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(m) : "memory");
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int task = tile / nrb;
-      const int row0 = (tile - task * nrb) * G::BM;
-      const FmmTask T = tasks[task];
-      for (int t = T.t_begin; t < T.t_end; ++t) {
-        const FmmTerm R = terms[t];
-        const CUtensorMap* ma = R.in_kind == IO_U ? tm_u : (R.in_kind == IO_PHI ? tm_phi : tm_psi);
-        for (int k0 = 0; k0 < R.K; k0 += KC) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          const int64_t brow = R.op_row + int64_t(k0 / KC) * R.npad + T.op_col0;
-          const double* bsrc = ops_raw + brow * 16;
-          unsigned char* bdst = sB + stage * G::B_BYTES;
-          for (int q = lane; q < BN * 8; q += 32) {
-            const int n = q >> 3, j = q & 7;
-            const int64_t row = brow + n;
-            const bool ok = row < ops_rows;
-            const unsigned sa = smem_u32(bdst + n * 128 + ((j ^ (n & 7)) << 4));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
-                         "l"(bsrc + (ok ? n * 16 + 2 * j : 0)), "r"(ok ? 16 : 0));
-          }
-          if (lane == 0) {
-            info[stage] = StageInfo{tile, (t == T.t_end - 1 && k0 + KC >= R.K) ? 1 : 0};
-            mbar_arrive_tx(&full[stage], G::A_BYTES);
-            tma_load_2d(sA + stage * G::A_BYTES, ma, R.col0 + k0, row0, &full[stage]);
-          }
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[stage])) : "memory");
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
+    int tile = blockIdx.x;
+    FmmTask T{};
+    if (tile < ntiles) T = tasks[tile_task(tile, nrb, ntask, rb_major)];
+    while (tile < ntiles) {
+      const int next = tile + gridDim.x;
+      FmmTask Tn{};
+      if (next < ntiles) Tn = tasks[tile_task(next, nrb, ntask, rb_major)];  // in flight while this tile is issued
+      const int row0 = tile_rb(tile, nrb, ntask, rb_major) * G::BM;
+      const int32_t kindN = (T.out_kind << 8) | T.N;
+      for (int tb = T.t_begin; tb < T.t_end; tb += 32) {
+        FmmTerm mine{};
+        if (tb + lane < T.t_end) mine = terms[tb + lane];
+        const int nterm = min(32, T.t_end - tb);
+        for (int q = 0; q < nterm; ++q) {
+          const int in_kind = __shfl_sync(0xffffffffu, mine.in_kind, q);
+          const int col0 = __shfl_sync(0xffffffffu, mine.col0, q);
+          const int K = __shfl_sync(0xffffffffu, mine.K, q);
+          const int npad = __shfl_sync(0xffffffffu, mine.npad, q);
+          const int64_t op_row = __shfl_sync(0xffffffffu, mine.op_row, q);
+          const CUtensorMap* ma = in_kind == IO_U ? tm_u : (in_kind == IO_PHI ? tm_phi : tm_psi);
+          const bool last_term = tb + q == T.t_end - 1;
+          for (int k0 = 0; k0 < K; k0 += KC) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const int64_t brow = op_row + int64_t(k0 / KC) * npad + T.op_col0;
+            const double* bsrc = ops_raw + brow * 16;
+            unsigned char* bdst = sB + stage * G::B_BYTES;
+            for (int e = lane; e < BN * 8; e += 32) {
+              const int n = e >> 3, j = e & 7;
+              const int64_t row = brow + n;
+              const bool ok = row < ops_rows;
+              const unsigned sa = smem_u32(bdst + n * 128 + ((j ^ (n & 7)) << 4));
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                           "l"(bsrc + (ok ? n * 16 + 2 * j : 0)), "r"(ok ? 16 : 0));
+            }
+            if (lane == 0) {
+              info[stage] = StageInfo{tile, (last_term && k0 + KC >= K) ? 1 : 0, kindN, T.col0};
+              mbar_arrive_tx(&full[stage], G::A_BYTES);
+              tma_load_2d(sA + stage * G::A_BYTES, ma, col0 + k0, row0, &full[stage]);
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[stage])) : "memory");
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
+      tile = next;
+      T = Tn;
     }
     mbar_wait(&empty[stage], phase ^ 1);
-    if (lane == 0) info[stage] = StageInfo{-1, -1};
+    if (lane == 0) info[stage] = StageInfo{-1, -1, 0, 0};
     __syncwarp();
     mbar_arrive(&full[stage]);
     if (lane == 0) mbar_arrive(&full[stage]);  // 33 arrivals per phase
@@ -501,10 +536,26 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
     for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   int stage = 0;
   uint32_t phase = 0;
+  int cur_tile = -1;
+  int dcol[NT][2];  // output columns of this lane's accumulators (IO_U: through dst[]),
+                    // loaded at the tile's first chunk, used by its epilogue
   for (;;) {
     mbar_wait(&full[stage], phase);
     const StageInfo I = info[stage];
     if (I.last < 0) break;
+    if (I.tile != cur_tile) {
+      cur_tile = I.tile;
+      const int N = I.kindN & 255;
+      if ((I.kindN >> 8) == IO_U) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int jj = nt * 8 + 2 * t4;
+          const int col = I.col0 + jj;
+          dcol[nt][0] = jj < N ? (dst ? __ldg(dst + col) : col) : -1;
+          dcol[nt][1] = jj + 1 < N ? (dst ? __ldg(dst + col + 1) : col + 1) : -1;
+        }
+      }
+    }
     const unsigned char* a = sA + stage * G::A_BYTES + a_row;
     const unsigned char* b = sB + stage * G::B_BYTES + b_row;
 #pragma unroll
@@ -515,13 +566,16 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
       for (int mt = 0; mt < 4; ++mt) af[mt] = lds128(a + mt * 8 * 128 + sw);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) bf[nt] = lds128(b + nt * 8 * 128 + sw);
+      // every accumulator's first k-step, then every accumulator's second: 4 NT
+      // independent DMMAs between two that share an accumulator
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          dmma_8x8x4(acc[mt][nt], af[mt].x, bf[nt].x);
-          dmma_8x8x4(acc[mt][nt], af[mt].y, bf[nt].y);
-        }
+        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt].x, bf[nt].x);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt].y, bf[nt].y);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -530,18 +584,18 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
       phase ^= 1;
     }
     if (I.last) {  // epilogue of tile I.tile (registers -> global)
-      const int task = I.tile / nrb;
-      const int64_t row0 = int64_t(I.tile - task * nrb) * G::BM;
-      const FmmTask T = tasks[task];
-      double* E = T.out_kind == IO_PHI ? phi : psi;
+      const int task = tile_task(I.tile, nrb, ntask, rb_major);
+      const int64_t row0 = int64_t(tile_rb(I.tile, nrb, ntask, rb_major)) * G::BM;
+      (void)task;
+      const int out_kind = I.kindN >> 8, N = I.kindN & 255;
+      double* E = out_kind == IO_PHI ? phi : psi;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int jj = nt * 8 + 2 * t4;
-        if (jj >= T.N) continue;
-        const int col = T.col0 + jj;
-        if (T.out_kind == IO_U) {
-          const int c0 = dst ? dst[col] : col;
-          const int c1 = (jj + 1 < T.N) ? (dst ? dst[col + 1] : col + 1) : -1;
+        if (jj >= N) continue;
+        const int col = I.col0 + jj;
+        if (out_kind == IO_U) {
+          const int c0 = dcol[nt][0], c1 = dcol[nt][1];
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) {
             const int64_t r = row0 + warp * 32 + mt * 8 + g;
@@ -549,7 +603,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
 #ifdef SVD1_BOUNDS
             if (c0 < 0 || c0 >= out_cols || c1 >= out_cols) {
               printf("[svd1 bounds] U_out col %d/%d of %lld (task %d N %d col %d)\n", c0, c1, (long long)out_cols,
-                     task, T.N, col);
+                     task, N, col);
               __trap();
             }
 #endif
@@ -793,7 +847,12 @@ svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms,
   int cap = max_ctas;
   if (const char* e = std::getenv("SVD1_GEMM_CTAS")) cap = std::max(1, atoi(e));  // diagnostics
   const int grid = int(std::min<int64_t>(ntiles, cap));
-  fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(maps, tasks, terms, int(ntiles), int(nrb), rows, U_out,
+  static const int rb_major = [] {
+    const char* e = std::getenv("SVD1_TILE_ORDER");
+    return (e && std::string(e) == "rb") ? 1 : 0;
+  }();
+  fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(maps, tasks, terms, int(ntiles), int(nrb), n_tasks, rb_major,
+                                                       rows, U_out,
                                                        ld_out, dst, phi, psi, ldE, out_cols, exp_elems,
                                                        ops_raw, ops_rows);
   return SVD1_OK;

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "svd1_internal.cuh"
 
@@ -845,6 +846,121 @@ __global__ void __launch_bounds__(kCT) colnorm_partial_kernel(
   if (threadIdx.x == 0) ctr[blockIdx.x] = 0;
 }
 
+// ------------------------------------------------------- K3a/K3b, warp per index
+// The same sums with a WARP per index (i for Loewner, j for the norms) and the lanes
+// striding the inner index: n warps of n/32 terms each (instead of blocks of short
+// chunks combined by a last block), so the kernels have enough resident warps to hide
+// the FP64 / MUFU latency.  The block's 8 warps share the inner index's tiles in shared
+// memory.  Every index's result depends on n only (lane partials combined by a fixed xor
+// tree), so a rank's slice of indices is bitwise the same as in the full range.
+constexpr int kWW = 8;     // warps (indices) per block
+constexpr int kWT = 256;   // inner-index tile
+
+__device__ __forceinline__ void mant_exp_mul(double& m, int& e, double m2, int e2) {
+  int ee;
+  m = frexp(m * m2, &ee);
+  e += e2 + ee;
+}
+
+__global__ void __launch_bounds__(32 * kWW) loewner_warp_kernel(
+    const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau, int n,
+    double rho, const double* __restrict__ z, double* __restrict__ zhat, int i_lo, int i_hi) {
+  __shared__ double s_d[kWT], s_mu[kWT], s_t[kWT];
+  const int lane = threadIdx.x & 31;
+  const int i = i_lo + blockIdx.x * kWW + (threadIdx.x >> 5);
+  const bool ok = i < i_hi;
+  const double di = ok ? d[i] : 0.0;
+  // two product chains per lane (even / odd tile strides), numerator and denominator
+  // apart (no division per term), renormalised with frexp every 8 factors
+  double Pn = 1.0, Pd = 1.0, Qn = 1.0, Qd = 1.0;
+  int E = 0, cnt = 0;
+  for (int jb = 0; jb < n; jb += kWT) {
+    const int nj = min(kWT, n - jb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nj; t += 32 * kWW) {
+      s_d[t] = d[jb + t];
+      s_mu[t] = d[k[jb + t]];
+      s_t[t] = tau[jb + t];
+    }
+    __syncthreads();
+    for (int t = lane; t < nj; t += 64) {
+      Pn *= fabs((s_mu[t] - di) + s_t[t]);
+      Pd *= (jb + t == i) ? 1.0 : fabs(s_d[t] - di);
+      if (t + 32 < nj) {
+        Qn *= fabs((s_mu[t + 32] - di) + s_t[t + 32]);
+        Qd *= (jb + t + 32 == i) ? 1.0 : fabs(s_d[t + 32] - di);
+      }
+      if (++cnt == 8) {
+        int e1, e2, e3, e4;
+        Pn = frexp(Pn, &e1);
+        Pd = frexp(Pd, &e2);
+        Qn = frexp(Qn, &e3);
+        Qd = frexp(Qd, &e4);
+        E += (e1 - e2) + (e3 - e4);
+        cnt = 0;
+      }
+    }
+  }
+  int e1, e2, e3, e4;
+  Pn = frexp(Pn, &e1);
+  Pd = frexp(Pd, &e2);
+  Qn = frexp(Qn, &e3);
+  Qd = frexp(Qd, &e4);
+  E += (e1 - e2) + (e3 - e4);
+  int e;
+  double m = frexp((Pn * Qn) / (Pd * Qd), &e);
+  E += e;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    mant_exp_mul(m, E, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, E, o));
+  if (ok && lane == 0) zhat[i] = copysign(sqrt(ldexp(m, E) / fabs(rho)), z[i]);
+}
+
+template <int NC>
+__global__ void __launch_bounds__(32 * kWW) colnorm_warp_kernel(
+    const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau,
+    const double* __restrict__ zhat, int n, const double* __restrict__ carry, double* __restrict__ colscale,
+    double* __restrict__ carry_out, int32_t* __restrict__ status, int j_lo, int j_hi, int64_t ldc) {
+  __shared__ double s_d[kWT], s_z[kWT], s_c[NC > 0 ? NC : 1][kWT];
+  const int lane = threadIdx.x & 31;
+  const int j = j_lo + blockIdx.x * kWW + (threadIdx.x >> 5);
+  const bool ok = j < j_hi;
+  const double dk = ok ? d[k[j]] : 0.0, tj = ok ? tau[j] : 1.0, at = fabs(tj);
+  double s = 0.0, t[NC > 0 ? NC : 1];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) t[q] = 0.0;
+  for (int ib = 0; ib < n; ib += kWT) {
+    const int ni = min(kWT, n - ib);
+    __syncthreads();
+    for (int u = threadIdx.x; u < ni; u += 32 * kWW) {
+      s_d[u] = d[ib + u];
+      s_z[u] = zhat[ib + u];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) s_c[q][u] = carry[int64_t(q) * n + ib + u];
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int u = lane; u < ni; u += 32) {
+      // y_i = zhat_i |tau_j| / ((d_i - d_kj) - tau_j): bounded by |zhat_i| (nearest pole)
+      const double y = s_z[u] * at * fast_rcp((s_d[u] - dk) - tj);
+      s = fma(y, y, s);
+#pragma unroll
+      for (int q = 0; q < NC; ++q) t[q] = fma(y, s_c[q][u], t[q]);
+    }
+  }
+  s = warp_sum(s);
+#pragma unroll
+  for (int q = 0; q < NC; ++q) t[q] = warp_sum(t[q]);
+  if (ok && lane == 0) {
+    const double rs = sqrt(s);
+    const double cs = at / rs;
+    if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
+    colscale[j] = cs;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) carry_out[int64_t(q) * ldc + j] = t[q] / rs;
+  }
+}
+
 // thread per (j, q): q = 0 -> colscale_j (and the status check), q >= 1 -> carried
 // vector q-1 (which also needs ||y||: recomputed, the partials are L2-resident)
 
@@ -1060,6 +1176,19 @@ svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, in
   return SVD1_OK;
 }
 
+// Loewner: warp per index (default; measured 30 vs 37 us at C3) or the round-1 chunked
+// kernel (environment SVD1_LOEWNER_CHUNKED=1).  Norms: the chunked kernel (its per-source
+// values are broadcast shared-memory reads; the warp-per-column variant, selected by
+// SVD1_COLNORM_WARP=1, reads twice the shared-memory wavefronts and measured 48 vs 36 us)
+static bool loewner_chunked() {
+  static const bool v = std::getenv("SVD1_LOEWNER_CHUNKED") != nullptr;
+  return v;
+}
+static bool colnorm_chunked() {
+  static const bool v = std::getenv("SVD1_COLNORM_WARP") == nullptr;
+  return v;
+}
+
 // chunks over the inner index: enough blocks to fill 148 SMs a few times over
 static int inner_chunks(int n, int threads) {
   const int outer = (n + threads - 1) / threads;
@@ -1097,6 +1226,13 @@ svd1_status loewner(const double* d, const int32_t* k, const double* tau, double
                     const double* z, int n, int i0, int i1, double* zhat, double* scratch, int* ctr,
                     cudaStream_t st, int64_t* launches) {
   if (n <= 0 || i1 <= i0) return SVD1_OK;
+  if (!loewner_chunked()) {
+    loewner_warp_kernel<<<unsigned((i1 - i0 + kWW - 1) / kWW), 32 * kWW, 0, st>>>(d, k, tau, n, rho, z, zhat,
+                                                                                  i0, i1);
+    *launches += 1;
+    SVD1_CUDA_TRY(cudaGetLastError());
+    return SVD1_OK;
+  }
   const int ch = loewner_chunks(n);
   const int chunk = (n + ch - 1) / ch;
   double* pm = scratch;
@@ -1113,6 +1249,19 @@ svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
                           double* colscale, double* carry_out, int64_t ldc, int32_t* status, double* scratch,
                           int* ctr, cudaStream_t st, int64_t* launches) {
   if (n <= 0 || j1 <= j0) return SVD1_OK;
+  if (!colnorm_chunked()) {
+    const unsigned gw = unsigned((j1 - j0 + kWW - 1) / kWW);
+    switch (ncarry) {
+#define SVD1_CW(NC) case NC: colnorm_warp_kernel<NC><<<gw, 32 * kWW, 0, st>>>(d, k, tau, zhat, n, carry, colscale, \
+                                                                     carry_out, status, j0, j1, ldc); break;
+      SVD1_CW(0) SVD1_CW(1) SVD1_CW(2) SVD1_CW(3) SVD1_CW(4) SVD1_CW(5) SVD1_CW(6)
+#undef SVD1_CW
+      default: return SVD1_E_INVALID;
+    }
+    *launches += 1;
+    SVD1_CUDA_TRY(cudaGetLastError());
+    return SVD1_OK;
+  }
   const int ch = inner_chunks(n, kCT);
   const int chunk = (n + ch - 1) / ch;
   const dim3 g(unsigned((j1 - j0 + kCT - 1) / kCT), unsigned(ch));

@@ -251,6 +251,7 @@ struct CauchyPrep {
   size_t h_maps_cap = 0;
   std::vector<cudaEvent_t> gev;  // events around each GEMM pass of the last launch
   int ngev = 0;
+  bool ops_ready = false;  // operator blocks already built (batch mode: on the upload stream)
   ~CauchyPrep() {
     if (h_maps) cudaFreeHost(h_maps);
     for (auto e : gev) cudaEventDestroy(e);
@@ -1384,6 +1385,18 @@ size_t cauchy_exp_elems(const CauchyPrep& C) {
   return C.fmm ? size_t(C.F.ncells) * size_t(C.p) * size_t(C.rows) : 0;
 }
 
+// K5: every operator block of the plan into the ops buffer (zeroed first: op chunks are
+// zero past K and N, which the GEMM relies on)
+svd1_status cauchy_build_ops(svd1_plan_t P, CauchyPrep& C, const double* d_da, const int32_t* d_k,
+                             const double* d_tau, const double* d_zhat, const double* d_cs, cudaStream_t st) {
+  if (!C.fmm) return SVD1_OK;
+  FmmHost& F = C.F;
+  auto* ops = static_cast<double*>(C.d_ops.p);
+  SVD1_CUDA_TRY(cudaMemsetAsync(ops, 0, size_t(std::max<int64_t>(F.ops_rows, 1)) * 16 * sizeof(double), st));
+  return fmm_build_ops(int(F.ops.size()), C.ddescs, C.dcells, C.p, d_da, d_k, d_tau, d_zhat, d_cs, C.dcol2src, ops,
+                       std::max<int64_t>(F.ops_rows, 1) * 16, st, &P->launches);
+}
+
 svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, const int32_t* d_k,
                           const double* d_tau, const double* d_zhat, const double* d_cs,
                           const double* U_in, int64_t ld_in, const int32_t* d_src, double* U_out,
@@ -1405,10 +1418,10 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   FmmTask* dk = C.dtasks;
   auto* ops = static_cast<double*>(C.d_ops.p);
   const int32_t* c2s = C.dcol2src;
-  // op chunks are zero past K and N (the GEMM relies on it)
-  SVD1_CUDA_TRY(cudaMemsetAsync(ops, 0, size_t(std::max<int64_t>(F.ops_rows, 1)) * 16 * sizeof(double), st));
-  TRY(fmm_build_ops(int(F.ops.size()), dd, dc, p, d_da, d_k, d_tau, d_zhat, d_cs, c2s, ops,
-                    std::max<int64_t>(F.ops_rows, 1) * 16, st, &P->launches));
+  if (!C.ops_ready) TRY(cauchy_build_ops(P, C, d_da, d_k, d_tau, d_zhat, d_cs, st));
+  C.ops_ready = false;
+  (void)dd;
+  (void)c2s;
   // TMA reads U_in: 16-byte aligned base and even leading dimension, else a padded copy
   if ((reinterpret_cast<uintptr_t>(U_in) & 15) || (ld_in & 1)) {
     const int64_t ldp = (C.n_in + 1) & ~int64_t(1);
@@ -2678,10 +2691,21 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     const int side = e < 2 ? 0 : 1;
     if (!B) return apply_upload(P, S[e], one_stream ? 0 : side);
     TRY(ensure_side(P, side + 4));
-    const cudaStream_t as = side_stream(P, side);
+    const cudaStream_t as = side_stream(P, side), us = side_stream(P, side + 4);
     SVD1_CUDA_TRY(cudaStreamWaitEvent(as, P->maps_ev[e], 0));
     TRY(upload_fmm(P, S[e], side + 4));
-    return stream_wait(P, e, side_stream(P, side + 4), as);
+    // the operator blocks (K5) are built on the upload stream as soon as the plan and the
+    // step's maps (column scales, with V2's sign alignment) are on the device, so the apply
+    // stream runs the GEMM passes back to back (this record's ops buffer was last read by
+    // the applies of update t - 2, which have completed)
+    if (S[e].rows > 0 && S[e].na > 0 && S[e].cp.fmm) {
+      SVD1_CUDA_TRY(cudaStreamWaitEvent(us, P->maps_ev[e], 0));
+      TRY(cauchy_build_ops(P, S[e].cp, static_cast<double*>(S[e].d_in.p), static_cast<int32_t*>(S[e].d_out.p),
+                           static_cast<double*>(S[e].d_out.p) + S[e].nap, static_cast<double*>(S[e].d_zhat.p),
+                           S[e].dcs, us));
+      S[e].cp.ops_ready = true;
+    }
+    return stream_wait(P, e, us, as);
   };
   // thin V: column m of V <- q before the first V apply reads it (V side's apply stream)
   auto null_dir = [&]() -> svd1_status {
