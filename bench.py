@@ -195,11 +195,16 @@ def main():
     ap.add_argument("--full-v", action="store_true",
                     help="keep the full n x n right factor for m < n configs (default: thin V, "
                          "SVD1_THIN_V, DESIGN.md §4.10)")
+    ap.add_argument("--fused", action="store_true",
+                    help="fused per-side pass (SVD1_FUSED_SIDE, SURVEY 8(f) #1): both applies of a side "
+                         "row chunk by row chunk, L2-resident")
     ap.add_argument("--sequential", action="store_true",
                     help="time the per-update API (svd1_update) instead of svd1_update_batch")
     ap.add_argument("--config", type=int, default=CFG_ID, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default C3, the headline metric's workload)")
     args = ap.parse_args()
+    if os.environ.get("SVD1_BENCH_FUSED"):  # (experiments: select the fused pass through the environment)
+        args.fused = True
     global WORKLOAD, METRIC
     if args.config != CFG_ID:
         WORKLOAD = WORKLOADS[args.config]
@@ -243,7 +248,8 @@ def main():
     from paper_1707_08369_b200.parallel import ShardedUpdater
     stream = torch.cuda.current_stream()
     thin = m < n and not args.full_v
-    upd = ShardedUpdater(m, n, rank, world, eps=cfg["eps"], stream=stream, flags=P.THIN_V if thin else 0)
+    upd = ShardedUpdater(m, n, rank, world, eps=cfg["eps"], stream=stream,
+                         flags=(P.THIN_V if thin else 0) | (P.FUSED_SIDE if args.fused else 0))
     u0, u1, v0, v1 = upd.u_lo, upd.u_hi, upd.v_lo, upd.v_hi
     U = U0[u0:u1].clone()
     if thin:  # V[:, :m] plus one workspace column (SVD1_THIN_V)
@@ -479,6 +485,7 @@ def main():
                                   f"inputs fit in L2 ({8 * (m * m + n * n) / 2**20:.1f} MiB); no flush"),
                            "parallelism": f"row-sharded x{world}" if world > 1 else "1 GPU",
                            "api": "svd1_update_batch (pipelined stream)" if batch else "svd1_update",
+                           "fused_side": bool(args.fused),
                            "thin_v": thin},
                 "sequential_api": seq,
                 "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,

@@ -67,6 +67,11 @@ typedef enum {
                                     process computes EVERY rank's slice of the spectral phase,
                                     so the all-gathers are concatenations in place; the rows
                                     are this process's as usual (normally all of them) */
+#define SVD1_FUSED_SIDE 0x80u    /* fused per-side pass: each
+                                    side's two applies (X1 then X2) run row chunk by
+                                    row chunk with the chunk's rows, intermediate and FMM
+                                    expansions L2-resident, so U and V are read and written once
+                                    per update; apply_ms[0] / [2] then hold the whole side */
 #define SVD1_FORCE_NCCL 0x40u    /* use the NCCL all-gathers even with world == 1 (test mode:
                                     exercises the communicator path on one GPU; nccl_id needed) */
 

@@ -91,6 +91,7 @@ SECULAR_DIRECT = 0x8  # secular solve with direct sums only
 THIN_V = 0x10         # thin right factor: V is n x (m+1), column m workspace (svd1.h)
 EMULATE_RANKS = 0x20  # world > 1 in one process: every rank's spectral slice computed here (tests)
 FORCE_NCCL = 0x40     # NCCL all-gathers even at world 1 (tests the communicator path on one GPU)
+FUSED_SIDE = 0x80     # fused per-side pass: X1 then X2 row chunk by row chunk
 
 
 def nccl_unique_id() -> bytes:

@@ -154,6 +154,38 @@ __global__ void __launch_bounds__(256) householder_kernel(int64_t rows, double* 
   }
 }
 
+// K4 for many small groups (C5: ~800 pairs of bitwise-equal sigma^2): a warp per row,
+// lanes over the groups (a group's few columns are read once, transformed in registers,
+// written once); the block-per-(rows, group) kernel above keeps the long groups (C4's
+// null space: one group of n - m columns).
+__global__ void __launch_bounds__(256) householder_rows_kernel(int64_t rows, double* __restrict__ U, int64_t ld,
+                                                              int ngroups, const int32_t* __restrict__ goff,
+                                                              const int32_t* __restrict__ cols,
+                                                              const double* __restrict__ hv) {
+  constexpr int kMaxSmall = 16;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  double* row = U + r * ld;
+  for (int g = lane; g < ngroups; g += 32) {
+    const int o0 = goff[g], len = min(goff[g + 1] - o0, kMaxSmall);
+    double x[kMaxSmall], v[kMaxSmall];
+    double vv = 0.0, dot = 0.0;
+#pragma unroll
+    for (int t = 0; t < kMaxSmall; ++t)
+      if (t < len) {
+        v[t] = hv[o0 + t];
+        x[t] = row[cols[o0 + t]];
+        vv = fma(v[t], v[t], vv);
+        dot = fma(x[t], v[t], dot);
+      }
+    const double f = (2.0 / vv) * dot;
+#pragma unroll
+    for (int t = 0; t < kMaxSmall; ++t)
+      if (t < len) row[cols[o0 + t]] = fma(-f, v[t], x[t]);
+  }
+}
+
 __global__ void col_rotate_kernel(int64_t rows, double* __restrict__ U, int64_t ld,
                                   const int32_t* __restrict__ goff, const int32_t* __restrict__ cols,
                                   const double* __restrict__ mats) {
@@ -751,9 +783,15 @@ svd1_status apply_few_rows(int rows, int n, const double* d, const int32_t* k, c
 }
 
 svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,
-                             const int32_t* goff, const int32_t* cols, const double* hv,
+                             const int32_t* goff, const int32_t* cols, const double* hv, int maxlen,
                              cudaStream_t st, int64_t* launches) {
   if (rows <= 0 || ngroups <= 0) return SVD1_OK;
+  if (maxlen <= 16) {  // many small groups: a warp per row
+    householder_rows_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(rows, U, ld, ngroups, goff, cols, hv);
+    *launches += 1;
+    SVD1_CUDA_TRY(cudaGetLastError());
+    return SVD1_OK;
+  }
   dim3 grid(unsigned((rows + 31) / 32), unsigned(ngroups));
   householder_kernel<<<grid, 256, 0, st>>>(rows, U, ld, goff, cols, hv);
   *launches += 1;

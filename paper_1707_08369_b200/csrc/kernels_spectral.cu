@@ -961,6 +961,86 @@ __global__ void __launch_bounds__(32 * kWW) colnorm_warp_kernel(
   }
 }
 
+// The chunked norm kernel with J columns per thread (columns j and j + kCT, ...): every
+// broadcast shared-memory read of a source feeds J terms.  Same partials / combine as
+// colnorm_partial_kernel (J = 1 is that kernel's arithmetic).
+template <int NC, int J>
+__global__ void __launch_bounds__(kCT) colnorm_multi_kernel(
+    const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau,
+    const double* __restrict__ zhat, int n, int chunk, const double* __restrict__ carry,
+    double* __restrict__ part, int* __restrict__ ctr, double* __restrict__ colscale,
+    double* __restrict__ carry_out, int32_t* __restrict__ status, int j_lo, int j_hi, int64_t ldc) {
+  __shared__ double s_d[kCI], s_z[kCI], s_c[NC > 0 ? NC : 1][kCI];
+  const int i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
+  int jj[J];
+  bool ok[J];
+  double dk[J], tj[J], at[J], s[J], t[J][NC > 0 ? NC : 1];
+#pragma unroll
+  for (int c = 0; c < J; ++c) {
+    jj[c] = j_lo + blockIdx.x * (kCT * J) + c * kCT + threadIdx.x;
+    ok[c] = jj[c] < j_hi;
+    dk[c] = ok[c] ? d[k[jj[c]]] : 0.0;
+    tj[c] = ok[c] ? tau[jj[c]] : 1.0;
+    at[c] = fabs(tj[c]);
+    s[c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) t[c][q] = 0.0;
+  }
+  for (int ib = i0; ib < i1; ib += kCI) {
+    const int ni = min(kCI, i1 - ib);
+    __syncthreads();
+    for (int u = threadIdx.x; u < ni; u += kCT) {
+      s_d[u] = d[ib + u];
+      s_z[u] = zhat[ib + u];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) s_c[q][u] = carry[int64_t(q) * n + ib + u];
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int u = 0; u < ni; ++u) {
+      const double du = s_d[u], zu = s_z[u];
+      double cq[NC > 0 ? NC : 1];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) cq[q] = s_c[q][u];
+#pragma unroll
+      for (int c = 0; c < J; ++c) {
+        const double y = zu * at[c] * fast_rcp((du - dk[c]) - tj[c]);
+        s[c] = fma(y, y, s[c]);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) t[c][q] = fma(y, cq[q], t[c][q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < J; ++c)
+    if (ok[c]) {
+      const int64_t base = int64_t(blockIdx.y) * (NC + 1) * n;
+      part[base + jj[c]] = s[c];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) part[base + int64_t(q + 1) * n + jj[c]] = t[c][q];
+    }
+  if (!last_block_of_column(ctr)) return;
+  const int64_t cstride = int64_t(NC + 1) * n;
+#pragma unroll
+  for (int c = 0; c < J; ++c)
+    if (ok[c]) {  // combine in chunk order
+      const int j = jj[c];
+      double ss = 0.0;
+      for (int b = 0; b < int(gridDim.y); ++b) ss += __ldcg(part + int64_t(b) * cstride + j);
+      const double rs = sqrt(ss);
+      const double cs = fabs(tj[c]) / rs;
+      if (!(cs > 0.0) || !isfinite(cs)) atomicOr(status, 4);
+      colscale[j] = cs;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        double tt = 0.0;
+        for (int b = 0; b < int(gridDim.y); ++b) tt += __ldcg(part + int64_t(b) * cstride + int64_t(q + 1) * n + j);
+        carry_out[int64_t(q) * ldc + j] = tt / rs;
+      }
+    }
+  if (threadIdx.x == 0) ctr[blockIdx.x] = 0;
+}
+
 // thread per (j, q): q = 0 -> colscale_j (and the status check), q >= 1 -> carried
 // vector q-1 (which also needs ||y||: recomputed, the partials are L2-resident)
 
@@ -1176,23 +1256,43 @@ svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, in
   return SVD1_OK;
 }
 
-// Loewner: warp per index (default; measured 30 vs 37 us at C3) or the round-1 chunked
-// kernel (environment SVD1_LOEWNER_CHUNKED=1).  Norms: the chunked kernel (its per-source
+// Loewner: warp per index below n = 8192 (C3: 30 vs 37 us), the chunked kernel above it
+// (C5, n = 16384: 222 vs 312 us -- the warp kernel's strided shared-memory reads become the
+// bound); SVD1_LOEWNER_CHUNKED=0/1 forces one.  Norms: the chunked kernel (its per-source
 // values are broadcast shared-memory reads; the warp-per-column variant, selected by
 // SVD1_COLNORM_WARP=1, reads twice the shared-memory wavefronts and measured 48 vs 36 us)
-static bool loewner_chunked() {
-  static const bool v = std::getenv("SVD1_LOEWNER_CHUNKED") != nullptr;
-  return v;
+static bool loewner_chunked(int n) {
+  static const int v = [] {
+    const char* e = std::getenv("SVD1_LOEWNER_CHUNKED");
+    return e ? atoi(e) : -1;
+  }();
+  return v >= 0 ? v != 0 : n >= 8192;
 }
 static bool colnorm_chunked() {
   static const bool v = std::getenv("SVD1_COLNORM_WARP") == nullptr;
   return v;
 }
 
-// chunks over the inner index: enough blocks to fill 148 SMs a few times over
-static int inner_chunks(int n, int threads) {
-  const int outer = (n + threads - 1) / threads;
-  int ch = (4 * 148 + outer - 1) / outer;
+static int colnorm_J() {  // columns per thread of the norm kernel (SVD1_COLNORM_J, tuning)
+  static const int v = [] {
+    const char* e = std::getenv("SVD1_COLNORM_J");
+    return e ? std::max(1, std::min(2, atoi(e))) : 1;
+  }();
+  return v;
+}
+static int chunk_blocks() {  // target blocks (x 148) of the chunked kernels (SVD1_CHUNK_BLOCKS, tuning)
+  static const int v = [] {
+    const char* e = std::getenv("SVD1_CHUNK_BLOCKS");
+    return e ? std::max(1, atoi(e)) : 8;  // measured: 8 (C5 norms 229 -> 200 us), C3 unchanged
+  }();
+  return v;
+}
+
+// chunks over the inner index: enough blocks to fill 148 SMs a few times over (a function
+// of n only: rank slices of the outer index see the same chunks)
+static int inner_chunks(int n, int threads, int per_thread = 1) {
+  const int outer = (n + threads * per_thread - 1) / (threads * per_thread);
+  int ch = (chunk_blocks() * 148 + outer - 1) / outer;
   ch = std::max(1, std::min(ch, (n + 255) / 256));
   return ch;
 }
@@ -1209,7 +1309,7 @@ static int loewner_chunks(int n) {
 
 
 int64_t spectral_scratch_elems(int n, int ncarry) {
-  const int ch = std::max(loewner_chunks(n), inner_chunks(n, kCT));
+  const int ch = std::max(loewner_chunks(n), std::max(inner_chunks(n, kCT), inner_chunks(n, kCT, 2)));
   return int64_t(ch) * n * (ncarry + 2) + 16;
 }
 
@@ -1226,7 +1326,7 @@ svd1_status loewner(const double* d, const int32_t* k, const double* tau, double
                     const double* z, int n, int i0, int i1, double* zhat, double* scratch, int* ctr,
                     cudaStream_t st, int64_t* launches) {
   if (n <= 0 || i1 <= i0) return SVD1_OK;
-  if (!loewner_chunked()) {
+  if (!loewner_chunked(n)) {
     loewner_warp_kernel<<<unsigned((i1 - i0 + kWW - 1) / kWW), 32 * kWW, 0, st>>>(d, k, tau, n, rho, z, zhat,
                                                                                   i0, i1);
     *launches += 1;
@@ -1256,6 +1356,21 @@ svd1_status colnorm_carry(const double* d, const int32_t* k, const double* tau,
                                                                      carry_out, status, j0, j1, ldc); break;
       SVD1_CW(0) SVD1_CW(1) SVD1_CW(2) SVD1_CW(3) SVD1_CW(4) SVD1_CW(5) SVD1_CW(6)
 #undef SVD1_CW
+      default: return SVD1_E_INVALID;
+    }
+    *launches += 1;
+    SVD1_CUDA_TRY(cudaGetLastError());
+    return SVD1_OK;
+  }
+  if (colnorm_J() == 2) {  // two columns per thread (chunks as for one: they depend on n only)
+    const int ch = inner_chunks(n, kCT, 2);
+    const int chunk = (n + ch - 1) / ch;
+    const dim3 g(unsigned((j1 - j0 + 2 * kCT - 1) / (2 * kCT)), unsigned(ch));
+    switch (ncarry) {
+#define SVD1_CM(NC) case NC: colnorm_multi_kernel<NC, 2><<<g, kCT, 0, st>>>(d, k, tau, zhat, n, chunk, carry, scratch, \
+                                                                 ctr, colscale, carry_out, status, j0, j1, ldc); break;
+      SVD1_CM(0) SVD1_CM(1) SVD1_CM(2) SVD1_CM(3) SVD1_CM(4) SVD1_CM(5) SVD1_CM(6)
+#undef SVD1_CM
       default: return SVD1_E_INVALID;
     }
     *launches += 1;

@@ -276,6 +276,11 @@ struct StepRecord {
   double rho = 0.0;
   std::vector<int32_t> h_goff, h_cols;  // Householder groups (buffer columns)
   std::vector<double> h_hv;
+  int h_maxlen() const {  // longest Householder group
+    int mx = 0;
+    for (size_t g = 0; g + 1 < h_goff.size(); ++g) mx = std::max(mx, h_goff[g + 1] - h_goff[g]);
+    return mx;
+  }
   std::vector<int32_t> src_cols;      // active source i -> input buffer column
   std::vector<int32_t> pass_src, pass_dst;  // deflated: input col -> output position
   std::vector<double> pass_scale;
@@ -1397,11 +1402,18 @@ svd1_status cauchy_build_ops(svd1_plan_t P, CauchyPrep& C, const double* d_da, c
                        std::max<int64_t>(F.ops_rows, 1) * 16, st, &P->launches);
 }
 
+constexpr int kMapSlots = 64;  // TMA descriptor sets per apply (one per row chunk, §4.11)
+
+// rows_n >= 0: the apply over rows_n rows starting at U_in / U_out (a row chunk of the fused
+// per-side pass), its TMA descriptors in slot `slot`; the operator blocks
+// are built by the first launch of the apply (or beforehand on the upload stream)
 svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, const int32_t* d_k,
                           const double* d_tau, const double* d_zhat, const double* d_cs,
                           const double* U_in, int64_t ld_in, const int32_t* d_src, double* U_out,
-                          int64_t ld_out, const int32_t* d_dst, cudaStream_t st, int side) {
-  const int64_t rows = C.rows;
+                          int64_t ld_out, const int32_t* d_dst, cudaStream_t st, int side,
+                          int64_t rows_n = -1, int slot = 0, bool last_chunk = true) {
+  const int64_t rows = rows_n >= 0 ? rows_n : C.rows;
+  if (rows <= 0) return SVD1_OK;
   if (!C.fmm)
     return apply_direct(rows, C.na, d_da, d_k, d_tau, d_zhat, d_cs, U_in, ld_in, d_src, U_out, ld_out,
                         d_dst, st, &P->launches);
@@ -1419,7 +1431,7 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   auto* ops = static_cast<double*>(C.d_ops.p);
   const int32_t* c2s = C.dcol2src;
   if (!C.ops_ready) TRY(cauchy_build_ops(P, C, d_da, d_k, d_tau, d_zhat, d_cs, st));
-  C.ops_ready = false;
+  C.ops_ready = !last_chunk;  // later chunks of the same apply reuse the operator blocks
   (void)dd;
   (void)c2s;
   // TMA reads U_in: 16-byte aligned base and even leading dimension, else a padded copy
@@ -1436,13 +1448,15 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   // stream; the kernel acquires them through the tensormap proxy before use)
   {
     void* hm = C.h_maps;  // sized at creation
-    TRY(pinned_reserve(&hm, &C.h_maps_cap, sizeof(FmmMaps)));
+    TRY(pinned_reserve(&hm, &C.h_maps_cap, sizeof(FmmMaps) * kMapSlots));
     C.h_maps = static_cast<FmmMaps*>(hm);
   }
-  TRY(fmm_make_maps(C.h_maps, rows, U_in, C.n_in, ld_in, phi, psi, ldE));
+  if (slot < 0 || slot >= kMapSlots) return SVD1_E_INVALID;
+  TRY(fmm_make_maps(C.h_maps + slot, rows, U_in, C.n_in, ld_in, phi, psi, ldE));
   FmmMaps* maps;
-  TRY(C.d_maps.get<FmmMaps>(1, &maps, st));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(maps, C.h_maps, sizeof(FmmMaps), cudaMemcpyHostToDevice, st));
+  TRY(C.d_maps.get<FmmMaps>(kMapSlots, &maps, st));
+  maps += slot;
+  SVD1_CUDA_TRY(cudaMemcpyAsync(maps, C.h_maps + slot, sizeof(FmmMaps), cudaMemcpyHostToDevice, st));
   const bool dbg = std::getenv("SVD1_DEBUG") != nullptr;
   if (dbg) {  // host-side validation of the task lists
     for (const FmmTask& T : F.tasks) {
@@ -2102,22 +2116,34 @@ svd1_status apply_upload(svd1_plan_t P, StepRecord& S, int side) {
   return SVD1_OK;
 }
 
+// One row chunk [r0, r0 + rows) of a step's apply (Householder in place on U_in, Cauchy
+// apply, passthrough): the whole apply is the chunk r0 = 0, rows = S.rows.
+svd1_status apply_chunk(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_in, double* U_out,
+                        int64_t ld_out, int64_t r0, int64_t rows, cudaStream_t st, int side, int slot,
+                        bool last_chunk) {
+  if (rows <= 0) return SVD1_OK;
+  U_in += r0 * ld_in;
+  U_out += r0 * ld_out;
+  if (S.h_goff.size() > 1)
+    TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, S.h_maxlen(), st,
+                         &P->launches));
+  if (S.na > 0)
+    TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
+                      static_cast<double*>(S.d_out.p) + S.nap, static_cast<double*>(S.d_zhat.p), S.dcs,
+                      U_in, ld_in, S.dsrc, U_out, ld_out, S.ddst, st, side, rows, slot, last_chunk));
+  if (!S.pass_src.empty())
+    TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, S.dpsrc, U_out, ld_out, S.dpdst, S.dpscale,
+                    st, &P->launches));
+  return SVD1_OK;
+}
+
 // Device half: Householder (in place on U_in), Cauchy apply, passthrough.
 svd1_status apply_launch(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_in, double* U_out,
                          int64_t ld_out, int ev0, cudaStream_t st, int side) {
   const int64_t rows = S.rows;
   if (rows <= 0) return SVD1_OK;
   TRY(ev_record(P, ev0, st));
-  if (S.h_goff.size() > 1)
-    TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, st,
-                         &P->launches));
-  if (S.na > 0)
-    TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
-                      static_cast<double*>(S.d_out.p) + S.nap, static_cast<double*>(S.d_zhat.p), S.dcs,
-                      U_in, ld_in, S.dsrc, U_out, ld_out, S.ddst, st, side));
-  if (!S.pass_src.empty())
-    TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, S.dpsrc, U_out, ld_out, S.dpdst, S.dpscale,
-                    st, &P->launches));
+  TRY(apply_chunk(P, S, U_in, ld_in, U_out, ld_out, 0, rows, st, side, 0, true));
   TRY(ev_record(P, ev0 + 1, st));
   if (std::getenv("SVD1_NANCHECK")) {  // diagnostics: first non-finite output column
     SVD1_CUDA_TRY(cudaStreamSynchronize(st));
@@ -2199,10 +2225,10 @@ svd1_status reserve_step(StepRecord& S, int64_t N, int p, int G) {
   TRY(S.blob.reserve<char>(maps_blob_bytes(N) + fmm_blob_estimate(N, p)));
   TRY(S.cp.blob.reserve<char>(fmm_blob_estimate(N, p)));
   TRY(S.cp.d_ops.reserve<double>(ops_estimate(N)));
-  TRY(S.cp.d_maps.reserve<FmmMaps>(1));
+  TRY(S.cp.d_maps.reserve<FmmMaps>(kMapSlots));
   {
     void* hm = S.cp.h_maps;
-    TRY(pinned_reserve(&hm, &S.cp.h_maps_cap, sizeof(FmmMaps)));
+    TRY(pinned_reserve(&hm, &S.cp.h_maps_cap, sizeof(FmmMaps) * kMapSlots));
     S.cp.h_maps = static_cast<FmmMaps*>(hm);
   }
   TRY(S.sec_blob.reserve<char>(size_t(N) * 64 + (size_t(64) << 10)));
@@ -2444,7 +2470,8 @@ svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, in
                        cudaStream_t st, int side) {
   if (rows <= 0) return SVD1_OK;
   if (S.h_goff.size() > 1)
-    TRY(householder_cols(rows, in, ld, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, st, &P->launches));
+    TRY(householder_cols(rows, in, ld, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, S.h_maxlen(), st,
+                         &P->launches));
   if (S.na > 0) {
     double* scr;
     TRY(P->few_scr[side].get<double>(size_t(few_rows_scratch_elems(rows, S.na)), &scr, st));
@@ -2456,6 +2483,31 @@ svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, in
     TRY(passthrough(rows, int(S.pass_src.size()), in, ld, S.dpsrc, out, ld, S.dpdst, S.dpscale, st,
                     &P->launches));
   return SVD1_OK;
+}
+
+// Rows per chunk of the fused per-side pass: the chunk's U/V rows and W rows (read and
+// written) plus the larger step's expansions (Phi, Psi over the tree's non-empty cells)
+// within ~64 MB of L2, a multiple of the GEMM's 128-row blocks, at most kMapSlots chunks
+// (SVD1_FUSED_ROWS overrides).
+int64_t fused_chunk_rows(const StepRecord& S1, const StepRecord& S2, int64_t ldx, int64_t ldw, int64_t rows) {
+  static const int64_t env = [] {
+    const char* e = std::getenv("SVD1_FUSED_ROWS");
+    return e ? std::max<int64_t>(1, atoll(e)) : 0;
+  }();
+  int64_t rc = env;
+  if (!rc) {
+    int64_t used = 0;
+    for (const StepRecord* S : {&S1, &S2})
+      if (S->na > 0 && S->cp.fmm) {
+        int64_t u = 0;
+        for (const FmmCell& C : S->cp.F.cells) u += C.hi > C.lo;
+        used = std::max(used, u * S->cp.p);
+      }
+    const int64_t per_row = 8 * (ldx + ldw + 2 * used);
+    rc = std::max<int64_t>(128, ((int64_t(64) << 20) / std::max<int64_t>(per_row, 1)) / 128 * 128);
+  }
+  rc = std::max(rc, (rows + kMapSlots - 1) / kMapSlots);
+  return std::min(rc, rows);
 }
 
 svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
@@ -2556,6 +2608,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   TRY(ensure_expansions(P, 0, expansion_elems(c.u_rows, m, P->p)));
   TRY(ensure_expansions(P, 1, expansion_elems(c.v_rows, nv, P->p)));
   const bool one_stream = !B && std::getenv("SVD1_ONE_STREAM") != nullptr;  // diagnostics
+  const bool fused = (c.flags & SVD1_FUSED_SIDE) != 0;
   // spectral work and uploads: the apply streams' sides (0, 1), or in batch mode the
   // spectral streams (2, 3), so the next update's spectral phase is not queued behind
   // this update's applies
@@ -2713,11 +2766,49 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     return null_direction(c.v_rows, V, ldv, m, b_dev, c.v_row0, B ? B->y_dev : proj + 5 * m,
                           beta_perp > 0.0 ? 1.0 / beta_perp : 0.0, stv, &P->launches);
   };
+  // Fused per-side pass (SVD1_FUSED_SIDE): once both steps
+  // of a side are planned, the side's rows go through X1 then X2 in chunks sized so that a
+  // chunk's U/V rows, its W rows and its expansions stay in L2: U and V are read and written
+  // once per update instead of twice.  Per chunk: Householder (step 1) on the chunk's rows,
+  // apply 1, passthrough 1, Householder (step 2), apply 2, passthrough 2 (V: pairing
+  // rotations); the operator blocks are built once per step.
+  auto fused_side = [&](int side) -> svd1_status {
+    const int e1 = side ? 2 : 0, e2 = e1 + 1;
+    const cudaStream_t st = side ? stv : P->st;
+    double* X = side ? V : U;
+    const int64_t ldx = side ? ldv : ldu;
+    double* Wb = side ? Wv : Wu;
+    const int64_t ldw = side ? nv : m;
+    const int64_t rows = side ? c.v_rows : c.u_rows;
+    if (rows <= 0) return SVD1_OK;
+    TRY(ev_record(P, side ? 18 : 16, st));
+    if (B) TRY(bwin_record(P, B->parity, side, st));
+    if (B && B->t == 0) TRY(bspan_record(P, side, st));
+    if (side) TRY(null_dir());
+    TRY(ev_record(P, 2 * e1, st));
+    const int64_t rc = fused_chunk_rows(S[e1], S[e2], ldx, ldw, rows);
+    int slot = 0;
+    for (int64_t r0 = 0; r0 < rows; r0 += rc, ++slot) {
+      const int64_t nr = std::min(rc, rows - r0);
+      const bool last = r0 + nr >= rows;
+      TRY(apply_chunk(P, S[e1], X, ldx, Wb, ldw, r0, nr, st, side, slot, last));
+      TRY(apply_chunk(P, S[e2], Wb, ldw, X, ldx, r0, nr, st, side, slot, last));
+      if (side && nrot_v() > 0)
+        TRY(col_rotate(nr, X + r0 * ldx, ldx, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
+                       static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), st,
+                       &P->launches));
+    }
+    // the side's whole time is reported on its first step (apply_ms[e1]); the second's is 0
+    TRY(ev_record(P, 2 * e1 + 1, st));
+    TRY(ev_record(P, 2 * e2, st));
+    TRY(ev_record(P, 2 * e2 + 1, st));
+    return SVD1_OK;
+  };
   auto first_apply = [&](int e) -> svd1_status {  // upload (+ launch when nothing in place)
     const int side = e == 0 ? 0 : 1;
     TRY(rare_grow(e, side));
     TRY(upload_step(e));
-    if (S[e].h_goff.size() <= 1) {  // nothing transformed in place: start now
+    if (!fused && S[e].h_goff.size() <= 1) {  // nothing transformed in place: start now
       if (e == 0) {
         TRY(ev_record(P, 16, P->st));
         if (B) TRY(bwin_record(P, B->parity, 0, P->st));
@@ -2946,34 +3037,47 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // eigen-update succeeded: the first applies that transform their input in place can
   // start now; the second applies follow as soon as their plans are uploaded.
   const double t4 = now_ms();
-  if (!launched_u1) {
+  if (fused) {  // both steps of a side row chunk by row chunk (§4.11)
+    plan_u2.join();
+    TRY(rare_grow(1, 0));
+    TRY(upload_step(1));
+    TRY(fused_side(0));
+    plan_v2.join();
+    TRY(rare_grow(3, 1));
+    TRY(upload_step(3));  // carries the sign alignment
+    if (!B) TRY(upload_rot(one_stream ? 0 : 1));
+    TRY(fused_side(1));
+  }
+  if (!fused && !launched_u1) {
     TRY(ev_record(P, 16, P->st));
     if (B) TRY(bwin_record(P, B->parity, 0, P->st));
     if (B && B->t == 0) TRY(bspan_record(P, 0, P->st));
     TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
   }
-  if (!launched_v1) {
+  if (!fused && !launched_v1) {
     TRY(ev_record(P, 18, stv));
     if (B) TRY(bwin_record(P, B->parity, 1, stv));
     if (B && B->t == 0) TRY(bspan_record(P, 1, stv));
     TRY(null_dir());
     TRY(apply_launch(P, S[2], V, ldv, Wv, nv, 4, stv, 1));
   }
-  plan_u2.join();
-  TRY(rare_grow(1, 0));
-  TRY(upload_step(1));
-  tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U2 apply", P->st);
-  TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
-  plan_v2.join();
-  TRY(rare_grow(3, 1));
-  TRY(upload_step(3));  // carries the sign alignment
-  if (!B) TRY(upload_rot(one_stream ? 0 : 1));
-  tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V2 apply", stv);
-  TRY(apply_launch(P, S[3], Wv, nv, V, ldv, 6, stv, 1));
-  if (nrot_v() > 0)
-    TRY(col_rotate(c.v_rows, V, ldv, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
-                   static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
-                   &P->launches));
+  if (!fused) {
+    plan_u2.join();
+    TRY(rare_grow(1, 0));
+    TRY(upload_step(1));
+    tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U2 apply", P->st);
+    TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
+    plan_v2.join();
+    TRY(rare_grow(3, 1));
+    TRY(upload_step(3));  // carries the sign alignment
+    if (!B) TRY(upload_rot(one_stream ? 0 : 1));
+    tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V2 apply", stv);
+    TRY(apply_launch(P, S[3], Wv, nv, V, ldv, 6, stv, 1));
+    if (nrot_v() > 0)
+      TRY(col_rotate(c.v_rows, V, ldv, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
+                     static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
+                     &P->launches));
+  }
   if (B) {  // no join, no sync: the next update's spectral phase overlaps these applies
     tl_mark(P, "u" + std::to_string(B->t) + " U2 end", P->st);
     tl_mark(P, "u" + std::to_string(B->t) + " V2 end", stv);

@@ -147,8 +147,9 @@ svd1_status apply_few_rows(int rows, int n, const double* d, const int32_t* k, c
 
 // K4: Householder column groups, in place: for each group g, cols idx[off_g..off_g+len_g)
 // U[:, idx] <- U[:, idx] (I - 2 v v^T / v^T v), v = hv[off_g..].
+// maxlen: the longest group (<= 16: a warp per row over all groups, else a block per group)
 svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,
-                             const int32_t* goff, const int32_t* cols, const double* hv,
+                             const int32_t* goff, const int32_t* cols, const double* hv, int maxlen,
                              cudaStream_t st, int64_t* launches);
 // pairing rotations: for group g with columns c_0..c_{k-1} (k <= 8) and row-major k x k R,
 // U[r, c_b] <- sum_a U[r, c_a] R[a][b]  (in place)

@@ -2,8 +2,8 @@
 # perf iteration: parity subset, bench (default + env variants), short ncu of the GEMM passes
 cd "$(dirname "$0")/.."
 TAG=${TAG:-p}
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_ranks.py -x -q 2>&1 | tail -3
-b() { timeout 300 env $1 python bench.py --steps 20 --warmup 5 --no-cpu --no-check > gpurun_out/b_$TAG.json 2> gpurun_out/b_$TAG.err;
+python -m pytest ${TESTS:-tests/test_gpu_parity.py tests/test_gpu_ranks.py} -x -q 2>&1 | tail -3
+b() { timeout 300 env $(echo $1 | tr "~" " ") python bench.py --steps 20 --warmup 5 --no-cpu --no-check > gpurun_out/b_$TAG.json 2> gpurun_out/b_$TAG.err;
       python - "$1" <<'PY'
 import json, sys; d=json.load(open('gpurun_out/b_' + __import__('os').environ.get('TAG','p') + '.json'))
 r=d['roofline']; print(f"[{sys.argv[1]}] value {d['value']:.1f} e2e {d['e2e']['value']:.1f} frac {r['frac']:.3f} iso {r['frac_isolated']:.3f} spec_ms/step {d['spectral_ms_per_step']:.2f} seq {d['sequential_api']['value']:.1f} allocs {d['allocations_in_timed_region']}")

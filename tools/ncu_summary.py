@@ -10,20 +10,33 @@ def raw(rep):
 
 
 def summary_rep(rep):
+    """One line per kernel; DRAM bytes converted to MB from the report's own units row."""
     hdr, units, rows = raw(rep)
     col = {h: i for i, h in enumerate(hdr)}
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+    tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "sm__inst_executed_pipe_tensor_subpipe_dmma.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
-            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
-            "launch__registers_per_thread", "Grid Size"]
-    print("kernel | grid | us | DRAM rd MB | DRAM wr MB | DMMA inst | tensor % | fp64 % | warps %")
+            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size"]
+    print("kernel | grid blocks | us | DRAM rd MB | DRAM wr MB | tensor (DMMA) pipe % | FP64 pipe % | warps active %")
+
+    def val(r, k):
+        if k not in col or not r[col[k]].strip():
+            return None
+        v = float(r[col[k]].replace(",", ""))
+        u = units[col[k]]
+        if k.startswith("dram__bytes"):
+            v *= scale.get(u, 1.0)
+        elif k == "gpu__time_duration.sum":
+            v *= tscale.get(u, 1.0)
+        return v
     for r in rows:
         name = re.sub(r"\(.*", "", r[col["Kernel Name"]]).replace("svd1::", "").replace("<unnamed>::", "")[-40:]
-        vals = []
-        for k in keys:
-            v = r[col[k]] if k in col else "-"
-            vals.append(v)
-        print(f"{name} | {vals[8]} | {vals[0]} | {vals[1]} | {vals[2]} | {vals[3]} | {vals[4]} | {vals[5]} | {vals[6]}")
+        v = [val(r, k) for k in keys]
+        f = lambda x, fmt: "-" if x is None else format(x, fmt)
+        print(f"{name} | {f(v[6], '.0f')} | {f(v[0], '.1f')} | {f(v[1], '.2f')} | {f(v[2], '.2f')} | "
+              f"{f(v[3], '.1f')} | {f(v[4], '.1f')} | {f(v[5], '.1f')}")
 
 
 def summary_csv(path):
