@@ -359,10 +359,10 @@ def main():
     launches = sum(r["kernel_launches"] for r in reps)
     traffic, traffic_src = None, None
     try:  # DRAM bytes per apply from the committed ncu capture of this workload
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")) as f:
             tj = json.load(f)
         if args.config == CFG_ID:
-            traffic, traffic_src = tj["traffic_bytes_per_apply"], "profiles/ncu_traffic_r01.json: " + tj["label"]
+            traffic, traffic_src = tj["traffic_bytes_per_apply"], "profiles/ncu_traffic_r02.json: " + tj["label"]
     except Exception:
         pass
     roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

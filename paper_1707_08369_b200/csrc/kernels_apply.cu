@@ -743,6 +743,58 @@ __global__ void __launch_bounds__(128) few_rows_partial_kernel(
   }
 }
 
+// The same partial sums with TWO targets per thread (j and j + 128): every broadcast
+// shared-memory read of a carried row's source value feeds two FMAs (the rows x n^2 products
+// of the carried rows are FP64-ALU work whose shared-memory reads were the other half)
+template <int RB>
+__global__ void __launch_bounds__(128) few_rows_partial2_kernel(
+    int rows, int n, const double* __restrict__ d, const int32_t* __restrict__ k,
+    const double* __restrict__ tau, const double* __restrict__ zhat, const double* __restrict__ U_in,
+    int64_t ld_in, const int32_t* __restrict__ src, double* __restrict__ part) {
+  __shared__ double s_u[RB][32];
+  __shared__ double s_d[32], s_z[32];
+  const int j0 = blockIdx.x * 256 + threadIdx.x, j1 = j0 + 128;
+  const int i_lo = blockIdx.y * kFewSplitChunk, i_hi = min(n, i_lo + kFewSplitChunk);
+  const double dk0 = j0 < n ? d[k[j0]] : 0.0, t0 = j0 < n ? tau[j0] : 1.0;
+  const double dk1 = j1 < n ? d[k[j1]] : 0.0, t1 = j1 < n ? tau[j1] : 1.0;
+  double a0[RB], a1[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) a0[r] = a1[r] = 0.0;
+  for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < RB * 32; e += 128) {
+      const int r = e >> 5, ii = e & 31, i = i0 + ii;
+      s_u[r][ii] = (r < rows && i < i_hi) ? U_in[int64_t(r) * ld_in + (src ? src[i] : i)] : 0.0;
+    }
+    if (threadIdx.x < 32) {
+      const int i = i0 + threadIdx.x;
+      s_d[threadIdx.x] = i < i_hi ? d[i] : 0.0;
+      s_z[threadIdx.x] = i < i_hi ? zhat[i] : 0.0;
+    }
+    __syncthreads();
+    const int cnt = min(32, i_hi - i0);
+#pragma unroll 2
+    for (int ii = 0; ii < 32; ++ii) {
+      const double z = s_z[ii], di = s_d[ii];
+      const double c0 = ii < cnt ? z * few_rcp((di - dk0) - t0) : 0.0;
+      const double c1 = ii < cnt ? z * few_rcp((di - dk1) - t1) : 0.0;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const double u = s_u[r][ii];
+        a0[r] = fma(c0, u, a0[r]);
+        a1[r] = fma(c1, u, a1[r]);
+      }
+    }
+  }
+  const int64_t base = int64_t(blockIdx.y) * rows * n;
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+    if (r < rows) {
+      if (j0 < n) part[base + int64_t(r) * n + j0] = a0[r];
+      if (j1 < n) part[base + int64_t(r) * n + j1] = a1[r];
+    }
+}
+
 __global__ void few_rows_combine_kernel(int rows, int n, int nsplit, const double* __restrict__ part,
                                         const double* __restrict__ cs, double* __restrict__ U_out,
                                         int64_t ld_out, const int32_t* __restrict__ dst) {
@@ -767,7 +819,14 @@ svd1_status apply_few_rows(int rows, int n, const double* d, const int32_t* k, c
   if (rows > 32) return SVD1_E_INVALID;
   const int nsplit = (n + kFewSplitChunk - 1) / kFewSplitChunk;
   const dim3 grid(unsigned((n + 127) / 128), unsigned(nsplit));
-  if (rows <= 8)
+  static const bool two = std::getenv("SVD1_FEW_ONE") == nullptr;  // two targets per thread (default)
+  const dim3 grid2(unsigned((n + 255) / 256), unsigned(nsplit));
+  if (two && rows <= 16) {
+    if (rows <= 8)
+      few_rows_partial2_kernel<8><<<grid2, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
+    else
+      few_rows_partial2_kernel<16><<<grid2, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
+  } else if (rows <= 8)
     few_rows_partial_kernel<8><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);
   else if (rows <= 16)
     few_rows_partial_kernel<16><<<grid, 128, 0, st>>>(rows, n, d, k, tau, zhat, U_in, ld_in, src, scratch);

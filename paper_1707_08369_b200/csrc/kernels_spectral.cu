@@ -75,16 +75,15 @@ __global__ void __launch_bounds__(256) proj_partial_kernel(const double* __restr
     if (c < cols) {
       const double* p = M + rb * ld + c;
       int rr = 0;
-      for (; rr + 4 <= nr; rr += 4) {
-        const double m0 = __ldg(p), m1 = __ldg(p + ld), m2 = __ldg(p + 2 * ld), m3 = __ldg(p + 3 * ld);
-        p += 4 * ld;
+      for (; rr + 8 <= nr; rr += 8) {  // 8 rows of loads in flight per thread (HBM-bound)
+        double mm[8];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          acc[v] = fma(m0, vec[v][rr], acc[v]);
-          acc[v] = fma(m1, vec[v][rr + 1], acc[v]);
-          acc[v] = fma(m2, vec[v][rr + 2], acc[v]);
-          acc[v] = fma(m3, vec[v][rr + 3], acc[v]);
-        }
+        for (int q = 0; q < 8; ++q) mm[q] = __ldg(p + q * ld);
+        p += 8 * ld;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[v] = fma(mm[q], vec[v][rr + q], acc[v]);
       }
       for (; rr < nr; ++rr, p += ld) {
         const double m0 = __ldg(p);
@@ -652,6 +651,62 @@ __global__ void __launch_bounds__(256) secfmm_phase_kernel(SecFmmDev F, const do
       }
       if (X.flags & 1) vr += v;
       else vl += v;
+    }
+    vl = warp_sum(vl);
+    vr = warp_sum(vr);
+    if (lane == 0) {
+      F.psiL[c * kSecP + i] = vl;
+      F.psiR[c * kSecP + i] = vr;
+    }
+  } else if (phase == 4) {  // direct P2M of EVERY cell from its own sources (replaces 0 + 1)
+    const int e32 = e >> 5, lane = threadIdx.x & 31;
+    if (e32 >= F.ncells * kSecP) return;
+    const int c = e32 / kSecP, i = e32 % kSecP;
+    const SecFmmCell C = F.cells[c];
+    double v = 0.0;
+    for (int s = C.lo + lane; s < C.hi; s += 32) v += z2[s] * fast_rcp(t[i] * (d[s] - C.c) - 3.0 * C.r);
+    v = warp_sum(v);
+    if (lane == 0) F.phi[c * kSecP + i] = v;
+  } else if (phase == 5) {  // every leaf's local expansions directly from the M2L / P2L partners of
+    // the leaf and of all its ancestors, evaluated at the leaf's nodes (replaces 2 + 3: the
+    // ancestors' expansions interpolate the same far field the leaf's nodes see, and the
+    // partners of an ancestor are admissible for every point of the leaf's interval)
+    const int e32 = e >> 5, lane = threadIdx.x & 31;
+    if (e32 >= (1 << L) * kSecP) return;
+    const int c = first_leaf + e32 / kSecP, i = e32 % kSecP;
+    const SecFmmCell Y = F.cells[c];
+    if (Y.hi <= Y.lo) return;
+    const double x = Y.ct + Y.rt * t[i];  // the node
+    double vl = 0.0, vr = 0.0;
+    // the (ancestor, partner) pairs of the chain, spread over the lanes: ancestor q's
+    // partners are parts[off_q, off_q + cnt_q) (a few per cell, ~L cells)
+    int offs[24], cnts[24], na = 0, total = 0;
+    for (int a = c;; a = (a - 1) / 2) {
+      if (na < 24) {
+        offs[na] = F.cells[a].m2l_off;
+        cnts[na] = F.cells[a + 1].m2l_off - offs[na];
+        total += cnts[na];
+        ++na;
+      }
+      if (a == 0) break;
+    }
+    for (int q = lane; q < total; q += 32) {
+      int qa = 0, r = q;
+      while (r >= cnts[qa]) r -= cnts[qa++];
+      {
+        const int g = offs[qa] + r;
+        const SecFmmPart X = F.parts[g];
+        const SecFmmCell C = F.cells[X.cell];
+        double v = 0.0;
+        if (X.flags & 2) {
+          for (int s2 = C.lo; s2 < C.hi; ++s2) v += z2[s2] * fast_rcp(d[s2] - x);
+        } else {
+          const double tx = 3.0 * C.r * fast_rcp(x - C.c);
+          v = tx * bary(t, w, F.phi + X.cell * kSecP, tx);
+        }
+        if (X.flags & 1) vr += v;
+        else vl += v;
+      }
     }
     vl = warp_sum(vl);
     vr = warp_sum(vr);
@@ -1244,14 +1299,22 @@ svd1_status secular_fmm(const double* d, const double* z2, double rho, int n, in
   if (n <= 0 || j1 <= j0) return SVD1_OK;
   auto grid = [](int items) { return unsigned(std::max(1, (items + 255) / 256)); };
   const int L = F.L;
-  secfmm_phase_kernel<<<grid((1 << L) * kSecP), 256, 0, st>>>(F, d, z2, 0);
-  secfmm_phase_kernel<<<grid(((1 << L) - 1) * kSecP * 32), 256, 0, st>>>(F, d, z2, 1);
-  secfmm_phase_kernel<<<grid(F.ncells * kSecP * 32), 256, 0, st>>>(F, d, z2, 2);
-  secfmm_phase_kernel<<<grid((1 << L) * kSecP * 32), 256, 0, st>>>(F, d, z2, 3);
+  static const bool chain = std::getenv("SVD1_SECFMM_CHAIN") != nullptr;  // the round-1 four phases
+  if (chain) {
+    secfmm_phase_kernel<<<grid((1 << L) * kSecP), 256, 0, st>>>(F, d, z2, 0);
+    secfmm_phase_kernel<<<grid(((1 << L) - 1) * kSecP * 32), 256, 0, st>>>(F, d, z2, 1);
+    secfmm_phase_kernel<<<grid(F.ncells * kSecP * 32), 256, 0, st>>>(F, d, z2, 2);
+    secfmm_phase_kernel<<<grid((1 << L) * kSecP * 32), 256, 0, st>>>(F, d, z2, 3);
+    *launches += 2;
+  } else {  // two launches: every cell's far field from its sources, every leaf's local
+            // expansions from the partners of its ancestor chain
+    secfmm_phase_kernel<<<grid(F.ncells * kSecP * 32), 256, 0, st>>>(F, d, z2, 4);
+    secfmm_phase_kernel<<<grid((1 << L) * kSecP * 32), 256, 0, st>>>(F, d, z2, 5);
+  }
   const int nfar = blocks_for_warps(j1 - j0);
   secular_kernel<true><<<nfar + F.ndirect, 256, 0, st>>>(d, z2, rho, n, k_out, tau_out, iters_out, status, F,
                                                           j0, j1);
-  *launches += 5;
+  *launches += 3;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

@@ -9,7 +9,7 @@ import json, sys; d=json.load(open('gpurun_out/b_' + __import__('os').environ.ge
 r=d['roofline']; print(f"[{sys.argv[1]}] value {d['value']:.1f} e2e {d['e2e']['value']:.1f} frac {r['frac']:.3f} iso {r['frac_isolated']:.3f} spec_ms/step {d['spectral_ms_per_step']:.2f} seq {d['sequential_api']['value']:.1f} allocs {d['allocations_in_timed_region']}")
 PY
 }
-b "X=1"; b "X=1"; for v in ${VARS:-}; do b "$v"; done
+for rep in 1 2 ${REPS3:+3}; do b "X=1"; for v in ${VARS:-}; do b "$v"; done; done
 if [ -n "$C5" ]; then
   timeout 600 python bench.py --config 5 --steps 8 --warmup 2 --no-cpu --no-check --no-e2e > gpurun_out/b5_$TAG.json 2> gpurun_out/b5_$TAG.err
   python -c "import json; d=json.load(open('gpurun_out/b5_$TAG.json')); print('C5', round(d['value'],2), 'ms/step', round(d['ms_per_step'],2), 'spec', round(d['spectral_ms_per_step'],2), 'apply', round(d['apply_ms_per_step'],2), 'frac', round(d['roofline']['frac'],3))"

@@ -14,7 +14,7 @@ def summary_rep(rep):
     hdr, units, rows = raw(rep)
     col = {h: i for i, h in enumerate(hdr)}
     scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
-    tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+    tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",

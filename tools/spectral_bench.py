@@ -11,7 +11,7 @@ dev = torch.device("cuda:0")
 for n in [int(x) for x in sys.argv[1:]] or [4096, 16384]:
     rng = np.random.default_rng(n)
     d, z, rho = random_secular(n, rng, kind="uniform")
-    plan = P.Plan(8, 8, eps=1e-10, flags=P.SECULAR_FMM if n >= 6144 else 0)
+    plan = P.Plan(8, 8, eps=1e-10, flags=P.SECULAR_FMM if n >= 3072 else 0)
     T = lambda x, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(x)).to(dev, dt)
     dd, zz = T(d), T(z)
     for rep in range(3):
