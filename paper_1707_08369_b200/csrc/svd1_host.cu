@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -336,6 +338,10 @@ struct StepRecord {
 
 }  // namespace
 
+// Kernel launches are counted per host thread (the U- and V-side chains of an update run on
+// two threads) and flushed into the plan's atomic total at the chains' ends.
+thread_local int64_t tl_launches = 0;
+
 struct svd1_plan_s {
   svd1_config cfg{};
   cudaStream_t st = nullptr;
@@ -349,7 +355,7 @@ struct svd1_plan_s {
   bool emulate = false;   // SVD1_EMULATE_RANKS: this process computes every rank's slices
   ncclComm_t comm[2] = {nullptr, nullptr};
   uint64_t probe_seed = 0x1707083691234567ull;
-  int64_t launches = 0;
+  std::atomic<int64_t> launches{0};
   DevBuf ctr;  // last-block counters for the test hooks (kept zero)
   DevBuf W_u, W_v, proj, partial, status, iters, ops, fmm_cells, fmm_descs, fmm_terms,
       fmm_tasks, scratch_i, scratch_d;
@@ -385,11 +391,20 @@ struct svd1_plan_s {
   // pinned upload arenas, one per side stream (U side: st, V side: st2): every
   // host->device upload is copied here first, so the DMA never reads pageable or
   // short-lived host memory; an arena is rewound only after its last copy (`ev`).
+  // A ring: `used` is the next write offset; every copy out of the ring is a region with an
+  // event, and a reservation waits only for the in-flight regions it would overwrite (the
+  // oldest ones, from the previous lap), never for the copies just enqueued.
   struct Arena {
+    struct Region {
+      size_t lo, hi;
+      cudaEvent_t ev;
+    };
     char* buf = nullptr;
     size_t cap = 0, used = 0;
-    cudaEvent_t ev = nullptr;
+    cudaEvent_t ev = nullptr;    // (unused; kept for the create/destroy bookkeeping)
     bool pending = false;
+    std::deque<Region> inflight;  // in allocation order
+    std::vector<cudaEvent_t> pool;  // recycled events
   } arena[6];  // sides 0, 1: apply streams; 2, 3: batch spectral streams; 4, 5: uploads
   CauchyPrep standalone;    // plan of the standalone svd1_cauchy_apply
   std::vector<int32_t> rot_goff, rot_cols;  // pairing rotations of repeated sigma clusters
@@ -399,6 +414,12 @@ struct svd1_plan_s {
 };
 
 namespace {
+
+int64_t* LC(svd1_plan_t) { return &tl_launches; }
+void flush_launches(svd1_plan_t P) {
+  P->launches += tl_launches;
+  tl_launches = 0;
+}
 
 svd1_status pinned(svd1_plan_t P, size_t doubles, double** out) {
   void* b = P->h_pin;
@@ -445,7 +466,11 @@ cudaStream_t side_stream(svd1_plan_t P, int side) {
 // Wait for the uploads in flight and rewind the arenas (called at API entry points).
 svd1_status arena_reset(svd1_plan_t P, int side) {
   auto& A = P->arena[side];
-  if (A.pending) SVD1_CUDA_TRY(cudaEventSynchronize(A.ev));
+  for (auto& R : A.inflight) {
+    SVD1_CUDA_TRY(cudaEventSynchronize(R.ev));
+    A.pool.push_back(R.ev);
+  }
+  A.inflight.clear();
   A.pending = false;
   A.used = 0;
   return SVD1_OK;
@@ -455,19 +480,39 @@ svd1_status arena_reset(svd1_plan_t P) {
   return SVD1_OK;
 }
 
-// reserve `bytes` of side's arena (rewinding or growing it when full): offset
+// reserve `bytes` of side's ring (growing it only if a single request exceeds it): offset.
+// Waits for the in-flight copies that still read [off, off + bytes).
 svd1_status arena_reserve(svd1_plan_t P, int side, size_t bytes, size_t* off_out) {
   auto& A = P->arena[side];
-  if (!A.ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&A.ev, cudaEventDisableTiming));
+  if (bytes > A.cap) {  // sized at creation; an outgrown estimate reallocates (counted)
+    TRY(arena_reset(P, side));
+    void* b = A.buf;
+    TRY(pinned_reserve(&b, &A.cap, std::max<size_t>(bytes * 2, size_t(4) << 20)));
+    A.buf = static_cast<char*>(b);
+  }
   size_t off = (A.used + 255) & ~size_t(255);
-  if (off + bytes > A.cap) {
-    TRY(arena_reset(P, side));  // everything staged so far has been consumed
-    if (bytes > A.cap) {  // sized at creation; an outgrown estimate reallocates (counted)
-      void* b = A.buf;
-      TRY(pinned_reserve(&b, &A.cap, std::max<size_t>(bytes * 2, size_t(4) << 20)));
-      A.buf = static_cast<char*>(b);
+  if (off + bytes > A.cap) off = 0;  // wrap
+  const size_t lo = off, hi = off + bytes;
+  while (!A.inflight.empty()) {
+    const auto& R = A.inflight.front();
+    // regions are in allocation order: the front is the oldest; once it does not overlap
+    // the new range the newer ones (beyond it in this lap, or behind the head) cannot either
+    // -- except after a wrap, where every region of the previous lap above `lo` may overlap
+    const bool overlap = R.lo < hi && lo < R.hi;
+    if (!overlap) {
+      // an older region entirely below lo (this lap) or above hi: check the rest only if it
+      // could still overlap (previous-lap regions above lo)
+      bool any = false;
+      for (const auto& Q : A.inflight)
+        if (Q.lo < hi && lo < Q.hi) {
+          any = true;
+          break;
+        }
+      if (!any) break;
     }
-    off = 0;
+    SVD1_CUDA_TRY(cudaEventSynchronize(R.ev));
+    A.pool.push_back(R.ev);
+    A.inflight.pop_front();
   }
   *off_out = off;
   return SVD1_OK;
@@ -477,7 +522,15 @@ svd1_status arena_commit(svd1_plan_t P, int side, size_t off, size_t bytes, void
   auto& A = P->arena[side];
   const cudaStream_t st = side_stream(P, side);
   SVD1_CUDA_TRY(cudaMemcpyAsync(dev, A.buf + off, bytes, cudaMemcpyHostToDevice, st));
-  SVD1_CUDA_TRY(cudaEventRecord(A.ev, st));
+  cudaEvent_t ev;
+  if (!A.pool.empty()) {
+    ev = A.pool.back();
+    A.pool.pop_back();
+  } else {
+    SVD1_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  SVD1_CUDA_TRY(cudaEventRecord(ev, st));
+  A.inflight.push_back({off, off + bytes, ev});
   A.pending = true;
   A.used = off + bytes;
   return SVD1_OK;
@@ -573,8 +626,10 @@ double bwin_ms(svd1_plan_t P, int par) {
   return std::max(el(0, 2), el(0, 3)) - std::min(0.0, el(0, 1));
 }
 
+std::mutex g_tl_mutex;  // the timeline's vectors (both side threads mark)
 void tl_mark(svd1_plan_t P, const std::string& label, cudaStream_t st, bool dev = true) {  // diagnostics
   if (!P->tl_on) return;
+  std::lock_guard<std::mutex> lock(g_tl_mutex);
   P->tl_host.push_back({label, now_ms() - P->tl_t0});
   if (dev) {
     cudaEvent_t e;
@@ -1251,38 +1306,70 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
   const Merged M = merge_points(da, mu);
   int L0 = 0;
   while ((2 * int64_t(na) + (int64_t(1) << L0) - 1) / (int64_t(1) << L0) > 2 * leaf) ++L0;
-  FmmHost best;
-  bool have = false;
-  for (int L = L0; L <= L0 + 2 && L <= 22; ++L) {
-    // a deeper tree only pays when the shallower one has wide leaves (outliers)
-    if (have && best.max_near <= 8) break;
-    FmmHost F2;
-    if (!fmm_cells(F2, leaf, L, M)) {
-      if (std::getenv("SVD1_DEBUG")) fprintf(stderr, "[svd1] fmm L=%d infeasible\n", L);
-      continue;
-    }
-    // a leaf whose hull spans a quarter of the spectrum (outliers packed with bulk
-    // points because the capacities left no room for a gap split) is near to every
-    // leaf: skip building lists for such a tree when a deeper one is still to come
+  // The candidate depths L0, L0 + 1, L0 + 2 are built concurrently (the plan is on the
+  // critical path of the stream: an apply starts when its plan is ready); the choice is then
+  // made over the results in depth order exactly as a sequential search would make it.
+  struct Cand {
+    FmmHost F;
+    int state = 0;  // 0 infeasible, 1 skipped (wide leaf), 2 built
+  };
+  const int Lhi = std::min(L0 + 2, 22);
+  std::vector<Cand> cand(size_t(std::max(0, Lhi - L0 + 1)));
+  auto build = [&](int L) {
+    Cand& C = cand[size_t(L - L0)];
+    if (!fmm_cells(C.F, leaf, L, M)) return;
+    // a leaf whose hull spans a quarter of the spectrum (outliers packed with bulk points
+    // because the capacities left no room for a gap split) is near to every leaf: such a
+    // tree is skipped when a deeper one is still to come
     if (L < L0 + 2) {
       double rmax = 0.0;
-      for (int i = 0; i < (1 << L); ++i) rmax = std::max(rmax, F2.cells[(1 << L) - 1 + i].r);
-      if (rmax >= 0.25 * F2.cells[0].r && F2.cells[0].r > 0.0) {
-        if (std::getenv("SVD1_DEBUG")) fprintf(stderr, "[svd1] fmm L=%d skipped (wide leaf)\n", L);
-        continue;
+      for (int i = 0; i < (1 << L); ++i) rmax = std::max(rmax, C.F.cells[(1 << L) - 1 + i].r);
+      if (rmax >= 0.25 * C.F.cells[0].r && C.F.cells[0].r > 0.0) {
+        C.state = 1;
+        return;
       }
     }
-    const double tl0 = now_ms();
-    fmm_lists(F2, p, src, rows);
-    if (std::getenv("SVD1_DEBUG"))
-      fprintf(stderr, "[svd1] fmm L=%d flops/row=%lld max_near=%d m2l=%d near=%d lists %.3f ms\n", L,
-              (long long)F2.flops_per_row, F2.max_near, F2.n_m2l_pairs, F2.n_near_pairs, now_ms() - tl0);
-    // cost: executed flops plus one launch-equivalent per pass
-    auto cost = [rows](const FmmHost& H) {
-      return double(H.flops_exec_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
-    };
-    if (!have || cost(F2) < cost(best)) {
-      best = std::move(F2);
+    fmm_lists(C.F, p, src, rows);
+    C.state = 2;
+  };
+  auto cost_of = [rows](const FmmHost& H) {
+    return double(H.flops_exec_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
+  };
+  static const bool parallel = std::getenv("SVD1_PLAN_PARALLEL") != nullptr;  // (experiments)
+  if (parallel) {
+    std::vector<std::thread> th;
+    for (int L = L0 + 1; L <= Lhi; ++L) th.emplace_back(build, L);
+    if (L0 <= Lhi) build(L0);
+    for (auto& t : th) t.join();
+  } else {  // sequential, building only the depths the search below looks at
+    int ib = -1;  // best built so far (the same rule as the selection loop)
+    for (int L = L0; L <= Lhi; ++L) {
+      if (ib >= 0 && cand[size_t(ib)].F.max_near <= 8) break;
+      build(L);
+      Cand& C = cand[size_t(L - L0)];
+      if (C.state == 2 && (ib < 0 || cost_of(C.F) < cost_of(cand[size_t(ib)].F))) ib = L - L0;
+    }
+  }
+  // cost: executed flops plus one launch-equivalent per pass
+  auto cost = [rows](const FmmHost& H) {
+    return double(H.flops_exec_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
+  };
+  FmmHost best;
+  bool have = false;
+  for (int L = L0; L <= Lhi; ++L) {
+    // a deeper tree only pays when the shallower one has wide leaves (outliers)
+    if (have && best.max_near <= 8) break;
+    Cand& C = cand[size_t(L - L0)];
+    if (std::getenv("SVD1_DEBUG")) {
+      if (C.state == 0) fprintf(stderr, "[svd1] fmm L=%d infeasible\n", L);
+      if (C.state == 1) fprintf(stderr, "[svd1] fmm L=%d skipped (wide leaf)\n", L);
+      if (C.state == 2)
+        fprintf(stderr, "[svd1] fmm L=%d flops/row=%lld max_near=%d m2l=%d near=%d\n", L,
+                (long long)C.F.flops_per_row, C.F.max_near, C.F.n_m2l_pairs, C.F.n_near_pairs);
+    }
+    if (C.state != 2) continue;
+    if (!have || cost(C.F) < cost(best)) {
+      best = std::move(C.F);
       have = true;
     }
   }
@@ -1399,7 +1486,7 @@ svd1_status cauchy_build_ops(svd1_plan_t P, CauchyPrep& C, const double* d_da, c
   auto* ops = static_cast<double*>(C.d_ops.p);
   SVD1_CUDA_TRY(cudaMemsetAsync(ops, 0, size_t(std::max<int64_t>(F.ops_rows, 1)) * 16 * sizeof(double), st));
   return fmm_build_ops(int(F.ops.size()), C.ddescs, C.dcells, C.p, d_da, d_k, d_tau, d_zhat, d_cs, C.dcol2src, ops,
-                       std::max<int64_t>(F.ops_rows, 1) * 16, st, &P->launches);
+                       std::max<int64_t>(F.ops_rows, 1) * 16, st, LC(P));
 }
 
 constexpr int kMapSlots = 64;  // TMA descriptor sets per apply (one per row chunk, §4.11)
@@ -1416,7 +1503,7 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   if (rows <= 0) return SVD1_OK;
   if (!C.fmm)
     return apply_direct(rows, C.na, d_da, d_k, d_tau, d_zhat, d_cs, U_in, ld_in, d_src, U_out, ld_out,
-                        d_dst, st, &P->launches);
+                        d_dst, st, LC(P));
   FmmHost& F = C.F;
   const int p = C.p;
   double *phi, *psi;
@@ -1562,7 +1649,7 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
     if (e <= b) continue;
     TRY(gmark());
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, maps, U_out, ld_out, d_dst, phi, psi, ldE,
-                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, st, &P->launches));
+                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, st, LC(P)));
     TRY(gmark());
     pmark();
     if (dbg) {
@@ -1886,23 +1973,23 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     // output index range [lo, hi); the solver works in the rho > 0 view (reflected for rho < 0)
     const int j0 = rho < 0.0 ? na - sl.hi : sl.lo, j1 = rho < 0.0 ? na - sl.lo : sl.hi;
     if (S.sec_fmm_used)  // with the far field by FMM
-      TRY(secular_fmm(ddr, dz2r, rho, na, j0, j1, F, dk, dtau, dit, dst + r, st, &P->launches));
+      TRY(secular_fmm(ddr, dz2r, rho, na, j0, j1, F, dk, dtau, dit, dst + r, st, LC(P)));
     else
-      TRY(secular(ddr, dz2r, rho, na, j0, j1, dk, dtau, dit, dst + r, st, &P->launches));
+      TRY(secular(ddr, dz2r, rho, na, j0, j1, dk, dtau, dit, dst + r, st, LC(P)));
   }
   TRY(exchange(P, chain, st, {{dk, c_sl, ncclInt32, 4}, {dtau, c_sl, ncclFloat64, 8}, {dit, c_sl, ncclInt32, 4},
                               {dst, 1, ncclInt32, 4}}));
   tl_mark(P, "  ev" + std::to_string(ev0) + " secular done", st);
   for (int r = r_lo; r < r_hi; ++r) {
     const Slice sl = slice_of(na, G, r);
-    TRY(loewner(dda, dk, dtau, rho, dza, na, sl.lo, sl.hi, dzh, scr, ctr, st, &P->launches));
+    TRY(loewner(dda, dk, dtau, rho, dza, na, sl.lo, sl.hi, dzh, scr, ctr, st, LC(P)));
   }
   TRY(exchange(P, chain, st, {{dzh, c_sl, ncclFloat64, 8}}));
   tl_mark(P, "  ev" + std::to_string(ev0) + " loewner done", st);
   for (int r = r_lo; r < r_hi; ++r) {
     const Slice sl = slice_of(na, G, r);
     TRY(colnorm_carry(dda, dk, dtau, dzh, na, sl.lo, sl.hi, dcar, nc, dcs, dco, nap, dst + r, scr, ctr, st,
-                      &P->launches));
+                      LC(P)));
   }
   {
     std::vector<GatherPart> parts{{dcs, c_sl, ncclFloat64, 8}, {dst, 1, ncclInt32, 4}};
@@ -2126,14 +2213,14 @@ svd1_status apply_chunk(svd1_plan_t P, StepRecord& S, double* U_in, int64_t ld_i
   U_out += r0 * ld_out;
   if (S.h_goff.size() > 1)
     TRY(householder_cols(rows, U_in, ld_in, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, S.h_maxlen(), st,
-                         &P->launches));
+                         LC(P)));
   if (S.na > 0)
     TRY(cauchy_launch(P, S.cp, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
                       static_cast<double*>(S.d_out.p) + S.nap, static_cast<double*>(S.d_zhat.p), S.dcs,
                       U_in, ld_in, S.dsrc, U_out, ld_out, S.ddst, st, side, rows, slot, last_chunk));
   if (!S.pass_src.empty())
     TRY(passthrough(rows, int(S.pass_src.size()), U_in, ld_in, S.dpsrc, U_out, ld_out, S.dpdst, S.dpscale,
-                    st, &P->launches));
+                    st, LC(P)));
   return SVD1_OK;
 }
 
@@ -2262,7 +2349,7 @@ svd1_status plan_reserve(svd1_plan_t P) {
   TRY(P->proj.reserve<double>(nproj));
   TRY(P->partial.reserve<double>(size_t(project_partial_elems(c.u_rows, m, c.v_rows, n))));
   TRY(P->probes.reserve<double>(size_t(4 * std::max<int64_t>(c.u_rows, 1))));
-  TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, static_cast<double*>(P->probes.p), P->st, &P->launches));
+  TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, static_cast<double*>(P->probes.p), P->st, LC(P)));
   P->probes_ready = true;
   // Phi, Psi of both sides for the deepest tree (zeroed: see ensure_expansions)
   for (int side = 0; side < 2; ++side) {
@@ -2406,6 +2493,8 @@ svd1_status svd1_plan_destroy(svd1_plan_t P) {
   for (auto& A : P->arena) {
     if (A.buf) cudaFreeHost(A.buf);
     if (A.ev) cudaEventDestroy(A.ev);
+    for (auto& R : A.inflight) cudaEventDestroy(R.ev);
+    for (auto e : A.pool) cudaEventDestroy(e);
   }
   for (auto& e : P->ev)
     if (e) cudaEventDestroy(e);
@@ -2436,11 +2525,11 @@ svd1_status svd1_project(svd1_plan_t P, const double* U, int64_t ldu, const doub
   if (!P->probes_ready) {  // the probes depend only on (seed, global row): once per plan
     double* g;
     TRY(P->probes.get<double>(size_t(4 * std::max<int64_t>(c.u_rows, 1)), &g, P->st));
-    TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, g, P->st, &P->launches));
+    TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, g, P->st, LC(P)));
     P->probes_ready = true;
   }
   return project(U, ldu, c.u_rows, c.m, c.u_row0, V, ldv, c.v_rows, c.n, c.v_row0, a, b, part, need,
-                 proj, static_cast<double*>(P->probes.p), P->st, &P->launches, thin ? c.m : c.n);
+                 proj, static_cast<double*>(P->probes.p), P->st, LC(P), thin ? c.m : c.n);
 }
 
 }  // extern "C"
@@ -2471,17 +2560,17 @@ svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, in
   if (rows <= 0) return SVD1_OK;
   if (S.h_goff.size() > 1)
     TRY(householder_cols(rows, in, ld, int(S.h_goff.size()) - 1, S.dgoff, S.dhcols, S.dhv, S.h_maxlen(), st,
-                         &P->launches));
+                         LC(P)));
   if (S.na > 0) {
     double* scr;
     TRY(P->few_scr[side].get<double>(size_t(few_rows_scratch_elems(rows, S.na)), &scr, st));
     TRY(apply_few_rows(rows, S.na, static_cast<double*>(S.d_in.p), static_cast<int32_t*>(S.d_out.p),
                        static_cast<double*>(S.d_out.p) + S.nap, static_cast<double*>(S.d_zhat.p), S.dcs, in, ld,
-                       S.dsrc, out, ld, S.ddst, scr, st, &P->launches));
+                       S.dsrc, out, ld, S.ddst, scr, st, LC(P)));
   }
   if (!S.pass_src.empty())
     TRY(passthrough(rows, int(S.pass_src.size()), in, ld, S.dpsrc, out, ld, S.dpdst, S.dpscale, st,
-                    &P->launches));
+                    LC(P)));
   return SVD1_OK;
 }
 
@@ -2524,11 +2613,11 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if (thin && ((c.v_rows && !b_dev) || (B && (!B->y_dev || !B->gram)))) return SVD1_E_INVALID;
   if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < nv))) return SVD1_E_INVALID;
   if (m > (int64_t(1) << 30) || n > (int64_t(1) << 30)) return SVD1_E_INVALID;
+  flush_launches(P);
   const int64_t launches0 = P->launches;
   const int64_t allocs0 = g_allocs.load();
   const double t0 = now_ms();
-  if (B) {  // the apply streams' arenas are unused in this mode
-    for (int sd = 2; sd < 6; ++sd) TRY(arena_reset(P, sd));
+  if (B) {  // (the rings of the batch streams recycle themselves: no wait here)
   } else {
     TRY(arena_reset(P));
   }
@@ -2558,6 +2647,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   R.t_ms[0] = now_ms() - t0;
   if (alpha == 0.0 || beta == 0.0) {  // A_hat = A
     R.noop = 1;
+    flush_launches(P);
     R.kernel_launches = P->launches - launches0;
     R.allocations = g_allocs.load() - allocs0;
     if (rep) *rep = R;
@@ -2645,11 +2735,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     cv1.insert(cv1.begin(), cv[0]);
     cu.swap(cu1);
     cv.swap(cv1);
-    const std::string ut = B ? "u" + std::to_string(B->t) + " " : "";
-    tl_mark(P, ut + "U1 spectral", side_stream(P, sp0));
-    TRY(spectral_launch(P, S[0], Du, zu, su.rho1, cu, 8, sp0, 0));
-    tl_mark(P, ut + "V1 spectral", side_stream(P, sp1));
-    TRY(spectral_launch(P, S[2], Dv, zv, sv.rho1, cv, 12, sp1, 1));
+    z1.swap(zu);
+    z3.swap(zv);
   }
   const double tA = now_ms();
   std::atomic<bool> planned[4] = {false, false, false, false};  // outlives the Joiners
@@ -2717,12 +2804,12 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     double* rout = static_cast<double*>(R[second ? 0 : 1].p);
     if (thin && e == 2)  // the later b's coordinates along this update's q
       TRY(thin_carry(rows, rin, ld, m, B->y_dev, B->gram, B->t, B->K, beta_perp > 0.0 ? 1.0 / beta_perp : 0.0,
-                     ss, &P->launches));
+                     ss, LC(P)));
     TRY(apply_rows(P, S[e], rin, rout, ld, rows, ss, side));
     if (e == 3 && rows > 0 && nrot_v() > 0)
       TRY(col_rotate(rows, rout, ld, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                      static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), ss,
-                     &P->launches));
+                     LC(P)));
     if (second) {  // read back the next update's rows: x_a | x_g (U side), y_b (V side)
       if (!P->rb_ev[side]) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->rb_ev[side], cudaEventDisableTiming));
       if (side == 0 && B->ru_next >= 0) {
@@ -2764,7 +2851,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   auto null_dir = [&]() -> svd1_status {
     if (!thin || !c.v_rows) return SVD1_OK;
     return null_direction(c.v_rows, V, ldv, m, b_dev, c.v_row0, B ? B->y_dev : proj + 5 * m,
-                          beta_perp > 0.0 ? 1.0 / beta_perp : 0.0, stv, &P->launches);
+                          beta_perp > 0.0 ? 1.0 / beta_perp : 0.0, stv, LC(P));
   };
   // Fused per-side pass (SVD1_FUSED_SIDE): once both steps
   // of a side are planned, the side's rows go through X1 then X2 in chunks sized so that a
@@ -2796,7 +2883,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       if (side && nrot_v() > 0)
         TRY(col_rotate(nr, X + r0 * ldx, ldx, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                        static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), st,
-                       &P->launches));
+                       LC(P)));
     }
     // the side's whole time is reported on its first step (apply_ms[e1]); the second's is 0
     TRY(ev_record(P, 2 * e1 + 1, st));
@@ -2828,72 +2915,126 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     }
     return SVD1_OK;
   };
-  while (!(fin[0] && fin[1] && fin[2] && fin[3])) {
-    if (fin[0] && !uploaded_u1 && planned[0].load(std::memory_order_acquire)) {
-      plan_u.join();
-      TRY(first_apply(0));
-      uploaded_u1 = true;
-      continue;
+  // The two sides' chains (U: STEP 4 -> STEP 5, V: STEP 6 -> STEP 7) are
+  // independent until the sign alignment: each runs on its own host thread (the V side on
+  // a second thread), so one side's host work (sort / deflation / secular-FMM plan before a
+  // launch, merge and maps after a read-back) overlaps the other side's, and each polls
+  // only its own readiness (cudaEventQuery, atomic plan flags).  Per side: launch step 1;
+  // when its read-back lands, finish it (host merge), start its FMM plan on a worker
+  // thread, transform the carried rows (batch mode), launch step 2; launch the first apply
+  // as soon as its plan is ready; finish step 2 and start its plan.
+  const std::string ut = B ? "u" + std::to_string(B->t) + " " : "";
+  auto chain = [&](int side) -> svd1_status {
+    const int e1 = side ? 2 : 0, e2 = e1 + 1;
+    const int sps = side ? sp1 : sp0;
+    std::vector<double>& Dd = side ? Dv : Du;
+    std::vector<std::vector<double>>& cc = side ? cv : cu;
+    Joiner& J1 = side ? plan_v : plan_u;
+    Joiner& J2 = side ? plan_v2 : plan_u2;
+    bool& uploaded = side ? uploaded_v1 : uploaded_u1;
+    const int64_t rows = side ? c.v_rows : c.u_rows;
+    const double rho1 = side ? sv.rho1 : su.rho1, rho2 = side ? sv.rho2 : su.rho2;
+    const char* nm = side ? "V" : "U";
+    tl_mark(P, ut + nm + "1 spectral", side_stream(P, sps));
+    TRY(spectral_launch(P, S[e1], Dd, side ? z3 : z1, rho1, cc, side ? 12 : 8, sps, side));
+    while (!landed(e1)) std::this_thread::yield();
+    t_dbg[side ? 3 : 0] = now_ms();
+    TRY(spectral_finish(P, S[e1], Dd, cc));
+    fin[e1] = true;
+    spawn_plan(J1, e1, false, side, rows);
+    if (B) TRY(rows_step(e1));
+    {
+      std::vector<double> z2 = cc[0];
+      cc.erase(cc.begin());
+      tl_mark(P, ut + nm + "1 finished; " + nm + "2 spectral", side_stream(P, sps));
+      TRY(spectral_launch(P, S[e2], Dd, z2, rho2, cc, side ? 14 : 10, sps, side));
     }
-    if (fin[2] && !uploaded_v1 && planned[2].load(std::memory_order_acquire)) {
-      plan_v.join();
-      TRY(first_apply(2));
-      uploaded_v1 = true;
-      continue;
+    t_fin[e1] = now_ms();
+    while (!fin[e2]) {
+      if (!uploaded && planned[e1].load(std::memory_order_acquire)) {
+        J1.join();
+        TRY(first_apply(e1));
+        uploaded = true;
+        continue;
+      }
+      if (landed(e2)) {
+        TRY(spectral_finish(P, S[e2], Dd, cc));
+        fin[e2] = true;
+        tl_mark(P, ut + nm + "2 finished", nullptr, false);
+        spawn_plan(J2, e2, true, side, rows);
+        if (B && side == 0) TRY(rows_step(1));  // (V2's rows need the sign alignment)
+        t_fin[e2] = now_ms();
+        continue;
+      }
+      std::this_thread::yield();
     }
-    if (!fin[0] && landed(0)) {  // U: finish STEP 4, launch STEP 5 (rho2, z2 = X1^T U^T b1)
-      t_dbg[0] = now_ms();
-      TRY(spectral_finish(P, S[0], Du, cu));
-      fin[0] = true;
-      t_dbg[1] = now_ms();
-      spawn_plan(plan_u, 0, false, 0, c.u_rows);
-      if (B) TRY(rows_step(0));
-      t_dbg[2] = now_ms();
-      std::vector<double> z2 = cu[0];
-      cu.erase(cu.begin());
-      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U1 finished; U2 spectral", side_stream(P, sp0));
-      TRY(spectral_launch(P, S[1], Du, z2, su.rho2, cu, 10, sp0, 0));
-      t_fin[0] = now_ms();
-      continue;
+    if (!uploaded) {
+      J1.join();
+      TRY(first_apply(e1));
+      uploaded = true;
     }
-    if (!fin[2] && landed(2)) {  // V: finish STEP 6, launch STEP 7 (rho4)
-      TRY(spectral_finish(P, S[2], Dv, cv));
-      fin[2] = true;
-      spawn_plan(plan_v, 2, false, 1, c.v_rows);
-      if (B) TRY(rows_step(2));
-      std::vector<double> z4 = cv[0];
-      cv.erase(cv.begin());
-      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V1 finished; V2 spectral", side_stream(P, sp1));
-      TRY(spectral_launch(P, S[3], Dv, z4, sv.rho2, cv, 14, sp1, 1));
-      t_fin[2] = now_ms();
-      continue;
+    return SVD1_OK;
+  };
+  // U-side applies (they need every eigen-update to have succeeded -- the factors stay
+  // untouched on a numerical error -- but not the sign alignment, which only scales V2's
+  // columns): launched from the U thread as soon as the V chain has finished.
+  auto u_applies = [&]() -> svd1_status {
+    if (fused) {  // both steps of the side row chunk by row chunk (§4.11)
+      plan_u2.join();
+      TRY(rare_grow(1, 0));
+      TRY(upload_step(1));
+      TRY(fused_side(0));
+    } else {
+      if (!launched_u1) {  // (its input had a Householder group: deferred to here)
+        TRY(ev_record(P, 16, P->st));
+        if (B) TRY(bwin_record(P, B->parity, 0, P->st));
+        if (B && B->t == 0) TRY(bspan_record(P, 0, P->st));
+        TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
+      }
+      plan_u2.join();
+      TRY(rare_grow(1, 0));
+      TRY(upload_step(1));
+      tl_mark(P, ut + "U2 apply", P->st);
+      TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
     }
-    if (fin[0] && !fin[1] && landed(1)) {
-      TRY(spectral_finish(P, S[1], Du, cu));
-      fin[1] = true;
-      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U2 finished", nullptr, false);
-      spawn_plan(plan_u2, 1, true, 0, c.u_rows);
-      if (B) TRY(rows_step(1));
-      t_fin[1] = now_ms();
-      continue;
+    if (B) {
+      tl_mark(P, ut + "U2 end", P->st);
+      TRY(bwin_record(P, B->parity, 2, P->st));
+      if (!P->bdone[B->parity][0])
+        SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][0], cudaEventDisableTiming));
+      SVD1_CUDA_TRY(cudaEventRecord(P->bdone[B->parity][0], P->st));
     }
-    if (fin[2] && !fin[3] && landed(3)) {
-      TRY(spectral_finish(P, S[3], Dv, cv));
-      fin[3] = true;
-      tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " V2 finished", nullptr, false);
-      spawn_plan(plan_v2, 3, true, 1, c.v_rows);
-      t_fin[3] = now_ms();
-      continue;
-    }
-    std::this_thread::yield();
+    return SVD1_OK;
+  };
+  // U chain + U applies on a second host thread, V chain here; the sign alignment (below)
+  // waits for both chains' spectral results.  States: 0 running, 1 succeeded, 2 failed.
+  std::atomic<int> u_state{0}, v_state{0};
+  svd1_status st_u = SVD1_OK, st_ua = SVD1_OK;
+  Joiner u_thread;
+  if (one_stream) {  // (diagnostics: both chains on one stream and one arena -> one thread)
+    st_u = chain(0);
+    u_state = st_u == SVD1_OK ? 1 : 2;
+  } else {
+    u_thread.add(std::thread([&] {
+      st_u = chain(0);
+      u_state.store(st_u == SVD1_OK ? 1 : 2, std::memory_order_release);
+      if (st_u == SVD1_OK) {
+        int v;
+        while ((v = v_state.load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+        if (v == 1) st_ua = u_applies();
+      }
+      flush_launches(P);
+    }));
   }
-  if (!uploaded_u1) {
-    plan_u.join();
-    TRY(first_apply(0));
-  }
-  if (!uploaded_v1) {
-    plan_v.join();
-    TRY(first_apply(2));
+  {
+    const svd1_status st_v = chain(1);
+    v_state.store(st_v == SVD1_OK ? 1 : 2, std::memory_order_release);
+    while (u_state.load(std::memory_order_acquire) == 0) std::this_thread::yield();
+    if (st_v != SVD1_OK || st_u != SVD1_OK) {
+      u_thread.join();
+      TRY(st_u);
+      return st_v;
+    }
   }
   if (std::getenv("SVD1_TIMING"))
     fprintf(stderr, "[svd1] host: launch1 %.3f finished U1 %.3f U2 %.3f V1 %.3f V2 %.3f (plans %.3f %.3f) U1 landed %.3f finish %.3f spawn %.3f\n",
@@ -3037,22 +3178,13 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // eigen-update succeeded: the first applies that transform their input in place can
   // start now; the second applies follow as soon as their plans are uploaded.
   const double t4 = now_ms();
+  if (one_stream) TRY(u_applies());
   if (fused) {  // both steps of a side row chunk by row chunk (§4.11)
-    plan_u2.join();
-    TRY(rare_grow(1, 0));
-    TRY(upload_step(1));
-    TRY(fused_side(0));
     plan_v2.join();
     TRY(rare_grow(3, 1));
     TRY(upload_step(3));  // carries the sign alignment
     if (!B) TRY(upload_rot(one_stream ? 0 : 1));
     TRY(fused_side(1));
-  }
-  if (!fused && !launched_u1) {
-    TRY(ev_record(P, 16, P->st));
-    if (B) TRY(bwin_record(P, B->parity, 0, P->st));
-    if (B && B->t == 0) TRY(bspan_record(P, 0, P->st));
-    TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
   }
   if (!fused && !launched_v1) {
     TRY(ev_record(P, 18, stv));
@@ -3062,11 +3194,6 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     TRY(apply_launch(P, S[2], V, ldv, Wv, nv, 4, stv, 1));
   }
   if (!fused) {
-    plan_u2.join();
-    TRY(rare_grow(1, 0));
-    TRY(upload_step(1));
-    tl_mark(P, (B ? "u" + std::to_string(B->t) : std::string()) + " U2 apply", P->st);
-    TRY(apply_launch(P, S[1], Wu, m, U, ldu, 2, P->st, 0));
     plan_v2.join();
     TRY(rare_grow(3, 1));
     TRY(upload_step(3));  // carries the sign alignment
@@ -3076,18 +3203,16 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     if (nrot_v() > 0)
       TRY(col_rotate(c.v_rows, V, ldv, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                      static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
-                     &P->launches));
+                     LC(P)));
   }
+  u_thread.join();  // the U-side applies are queued
+  TRY(st_ua);
   if (B) {  // no join, no sync: the next update's spectral phase overlaps these applies
-    tl_mark(P, "u" + std::to_string(B->t) + " U2 end", P->st);
     tl_mark(P, "u" + std::to_string(B->t) + " V2 end", stv);
-    TRY(bwin_record(P, B->parity, 2, P->st));
     TRY(bwin_record(P, B->parity, 3, stv));
-    for (int sd = 0; sd < 2; ++sd) {
-      if (!P->bdone[B->parity][sd])
-        SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][sd], cudaEventDisableTiming));
-      SVD1_CUDA_TRY(cudaEventRecord(P->bdone[B->parity][sd], side_stream(P, sd)));
-    }
+    if (!P->bdone[B->parity][1])
+      SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][1], cudaEventDisableTiming));
+    SVD1_CUDA_TRY(cudaEventRecord(P->bdone[B->parity][1], stv));
     P->bdone_rec[B->parity] = true;
     R.t_ms[2] = now_ms() - t4;
     *B->sig = sig_new;
@@ -3104,6 +3229,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       R.mean_iter[e] = S[e].mean_iter;
     }
     R.t_ms[4] = now_ms() - t0;
+    flush_launches(P);
     R.kernel_launches = P->launches - launches0;
     R.allocations = g_allocs.load() - allocs0;
     if (rep) *rep = R;
@@ -3141,6 +3267,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     fprintf(stderr, "[svd1] dev end %.3f; host: spectral rounds %.3f, t4 %.3f, end %.3f\n", ev_ms(P, 8, 17),
             t3 - t1, t4 - t1, now_ms() - t1);
   }
+  flush_launches(P);
   R.kernel_launches = P->launches - launches0;
   R.allocations = g_allocs.load() - allocs0;
   if (rep) *rep = R;
@@ -3180,7 +3307,7 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
     TRY(P->partial.get<double>(size_t(need), &part, P->st));
     TRY(project_many(U, ldu, c.u_rows, m, c.u_row0, V, ldv, c.v_rows, n, c.v_row0, thin ? m : n, A + lda, lda,
                      Bv + ldb, ldb, int(K) - 1, static_cast<double*>(P->probes.p), part, need, pj + nproj,
-                     int64_t(nproj), P->st, &P->launches));
+                     int64_t(nproj), P->st, LC(P)));
   }
   return svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, Bv, ldb, K, eps, reps);
 }
@@ -3233,7 +3360,7 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   double* gram = nullptr;  // thin: b_t . b_s
   if (thin) {
     TRY(P->bgram.get<double>(size_t(kMaxBatch) * kMaxBatch, &gram, P->st));
-    TRY(gram_rows(k, P->batch_b, P->batch_ldb, n, gram, P->st, &P->launches));
+    TRY(gram_rows(k, P->batch_b, P->batch_ldb, n, gram, P->st, LC(P)));
   }
   // host copies of the projections (dots of every update; x's of update 0) and sigma
   double* h;
@@ -3436,7 +3563,7 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
   SVD1_CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(int32_t), P->st));
   double* orient;
   TRY(P->scratch_d.get<double>(size_t(2 * n), &orient, P->st));
-  TRY(secular_orient(d, z, rho, int(n), orient, orient + n, P->st, &P->launches));
+  TRY(secular_orient(d, z, rho, int(n), orient, orient + n, P->st, LC(P)));
   if (use_sec_fmm(P->cfg.flags, int(n), false)) {  // plan from the oriented sources (host copy)
     std::vector<double> dr(n);
     SVD1_CUDA_TRY(cudaMemcpyAsync(dr.data(), orient, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
@@ -3444,9 +3571,9 @@ svd1_status svd1_secular_solve(svd1_plan_t P, int64_t n, const double* d, const 
     SecFmmDev F;
     TRY(arena_reset(P));
     TRY(secfmm_prepare(P, P->steps[0].sec, P->steps[0].sec_blob, P->steps[0].sec_scr, dr.data(), int(n), 0, &F));
-    TRY(secular_fmm(orient, orient + n, rho, int(n), 0, int(n), F, k_out, tau_out, dit, dst, P->st, &P->launches));
+    TRY(secular_fmm(orient, orient + n, rho, int(n), 0, int(n), F, k_out, tau_out, dit, dst, P->st, LC(P)));
   } else {
-    TRY(secular(orient, orient + n, rho, int(n), 0, int(n), k_out, tau_out, dit, dst, P->st, &P->launches));
+    TRY(secular(orient, orient + n, rho, int(n), 0, int(n), k_out, tau_out, dit, dst, P->st, LC(P)));
   }
   std::vector<int32_t> it(n);
   int32_t st_h = 0;
@@ -3466,7 +3593,7 @@ svd1_status svd1_loewner(svd1_plan_t P, int64_t n, const double* d, const int32_
   TRY(P->scratch_d.get<double>(size_t(spectral_scratch_elems(int(n), 0)), &scr, P->st));
   int* ctr;
   TRY(counters(P->ctr, int(n), P->st, &ctr));
-  TRY(loewner(d, k, tau, rho, z, int(n), 0, int(n), zhat_out, scr, ctr, P->st, &P->launches));
+  TRY(loewner(d, k, tau, rho, z, int(n), 0, int(n), zhat_out, scr, ctr, P->st, LC(P)));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   return SVD1_OK;
 }
@@ -3485,7 +3612,7 @@ svd1_status svd1_colnorms(svd1_plan_t P, int64_t n, const double* d, const int32
   int* ctr;
   TRY(counters(P->ctr, int(n), P->st, &ctr));
   TRY(colnorm_carry(d, k, tau, zhat, int(n), 0, int(n), nullptr, 0, cs, nullptr, n, dst, scr, ctr, P->st,
-                    &P->launches));
+                    LC(P)));
   std::vector<double> h(n);
   SVD1_CUDA_TRY(cudaMemcpyAsync(h.data(), cs, n * sizeof(double), cudaMemcpyDeviceToHost, P->st));
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
