@@ -306,7 +306,13 @@ struct StepRecord {
   cudaEvent_t done_ev = nullptr;  // recorded after the read-back copy
   double plan_ms = 0.0;           // host time of the last apply_plan (diagnostics)
   bool pending = false;           // spectral work in flight (wait on done_ev)
+  std::thread plan_thread;            // apply_plan on a worker thread (plan-owned: it may
+  std::atomic<bool> planned{false};   // outlive the update_impl call that started it)
+  void join_plan() {
+    if (plan_thread.joinable()) plan_thread.join();
+  }
   ~StepRecord() {
+    join_plan();
     if (rb) cudaFreeHost(rb);
     if (done_ev) cudaEventDestroy(done_ev);
   }
@@ -377,8 +383,14 @@ struct svd1_plan_s {
   int64_t batch_ldb = 0;
   cudaEvent_t bdone[2][2] = {};  // [parity][side]
   bool bdone_rec[2] = {false, false};
+  // batch mode: each side's remaining apply launches of the last update (its second apply
+  // waits for its FMM plan) run on a launcher thread, so the next update's spectral chain
+  // starts without waiting for them; joined before the side's next apply launch
+  std::thread launcher[2];
+  svd1_status launcher_status[2] = {SVD1_OK, SVD1_OK};
+  int launcher_parity[2] = {-1, -1};  // parity of the update whose launches they are
   cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
-  cudaEvent_t maps_ev[4] = {};   // step e's column maps uploaded (spectral stream)
+  cudaEvent_t maps_ev[2][4] = {};  // [parity] step e's column maps uploaded (spectral stream)
   cudaEvent_t bwin[2][4] = {};   // [parity]: apply start U, V; apply end U, V (timing)
   cudaEvent_t bspan[4] = {};     // the batch's first apply start U, V; last apply end U, V
   // SVD1_TIMELINE diagnostics (batch mode): labelled device events and host stamps
@@ -2480,6 +2492,8 @@ svd1_status svd1_plan_create(const svd1_config* cfg, svd1_plan_t* out) {
 
 svd1_status svd1_plan_destroy(svd1_plan_t P) {
   if (!P) return SVD1_E_INVALID;
+  for (auto& th : P->launcher)
+    if (th.joinable()) th.join();
   cudaStreamSynchronize(P->st);
   if (P->st2) cudaStreamSynchronize(P->st2);
   for (auto& q : P->sp)
@@ -2572,6 +2586,102 @@ svd1_status apply_rows(svd1_plan_t P, StepRecord& S, double* in, double* out, in
     TRY(passthrough(rows, int(S.pass_src.size()), in, ld, S.dpsrc, out, ld, S.dpdst, S.dpscale, st,
                     LC(P)));
   return SVD1_OK;
+}
+
+// expansions are sized at creation for the deepest tree; this only grows them (stream-
+// ordered on the side's apply stream, no device synchronisation) if the call's eps is
+// smaller than the plan's
+svd1_status rare_grow_fn(svd1_plan_t P, StepRecord& Se, int side) {
+  if (Se.rows > 0 && Se.na > 0 && cauchy_exp_elems(Se.cp) > P->phi[side].cap / sizeof(double))
+    TRY(ensure_expansions(P, side, cauchy_exp_elems(Se.cp)));
+  return SVD1_OK;
+}
+
+// batch mode: step e's FMM plan on the side's upload stream (never queued behind compute),
+// its operator blocks (K5) built there as soon as the plan and the step's maps (column
+// scales, with V2's sign alignment) are on the device; the apply stream waits for that work
+// and for the maps only.  (This record's ops buffer was last read by the applies of update
+// t - 2, which have completed.)
+svd1_status upload_step_batch(svd1_plan_t P, StepRecord* S, int e) {
+  const int side = e < 2 ? 0 : 1;
+  const int par = S == P->bsteps[1] ? 1 : 0;  // (the records' parity: a launcher of update t may
+                                              // run while update t + 1 records its own maps)
+  TRY(ensure_side(P, side + 4));
+  const cudaStream_t as = side_stream(P, side), us = side_stream(P, side + 4);
+  SVD1_CUDA_TRY(cudaStreamWaitEvent(as, P->maps_ev[par][e], 0));
+  TRY(upload_fmm(P, S[e], side + 4));
+  if (S[e].rows > 0 && S[e].na > 0 && S[e].cp.fmm) {
+    SVD1_CUDA_TRY(cudaStreamWaitEvent(us, P->maps_ev[par][e], 0));
+    TRY(cauchy_build_ops(P, S[e].cp, static_cast<double*>(S[e].d_in.p), static_cast<int32_t*>(S[e].d_out.p),
+                         static_cast<double*>(S[e].d_out.p) + S[e].nap, static_cast<double*>(S[e].d_zhat.p),
+                         S[e].dcs, us));
+    S[e].cp.ops_ready = true;
+  }
+  return stream_wait(P, e, us, as);
+}
+
+// One side's remaining apply launches of a batch update (everything by value: it runs on the
+// plan's launcher thread after update_impl has returned): the first apply if it was deferred
+// (its input had a Householder group), then, once the second step's plan is ready, the second
+// apply (V: pairing rotations), and the events the next updates wait on.
+struct SideJob {
+  int side = 0, parity = 0, t = 0;
+  bool first_done = false;
+  StepRecord* S = nullptr;
+  double *X = nullptr, *W = nullptr;
+  int64_t ldx = 0, ldw = 0;
+  cudaStream_t st = nullptr;
+  // thin V: the null direction before a deferred first V apply
+  bool thin = false;
+  int64_t v_rows = 0, m = 0, v_row0 = 0;
+  const double *b_dev = nullptr, *y_dev = nullptr;
+  double inv_beta = 0.0;
+  int nrot = 0;  // V: pairing rotation groups of this update
+  std::string ut;
+};
+svd1_status side_job(svd1_plan_t P, const SideJob& J) {
+  const int e1 = J.side ? 2 : 0, e2 = e1 + 1;
+  StepRecord* S = J.S;
+  if (!J.first_done) {
+    TRY(ev_record(P, J.side ? 18 : 16, J.st));
+    TRY(bwin_record(P, J.parity, J.side, J.st));
+    if (J.t == 0) TRY(bspan_record(P, J.side, J.st));
+    if (J.side && J.thin && J.v_rows)
+      TRY(null_direction(J.v_rows, J.X, J.ldx, J.m, J.b_dev, J.v_row0, J.y_dev, J.inv_beta, J.st, LC(P)));
+    TRY(apply_launch(P, S[e1], J.X, J.ldx, J.W, J.ldw, 2 * e1, J.st, J.side));
+  }
+  S[e2].join_plan();
+  TRY(rare_grow_fn(P, S[e2], J.side));
+  TRY(upload_step_batch(P, S, e2));
+  tl_mark(P, J.ut + (J.side ? "V2 apply" : "U2 apply"), J.st);
+  TRY(apply_launch(P, S[e2], J.W, J.ldw, J.X, J.ldx, 2 * e2, J.st, J.side));
+  if (J.side && J.nrot > 0)
+    TRY(col_rotate(S[3].rows, J.X, J.ldx, J.nrot, static_cast<int32_t*>(S[3].rot_goff.p),
+                   static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), J.st, LC(P)));
+  tl_mark(P, J.ut + (J.side ? "V2 end" : "U2 end"), J.st);
+  TRY(bwin_record(P, J.parity, 2 + J.side, J.st));
+  SVD1_CUDA_TRY(cudaEventRecord(P->bdone[J.parity][J.side], J.st));  // (created by update_impl)
+  return SVD1_OK;
+}
+
+svd1_status join_launcher(svd1_plan_t P, int side) {
+  if (P->launcher[side].joinable()) P->launcher[side].join();
+  P->launcher_parity[side] = -1;
+  const svd1_status s = P->launcher_status[side];
+  P->launcher_status[side] = SVD1_OK;
+  return s;
+}
+
+// a batch update's apply statistics (its plans complete)
+void fill_apply_fields(svd1_report& R, const StepRecord* S) {
+  for (int e = 0; e < 4; ++e) {
+    const bool has = S[e].rows > 0 && S[e].na > 0;
+    R.apply_flops[e] = has ? S[e].cp.flops : 0.0;
+    R.apply_flops_exec[e] = has ? S[e].cp.flops_exec : 0.0;
+    R.fmm_used[e] = has ? S[e].cp.fmm : 0;
+    R.fmm_levels[e] = (has && S[e].cp.fmm) ? S[e].cp.F.L : 0;
+    R.fmm_max_near[e] = (has && S[e].cp.fmm) ? S[e].cp.F.max_near : 0;
+  }
 }
 
 // Rows per chunk of the fused per-side pass: the chunk's U/V rows and W rows (read and
@@ -2718,6 +2828,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // eigen-update has succeeded.
   const double t1 = now_ms();
   StepRecord* S = B ? P->bsteps[B->parity] : P->steps;
+  if (B)  // launchers still holding this parity's records (update t - 2 when t - 1 was a no-op)
+    for (int sd = 0; sd < 2; ++sd)
+      if (P->launcher_parity[sd] == B->parity) TRY(join_launcher(P, sd));
   if (B && P->bdone_rec[B->parity]) {  // the applies that last used these records are done
     SVD1_CUDA_TRY(cudaEventSynchronize(P->bdone[B->parity][0]));
     SVD1_CUDA_TRY(cudaEventSynchronize(P->bdone[B->parity][1]));
@@ -2739,30 +2852,34 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     z3.swap(zv);
   }
   const double tA = now_ms();
-  std::atomic<bool> planned[4] = {false, false, false, false};  // outlives the Joiners
-  Joiner plan_u, plan_v, plan_u2, plan_v2;
   const svd1_config pcfg = P->cfg;
   const int pp = P->p;
-  // expansions are sized at creation for the deepest tree; this only grows them (stream-
-  // ordered on the side's apply stream, no device synchronisation) if the call's eps is
-  // smaller than the plan's
-  auto rare_grow = [&](int e, int side) -> svd1_status {
-    if (S[e].rows > 0 && S[e].na > 0 && cauchy_exp_elems(S[e].cp) > P->phi[side].cap / sizeof(double))
-      TRY(ensure_expansions(P, side, cauchy_exp_elems(S[e].cp)));
-    return SVD1_OK;
+  // plan threads still running if an error returns early are joined here (they touch only
+  // plan-owned step records)
+  struct PlanJoin {
+    StepRecord* S;
+    bool active = true;
+    ~PlanJoin() {
+      if (active)
+        for (int e = 0; e < 4; ++e) S[e].join_plan();
+    }
   };
+  PlanJoin plan_join_on_error{S};
+  auto rare_grow = [&](int e, int side) -> svd1_status { return rare_grow_fn(P, S[e], side); };
   // Host scheduler of the two chains: each round takes the first ready action in
   // priority order — launch a planned first apply (GPU work as early as possible), then
   // finish an eigen-update whose read-back has landed (and launch its successor / start
   // its plan on a worker thread).  Readiness is polled (cudaEventQuery, atomic flags),
   // so neither side's host step waits behind the other side's GPU work.
-  auto spawn_plan = [&](Joiner& J, int e, bool reverse, int side, int64_t rows) {
-    (void)side;
-    set_out_cols(S[e], rows, reverse);
-    J.add(std::thread([&S, &planned, pcfg, pp, e] {
-      apply_plan(pcfg, pp, S[e]);
-      planned[e].store(true, std::memory_order_release);
-    }));
+  auto spawn_plan = [&](int e, bool reverse, int64_t rows) {
+    StepRecord* Se = &S[e];
+    Se->join_plan();
+    set_out_cols(*Se, rows, reverse);
+    Se->planned.store(false, std::memory_order_relaxed);
+    Se->plan_thread = std::thread([Se, pcfg, pp] {
+      apply_plan(pcfg, pp, *Se);
+      Se->planned.store(true, std::memory_order_release);
+    });
   };
   auto landed = [&](int e) {
     if (!S[e].pending) return true;
@@ -2794,8 +2911,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     const cudaStream_t ss = side_stream(P, us);
     TRY(upload_maps(P, S[e], us));
     if (e == 3) TRY(upload_rot(us));
-    if (!P->maps_ev[e]) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->maps_ev[e], cudaEventDisableTiming));
-    SVD1_CUDA_TRY(cudaEventRecord(P->maps_ev[e], ss));
+    cudaEvent_t& mev = P->maps_ev[B->parity][e];
+    if (!mev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&mev, cudaEventDisableTiming));
+    SVD1_CUDA_TRY(cudaEventRecord(mev, ss));
     DevBuf* R = side ? P->RV : P->RU;
     const int rows = side ? B->rv_rows : B->ru_rows;
     const int64_t ld = side ? nv : m;
@@ -2830,22 +2948,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   auto upload_step = [&](int e) -> svd1_status {
     const int side = e < 2 ? 0 : 1;
     if (!B) return apply_upload(P, S[e], one_stream ? 0 : side);
-    TRY(ensure_side(P, side + 4));
-    const cudaStream_t as = side_stream(P, side), us = side_stream(P, side + 4);
-    SVD1_CUDA_TRY(cudaStreamWaitEvent(as, P->maps_ev[e], 0));
-    TRY(upload_fmm(P, S[e], side + 4));
-    // the operator blocks (K5) are built on the upload stream as soon as the plan and the
-    // step's maps (column scales, with V2's sign alignment) are on the device, so the apply
-    // stream runs the GEMM passes back to back (this record's ops buffer was last read by
-    // the applies of update t - 2, which have completed)
-    if (S[e].rows > 0 && S[e].na > 0 && S[e].cp.fmm) {
-      SVD1_CUDA_TRY(cudaStreamWaitEvent(us, P->maps_ev[e], 0));
-      TRY(cauchy_build_ops(P, S[e].cp, static_cast<double*>(S[e].d_in.p), static_cast<int32_t*>(S[e].d_out.p),
-                           static_cast<double*>(S[e].d_out.p) + S[e].nap, static_cast<double*>(S[e].d_zhat.p),
-                           S[e].dcs, us));
-      S[e].cp.ops_ready = true;
-    }
-    return stream_wait(P, e, us, as);
+    return upload_step_batch(P, S, e);
   };
   // thin V: column m of V <- q before the first V apply reads it (V side's apply stream)
   auto null_dir = [&]() -> svd1_status {
@@ -2929,8 +3032,6 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     const int sps = side ? sp1 : sp0;
     std::vector<double>& Dd = side ? Dv : Du;
     std::vector<std::vector<double>>& cc = side ? cv : cu;
-    Joiner& J1 = side ? plan_v : plan_u;
-    Joiner& J2 = side ? plan_v2 : plan_u2;
     bool& uploaded = side ? uploaded_v1 : uploaded_u1;
     const int64_t rows = side ? c.v_rows : c.u_rows;
     const double rho1 = side ? sv.rho1 : su.rho1, rho2 = side ? sv.rho2 : su.rho2;
@@ -2941,7 +3042,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     t_dbg[side ? 3 : 0] = now_ms();
     TRY(spectral_finish(P, S[e1], Dd, cc));
     fin[e1] = true;
-    spawn_plan(J1, e1, false, side, rows);
+    spawn_plan(e1, false, rows);
     if (B) TRY(rows_step(e1));
     {
       std::vector<double> z2 = cc[0];
@@ -2951,8 +3052,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     }
     t_fin[e1] = now_ms();
     while (!fin[e2]) {
-      if (!uploaded && planned[e1].load(std::memory_order_acquire)) {
-        J1.join();
+      if (!uploaded && S[e1].planned.load(std::memory_order_acquire)) {
+        S[e1].join_plan();
+        if (B) TRY(join_launcher(P, side));  // the previous update's launches on this side first
         TRY(first_apply(e1));
         uploaded = true;
         continue;
@@ -2961,7 +3063,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
         TRY(spectral_finish(P, S[e2], Dd, cc));
         fin[e2] = true;
         tl_mark(P, ut + nm + "2 finished", nullptr, false);
-        spawn_plan(J2, e2, true, side, rows);
+        spawn_plan(e2, true, rows);
         if (B && side == 0) TRY(rows_step(1));  // (V2's rows need the sign alignment)
         t_fin[e2] = now_ms();
         continue;
@@ -2969,7 +3071,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       std::this_thread::yield();
     }
     if (!uploaded) {
-      J1.join();
+      S[e1].join_plan();
+      if (B) TRY(join_launcher(P, side));
       TRY(first_apply(e1));
       uploaded = true;
     }
@@ -2980,7 +3083,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // columns): launched from the U thread as soon as the V chain has finished.
   auto u_applies = [&]() -> svd1_status {
     if (fused) {  // both steps of the side row chunk by row chunk (§4.11)
-      plan_u2.join();
+      S[1].join_plan();
       TRY(rare_grow(1, 0));
       TRY(upload_step(1));
       TRY(fused_side(0));
@@ -2991,7 +3094,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
         if (B && B->t == 0) TRY(bspan_record(P, 0, P->st));
         TRY(apply_launch(P, S[0], U, ldu, Wu, m, 0, P->st, 0));
       }
-      plan_u2.join();
+      S[1].join_plan();
       TRY(rare_grow(1, 0));
       TRY(upload_step(1));
       tl_mark(P, ut + "U2 apply", P->st);
@@ -3021,7 +3124,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       if (st_u == SVD1_OK) {
         int v;
         while ((v = v_state.load(std::memory_order_acquire)) == 0) std::this_thread::yield();
-        if (v == 1) st_ua = u_applies();
+        if (v == 1 && (!B || fused)) st_ua = u_applies();  // (batch: the U launcher, below)
       }
       flush_launches(P);
     }));
@@ -3035,6 +3138,34 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       TRY(st_u);
       return st_v;
     }
+  }
+  // batch mode: the U side's remaining apply launches (a deferred first apply, the second
+  // apply once its plan is ready) go to the U launcher thread now -- every eigen-update has
+  // succeeded -- so neither this update's return nor the next update's spectral chain waits
+  // for the U2 plan
+  const bool launchers = B && !fused && !one_stream;
+  if (launchers) {
+    u_thread.join();  // (the U chain is done; its thread only ran the chain in this mode)
+    TRY(join_launcher(P, 0));
+    SideJob ju;
+    ju.side = 0;
+    ju.parity = B->parity;
+    ju.t = B->t;
+    ju.first_done = launched_u1;
+    ju.S = S;
+    ju.X = U;
+    ju.ldx = ldu;
+    ju.W = Wu;
+    ju.ldw = m;
+    ju.st = P->st;
+    ju.ut = ut;
+    if (!P->bdone[B->parity][0])
+      SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][0], cudaEventDisableTiming));
+    P->launcher_parity[0] = B->parity;
+    P->launcher[0] = std::thread([P, ju] {
+      P->launcher_status[0] = side_job(P, ju);
+      flush_launches(P);
+    });
   }
   if (std::getenv("SVD1_TIMING"))
     fprintf(stderr, "[svd1] host: launch1 %.3f finished U1 %.3f U2 %.3f V1 %.3f V2 %.3f (plans %.3f %.3f) U1 landed %.3f finish %.3f spawn %.3f\n",
@@ -3178,9 +3309,55 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   // eigen-update succeeded: the first applies that transform their input in place can
   // start now; the second applies follow as soon as their plans are uploaded.
   const double t4 = now_ms();
+  if (launchers) {  // the V side's remaining launches likewise (they carry the sign alignment)
+    TRY(join_launcher(P, 1));
+    SideJob jv;
+    jv.side = 1;
+    jv.parity = B->parity;
+    jv.t = B->t;
+    jv.first_done = launched_v1;
+    jv.S = S;
+    jv.X = V;
+    jv.ldx = ldv;
+    jv.W = Wv;
+    jv.ldw = nv;
+    jv.st = stv;
+    jv.thin = thin;
+    jv.v_rows = c.v_rows;
+    jv.m = m;
+    jv.v_row0 = c.v_row0;
+    jv.b_dev = b_dev;
+    jv.y_dev = B->y_dev;
+    jv.inv_beta = beta_perp > 0.0 ? 1.0 / beta_perp : 0.0;
+    jv.nrot = nrot_v();
+    jv.ut = ut;
+    if (!P->bdone[B->parity][1])
+      SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][1], cudaEventDisableTiming));
+    P->launcher_parity[1] = B->parity;
+    P->launcher[1] = std::thread([P, jv] {
+      P->launcher_status[1] = side_job(P, jv);
+      flush_launches(P);
+    });
+    P->bdone_rec[B->parity] = true;
+    R.t_ms[2] = now_ms() - t4;
+    *B->sig = sig_new;
+    for (int e = 0; e < 4; ++e) {
+      R.spectral_ms[e] = S[e].spectral_ms;
+      R.mean_iter[e] = S[e].mean_iter;
+    }
+    // (apply flops / tree statistics: filled by the batch loop once this update's launchers
+    // have been joined -- the second steps' plans may still be running now)
+    R.t_ms[4] = now_ms() - t0;
+    flush_launches(P);
+    R.kernel_launches = P->launches - launches0;
+    R.allocations = g_allocs.load() - allocs0;
+    if (rep) *rep = R;
+    plan_join_on_error.active = false;  // the second steps' plans belong to the launchers now
+    return SVD1_OK;
+  }
   if (one_stream) TRY(u_applies());
   if (fused) {  // both steps of a side row chunk by row chunk (§4.11)
-    plan_v2.join();
+    S[3].join_plan();
     TRY(rare_grow(3, 1));
     TRY(upload_step(3));  // carries the sign alignment
     if (!B) TRY(upload_rot(one_stream ? 0 : 1));
@@ -3194,7 +3371,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     TRY(apply_launch(P, S[2], V, ldv, Wv, nv, 4, stv, 1));
   }
   if (!fused) {
-    plan_v2.join();
+    S[3].join_plan();
     TRY(rare_grow(3, 1));
     TRY(upload_step(3));  // carries the sign alignment
     if (!B) TRY(upload_rot(one_stream ? 0 : 1));
@@ -3377,6 +3554,8 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   P->tl_on = std::getenv("SVD1_TIMELINE") != nullptr;
   P->tl_t0 = now_ms();
   tl_mark(P, "batch start", P->st);
+  const bool launched_by_launchers = (c.flags & SVD1_FUSED_SIDE) == 0;  // (see update_impl)
+  int pending = -1;  // the update whose launchers are in flight (its report still to complete)
   for (int t = 0; t < k && st == SVD1_OK; ++t) {
     if (t > 0) {  // x's from the carried rows, dots from update t's projection
       std::memcpy(hp.data(), hn, size_t(5 * m + n) * sizeof(double));
@@ -3403,6 +3582,12 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
     svd1_report R;
     st = update_impl(P, U, ldu, sigma, V, ldv, nullptr, eps, &R, &b);
     if (reps) reps[t] = R;
+    if (launched_by_launchers && st == SVD1_OK && !R.noop) {
+      // update t joined the launchers of the previous such update before its own applies:
+      // that update's plans are complete, its apply statistics can be reported
+      if (pending >= 0 && reps) fill_apply_fields(reps[pending], P->bsteps[pending & 1]);
+      pending = t;
+    }
     if (st != SVD1_OK || t + 1 >= k) break;
     if (R.noop) {  // nothing transformed: the next rows are where they were
       SVD1_CUDA_TRY(cudaDeviceSynchronize());
@@ -3415,6 +3600,12 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
       SVD1_CUDA_TRY(cudaEventSynchronize(P->rb_ev[1]));
     }
   }
+  // the last update's launchers: its remaining apply launches are queued after this
+  for (int sd = 0; sd < 2; ++sd) {
+    const svd1_status ls = join_launcher(P, sd);
+    if (st == SVD1_OK) st = ls;
+  }
+  if (pending >= 0 && reps) fill_apply_fields(reps[pending], P->bsteps[pending & 1]);
   const bool span_ok = st == SVD1_OK;
   if (span_ok) {
     TRY(bspan_record(P, 2, P->st));
