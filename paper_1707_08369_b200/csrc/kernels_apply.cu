@@ -455,7 +455,7 @@ struct StageInfo {
 template <int BN>
 __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
     const FmmMaps* __restrict__ maps, const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int ntiles, int nrb,
-    int ntask, int rb_major,
+    int ntask, int rb_major, int* __restrict__ tile_ctr,
     int64_t rows, double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst,
     double* __restrict__ phi, double* __restrict__ psi, int64_t ldE, int64_t out_cols, int64_t exp_elems,
     const double* __restrict__ ops_raw, int64_t ops_rows) {
@@ -496,11 +496,18 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(m) : "memory");
     int stage = 0;
     uint32_t phase = 0;
-    int tile = blockIdx.x;
+    // tiles are claimed dynamically (an atomic counter per pass, in the host's longest-first
+    // order) when tile_ctr is given, else strided by the grid
+    auto claim = [&]() -> int {
+      int tl = 0;
+      if (lane == 0) tl = atomicAdd(tile_ctr, 1);
+      return __shfl_sync(0xffffffffu, tl, 0);
+    };
+    int tile = tile_ctr ? claim() : int(blockIdx.x);
     FmmTask T{};
     if (tile < ntiles) T = tasks[tile_task(tile, nrb, ntask, rb_major)];
     while (tile < ntiles) {
-      const int next = tile + gridDim.x;
+      const int next = tile_ctr ? claim() : tile + int(gridDim.x);
       FmmTask Tn{};
       if (next < ntiles) Tn = tasks[tile_task(next, nrb, ntask, rb_major)];  // in flight while this tile is issued
       const int row0 = tile_rb(tile, nrb, ntask, rb_major) * G::BM;
@@ -927,7 +934,7 @@ template <int BN>
 svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
                         const FmmMaps* maps, double* U_out, int64_t ld_out, const int32_t* dst,
                         double* phi, double* psi, int64_t ldE, int64_t out_cols, int64_t exp_elems,
-                        const double* ops_raw, int64_t ops_rows, cudaStream_t st) {
+                        const double* ops_raw, int64_t ops_rows, int* tile_ctr, cudaStream_t st) {
   using G = GemmCfg<BN>;
   static int max_ctas = 0;  // resident CTAs on the whole device (persistent grid)
   if (!max_ctas) {
@@ -952,8 +959,13 @@ svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms,
     const char* e = std::getenv("SVD1_TILE_ORDER");
     return (e && std::string(e) == "rb") ? 1 : 0;
   }();
+  // tiles strided by the grid (default) or claimed from an atomic counter per pass
+  // (SVD1_GEMM_DYNAMIC=1; measured the same in the C3 stream: 430-437 vs 434-438 updates/s;
+  // reserving SMs for the spectral kernels -- CTAs on every 8th / 16th SM exiting at once --
+  // measured 266-361)
+  static const bool dynamic = std::getenv("SVD1_GEMM_DYNAMIC") != nullptr;
   fmm_gemm_kernel<BN><<<grid, G::NTHR, G::SMEM, st>>>(maps, tasks, terms, int(ntiles), int(nrb), n_tasks, rb_major,
-                                                       rows, U_out,
+                                                       dynamic ? tile_ctr : nullptr, rows, U_out,
                                                        ld_out, dst, phi, psi, ldE, out_cols, exp_elems,
                                                        ops_raw, ops_rows);
   return SVD1_OK;
@@ -974,13 +986,13 @@ svd1_status fmm_make_maps(FmmMaps* m, int64_t rows, const double* U_in, int64_t 
 svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
                           int64_t rows, const FmmMaps* maps, double* U_out, int64_t ld_out,
                           const int32_t* dst, double* phi, double* psi, int64_t ldE, int64_t out_cols,
-                          int64_t exp_elems, const double* ops_raw, int64_t ops_rows, cudaStream_t st,
-                          int64_t* launches) {
+                          int64_t exp_elems, const double* ops_raw, int64_t ops_rows, int* tile_ctr,
+                          cudaStream_t st, int64_t* launches) {
   if (n_tasks <= 0 || rows <= 0) return SVD1_OK;
   svd1_status s = bn <= 16 ? launch_gemm<16>(n_tasks, tasks, terms, rows, maps, U_out, ld_out, dst, phi, psi,
-                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, st)
+                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, tile_ctr, st)
                            : launch_gemm<32>(n_tasks, tasks, terms, rows, maps, U_out, ld_out, dst, phi, psi,
-                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, st);
+                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, tile_ctr, st);
   if (s != SVD1_OK) return s;
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());

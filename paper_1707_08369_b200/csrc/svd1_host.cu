@@ -366,6 +366,7 @@ struct svd1_plan_s {
   DevBuf W_u, W_v, proj, partial, status, iters, ops, fmm_cells, fmm_descs, fmm_terms,
       fmm_tasks, scratch_i, scratch_d;
   DevBuf phi[2], psi[2];         // FMM expansions per side (U applies, V applies)
+  DevBuf tile_ctr[2];            // per side: the GEMM passes' tile counters of one apply
   DevBuf upad[2];                // even-ld copy of an apply input TMA cannot read in place
   DevBuf probes;                 // 4 x u_rows sign probes
   bool probes_ready = false;
@@ -1502,6 +1503,7 @@ svd1_status cauchy_build_ops(svd1_plan_t P, CauchyPrep& C, const double* d_da, c
 }
 
 constexpr int kMapSlots = 64;  // TMA descriptor sets per apply (one per row chunk, §4.11)
+constexpr int kMaxPasses = 64; // GEMM passes per apply (tile counters)
 
 // rows_n >= 0: the apply over rows_n rows starting at U_in / U_out (a row chunk of the fused
 // per-side pass), its TMA descriptors in slot `slot`; the operator blocks
@@ -1656,12 +1658,17 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
     SVD1_CUDA_TRY(cudaEventRecord(C.gev[C.ngev++], st));
     return SVD1_OK;
   };
+  // one tile counter per pass, zeroed for this launch (stream-ordered)
+  int* ctrs;
+  TRY(P->tile_ctr[side].get<int>(kMaxPasses, &ctrs, st));
+  if (F.pass_begin.size() > size_t(kMaxPasses)) return SVD1_E_INVALID;
+  SVD1_CUDA_TRY(cudaMemsetAsync(ctrs, 0, sizeof(int) * kMaxPasses, st));
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
     if (e <= b) continue;
     TRY(gmark());
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, maps, U_out, ld_out, d_dst, phi, psi, ldE,
-                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, st, LC(P)));
+                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, ctrs + s, st, LC(P)));
     TRY(gmark());
     pmark();
     if (dbg) {
@@ -2361,6 +2368,7 @@ svd1_status plan_reserve(svd1_plan_t P) {
   TRY(P->proj.reserve<double>(nproj));
   TRY(P->partial.reserve<double>(size_t(project_partial_elems(c.u_rows, m, c.v_rows, n))));
   TRY(P->probes.reserve<double>(size_t(4 * std::max<int64_t>(c.u_rows, 1))));
+  for (int sd = 0; sd < 2; ++sd) TRY(P->tile_ctr[sd].reserve<int>(kMaxPasses));
   TRY(fill_probes(P->probe_seed, c.u_row0, c.u_rows, static_cast<double*>(P->probes.p), P->st, LC(P)));
   P->probes_ready = true;
   // Phi, Psi of both sides for the deepest tree (zeroed: see ensure_expansions)

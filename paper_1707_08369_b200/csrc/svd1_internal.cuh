@@ -218,11 +218,13 @@ struct FmmMaps {
 // U_in must be 16-byte aligned with even ld (the host pads otherwise)
 svd1_status fmm_make_maps(FmmMaps* m, int64_t rows, const double* U_in, int64_t ncols_in, int64_t ld_in,
                           const double* phi, const double* psi, int64_t ldE);
+// tile_ctr (device int, zero on entry; nullptr: static striding): the pass's tiles are
+// claimed with an atomic counter in the host's longest-first order
 svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
                           int64_t rows, const FmmMaps* maps /* device */, double* U_out, int64_t ld_out,
                           const int32_t* dst, double* phi, double* psi, int64_t ldE, int64_t out_cols,
-                          int64_t exp_elems, const double* ops_raw, int64_t ops_rows, cudaStream_t st,
-                          int64_t* launches);
+                          int64_t exp_elems, const double* ops_raw, int64_t ops_rows, int* tile_ctr,
+                          cudaStream_t st, int64_t* launches);
 
 
 }  // namespace svd1
