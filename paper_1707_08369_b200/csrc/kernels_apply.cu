@@ -452,8 +452,11 @@ struct StageInfo {
   int32_t col0;   //   memory, not from global memory)
 };
 
+#ifndef SVD1_MINB32
+#define SVD1_MINB32 1  // minimum resident CTAs per SM the 32-wide kernel is compiled for (experiments)
+#endif
 template <int BN>
-__global__ void __launch_bounds__(GemmCfg<BN>::NTHR) fmm_gemm_kernel(
+__global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : 1) fmm_gemm_kernel(
     const FmmMaps* __restrict__ maps, const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int ntiles, int nrb,
     int ntask, int rb_major, int* __restrict__ tile_ctr,
     int64_t rows, double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst,

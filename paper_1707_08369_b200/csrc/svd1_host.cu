@@ -1349,6 +1349,12 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
     return double(H.flops_exec_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
   };
   static const bool parallel = std::getenv("SVD1_PLAN_PARALLEL") != nullptr;  // (experiments)
+  if (const char* e = std::getenv("SVD1_FMM_FORCE_L")) {  // (experiments) one depth: L0 + value
+    const int L = std::min(Lhi, L0 + std::max(0, atoi(e)));
+    build(L);
+    if (cand[size_t(L - L0)].state == 2) F = std::move(cand[size_t(L - L0)].F);
+    return;
+  }
   if (parallel) {
     std::vector<std::thread> th;
     for (int L = L0 + 1; L <= Lhi; ++L) th.emplace_back(build, L);
