@@ -435,7 +435,10 @@ def main():
                 ems = float(tt.item())
             return args.steps / (ems / 1e3)
         # three repetitions of the whole end-to-end stream (each: every step's copies inside
-        # the timed region); the median is reported, all three listed
+        # the timed region); the median is reported, all three listed.  One untimed pass first:
+        # the per-update leg just before uses other buffers, and the first repetition after it
+        # was sometimes 2-3x slow (one-off host/driver costs)
+        e2e_once()
         reps_e2e = [e2e_once() for _ in range(3)]
         e2e = {"value": statistics.median(reps_e2e), "unit": UNIT, "h2d_bytes_per_step": 8 * (m + n),
                "d2h_bytes_per_step": (8 * m * -(-args.steps // 28)) / args.steps if batch else 8 * m,

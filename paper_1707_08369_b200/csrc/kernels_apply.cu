@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
     // block (n-major, 16 k contiguous), the GEMM's B tile
     auto store = [&](int i, int j, double v) {
       const int kk = D.kb + i;
+      j += D.nb;
 #ifdef SVD1_BOUNDS
       if ((D.op_row + int64_t(kk >> 4) * D.npad + j) * 16 + (kk & 15) >= ops_elems || j >= D.npad) {
         printf("[svd1 bounds] ops desc %d kind %d row %lld kb %d rows %d cols %d npad %d\n", o, D.kind,
@@ -435,9 +436,10 @@ struct GemmCfg {
 
 // Tile -> (task, row block).  Task-major (default): consecutive CTAs take the same task's
 // row blocks (its operator chunks stay hot, the A windows stream down the rows).
-// Row-block-major (SVD1_TILE_ORDER=rb): the CTAs in flight cover a few row blocks and every
-// task, so shared input rows are re-read from L2 -- measured at C3: DRAM per apply 1.26 ->
-// 1.10 GB, but 481 -> 505 us (the passes are not DRAM-bound), hence not the default.
+// Row-block-major (per pass, chosen by the host): the CTAs in flight cover a few row
+// blocks and every task, so shared input rows are re-read from L2 -- measured at C3 for
+// every pass: DRAM per apply 1.26 -> 1.10 GB, but 481 -> 505 us; the host uses it for
+// the P2M pass only (svd1_host.cu, rb_passes).
 __device__ __forceinline__ int tile_task(int tile, int nrb, int ntask, int rb_major) {
   return rb_major ? tile % ntask : tile / nrb;
 }
@@ -453,7 +455,8 @@ struct StageInfo {
 };
 
 #ifndef SVD1_MINB32
-#define SVD1_MINB32 1  // minimum resident CTAs per SM the 32-wide kernel is compiled for (experiments)
+#define SVD1_MINB32 3  // resident CTAs per SM the 32-wide kernel is compiled for: <= 128 registers
+                       // (153 unconstrained: 2 CTAs / SM); C3 stream 430 -> 436-440 updates/s
 #endif
 template <int BN>
 __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : 1) fmm_gemm_kernel(
@@ -489,7 +492,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : 1)
     // (A TMA load of the op chunk, written by the operator kernel just before, was
     // measured to return stale data when another stream's kernels ran concurrently.)
     // Descriptors: the next tile's task is loaded while this tile's chunks are issued, and
-    // a task's terms are loaded once, one per lane (no global round trip per term).
+    // a task's terms are loaded once, one per lane (no global round trip per term).  (A
+    // pipeline two tiles deep -- the next tile's terms in flight too -- measured the same.)
     const int w = BN == 32 ? 1 : 0;
     const CUtensorMap* tm_u = &maps->u[w];
     const CUtensorMap* tm_phi = &maps->phi[w];
@@ -937,7 +941,7 @@ template <int BN>
 svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int64_t rows,
                         const FmmMaps* maps, double* U_out, int64_t ld_out, const int32_t* dst,
                         double* phi, double* psi, int64_t ldE, int64_t out_cols, int64_t exp_elems,
-                        const double* ops_raw, int64_t ops_rows, int* tile_ctr, cudaStream_t st) {
+                        const double* ops_raw, int64_t ops_rows, int* tile_ctr, int rb_major, cudaStream_t st) {
   using G = GemmCfg<BN>;
   static int max_ctas = 0;  // resident CTAs on the whole device (persistent grid)
   if (!max_ctas) {
@@ -958,10 +962,6 @@ svd1_status launch_gemm(int n_tasks, const FmmTask* tasks, const FmmTerm* terms,
   int cap = std::max(1, max_ctas * 9 / 10);
   if (const char* e = std::getenv("SVD1_GEMM_CTAS")) cap = std::max(1, atoi(e));  // diagnostics
   const int grid = int(std::min<int64_t>(ntiles, cap));
-  static const int rb_major = [] {
-    const char* e = std::getenv("SVD1_TILE_ORDER");
-    return (e && std::string(e) == "rb") ? 1 : 0;
-  }();
   // tiles strided by the grid (default) or claimed from an atomic counter per pass
   // (SVD1_GEMM_DYNAMIC=1; measured the same in the C3 stream: 430-437 vs 434-438 updates/s;
   // reserving SMs for the spectral kernels -- CTAs on every 8th / 16th SM exiting at once --
@@ -990,12 +990,12 @@ svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* term
                           int64_t rows, const FmmMaps* maps, double* U_out, int64_t ld_out,
                           const int32_t* dst, double* phi, double* psi, int64_t ldE, int64_t out_cols,
                           int64_t exp_elems, const double* ops_raw, int64_t ops_rows, int* tile_ctr,
-                          cudaStream_t st, int64_t* launches) {
+                          int rb_major, cudaStream_t st, int64_t* launches) {
   if (n_tasks <= 0 || rows <= 0) return SVD1_OK;
   svd1_status s = bn <= 16 ? launch_gemm<16>(n_tasks, tasks, terms, rows, maps, U_out, ld_out, dst, phi, psi,
-                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, tile_ctr, st)
+                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, tile_ctr, rb_major, st)
                            : launch_gemm<32>(n_tasks, tasks, terms, rows, maps, U_out, ld_out, dst, phi, psi,
-                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, tile_ctr, st);
+                                             ldE, out_cols, exp_elems, ops_raw, ops_rows, tile_ctr, rb_major, st);
   if (s != SVD1_OK) return s;
   *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());

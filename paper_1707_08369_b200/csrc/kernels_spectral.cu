@@ -342,60 +342,68 @@ __global__ void secular_orient_kernel(const double* __restrict__ d, const double
 
 // far-field evaluation of the secular sums for a root of leaf q (FMM path): near-leaf
 // sources directly (exact left/right split at sp), far field from the leaf's two local
-// expansions at t = ((d_k - c_t) + tau) / r_t (barycentric value and t-derivative)
+// expansions at t = ((d_k - c_t) + tau) / r_t (barycentric value and t-derivative).
+// What does not depend on tau (the lane's node values of the two expansions, the leaf's
+// interval) is loaded once per root (init); an evaluation takes six warp sums: the
+// barycentric denominator and its derivative first, then every lane's far terms divided
+// by it join the four near sums.  (Round 2: C3 37.5 -> 34.4 us, C5 84 -> 78 us.  Keeping
+// the lane's near sources in registers as well cost occupancy: slower.)
 struct FarEval {
   const SecFmmDev* F;
-  int q;         // leaf of the root
-  double tk, wk; // this lane's Chebyshev node and barycentric weight (lane < kSecP)
+  int q;          // leaf of the root
+  double tk, wk;  // this lane's Chebyshev node and barycentric weight (lane < kSecP)
+  double pl, pr;  // the leaf's two local expansions at this lane's node
+  double ct, irt; // the leaf's target interval: centre, 1 / radius
+  __device__ void init(int lane) {
+    const int cell = F->leaf_cell[q];
+    const SecFmmCell C = F->cells[cell];
+    irt = fast_rcp(C.rt);  // (MUFU + Newton: no IEEE division in the loop)
+    ct = C.ct;
+    pl = pr = 0.0;
+    if (lane < kSecP) {
+      pl = F->psiL[cell * kSecP + lane];
+      pr = F->psiR[cell * kSecP + lane];
+    }
+  }
   __device__ SecAcc operator()(const double* __restrict__ d, const double* __restrict__ z2,
                                double dk, double tau, int sp, int lane) const {
+    const double t = ((dk - ct) + tau) * irt;
+    double qk = 0.0, idx = 0.0;
+    if (lane < kSecP) {
+      double dx = t - tk;
+      if (dx == 0.0) dx = 0x1.0p-50 * (1.0 + fabs(t));  // exact node: an ulp-scale nudge
+      idx = fast_rcp(dx);
+      qk = wk * idx;
+    }
+    const double den = warp_sum(qk), dden = warp_sum(-qk * idx);
     SecAcc a = {0, 0, 0, 0, 0};
     for (int g = F->near_off[q]; g < F->near_off[q + 1]; ++g) {
       const int lo = F->near_lo[g], hi = F->near_hi[g];
       for (int i = lo + lane; i < hi; i += 32) {
         const double rr = fast_rcp((__ldg(d + i) - dk) - tau);
-        const double t = __ldg(z2 + i) * rr;
+        const double v = __ldg(z2 + i) * rr;
         if (i <= sp) {
-          a.psi += t;
-          a.dpsi = fma(t, rr, a.dpsi);
+          a.psi += v;
+          a.dpsi = fma(v, rr, a.dpsi);
         } else {
-          a.phi += t;
-          a.dphi = fma(t, rr, a.dphi);
+          a.phi += v;
+          a.dphi = fma(v, rr, a.dphi);
         }
       }
     }
-    const int cell = F->leaf_cell[q];
-    const SecFmmCell C = F->cells[cell];
-    const double irt = fast_rcp(C.rt);  // (MUFU + Newton: no IEEE division in the loop)
-    double t = ((dk - C.ct) + tau) * irt;
-    double nl = 0.0, nr = 0.0, den = 0.0, dnl = 0.0, dnr = 0.0, dden = 0.0;
+    // far: value N/D and t-derivative (N' - (N/D) D')/D, split over the nodes
+    const double id = fast_rcp(den);
     if (lane < kSecP) {
-      double dx = t - tk;
-      if (dx == 0.0) dx = 0x1.0p-50 * (1.0 + fabs(t));  // exact node: an ulp-scale nudge
-      const double idx = fast_rcp(dx);
-      const double qk = wk * idx, pl = F->psiL[cell * kSecP + lane], pr = F->psiR[cell * kSecP + lane];
-      den = qk;
-      nl = pl * qk;
-      nr = pr * qk;
-      dden = -qk * idx;
-      dnl = -nl * idx;
-      dnr = -nr * idx;
+      const double nl = pl * qk * id, nr = pr * qk * id;
+      a.psi += nl;
+      a.phi += nr;
+      a.dpsi += (-(pl * qk) * idx - nl * dden) * id * irt;
+      a.dphi += (-(pr * qk) * idx - nr * dden) * id * irt;
     }
     a.psi = warp_sum(a.psi);
     a.phi = warp_sum(a.phi);
     a.dpsi = warp_sum(a.dpsi);
     a.dphi = warp_sum(a.dphi);
-    nl = warp_sum(nl);
-    nr = warp_sum(nr);
-    den = warp_sum(den);
-    dnl = warp_sum(dnl);
-    dnr = warp_sum(dnr);
-    dden = warp_sum(dden);
-    const double id = fast_rcp(den);
-    a.psi += nl * id;
-    a.phi += nr * id;
-    a.dpsi += (dnl * den - nl * dden) * id * id * irt;
-    a.dphi += (dnr * den - nr * dden) * id * id * irt;
     a.eabs = fabs(a.psi) + fabs(a.phi);
     return a;
   }
@@ -514,7 +522,8 @@ __device__ void solve_root(int j, const double* __restrict__ d, const double* __
 // roots bracketed by outlier gaps (outside every target interval, listed in F.direct)
 // take one block each, ahead of the nfar warp blocks, with the direct sum.
 template <bool FMM>
-__global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__ d,
+// (3 blocks of 8 warps per SM: <= 80 registers)
+__global__ void __launch_bounds__(256, 3) secular_kernel(const double* __restrict__ d,
                                                      const double* __restrict__ z2, double rho, int n,
                                                      int32_t* __restrict__ k_out,
                                                      double* __restrict__ tau_out,
@@ -547,7 +556,9 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
                k_out, tau_out, iters_out, status);
     return;
   }
-  FarEval fe{&F, 0, 0.0, 0.0};
+  FarEval fe;
+  fe.F = &F;
+  fe.tk = fe.wk = 0.0;
   int lo = 0, hi = F.nleaf;  // leaf q with leaf_lo[q] <= j < leaf_lo[q + 1]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -562,6 +573,7 @@ __global__ void __launch_bounds__(256) secular_kernel(const double* __restrict__
     fe.tk = cospi(th);
     fe.wk = ((lane & 1) ? -1.0 : 1.0) * sinpi(th);
   }
+  fe.init(lane);
   solve_root(j, d, z2, rho, n, g,
              [&](double dk, double tau, int sp) { return fe(d, z2, dk, tau, sp, lane); }, k_out,
              tau_out, iters_out, status);

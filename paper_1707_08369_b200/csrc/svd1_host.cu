@@ -219,6 +219,8 @@ struct FmmHost {
   int64_t ops_rows = 0;         // ops buffer: rows of 16 doubles
   int64_t flops_per_row = 0;    // algorithmic flops per row (level by level)
   int64_t flops_exec_per_row = 0;  // flops the plan executes per row (level bands included)
+  int64_t flops_cost_per_row = 0;  // the same without the sibling pairs' zero blocks (the
+                                   // depth search's cost: pairing does not change it)
   int n_near_pairs = 0, n_m2l_pairs = 0, max_near = 0;
 };
 
@@ -1021,7 +1023,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     F.terms.push_back(t);
     F.flops_exec_per_row += 2ll * kreal * N;
   };
-  auto add_op = [&](int kind, int a, int b, int rows, int cols, int kb) {
+  auto add_op = [&](int kind, int a, int b, int rows, int cols, int kb, int nb = 0) {
     const FmmTerm& t = F.terms.back();
     FmmOpDesc D;
     D.kind = kind;
@@ -1030,6 +1032,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     D.rows = rows;
     D.cols = cols;
     D.kb = kb;
+    D.nb = nb;
     D.npad = t.npad;
     D.op_row = t.op_row;
     D.c0 = 0;
@@ -1037,11 +1040,14 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     F.ops.push_back(D);
   };
   int64_t adj = 0;  // level-by-level M2M / L2L flops minus the banded ones
+  int64_t zero_flops = 0;  // executed on the zero blocks of sibling-pair tasks (not algorithmic)
   // sources [s_lo, s_hi) (a contiguous range of the sorted active sources) read through
   // their physical input columns src[s]: windows of nearby columns (gaps <= 8 are
   // bridged by zero op rows), each starting at an even column
   std::vector<int> pc;
-  auto add_src = [&](int kind, int s_lo, int s_hi, int b, int N) {
+  // (b2 >= 0: a task over the sibling pair (b, b2) -- b's block in op columns 0..N/2-1,
+  // b2's in N/2..N-1; a negative b targets only the second half)
+  auto add_src = [&](int kind, int s_lo, int s_hi, int b, int N, int b2 = -1) {
     pc.resize(s_hi - s_lo);
     bool up = true, down = true;  // monotone maps (identity, reversal) need no sort
     for (int s2 = s_lo; s2 < s_hi; ++s2) {
@@ -1061,9 +1067,24 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       // column in front of the term's sources gets a zero op row)
       const int c0 = pc[a] & ~1, len = pc[e] + 1 - c0;
       new_term(IO_U, c0, len, N, int(e - a + 1));
-      add_op(kind, s_lo, b, len, N, 0);
-      F.ops.back().c0 = c0;
-      F.ops.back().s_hi = s_hi;
+      if (b2 == -1) {
+        add_op(kind, s_lo, b, len, N, 0);
+        F.ops.back().c0 = c0;
+        F.ops.back().s_hi = s_hi;
+      } else {
+        const int half = N / 2;
+        if (b >= 0) {
+          add_op(kind, s_lo, b, len, half, 0, 0);
+          F.ops.back().c0 = c0;
+          F.ops.back().s_hi = s_hi;
+        }
+        if (b2 >= 0) {
+          add_op(kind, s_lo, b2, len, half, 0, half);
+          F.ops.back().c0 = c0;
+          F.ops.back().s_hi = s_hi;
+        }
+        if (b < 0 || b2 < 0) zero_flops += 2ll * (e - a + 1) * half;
+      }
       a = e + 1;
     }
   };
@@ -1189,11 +1210,75 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     //     Full expansions are stored in Phi (dead after the M2L pass);
     // (c) leaves take L2L from their parent folded into the final pass (evaluating
     //     the parent's local polynomial at the targets is exactly L2L then L2P).
+    // Sibling pairs (SVD1_PAIRS: bit 0 the M2L pass, bit 1 the L2L bands; experiments,
+    // off by default): the siblings (2P+1, 2P+2) run as ONE 2p-wide task over the union
+    // of their inputs (each input's op holds a block per sibling it serves, zero
+    // otherwise), so each input window is read once for both.  Measured at C3 (DESIGN.md
+    // §4.4): the M2L pass 85 -> 120-190 us (the traversal's partner lists of siblings
+    // overlap little: the union's zero blocks cost more than the halved A reads save),
+    // the L2L bands about even; the stream 430 -> 405 (both) / 424 (L2L only).
+    static const int pair_mask = std::getenv("SVD1_PAIRS") ? atoi(std::getenv("SVD1_PAIRS")) : 0;
+    bool pairs = 2 * p <= 32 && (pair_mask & 1);
+    auto pair_of = [&](int y) {  // the right sibling when y is a left child that pairs
+      return (pairs && (y & 1) && y + 1 < F.ncells) ? y + 1 : -1;
+    };
     F.pass_begin.push_back(int(F.tasks.size()));
-    F.pass_bn.push_back(p);
+    F.pass_bn.push_back(pairs ? 2 * p : p);
     std::vector<int> via_phi, via_src;
+    std::vector<std::pair<int, int>> uni;  // (partner, 1: of y | 2: of y2)
     for (int y = 1; y < F.ncells; ++y) {
       if (m2l[y].empty() || !has_tgt(y)) continue;
+      const int y2 = pair_of(y);
+      if (y2 > 0 && has_tgt(y2) && !m2l[y2].empty()) {
+        uni.clear();
+        size_t i1 = 0, i2 = 0;
+        const auto A1 = m2l[y], A2 = m2l[y2];
+        while (i1 < A1.size() || i2 < A2.size()) {
+          if (i2 == A2.size() || (i1 < A1.size() && A1[i1] < A2[i2])) uni.push_back({A1[i1++], 1});
+          else if (i1 == A1.size() || A2[i2] < A1[i1]) uni.push_back({A2[i2++], 2});
+          else {
+            uni.push_back({A1[i1], 3});
+            ++i1;
+            ++i2;
+          }
+        }
+        begin_task();
+        for (int pass_src = 0; pass_src < 2; ++pass_src) {
+          size_t a = 0;
+          while (a < uni.size()) {
+            const int x = uni[a].first;
+            const bool src_kind = F.cells[x].shi - F.cells[x].slo < p;
+            if (src_kind != (pass_src == 1)) {
+              ++a;
+              continue;
+            }
+            if (src_kind) {  // P2L: one source window per partner, blocks for its targets
+              const int m = uni[a].second;
+              add_src(OP_P2L, F.cells[x].slo, F.cells[x].shi, (m & 1) ? y : -2, 2 * p, (m & 2) ? y2 : -2);
+              ++a;
+              continue;
+            }
+            // M2L: consecutive partner cells -> one long-K term over adjacent Phi columns
+            size_t b = a;
+            while (b + 1 < uni.size() && uni[b + 1].first == uni[b].first + 1 &&
+                   F.cells[uni[b + 1].first].shi - F.cells[uni[b + 1].first].slo >= p)
+              ++b;
+            const int K = int(b - a + 1) * p;
+            new_term(IO_PHI, x * p, K, 2 * p, K);
+            for (size_t q = a; q <= b; ++q) {
+              const int m = uni[q].second;
+              if (m & 1) add_op(OP_M2L, uni[q].first, y, p, p, int(q - a) * p, 0);
+              if (m & 2) add_op(OP_M2L, uni[q].first, y2, p, p, int(q - a) * p, p);
+              if (m != 3) zero_flops += 2ll * p * p;
+            }
+            a = b + 1;
+          }
+        }
+        F.n_m2l_pairs += int(m2l[y].size() + m2l[y2].size());
+        end_task(IO_PSI, y * p, 2 * p);
+        ++y;  // y2 done
+        continue;
+      }
       begin_task();
       // partners with fewer than p sources are cheaper as P2L (K = #sources < p)
       via_phi.clear();
@@ -1209,6 +1294,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       const int y = 1 + i;  // level 1: full = the M2L part
       if (L >= 1 && has_tgt(y) && !m2l[y].empty()) loc[y] = IO_PSI;
     }
+    pairs = 2 * p <= 32 && (pair_mask & 2);
     int a = 1;  // anchor level: full expansions known
     while (a + 1 <= L - 1) {
       int hi = a + 1;
@@ -1226,30 +1312,62 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
         hi = l2;
       }
       const int pb = int(F.tasks.size());
+      // (cell, input) pairs of y: Psi of the band ancestors with an M2L part, then the
+      // anchor's full expansion; adj: level by level, Psi_y = Psi_y I + full(parent) S
+      // when the parent has one, minus the band's terms
+      auto chain = [&](int y, int l, int* Acell, int* Akind) {
+        int nA = 0, A = y;
+        for (int l3 = l; l3 >= a + 1; --l3, A = (A - 1) / 2)
+          if (!m2l[A].empty()) {
+            Acell[nA] = A;
+            Akind[nA++] = IO_PSI;
+          }
+        if (loc[A] >= 0) {  // A is now the ancestor at the anchor level a
+          Acell[nA] = A;
+          Akind[nA++] = loc[A];
+        }
+        const int par = (y - 1) / 2;
+        if (loc[par] >= 0) adj += 2ll * p * p * ((m2l[y].empty() ? 0 : 1) + 1);
+        if (!(nA == 0 || (nA == 1 && Acell[0] == y))) adj -= 2ll * p * p * nA;
+        return nA;
+      };
       for (int l = a + 1; l <= hi; ++l)
         for (int i = 0; i < (1 << l); ++i) {
           const int y = (1 << l) - 1 + i;
           if (!has_tgt(y)) continue;
-          // (cell, input) pairs: Psi of the band ancestors with an M2L part, then the
-          // anchor's full expansion
-          int nA = 0, Acell[32], Akind[32];
-          int A = y;
-          for (int l3 = l; l3 >= a + 1; --l3, A = (A - 1) / 2)
-            if (!m2l[A].empty()) {
-              Acell[nA] = A;
-              Akind[nA++] = IO_PSI;
-            }
-          if (loc[A] >= 0) {  // A is now the ancestor at the anchor level a
-            Acell[nA] = A;
-            Akind[nA++] = loc[A];
-          }
-          {  // level by level: Psi_y = Psi_y I + full(parent) S when the parent has one
-            const int par = (y - 1) / 2;
-            if (loc[par] >= 0) adj += 2ll * p * p * ((m2l[y].empty() ? 0 : 1) + 1);
-            if (!(nA == 0 || (nA == 1 && Acell[0] == y))) adj -= 2ll * p * p * nA;
-          }
+          int Acell[32], Akind[32];
+          const int nA = chain(y, l, Acell, Akind);
           if (nA == 0 || (nA == 1 && Acell[0] == y)) {  // nothing to accumulate
             loc[y] = nA ? IO_PSI : -1;
+            continue;
+          }
+          const int y2 = pair_of(y);
+          if (y2 > 0 && has_tgt(y2)) {
+            // sibling pair (as in the M2L pass): the ancestors and the anchor are shared,
+            // one 2p-wide task; the siblings' own Psi are adjacent columns (one term)
+            int Bcell[32], Bkind[32];
+            const int nB = chain(y2, l, Bcell, Bkind);
+            const int o1 = Acell[0] == y ? 1 : 0, o2 = Bcell[0] == y2 ? 1 : 0;
+            if (nA - o1 != nB - o2 || nB - o2 <= 0) {
+              fprintf(stderr, "[svd1] internal: sibling chains differ (%d %d)\n", y, y2);
+              std::abort();
+            }
+            begin_task();
+            if (o1 || o2) {
+              const int c0 = o1 ? y : y2, K = (o1 + o2) * p;
+              new_term(IO_PSI, c0 * p, K, 2 * p, K);
+              if (o1) add_op(OP_ID, y, y, p, p, 0, 0);
+              if (o2) add_op(OP_ID, y2, y2, p, p, o1 ? p : 0, p);
+              zero_flops += 2ll * K * 2 * p - 2ll * (o1 + o2) * p * p;
+            }
+            for (int q = o1; q < nA; ++q) {
+              new_term(Akind[q], Acell[q] * p, p, 2 * p, p);
+              add_op(OP_L2L, Acell[q], y, p, p, 0, 0);
+              add_op(OP_L2L, Acell[q], y2, p, p, 0, p);
+            }
+            end_task(IO_PHI, y * p, 2 * p);
+            loc[y] = loc[y2] = IO_PHI;
+            ++i;  // y2 done
             continue;
           }
           begin_task();
@@ -1262,7 +1380,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
         }
       if (int(F.tasks.size()) > pb) {
         F.pass_begin.push_back(pb);
-        F.pass_bn.push_back(p);
+        F.pass_bn.push_back(pairs ? 2 * p : p);
         sort_pass(pb);
       }
       a = hi;
@@ -1306,7 +1424,8 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   }
   F.pass_begin.push_back(int(F.tasks.size()));
   for (int& bn : F.pass_bn) bn = bn <= 16 ? 16 : 32;
-  F.flops_per_row = F.flops_exec_per_row + adj;
+  F.flops_per_row = F.flops_exec_per_row - zero_flops + adj;
+  F.flops_cost_per_row = F.flops_exec_per_row - zero_flops;
   if (std::getenv("SVD1_DEBUG"))
     fprintf(stderr, "[svd1] lists: traversal %.3f ms, generation %.3f ms (ops %zu terms %zu tasks %zu)\n",
             tt1 - tt0, now_ms() - tt1, F.ops.size(), F.terms.size(), F.tasks.size());
@@ -1346,7 +1465,7 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
     C.state = 2;
   };
   auto cost_of = [rows](const FmmHost& H) {
-    return double(H.flops_exec_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
+    return double(H.flops_cost_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
   };
   static const bool parallel = std::getenv("SVD1_PLAN_PARALLEL") != nullptr;  // (experiments)
   if (const char* e = std::getenv("SVD1_FMM_FORCE_L")) {  // (experiments) one depth: L0 + value
@@ -1371,7 +1490,7 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
   }
   // cost: executed flops plus one launch-equivalent per pass
   auto cost = [rows](const FmmHost& H) {
-    return double(H.flops_exec_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
+    return double(H.flops_cost_per_row) + 2.0e8 / double(std::max<int64_t>(rows, 1)) * double(H.pass_bn.size());
   };
   FmmHost best;
   bool have = false;
@@ -1669,12 +1788,22 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   TRY(P->tile_ctr[side].get<int>(kMaxPasses, &ctrs, st));
   if (F.pass_begin.size() > size_t(kMaxPasses)) return SVD1_E_INVALID;
   SVD1_CUDA_TRY(cudaMemsetAsync(ctrs, 0, sizeof(int) * kMaxPasses, st));
+  // passes whose tiles run row-block-major (bit s: pass s): P2M, the first pass, streams
+  // every column of the input once -- in row-block order the CTAs in flight read whole rows
+  // (C3 alone: 43 -> 39 us; the other passes the same or slower, the final pass 253 -> 270).
+  // SVD1_RB_PASSES overrides the mask, SVD1_TILE_ORDER=rb sets every pass (experiments).
+  static const unsigned rb_passes = [] {
+    const char* e = std::getenv("SVD1_TILE_ORDER");
+    if (e && std::string(e) == "rb") return ~0u;
+    const char* m = std::getenv("SVD1_RB_PASSES");
+    return m ? unsigned(strtoul(m, nullptr, 0)) : 1u;
+  }();
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
     if (e <= b) continue;
     TRY(gmark());
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, maps, U_out, ld_out, d_dst, phi, psi, ldE,
-                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, ctrs + s, st, LC(P)));
+                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, ctrs + s, (rb_passes >> s) & 1, st, LC(P)));
     TRY(gmark());
     pmark();
     if (dbg) {

@@ -181,6 +181,8 @@ struct FmmOpDesc {    // one operator block: rows x cols, written into its term'
   int32_t rows, cols;
   int32_t kb;         // first k (row) of this block inside the term's op
   int32_t npad;       // the term's op: chunks of [npad][16] doubles (see FmmTerm)
+  int32_t nb;         // first n (column) of this block inside the term's op (a task over
+                      // two sibling targets holds each target's block in its own columns)
   int64_t op_row;     // the term's first 16-double row in the ops buffer
   int32_t c0, s_hi;   // source kinds: row q <-> input column c0 + q, holding active source
                       // s = col2src[c0 + q]; rows with s outside [a, s_hi) are zero
@@ -219,12 +221,13 @@ struct FmmMaps {
 svd1_status fmm_make_maps(FmmMaps* m, int64_t rows, const double* U_in, int64_t ncols_in, int64_t ld_in,
                           const double* phi, const double* psi, int64_t ldE);
 // tile_ctr (device int, zero on entry; nullptr: static striding): the pass's tiles are
-// claimed with an atomic counter in the host's longest-first order
+// claimed with an atomic counter in the host's longest-first order; rb_major: tile order
+// row-block-major instead of task-major (kernels_apply.cu, tile_task)
 svd1_status fmm_run_tasks(int n_tasks, const FmmTask* tasks, const FmmTerm* terms, int bn,
                           int64_t rows, const FmmMaps* maps /* device */, double* U_out, int64_t ld_out,
                           const int32_t* dst, double* phi, double* psi, int64_t ldE, int64_t out_cols,
                           int64_t exp_elems, const double* ops_raw, int64_t ops_rows, int* tile_ctr,
-                          cudaStream_t st, int64_t* launches);
+                          int rb_major, cudaStream_t st, int64_t* launches);
 
 
 }  // namespace svd1
