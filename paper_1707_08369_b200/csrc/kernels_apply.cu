@@ -458,8 +458,11 @@ struct StageInfo {
 #define SVD1_MINB32 3  // resident CTAs per SM the 32-wide kernel is compiled for: <= 128 registers
                        // (153 unconstrained: 2 CTAs / SM); C3 stream 430 -> 436-440 updates/s
 #endif
+#ifndef SVD1_MINB16
+#define SVD1_MINB16 1  // the same for the 16-wide kernel (101 registers: 3 CTAs / SM; experiments)
+#endif
 template <int BN>
-__global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : 1) fmm_gemm_kernel(
+__global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SVD1_MINB16) fmm_gemm_kernel(
     const FmmMaps* __restrict__ maps, const FmmTask* __restrict__ tasks, const FmmTerm* __restrict__ terms, int ntiles, int nrb,
     int ntask, int rb_major, int* __restrict__ tile_ctr,
     int64_t rows, double* __restrict__ U_out, int64_t ld_out, const int32_t* __restrict__ dst,

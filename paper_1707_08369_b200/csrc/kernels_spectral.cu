@@ -522,8 +522,12 @@ __device__ void solve_root(int j, const double* __restrict__ d, const double* __
 // roots bracketed by outlier gaps (outside every target interval, listed in F.direct)
 // take one block each, ahead of the nfar warp blocks, with the direct sum.
 template <bool FMM>
-// (3 blocks of 8 warps per SM: <= 80 registers)
-__global__ void __launch_bounds__(256, 3) secular_kernel(const double* __restrict__ d,
+// 4 blocks of 8 warps per SM (<= 64 registers, a few bytes spilled): a C3 solve's 4096
+// warps fit in one wave (3 blocks: 80 registers, two waves; 34.7 -> 29.5 us)
+#ifndef SVD1_SEC_MINB
+#define SVD1_SEC_MINB 4
+#endif
+__global__ void __launch_bounds__(256, SVD1_SEC_MINB) secular_kernel(const double* __restrict__ d,
                                                      const double* __restrict__ z2, double rho, int n,
                                                      int32_t* __restrict__ k_out,
                                                      double* __restrict__ tau_out,
@@ -770,6 +774,25 @@ __device__ __forceinline__ bool last_block_of_column(int* ctr) {
   return last;
 }
 
+// frexp by the exponent bits (the same mantissa in [0.5, 1) and exponent as frexp for a
+// positive normal x; a zero, denormal, inf or NaN sets `bad`, and the caller redoes the
+// index with frexp): a quarter of frexp's instructions, which dominated the kernel
+__device__ __forceinline__ double frexp_bits(double x, int& e, bool& bad) {
+  const int hi = __double2hiint(x), ex = (hi >> 20) & 0x7ff;
+  bad |= (ex == 0) | (ex == 0x7ff);
+  e = ex - 1022;
+  return __hiloint2double((hi & 0x800fffff) | (1022 << 20), __double2loint(x));
+}
+__device__ __forceinline__ void renorm4_bits(double& Pn, double& Pd, double& Qn, double& Qd, int& E,
+                                             bool& bad) {
+  int e1, e2, e3, e4;
+  Pn = frexp_bits(Pn, e1, bad);
+  Pd = frexp_bits(Pd, e2, bad);
+  Qn = frexp_bits(Qn, e3, bad);
+  Qd = frexp_bits(Qd, e4, bad);
+  E += (e1 - e2) + (e3 - e4);
+}
+
 __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
     const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau, int n,
     int chunk, double* __restrict__ pm, int32_t* __restrict__ pe, int* __restrict__ ctr, double rho,
@@ -781,6 +804,7 @@ __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
   const double di = i < i_hi ? d[i] : 0.0;
   double Pn = 1.0, Pd = 1.0;
   int E = 0;
+  bool bad = false;  // a product left the normal range between two renormalisations
   for (int jb = j0; jb < j1; jb += kLJ) {
     const int nj = min(kLJ, j1 - jb);
     __syncthreads();
@@ -801,12 +825,7 @@ __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
       Qn *= fabs((s_mu[t + 1] - di) + s_t[t + 1]);
       Qd *= (j + 1 == i) ? 1.0 : fabs(s_d[t + 1] - di);
       if (++cnt == 8) {
-        int e1, e2, e3, e4;
-        Pn = frexp(Pn, &e1);
-        Pd = frexp(Pd, &e2);
-        Qn = frexp(Qn, &e3);
-        Qd = frexp(Qd, &e4);
-        E += (e1 - e2) + (e3 - e4);
+        renorm4_bits(Pn, Pd, Qn, Qd, E, bad);
         cnt = 0;
       }
     }
@@ -814,14 +833,21 @@ __global__ void __launch_bounds__(kLT) loewner_partial_kernel(
       Pn *= fabs((s_mu[t] - di) + s_t[t]);
       Pd *= (jb + t == i) ? 1.0 : fabs(s_d[t] - di);
     }
-    int e1, e2, e3, e4;
-    Pn = frexp(Pn, &e1);
-    Pd = frexp(Pd, &e2);
-    Qn = frexp(Qn, &e3);
-    Qd = frexp(Qd, &e4);
-    E += (e1 - e2) + (e3 - e4);
+    renorm4_bits(Pn, Pd, Qn, Qd, E, bad);
     Pn *= Qn;
     Pd *= Qd;
+  }
+  if (bad && i < i_hi) {
+    // a product left the normal range between two renormalisations (extreme spectra):
+    // this chunk again from global memory, renormalised after every factor
+    Pn = Pd = 1.0;
+    E = 0;
+    for (int j = j0; j < j1; ++j) {
+      int e1, e2;
+      Pn = frexp(Pn * fabs((d[k[j]] - di) + tau[j]), &e1);
+      Pd = frexp(Pd * (j == i ? 1.0 : fabs(d[j] - di)), &e2);
+      E += e1 - e2;
+    }
   }
   if (i < i_hi) {
     int e;
@@ -929,27 +955,78 @@ __device__ __forceinline__ void mant_exp_mul(double& m, int& e, double m2, int e
   e += e2 + ee;
 }
 
+// j tiles of 1024 (24 KB of shared memory), the next tile's values prefetched into
+// registers while the current one is multiplied (its k two tiles ahead: d[k[j]] is a
+// dependent load), so the global-memory latency is not exposed once per tile
+constexpr int kLWT = 1024;
+constexpr int kLWQ = kLWT / (32 * kWW);  // tile elements per thread
+
 __global__ void __launch_bounds__(32 * kWW) loewner_warp_kernel(
     const double* __restrict__ d, const int32_t* __restrict__ k, const double* __restrict__ tau, int n,
     double rho, const double* __restrict__ z, double* __restrict__ zhat, int i_lo, int i_hi) {
-  __shared__ double s_d[kWT], s_mu[kWT], s_t[kWT];
+  __shared__ double s_d[kLWT], s_mu[kLWT], s_t[kLWT];
   const int lane = threadIdx.x & 31;
   const int i = i_lo + blockIdx.x * kWW + (threadIdx.x >> 5);
   const bool ok = i < i_hi;
   const double di = ok ? d[i] : 0.0;
-  // two product chains per lane (even / odd tile strides), numerator and denominator
-  // apart (no division per term), renormalised with frexp every 8 factors
+  // two product chains per lane (even / odd 32-strides), numerator and denominator apart
+  // (no division per term), renormalised with frexp (exact) every 4 factors per chain
   double Pn = 1.0, Pd = 1.0, Qn = 1.0, Qd = 1.0;
   int E = 0, cnt = 0;
-  for (int jb = 0; jb < n; jb += kWT) {
-    const int nj = min(kWT, n - jb);
+  bool bad = false;  // a product left the normal range between two exponent-bit renorms
+  double rd[kLWQ], rm[kLWQ], rt[kLWQ];
+  int rk[kLWQ];
+  auto fetch_k = [&](int jb) {
+#pragma unroll
+    for (int q = 0; q < kLWQ; ++q) {
+      const int j = jb + int(threadIdx.x) + 32 * kWW * q;
+      rk[q] = j < n ? __ldg(k + j) : 0;
+    }
+  };
+  auto fetch = [&](int jb) {  // (rk holds tile jb's k)
+#pragma unroll
+    for (int q = 0; q < kLWQ; ++q) {
+      const int j = jb + int(threadIdx.x) + 32 * kWW * q;
+      if (j < n) {
+        rd[q] = __ldg(d + j);
+        rm[q] = __ldg(d + rk[q]);
+        rt[q] = __ldg(tau + j);
+      }
+    }
+  };
+  fetch_k(0);
+  fetch(0);
+  fetch_k(kLWT);
+  for (int jb = 0; jb < n; jb += kLWT) {
+    const int nj = min(kLWT, n - jb);
     __syncthreads();
-    for (int t = threadIdx.x; t < nj; t += 32 * kWW) {
-      s_d[t] = d[jb + t];
-      s_mu[t] = d[k[jb + t]];
-      s_t[t] = tau[jb + t];
+#pragma unroll
+    for (int q = 0; q < kLWQ; ++q) {
+      const int t = int(threadIdx.x) + 32 * kWW * q;
+      if (t < nj) {
+        s_d[t] = rd[q];
+        s_mu[t] = rm[q];
+        s_t[t] = rt[q];
+      }
     }
     __syncthreads();
+    if (jb + kLWT < n) {  // next tile in flight during this one
+      fetch(jb + kLWT);
+      fetch_k(jb + 2 * kLWT);
+    }
+    if (nj == kLWT && (i < jb || i >= jb + kLWT)) {
+      // a full tile without the diagonal (warp-uniform): unrolled, no j == i select
+#pragma unroll
+      for (int u = 0; u < kLWT / 64; ++u) {
+        const int t = lane + 64 * u;
+        Pn *= fabs((s_mu[t] - di) + s_t[t]);
+        Pd *= fabs(s_d[t] - di);
+        Qn *= fabs((s_mu[t + 32] - di) + s_t[t + 32]);
+        Qd *= fabs(s_d[t + 32] - di);
+        if ((u & 3) == 3) renorm4_bits(Pn, Pd, Qn, Qd, E, bad);
+      }
+      continue;
+    }
     for (int t = lane; t < nj; t += 64) {
       Pn *= fabs((s_mu[t] - di) + s_t[t]);
       Pd *= (jb + t == i) ? 1.0 : fabs(s_d[t] - di);
@@ -957,23 +1034,30 @@ __global__ void __launch_bounds__(32 * kWW) loewner_warp_kernel(
         Qn *= fabs((s_mu[t + 32] - di) + s_t[t + 32]);
         Qd *= (jb + t + 32 == i) ? 1.0 : fabs(s_d[t + 32] - di);
       }
-      if (++cnt == 8) {
-        int e1, e2, e3, e4;
-        Pn = frexp(Pn, &e1);
-        Pd = frexp(Pd, &e2);
-        Qn = frexp(Qn, &e3);
-        Qd = frexp(Qd, &e4);
-        E += (e1 - e2) + (e3 - e4);
+      if (++cnt == 4) {
+        renorm4_bits(Pn, Pd, Qn, Qd, E, bad);
         cnt = 0;
       }
     }
   }
-  int e1, e2, e3, e4;
-  Pn = frexp(Pn, &e1);
-  Pd = frexp(Pd, &e2);
-  Qn = frexp(Qn, &e3);
-  Qd = frexp(Qd, &e4);
-  E += (e1 - e2) + (e3 - e4);
+  renorm4_bits(Pn, Pd, Qn, Qd, E, bad);
+  if (__any_sync(0xffffffffu, bad)) {
+    // out of range between renorms (extreme spectra): this index again, from global
+    // memory, renormalised after every factor (the same products, the same order)
+    Pn = Pd = Qn = Qd = 1.0;
+    E = 0;
+    for (int jb = 0; jb < n; jb += 64)
+      for (int h = 0; h < 2; ++h) {
+        const int j = jb + lane + 32 * h;
+        if (j >= n) continue;
+        double& N = h ? Qn : Pn;
+        double& D = h ? Qd : Pd;
+        int e1, e2;
+        N = frexp(N * fabs((d[k[j]] - di) + tau[j]), &e1);
+        D = frexp(D * (j == i ? 1.0 : fabs(d[j] - di)), &e2);
+        E += e1 - e2;
+      }
+  }
   int e;
   double m = frexp((Pn * Qn) / (Pd * Qd), &e);
   E += e;
@@ -1367,8 +1451,12 @@ static int chunk_blocks() {  // target blocks (x 148) of the chunked kernels (SV
 // of n only: rank slices of the outer index see the same chunks)
 static int inner_chunks(int n, int threads, int per_thread = 1) {
   const int outer = (n + threads * per_thread - 1) / (threads * per_thread);
+  static const int min_chunk = [] {  // smallest inner chunk (SVD1_CHUNK_MIN, tuning)
+    const char* e = std::getenv("SVD1_CHUNK_MIN");
+    return e ? std::max(32, atoi(e)) : 256;
+  }();
   int ch = (chunk_blocks() * 148 + outer - 1) / outer;
-  ch = std::max(1, std::min(ch, (n + 255) / 256));
+  ch = std::max(1, std::min(ch, (n + min_chunk - 1) / min_chunk));
   return ch;
 }
 

@@ -143,7 +143,8 @@ def paper_uniform(m, n, seed_or_rng, lo=1.0, hi=9.0):
 
 def random_secular(n, seed_or_rng, rho=None, kind="gaussian", n_zero=0, n_dup=0):
     """A symmetric rank-one eigenproblem D + rho z z^T: d ascending, z, rho.
-    kind: 'gaussian' d ~ N(0,1); 'graded' d = 10^(-12 i/n); 'uniform' d ~ U[1,100]^2.
+    kind: 'gaussian' d ~ N(0,1); 'graded' d = 10^(-12 i/n); 'uniform' d ~ U[1,100]^2;
+    'wide' d = 10^(-140 .. 140) (products of a few gaps leave the double range).
     n_zero forced zero weights and n_dup bitwise-duplicated d values exercise
     deflation (SPEC.md:610 acceptance shape)."""
     rng = _rng(seed_or_rng)
@@ -153,6 +154,8 @@ def random_secular(n, seed_or_rng, rho=None, kind="gaussian", n_zero=0, n_dup=0)
         d = 10.0 ** (-12.0 * np.arange(n) / n)
     elif kind == "uniform":
         d = rng.uniform(1.0, 100.0, size=n) ** 2
+    elif kind == "wide":
+        d = 10.0 ** np.linspace(-140.0, 140.0, n)
     else:
         raise ValueError(kind)
     if n_dup:

@@ -58,14 +58,20 @@ def test_secular_parity(plan, n, kind, sgn):
     assert iters <= 40
 
 
-@pytest.mark.parametrize("n,kind", [(3, "gaussian"), (300, "graded"), (1000, "uniform")])
+@pytest.mark.parametrize("n,kind", [(3, "gaussian"), (300, "graded"), (1000, "uniform"), (2500, "uniform"),
+                                    (1500, "wide"), (8192, "wide")])
 def test_loewner_and_colnorm_parity(plan, n, kind):
+    """(2500: full shared-memory tiles with and without the diagonal; 'wide': products of a
+    few gaps overflow between the fast renormalisations -> the per-index / per-chunk frexp
+    redo, in the warp kernel (n < 8192) and the chunked kernel (8192))"""
     rng = np.random.default_rng(11 + n)
     d, z, rho = random_secular(n, rng, kind=kind)
     k, tau = O.secular_roots_bisect(d, z, rho)
     zo = O.loewner_zhat(d, k, tau, rho, z)
     zg = N(plan.loewner(T(d), T(k, torch.int32), T(tau), rho, T(z)))
     assert np.max(np.abs(zg / zo - 1)) <= 1e-12
+    if n > 4096:
+        return  # (the norms' explicit X would be n^2 doubles; covered at the other sizes)
     _, cn = O.cauchy_X(d, k, tau, zo)
     cg = N(plan.colnorms(T(d), T(k, torch.int32), T(tau), T(zo)))
     assert np.max(np.abs(cg / cn - 1)) <= 1e-13

@@ -18,7 +18,7 @@ timeout 900 python bench.py --fused --steps 16 --warmup 3 --no-cpu > $O/bench_fu
 # 3. in-sequence DRAM bytes of every libsvd1 kernel, unfused and fused (C3, caches not flushed)
 for f in "" "--fused"; do
   timeout 900 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-     -k regex:svd1 --csv --log-file $O/dram_all${f}_$TAG.csv python bench.py $f --steps 2 --warmup 3 --no-e2e --no-check --no-cpu > /dev/null 2>&1; echo "dram$f rc=$?"
+     -k 'regex:fmm_|secular|secfmm|loewner|colnorm|proj_|few_rows|householder|passthrough|col_rotate|probe|null_dir|gram_rows|thin_carry|apply_direct' --csv --log-file $O/dram_all${f}_$TAG.csv python bench.py $f --steps 2 --warmup 3 --no-e2e --no-check --no-cpu > /dev/null 2>&1; echo "dram$f rc=$?"
 done
 # 4. --set full of the HBM-bound kernels (projections, Householder, passthrough, few-rows) at C3 and C5
 timeout 900 ncu --set full --clock-control none -k 'regex:proj_partial|proj_multi|householder|passthrough|few_rows|col_rotate|null_dir' -c 12 \
