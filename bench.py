@@ -200,6 +200,8 @@ def main():
                          "row chunk by row chunk, L2-resident")
     ap.add_argument("--sequential", action="store_true",
                     help="time the per-update API (svd1_update) instead of svd1_update_batch")
+    ap.add_argument("--no-seq", action="store_true",
+                    help="skip the per-update API reference leg (profiling the stream alone)")
     ap.add_argument("--config", type=int, default=CFG_ID, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default C3, the headline metric's workload)")
     args = ap.parse_args()
@@ -320,7 +322,7 @@ def main():
         ms = float(tt.item())
     value = args.steps / (ms / 1e3)
     seq = None
-    if batch:  # the per-update API on the same stream, for reference (not the headline)
+    if batch and not args.no_seq:  # the per-update API on the same stream, for reference (not the headline)
         restore()
         for t in range(max(args.warmup, args.steps)):  # its own buffers warm too
             step(t)
