@@ -473,19 +473,18 @@ def main():
         if m * n <= 4096 * 4096:
             # sigma against the singular values of the accumulated A_hat (cuSOLVER, a library
             # reference for verification; the oracle parity is in tests/): Gram-normalised
-            # error (reading D2), strict relative error, and that error over the Gram
-            # sensitivity eps (sigma_1 / sigma_i)^2 / 2 of the computed sigma^2
+            # error (reading D2), strict relative error over all sigma and over sigma >= 0.1 sigma_1
             sv = torch.linalg.svdvals(A)
             kk = min(m, n)
             ref, got = sv[:kk], sig[:kk]
             rel = (got - ref).abs() / ref.clamp_min(1e-300)
-            sens = 2.220446049250313e-16 * (ref[0] / ref.clamp_min(1e-300)) ** 2 / 2
             top = ref >= 0.1 * ref[0]
             check["sigma_vs_svdvals"] = {
                 "gram": float((got * got - ref * ref).abs().max() / (ref[0] * ref[0])),
                 "max_rel": float(rel.max()), "max_rel_top": float(rel[top].max()),
-                "max_rel_over_sens": float((rel / sens).max()),
-                "note": "reference: torch.linalg.svdvals of the explicitly accumulated A_hat (fp64)"}
+                "note": ("reference: torch.linalg.svdvals of the explicitly accumulated A_hat (fp64), after all "
+                         "the timed updates; sigma^2 are Gram eigenvalues (D2), so the error of a small sigma_i "
+                         "scales with (sigma_1 / sigma_i)^2, and the FMM tolerance eps bounds the factors")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == CFG_ID:
