@@ -12,7 +12,8 @@ itself under torch.distributed.run), rows of U and V sharded across ranks, the S
 projections all-reduced over NCCL and every eigen-update's spectral phase sliced across
 the ranks and all-gathered inside libsvd1; time = max over ranks.
 `--impl reference` times the CPU oracle (oracle/, the base contract's reference arm
-for this tier) on bounded samples of the same workload.
+for this tier) on whole updates of the same workload (one whole C3 update per step,
+about 8 s each on a 16-core host).
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
