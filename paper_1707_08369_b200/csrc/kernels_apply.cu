@@ -228,7 +228,8 @@ __global__ void passthrough_kernel(int64_t rows, int nq, const double* __restric
 // per column instead of p per element).  blockIdx.y = 0: source kinds (P2M, P2L, P2P)
 // and ID, a block per operator, one division per element.
 __device__ __forceinline__ bool is_lagrange(int kind) {
-  return kind == OP_M2M || kind == OP_M2L || kind == OP_L2L || kind == OP_L2P || kind == OP_L2P_FROM;
+  return kind == OP_M2M || kind == OP_M2L || kind == OP_L2L || kind == OP_L2P || kind == OP_L2P_FROM ||
+         kind == OP_M2P;
 }
 
 __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc* __restrict__ descs,
@@ -296,6 +297,13 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
             const int jt = Y.tlo + j;
             x = ((d[k[jt]] - Y.c) + tau[jt]) / Y.r;
             f = cs[jt];
+            break;
+          }
+          case OP_M2P: {  // far field of leaf a at the targets of leaf b: t_X = 3 r_X / (mu_j - c_X)
+            const FmmCell X = cells[D.a], Y = cells[D.b];
+            const int jt = Y.tlo + j;
+            x = 3.0 * X.r / ((d[k[jt]] - X.c) + tau[jt]);
+            f = x * cs[jt];
             break;
           }
           default: {  // OP_L2P_FROM: expansion of cell a (an ancestor) at the targets of leaf b

@@ -979,7 +979,15 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   // target cell only separates from the narrow sources below it at a finer level.
   // interaction lists as CSR (target cell -> sorted partner cells), built from the
   // traversal's pairs with one sort (no per-cell allocations)
-  std::vector<std::pair<int, int>> near_pairs, m2l_pairs;
+  std::vector<std::pair<int, int>> near_pairs, m2l_pairs, p2l_pairs, m2p_pairs;
+  // one-sided separation of near leaves (SVD1_ONE_SIDED=0 disables; experiments)
+  static const bool one_sided = [] {
+    const char* e = std::getenv("SVD1_ONE_SIDED");
+    return !(e && atoi(e) == 0);
+  }();
+  // measured pass rates (TFLOP/s, ncu, C3: profiles/ncu_full_r02_gemm.md) weighing the choice
+  static const double kRate16 = std::getenv("SVD1_RATE16") ? atof(std::getenv("SVD1_RATE16")) : 18.0;
+  constexpr double kRate32 = 24.5;
   near_pairs.reserve(size_t(F.ncells) * 4);
   m2l_pairs.reserve(size_t(F.ncells) * 4);
   const int first_leaf = (1 << L) - 1;
@@ -995,6 +1003,32 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       continue;
     }
     if (is_leaf(x) && is_leaf(y)) {
+      // Two leaves that fail the symmetric test may still be separated on one side (the
+      // adaptive FMM's X and W lists): X's sources far from Y's box -> P2L into Y's local
+      // expansion (Y's Chebyshev interpolant converges as for M2L); Y's targets far from
+      // X's box -> M2P, X's far field evaluated at Y's targets.  Each is taken when its
+      // estimated time beats the near-field product's (flops over the measured rate of the
+      // pass it lands in: the 16-wide M2L pass, the 32-wide final pass).
+      if (x != y && one_sided) {
+        const FmmCell &X = F.cells[x], &Y = F.cells[y];
+        const double D = std::fabs(X.c - Y.c);
+        const double ns = X.shi - X.slo, nt = Y.thi - Y.tlo;
+        double best = ns * nt / kRate32;  // P2P
+        int kind = 0;
+        if (D - X.r >= 3.0 * Y.r && ns * p / kRate16 < best) {
+          best = ns * p / kRate16;
+          kind = 1;
+        }
+        if (D - Y.r >= 3.0 * X.r && double(p) * nt / kRate32 < best) kind = 2;
+        if (kind == 1) {
+          p2l_pairs.push_back({y, x});
+          continue;
+        }
+        if (kind == 2) {
+          m2p_pairs.push_back({y, x});
+          continue;
+        }
+      }
       near_pairs.push_back({y, x});
       continue;
     }
@@ -1007,7 +1041,9 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       stack.push_back({x, 2 * y + 1});
     }
   }
-  const Csr near(near_pairs, F.ncells), m2l(m2l_pairs, F.ncells);
+  const Csr near(near_pairs, F.ncells), m2l(m2l_pairs, F.ncells), p2l(p2l_pairs, F.ncells),
+      m2p(m2p_pairs, F.ncells);
+  auto has_local = [&](int y) { return !m2l[y].empty() || !p2l[y].empty(); };  // Psi_y non-zero
   const double tt1 = now_ms();
   // A term's op (K x N) is stored chunk-transposed (FmmTerm): new_term reserves its
   // ceil(K/16) chunks of [npad][16] doubles; add_op adds a block of its rows.
@@ -1226,10 +1262,11 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     F.pass_bn.push_back(pairs ? 2 * p : p);
     std::vector<int> via_phi, via_src;
     std::vector<std::pair<int, int>> uni;  // (partner, 1: of y | 2: of y2)
+    std::vector<int> xs;
     for (int y = 1; y < F.ncells; ++y) {
-      if (m2l[y].empty() || !has_tgt(y)) continue;
+      if (!has_local(y) || !has_tgt(y)) continue;
       const int y2 = pair_of(y);
-      if (y2 > 0 && has_tgt(y2) && !m2l[y2].empty()) {
+      if (y2 > 0 && has_tgt(y2) && !m2l[y2].empty() && p2l[y].empty() && p2l[y2].empty() && !m2l[y].empty()) {
         uni.clear();
         size_t i1 = 0, i2 = 0;
         const auto A1 = m2l[y], A2 = m2l[y2];
@@ -1286,13 +1323,15 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       for (int x : m2l[y]) (F.cells[x].shi - F.cells[x].slo >= p ? via_phi : via_src).push_back(x);
       add_runs(via_phi, IO_PHI, OP_M2L, y, p);
       add_runs(via_src, IO_U, OP_P2L, y, p);
-      F.n_m2l_pairs += int(m2l[y].size());
+      xs.assign(p2l[y].begin(), p2l[y].end());  // one-sided: sources straight into Psi_y
+      add_runs(xs, IO_U, OP_P2L, y, p);
+      F.n_m2l_pairs += int(m2l[y].size() + p2l[y].size());
       end_task(IO_PSI, y * p, p);
     }
     sort_pass(F.pass_begin.back());
     for (int i = 0; i < 2 && i < (1 << L); ++i) {
       const int y = 1 + i;  // level 1: full = the M2L part
-      if (L >= 1 && has_tgt(y) && !m2l[y].empty()) loc[y] = IO_PSI;
+      if (L >= 1 && has_tgt(y) && has_local(y)) loc[y] = IO_PSI;
     }
     pairs = 2 * p <= 32 && (pair_mask & 2);
     int a = 1;  // anchor level: full expansions known
@@ -1407,9 +1446,13 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     if (split_narrow && (ty > 16) != (wide == 1)) continue;
     begin_task();
     const int par = (y - 1) / 2;
-    if (!m2l[y].empty()) {
+    if (has_local(y)) {
       new_term(IO_PSI, y * p, p, ty, p);
       add_op(OP_L2P, y, y, p, ty, 0);
+    }
+    if (!m2p[y].empty()) {  // one-sided: far fields of near-ish narrow leaves at the targets
+      std::vector<int> ws(m2p[y].begin(), m2p[y].end());
+      add_runs(ws, IO_PHI, OP_M2P, y, ty);
     }
     if (par >= 1 && loc[par] >= 0) {
       new_term(loc[par], par * p, p, ty, p);

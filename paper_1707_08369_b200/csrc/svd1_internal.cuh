@@ -173,7 +173,8 @@ enum FmmOpKind : int32_t {
   OP_P2M = 0, OP_M2M = 1, OP_M2L = 2, OP_L2L = 3, OP_L2P = 4, OP_P2P = 5,
   OP_P2L = 6,       // sources of a cell with fewer than p points straight into a local expansion
   OP_ID = 7,        // p x p identity (in-place accumulation of the L2L chain)
-  OP_L2P_FROM = 8   // local expansion of cell a evaluated at the targets of leaf b
+  OP_L2P_FROM = 8,  // local expansion of cell a evaluated at the targets of leaf b
+  OP_M2P = 9        // far field of leaf a evaluated at the targets of leaf b (adaptive W list)
 };
 struct FmmOpDesc {    // one operator block: rows x cols, written into its term's op
   int32_t kind, a, b; // a = source cell (expansion kinds) or first source index (source
