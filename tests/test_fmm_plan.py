@@ -72,3 +72,28 @@ def test_secular_fmm_plan_outliers():
     d = np.sort(np.concatenate([10.0 ** (-12 * np.arange(n - 16) / n), 1.7e7 * (1 + rng.random(16))]))
     st = secfmm_plan_stats(d)
     assert st["max_near_terms"] <= 6 * 32 and st["direct_roots"] >= 2, st
+
+
+def test_one_sided_lists_shrink_the_near_field():
+    """One-sided separation (P2L / M2P for leaf pairs the symmetric test
+    rejects) on a graded spectrum: fewer near pairs and fewer flops than the symmetric
+    lists (SVD1_ONE_SIDED=0, read once per process: compared in a subprocess)."""
+    import json, os, subprocess, sys
+    n = 2048
+    d, z, _ = random_secular(n, np.random.default_rng(5), kind="graded")
+    k, tau = _roots(d, z, 1.0)
+    on = fmm_tree_stats(d, k, tau, 1e-10)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r); "
+            "from paper_1707_08369_b200._lib import fmm_tree_stats; "
+            "a = np.load(sys.argv[1]); print(json.dumps(fmm_tree_stats(a['d'], a['k'], a['tau'], 1e-10)))" % root)
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        f = os.path.join(td, "s.npz")
+        np.savez(f, d=d, k=k, tau=tau)
+        out = subprocess.run([sys.executable, "-c", code, f], capture_output=True, text=True, check=True,
+                             env={**os.environ, "SVD1_ONE_SIDED": "0"}).stdout
+    off = json.loads(out.strip().splitlines()[-1])
+    assert on["near_pairs"] < off["near_pairs"], (on, off)
+    assert on["flops_per_row"] < off["flops_per_row"], (on, off)
+    assert on["max_near"] <= off["max_near"]
