@@ -379,7 +379,9 @@ def main():
             "apply_phase_ms_per_update": ap_ms / args.steps,
             "flops_exec_per_apply": ap_fx / max(n_apply, 1),
             "flops_note": "achieved counts the algorithmic flops of SURVEY §8(d) (level-by-level "
-                          "P2M/M2M/M2L/L2L/L2P/P2P from the plan); the plan executes "
+                          "P2M/M2M/M2L/L2L/L2P/P2P from the plan, plus the one-sided P2L/M2P terms that "
+                          "replace near-field products: about 11 % fewer flops than the symmetric lists at "
+                          "C3, so frac reads lower for a faster apply); the plan executes "
                           "flops_exec_per_apply (coarse levels in bands, DESIGN.md §4.4)",
             "timing": ("CUDA events on the launching streams around the apply phase of every update in "
                        "the timed region; svd1_update_batch: achieved = algorithmic apply flops over the "

@@ -210,6 +210,8 @@ Split schur_split(double beta) {
 
 struct FmmHost {
   int L = 0, ncells = 0;
+  int ecells = 0;     // expansion columns / p: the cells, then one slot per fused P2L pair
+  int64_t cap_cells = 0;  // expansion columns / p the plan's workspaces hold (0: no slots)
   std::vector<FmmCell> cells;
   std::vector<FmmOpDesc> ops;
   std::vector<FmmTerm> terms;
@@ -1044,6 +1046,25 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   const Csr near(near_pairs, F.ncells), m2l(m2l_pairs, F.ncells), p2l(p2l_pairs, F.ncells),
       m2p(m2p_pairs, F.ncells);
   auto has_local = [&](int y) { return !m2l[y].empty() || !p2l[y].empty(); };  // Psi_y non-zero
+  // Fused P2L (SVD1_P2L_FUSED=1; experiments, off): the P2L pairs computed in the P2M
+  // pass, which reads the same source windows of U, each into a slot of its own past the
+  // cells' columns of Phi, and the M2L pass adding a target's slots with identity operators
+  // (2 p^2 per pair instead of re-reading the sources from DRAM).  Needs room for the slots
+  // in the plan's expansion workspace.  Measured at C3: P2M 39 -> 52 us, M2L 98 -> 93 us,
+  // the stream 444-454 -> 442-448 updates/s, hence off.
+  static const bool p2l_fuse_env = [] {
+    const char* e = std::getenv("SVD1_P2L_FUSED");
+    return e && atoi(e) != 0;
+  }();
+  const int npl = int(p2l.val.size());
+  const bool p2l_fused = p2l_fuse_env && npl > 0 && int64_t(F.ncells) + npl <= F.cap_cells;
+  F.ecells = F.ncells + (p2l_fused ? npl : 0);
+  std::vector<std::vector<std::pair<int, int>>> p2l_by_src;  // x -> (target y, slot)
+  if (p2l_fused) {
+    p2l_by_src.resize(F.ncells);
+    for (int y = 0; y < F.ncells; ++y)
+      for (int q = p2l.off[y]; q < p2l.off[y + 1]; ++q) p2l_by_src[p2l.val[q]].push_back({y, F.ncells + q});
+  }
   const double tt1 = now_ms();
   // A term's op (K x N) is stored chunk-transposed (FmmTerm): new_term reserves its
   // ceil(K/16) chunks of [npad][16] doubles; add_op adds a block of its rows.
@@ -1076,7 +1097,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     F.ops.push_back(D);
   };
   int64_t adj = 0;  // level-by-level M2M / L2L flops minus the banded ones
-  int64_t zero_flops = 0;  // executed on the zero blocks of sibling-pair tasks (not algorithmic)
+  int64_t zero_flops = 0;  // executed, not algorithmic: sibling-pair zero blocks, fused-P2L accumulation
   // sources [s_lo, s_hi) (a contiguous range of the sorted active sources) read through
   // their physical input columns src[s]: windows of nearby columns (gaps <= 8 are
   // bridged by zero op rows), each starting at an even column
@@ -1194,6 +1215,12 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       begin_task();
       add_src(OP_P2M, F.cells[x].slo, F.cells[x].shi, x, p);
       end_task(IO_PHI, x * p, p);
+      if (p2l_fused)
+        for (const auto& [y, slot] : p2l_by_src[x]) {  // fused P2L: same window, next task
+          begin_task();
+          add_src(OP_P2L, F.cells[x].slo, F.cells[x].shi, y, p);
+          end_task(IO_PHI, slot * p, p);
+        }
     }
     sort_pass(F.pass_begin.back());
     // M2M (STEP 6; operator re-derived), levels L-1 .. 1 in
@@ -1323,8 +1350,17 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       for (int x : m2l[y]) (F.cells[x].shi - F.cells[x].slo >= p ? via_phi : via_src).push_back(x);
       add_runs(via_phi, IO_PHI, OP_M2L, y, p);
       add_runs(via_src, IO_U, OP_P2L, y, p);
-      xs.assign(p2l[y].begin(), p2l[y].end());  // one-sided: sources straight into Psi_y
-      add_runs(xs, IO_U, OP_P2L, y, p);
+      if (p2l_fused) {  // one-sided: the slots the P2M pass filled, by identity operators
+        if (!p2l[y].empty()) {
+          const int cnt = int(p2l[y].size()), c0 = F.ncells + p2l.off[y];
+          new_term(IO_PHI, c0 * p, cnt * p, p, cnt * p);
+          for (int q = 0; q < cnt; ++q) add_op(OP_ID, y, y, p, p, q * p);
+          zero_flops += 2ll * cnt * p * p;  // accumulation, not algorithmic work
+        }
+      } else {  // one-sided: sources straight into Psi_y
+        xs.assign(p2l[y].begin(), p2l[y].end());
+        add_runs(xs, IO_U, OP_P2L, y, p);
+      }
       F.n_m2l_pairs += int(m2l[y].size() + p2l[y].size());
       end_task(IO_PSI, y * p, p);
     }
@@ -1476,6 +1512,8 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
 
 }  // namespace
 
+int64_t max_cells(int64_t N, int leaf);
+
 void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<double>& da,
                     const std::vector<double>& mu, const int32_t* src, int64_t rows) {
   const Merged M = merge_points(da, mu);
@@ -1493,6 +1531,7 @@ void fmm_build_host(FmmHost& F, int na, int leaf, int p, const std::vector<doubl
   auto build = [&](int L) {
     Cand& C = cand[size_t(L - L0)];
     if (!fmm_cells(C.F, leaf, L, M)) return;
+    C.F.cap_cells = max_cells(na, leaf);
     // a leaf whose hull spans a quarter of the spectrum (outliers packed with bulk points
     // because the capacities left no room for a gap split) is near to every leaf: such a
     // tree is skipped when a deeper one is still to come
@@ -1655,7 +1694,7 @@ svd1_status cauchy_prepare(svd1_plan_t P, CauchyPrep& C, int64_t rows, int na,
 }
 
 size_t cauchy_exp_elems(const CauchyPrep& C) {
-  return C.fmm ? size_t(C.F.ncells) * size_t(C.p) * size_t(C.rows) : 0;
+  return C.fmm ? size_t(std::max(C.F.ecells, C.F.ncells)) * size_t(C.p) * size_t(C.rows) : 0;
 }
 
 // K5: every operator block of the plan into the ops buffer (zeroed first: op chunks are
@@ -1692,7 +1731,7 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   const size_t exp_elems = cauchy_exp_elems(C);
   TRY(P->phi[side].get<double>(exp_elems, &phi, st));  // sized at creation (no growth here)
   TRY(P->psi[side].get<double>(exp_elems, &psi, st));
-  const int64_t ldE = int64_t(F.ncells) * p;
+  const int64_t ldE = int64_t(std::max(F.ecells, F.ncells)) * p;
   FmmCell* dc = C.dcells;
   FmmOpDesc* dd = C.ddescs;
   FmmTerm* dt = C.dterms;
