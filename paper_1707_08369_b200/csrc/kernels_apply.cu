@@ -446,8 +446,8 @@ struct GemmCfg {
 // row blocks (its operator chunks stay hot, the A windows stream down the rows).
 // Row-block-major (per pass, chosen by the host): the CTAs in flight cover a few row
 // blocks and every task, so shared input rows are re-read from L2 -- measured at C3 for
-// every pass: DRAM per apply 1.26 -> 1.10 GB, but 481 -> 505 us; the host uses it for
-// the P2M pass only (svd1_host.cu, rb_passes).
+// every pass: DRAM per apply 1.26 -> 1.10 GB, but 481 -> 505 us (the final pass loses);
+// the host uses it for the 16-wide passes (svd1_host.cu, rb_kinds).
 __device__ __forceinline__ int tile_task(int tile, int nrb, int ntask, int rb_major) {
   return rb_major ? tile % ntask : tile / nrb;
 }

@@ -218,6 +218,7 @@ struct FmmHost {
   std::vector<FmmTask> tasks;
   std::vector<int> pass_begin;  // task index where each pass starts (+ end sentinel)
   std::vector<int> pass_bn;     // tile width (16 or 32) of each pass
+  std::vector<int> pass_kind;   // 0 P2M, 1 M2M band, 2 M2L, 3 L2L band, 4 final (L2P + M2P + P2P)
   int64_t ops_rows = 0;         // ops buffer: rows of 16 doubles
   int64_t flops_per_row = 0;    // algorithmic flops per row (level by level)
   int64_t flops_exec_per_row = 0;  // flops the plan executes per row (level bands included)
@@ -1209,6 +1210,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     // P2M (STEP 5) in the scaled far-field form
     F.pass_begin.push_back(int(F.tasks.size()));
     F.pass_bn.push_back(p);
+    F.pass_kind.push_back(0);
     for (int i = 0; i < nleaf; ++i) {
       const int x = lf0 + i;
       if (!has_src(x)) continue;
@@ -1247,6 +1249,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       }
       F.pass_begin.push_back(int(F.tasks.size()));
       F.pass_bn.push_back(p);
+      F.pass_kind.push_back(1);
       for (int l = f - 1; l >= lo; --l)
         for (int i = 0; i < (1 << l); ++i) {
           const int c = (1 << l) - 1 + i;
@@ -1287,6 +1290,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
     };
     F.pass_begin.push_back(int(F.tasks.size()));
     F.pass_bn.push_back(pairs ? 2 * p : p);
+    F.pass_kind.push_back(2);
     std::vector<int> via_phi, via_src;
     std::vector<std::pair<int, int>> uni;  // (partner, 1: of y | 2: of y2)
     std::vector<int> xs;
@@ -1456,6 +1460,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
       if (int(F.tasks.size()) > pb) {
         F.pass_begin.push_back(pb);
         F.pass_bn.push_back(pairs ? 2 * p : p);
+        F.pass_kind.push_back(3);
         sort_pass(pb);
       }
       a = hi;
@@ -1475,6 +1480,7 @@ void fmm_lists(FmmHost& F, int p, const int32_t* src, int64_t rows) {
   if (!split_narrow && wide == 0) continue;
   F.pass_begin.push_back(int(F.tasks.size()));
   F.pass_bn.push_back(wide ? 32 : 16);
+  F.pass_kind.push_back(4);
   for (int i = 0; i < nleaf; ++i) {
     const int y = lf0 + i;
     if (!has_tgt(y)) continue;
@@ -1870,22 +1876,24 @@ svd1_status cauchy_launch(svd1_plan_t P, CauchyPrep& C, const double* d_da, cons
   TRY(P->tile_ctr[side].get<int>(kMaxPasses, &ctrs, st));
   if (F.pass_begin.size() > size_t(kMaxPasses)) return SVD1_E_INVALID;
   SVD1_CUDA_TRY(cudaMemsetAsync(ctrs, 0, sizeof(int) * kMaxPasses, st));
-  // passes whose tiles run row-block-major (bit s: pass s): P2M, the first pass, streams
-  // every column of the input once -- in row-block order the CTAs in flight read whole rows
-  // (C3 alone: 43 -> 39 us; the other passes the same or slower, the final pass 253 -> 270).
-  // SVD1_RB_PASSES overrides the mask, SVD1_TILE_ORDER=rb sets every pass (experiments).
-  static const unsigned rb_passes = [] {
+  // pass kinds whose tiles run row-block-major (bit k: pass_kind k): every 16-wide pass
+  // (P2M, M2M, M2L, L2L) -- the CTAs in flight cover a few row blocks and every task, so
+  // the input rows they share (U windows, expansion windows of neighbouring cells) are read
+  // from DRAM once.  C3 stream, 4 runs each: P2M only 447, P2M + M2L + L2L 454, all four
+  // 457 updates/s; the final pass (32-wide, compute-bound) stays task-major (253 -> 270 us
+  // row-block-major).  SVD1_RB_KINDS overrides the mask, SVD1_TILE_ORDER=rb sets every pass.
+  static const unsigned rb_kinds = [] {
     const char* e = std::getenv("SVD1_TILE_ORDER");
     if (e && std::string(e) == "rb") return ~0u;
-    const char* m = std::getenv("SVD1_RB_PASSES");
-    return m ? unsigned(strtoul(m, nullptr, 0)) : 1u;
+    const char* m = std::getenv("SVD1_RB_KINDS");
+    return m ? unsigned(strtoul(m, nullptr, 0)) : 15u;
   }();
   for (size_t s = 0; s + 1 < F.pass_begin.size(); ++s) {
     const int b = F.pass_begin[s], e = F.pass_begin[s + 1];
     if (e <= b) continue;
     TRY(gmark());
     TRY(fmm_run_tasks(e - b, dk + b, dt, F.pass_bn[s], rows, maps, U_out, ld_out, d_dst, phi, psi, ldE,
-                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, ctrs + s, (rb_passes >> s) & 1, st, LC(P)));
+                      C.n_out, int64_t(exp_elems), ops, F.ops_rows, ctrs + s, (rb_kinds >> F.pass_kind[s]) & 1, st, LC(P)));
     TRY(gmark());
     pmark();
     if (dbg) {
