@@ -303,11 +303,17 @@ def main():
 
     # warm-up: W steps, and at least the timed stream's length (its later updates build deeper
     # trees than the first W: their first-time host / device costs stay out of the timed region)
-    run(0, max(args.warmup, args.steps))
-    restore()
+    # (twice: the first stream of a process pays one-off host costs -- thread start, first
+    # touch of the host-side plan buffers -- measured as a 5-7 % slower first run)
+    for _ in range(2):
+        run(0, max(args.warmup, args.steps))
+        restore()
     torch.cuda.synchronize()
     reps = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    import gc
+    gc.collect()
+    gc.disable()  # no Python collector pause inside the timed region
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -315,6 +321,7 @@ def main():
         reps = run(0, args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
+    gc.enable()
     barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
