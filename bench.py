@@ -518,6 +518,7 @@ def main():
                 "data": "synthetic (seeded, BASELINE.json C3 recipe)",
                 "config": {"workload": WORKLOAD, "m": m, "n": n, "eps": cfg["eps"], "p": reps[-1]["p"],
                            "updates_in_stream": cfg["updates"],
+                           "warmup_updates": 2 * max(args.warmup, args.steps),
                            "l2": (f"inputs larger than L2 (U + V = {8 * (m * m + n * n) / 2**20:.0f} MiB > 126 MB)"
                                   if 8 * (m * m + n * n) > 126e6 else
                                   f"inputs fit in L2 ({8 * (m * m + n * n) / 2**20:.1f} MiB); no flush"),
