@@ -21,8 +21,11 @@ for f in "" "--fused"; do
      -k 'regex:fmm_|secular|secfmm|loewner|colnorm|proj_|few_rows|householder|passthrough|col_rotate|probe|null_dir|gram_rows|thin_carry|apply_direct' --csv --log-file $O/dram_all${f}_$TAG.csv python bench.py $f --steps 2 --warmup 3 --no-e2e --no-check --no-cpu > /dev/null 2>&1; echo "dram$f rc=$?"
 done
 # 4. --set full of the HBM-bound kernels (projections, Householder, passthrough, few-rows) at C3 and C5
+#    (HBM=0 skips it: gpurun brings back at most 64 MiB of gpurun_out/)
+if [ "${HBM:-1}" != 0 ]; then
 timeout 900 ncu --set full --clock-control none -k 'regex:proj_partial|proj_multi|householder|passthrough|few_rows|col_rotate|null_dir' -c 12 \
    -o $O/hbm_c3_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-check --no-cpu > /dev/null 2>&1; echo "hbm c3 rc=$?"
 timeout 1200 ncu --set full --clock-control none -k 'regex:proj_partial|householder|passthrough|few_rows' -c 10 \
    -o $O/hbm_c5_$TAG -f python bench.py --config 5 --steps 2 --warmup 1 --no-e2e --no-check --no-cpu > /dev/null 2>&1; echo "hbm c5 rc=$?"
+fi
 ls -la $O/*_$TAG*
