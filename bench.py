@@ -385,6 +385,7 @@ def main():
             "flops_per_apply": kern_fl / max(n_apply, 1), "ms_per_apply": kern_ms / max(n_apply, 1),
             "apply_phase_ms_per_update": ap_ms / args.steps,
             "flops_exec_per_apply": ap_fx / max(n_apply, 1),
+            "frac_executed": (ap_fx / ((kern_ms if kern_ms > 0 else 1.0) / 1e3) / 1e12) / FP64_PEAK_TFLOPS,
             "flops_note": "achieved counts the algorithmic flops of SURVEY §8(d) (level-by-level "
                           "P2M/M2M/M2L/L2L/L2P/P2P from the plan, plus the one-sided P2L/M2P terms that "
                           "replace near-field products: about 11 % fewer flops than the symmetric lists at "
