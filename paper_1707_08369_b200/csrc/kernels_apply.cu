@@ -222,14 +222,23 @@ __global__ void passthrough_kernel(int64_t rows, int nq, const double* __restric
 // Chebyshev nodes t_k = cos((2k+1) pi / 2p) (k 0-based) and barycentric weights
 // w_k = (-1)^k sin((2k+1) pi / 2p); u_k(t) = [w_k/(t - t_k)] / sum_m w_m/(t - t_m).
 
-// blockIdx.y = 1: expansion kinds (M2M, M2L, L2L, L2P, L2P_FROM), a warp per operator
-// block: they are Lagrange bases evaluated at a point that depends only on the column
-// j, so lane j forms the barycentric denominator once and then the p rows (2p divisions
-// per column instead of p per element).  blockIdx.y = 0: source kinds (P2M, P2L, P2P)
-// and ID, a block per operator, one division per element.
+// blockIdx.y = 1: expansion kinds (M2M, M2L, L2L, L2P, L2P_FROM, M2P), a warp per
+// operator block: they are Lagrange bases evaluated at a point that depends only on the
+// column j, so lane j forms the barycentric denominator once and then the p rows (2p
+// reciprocals and one division per column).  blockIdx.y = 0: source kinds (P2M, P2L, P2P)
+// and ID, a block per operator, one reciprocal per element (MUFU seed + 2 Newton steps).
 __device__ __forceinline__ bool is_lagrange(int kind) {
   return kind == OP_M2M || kind == OP_M2L || kind == OP_L2L || kind == OP_L2P || kind == OP_L2P_FROM ||
          kind == OP_M2P;
+}
+
+__device__ __forceinline__ double ops_rcp(double x) {  // 1/x to ~1 ulp: MUFU seed + 2 Newton steps
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
 }
 
 __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc* __restrict__ descs,
@@ -314,17 +323,20 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
             break;
           }
         }
-        // barycentric form u_i(x) = (w_i / (x - t_i)) / sum_m w_m / (x - t_m)
+        // barycentric form u_i(x) = (w_i / (x - t_i)) / sum_m w_m / (x - t_m), with
+        // reciprocals by MUFU + Newton (<= 1 ulp) and one division for the column's scale
+        // (instead of 3p IEEE divisions per column)
         double den = 0.0;
         int hit = -1;
         for (int m = 0; m < p; ++m) {
           const double dx = x - t[m];
           if (dx == 0.0) hit = m;
-          else den += w[m] / dx;
+          else den = fma(w[m], ops_rcp(dx), den);
         }
+        const double sc = f / den;
         for (int i = 0; i < D.rows; ++i) {
-          const double v = hit >= 0 ? (i == hit ? f : 0.0) : f * (w[i] / (x - t[i])) / den;
-          store(i, j, v);
+          const double dx = x - t[i];
+          store(i, j, hit >= 0 ? (i == hit ? f : 0.0) : (w[i] * ops_rcp(dx)) * sc);
         }
       }
       continue;
@@ -344,14 +356,14 @@ __global__ void __launch_bounds__(256) fmm_ops_kernel(int n_ops, const FmmOpDesc
           if (s < D.a || s >= D.s_hi) break;
           if (D.kind == OP_P2M) {  // Phi~_X[j] += zhat_s U_s / (t_j (x_s - c_X) - 3 r_X), X = b
             const FmmCell X = cells[D.b];
-            v = zhat[s] / (t[j] * (d[s] - X.c) - 3.0 * X.r);
+            v = zhat[s] * ops_rcp(t[j] * (d[s] - X.c) - 3.0 * X.r);
           } else if (D.kind == OP_P2L) {  // source s -> local expansion of Y (b) at c_Y + r_Y t_j
             const FmmCell Y = cells[D.b];
-            v = zhat[s] / ((d[s] - Y.c) - Y.r * t[j]);
+            v = zhat[s] * ops_rcp((d[s] - Y.c) - Y.r * t[j]);
           } else {  // OP_P2P: source s, target leaf Y (b)
             const FmmCell Y = cells[D.b];
             const int jt = Y.tlo + j;
-            v = (zhat[s] * cs[jt]) / ((d[s] - d[k[jt]]) - tau[jt]);
+            v = (zhat[s] * cs[jt]) * ops_rcp((d[s] - d[k[jt]]) - tau[jt]);
           }
           break;
         }
