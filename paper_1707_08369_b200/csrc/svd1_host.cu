@@ -845,7 +845,13 @@ void secfmm_plan(const double* d, int n, SecPlanHost& S) {
   };
   const int first_leaf = (1 << L) - 1;
   auto is_leaf = [&](int c) { return c >= first_leaf; };
-  std::vector<std::pair<int, int>> m2l_pairs, near_pairs;
+  std::vector<std::pair<int, int>> m2l_pairs, near_pairs, p2l_pairs;
+  // one-sided separation of near leaves (as the apply's, §4.4): X's sources far enough from
+  // the target interval of Y for Y's local expansion -> P2L instead of the direct sum
+  static const bool one_sided = [] {
+    const char* e = std::getenv("SVD1_ONE_SIDED");
+    return !(e && atoi(e) == 0);
+  }();
   std::vector<std::pair<int, int>> stack{{0, 0}};
   while (!stack.empty()) {
     const auto [x, y] = stack.back();
@@ -856,7 +862,9 @@ void secfmm_plan(const double* d, int n, SecPlanHost& S) {
       continue;
     }
     if (is_leaf(x) && is_leaf(y)) {
-      near_pairs.push_back({y, x});
+      const SecFmmCell &X = S.cells[x], &Y = S.cells[y];
+      if (one_sided && x != y && std::fabs(X.c - Y.ct) - X.r >= 3.0 * Y.rt) p2l_pairs.push_back({y, x});
+      else near_pairs.push_back({y, x});
       continue;
     }
     const bool split_x = is_leaf(y) || (!is_leaf(x) && S.cells[x].r > S.cells[y].rt);
@@ -879,10 +887,11 @@ void secfmm_plan(const double* d, int n, SecPlanHost& S) {
     for (int c = 0; c < nc; ++c)
       if (off[c + 1] - off[c] > 1) std::sort(val.begin() + off[c], val.begin() + off[c + 1]);
   };
-  std::vector<int> m_off, m_val;
+  std::vector<int> m_off, m_val, o_off, o_val;
   group(m2l_pairs, m_off, m_val);
+  group(p2l_pairs, o_off, o_val);
   S.parts.clear();
-  S.parts.reserve(m_val.size());
+  S.parts.reserve(m_val.size() + o_val.size());
   for (int c = 0; c < nc; ++c) {
     S.cells[c].m2l_off = int32_t(S.parts.size());
     for (int q = m_off[c]; q < m_off[c + 1]; ++q) {
@@ -891,6 +900,10 @@ void secfmm_plan(const double* d, int n, SecPlanHost& S) {
       int32_t fl = X.c > S.cells[c].ct ? 1 : 0;
       if (X.hi - X.lo < kSecP) fl |= 2;
       S.parts.push_back(SecFmmPart{x, fl});
+    }
+    for (int q = o_off[c]; q < o_off[c + 1]; ++q) {  // one-sided: always from the sources
+      const int x = o_val[q];
+      S.parts.push_back(SecFmmPart{x, int32_t((S.cells[x].c > S.cells[c].ct ? 1 : 0) | 2)});
     }
   }
   S.cells[nc].m2l_off = int32_t(S.parts.size());
