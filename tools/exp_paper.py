@@ -1,5 +1,5 @@
 """Run the paper's experiments E3 (error vs p) and E4 (Table 2 analogue) on the GPU and
-write profiles/exp_paper_r01.json.  usage: python tools/exp_paper.py"""
+write profiles/exp_paper_r02.json.  usage: python tools/exp_paper.py"""
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -28,7 +28,7 @@ res["note"] = ("E3: PAPER.md:435-445 recipe (entries U[0,1]), FMM forced, eps = 
                "U[1,9]; the paper's values are its implementation's (a ceiling).")
 for d in ("profiles", "gpurun_out"):  # gpurun_out/ travels back from the GPU box
     os.makedirs(os.path.join(ROOT, d), exist_ok=True)
-    json.dump(res, open(os.path.join(ROOT, d, "exp_paper_r01.json"), "w"), indent=1)
+    json.dump(res, open(os.path.join(ROOT, d, "exp_paper_r02.json"), "w"), indent=1)
 for n, v in res["E3"].items():
     print("E3 n=%s direct %.2e" % (n, v["direct_error"]), [("p%d" % r["p"], "%.1e" % r["error"]) for r in v["sweep"]])
 for e in res["E4"]:
