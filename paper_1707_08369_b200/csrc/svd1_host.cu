@@ -8,6 +8,9 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <memory>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -276,6 +279,118 @@ struct CauchyPrep {
 };
 
 // Everything one RankOneUpdate (Alg 6.2) needs at apply time.
+// Host worker threads (apply planners, the U chain, the apply launchers: ~7 per update) are
+// taken from a cache of persistent threads instead of being created and destroyed each
+// time: a job starts on an idle worker (or on a new one when none is idle, so a job that
+// waits for another never starves it), and the handle's join() waits for that job only.
+// SVD1_THREAD_POOL=0 falls back to one std::thread per job (experiments).
+class WorkerPool {
+ public:
+  struct Done {
+    std::mutex m;
+    std::condition_variable cv;
+    bool done = false;
+  };
+  static WorkerPool& get() {
+    static WorkerPool* pool = new WorkerPool;  // never destroyed: idle workers outlive exit
+    return *pool;
+  }
+  std::shared_ptr<Done> submit(std::function<void()> f) {
+    auto d = std::make_shared<Done>();
+    Worker* w = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      if (!idle_.empty()) {
+        w = idle_.back();
+        idle_.pop_back();
+      } else {
+        all_.push_back(std::make_unique<Worker>());
+        w = all_.back().get();
+        std::thread([this, w] { loop(w); }).detach();
+      }
+    }
+    {
+      std::lock_guard<std::mutex> lk(w->m);
+      w->job = [f = std::move(f), d] {
+        f();
+        {
+          std::lock_guard<std::mutex> l2(d->m);
+          d->done = true;
+        }
+        d->cv.notify_all();
+      };
+      w->has_job = true;
+    }
+    w->cv.notify_one();
+    return d;
+  }
+
+ private:
+  struct Worker {
+    std::mutex m;
+    std::condition_variable cv;
+    std::function<void()> job;
+    bool has_job = false;
+  };
+  void loop(Worker* w) {
+    for (;;) {
+      std::function<void()> job;
+      {
+        std::unique_lock<std::mutex> lk(w->m);
+        w->cv.wait(lk, [w] { return w->has_job; });
+        job = std::move(w->job);
+        w->has_job = false;
+      }
+      job();
+      job = nullptr;
+      std::lock_guard<std::mutex> lk(m_);
+      idle_.push_back(w);
+    }
+  }
+  std::mutex m_;
+  std::vector<Worker*> idle_;
+  std::vector<std::unique_ptr<Worker>> all_;
+};
+
+// std::thread-like handle (start at construction, joinable(), join()) over the pool
+class WorkThread {
+ public:
+  WorkThread() = default;
+  template <class F>
+  explicit WorkThread(F&& f) {
+    static const bool pooled = [] {
+      const char* e = std::getenv("SVD1_THREAD_POOL");
+      return !(e && atoi(e) == 0);
+    }();
+    if (pooled) d_ = WorkerPool::get().submit(std::function<void()>(std::forward<F>(f)));
+    else t_ = std::thread(std::forward<F>(f));
+  }
+  WorkThread(WorkThread&&) = default;
+  WorkThread& operator=(WorkThread&& o) {
+    if (joinable()) std::terminate();  // as std::thread: never overwrite a running job
+    d_ = std::move(o.d_);
+    t_ = std::move(o.t_);
+    return *this;
+  }
+  ~WorkThread() {
+    if (joinable()) std::terminate();
+  }
+  bool joinable() const { return bool(d_) || t_.joinable(); }
+  void join() {
+    if (d_) {
+      std::unique_lock<std::mutex> lk(d_->m);
+      d_->cv.wait(lk, [this] { return d_->done; });
+      lk.unlock();
+      d_.reset();
+    }
+    if (t_.joinable()) t_.join();
+  }
+
+ private:
+  std::shared_ptr<WorkerPool::Done> d_;
+  std::thread t_;
+};
+
 struct StepRecord {
   int N = 0;                          // size of the eigenproblem (columns of the buffer)
   int na = 0;                         // active (secular) size
@@ -311,7 +426,7 @@ struct StepRecord {
   cudaEvent_t done_ev = nullptr;  // recorded after the read-back copy
   double plan_ms = 0.0;           // host time of the last apply_plan (diagnostics)
   bool pending = false;           // spectral work in flight (wait on done_ev)
-  std::thread plan_thread;            // apply_plan on a worker thread (plan-owned: it may
+  WorkThread plan_thread;             // apply_plan on a worker thread (plan-owned: it may
   std::atomic<bool> planned{false};   // outlive the update_impl call that started it)
   void join_plan() {
     if (plan_thread.joinable()) plan_thread.join();
@@ -392,7 +507,7 @@ struct svd1_plan_s {
   // batch mode: each side's remaining apply launches of the last update (its second apply
   // waits for its FMM plan) run on a launcher thread, so the next update's spectral chain
   // starts without waiting for them; joined before the side's next apply launch
-  std::thread launcher[2];
+  WorkThread launcher[2];
   svd1_status launcher_status[2] = {SVD1_OK, SVD1_OK};
   int launcher_parity[2] = {-1, -1};  // parity of the update whose launches they are
   cudaEvent_t rb_ev[2] = {};     // carried rows read back (U, V)
@@ -2007,8 +2122,8 @@ svd1_status secfmm_prepare(svd1_plan_t P, SecPlanHost& H, DevBuf& blob, DevBuf& 
 
 // joins its threads on scope exit (early error returns included)
 struct Joiner {
-  std::vector<std::thread> ts;
-  void add(std::thread&& t) { ts.push_back(std::move(t)); }
+  std::vector<WorkThread> ts;
+  void add(WorkThread&& t) { ts.push_back(std::move(t)); }
   void join() {
     for (auto& t : ts)
       if (t.joinable()) t.join();
@@ -3122,7 +3237,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     Se->join_plan();
     set_out_cols(*Se, rows, reverse);
     Se->planned.store(false, std::memory_order_relaxed);
-    Se->plan_thread = std::thread([Se, pcfg, pp] {
+    Se->plan_thread = WorkThread([Se, pcfg, pp] {
       apply_plan(pcfg, pp, *Se);
       Se->planned.store(true, std::memory_order_release);
     });
@@ -3364,7 +3479,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     st_u = chain(0);
     u_state = st_u == SVD1_OK ? 1 : 2;
   } else {
-    u_thread.add(std::thread([&] {
+    u_thread.add(WorkThread([&] {
       st_u = chain(0);
       u_state.store(st_u == SVD1_OK ? 1 : 2, std::memory_order_release);
       if (st_u == SVD1_OK) {
@@ -3408,7 +3523,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     if (!P->bdone[B->parity][0])
       SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][0], cudaEventDisableTiming));
     P->launcher_parity[0] = B->parity;
-    P->launcher[0] = std::thread([P, ju] {
+    P->launcher[0] = WorkThread([P, ju] {
       P->launcher_status[0] = side_job(P, ju);
       flush_launches(P);
     });
@@ -3580,7 +3695,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     if (!P->bdone[B->parity][1])
       SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][1], cudaEventDisableTiming));
     P->launcher_parity[1] = B->parity;
-    P->launcher[1] = std::thread([P, jv] {
+    P->launcher[1] = WorkThread([P, jv] {
       P->launcher_status[1] = side_job(P, jv);
       flush_launches(P);
     });
