@@ -289,11 +289,24 @@ class WorkerPool {
   struct Done {
     std::mutex m;
     std::condition_variable cv;
-    bool done = false;
+    std::atomic<bool> done{false};
   };
   static WorkerPool& get() {
     static WorkerPool* pool = new WorkerPool;  // never destroyed: idle workers outlive exit
     return *pool;
+  }
+  // spin up to kSpinUs before blocking on a condition variable: a job's start and its join
+  // are on the update's critical path, and a futex wake-up costs tens of microseconds
+  static constexpr int kSpinUs = 60;
+  template <class Pred>
+  static bool spin(Pred ready) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0;; ++i) {
+      if (ready()) return true;
+      if ((i & 63) == 63 &&
+          std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(kSpinUs))
+        return false;
+    }
   }
   std::shared_ptr<Done> submit(std::function<void()> f) {
     auto d = std::make_shared<Done>();
@@ -315,14 +328,19 @@ class WorkerPool {
         f();
         {
           std::lock_guard<std::mutex> l2(d->m);
-          d->done = true;
+          d->done.store(true, std::memory_order_release);
         }
         d->cv.notify_all();
       };
-      w->has_job = true;
+      w->has_job.store(true, std::memory_order_release);
     }
     w->cv.notify_one();
     return d;
+  }
+  static void wait(Done& d) {
+    if (spin([&d] { return d.done.load(std::memory_order_acquire); })) return;
+    std::unique_lock<std::mutex> lk(d.m);
+    d.cv.wait(lk, [&d] { return d.done.load(std::memory_order_acquire); });
   }
 
  private:
@@ -330,16 +348,17 @@ class WorkerPool {
     std::mutex m;
     std::condition_variable cv;
     std::function<void()> job;
-    bool has_job = false;
+    std::atomic<bool> has_job{false};
   };
   void loop(Worker* w) {
     for (;;) {
       std::function<void()> job;
+      spin([w] { return w->has_job.load(std::memory_order_acquire); });
       {
         std::unique_lock<std::mutex> lk(w->m);
-        w->cv.wait(lk, [w] { return w->has_job; });
+        w->cv.wait(lk, [w] { return w->has_job.load(std::memory_order_acquire); });
         job = std::move(w->job);
-        w->has_job = false;
+        w->has_job.store(false, std::memory_order_relaxed);
       }
       job();
       job = nullptr;
@@ -378,9 +397,7 @@ class WorkThread {
   bool joinable() const { return bool(d_) || t_.joinable(); }
   void join() {
     if (d_) {
-      std::unique_lock<std::mutex> lk(d_->m);
-      d_->cv.wait(lk, [this] { return d_->done; });
-      lk.unlock();
+      WorkerPool::wait(*d_);
       d_.reset();
     }
     if (t_.joinable()) t_.join();
