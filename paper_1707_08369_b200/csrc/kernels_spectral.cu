@@ -169,7 +169,12 @@ __global__ void __launch_bounds__(256) proj_dots_kernel(const double* __restrict
                                                        int64_t u_row0, const double* __restrict__ b,
                                                        int64_t v_rows, int64_t v_row0,
                                                        const double* __restrict__ probes,
-                                                       double* __restrict__ part) {
+                                                       double* __restrict__ part, int64_t lda = 0,
+                                                       int64_t ldb = 0) {
+  // blockIdx.y: the update (project_many: a_t = a + t lda, b_t = b + t ldb, its own partials)
+  a += int64_t(blockIdx.y) * lda;
+  b += int64_t(blockIdx.y) * ldb;
+  part += int64_t(blockIdx.y) * gridDim.x * 6;
   __shared__ double red[6][8];
   double acc[6] = {0, 0, 0, 0, 0, 0};
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -197,7 +202,11 @@ __global__ void __launch_bounds__(256) proj_dots_kernel(const double* __restrict
   }
 }
 
-__global__ void proj_dots_final(const double* __restrict__ part, int nblocks, double* __restrict__ out) {
+__global__ void proj_dots_final(const double* __restrict__ part, int nblocks, double* __restrict__ out,
+                                int64_t ldo = 0) {
+  // blockIdx.x: the update (its partials, its output at out + t ldo)
+  part += int64_t(blockIdx.x) * nblocks * 6;
+  out += int64_t(blockIdx.x) * ldo;
   if (threadIdx.x < 6) {
     double s = 0.0;
     for (int i = 0; i < nblocks; ++i) s += part[i * 6 + threadIdx.x];
@@ -1203,12 +1212,13 @@ inline unsigned blocks_for_warps(int64_t nwarps, int threads = 256) {
 
 // ------------------------------------------------------------------ wrappers
 constexpr int kDotBlocks = 64;
+constexpr int kMaxDotVecs = 32;  // project_many: the dots of up to this many updates in one launch
 
 int64_t project_partial_elems(int64_t u_rows, int64_t m, int64_t v_rows, int64_t n) {
   const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
   const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
   // (also enough for project_many's 8-vector passes)
-  return std::max(cu * 5 * m + cv * n, std::max(cu * 8 * m, cv * 8 * n)) + 6 * kDotBlocks;
+  return std::max(cu * 5 * m + cv * n, std::max(cu * 8 * m, cv * 8 * n)) + 6 * kDotBlocks * kMaxDotVecs;
 }
 
 svd1_status fill_probes(uint64_t seed, int64_t row0, int64_t rows, double* g, cudaStream_t st,
@@ -1255,6 +1265,28 @@ svd1_status project(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int
   proj_dots_kernel<<<kDotBlocks, 256, 0, st>>>(a, u_rows, u_row0, b, v_rows, v_row0, probes, part_d);
   proj_dots_final<<<1, 32, 0, st>>>(part_d, kDotBlocks, proj + 5 * m + n);
   *launches += 2;
+  SVD1_CUDA_TRY(cudaGetLastError());
+  return SVD1_OK;
+}
+
+// dst row (base - s) <- src row s for s = 1 .. count (the batch's carried rows are stored
+// newest-last: row 4 + (K - 1 - s) of the U side holds update s's x_a)
+__global__ void copy_rows_rev_kernel(double* __restrict__ dst, int64_t ldd, int64_t base,
+                                     const double* __restrict__ src, int64_t lds, int64_t cols, int count) {
+  const int s = 1 + int(blockIdx.y);
+  if (s > count) return;
+  const double* in = src + int64_t(s) * lds;
+  double* out = dst + (base - s) * ldd;
+  for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < cols; c += int64_t(gridDim.x) * blockDim.x)
+    out[c] = in[c];
+}
+
+svd1_status copy_rows_rev(double* dst, int64_t ldd, int64_t base, const double* src, int64_t lds, int64_t cols,
+                          int count, cudaStream_t st, int64_t* launches) {
+  if (count <= 0 || cols <= 0) return SVD1_OK;
+  copy_rows_rev_kernel<<<dim3(unsigned(std::min<int64_t>(16, (cols + 255) / 256)), unsigned(count)), 256, 0, st>>>(
+      dst, ldd, base, src, lds, cols, count);
+  *launches += 1;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }
@@ -1344,7 +1376,8 @@ svd1_status project_many(const double* U, int64_t ldu, int64_t u_rows, int64_t m
   if (K <= 0) return SVD1_OK;
   const int64_t cu = std::min<int64_t>(64, std::max<int64_t>(1, (u_rows + 31) / 32));
   const int64_t cv = std::min<int64_t>(64, std::max<int64_t>(1, (v_rows + 31) / 32));
-  if (std::max(cu * kMV * m, cv * kMV * n) + 6 * kDotBlocks > partial_cap) return SVD1_E_NOMEM;
+  if (K > kMaxDotVecs || std::max(cu * kMV * m, cv * kMV * n) + 6 * kDotBlocks * K > partial_cap)
+    return SVD1_E_NOMEM;
   const int rpc_u = int((u_rows + cu - 1) / cu), rpc_v = int((v_rows + cv - 1) / cv);
   for (int t0 = 0; t0 < K; t0 += kMV) {
     const int nv = std::min(kMV, K - t0);
@@ -1363,17 +1396,19 @@ svd1_status project_many(const double* U, int64_t ldu, int64_t u_rows, int64_t m
     *launches += 4;
   }
   double* part_d = part + std::max(cu * kMV * m, cv * kMV * n);
-  for (int t = 0; t < K; ++t) {  // the dots of every update (and zeros where nothing is projected)
+  for (int t = 0; t < K; ++t) {  // zeros where nothing is projected
     double* pt = proj + int64_t(t) * nproj;
     if (u_rows <= 0) SVD1_CUDA_TRY(cudaMemsetAsync(pt, 0, sizeof(double) * m, st));
     if (v_rows <= 0 || vcols < n)
       SVD1_CUDA_TRY(cudaMemsetAsync(pt + 5 * m + (v_rows > 0 ? vcols : 0), 0,
                                     sizeof(double) * (n - (v_rows > 0 ? vcols : 0)), st));
-    proj_dots_kernel<<<kDotBlocks, 256, 0, st>>>(A + int64_t(t) * lda, u_rows, u_row0, B + int64_t(t) * ldb,
-                                                 v_rows, v_row0, probes, part_d);
-    proj_dots_final<<<1, 32, 0, st>>>(part_d, kDotBlocks, pt + 5 * m + n);
-    *launches += 2;
   }
+  // the dots of every update: one launch each for the block partials and their sums (the
+  // same blocks and order as one update's, so bitwise the per-update values)
+  proj_dots_kernel<<<dim3(kDotBlocks, unsigned(K)), 256, 0, st>>>(A, u_rows, u_row0, B, v_rows, v_row0, probes,
+                                                                  part_d, lda, ldb);
+  proj_dots_final<<<unsigned(K), 32, 0, st>>>(part_d, kDotBlocks, proj + 5 * m + n, nproj);
+  *launches += 2;
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

@@ -510,6 +510,10 @@ struct svd1_plan_s {
   cudaStream_t st2 = nullptr;    // V-side applies run here, concurrently with the U side
   cudaStream_t sp[4] = {};       // batch mode: spectral + carried-row streams (U, V side),
                                  // then upload streams for the FMM plans (U, V side)
+  // svd1_update_batch: the projections of updates 1.. (project_many) run here while update
+  // 0's spectral phase runs; proj_ev marks them (and their copies) done
+  cudaStream_t st_proj = nullptr;
+  cudaEvent_t proj_ev = nullptr;
   cudaEvent_t sync_ev[4] = {};
   StepRecord steps[4];
   // batch mode (svd1_update_batch): step records per update parity (the
@@ -536,6 +540,7 @@ struct svd1_plan_s {
   std::vector<std::pair<std::string, double>> tl_host;
   double tl_t0 = 0.0;
   bool tl_on = false;
+  bool tl_pre = false;  // the timeline was started by svd1_update_batch's projections
   double* h_pin = nullptr;  // pinned staging for read-backs
   size_t h_pin_cap = 0;
   // pinned upload arenas, one per side stream (U side: st, V side: st2): every
@@ -616,10 +621,9 @@ cudaStream_t side_stream(svd1_plan_t P, int side) {
 // Wait for the uploads in flight and rewind the arenas (called at API entry points).
 svd1_status arena_reset(svd1_plan_t P, int side) {
   auto& A = P->arena[side];
-  for (auto& R : A.inflight) {
-    SVD1_CUDA_TRY(cudaEventSynchronize(R.ev));
-    A.pool.push_back(R.ev);
-  }
+  // the side's copies run in order on one stream: its newest region is the last to finish
+  if (!A.inflight.empty()) SVD1_CUDA_TRY(cudaEventSynchronize(A.inflight.back().ev));
+  for (auto& R : A.inflight) A.pool.push_back(R.ev);
   A.inflight.clear();
   A.pending = false;
   A.used = 0;
@@ -2898,6 +2902,11 @@ svd1_status svd1_plan_destroy(svd1_plan_t P) {
   }
   for (auto& q : P->sp)
     if (q) cudaStreamDestroy(q);
+  if (P->st_proj) {
+    cudaStreamSynchronize(P->st_proj);
+    cudaStreamDestroy(P->st_proj);
+  }
+  if (P->proj_ev) cudaEventDestroy(P->proj_ev);
   for (auto& cm : P->comm)
     if (cm) nccl_api().CommDestroy(cm);
   delete P;
@@ -2943,6 +2952,8 @@ struct BatchCtx {
   const double* gram = nullptr;
   int K = 0;
   int ru_next = -1, rv_next = -1;   // carried row index of the next update's a / b (-1: none)
+  cudaEvent_t rows_wait = nullptr;  // update 0 of svd1_update_batch: the carried rows' initial
+                                    // values (project_many) land after this event
 };
 
 // carried rows through one step's transform: Householder (in place on `in`), Cauchy
@@ -3298,6 +3309,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     const bool second = e == 1 || e == 3;  // R[0] -> R[1] (first step), R[1] -> R[0]
     double* rin = static_cast<double*>(R[second ? 1 : 0].p);
     double* rout = static_cast<double*>(R[second ? 0 : 1].p);
+    if (B->rows_wait) SVD1_CUDA_TRY(cudaStreamWaitEvent(ss, B->rows_wait, 0));
     if (thin && e == 2)  // the later b's coordinates along this update's q
       TRY(thin_carry(rows, rin, ld, m, B->y_dev, B->gram, B->t, B->K, beta_perp > 0.0 ? 1.0 / beta_perp : 0.0,
                      ss, LC(P)));
@@ -3828,6 +3840,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   if (rep) *rep = R;
   return SVD1_OK;
 }
+svd1_status batch_run(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                      const double* proj, const double* Bv, int64_t ldb, int64_t K, double eps,
+                      svd1_report* reps, const std::function<svd1_status()>& many);
 }  // namespace
 
 extern "C" {
@@ -3852,24 +3867,55 @@ svd1_status svd1_update_batch(svd1_plan_t P, double* U, int64_t ldu, double* sig
   // every update's STEP-1 projections against the initial factors
   const size_t nproj = size_t(5 * m + n + 6);
   double* pj;
+  // (a previous call that failed part-way may have left its project_many in flight)
+  if (P->st_proj) SVD1_CUDA_TRY(cudaStreamSynchronize(P->st_proj));
   TRY(P->bproj.get<double>(size_t(kMaxBatch) * nproj, &pj, P->st));
+  P->tl_on = std::getenv("SVD1_TIMELINE") != nullptr;
+  P->tl_t0 = now_ms();
+  P->tl_pre = P->tl_on;
+  tl_mark(P, "batch enter", P->st);
   // update 0 in full (its probe block too), updates 1.. with one pass over U and V per
   // 8 of them (only their x_a, y_b and dots are used: the probes are carried)
   TRY(svd1_project(P, U, ldu, V, ldv, A, Bv, pj));
+  tl_mark(P, "update 0 projected", P->st);
+  // updates 1.. on their own stream, alongside update 0's spectral phase: launched by
+  // batch_run once update 0's projection has been read back (its blocks would otherwise
+  // hold the SMs the plan stream's small copies need)
+  std::function<svd1_status()> many;
   if (K > 1) {
     double* part;
     const int64_t need = project_partial_elems(c.u_rows, m, c.v_rows, n);
     TRY(P->partial.get<double>(size_t(need), &part, P->st));
-    TRY(project_many(U, ldu, c.u_rows, m, c.u_row0, V, ldv, c.v_rows, n, c.v_row0, thin ? m : n, A + lda, lda,
-                     Bv + ldb, ldb, int(K) - 1, static_cast<double*>(P->probes.p), part, need, pj + nproj,
-                     int64_t(nproj), P->st, LC(P)));
+    if (!P->st_proj) SVD1_CUDA_TRY(cudaStreamCreateWithFlags(&P->st_proj, cudaStreamNonBlocking));
+    if (!P->proj_ev) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->proj_ev, cudaEventDisableTiming));
+    many = [=]() -> svd1_status {
+      TRY(project_many(U, ldu, c.u_rows, m, c.u_row0, V, ldv, c.v_rows, n, c.v_row0, thin ? m : n, A + lda, lda,
+                       Bv + ldb, ldb, int(K) - 1, static_cast<double*>(P->probes.p), part, need, pj + nproj,
+                       int64_t(nproj), P->st_proj, LC(P)));
+      tl_mark(P, "projections queued", P->st_proj);
+      return SVD1_OK;
+    };
   }
-  return svd1_update_batch_projected(P, U, ldu, sigma, V, ldv, pj, Bv, ldb, K, eps, reps);
+  return batch_run(P, U, ldu, sigma, V, ldv, pj, Bv, ldb, K, eps, reps, many);
 }
 
 svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V,
                                         int64_t ldv, const double* proj, const double* Bv, int64_t ldb,
                                         int64_t K, double eps, svd1_report* reps) {
+  return batch_run(P, U, ldu, sigma, V, ldv, proj, Bv, ldb, K, eps, reps, nullptr);
+}
+}  // extern "C"
+
+namespace {
+// The pipelined stream.  many (svd1_update_batch): launches the
+// projections of updates 1..K-1 on st_proj; only update 0's are complete in stream order
+// on the plan stream.  Their results are needed by update 0's carried-row transforms and
+// the dots by update 1; every apply waits for them (they read the initial factors).
+svd1_status batch_run(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+                      const double* proj, const double* Bv, int64_t ldb, int64_t K, double eps,
+                      svd1_report* reps, const std::function<svd1_status()>& many) {
+  const bool deferred = bool(many);
+
   if (!P || !sigma || (K > 0 && !proj) || K < 0 || K > kMaxBatch) return SVD1_E_INVALID;
   const svd1_config& c = P->cfg;
   const int64_t m = c.m, n = c.n;
@@ -3886,7 +3932,9 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   if ((c.u_rows && (!U || ldu < m)) || (c.v_rows && (!V || ldv < nv))) return SVD1_E_INVALID;
   if (K == 0) return SVD1_OK;
   const int k = int(K);
+  tl_mark(P, "batch_run", nullptr, false);
   TRY(arena_reset(P));
+  tl_mark(P, "arenas reset", nullptr, false);
   TRY(ensure_st2(P));
   TRY(ensure_side(P, 2));
   TRY(ensure_side(P, 3));
@@ -3905,13 +3953,16 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   double* scr;  // few-rows scratch at its largest
   TRY(P->few_scr[0].get<double>(size_t(few_rows_scratch_elems(ru_max, int(m))), &scr, P->st));
   TRY(P->few_scr[1].get<double>(size_t(few_rows_scratch_elems(rv_max, int(nv))), &scr, P->st));
+  // (deferred: the rows of updates 1.. are copied on st_proj after project_many; the
+  // buffers above are ordered on P->st, which st_proj joins first)
+  const cudaStream_t qs = deferred ? P->st_proj : P->st;
   SVD1_CUDA_TRY(cudaMemcpyAsync(ru0, pj + m, 4 * m * sizeof(double), cudaMemcpyDeviceToDevice, P->st));
-  for (int s = 1; s < k; ++s) {
-    SVD1_CUDA_TRY(cudaMemcpyAsync(ru0 + int64_t(4 + (k - 1 - s)) * m, pj + size_t(s) * nproj, m * sizeof(double),
-                                  cudaMemcpyDeviceToDevice, P->st));
-    SVD1_CUDA_TRY(cudaMemcpyAsync(rv0 + int64_t(k - 1 - s) * nv, pj + size_t(s) * nproj + 5 * m,
-                                  (thin ? m : n) * sizeof(double), cudaMemcpyDeviceToDevice, P->st));
-  }
+  auto carried_copies = [&]() -> svd1_status {  // the later updates' x_a, y_b as carried rows
+    TRY(copy_rows_rev(ru0, m, 4 + (k - 1), pj, int64_t(nproj), m, k - 1, qs, LC(P)));
+    TRY(copy_rows_rev(rv0, nv, k - 1, pj + 5 * m, int64_t(nproj), thin ? m : n, k - 1, qs, LC(P)));
+    return SVD1_OK;
+  };
+  if (!deferred) TRY(carried_copies());
   double* gram = nullptr;  // thin: b_t . b_s
   if (thin) {
     TRY(P->bgram.get<double>(size_t(kMaxBatch) * kMaxBatch, &gram, P->st));
@@ -3920,21 +3971,33 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   // host copies of the projections (dots of every update; x's of update 0) and sigma
   double* h;
   TRY(pinned(P, size_t(kMaxBatch) * nproj + size_t(m) + size_t(5 * m + n), &h));
-  SVD1_CUDA_TRY(cudaMemcpyAsync(h, pj, size_t(k) * nproj * sizeof(double), cudaMemcpyDeviceToHost, P->st));
+  SVD1_CUDA_TRY(cudaMemcpyAsync(h, pj, size_t(deferred ? 1 : k) * nproj * sizeof(double), cudaMemcpyDeviceToHost,
+                                P->st));
   SVD1_CUDA_TRY(cudaMemcpyAsync(h + size_t(k) * nproj, sigma, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost,
                                 P->st));
+  tl_mark(P, "read-backs queued", P->st);
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));  // also orders the copies before the V stream
+  tl_mark(P, "read-backs done", nullptr, false);
+  if (deferred) {  // (after the plan stream's read-backs: copy queues are in order)
+    TRY(many());
+    TRY(carried_copies());
+    SVD1_CUDA_TRY(cudaEventRecord(P->proj_ev, qs));
+  }
+  if (deferred)  // no apply writes U or V before project_many has read them
+    for (cudaStream_t q : {P->st, P->st2}) SVD1_CUDA_TRY(cudaStreamWaitEvent(q, P->proj_ev, 0));
   double* hn = h + size_t(k) * nproj + m;  // next update's x_a | x_g | y_b (read back)
   std::memset(hn, 0, size_t(5 * m + n) * sizeof(double));  // (thin: y_b past m stays 0)
   std::vector<double> sig(h + size_t(k) * nproj, h + size_t(k) * nproj + m);
   std::vector<double> hp(h, h + nproj);
   svd1_status st = SVD1_OK;
   P->tl_on = std::getenv("SVD1_TIMELINE") != nullptr;
-  P->tl_t0 = now_ms();
+  if (!P->tl_pre) P->tl_t0 = now_ms();  // (svd1_update_batch marked its projections)
+  P->tl_pre = false;
   tl_mark(P, "batch start", P->st);
   const bool launched_by_launchers = (c.flags & SVD1_FUSED_SIDE) == 0;  // (see update_impl)
   int pending = -1;  // the update whose launchers are in flight (its report still to complete)
   for (int t = 0; t < k && st == SVD1_OK; ++t) {
+    if (t == 1 && deferred) SVD1_CUDA_TRY(cudaStreamSynchronize(qs));  // the later updates' dots
     if (t > 0) {  // x's from the carried rows, dots from update t's projection
       std::memcpy(hp.data(), hn, size_t(5 * m + n) * sizeof(double));
       std::memcpy(hp.data() + 5 * m + n, h + size_t(t) * nproj + 5 * m + n, 6 * sizeof(double));
@@ -3949,6 +4012,7 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
     b.ru_next = t + 1 < k ? 4 + (k - 2 - t) : -1;
     b.rv_next = t + 1 < k ? k - 2 - t : -1;
     b.h_next = hn;
+    b.rows_wait = (deferred && t == 0) ? P->proj_ev : nullptr;
     b.prev_win = (reps && t >= 2) ? &reps[t - 2].t_ms[5] : nullptr;
     b.prev_gemm = (reps && t >= 2) ? reps[t - 2].gemm_ms : nullptr;
     if (thin) {
@@ -3960,6 +4024,10 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
     svd1_report R;
     st = update_impl(P, U, ldu, sigma, V, ldv, nullptr, eps, &R, &b);
     if (reps) reps[t] = R;
+    if (t == 0 && deferred && k > 1)  // the 6 dots of updates 1.. (project_many is long done)
+      SVD1_CUDA_TRY(cudaMemcpy2DAsync(h + nproj + 5 * m + n, nproj * sizeof(double), pj + nproj + 5 * m + n,
+                                      nproj * sizeof(double), 6 * sizeof(double), size_t(k - 1),
+                                      cudaMemcpyDeviceToHost, qs));
     if (launched_by_launchers && st == SVD1_OK && !R.noop) {
       // update t joined the launchers of the previous such update before its own applies:
       // that update's plans are complete, its apply statistics can be reported
@@ -3990,7 +4058,7 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
     TRY(bspan_record(P, 3, P->st2));
   }
   // drain every stream; the factors now hold updates 0..t; sigma of the last success
-  for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1], P->sp[2], P->sp[3]})
+  for (cudaStream_t q : {P->st, P->st2, P->sp[0], P->sp[1], P->sp[2], P->sp[3], P->st_proj})
     if (q || q == P->st) SVD1_CUDA_TRY(cudaStreamSynchronize(q));
   if (P->tl_on) {  // host stamps and device times (ms from the batch start)
     cudaEvent_t base = P->tl_dev.empty() ? nullptr : P->tl_dev.front().second;
@@ -4022,6 +4090,9 @@ svd1_status svd1_update_batch_projected(svd1_plan_t P, double* U, int64_t ldu, d
   SVD1_CUDA_TRY(cudaStreamSynchronize(P->st));
   return st;
 }
+}  // namespace
+
+extern "C" {
 
 svd1_status svd1_update(svd1_plan_t P, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
                         const double* a, const double* b, double eps, svd1_report* rep) {

@@ -39,6 +39,9 @@ __host__ __device__ inline uint64_t splitmix64(uint64_t x) {
 // the projections of K updates (a_t at A + t*lda, b_t at B + t*ldb) against the same
 // factors into proj + t*nproj (svd1_project's layout; the probe block is NOT written):
 // one pass over U (and V) per 8 updates
+// dst row (base - s) <- src row s, s = 1 .. count, cols doubles each (batch carried rows)
+svd1_status copy_rows_rev(double* dst, int64_t ldd, int64_t base, const double* src, int64_t lds, int64_t cols,
+                          int count, cudaStream_t st, int64_t* launches);
 svd1_status project_many(const double* U, int64_t ldu, int64_t u_rows, int64_t m, int64_t u_row0,
                          const double* V, int64_t ldv, int64_t v_rows, int64_t n, int64_t v_row0, int64_t vcols,
                          const double* A, int64_t lda, const double* B, int64_t ldb, int K, const double* probes,
