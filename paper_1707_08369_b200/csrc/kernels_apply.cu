@@ -441,12 +441,20 @@ __device__ __forceinline__ double2 lds128(const unsigned char* p) {
 #ifndef SVD1_CW32
 #define SVD1_CW32 4  // consumer warps of the 32-wide passes (experiments)
 #endif
+#ifndef SVD1_MT16
+#define SVD1_MT16 4  // 8-row m-tiles per consumer warp of the 16-wide passes (experiments)
+#endif
+#ifndef SVD1_MT32
+#define SVD1_MT32 4  // the same for the 32-wide passes
+#endif
 template <int BN>
 struct GemmCfg {
-  static constexpr int CW = BN <= 16 ? SVD1_CW16 : SVD1_CW32;  // consumer warps (32 rows each)
+  static constexpr int CW = BN <= 16 ? SVD1_CW16 : SVD1_CW32;  // consumer warps (RW rows each)
+  static constexpr int MT = BN <= 16 ? SVD1_MT16 : SVD1_MT32;  // 8-row m-tiles per consumer warp
+  static constexpr int RW = 8 * MT;
   static constexpr int NTHR = 32 * (CW + 1); // + one producer warp
   static constexpr int NT = BN / 8;
-  static constexpr int BM = 32 * CW;
+  static constexpr int BM = RW * CW;
   static constexpr int STAGES = BN <= 16 ? SVD1_STAGES16 : SVD1_STAGES32;
   static constexpr int A_BYTES = BM * KC * 8;
   static constexpr int B_BYTES = BN * KC * 8;
@@ -590,17 +598,18 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
     if (lane == 0) mbar_arrive(&full[stage]);  // 33 arrivals per phase
     return;
   }
-  // ------------------------------------ consumers: warp owns rows warp*32 .. +31
+  // ------------------------------------ consumers: warp owns rows warp*RW .. +RW-1
   const int g = lane >> 2, t4 = lane & 3;
   // byte offsets (within a stage) of this lane's 16-byte fragment runs: row r, k pair j
   // sits at r*128 + ((j ^ (r & 7)) << 4) (TMA SWIZZLE_128B); r & 7 == g for every row
   // this lane reads (fragment rows are 8-aligned)
   const int sw0 = ((2 * t4) ^ g) << 4, sw1 = ((2 * t4 + 1) ^ g) << 4;
-  const int a_row = (warp * 32 + g) * 128;
+  constexpr int MT = G::MT, RW = G::RW;
+  const int a_row = (warp * RW + g) * 128;
   const int b_row = g * 128;
-  double acc[4][NT][2];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
+  for (int x = 0; x < MT; ++x)
 #pragma unroll
     for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   int stage = 0;
@@ -630,19 +639,19 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // k-steps q = 2h, 2h + 1
       const int sw = h ? sw1 : sw0;
-      double2 af[4], bf[NT];
+      double2 af[MT], bf[NT];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = lds128(a + mt * 8 * 128 + sw);
+      for (int mt = 0; mt < MT; ++mt) af[mt] = lds128(a + mt * 8 * 128 + sw);
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) bf[nt] = lds128(b + nt * 8 * 128 + sw);
       // every accumulator's first k-step, then every accumulator's second: 4 NT
       // independent DMMAs between two that share an accumulator
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt].x, bf[nt].x);
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt].y, bf[nt].y);
     }
@@ -666,8 +675,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
         if (out_kind == IO_U) {
           const int c0 = dcol[nt][0], c1 = dcol[nt][1];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
-            const int64_t r = row0 + warp * 32 + mt * 8 + g;
+          for (int mt = 0; mt < MT; ++mt) {
+            const int64_t r = row0 + warp * RW + mt * 8 + g;
             if (r >= rows) continue;
 #ifdef SVD1_BOUNDS
             if (c0 < 0 || c0 >= out_cols || c1 >= out_cols) {
@@ -681,8 +690,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
           }
         } else {  // expansions: N is a multiple of 4, col0 even -> 16-byte stores
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt) {
-            const int64_t r = row0 + warp * 32 + mt * 8 + g;
+          for (int mt = 0; mt < MT; ++mt) {
+            const int64_t r = row0 + warp * RW + mt * 8 + g;
             if (r >= rows) continue;
 #ifdef SVD1_BOUNDS
             if (col + 1 >= ldE || r * ldE + col + 1 >= exp_elems) {
@@ -696,7 +705,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
         }
       }
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < MT; ++x)
 #pragma unroll
         for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
     }
@@ -954,9 +963,18 @@ svd1_status make_tmap(CUtensorMap* map, const double* base, int64_t inner, int64
   const cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
   const cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
   const cuuint32_t estr[2] = {1, 1};
+  // L2 promotion of the box's 128-byte rows (experiments: SVD1_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B)
+  static const int promo = [] {
+    const char* e = std::getenv("SVD1_L2PROMO");
+    return e ? std::atoi(e) : 0;
+  }();
+  const CUtensorMapL2promotion pr = promo == 1   ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                    : promo == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_NONE;
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? SVD1_OK : SVD1_E_INVALID;
 }
 
