@@ -11,5 +11,5 @@ from .svd1_oracle import (  # noqa: F401
     EPS, schur_sym_2x2, schur_update_2x2, prepare_update, deflate, secular_w,
     secular_roots_bisect, loewner_zhat, cauchy_X, cauchy_apply_explicit,
     rank_one_update, svd_update, paper_error, orth_defect, column_residual,
-    sym_rank_one_eig, DeflationResult,
+    sym_rank_one_eig, DeflationResult, balance_factor,
 )

@@ -384,6 +384,24 @@ def sym_rank_one_eig(U, D, a1, rho):
 
 
 # --------------------------------------------------------------- Alg 6.1
+def balance_factor(x_norm, y_norm):
+    """Reading D9: c = 2^floor(e / 2) where x_norm / y_norm = f 2^e,
+    f in [0.5, 1) -- a power of two with c^2 within a factor of 4 of x_norm / y_norm (1 if
+    either norm is 0 or not finite).  Alg 6.1 splits a side's symmetric update through the
+    2x2 Schur form of [[beta, 1], [1, 0]], which is not invariant under the exact
+    rewriting a b^T = (c a)(b / c)^T: with ||a|| >> ||A b|| the two eigen-updates
+    rho1 a1 a1^T + rho2 b1 b1^T cancel to eps ||a||^2 (not eps ||a|| ||A b||).  Each side
+    takes its own c so that its two vectors have comparable norms; a power of two keeps the
+    rescaled vectors exact, and e (from the two norms' exponents) shifts by exactly 2t when
+    the inputs are (2^t a, b / 2^t), so such inputs give bitwise the same result."""
+    if not (x_norm > 0.0 and y_norm > 0.0 and math.isfinite(x_norm) and math.isfinite(y_norm)):
+        return 1.0
+    mx, ex = math.frexp(x_norm)
+    my, ey = math.frexp(y_norm)
+    _, e2 = math.frexp(mx / my)
+    return math.ldexp(1.0, (ex - ey + e2) // 2)
+
+
 def svd_update(U, sigma, V, a, b, sign_rule="explicit", probes=None, rows=None):
     """Alg 6.1 "Update SVD of rank-1 modified matrix using FMM",
     O1-O8, with the explicit product in place of the FMM.
@@ -421,11 +439,19 @@ def svd_update(U, sigma, V, a, b, sign_rule="explicit", probes=None, rows=None):
         alpha, beta = float(a @ a), float(b @ b)
     Du = sigma * sigma
     Dv = np.concatenate([Du, np.zeros(n - m)])
-    # STEPS 2-3 (P:339-340), Q2: right-side eigenvalues are rho3, rho4
-    rho1, rho2, Qu = schur_update_2x2(beta)
-    rho3, rho4, Qv = schur_update_2x2(alpha)
     xa = U.T @ a                       # U^T a
     yb = V.T @ b                       # V^T b
+    # D9: per-side balance of the rank-1 term before the Schur split (exact rewriting):
+    # U side [c_u a, b~ / c_u] with beta / c_u^2, V side [b / c_v, c_v a~] with alpha c_v^2
+    if not large:
+        c_u = balance_factor(float(np.linalg.norm(b_tilde)), math.sqrt(alpha))
+        c_v = balance_factor(math.sqrt(beta), float(np.linalg.norm(a_tilde)))
+    else:                              # ||b~|| = ||Sigma V^T b||, ||a~|| = ||Sigma^T U^T a|| (B7)
+        c_u = balance_factor(float(np.linalg.norm(sigma * yb[:m])), math.sqrt(alpha))
+        c_v = balance_factor(math.sqrt(beta), float(np.linalg.norm(sigma * xa)))
+    # STEPS 2-3 (P:339-340), Q2: right-side eigenvalues are rho3, rho4
+    rho1, rho2, Qu = schur_update_2x2(beta / (c_u * c_u))
+    rho3, rho4, Qv = schur_update_2x2(alpha * (c_v * c_v))
     if probes is None:
         probes = np.random.default_rng(12345).standard_normal((4, m))
     probes = np.asarray(probes, np.float64)
@@ -436,10 +462,12 @@ def svd_update(U, sigma, V, a, b, sign_rule="explicit", probes=None, rows=None):
         carry_v = [np.concatenate([sigma * x, np.zeros(n - m)]) + yb * float(a @ g)
                    for x, g in zip(xg, probes)]
     if not large:
-        a1 = Qu[0, 0] * a + Qu[1, 0] * b_tilde       # [a b~] Q_u = [a1 b1]
-        b1 = Qu[0, 1] * a + Qu[1, 1] * b_tilde
-        a2 = Qv[0, 0] * b + Qv[1, 0] * a_tilde       # [b a~] Q_v = [a2 b2]
-        b2 = Qv[0, 1] * b + Qv[1, 1] * a_tilde
+        au, btu = c_u * a, b_tilde / c_u              # D9
+        bv, atv = b / c_v, c_v * a_tilde
+        a1 = Qu[0, 0] * au + Qu[1, 0] * btu          # [a b~] Q_u = [a1 b1]
+        b1 = Qu[0, 1] * au + Qu[1, 1] * btu
+        a2 = Qv[0, 0] * bv + Qv[1, 0] * atv          # [b a~] Q_v = [a2 b2]
+        b2 = Qv[0, 1] * bv + Qv[1, 1] * atv
         # STEP 4, STEP 5 (Q3 reads "(U~, b1, D~, rho2)")
         Ut, Dt, cu, i1 = rank_one_update(U, Du, rho1, a1=a1, carry=carry_u)
         Uh, Dh, cu, i2 = rank_one_update(Ut, Dt, rho2, a1=b1, carry=cu)
@@ -448,12 +476,14 @@ def svd_update(U, sigma, V, a, b, sign_rule="explicit", probes=None, rows=None):
         Vh, Dvh, cv, i4 = rank_one_update(Vt, Dvt, rho4, a1=b2, carry=cv)
     else:
         ru, rv = rows
-        sx = sigma * yb[:m]                           # U^T b~ = Sigma V^T b (B7)
-        z1 = Qu[0, 0] * xa + Qu[1, 0] * sx
-        w1 = Qu[0, 1] * xa + Qu[1, 1] * sx
-        sxa = np.concatenate([sigma * xa, np.zeros(n - m)])   # V^T a~ = Sigma^T U^T a
-        z3 = Qv[0, 0] * yb + Qv[1, 0] * sxa
-        w3 = Qv[0, 1] * yb + Qv[1, 1] * sxa
+        sx = sigma * yb[:m] / c_u                     # U^T b~ = Sigma V^T b (B7), D9
+        xu = c_u * xa
+        z1 = Qu[0, 0] * xu + Qu[1, 0] * sx
+        w1 = Qu[0, 1] * xu + Qu[1, 1] * sx
+        sxa = c_v * np.concatenate([sigma * xa, np.zeros(n - m)])   # V^T a~ = Sigma^T U^T a
+        ybv = yb / c_v
+        z3 = Qv[0, 0] * ybv + Qv[1, 0] * sxa
+        w3 = Qv[0, 1] * ybv + Qv[1, 1] * sxa
         Ut, Dt, cu, i1 = rank_one_update(U[ru], Du, rho1, z=z1, carry=[w1] + list(carry_u))
         Uh, Dh, cu, i2 = rank_one_update(Ut, Dt, rho2, z=cu[0], carry=cu[1:])
         Vt, Dvt, cv, i3 = rank_one_update(V[rv], Dv, rho3, z=z3, carry=[w3] + list(carry_v))

@@ -208,6 +208,38 @@ __global__ void col_rotate_kernel(int64_t rows, double* __restrict__ U, int64_t 
   for (int b = 0; b < k; ++b) U[r * ld + cols[o0 + b]] = o[b];
 }
 
+// The same rotation for groups of more than 8 columns (D5 clusters paired from the tracked
+// coordinates, up to 256 columns): a block per 8 rows and group, the rows' k values staged in
+// shared memory before any is overwritten.
+constexpr int kRotRows = 8;
+__global__ void __launch_bounds__(256) col_rotate_big_kernel(int64_t rows, double* __restrict__ U, int64_t ld,
+                                                             const int32_t* __restrict__ goff,
+                                                             const int32_t* __restrict__ cols,
+                                                             const double* __restrict__ mats) {
+  extern __shared__ double s_v[];  // [kRotRows][k]
+  const int g = blockIdx.y;
+  const int o0 = goff[g], k = goff[g + 1] - o0;
+  if (k <= 8) return;
+  int64_t moff = 0;
+  for (int h = 0; h < g; ++h) {
+    const int kh = goff[h + 1] - goff[h];
+    moff += int64_t(kh) * kh;
+  }
+  const int64_t r0 = int64_t(blockIdx.x) * kRotRows;
+  for (int e = threadIdx.x; e < kRotRows * k; e += blockDim.x) {
+    const int rr = e / k, a = e % k;
+    s_v[e] = r0 + rr < rows ? U[(r0 + rr) * ld + cols[o0 + a]] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kRotRows * k; e += blockDim.x) {
+    const int rr = e / k, b = e % k;
+    if (r0 + rr >= rows) continue;
+    double acc = 0.0;
+    for (int a = 0; a < k; ++a) acc = fma(s_v[rr * k + a], mats[moff + int64_t(a) * k + b], acc);
+    U[(r0 + rr) * ld + cols[o0 + b]] = acc;
+  }
+}
+
 __global__ void passthrough_kernel(int64_t rows, int nq, const double* __restrict__ U_in,
                                    int64_t ld_in, const int32_t* __restrict__ src,
                                    double* __restrict__ U_out, int64_t ld_out,
@@ -905,11 +937,17 @@ svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,
 }
 
 svd1_status col_rotate(int64_t rows, double* U, int64_t ld, int ngroups, const int32_t* goff,
-                       const int32_t* cols, const double* mats, cudaStream_t st, int64_t* launches) {
+                       const int32_t* cols, const double* mats, cudaStream_t st, int64_t* launches, int max_k) {
   if (rows <= 0 || ngroups <= 0) return SVD1_OK;
   dim3 grid(unsigned((rows + 255) / 256), unsigned(ngroups));
   col_rotate_kernel<<<grid, 256, 0, st>>>(rows, U, ld, goff, cols, mats);
   *launches += 1;
+  if (max_k > 8) {  // groups beyond the register kernel's 8 columns
+    if (max_k > 256) return SVD1_E_INVALID;
+    dim3 gb(unsigned((rows + kRotRows - 1) / kRotRows), unsigned(ngroups));
+    col_rotate_big_kernel<<<gb, 256, size_t(kRotRows) * max_k * sizeof(double), st>>>(rows, U, ld, goff, cols, mats);
+    *launches += 1;
+  }
   SVD1_CUDA_TRY(cudaGetLastError());
   return SVD1_OK;
 }

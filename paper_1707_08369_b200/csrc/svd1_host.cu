@@ -128,6 +128,7 @@ svd1_status pinned_reserve(void** buf, size_t* cap, size_t bytes) {
   return SVD1_OK;
 }
 
+constexpr int kMaxPairTracked = 256;  // D5: repeated-sigma columns tracked for clusters beyond the probes
 constexpr int kMaxBatch = 28;  // svd1_update_batch: buffers are sized for this many updates per call
 
 // ---- NCCL, opened at run time (no link-time dependency; in a process that already
@@ -209,6 +210,21 @@ Split schur_split(double beta) {
   s.q01 = -1.0 / h;
   s.q11 = s.rho1 / h;
   return s;
+}
+
+// Reading D9 (oracle balance_factor): c = 2^floor(e / 2) with
+// x / y = f 2^e, f in [0.5, 1); 1 if either norm is 0 or not finite.  A side's Schur split
+// takes the rank-1 term as (c a)(b / c)^T with its two vectors' norms within a
+// factor of 2 of each other: [[beta, 1], [1, 0]] is not invariant under that exact rewriting,
+// and with ||a|| >> ||A b|| its two eigen-updates cancel to eps ||a||^2.  A power of two
+// keeps the rescaled vectors exact and makes (2^t a, b / 2^t) give bitwise the same update.
+double balance_factor(double x, double y) {
+  if (!(x > 0.0 && y > 0.0 && std::isfinite(x) && std::isfinite(y))) return 1.0;
+  int ex = 0, ey = 0, e2 = 0;
+  const double mx = std::frexp(x, &ex), my = std::frexp(y, &ey);
+  std::frexp(mx / my, &e2);
+  const int e = ex - ey + e2;
+  return std::ldexp(1.0, e >= 0 ? e / 2 : -((1 - e) / 2));  // floor(e / 2)
 }
 
 struct FmmHost {
@@ -438,6 +454,11 @@ struct StepRecord {
   std::vector<std::vector<double>> cs_sorted;
   std::vector<double> Dn;              // next eigenvalues / carries (recycled storage)
   std::vector<std::vector<double>> cn;
+  // host-only carries (D5, clusters larger than the probes): the coordinates of a repeated
+  // singular value's original columns in this step's basis, through the deflation
+  // reflections and the merge only (their active entries are not needed: set to 0)
+  std::vector<std::vector<double>>* gcar = nullptr;
+  std::vector<std::vector<double>> gs_sorted, gn;
   double* rb = nullptr;  // pinned read-back
   size_t rb_cap = 0;
   cudaEvent_t done_ev = nullptr;  // recorded after the read-back copy
@@ -2234,6 +2255,12 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
     const double* srcq = carries[q].data();
     for (int s = 0; s < N; ++s) dstq[s] = srcq[perm[s]];
   }
+  const int ng = S.gcar ? int(S.gcar->size()) : 0;
+  S.gs_sorted.resize(ng);
+  for (int q = 0; q < ng; ++q) {
+    S.gs_sorted[q].resize(N);
+    for (int s = 0; s < N; ++s) S.gs_sorted[q][s] = (*S.gcar)[q][perm[s]];
+  }
   // deflation (DESIGN.md §3.2 D1): (i) zero weights, (iii) exact repeats
   double zn2 = 0.0;
   for (double v : zs) zn2 += v * v;
@@ -2274,6 +2301,12 @@ svd1_status spectral_launch(svd1_plan_t P, StepRecord& S, const std::vector<doub
           for (size_t q = t; q <= u; ++q) dot += v[q - t] * cs_sorted[qq][surv[q]];
           const double f = 2.0 * dot / vv;
           for (size_t q = t; q <= u; ++q) cs_sorted[qq][surv[q]] -= f * v[q - t];
+        }
+        for (int qq = 0; qq < ng; ++qq) {
+          double dot = 0.0;
+          for (size_t q = t; q <= u; ++q) dot += v[q - t] * S.gs_sorted[qq][surv[q]];
+          const double f = 2.0 * dot / vv;
+          for (size_t q = t; q <= u; ++q) S.gs_sorted[qq][surv[q]] -= f * v[q - t];
         }
         for (size_t q = t; q < u; ++q) {
           zs[surv[q]] = 0.0;
@@ -2512,6 +2545,15 @@ svd1_status spectral_finish(svd1_plan_t P, StepRecord& S, std::vector<double>& D
   }
   D.swap(Dn);
   carries.swap(cn);
+  if (S.gcar) {  // host-only carries: deflated entries move with their columns, active ones 0
+    const int ng = int(S.gcar->size());
+    S.gn.resize(ng);
+    for (int qq = 0; qq < ng; ++qq) {
+      S.gn[qq].resize(N);
+      for (int q = 0; q < N; ++q) S.gn[qq][q] = items[q].flag == 0 ? S.gs_sorted[qq][items[q].pos] : 0.0;
+    }
+    S.gcar->swap(S.gn);
+  }
   return SVD1_OK;
 }
 
@@ -2715,7 +2757,7 @@ svd1_status reserve_step(StepRecord& S, int64_t N, int p, int G) {
   TRY(S.sec_scr.reserve<double>(size_t(3) * size_t(N + 64) * kSecP));
   TRY(S.rot_goff.reserve<int32_t>(size_t(N / 2 + 2)));
   TRY(S.rot_cols.reserve<int32_t>(size_t(N + 1)));
-  TRY(S.rot_mats.reserve<double>(size_t(N) * kNumProbes + 16));
+  TRY(S.rot_mats.reserve<double>(size_t(N) * kNumProbes + size_t(kMaxPairTracked) * kMaxPairTracked + 16));
   return SVD1_OK;
 }
 
@@ -3026,6 +3068,7 @@ struct SideJob {
   const double *b_dev = nullptr, *y_dev = nullptr;
   double inv_beta = 0.0;
   int nrot = 0;  // V: pairing rotation groups of this update
+  int rot_maxk = 0;  // and the largest group's size
   std::string ut;
 };
 svd1_status side_job(svd1_plan_t P, const SideJob& J) {
@@ -3046,7 +3089,8 @@ svd1_status side_job(svd1_plan_t P, const SideJob& J) {
   TRY(apply_launch(P, S[e2], J.W, J.ldw, J.X, J.ldx, 2 * e2, J.st, J.side));
   if (J.side && J.nrot > 0)
     TRY(col_rotate(S[3].rows, J.X, J.ldx, J.nrot, static_cast<int32_t*>(S[3].rot_goff.p),
-                   static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), J.st, LC(P)));
+                   static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), J.st, LC(P),
+                   J.rot_maxk));
   tl_mark(P, J.ut + (J.side ? "V2 end" : "U2 end"), J.st);
   TRY(bwin_record(P, J.parity, 2 + J.side, J.st));
   SVD1_CUDA_TRY(cudaEventRecord(P->bdone[J.parity][J.side], J.st));  // (created by update_impl)
@@ -3153,7 +3197,15 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     return SVD1_OK;
   }
   // ---- STEPS 2-3: Schur splits; Q2: right side uses rho3, rho4
-  const Split su = schur_split(beta), sv = schur_split(alpha);
+  // D9: per-side balance of the rank-1 term, ||b~|| = ||Sigma V^T b||, ||a~|| = ||Sigma^T U^T a||
+  double bt2 = 0.0, at2 = 0.0;
+  for (int64_t i = 0; i < m; ++i) {
+    bt2 += (sig[i] * yb[i]) * (sig[i] * yb[i]);
+    at2 += (sig[i] * xa[i]) * (sig[i] * xa[i]);
+  }
+  const double c_u = balance_factor(std::sqrt(bt2), std::sqrt(alpha));
+  const double c_v = balance_factor(std::sqrt(beta), std::sqrt(at2));
+  const Split su = schur_split(beta / (c_u * c_u)), sv = schur_split(alpha * (c_v * c_v));
   // small vectors in the U and V column bases (B7 identities):
   // U^T b~ = Sigma (V^T b)[:m],  V^T a~ = Sigma^T (U^T a)
   std::vector<double> z1(m), Du(m), z3(nv), Dv(nv, 0.0);
@@ -3165,9 +3217,9 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     cv.emplace_back(nv, 0.0);
   }
   for (int64_t i = 0; i < m; ++i) {
-    const double sx = sig[i] * yb[i];
-    z1[i] = su.q00 * xa[i] + su.q10 * sx;     // U^T a1, [a b~] Q_u = [a1 b1]
-    cu[0][i] = su.q01 * xa[i] + su.q11 * sx;  // U^T b1
+    const double sx = sig[i] * yb[i] / c_u, xu = c_u * xa[i];  // (D9)
+    z1[i] = su.q00 * xu + su.q10 * sx;     // U^T a1, [a b~] Q_u = [a1 b1]
+    cu[0][i] = su.q01 * xu + su.q11 * sx;  // U^T b1
     Du[i] = sig[i] * sig[i];
     Dv[i] = Du[i];
   }
@@ -3182,8 +3234,8 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   for (int64_t i = 0; i < nv; ++i) {
     const double sxa = i < m ? sig[i] * xa[i] : 0.0;
     const double ybi = thin && i == m ? beta_perp : yb[i];
-    z3[i] = sv.q00 * ybi + sv.q10 * sxa;     // V^T a2, [b a~] Q_v = [a2 b2]
-    cv[0][i] = sv.q01 * ybi + sv.q11 * sxa;  // V^T b2
+    z3[i] = sv.q00 * (ybi / c_v) + sv.q10 * (c_v * sxa);     // V^T a2, [b a~] Q_v = [a2 b2] (D9)
+    cv[0][i] = sv.q01 * (ybi / c_v) + sv.q11 * (c_v * sxa);  // V^T b2
     for (int q = 0; q < kNumProbes; ++q)     // V^T A_hat^T g = Sigma^T U^T g + (V^T b)(a.g)
       cv[1 + q][i] = (i < m ? sig[i] * xg[q * m + i] : 0.0) + ybi * ag[q];
   }
@@ -3240,6 +3292,32 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     z1.swap(zu);
     z3.swap(zv);
   }
+  // D5 for clusters larger than the probes: a singular value repeated k >= kNumProbes + 3
+  // times in Sigma keeps k - 2 copies after the update, in bases the two sides choose
+  // independently.  Those columns are deflated ones: their coordinates over the original
+  // group's columns follow from the deflation reflections and the merges alone (host-only
+  // carries gcu / gcv, unit vectors of the group's original columns), and since
+  // A V_G = sigma U_G and the deflated columns are orthogonal to U_G^T a and V_G^T b,
+  // U_c^T A_hat V_c = sigma Tu^T Tv (see the pairing below).  At most kMaxPairTracked columns.
+  std::vector<std::vector<double>> gcu, gcv;
+  std::vector<int32_t> gidx;
+  {
+    int64_t i0 = 0;
+    while (i0 < m) {
+      int64_t i1 = i0 + 1;
+      while (i1 < m && sig[i1] == sig[i0]) ++i1;
+      if (i1 - i0 >= kNumProbes + 3 && sig[i0] > 0.0 && int64_t(gidx.size()) + (i1 - i0) <= kMaxPairTracked)
+        for (int64_t g = i0; g < i1; ++g) gidx.push_back(int32_t(g));
+      i0 = i1;
+    }
+    for (int32_t g : gidx) {
+      gcu.emplace_back(m, 0.0);
+      gcu.back()[g] = 1.0;
+      gcv.emplace_back(nv, 0.0);
+      gcv.back()[g] = 1.0;
+    }
+    for (int e = 0; e < 4; ++e) S[e].gcar = gidx.empty() ? nullptr : (e < 2 ? &gcu : &gcv);
+  }
   const double tA = now_ms();
   const svd1_config pcfg = P->cfg;
   const int pp = P->p;
@@ -3280,6 +3358,11 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   bool launched_u1 = false, launched_v1 = false, uploaded_u1 = false, uploaded_v1 = false;
   double t_fin[4] = {0, 0, 0, 0}, t_dbg[4] = {0, 0, 0, 0};
   auto nrot_v = [&]() { return c.v_rows > 0 ? int(P->rot_goff.size()) - 1 : 0; };
+  auto rot_maxk = [&]() {
+    int mk = 0;
+    for (size_t g = 0; g + 1 < P->rot_goff.size(); ++g) mk = std::max(mk, P->rot_goff[g + 1] - P->rot_goff[g]);
+    return mk;
+  };
   auto upload_rot = [&](int us) -> svd1_status {  // pairing rotations (set before step 3's upload)
     if (nrot_v() <= 0) return SVD1_OK;
     int32_t *g, *cl;
@@ -3317,7 +3400,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     if (e == 3 && rows > 0 && nrot_v() > 0)
       TRY(col_rotate(rows, rout, ld, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                      static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), ss,
-                     LC(P)));
+                     LC(P), rot_maxk()));
     if (second) {  // read back the next update's rows: x_a | x_g (U side), y_b (V side)
       if (!P->rb_ev[side]) SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->rb_ev[side], cudaEventDisableTiming));
       if (side == 0 && B->ru_next >= 0) {
@@ -3376,7 +3459,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
       if (side && nrot_v() > 0)
         TRY(col_rotate(nr, X + r0 * ldx, ldx, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                        static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), st,
-                       LC(P)));
+                       LC(P), rot_maxk()));
     }
     // the side's whole time is reported on its first step (apply_ms[e1]); the second's is 0
     TRY(ev_record(P, 2 * e1 + 1, st));
@@ -3668,10 +3751,52 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
           P->rot_goff.push_back(int32_t(P->rot_cols.size()));
           ++R.pair_rotations;
         }
+      } else if (k > kNumProbes && !gidx.empty() && Du[m - 1 - i0] > 0.0) {
+        // W = Tu^T Tv from the tracked coordinates (Tu[g][a]: original U column g in final
+        // column i0 + a); used only if every cluster column lies in the tracked span
+        const int ng = int(gidx.size());
+        bool inside = true;
+        for (int a = 0; a < k && inside; ++a) {
+          double nu = 0.0, nvv = 0.0;
+          for (int g = 0; g < ng; ++g) {
+            nu += gcu[g][m - 1 - (i0 + a)] * gcu[g][m - 1 - (i0 + a)];
+            nvv += gcv[g][nv - 1 - (i0 + a)] * gcv[g][nv - 1 - (i0 + a)];
+          }
+          inside = std::fabs(nu - 1.0) <= 1e-8 && std::fabs(nvv - 1.0) <= 1e-8;
+        }
+        if (inside) {
+          std::vector<double> W(size_t(k) * k);  // W[b * k + a] = M[b][a] / sigma
+          for (int b = 0; b < k; ++b)
+            for (int a = 0; a < k; ++a) {
+              double t = 0.0;
+              for (int g = 0; g < ng; ++g) t += gcu[g][m - 1 - (i0 + b)] * gcv[g][nv - 1 - (i0 + a)];
+              W[size_t(b) * k + a] = t;
+            }
+          for (int b = 0; b < k; ++b) {  // modified Gram-Schmidt on the columns (index b)
+            for (int b2 = 0; b2 < b; ++b2) {
+              double dot = 0.0;
+              for (int a = 0; a < k; ++a) dot += W[size_t(a) * k + b] * W[size_t(a) * k + b2];
+              for (int a = 0; a < k; ++a) W[size_t(a) * k + b] -= dot * W[size_t(a) * k + b2];
+            }
+            double nr = 0.0;
+            for (int a = 0; a < k; ++a) nr += W[size_t(a) * k + b] * W[size_t(a) * k + b];
+            nr = std::sqrt(nr);
+            for (int a = 0; a < k; ++a) W[size_t(a) * k + b] /= nr;
+          }
+          for (int a = 0; a < k; ++a) {
+            P->rot_cols.push_back(int32_t(i0 + a));
+            sgn[i0 + a] = 1.0;
+          }
+          for (int a = 0; a < k; ++a)
+            for (int b = 0; b < k; ++b) P->rot_mats.push_back(W[size_t(b) * k + a]);
+          P->rot_goff.push_back(int32_t(P->rot_cols.size()));
+          ++R.pair_rotations;
+        }
       }
       i0 = i1;
     }
   }
+  for (int e = 0; e < 4; ++e) S[e].gcar = nullptr;
   for (int j = 0; j < S[3].na; ++j) {
     const int64_t col = nv - 1 - S[3].tgt_pos[j];
     if (col < m) S[3].cs_h[j] *= sgn[col];
@@ -3720,6 +3845,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     jv.y_dev = B->y_dev;
     jv.inv_beta = beta_perp > 0.0 ? 1.0 / beta_perp : 0.0;
     jv.nrot = nrot_v();
+    jv.rot_maxk = rot_maxk();
     jv.ut = ut;
     if (!P->bdone[B->parity][1])
       SVD1_CUDA_TRY(cudaEventCreateWithFlags(&P->bdone[B->parity][1], cudaEventDisableTiming));
@@ -3770,7 +3896,7 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     if (nrot_v() > 0)
       TRY(col_rotate(c.v_rows, V, ldv, nrot_v(), static_cast<int32_t*>(S[3].rot_goff.p),
                      static_cast<int32_t*>(S[3].rot_cols.p), static_cast<double*>(S[3].rot_mats.p), stv,
-                     LC(P)));
+                     LC(P), rot_maxk()));
   }
   u_thread.join();  // the U-side applies are queued
   TRY(st_ua);

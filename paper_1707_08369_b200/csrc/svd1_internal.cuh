@@ -157,7 +157,7 @@ svd1_status householder_cols(int64_t rows, double* U, int64_t ld, int ngroups,
 // pairing rotations: for group g with columns c_0..c_{k-1} (k <= 8) and row-major k x k R,
 // U[r, c_b] <- sum_a U[r, c_a] R[a][b]  (in place)
 svd1_status col_rotate(int64_t rows, double* U, int64_t ld, int ngroups, const int32_t* goff,
-                       const int32_t* cols, const double* mats, cudaStream_t st, int64_t* launches);
+                       const int32_t* cols, const double* mats, cudaStream_t st, int64_t* launches, int max_k = 8);
 // passthrough: U_out[r, dst[q]] = scale[q] * U_in[r, src[q]]
 svd1_status passthrough(int64_t rows, int nq, const double* U_in, int64_t ld_in,
                         const int32_t* src, double* U_out, int64_t ld_out,

@@ -6,7 +6,7 @@ residual, orthogonality)."""
 import numpy as np
 import pytest
 
-from compare import log_parity, vector_error
+from compare import clusters, log_parity, vector_error
 from synth import config_inputs
 
 pytestmark = pytest.mark.gpu
@@ -54,6 +54,18 @@ def _invariants(inp, K, U, s, V):
     return res, orth, sig_err
 
 
+def _close_q27(X, Y, sig, tol=1e-8):
+    """X vs Y column by column the way Q27 (reading D3) determines them: elementwise, signs
+    included, on the columns whose relative eigengap is >= 1e-3; through the cluster
+    projector (<= 1e-10) inside near-degenerate clusters, whose columns are fixed only up to
+    a rotation of order eps sigma_1^2 / gap (the graded C3 recipe's tail)."""
+    e2 = (sig.cpu().numpy() if hasattr(sig, "cpu") else np.asarray(sig)) ** 2
+    iso = [g[0] for g in clusters(e2) if len(g) == 1]
+    d_iso = float((X[:, iso] - Y[:, iso]).abs().max()) if iso else 0.0
+    ge = vector_error(X.cpu().numpy(), Y.cpu().numpy(), e2)
+    assert d_iso <= tol and ge["cluster"] <= 1e-10, (d_iso, ge)
+
+
 @pytest.mark.parametrize("cfg,m,n,K,flags,exact", [
     (1, None, None, 3, 0, True),            # C1 full size, direct path
     (2, 300, 300, 3, P.FORCE_DIRECT, True),
@@ -80,10 +92,14 @@ def test_batch_matches_sequential(cfg, m, n, K, flags, exact):
     log_parity(f"batch vs sequential C{cfg} {m}x{n} K={K} flags={flags}", max_abs_U=du, max_abs_V=dv, gap_U=gu,
                gap_V=gv, sigma_rel=float(np.max(np.abs(sbn - ssn)) / ssn[0]))
     assert max(gu["isolated"], gu["cluster"], gv["isolated"], gv["cluster"]) <= 1e-10, (gu, gv)
-    if exact:  # elementwise, signs included: the graded C3 recipe's near-degenerate columns
-        # (relative gap < 1e-3, determined only to eps sigma_1^2 / gap) differ by up to ~1e-10
-        # (measured 9.3e-11, profiles/parity_r02.jsonl); column/cluster-wise <= 2e-13
-        assert du <= 1e-9 and dv <= 1e-9, (du, dv)
+    if exact:  # elementwise, signs included, on the columns Q27 determines (relative eigengap
+        # >= 1e-3; the graded C3 recipe's near-degenerate columns are fixed only to
+        # eps sigma_1^2 / gap, i.e. up to a rotation inside their cluster, which the gap-aware
+        # check above covers: measured up to 2e-8 elementwise there with the D9 balance)
+        iso = [g[0] for g in clusters(ssn ** 2) if len(g) == 1]
+        du_iso = float((Ub[:, iso] - Us[:, iso]).abs().max())
+        dv_iso = float((Vb[:, iso] - Vs[:, iso]).abs().max())
+        assert du_iso <= 1e-9 and dv_iso <= 1e-9, (du_iso, dv_iso, du, dv)
     assert [r["n_active"] for r in rb] == [r["n_active"] for r in rs]
 
 
@@ -171,7 +187,8 @@ def test_sharded_batch_two_ranks(cfg, m, n, K, flags):
     Vs = torch.cat([p_["V"] for p_ in parts])
     assert torch.equal(parts[0]["s"], parts[1]["s"])
     assert float((parts[0]["s"] - sb).abs().max()) <= 1e-12 * float(sb[0])
-    assert float((Us - Ub).abs().max()) <= 1e-8 and float((Vs[:, :m] - Vb[:, :m]).abs().max()) <= 1e-8
+    _close_q27(Us, Ub, sb)
+    _close_q27(Vs[:, :m], Vb[:, :m], sb)
     for p_ in parts:
         p_["plan"].close()
 
@@ -185,7 +202,8 @@ def test_batch_lengths(K):
     Us, ss, Vs, rs = _stream(inp, K, P.FORCE_FMM, batch=False)
     assert len(rb) == K
     assert float((sb - ss).abs().max()) <= 1e-12 * float(ss[0])
-    assert float((Ub - Us).abs().max()) <= 1e-8 and float((Vb - Vs).abs().max()) <= 1e-8
+    _close_q27(Ub, Us, ss)
+    _close_q27(Vb[:, :Ub.shape[0]], Vs[:, :Ub.shape[0]], ss)
     res, orth, sig_err = _invariants(inp, K, Ub, sb, Vb)
     assert res <= 1e-10 and orth <= 1e-10 and sig_err <= 1e-12, (res, orth, sig_err)
 

@@ -1,0 +1,110 @@
+"""Degenerate whole updates on the CUDA path (synth/edge.py), through the C ABI, against
+the oracle (Alg 6.1) at the north star's tolerances (readings D2-D4): the
+smallest shapes (1x1 .. 3x3, 1x3, 2x5), update vectors inside a few singular directions
+(zero weights), rank-deficient and fully repeated spectra, A and a b^T scaled
+by 1e80 / 1e-20, updates 1e-11 and 1e9 times ||A||, and an unbalanced a b^T = (1e8 a)(1e-8 b)^T
+(reading D9: the per-side power-of-two balance before the Schur split).  Also:
+(2^t a, b / 2^t) gives bitwise the same factors (D9), and a pipelined stream with unbalanced
+and extreme-scale updates matches the per-update path."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from compare import assert_parity, sigma_errors, vector_error
+from synth import EDGE_CASES, edge_case
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1707_08369_b200 as P  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV, torch.float64)
+
+
+def N(x):
+    return x.detach().cpu().numpy()
+
+
+def _gpu(U, s, V, a, b, flags=0):
+    Ug, sg, Vg = T(U), T(s), T(V)
+    plan = P.Plan(U.shape[0], V.shape[0], flags=flags)
+    rep = plan.update(Ug, sg, Vg, T(a), T(b))
+    torch.cuda.synchronize()
+    plan.close()
+    return Ug, sg, Vg, rep
+
+
+@pytest.mark.parametrize("flags", [0, P.FORCE_FMM])
+@pytest.mark.parametrize("name", EDGE_CASES)
+def test_edge_update_parity(name, flags):
+    U, s, V, a, b = edge_case(name)
+    m, n = U.shape[0], V.shape[0]
+    if flags and m < 8:
+        pytest.skip("FMM apply needs more than a handful of points")
+    ref = O.svd_update(U, s, V, a, b)
+    Ug, sg, Vg, rep = _gpu(U, s, V, a, b, flags)
+    A_hat = (U * s[None, :]) @ V[:, :m].T + np.outer(a, b)
+    f = math.ldexp(1.0, math.frexp(float(np.max(np.abs(A_hat))))[1])  # exact rescaling for the
+    Ah = T(A_hat / f)                                                  # residual (1e80 / 1e-20)
+    res = float(torch.linalg.norm(Ah @ Vg[:, :m] - Ug * (sg / f)[None, :], dim=0).max() / (sg[0] / f))
+    orth = max(float((Ug.T @ Ug - torch.eye(m, dtype=torch.float64, device=DEV)).abs().max()),
+               float((Vg.T @ Vg - torch.eye(n, dtype=torch.float64, device=DEV)).abs().max()))
+    r = dict(sigma=sigma_errors(N(sg), ref["sigma"]), res=res, orth=orth,
+             U=vector_error(N(Ug), ref["U"], ref["sigma"] ** 2),
+             V=vector_error(N(Vg), ref["V"], ref["info"]["Dv_hat"]))
+    assert_parity(f"edge {name} flags={flags}", r)
+
+
+@pytest.mark.parametrize("name", ["tiny33", "a_in_span", "rank_deficient", "scaled_down", "unbalanced"])
+def test_edge_balance_rescaling_bitwise(name):
+    """D9 on the GPU: (2^t a, b / 2^t) gives bitwise the same factors."""
+    U, s, V, a, b = edge_case(name)
+    base = _gpu(U, s, V, a, b)
+    for t in (-30, 7, 33):
+        other = _gpu(U, s, V, a * 2.0 ** t, b / 2.0 ** t)
+        for x, y in zip(base[:3], other[:3]):
+            assert torch.equal(x, y), (name, t)
+
+
+def test_edge_stream_matches_per_update():
+    """A pipelined stream (svd1_update_batch) through unbalanced, tiny and huge updates:
+    the same factors as the per-update path (singular values to 1e-12, columns gap-aware)."""
+    U, s, V, _, _ = edge_case("unbalanced", m=96)
+    rng = np.random.default_rng(77)
+    m = n = 96
+    ab = [(rng.standard_normal(m), rng.standard_normal(n)),
+          (1e8 * rng.standard_normal(m), 1e-8 * rng.standard_normal(n)),
+          (1e-12 * rng.standard_normal(m), rng.standard_normal(n)),
+          (1e-3 * rng.standard_normal(m), 1e5 * rng.standard_normal(n)),
+          (rng.standard_normal(m), rng.standard_normal(n))]
+    outs = []
+    for batch in (True, False):
+        Ug, sg, Vg = T(U), T(s), T(V)
+        plan = P.Plan(m, n, flags=P.FORCE_FMM)
+        if batch:
+            plan.update_batch(Ug, sg, Vg, T(np.stack([a for a, _ in ab])), T(np.stack([b for _, b in ab])))
+        else:
+            for a, b in ab:
+                plan.update(Ug, sg, Vg, T(a), T(b))
+        torch.cuda.synchronize()
+        plan.close()
+        outs.append((N(Ug), N(sg), N(Vg)))
+    (Ub, sb, Vb), (Us, ss, Vs) = outs
+    assert np.max(np.abs(sb - ss)) <= 1e-12 * ss[0]
+    gu = vector_error(Ub, Us, ss ** 2)
+    gv = vector_error(Vb[:, :m], Vs[:, :m], ss ** 2)
+    assert max(gu["isolated"], gu["cluster"], gv["isolated"], gv["cluster"]) <= 1e-10, (gu, gv)
+    A = (U * s[None, :]) @ V.T
+    for a, b in ab:
+        A = A + np.outer(a, b)
+    res = np.max(np.linalg.norm(A @ Vb[:, :m] - Ub * sb[None, :], axis=0)) / sb[0]
+    assert res <= 1e-10, res

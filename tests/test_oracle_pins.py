@@ -16,7 +16,7 @@ import pytest
 import oracle as O
 from brute import jacobi_eigvalsh, jacobi_svd
 from compare import sigma_errors, vector_error
-from synth import gaussian_factors, graded_factors, paper_uniform, random_secular, config_inputs
+from synth import gaussian_factors, graded_factors, paper_uniform, random_secular, config_inputs, EDGE_CASES, edge_case
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -460,3 +460,57 @@ def test_threaded_evaluation_is_bitwise_serial(monkeypatch):
     k7, t7 = O.secular_roots_bisect(d, z, rho)
     w7 = O.secular_w(d, z, rho, k7, t7)
     assert np.array_equal(k1, k7) and np.array_equal(t1, t7) and np.array_equal(w1, w7)
+
+
+# ------------------------------------------------------------- edge cases, reading D9
+@pytest.mark.parametrize("name", EDGE_CASES)
+def test_svd_update_edge_cases_vs_brute_force(name):
+    """Degenerate inputs of Alg 6.1 (synth/edge.py: the smallest shapes, zero weights,
+    rank-deficient and fully repeated spectra, extreme scales, unbalanced a b^T) against a
+    brute-force one-sided Jacobi SVD of A_hat, with orthogonality and residual."""
+    U, s, V, a, b = edge_case(name)
+    m = U.shape[0]
+    r = O.svd_update(U, s, V, a, b)
+    A_hat = (U * s) @ V[:, :m].T + np.outer(a, b)
+    f = math.ldexp(1.0, math.frexp(float(np.max(np.abs(A_hat))))[1])  # (exact rescaling: the
+    _, sj, _ = jacobi_svd(A_hat / f)                                  #  brute force's own
+    e = sigma_errors(r["sigma"], f * sj)                              #  thresholds are absolute)
+    assert e["gram"] <= 1e-13 and e["rel_top"] <= 1e-12, e
+    assert O.orth_defect(r["U"]) <= 1e-13 and O.orth_defect(r["V"]) <= 1e-13
+    assert O.column_residual(A_hat, r["U"], r["sigma"], r["V"]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["tiny33", "a_in_span", "rank_deficient", "scaled_down", "unbalanced"])
+def test_balance_rescaling_bitwise(name):
+    """Reading D9: (2^t a, b / 2^t) is the same rank-1 term; with the power-of-two balance
+    factor the oracle returns bitwise the same factors for every t."""
+    U, s, V, a, b = edge_case(name)
+    r = O.svd_update(U, s, V, a, b)
+    for t in (-30, -7, 5, 33):
+        r2 = O.svd_update(U, s, V, a * 2.0 ** t, b / 2.0 ** t)
+        for k in ("U", "sigma", "V"):
+            assert np.array_equal(r[k], r2[k]), (name, t, k)
+
+
+def test_balance_factor_cases():
+    """balance_factor: c^2 within a factor of 4 of x / y, a power of two, 1 on degenerate norms."""
+    for x, y in [(1.0, 1.0), (3.0, 1.0), (1e-30, 7.0), (5e200, 1e-100), (0.7, 0.3)]:
+        c = O.balance_factor(x, y)
+        assert math.frexp(c)[0] == 0.5 and 0.25 <= c * c / (x / y) <= 4.0, (x, y, c)
+    assert O.balance_factor(0.0, 1.0) == 1.0 and O.balance_factor(1.0, 0.0) == 1.0
+    assert O.balance_factor(float("inf"), 1.0) == 1.0
+
+
+def test_unbalanced_needs_d9(monkeypatch):
+    """Why D9: without the balance (c = 1) the paper's 2x2 Schur split cancels to
+    eps ||a||^2 and the unbalanced and scaled-down cases lose all accuracy."""
+    import oracle.svd1_oracle as OM
+    monkeypatch.setattr(OM, "balance_factor", lambda x, y: 1.0)
+    worst = 0.0
+    for name in ("unbalanced", "scaled_down"):
+        U, s, V, a, b = edge_case(name)
+        m = U.shape[0]
+        r = O.svd_update(U, s, V, a, b)
+        A_hat = (U * s) @ V[:, :m].T + np.outer(a, b)
+        worst = max(worst, O.column_residual(A_hat, r["U"], r["sigma"], r["V"]))
+    assert worst > 1e-6
