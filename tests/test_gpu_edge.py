@@ -108,3 +108,36 @@ def test_edge_stream_matches_per_update():
         A = A + np.outer(a, b)
     res = np.max(np.linalg.norm(A @ Vb[:, :m] - Ub * sb[None, :], axis=0)) / sb[0]
     assert res <= 1e-10, res
+
+
+def test_edge_stream_repeated_sigma():
+    """A pipelined stream on A = 2 Q1 Q2^T (one singular value of multiplicity 48): every
+    update leaves a cluster of 46, 44, 42 equal values paired from the tracked coordinates
+    (D5 beyond the probes); the factors match the per-update path and the accumulated A."""
+    U, s, V, _, _ = edge_case("all_equal")
+    rng = np.random.default_rng(78)
+    m = n = U.shape[0]
+    ab = [(rng.standard_normal(m), rng.standard_normal(n)) for _ in range(3)]
+    outs = []
+    for batch in (True, False):
+        Ug, sg, Vg = T(U), T(s), T(V)
+        plan = P.Plan(m, n)
+        if batch:
+            reps = plan.update_batch(Ug, sg, Vg, T(np.stack([a for a, _ in ab])), T(np.stack([b for _, b in ab])))
+        else:
+            reps = [plan.update(Ug, sg, Vg, T(a), T(b)) for a, b in ab]
+        torch.cuda.synchronize()
+        plan.close()
+        assert all(r["pair_rotations"] >= 1 for r in reps), [r["pair_rotations"] for r in reps]
+        outs.append((N(Ug), N(sg), N(Vg)))
+    (Ub, sb, Vb), (Us, ss, Vs) = outs
+    assert np.max(np.abs(sb - ss)) <= 1e-12 * ss[0]
+    A = (U * s[None, :]) @ V.T
+    for a, b in ab:
+        A = A + np.outer(a, b)
+    for Uo, so, Vo in outs:
+        res = np.max(np.linalg.norm(A @ Vo[:, :m] - Uo * so[None, :], axis=0)) / so[0]
+        orth = max(np.max(np.abs(Uo.T @ Uo - np.eye(m))), np.max(np.abs(Vo.T @ Vo - np.eye(n))))
+        assert res <= 1e-10 and orth <= 1e-10, (res, orth)
+        e = sigma_errors(so, np.linalg.svd(A, compute_uv=False))
+        assert e["gram"] <= 1e-12, e
