@@ -14,8 +14,8 @@ scaled by sign(diag R).  The paper itself uses random matrices with entries in
 from .gen import (SEED_BASE, haar, config_inputs, update_vectors, gaussian_factors,
                   graded_factors, paper_uniform, random_secular, interlaced_cauchy,
                   CONFIGS)
-from .edge import EDGE_CASES, edge_case
+from .edge import EDGE_CASES, EDGE_RES_TOL, edge_case
 
 __all__ = ["SEED_BASE", "haar", "config_inputs", "update_vectors", "gaussian_factors",
            "graded_factors", "paper_uniform", "random_secular", "interlaced_cauchy",
-           "CONFIGS", "EDGE_CASES", "edge_case"]
+           "CONFIGS", "EDGE_CASES", "EDGE_RES_TOL", "edge_case"]

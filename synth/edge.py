@@ -12,9 +12,15 @@ from .gen import haar
 
 EDGE_CASES = ["tiny11", "tiny22", "tiny13", "tiny25", "tiny33", "a_in_span", "b_one_dir",
               "rank_deficient", "all_equal", "scaled_up", "scaled_down", "small_update",
-              "large_update", "unbalanced"]
+              "large_update", "unbalanced", "downdate_top", "zero_matrix", "coordinate_update",
+              "b_null_space"]
 _TINY = {"tiny11": (1, 1), "tiny22": (2, 2), "tiny13": (1, 3), "tiny25": (2, 5), "tiny33": (3, 3)}
 EDGE_SEED = 1000
+# column residual bound per case where the method's own accuracy is looser than the north
+# star's 1e-10: an exact zero singular value of A_hat comes out of the Gram eigenvalues
+# as sqrt(O(eps) sigma_1^2), so reading D2's 1e-12 sigma_1^2 allows a residual
+# of sqrt(1e-12) = 1e-6 on that column
+EDGE_RES_TOL = {"downdate_top": 1e-6}
 
 
 def edge_case(name, m=48):
@@ -59,4 +65,19 @@ def edge_case(name, m=48):
     if name == "unbalanced":      # a b^T of unit size written as (1e8 a)(1e-8 b)^T
         U, s, V = fac(m, n, spread(m))
         return U, s, V, 1e8 * rng.standard_normal(m), 1e-8 * rng.standard_normal(n)
+    if name == "downdate_top":    # a b^T = -sigma_1 u_1 v_1^T: A_hat has an exact zero singular value
+        U, s, V = fac(m, n, spread(m))
+        return U, s, V, -s[0] * U[:, 0], V[:, 0].copy()
+    if name == "zero_matrix":     # A = 0: A_hat = a b^T, every other singular value 0
+        U, s, V = fac(m, n, np.zeros(m))
+        return U, s, V, rng.standard_normal(m), rng.standard_normal(n)
+    if name == "coordinate_update":  # a = e_3, b = e_7 (one entry of A changes)
+        U, s, V = fac(m, n, spread(m))
+        a, b = np.zeros(m), np.zeros(n)
+        a[3], b[7] = 1.0, 1.0
+        return U, s, V, a, b
+    if name == "b_null_space":    # m < n, b orthogonal to the row space of A (V^T b has no first m part)
+        mm, nn = 24, 40
+        U, s, V = fac(mm, nn, np.sort(rng.uniform(1.0, 10.0, mm))[::-1].copy())
+        return U, s, V, rng.standard_normal(mm), V[:, mm:] @ rng.standard_normal(nn - mm)
     raise KeyError(name)

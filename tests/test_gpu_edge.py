@@ -3,7 +3,9 @@ the oracle (Alg 6.1) at the north star's tolerances (readings D2-D4):
 smallest shapes (1x1 .. 3x3, 1x3, 2x5), update vectors inside a few singular directions
 (zero weights), rank-deficient and fully repeated spectra, A and a b^T scaled
 by 1e80 / 1e-20, updates 1e-11 and 1e9 times ||A||, and an unbalanced a b^T = (1e8 a)(1e-8 b)^T
-(reading D9: the per-side power-of-two balance before the Schur split).  Also:
+(reading D9: the per-side power-of-two balance before the Schur split), a
+downdate to an exact zero singular value, A = 0, a one-entry change and b in the null space
+of A's rows.  Also:
 (2^t a, b / 2^t) gives bitwise the same factors (D9), and a pipelined stream with unbalanced
 and extreme-scale updates matches the per-update path."""
 import math
@@ -13,7 +15,7 @@ import pytest
 
 import oracle as O
 from compare import assert_parity, sigma_errors, vector_error
-from synth import EDGE_CASES, edge_case
+from synth import EDGE_CASES, EDGE_RES_TOL, edge_case
 
 pytestmark = pytest.mark.gpu
 
@@ -61,7 +63,7 @@ def test_edge_update_parity(name, flags):
     r = dict(sigma=sigma_errors(N(sg), ref["sigma"]), res=res, orth=orth,
              U=vector_error(N(Ug), ref["U"], ref["sigma"] ** 2),
              V=vector_error(N(Vg), ref["V"], ref["info"]["Dv_hat"]))
-    assert_parity(f"edge {name} flags={flags}", r)
+    assert_parity(f"edge {name} flags={flags}", r, res_tol=EDGE_RES_TOL.get(name, 1e-10))
 
 
 @pytest.mark.parametrize("name", ["tiny33", "a_in_span", "rank_deficient", "scaled_down", "unbalanced"])
