@@ -21,7 +21,7 @@
  *     NULL = legacy default stream).  svd1_update blocks the host until its
  *     result is on the device (it reads small vectors back several times).
  *   - Errors: every function returns svd1_status; on SVD1_E_NOCONV,
- *     SVD1_E_NONFINITE, SVD1_E_POLE or SVD1_E_ZEROCOL from svd1_update the
+ *     SVD1_E_NONFINITE, SVD1_E_POLE, SVD1_E_ZEROCOL or SVD1_E_UNSUPPORTED from svd1_update the
  *     matrices are left UNMODIFIED (all checks happen in the spectral phase,
  *     before any write to U, Sigma or V).  SVD1_E_CUDA leaves them undefined.
  *   - Determinism: fixed reduction orders, no floating-point atomics: identical
@@ -48,7 +48,10 @@ typedef enum {
   SVD1_E_ZEROCOL = 5,   /* ||c_j|| underflow/overflow */
   SVD1_E_CUDA = 6,      /* CUDA runtime error */
   SVD1_E_NOMEM = 7,     /* device or host allocation failed */
-  SVD1_E_NCCL = 8       /* NCCL unavailable or a collective failed (world > 1) */
+  SVD1_E_NCCL = 8,      /* NCCL unavailable or a collective failed (world > 1) */
+  SVD1_E_UNSUPPORTED = 9 /* a singular value repeated beyond what the pairing of U_hat and V_hat
+                            tracks (DESIGN.md §3.2 D5: more than 256 bitwise-equal positive
+                            sigma in one update) -- refused, not paired wrongly */
 } svd1_status;
 
 /* flags */

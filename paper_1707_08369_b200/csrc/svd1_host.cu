@@ -3306,8 +3306,10 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
     while (i0 < m) {
       int64_t i1 = i0 + 1;
       while (i1 < m && sig[i1] == sig[i0]) ++i1;
-      if (i1 - i0 >= kNumProbes + 3 && sig[i0] > 0.0 && int64_t(gidx.size()) + (i1 - i0) <= kMaxPairTracked)
+      if (i1 - i0 >= kNumProbes + 3 && sig[i0] > 0.0) {
+        if (int64_t(gidx.size()) + (i1 - i0) > kMaxPairTracked) return SVD1_E_UNSUPPORTED;  // nothing written yet
         for (int64_t g = i0; g < i1; ++g) gidx.push_back(int32_t(g));
+      }
       i0 = i1;
     }
     for (int32_t g : gidx) {

@@ -143,3 +143,17 @@ def test_edge_stream_repeated_sigma():
         assert res <= 1e-10 and orth <= 1e-10, (res, orth)
         e = sigma_errors(so, np.linalg.svd(A, compute_uv=False))
         assert e["gram"] <= 1e-12, e
+
+
+def test_edge_cluster_beyond_tracking_refused():
+    """A singular value repeated 300 times (> the 256 columns D5 tracks) is refused with
+    SVD1_E_UNSUPPORTED before any write: the factors are left unchanged."""
+    U, s, V, a, b = edge_case("all_equal", m=300)
+    Ug, sg, Vg = T(U), T(s), T(V)
+    plan = P.Plan(300, 300)
+    with pytest.raises(P.SVD1Error) as e:
+        plan.update(Ug, sg, Vg, T(a), T(b))
+    torch.cuda.synchronize()
+    plan.close()
+    assert e.value.code == 9
+    assert np.array_equal(N(Ug), U) and np.array_equal(N(sg), s) and np.array_equal(N(Vg), V)
