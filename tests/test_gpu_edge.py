@@ -157,3 +157,24 @@ def test_edge_cluster_beyond_tracking_refused():
     plan.close()
     assert e.value.code == 9
     assert np.array_equal(N(Ug), U) and np.array_equal(N(sg), s) and np.array_equal(N(Vg), V)
+
+
+@pytest.mark.parametrize("name,m", [("all_equal", 200), ("rank_deficient", 400), ("scaled_down", 600),
+                                    ("unbalanced", 600), ("a_in_span", 500), ("downdate_top", 500)])
+def test_edge_update_parity_fmm_sizes(name, m):
+    """The same recipes at sizes where the forced FMM apply has a real tree (several levels,
+    far-field and one-sided terms)."""
+    U, s, V, a, b = edge_case(name, m=m)
+    ref = O.svd_update(U, s, V, a, b)
+    Ug, sg, Vg, rep = _gpu(U, s, V, a, b, P.FORCE_FMM)
+    n = V.shape[0]
+    A_hat = (U * s[None, :]) @ V[:, :m].T + np.outer(a, b)
+    f = math.ldexp(1.0, math.frexp(float(np.max(np.abs(A_hat))))[1])
+    Ah = T(A_hat / f)
+    res = float(torch.linalg.norm(Ah @ Vg[:, :m] - Ug * (sg / f)[None, :], dim=0).max() / (sg[0] / f))
+    orth = max(float((Ug.T @ Ug - torch.eye(m, dtype=torch.float64, device=DEV)).abs().max()),
+               float((Vg.T @ Vg - torch.eye(n, dtype=torch.float64, device=DEV)).abs().max()))
+    r = dict(sigma=sigma_errors(N(sg), ref["sigma"]), res=res, orth=orth,
+             U=vector_error(N(Ug), ref["U"], ref["sigma"] ** 2),
+             V=vector_error(N(Vg), ref["V"], ref["info"]["Dv_hat"]))
+    assert_parity(f"edge {name} m={m} FMM", r, res_tol=EDGE_RES_TOL.get(name, 1e-10))
