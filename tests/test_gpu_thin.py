@@ -102,3 +102,26 @@ def test_thin_b_in_span():
     assert bool(torch.isfinite(Vt).all())
     assert float((sf - st).abs().max()) <= 1e-12 * float(sf[0])
     assert float((Uf - Ut).abs().max()) <= 1e-8 and float((Vf[:, :m] - Vt[:, :m]).abs().max()) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["tiny13", "tiny25", "b_null_space"])
+def test_thin_edge_cases(name):
+    """Thin right factor on the rectangular edge recipes (synth/edge.py): m = 1 and 2, and b
+    entirely in the null space of A's rows (V^T b = 0 on the first m columns: the whole V-side
+    update lives in the extra direction q)."""
+    from synth import edge_case
+    U, s, V, a, b = edge_case(name)
+    m, n = U.shape[0], V.shape[0]
+    ref = O.svd_update(U, s, V, a, b)
+    Ug, sg, Vt = T(U), T(s), _thin(V, m)
+    plan = P.Plan(m, n, flags=P.THIN_V)
+    plan.update(Ug, sg, Vt, T(a), T(b))
+    se = sigma_errors(sg.cpu().numpy(), ref["sigma"])
+    assert se["gram"] <= 1e-12 and se["rel_top"] <= 1e-12, se
+    eu = vector_error(Ug.cpu().numpy(), ref["U"], ref["sigma"] ** 2)
+    ev = vector_error(Vt[:, :m].cpu().numpy(), ref["V"][:, :m], ref["sigma"] ** 2)
+    assert max(eu["isolated"], eu["cluster"], ev["isolated"], ev["cluster"]) <= 1e-9, (eu, ev)
+    A_hat = T((U * s[None, :]) @ V[:, :m].T + np.outer(a, b))
+    res = float(torch.linalg.norm(A_hat @ Vt[:, :m] - Ug * sg[None, :], dim=0).max() / sg[0])
+    orth = float((Vt[:, :m].T @ Vt[:, :m] - torch.eye(m, dtype=torch.float64, device=DEV)).abs().max())
+    assert res <= 1e-10 and orth <= 1e-10, (res, orth)
