@@ -90,3 +90,15 @@ def test_rank_config_errors():
     with pytest.raises(P.SVD1Error) as e:
         P.Plan(64, 64, world=2, rank=2, flags=P.EMULATE_RANKS)
     assert e.value.code == 1
+
+
+@pytest.mark.parametrize("name", ["all_equal", "unbalanced", "scaled_down"])
+def test_emulated_ranks_bitwise_edge(name):
+    """Sliced spectral phases on the edge recipes whose host decisions are new (the D9
+    balance, the D5 pairing of a 46-column cluster): bitwise the world = 1 result."""
+    from synth import edge_case
+    U, s, V, a, b = edge_case(name, m=96)
+    inp = dict(U=U, sigma=s, V=V, ab=[(a, b)])
+    ref = _run(inp, 1, False, flags=P.FORCE_FMM)
+    got = _run(inp, 1, False, flags=P.FORCE_FMM | P.EMULATE_RANKS, world=3)
+    assert _bitwise(ref, got)
