@@ -34,7 +34,7 @@ class Report(C.Structure):
                 ("apply_ms", dbl * 4), ("apply_flops", dbl * 4), ("spectral_ms", dbl * 4),
                 ("fmm_levels", i32 * 4), ("fmm_max_near", i32 * 4), ("mean_iter", dbl * 4),
                 ("pair_rotations", i32), ("apply_flops_exec", dbl * 4), ("gemm_ms", dbl * 4),
-                ("allocations", i64)]
+                ("allocations", i64), ("unpaired_clusters", i32)]
 
     def as_dict(self):
         return dict(t_ms=list(self.t_ms)[:7], n_active=list(self.n_active),
@@ -46,7 +46,7 @@ class Report(C.Structure):
                     fmm_levels=list(self.fmm_levels), fmm_max_near=list(self.fmm_max_near),
                     mean_iter=list(self.mean_iter), pair_rotations=self.pair_rotations,
                     apply_flops_exec=list(self.apply_flops_exec), gemm_ms=list(self.gemm_ms),
-                    allocations=self.allocations)
+                    allocations=self.allocations, unpaired_clusters=self.unpaired_clusters)
 
 
 def _sig(name, args):

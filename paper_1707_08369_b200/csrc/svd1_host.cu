@@ -3793,7 +3793,11 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
             for (int b = 0; b < k; ++b) P->rot_mats.push_back(W[size_t(b) * k + a]);
           P->rot_goff.push_back(int32_t(P->rot_cols.size()));
           ++R.pair_rotations;
+        } else {
+          ++R.unpaired_clusters;
         }
+      } else if (k > kNumProbes && Du[m - 1 - i0] > 0.0) {
+        ++R.unpaired_clusters;
       }
       i0 = i1;
     }
