@@ -479,8 +479,15 @@ __device__ __forceinline__ double2 lds128(const unsigned char* p) {
 #ifndef SVD1_MT32
 #define SVD1_MT32 4  // the same for the 32-wide passes
 #endif
+#ifndef SVD1_CPS16
+#define SVD1_CPS16 1  // KC-column chunks per ring stage of the 16-wide passes (experiments)
+#endif
+#ifndef SVD1_CPS32
+#define SVD1_CPS32 1  // the same for the 32-wide passes
+#endif
 template <int BN>
 struct GemmCfg {
+  static constexpr int CPS = BN <= 16 ? SVD1_CPS16 : SVD1_CPS32;  // chunks per stage
   static constexpr int CW = BN <= 16 ? SVD1_CW16 : SVD1_CW32;  // consumer warps (RW rows each)
   static constexpr int MT = BN <= 16 ? SVD1_MT16 : SVD1_MT32;  // 8-row m-tiles per consumer warp
   static constexpr int RW = 8 * MT;
@@ -490,8 +497,9 @@ struct GemmCfg {
   static constexpr int STAGES = BN <= 16 ? SVD1_STAGES16 : SVD1_STAGES32;
   static constexpr int A_BYTES = BM * KC * 8;
   static constexpr int B_BYTES = BN * KC * 8;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STAGES * (16 + 16);
+  static constexpr int STAGE_A = CPS * A_BYTES, STAGE_B = CPS * B_BYTES;
+  static constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STAGES * (16 + 32);
 };
 
 // Tile -> (task, row block).  Task-major (default): consecutive CTAs take the same task's
@@ -512,6 +520,7 @@ struct StageInfo {
   int32_t last;   // 1: last chunk of the tile (epilogue after it)
   int32_t kindN;  // the tile's task: out_kind << 8 | N (read by the epilogue from shared
   int32_t col0;   //   memory, not from global memory)
+  int32_t nch;    // KC-column chunks in this stage (1 .. CPS)
 };
 
 #ifndef SVD1_MINB32
@@ -533,9 +542,9 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // SWIZZLE_128B tiles need 1024-byte aligned shared addresses
   unsigned char* sbase = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  unsigned char* sA = sbase;                  // [S][BM][16] doubles, swizzled
-  unsigned char* sB = sbase + S * G::A_BYTES; // [S][BN][16] doubles, swizzled
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * G::B_BYTES);
+  unsigned char* sA = sbase;                   // [S][CPS][BM][16] doubles, swizzled
+  unsigned char* sB = sbase + S * G::STAGE_A;  // [S][CPS][BN][16] doubles, swizzled
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * G::STAGE_B);
   uint64_t* empty = full + S;
   StageInfo* info = reinterpret_cast<StageInfo*>(empty + S);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -594,23 +603,27 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
           const int64_t op_row = __shfl_sync(0xffffffffu, mine.op_row, q);
           const CUtensorMap* ma = in_kind == IO_U ? tm_u : (in_kind == IO_PHI ? tm_phi : tm_psi);
           const bool last_term = tb + q == T.t_end - 1;
-          for (int k0 = 0; k0 < K; k0 += KC) {
+          for (int k0 = 0; k0 < K; k0 += KC * G::CPS) {
+            const int nch = G::CPS == 1 ? 1 : min(G::CPS, (K - k0 + KC - 1) / KC);
             mbar_wait(&empty[stage], phase ^ 1);
-            const int64_t brow = op_row + int64_t(k0 / KC) * npad + T.op_col0;
-            const double* bsrc = ops_raw + brow * 16;
-            unsigned char* bdst = sB + stage * G::B_BYTES;
-            for (int e = lane; e < BN * 8; e += 32) {
-              const int n = e >> 3, j = e & 7;
-              const int64_t row = brow + n;
-              const bool ok = row < ops_rows;
-              const unsigned sa = smem_u32(bdst + n * 128 + ((j ^ (n & 7)) << 4));
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
-                           "l"(bsrc + (ok ? n * 16 + 2 * j : 0)), "r"(ok ? 16 : 0));
+            for (int c = 0; c < nch; ++c) {
+              const int64_t brow = op_row + int64_t((k0 + c * KC) / KC) * npad + T.op_col0;
+              const double* bsrc = ops_raw + brow * 16;
+              unsigned char* bdst = sB + stage * G::STAGE_B + c * G::B_BYTES;
+              for (int e = lane; e < BN * 8; e += 32) {
+                const int n = e >> 3, j = e & 7;
+                const int64_t row = brow + n;
+                const bool ok = row < ops_rows;
+                const unsigned sa = smem_u32(bdst + n * 128 + ((j ^ (n & 7)) << 4));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                             "l"(bsrc + (ok ? n * 16 + 2 * j : 0)), "r"(ok ? 16 : 0));
+              }
             }
             if (lane == 0) {
-              info[stage] = StageInfo{tile, (last_term && k0 + KC >= K) ? 1 : 0, kindN, T.col0};
-              mbar_arrive_tx(&full[stage], G::A_BYTES);
-              tma_load_2d(sA + stage * G::A_BYTES, ma, col0 + k0, row0, &full[stage]);
+              info[stage] = StageInfo{tile, (last_term && k0 + KC * G::CPS >= K) ? 1 : 0, kindN, T.col0, nch};
+              mbar_arrive_tx(&full[stage], uint32_t(nch * G::A_BYTES));
+              for (int c = 0; c < nch; ++c)
+                tma_load_2d(sA + stage * G::STAGE_A + c * G::A_BYTES, ma, col0 + k0 + c * KC, row0, &full[stage]);
             }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full[stage])) : "memory");
             if (++stage == S) {
@@ -624,7 +637,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
       T = Tn;
     }
     mbar_wait(&empty[stage], phase ^ 1);
-    if (lane == 0) info[stage] = StageInfo{-1, -1, 0, 0};
+    if (lane == 0) info[stage] = StageInfo{-1, -1, 0, 0, 0};
     __syncwarp();
     mbar_arrive(&full[stage]);
     if (lane == 0) mbar_arrive(&full[stage]);  // 33 arrivals per phase
@@ -666,8 +679,10 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
         }
       }
     }
-    const unsigned char* a = sA + stage * G::A_BYTES + a_row;
-    const unsigned char* b = sB + stage * G::B_BYTES + b_row;
+#pragma unroll 1
+    for (int c = 0; c < (G::CPS == 1 ? 1 : I.nch); ++c) {
+    const unsigned char* a = sA + stage * G::STAGE_A + c * G::A_BYTES + a_row;
+    const unsigned char* b = sB + stage * G::STAGE_B + c * G::B_BYTES + b_row;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // k-steps q = 2h, 2h + 1
       const int sw = h ? sw1 : sw0;
@@ -686,6 +701,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], af[mt].y, bf[nt].y);
+    }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
