@@ -493,12 +493,20 @@ def main():
             ref, got = sv[:kk], sig[:kk]
             rel = (got - ref).abs() / ref.clamp_min(1e-300)
             top = ref >= 0.1 * ref[0]
+            # strict relative error in units of its rounding sensitivity eps (sigma_1/sigma_i)^2 / 2
+            # (a Gram eigenvalue perturbed by eps sigma_1^2)
+            sens = (2.0 ** -52) * (ref[0] / ref.clamp_min(1e-300)) ** 2 / 2.0
+            rs = rel / sens
             check["sigma_vs_svdvals"] = {
                 "gram": float((got * got - ref * ref).abs().max() / (ref[0] * ref[0])),
                 "max_rel": float(rel.max()), "max_rel_top": float(rel[top].max()),
+                "rel_sens": float(rs.max()), "rel_sens_at": float(ref[int(rs.argmax())] / ref[0]),
                 "note": ("reference: torch.linalg.svdvals of the explicitly accumulated A_hat (fp64), after all "
                          "the timed updates; sigma^2 are Gram eigenvalues (D2), so the error of a small sigma_i "
-                         "scales with (sigma_1 / sigma_i)^2, and the FMM tolerance eps bounds the factors")}
+                         "scales with (sigma_1 / sigma_i)^2, and the FMM tolerance eps bounds the factors; rel_sens = "
+                         "max_i rel_i / (eps (sigma_1/sigma_i)^2 / 2), the strict error in units of one rounding of "
+                         "the Gram eigenvalue, accumulated over the whole stream of updates (the per-update parity "
+                         "against the oracle is in tests/, profiles/parity_r02.jsonl)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == CFG_ID:
