@@ -139,12 +139,12 @@ typedef struct {
                             update (0 in steady state: every workspace is sized by
                             svd1_plan_create; a buffer that depends on the FMM tree and
                             outgrows its create-time estimate grows once, stream-ordered) */
-  int32_t unpaired_clusters; /* clusters of numerically equal final singular values (consecutive
-                            gaps <= 64 eps sigma_1^2) of more than 4 columns that are neither
-                            paired by the probes nor made of tracked repeated columns (D5):
-                            near-equal but distinct sigma, whose U_hat / V_hat columns inside
-                            the cluster may be mismatched by a rotation;
-                            0 otherwise */
+  int32_t unpaired_clusters; /* clusters of more than 4 final singular values equal to within
+                            64 eps of their own size (so their columns are not determined one
+                            by one) that are neither paired by the probes nor made of tracked
+                            repeated columns (D5): near-equal but distinct sigma, whose U_hat /
+                            V_hat columns inside the cluster may be mismatched by a rotation
+                            (see DESIGN.md §10); 0 otherwise */
 } svd1_report;
 
 /* Plan: owns every workspace, allocated HERE (FMM STEPS 1-2 fix p, s and

@@ -3675,6 +3675,14 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   {
     const double dmax = std::max(Du[m - 1], 0.0);
     const double tolc = 64.0 * kEps * dmax;
+    // a cluster (gaps <= 64 eps D_1) whose gaps are also within 64 eps of its own values: its
+    // columns are not determined one by one (a graded tail's clusters are: its relative gaps
+    // are far above eps, and the solver's relative accuracy fixes each column up to sign)
+    auto self_near = [&](int64_t a0, int64_t a1) {
+      for (int64_t t = a0 + 1; t < a1; ++t)
+        if (Du[m - 1 - (t - 1)] - Du[m - 1 - t] > 64.0 * kEps * Du[m - 1 - (t - 1)]) return false;
+      return true;
+    };
     int64_t i0 = 0;
     while (i0 < m) {
       int64_t i1 = i0 + 1;
@@ -3793,10 +3801,10 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
             for (int b = 0; b < k; ++b) P->rot_mats.push_back(W[size_t(b) * k + a]);
           P->rot_goff.push_back(int32_t(P->rot_cols.size()));
           ++R.pair_rotations;
-        } else {
+        } else if (self_near(i0, i1)) {
           ++R.unpaired_clusters;
         }
-      } else if (k > kNumProbes && Du[m - 1 - i0] > 0.0) {
+      } else if (k > kNumProbes && Du[m - 1 - i0] > 0.0 && self_near(i0, i1)) {
         ++R.unpaired_clusters;
       }
       i0 = i1;

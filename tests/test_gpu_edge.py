@@ -202,3 +202,17 @@ def test_edge_near_equal_run(k):
     else:
         assert k > 5
     assert (rep["unpaired_clusters"] > 0) == (k == 10), rep["unpaired_clusters"]
+
+
+def test_graded_tail_not_reported_unpaired():
+    """The graded C3 recipe's tail forms clusters under the absolute 64 eps sigma_1^2 rule, but
+    its values are 0.7 % apart relative to themselves, so every column is fixed up to sign:
+    none of them is reported as unpaired."""
+    from synth import config_inputs
+    inp = config_inputs(3, m=1024, n=1024, updates=4)
+    Ug, sg, Vg = T(inp["U"]), T(inp["sigma"]), T(inp["V"])
+    plan = P.Plan(1024, 1024)
+    reps = plan.update_batch(Ug, sg, Vg, T(np.stack([a for a, _ in inp["ab"]])), T(np.stack([b for _, b in inp["ab"]])))
+    torch.cuda.synchronize()
+    plan.close()
+    assert all(r["unpaired_clusters"] == 0 for r in reps), [r["unpaired_clusters"] for r in reps]
