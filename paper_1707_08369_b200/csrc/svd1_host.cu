@@ -3187,6 +3187,21 @@ svd1_status update_impl(svd1_plan_t P, double* U, int64_t ldu, double* sigma, do
   const double* ag = h + 5 * m + n;
   const double alpha = ag[4], beta = ag[5];
   std::vector<double> sig = B ? *B->sig : std::vector<double>(h + nproj, h + nproj + m);
+  // Reading D10: a run of more than kNumProbes + 2 singular values within
+  // 64 eps of each other relative to their size is taken as one repeated value (the run's
+  // largest), a backward perturbation of A by <= 64 eps ||A||.  Such a run is otherwise
+  // solved as distinct poles whose final columns the probes cannot pair (D5); as a bitwise
+  // repetition it deflates (D1) and its columns are paired from their tracked coordinates.
+  // (Runs of graded or random spectra are far apart relative to themselves: untouched.)
+  for (int64_t i0 = 0; i0 < m;) {
+    int64_t i1 = i0 + 1;
+    while (i1 < m && sig[i1] > 0.0 &&
+           std::fabs(sig[i1 - 1] - sig[i1]) <= 64.0 * kEps * std::max(sig[i1 - 1], sig[i1]))
+      ++i1;
+    if (i1 - i0 >= kNumProbes + 3 && sig[i0] > 0.0)
+      for (int64_t t = i0 + 1; t < i1; ++t) sig[t] = sig[i0];  // (adjacent in the given order)
+    i0 = i1;
+  }
   R.t_ms[0] = now_ms() - t0;
   if (alpha == 0.0 || beta == 0.0) {  // A_hat = A
     R.noop = 1;
