@@ -499,7 +499,7 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * KC * 8;
   static constexpr int STAGE_A = CPS * A_BYTES, STAGE_B = CPS * B_BYTES;
   static constexpr int STAGE_BYTES = STAGE_A + STAGE_B;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STAGES * (16 + 32);
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + STAGES * (16 + 16);
 };
 
 // Tile -> (task, row block).  Task-major (default): consecutive CTAs take the same task's
@@ -517,10 +517,10 @@ __device__ __forceinline__ int tile_rb(int tile, int nrb, int ntask, int rb_majo
 
 struct StageInfo {
   int32_t tile;   // tile the chunk belongs to; -1: no more chunks
-  int32_t last;   // 1: last chunk of the tile (epilogue after it)
+  int32_t last;   // bit 0: last chunk of the tile (epilogue after it); CPS > 1: the stage's
+                  // KC-column chunks (1 .. CPS) in bits 8..; -1: end of the ring
   int32_t kindN;  // the tile's task: out_kind << 8 | N (read by the epilogue from shared
   int32_t col0;   //   memory, not from global memory)
-  int32_t nch;    // KC-column chunks in this stage (1 .. CPS)
 };
 
 #ifndef SVD1_MINB32
@@ -620,7 +620,8 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
               }
             }
             if (lane == 0) {
-              info[stage] = StageInfo{tile, (last_term && k0 + KC * G::CPS >= K) ? 1 : 0, kindN, T.col0, nch};
+              info[stage] = StageInfo{tile, ((last_term && k0 + KC * G::CPS >= K) ? 1 : 0) | (G::CPS > 1 ? nch << 8 : 0),
+                                      kindN, T.col0};
               mbar_arrive_tx(&full[stage], uint32_t(nch * G::A_BYTES));
               for (int c = 0; c < nch; ++c)
                 tma_load_2d(sA + stage * G::STAGE_A + c * G::A_BYTES, ma, col0 + k0 + c * KC, row0, &full[stage]);
@@ -637,7 +638,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
       T = Tn;
     }
     mbar_wait(&empty[stage], phase ^ 1);
-    if (lane == 0) info[stage] = StageInfo{-1, -1, 0, 0, 0};
+    if (lane == 0) info[stage] = StageInfo{-1, -1, 0, 0};
     __syncwarp();
     mbar_arrive(&full[stage]);
     if (lane == 0) mbar_arrive(&full[stage]);  // 33 arrivals per phase
@@ -680,7 +681,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
       }
     }
 #pragma unroll 1
-    for (int c = 0; c < (G::CPS == 1 ? 1 : I.nch); ++c) {
+    for (int c = 0; c < (G::CPS == 1 ? 1 : (I.last >> 8)); ++c) {
     const unsigned char* a = sA + stage * G::STAGE_A + c * G::A_BYTES + a_row;
     const unsigned char* b = sB + stage * G::STAGE_B + c * G::B_BYTES + b_row;
 #pragma unroll
@@ -709,7 +710,7 @@ __global__ void __launch_bounds__(GemmCfg<BN>::NTHR, BN == 32 ? SVD1_MINB32 : SV
       stage = 0;
       phase ^= 1;
     }
-    if (I.last) {  // epilogue of tile I.tile (registers -> global)
+    if (G::CPS == 1 ? I.last : (I.last & 1)) {  // epilogue of tile I.tile (registers -> global)
       const int task = tile_task(I.tile, nrb, ntask, rb_major);
       const int64_t row0 = int64_t(tile_rb(I.tile, nrb, ntask, rb_major)) * G::BM;
       (void)task;
